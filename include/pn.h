@@ -1,0 +1,182 @@
+/*
+ * pn.h -- C ABI of the B200-native LeNet-style training path
+ * (arxiv 2005.13076, "Using PHAST to port Caffe library").
+ *
+ * The paper's system is Caffe's Net/Solver/Layer stack: a net of
+ * layers exchanging Blobs (data + diff), run feed-forward in order and
+ * back-propagated in reverse order after the loss, then updated by the
+ * solver.  This header exposes exactly that: build a net from a layer spec,
+ * forward, backward, solver update, plus blob access.  SPEC.md S:509-544 gives
+ * the operation list (net_build / net_forward / net_backward / sgd_step) and
+ * S:580 the spec text format.
+ *
+ * Conventions (all functions):
+ *  - Plain C types only; no C++ types or exceptions cross this boundary.
+ *  - Every function returns a pn_status; on non-OK, pn_last_error() returns a
+ *    thread-local human-readable message.
+ *  - "stream" is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  All device work is stream-ordered; nothing synchronises the
+ *    host except net_sync_errors(), net_get_blob(..., host) and the *_host
+ *    entry points, which say so.
+ *  - Ownership: the library owns every blob (activations, masks, parameters,
+ *    parameter diffs, momentum history), allocated in net_create on the net's
+ *    device and freed in net_destroy.  Caller-owned input buffers (images,
+ *    labels, loss output) must stay alive until the stream work that uses them
+ *    completes, as with any CUDA async API.
+ *  - Layout: every blob is NCHW fp32 row-major.  Labels are int32 class
+ *    ids.  Inner-product weights are [num_output, K] (Listing 1).
+ *  - Errors: PN_ERR_INVALID_ARG (NULL / bad enum / size mismatch),
+ *    PN_ERR_PARSE (spec syntax, unknown key), PN_ERR_UNKNOWN_LAYER,
+ *    PN_ERR_DANGLING_BLOB (bottom not produced earlier), PN_ERR_SHAPE (shape
+ *    inference failure, non-positive output size), PN_ERR_LABEL_RANGE
+ *    (a label outside [0, classes): detected on the device, reported by
+ *    net_sync_errors), PN_ERR_CUDA, PN_ERR_NCCL, PN_ERR_STATE (call
+ *    order misuse, e.g. backward before forward, or a blob that the fused plan
+ *    does not materialise).
+ */
+#ifndef PN_H
+#define PN_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pn_net pn_net; /* opaque; one per device */
+
+typedef enum {
+  PN_OK = 0,
+  PN_ERR_INVALID_ARG = 1,
+  PN_ERR_PARSE = 2,
+  PN_ERR_UNKNOWN_LAYER = 3,
+  PN_ERR_DANGLING_BLOB = 4,
+  PN_ERR_SHAPE = 5,
+  PN_ERR_LABEL_RANGE = 6,
+  PN_ERR_CUDA = 7,
+  PN_ERR_NCCL = 8,
+  PN_ERR_STATE = 9
+} pn_status;
+
+/* net_create flags */
+enum {
+  PN_FP32 = 0,      /* fp32 SIMT FFMA contractions (1e-5 parity class)        */
+  PN_TF32 = 1,      /* TF32 tcgen05 tensor-core contractions, fp32 accumulate,
+                       operands rounded to nearest (2e-3 parity class)         */
+  PN_LAYERWISE = 2  /* one generic kernel per layer, every blob materialised
+                       (debug / teacher-forcing plan); default is the fused
+                       plan when the net matches a fused pattern              */
+};
+
+/* which buffer of a blob */
+enum { PN_DATA = 0, PN_DIFF = 1, PN_MASK = 2, PN_HISTORY = 3 };
+
+/* Solver settings (Caffe SGD, R11). lr_policy: 0 fixed,
+ * 1 inv: lr = base_lr * (1 + gamma*iter)^(-power), evaluated on the host in
+ * double and rounded to fp32 once per step. */
+typedef struct {
+  float base_lr, momentum, weight_decay, gamma, power;
+  int lr_policy;
+} pn_sgd;
+
+/* Build a net.  spec_text: NUL-terminated "[input]" + "[layer]"
+ * sections of key = value lines (unknown keys are PN_ERR_PARSE).
+ * batch: images per forward on this device (fixed for the net's lifetime).
+ * device: CUDA ordinal.  flags: PN_FP32 | PN_TF32, optionally | PN_LAYERWISE.
+ * Parameters start at zero; set them with net_set_param. */
+pn_status net_create(const char* spec_text, int batch, int device, int flags,
+                     pn_net** out);
+void net_destroy(pn_net* net);
+const char* pn_last_error(void);
+
+/* Describe the net.  Blob i in [0, count): name (library-owned string),
+ * dims (N,C,H,W), is_param (1 for "<layer>.w" / "<layer>.b" parameters),
+ * materialised (0 if the fused plan never writes it to memory). */
+pn_status net_blob_count(const pn_net* net, int* count);
+pn_status net_blob_info(const pn_net* net, int i, const char** name,
+                        int dims[4], int* is_param, int* materialised);
+/* Total learnable floats (sum of all weights and biases). */
+pn_status net_param_count(const pn_net* net, int64_t* count);
+/* Library-owned device pointer of a blob's DATA / DIFF / HISTORY buffer
+ * (HISTORY: momentum, parameters only).  Valid until net_destroy. */
+pn_status net_blob_ptr(pn_net* net, const char* name, int which,
+                       void** dev_ptr);
+
+/* Copy count floats into parameter blob `name` ("conv1.w", "ip2.b", ...)
+ * from src (device pointer, or host pointer if src_on_host; a host copy is
+ * synchronous).  count must equal the blob's element count. */
+pn_status net_set_param(pn_net* net, const char* name, const float* src,
+                        int64_t count, int src_on_host, void* stream);
+/* Copy a blob buffer out.  which = PN_DATA / PN_DIFF / PN_HISTORY copy fp32
+ * values; PN_MASK copies the max-pool origin mask of a Pooling layer's top
+ * as int32 plane-local indices h*W+w (R5).  bytes must equal the
+ * blob's element count times 4.  dst_on_host: synchronous host copy. */
+pn_status net_get_blob(pn_net* net, const char* name, int which, void* dst,
+                       int64_t bytes, int dst_on_host, void* stream);
+/* Overwrite a blob buffer (teacher forcing: feed a stage the oracle's
+ * inputs).  PN_MASK takes int32 plane-local indices. */
+pn_status net_put_blob(pn_net* net, const char* name, int which,
+                       const void* src, int64_t bytes, int src_on_host,
+                       void* stream);
+
+/* Forward (P:94 feed-forward).  x: device N*C*H*W fp32, labels:
+ * device N int32, loss: device float (may be NULL).  Also leaves the class
+ * probabilities in blob "prob" and the predictions (lowest-index argmax) in
+ * blob "pred" (int32 values stored in the blob's 4-byte slots). */
+pn_status net_forward(pn_net* net, const float* x, const int32_t* labels,
+                      float* loss, void* stream);
+/* Backward in reverse layer order.  Overwrites every parameter
+ * diff (equivalent to S:573's zero-then-accumulate).  With data parallelism
+ * enabled the diffs are summed over ranks (NCCL) before returning. */
+pn_status net_backward(pn_net* net, void* stream);
+/* Solver update: for every parameter, in fp32 without FMA:
+ * g = diff*(1/nranks) + weight_decay*w; v = momentum*v + lr*g; w -= v,
+ * with lr the policy value at `iter`. */
+pn_status sgd_update(pn_net* net, const pn_sgd* sgd, int64_t iter,
+                     void* stream);
+/* forward + backward + sgd_update as one CUDA-graph replay on `stream`. */
+pn_status net_train_step(pn_net* net, const float* x, const int32_t* labels,
+                         const pn_sgd* sgd, int64_t iter, float* loss,
+                         void* stream);
+/* Same step from HOST buffers (e2e path): copies x (N*C*H*W floats) and
+ * labels (N int32) host->device, runs the step, copies the loss back to
+ * *loss_host and synchronises `stream`.  Host buffers should be pinned. */
+pn_status net_train_step_host(pn_net* net, const float* x_host,
+                              const int32_t* labels_host, const pn_sgd* sgd,
+                              int64_t iter, float* loss_host, void* stream);
+/* Forward-only (inference) from the same graph machinery. */
+pn_status net_infer(pn_net* net, const float* x, const int32_t* labels,
+                    float* loss, void* stream);
+
+/* Teacher forcing / profiling: the plan is a list of stages (one kernel
+ * launch each).  Stage i of the forward (phase 0), backward (phase 1) or
+ * update (phase 2) list can be run alone against the current blob contents. */
+pn_status net_stage_count(const pn_net* net, int phase, int* count);
+pn_status net_stage_name(const pn_net* net, int phase, int i,
+                         const char** name);
+pn_status net_run_stage(pn_net* net, int phase, int i, const float* x,
+                        const int32_t* labels, void* stream);
+/* Time `steps` eager training steps with CUDA events around every stage on
+ * `stream`; ms_out[phase-major stage order] = mean milliseconds per launch.
+ * Synchronises.  n_out: number of entries written (must be >= total stages). */
+pn_status net_profile_stages(pn_net* net, const float* x,
+                             const int32_t* labels, const pn_sgd* sgd,
+                             int64_t iter, int steps, float* ms_out, int cap,
+                             int* n_out, void* stream);
+/* Number of kernels one net_train_step launches on the device. */
+pn_status net_launches_per_step(const pn_net* net, int* n);
+
+/* Synchronise `stream` and surface device-side errors (label range). */
+pn_status net_sync_errors(pn_net* net, void* stream);
+
+/* Data parallelism (R13).  Rank 0 calls pn_nccl_unique_id and
+ * broadcasts the 128 bytes; every rank then calls net_dp_init.  Afterwards
+ * net_backward allreduces the parameter diffs (sum) over NCCL, overlapped
+ * with the rest of the backward pass, and sgd_update scales by 1/nranks. */
+pn_status pn_nccl_unique_id(void* out128);
+pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* id128);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PN_H */

@@ -1,0 +1,32 @@
+// kernels.h -- declarations of every __global__ kernel of the library.
+#pragma once
+#include "params.h"
+
+namespace pn {
+// generic per-layer kernels (kernels_generic.cu)
+__global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p);
+__global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p);
+__global__ void conv_bwd_weight_generic(const __grid_constant__ ConvBwdWeightP p);
+__global__ void reduce_partials(const __grid_constant__ ReduceP p);
+__global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p);
+__global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
+__global__ void gemm_generic(const __grid_constant__ GemmP p);
+__global__ void colsum_generic(const __grid_constant__ ColSumP p);
+__global__ void relu_fwd_generic(const __grid_constant__ ReluP p);
+__global__ void relu_bwd_generic(const __grid_constant__ ReluP p);
+__global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p);
+__global__ void loss_reduce(const __grid_constant__ LossReduceP p);
+__global__ void sgd_update_kernel(const __grid_constant__ SgdP p);
+__global__ void mask_convert(const __grid_constant__ MaskExpandP p);
+
+// fused LeNet kernels (kernels_lenet.cu)
+__global__ void lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p);
+__global__ void lenet_conv2_pool2_simt(const __grid_constant__ Conv2Pool2P p);
+__global__ void lenet_ip2_loss(const __grid_constant__ Ip2LossP p);
+__global__ void lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p);
+__global__ void lenet_unpool2(const __grid_constant__ Unpool2P p);
+__global__ void lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p);
+
+constexpr int kGemmTile = 64;
+constexpr int kWgradSplits = 32;
+}  // namespace pn

@@ -1,0 +1,409 @@
+// kernels_generic.cu -- one generic fp32 SIMT kernel per Caffe layer
+// (PN_LAYERWISE plan, and the fallback for nets with no fused pattern).
+//
+// Each kernel implements the layer definition the paper's blocks compute
+// for any geometry; reductions are in fixed order so reruns are
+// bitwise identical (no atomics on data).  The fused LeNet kernels in
+// kernels_lenet.cu / kernels_tc.cu are the performance path.
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace pn {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block-wide sum in fixed order (warp trees, then warp 0 over warp partials).
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* sm) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  float r = 0.f;
+  if (w == 0) {
+    r = (l < NT / 32) ? sm[l] : 0.f;
+    r = warp_sum(r);
+  }
+  return r;  // valid in thread 0
+}
+
+// ---------------------------------------------------------------- conv fwd
+// each output is the inner product of a filter with one sliding
+// window (cross-correlation, R1); bias after the sum (Listing 1).
+__global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)p.N * p.F * p.Ho * p.Wo;
+  if (idx >= total) return;
+  int wo = idx % p.Wo;
+  int ho = (idx / p.Wo) % p.Ho;
+  int f = (idx / ((long long)p.Wo * p.Ho)) % p.F;
+  int n = idx / ((long long)p.Wo * p.Ho * p.F);
+  float acc = 0.f;
+  for (int c = 0; c < p.C; ++c) {
+    const float* xp = p.x + ((long long)n * p.C + c) * p.H * p.W;
+    const float* wp = p.w + ((long long)f * p.C + c) * p.kh * p.kw;
+    for (int i = 0; i < p.kh; ++i) {
+      int h = ho * p.sh - p.ph + i;
+      if (h < 0 || h >= p.H) continue;
+      for (int j = 0; j < p.kw; ++j) {
+        int w = wo * p.sw - p.pw + j;
+        if (w < 0 || w >= p.W) continue;
+        acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(xp + h * p.W + w), acc);
+      }
+    }
+  }
+  if (p.b) acc += __ldg(p.b + f);
+  p.y[idx] = acc;
+}
+
+// col2im(W^T dy) evaluated per input element (gather form).
+__global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)p.N * p.C * p.H * p.W;
+  if (idx >= total) return;
+  int w = idx % p.W;
+  int h = (idx / p.W) % p.H;
+  int c = (idx / ((long long)p.W * p.H)) % p.C;
+  int n = idx / ((long long)p.W * p.H * p.C);
+  float acc = 0.f;
+  for (int f = 0; f < p.F; ++f) {
+    const float* dyp = p.dy + ((long long)n * p.F + f) * p.Ho * p.Wo;
+    const float* wp = p.w + ((long long)f * p.C + c) * p.kh * p.kw;
+    for (int i = 0; i < p.kh; ++i) {
+      int t = h + p.ph - i;
+      if (t < 0 || t % p.sh) continue;
+      int ho = t / p.sh;
+      if (ho >= p.Ho) continue;
+      for (int j = 0; j < p.kw; ++j) {
+        int u = w + p.pw - j;
+        if (u < 0 || u % p.sw) continue;
+        int wo = u / p.sw;
+        if (wo >= p.Wo) continue;
+        acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(dyp + ho * p.Wo + wo), acc);
+      }
+    }
+  }
+  p.dx[idx] = acc;
+}
+
+// dW[f,c,i,j] partial over the images of split s; 16 taps per pass.
+// grid = (F*C, splits), block = 256.
+__global__ void __launch_bounds__(256) conv_bwd_weight_generic(
+    const __grid_constant__ ConvBwdWeightP p) {
+  __shared__ float sm[32];
+  const int f = blockIdx.x / p.C, c = blockIdx.x % p.C, s = blockIdx.y;
+  const int n0 = (int)((long long)p.N * s / p.splits);
+  const int n1 = (int)((long long)p.N * (s + 1) / p.splits);
+  const int P = p.Ho * p.Wo;
+  const long long cnt = (long long)(n1 - n0) * P;
+  const int taps = p.kh * p.kw;
+  for (int t0 = 0; t0 < taps; t0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+    float bacc = 0.f;
+    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
+      int n = n0 + (int)(e / P);
+      int pos = (int)(e % P);
+      int ho = pos / p.Wo, wo = pos % p.Wo;
+      float g = __ldg(p.dy + ((long long)n * p.F + f) * P + pos);
+      if (t0 == 0) bacc += g;
+      const float* xp = p.x + ((long long)n * p.C + c) * p.H * p.W;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        int t = t0 + q;
+        if (t < taps) {
+          int i = t / p.kw, j = t % p.kw;
+          int h = ho * p.sh - p.ph + i, w = wo * p.sw - p.pw + j;
+          if (h >= 0 && h < p.H && w >= 0 && w < p.W)
+            acc[q] = fmaf(g, __ldg(xp + h * p.W + w), acc[q]);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int q = 0; q < 16; ++q) {
+      if (t0 + q >= taps) break;
+      float r = block_sum<256>(acc[q], sm);
+      if (threadIdx.x == 0)
+        p.part_w[(long long)s * p.pstride + ((long long)f * p.C + c) * taps + t0 + q] = r;
+    }
+    if (t0 == 0 && c == 0 && p.part_b) {
+      float r = block_sum<256>(bacc, sm);
+      if (threadIdx.x == 0) p.part_b[(long long)s * p.pstride + f] = r;
+    }
+  }
+}
+
+__global__ void reduce_partials(const __grid_constant__ ReduceP p) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  float acc = 0.f;
+  for (int s = 0; s < p.splits; ++s) acc += p.part[(long long)s * p.n + i];
+  p.out[i] = acc;
+}
+
+// ------------------------------------------------------------------ pooling
+// P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
+// a row-major scan (strict >) and stores its plane-local index h*W+w.
+__global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)p.N * p.C * p.Hp * p.Wp;
+  if (idx >= total) return;
+  int b = idx % p.Wp;
+  int a = (idx / p.Wp) % p.Hp;
+  long long nc = idx / ((long long)p.Wp * p.Hp);
+  const float* xp = p.x + nc * p.H * p.W;
+  int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
+  int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+  int size = (he - hs) * (we - ws);
+  hs = max(hs, 0);
+  ws = max(ws, 0);
+  he = min(he, p.H);
+  we = min(we, p.W);
+  if (p.method == 0) {
+    float best = xp[hs * p.W + ws];
+    int arg = hs * p.W + ws;
+    for (int h = hs; h < he; ++h)
+      for (int w = ws; w < we; ++w) {
+        float v = xp[h * p.W + w];
+        if (v > best) {
+          best = v;
+          arg = h * p.W + w;
+        }
+      }
+    p.y[idx] = best;
+    p.mask[idx] = arg;
+  } else {
+    float acc = 0.f;
+    for (int h = hs; h < he; ++h)
+      for (int w = ws; w < we; ++w) acc += xp[h * p.W + w];
+    p.y[idx] = __fdiv_rn(acc, (float)size);
+  }
+}
+
+// each input sums the output gradients routed to it, in ascending
+// output order (the oracle's scatter order) -- no atomics.
+__global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)p.N * p.C * p.H * p.W;
+  if (idx >= total) return;
+  int w = idx % p.W;
+  int h = (idx / p.W) % p.H;
+  long long nc = idx / ((long long)p.W * p.H);
+  int a0 = (h + p.ph < p.kh) ? 0 : (h + p.ph - p.kh) / p.sh + 1;
+  int a1 = min((h + p.ph) / p.sh, p.Hp - 1);
+  int b0 = (w + p.pw < p.kw) ? 0 : (w + p.pw - p.kw) / p.sw + 1;
+  int b1 = min((w + p.pw) / p.sw, p.Wp - 1);
+  const float* dyp = p.dy + nc * p.Hp * p.Wp;
+  float acc = 0.f;
+  if (p.method == 0) {
+    const int32_t* mp = p.mask + nc * p.Hp * p.Wp;
+    int me = h * p.W + w;
+    for (int a = a0; a <= a1; ++a)
+      for (int b = b0; b <= b1; ++b)
+        if (mp[a * p.Wp + b] == me) acc += dyp[a * p.Wp + b];
+  } else {
+    for (int a = a0; a <= a1; ++a)
+      for (int b = b0; b <= b1; ++b) {
+        int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
+        int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+        int size = (he - hs) * (we - ws);
+        acc += __fdiv_rn(dyp[a * p.Wp + b], (float)size);
+      }
+  }
+  p.dx[idx] = acc;
+}
+
+// -------------------------------------------------------------------- GEMM
+// 64x64 tile, BK 16, 256 threads x (4x4) outputs; arbitrary strides so one
+// kernel serves ip fwd (x W^T), dgrad (dy W) and wgrad (dy^T x).
+__global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ GemmP p) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < p.K; k0 += 16) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      int e = tid + 256 * r;
+      int mm, kk;
+      if (p.sak == 1) { mm = e / 16; kk = e % 16; } else { kk = e / 64; mm = e % 64; }
+      int gm = m0 + mm, gk = k0 + kk;
+      As[kk][mm] = (gm < p.M && gk < p.K) ? p.A[gm * p.sam + gk * p.sak] : 0.f;
+      int nn;
+      if (p.sbn == 1) { kk = e / 64; nn = e % 64; } else { nn = e / 16; kk = e % 16; }
+      int gn = n0 + nn;
+      gk = k0 + kk;
+      Bs[kk][nn] = (gn < p.N && gk < p.K) ? p.B[gk * p.sbk + gn * p.sbn] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][tm + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tn + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + tm + i;
+    if (gm >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + tn + j;
+      if (gn >= p.N) continue;
+      float v = acc[i][j];
+      if (p.bias) v += p.bias[gn];
+      if (p.relu) v = v > 0.f ? v : 0.f;
+      p.C[(long long)gm * p.N + gn] = v;
+    }
+  }
+}
+
+// db[n] = sum_m dy[m, n] (InnerProduct bias gradient)
+__global__ void __launch_bounds__(256) colsum_generic(const __grid_constant__ ColSumP p) {
+  __shared__ float sm[32];
+  const int n = blockIdx.x;
+  float acc = 0.f;
+  for (int m = threadIdx.x; m < p.M; m += blockDim.x) acc += p.a[(long long)m * p.N + n];
+  float r = block_sum<256>(acc, sm);
+  if (threadIdx.x == 0) p.out[n] = r;
+}
+
+// --------------------------------------------------------------------- ReLU
+__global__ void relu_fwd_generic(const __grid_constant__ ReluP p) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  float v = p.x[i];
+  p.out[i] = v > 0.f ? v : __fmul_rn(p.slope, v);
+}
+
+// dX = dY * (y > 0 ? 1 : slope), y = in-place forward output (R8)
+__global__ void relu_bwd_generic(const __grid_constant__ ReluP p) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= p.n) return;
+  float g = p.x[i];
+  p.out[i] = p.y[i] > 0.f ? g : __fmul_rn(g, p.slope);
+}
+
+// ----------------------------------------------------------- softmax + loss
+// One warp per sample: stable softmax, per-row loss term, lowest-index
+// argmax, and the loss gradient (p - onehot) * loss_weight / M.
+__global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p) {
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (row >= p.M) return;
+  const float* x = p.logits + (long long)row * p.D;
+  float best = -FLT_MAX;
+  int arg = 0x7fffffff;
+  for (int j = lane; j < p.D; j += 32) {
+    float v = x[j];
+    if (v > best || arg == 0x7fffffff) { best = v; arg = j; }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+    if (ob > best || (ob == best && oa < arg)) { best = ob; arg = oa; }
+  }
+  float s = 0.f;
+  for (int j = lane; j < p.D; j += 32) s += expf(x[j] - best);
+  s = warp_sum(s);
+  int y = p.labels[row];
+  bool bad = (y < 0 || y >= p.D);
+  if (bad && lane == 0) atomicOr(p.err, 1u);
+  if (bad) y = 0;
+  for (int j = lane; j < p.D; j += 32) {
+    float pj = __fdiv_rn(expf(x[j] - best), s);
+    p.prob[(long long)row * p.D + j] = pj;
+    p.dlogits[(long long)row * p.D + j] = __fmul_rn(pj - (j == y ? 1.f : 0.f), p.grad_scale);
+  }
+  if (lane == 0) {
+    float py = __fdiv_rn(expf(x[y] - best), s);
+    p.row_loss[row] = -logf(fmaxf(py, FLT_MIN));
+    p.pred[row] = arg;
+  }
+}
+
+// loss = (1/M) sum_i row_loss[i], fixed-order block reduction (one block)
+__global__ void __launch_bounds__(256) loss_reduce(const __grid_constant__ LossReduceP p) {
+  __shared__ float sm[32];
+  float acc = 0.f;
+  for (int i = threadIdx.x; i < p.M; i += blockDim.x) acc += p.row_loss[i];
+  float r = block_sum<256>(acc, sm);
+  if (threadIdx.x == 0) {
+    r = r * p.inv_M;
+    p.loss_blob[0] = r;
+    if (p.loss_out) p.loss_out[0] = r;
+  }
+}
+
+// ---------------------------------------------------------------------- SGD
+// S:536-544 / DESIGN.md R11: one IEEE fp32 rounding per op, no contraction.
+__device__ __forceinline__ void sgd_one(float& w, float d, float& v, float lr, float mom,
+                                        float decay, float gs) {
+  float g = __fmul_rn(d, gs);
+  g = __fadd_rn(g, __fmul_rn(decay, w));
+  v = __fadd_rn(__fmul_rn(mom, v), __fmul_rn(lr, g));
+  w = __fsub_rn(w, v);
+}
+
+__global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
+  long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long n4 = p.n / 4;
+  for (; i4 < n4; i4 += (long long)gridDim.x * blockDim.x) {
+    float4 w = reinterpret_cast<float4*>(p.w)[i4];
+    float4 v = reinterpret_cast<float4*>(p.v)[i4];
+    float4 g = reinterpret_cast<const float4*>(p.g)[i4];
+    sgd_one(w.x, g.x, v.x, p.lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.y, g.y, v.y, p.lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.z, g.z, v.z, p.lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.w, g.w, v.w, p.lr, p.mom, p.decay, p.gscale);
+    reinterpret_cast<float4*>(p.w)[i4] = w;
+    reinterpret_cast<float4*>(p.v)[i4] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x < (p.n & 3)) {
+    long long i = n4 * 4 + threadIdx.x;
+    float w = p.w[i], v = p.v[i];
+    sgd_one(w, p.g[i], v, p.lr, p.mom, p.decay, p.gscale);
+    p.w[i] = w;
+    p.v[i] = v;
+  }
+}
+
+// ----------------------------------------------------- mask representation
+// The fused plan stores the max-pool origin as a uint8 offset inside the
+// (clipped) window: (h - hs)*kw + (w - ws).  The ABI view is int32 h*W + w.
+__global__ void mask_convert(const __grid_constant__ MaskExpandP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long total = (long long)p.N * p.C * p.Hp * p.Wp;
+  if (idx >= total) return;
+  int b = idx % p.Wp;
+  int a = (idx / p.Wp) % p.Hp;
+  int hs = max(a * p.sh - p.ph, 0), ws = max(b * p.sw - p.pw, 0);
+  if (p.to32) {
+    int off = p.m8[idx];
+    p.m32[idx] = (hs + off / p.kw) * p.W + ws + off % p.kw;
+  } else {
+    int m = p.m32[idx];
+    p.m8[idx] = (uint8_t)((m / p.W - hs) * p.kw + (m % p.W - ws));
+  }
+}
+
+}  // namespace pn

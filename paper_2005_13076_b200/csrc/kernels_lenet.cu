@@ -1,0 +1,319 @@
+// kernels_lenet.cu -- fused SIMT fp32 kernels for the LeNet chain
+// (conv1 5x5 1->20 on 28x28, pool 2x2/2, conv2 5x5 20->50, pool 2x2/2,
+// ip1 800->500 + relu, ip2 500->10 + softmax-loss).
+//
+// Fusion: conv1+pool1 never stores the 24x24 conv output;
+// ip2+softmax+loss+argmax+dlogits is one pass; ip2 backward also applies the
+// relu1 derivative; conv1's weight gradient reads the pooled gradient and
+// the pool mask directly (the unpooled 24x24 gradient is never stored).
+// Max-pool origins are stored as uint8 window offsets.
+#include <cfloat>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace pn {
+
+// ------------------------------------------------------------ conv1 + pool1
+// Block: 2 images, 288 threads; item = (image, filter group of 4, pooled
+// position q of 144) -> 4 pooled outputs per item (each = max of 4 conv
+// values of 25 MACs).  Ties: first of (0,0),(0,1),(1,0),(1,1).
+constexpr int C1_IMGS = 2;
+__global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+  __shared__ float xs[C1_IMGS][28 * 28];
+  __shared__ __align__(16) float ws[20][28];
+  __shared__ float bs[20];
+  const int n0 = blockIdx.x * C1_IMGS;
+  for (int i = threadIdx.x; i < C1_IMGS * 784; i += blockDim.x) {
+    int im = i / 784, e = i % 784;
+    xs[im][e] = (n0 + im < p.N) ? __ldg(p.x + (long long)(n0 + im) * 784 + e) : 0.f;
+  }
+  for (int i = threadIdx.x; i < 20 * 28; i += blockDim.x) {
+    int f = i / 28, t = i % 28;
+    ws[f][t] = t < 25 ? __ldg(p.w + f * 25 + t) : 0.f;
+  }
+  if (threadIdx.x < 20) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
+  __syncthreads();
+  for (int it = threadIdx.x; it < C1_IMGS * 720; it += blockDim.x) {
+    const int im = it / 720, r = it % 720, g = r / 144, q = r % 144;
+    const int n = n0 + im;
+    if (n >= p.N) break;
+    const int ph = q / 12, pw = q % 12;
+    float patch[6][6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a)
+#pragma unroll
+      for (int b = 0; b < 6; ++b) patch[a][b] = xs[im][(2 * ph + a) * 28 + 2 * pw + b];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int f = 4 * g + t;
+      float c00 = 0.f, c01 = 0.f, c10 = 0.f, c11 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const float wv = ws[f][i * 5 + j];
+          c00 = fmaf(wv, patch[i][j], c00);
+          c01 = fmaf(wv, patch[i][j + 1], c01);
+          c10 = fmaf(wv, patch[i + 1][j], c10);
+          c11 = fmaf(wv, patch[i + 1][j + 1], c11);
+        }
+      const float bb = bs[f];
+      c00 += bb; c01 += bb; c10 += bb; c11 += bb;
+      float best = c00;
+      int off = 0;
+      if (c01 > best) { best = c01; off = 1; }
+      if (c10 > best) { best = c10; off = 2; }
+      if (c11 > best) { best = c11; off = 3; }
+      const long long o = ((long long)n * 20 + f) * 144 + q;
+      p.p1[o] = best;
+      p.m1[o] = (uint8_t)off;
+    }
+  }
+}
+
+// ------------------------------------------------------------ conv2 + pool2
+// Persistent: each CTA stages all conv2 weights (50x20x25, padded to 28 per
+// (f,c)) once, then loops over image pairs.  Thread = (image, filter group
+// of 5, pooled position of 16): 20 accumulators (2x2 window x 5 filters).
+constexpr int C2_IMGS = 2;
+constexpr int C2_THREADS = 320;
+__global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
+    const __grid_constant__ Conv2Pool2P p) {
+  extern __shared__ __align__(16) float smem[];
+  float* ws = smem;                    // [50][20][28]
+  float* xs = smem + 50 * 20 * 28;     // [2][20][144]
+  __shared__ float bs[50];
+  for (int i = threadIdx.x; i < 50 * 20 * 28; i += blockDim.x) {
+    int fc = i / 28, t = i % 28;
+    ws[i] = t < 25 ? __ldg(p.w + fc * 25 + t) : 0.f;
+  }
+  if (threadIdx.x < 50) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
+  const int im = threadIdx.x / 160, r = threadIdx.x % 160, g = r / 16, q = r % 16;
+  const int ph = q / 4, pw = q % 4;
+  for (int n0 = blockIdx.x * C2_IMGS; n0 < p.N; n0 += gridDim.x * C2_IMGS) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < C2_IMGS * 2880; i += blockDim.x) {
+      int ii = i / 2880, e = i % 2880;
+      xs[i] = (n0 + ii < p.N) ? __ldg(p.p1 + (long long)(n0 + ii) * 2880 + e) : 0.f;
+    }
+    __syncthreads();
+    const int n = n0 + im;
+    float acc[5][4];
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc[t][u] = 0.f;
+    const float* xi = xs + im * 2880;
+#pragma unroll 1
+    for (int c = 0; c < 20; ++c) {
+      float patch[6][6];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 6; ++b) patch[a][b] = xi[c * 144 + (2 * ph + a) * 12 + 2 * pw + b];
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const float4* wv4 = reinterpret_cast<const float4*>(ws + ((5 * g + t) * 20 + c) * 28);
+        float wv[28];
+#pragma unroll
+        for (int z = 0; z < 7; ++z) {
+          float4 v = wv4[z];
+          wv[4 * z] = v.x; wv[4 * z + 1] = v.y; wv[4 * z + 2] = v.z; wv[4 * z + 3] = v.w;
+        }
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+          for (int j = 0; j < 5; ++j) {
+            const float w = wv[i * 5 + j];
+            acc[t][0] = fmaf(w, patch[i][j], acc[t][0]);
+            acc[t][1] = fmaf(w, patch[i][j + 1], acc[t][1]);
+            acc[t][2] = fmaf(w, patch[i + 1][j], acc[t][2]);
+            acc[t][3] = fmaf(w, patch[i + 1][j + 1], acc[t][3]);
+          }
+      }
+    }
+    if (n < p.N) {
+#pragma unroll
+      for (int t = 0; t < 5; ++t) {
+        const int f = 5 * g + t;
+        const float bb = bs[f];
+        float best = acc[t][0] + bb;
+        int off = 0;
+        float v;
+        v = acc[t][1] + bb; if (v > best) { best = v; off = 1; }
+        v = acc[t][2] + bb; if (v > best) { best = v; off = 2; }
+        v = acc[t][3] + bb; if (v > best) { best = v; off = 3; }
+        const long long o = ((long long)n * 50 + f) * 16 + q;
+        p.p2[o] = best;
+        p.m2[o] = (uint8_t)off;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------- ip2 + softmax-with-loss
+// Warp per sample: logits = a1 . W2^T + b2 (W2 staged in smem), then the
+// stable softmax, per-row loss term, lowest-index argmax and the loss
+// gradient dz = (p - onehot) * loss_weight / M.
+__global__ void __launch_bounds__(256) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
+  __shared__ __align__(16) float ws[10 * 500];
+  __shared__ float bs[10];
+  for (int i = threadIdx.x; i < 5000; i += blockDim.x) ws[i] = __ldg(p.w + i);
+  if (threadIdx.x < 10) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (row >= p.N) return;
+  const float* a = p.a1 + (long long)row * 500;
+  float acc[10];
+#pragma unroll
+  for (int o = 0; o < 10; ++o) acc[o] = 0.f;
+  for (int k = lane; k < 500; k += 32) {
+    const float av = __ldg(a + k);
+#pragma unroll
+    for (int o = 0; o < 10; ++o) acc[o] = fmaf(av, ws[o * 500 + k], acc[o]);
+  }
+#pragma unroll
+  for (int o = 0; o < 10; ++o) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) acc[o] += __shfl_xor_sync(0xffffffffu, acc[o], s);
+    acc[o] += bs[o];
+  }
+  float best = acc[0];
+  int arg = 0;
+#pragma unroll
+  for (int o = 1; o < 10; ++o)
+    if (acc[o] > best) { best = acc[o]; arg = o; }
+  float e[10], s = 0.f;
+#pragma unroll
+  for (int o = 0; o < 10; ++o) { e[o] = expf(acc[o] - best); s += e[o]; }
+  int y = p.labels[row];
+  bool bad = (y < 0 || y >= 10);
+  if (bad) { if (lane == 0) atomicOr(p.err, 1u); y = 0; }
+  if (lane < 10) {
+    float lo = 0.f, pv = 0.f;
+#pragma unroll
+    for (int o = 0; o < 10; ++o)
+      if (o == lane) { lo = acc[o]; pv = __fdiv_rn(e[o], s); }
+    p.logits[(long long)row * 10 + lane] = lo;
+    p.prob[(long long)row * 10 + lane] = pv;
+    p.dz[(long long)row * 10 + lane] = __fmul_rn(pv - (lane == y ? 1.f : 0.f), p.grad_scale);
+  }
+  if (lane == 0) {
+    float ey = 0.f;
+#pragma unroll
+    for (int o = 0; o < 10; ++o)
+      if (o == y) ey = e[o];
+    p.row_loss[row] = -logf(fmaxf(__fdiv_rn(ey, s), FLT_MIN));
+    p.pred[row] = arg;
+  }
+}
+
+// ------------------------------------------------ ip2 backward + relu1 bwd
+// grid (4 column chunks of 128, splits over samples).  Thread = column k:
+// da1[m,k] = (a1[m,k] > 0) * sum_o dz[m,o] W2[o,k]   (S:387 + S:405)
+// partial dW2[o,k] = sum_{m in split} dz[m,o] a1[m,k];  partial db2[o].
+__global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p) {
+  const int k = blockIdx.x * 128 + threadIdx.x;
+  const int s = blockIdx.y;
+  const int m0 = (int)((long long)p.N * s / p.splits), m1 = (int)((long long)p.N * (s + 1) / p.splits);
+  __shared__ float dzs[64][10];
+  float w2[10], acc[10];
+  const bool valid = k < 500;
+#pragma unroll
+  for (int o = 0; o < 10; ++o) {
+    w2[o] = valid ? __ldg(p.w + o * 500 + k) : 0.f;
+    acc[o] = 0.f;
+  }
+  float bacc = 0.f;
+  for (int mb = m0; mb < m1; mb += 64) {
+    const int cnt = min(64, m1 - mb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * 10; i += 128) dzs[i / 10][i % 10] = p.dz[(long long)mb * 10 + i];
+    __syncthreads();
+    for (int mm = 0; mm < cnt; ++mm) {
+      const int m = mb + mm;
+      if (valid) {
+        const float a = p.a1[(long long)m * 500 + k];
+        float g = 0.f;
+#pragma unroll
+        for (int o = 0; o < 10; ++o) {
+          const float d = dzs[mm][o];
+          g = fmaf(d, w2[o], g);
+          acc[o] = fmaf(d, a, acc[o]);
+        }
+        p.da1[(long long)m * 500 + k] = a > 0.f ? g : 0.f;
+      }
+      if (blockIdx.x == 0 && threadIdx.x < 10) bacc += dzs[mm][threadIdx.x];
+    }
+  }
+  if (valid) {
+#pragma unroll
+    for (int o = 0; o < 10; ++o) p.part_w[(long long)s * p.pstride + o * 500 + k] = acc[o];
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 10) p.part_b[(long long)s * p.pstride + threadIdx.x] = bacc;
+}
+
+// dp2 [N, 50*16] + mask -> dense conv2 output gradient G2 [N,50,8,8]
+// (max-pool backward: each gradient goes to its stored origin).
+__global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over N*50*64
+  if (idx >= (long long)p.N * 3200) return;
+  const int pos = idx % 64;
+  const long long nf = idx / 64;
+  const int h = pos / 8, w = pos % 8;
+  const int q = (h >> 1) * 4 + (w >> 1);
+  const int off = (h & 1) * 2 + (w & 1);
+  const long long o = nf * 16 + q;
+  p.g2[idx] = (p.m2[o] == off) ? p.dp2[o] : 0.f;
+}
+
+// ---------------------------------------------------- conv1 weight gradient
+// dW1[f,i,j] = sum_n sum_q dp1[n,f,q] * x[n, h_q + i, w_q + j] where (h_q,w_q)
+// is the conv1 position pool1 routed gradient q to (P:220-222 composed with
+// S:351); db1[f] = sum dp1.  grid = splits over images, block = 320 threads
+// (20 filters x 16 lanes), images staged in smem.
+__global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
+  __shared__ float xs[4][784];
+  const int s = blockIdx.x;
+  const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
+  const int f = threadIdx.x / 16, l = threadIdx.x % 16;
+  float acc[25], bacc = 0.f;
+#pragma unroll
+  for (int t = 0; t < 25; ++t) acc[t] = 0.f;
+  for (int nb = n0; nb < n1; nb += 4) {
+    const int cnt = min(4, n1 - nb);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x) xs[i / 784][i % 784] = __ldg(p.x + (long long)nb * 784 + i);
+    __syncthreads();
+    for (int im = 0; im < cnt; ++im) {
+      const long long base = ((long long)(nb + im) * 20 + f) * 144;
+      for (int q = l; q < 144; q += 16) {
+        const float g = __ldg(p.dp1 + base + q);
+        const int off = p.m1[base + q];
+        const int h = 2 * (q / 12) + (off >> 1), w = 2 * (q % 12) + (off & 1);
+        bacc += g;
+        const float* xp = &xs[im][h * 28 + w];
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+#pragma unroll
+          for (int j = 0; j < 5; ++j) acc[i * 5 + j] = fmaf(g, xp[i * 28 + j], acc[i * 5 + j]);
+      }
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 25; ++t) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) acc[t] += __shfl_xor_sync(0xffffffffu, acc[t], o);
+  }
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) bacc += __shfl_xor_sync(0xffffffffu, bacc, o);
+  if (l == 0) {
+#pragma unroll
+    for (int t = 0; t < 25; ++t) p.part_w[(long long)s * p.pstride + f * 25 + t] = acc[t];
+    p.part_b[(long long)s * p.pstride + f] = bacc;
+  }
+}
+
+}  // namespace pn

@@ -1,0 +1,1189 @@
+// net.cu -- the C ABI (include/pn.h): spec parsing, shape inference, device
+// memory, the stage plan (fused LeNet or layerwise), eager execution, CUDA
+// graph capture/replay with per-step kernel-node patching, profiling, and the
+// NCCL data-parallel gradient exchange.
+//
+// The paper's Net runs every layer forward in order and back-propagates in
+// reverse order after the loss; the solver then updates.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "../../include/pn.h"
+#include "kernels.h"
+#include "runtime.h"
+#include "tc.h"
+
+using namespace pn;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+static pn_status fail(pn_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+#define CU(x)                                                                        \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(PN_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+#define NC(x)                                                                        \
+  do {                                                                               \
+    ncclResult_t r_ = (x);                                                           \
+    if (r_ != ncclSuccess)                                                           \
+      return fail(PN_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+#define TRY(x)                  \
+  do {                          \
+    pn_status s_ = (x);         \
+    if (s_ != PN_OK) return s_; \
+  } while (0)
+
+extern "C" const char* pn_last_error(void) { return g_err.c_str(); }
+
+// -------------------------------------------------------------- spec model
+namespace {
+
+enum LType { L_CONV, L_POOL, L_IP, L_RELU, L_LOSS };
+
+struct Layer {
+  LType type;
+  std::string name, bottom, top;
+  int in[4] = {0, 0, 0, 0}, out[4] = {0, 0, 0, 0};
+  int F = 0, kh = 0, kw = 0, sh = 1, sw = 1, ph = 0, pw = 0;  // conv / pool
+  int method = 0;                                             // pool
+  int K = 0, Nout = 0;                                        // ip
+  bool bias = true;
+  float slope = 0.f;
+  // parameters (conv / ip)
+  int64_t wcount = 0, bcount = 0, off = -1;  // offset of w in the flat buffers, b follows w
+  int64_t part_off = -1;                     // partial-sum region (split wgrads)
+  int splits = 0;
+};
+
+struct Blob {
+  std::string name;
+  int dims[4] = {0, 0, 0, 0};
+  bool is_param = false, materialised = true, is_input = false;
+  float* data = nullptr;
+  float* diff = nullptr;
+  float* hist = nullptr;
+  int32_t* m32 = nullptr;  // layerwise max-pool mask (plane-local)
+  uint8_t* m8 = nullptr;   // fused max-pool mask (window offset)
+  int pool_layer = -1;     // index of the pooling layer producing it
+  int64_t count() const { return (int64_t)dims[0] * dims[1] * dims[2] * dims[3]; }
+};
+
+std::string trim(const std::string& s) {
+  size_t a = s.find_first_not_of(" \t\r"), b = s.find_last_not_of(" \t\r");
+  return a == std::string::npos ? "" : s.substr(a, b - a + 1);
+}
+
+typedef std::vector<std::pair<std::string, std::string>> KV;
+
+bool allowed_key(const std::string& type, const std::string& k) {
+  static const char* common[] = {"name", "type", "bottom", "top"};
+  for (auto c : common)
+    if (k == c) return true;
+  static const char* geo[] = {"kernel_size", "kernel_h", "kernel_w", "stride", "stride_h",
+                              "stride_w",    "pad",      "pad_h",    "pad_w"};
+  if (type == "Convolution") {
+    if (k == "num_output" || k == "bias_term") return true;
+    for (auto g : geo)
+      if (k == g) return true;
+  } else if (type == "Pooling") {
+    if (k == "pool") return true;
+    for (auto g : geo)
+      if (k == g) return true;
+  } else if (type == "InnerProduct") {
+    return k == "num_output" || k == "bias_term";
+  } else if (type == "ReLU") {
+    return k == "negative_slope";
+  }
+  return false;
+}
+
+const std::string* get(const KV& kv, const std::string& k) {
+  for (auto& p : kv)
+    if (p.first == k) return &p.second;
+  return nullptr;
+}
+
+bool parse_int(const std::string& s, int* v) {
+  char* e = nullptr;
+  long x = strtol(s.c_str(), &e, 10);
+  if (!e || *e) return false;
+  *v = (int)x;
+  return true;
+}
+
+int conv_out(int in, int k, int s, int p) {
+  int num = in + 2 * p - k;
+  if (in <= 0 || k <= 0 || s <= 0 || p < 0 || num < 0) return -1;
+  return num / s + 1;
+}
+// DESIGN.md R4 (Caffe ceil sizing)
+int pool_out(int in, int k, int s, int p) {
+  int num = in + 2 * p - k;
+  if (in <= 0 || k <= 0 || s <= 0 || p < 0 || p >= k || num < 0) return -1;
+  int o = (num + s - 1) / s + 1;
+  if (p > 0 && (o - 1) * s >= in + p) o--;
+  return o;
+}
+
+}  // namespace
+
+// -------------------------------------------------------------------- net
+struct pn_net {
+  int device = 0, batch = 0, flags = 0;
+  bool tf32 = false, fused = false;
+  std::vector<Layer> layers;
+  std::vector<Blob> blobs;
+  std::string input_name;
+  int classes = 0;
+
+  float* params = nullptr;
+  float* grads = nullptr;
+  float* hist = nullptr;
+  int64_t nparams = 0;      // padded total
+  int64_t nlearn = 0;       // unpadded learnable count
+  float* partials = nullptr;
+  int64_t npartials = 0;
+  float* row_loss = nullptr;
+  unsigned* err = nullptr;
+  std::vector<void*> allocs;
+
+  std::vector<Stage> phase[3];  // 0 fwd, 1 bwd, 2 update
+  bool forward_done = false;
+  StepArgs last;  // for eager stage patching
+
+  cudaStream_t cap = nullptr;  // capture stream
+  cudaGraphExec_t step_exec = nullptr, infer_exec = nullptr;
+  StepArgs step_args, infer_args;  // args baked into the executable graphs
+  int launches_per_step = 0;
+
+  // data parallel
+  int nranks = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
+  int64_t bucket_split = 0;  // params [0, split) = ip bucket, [split, n) = conv bucket
+  int tc_sms = 148;
+
+  int blob(const std::string& n) const {
+    for (size_t i = 0; i < blobs.size(); ++i)
+      if (blobs[i].name == n) return (int)i;
+    return -1;
+  }
+  template <class T>
+  pn_status alloc(T** p, size_t count) {
+    void* v = nullptr;
+    cudaError_t e = cudaMalloc(&v, count * sizeof(T) + 16);
+    if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+    cudaMemset(v, 0, count * sizeof(T) + 16);
+    allocs.push_back(v);
+    *p = (T*)v;
+    return PN_OK;
+  }
+};
+
+// ------------------------------------------------------------ spec parsing
+static pn_status parse_and_infer(pn_net* net, const char* text) {
+  std::vector<std::pair<std::string, KV>> sections;
+  std::istringstream in(text);
+  std::string raw;
+  int lineno = 0;
+  while (std::getline(in, raw)) {
+    ++lineno;
+    std::string line = raw.substr(0, raw.find('#'));
+    line = trim(line);
+    if (line.empty()) continue;
+    if (line.front() == '[' && line.back() == ']') {
+      sections.push_back({trim(line.substr(1, line.size() - 2)), KV()});
+      continue;
+    }
+    size_t eq = line.find('=');
+    if (sections.empty() || eq == std::string::npos)
+      return fail(PN_ERR_PARSE, "spec line " + std::to_string(lineno) + ": expected key = value");
+    sections.back().second.push_back({trim(line.substr(0, eq)), trim(line.substr(eq + 1))});
+  }
+  if (sections.empty() || sections[0].first != "input")
+    return fail(PN_ERR_PARSE, "spec must start with an [input] section");
+  int C = 0, H = 0, W = 0;
+  for (auto& kv : sections[0].second) {
+    int v = 0;
+    if (kv.first == "name") net->input_name = kv.second;
+    else if (kv.first == "channels" && parse_int(kv.second, &v)) C = v;
+    else if (kv.first == "height" && parse_int(kv.second, &v)) H = v;
+    else if (kv.first == "width" && parse_int(kv.second, &v)) W = v;
+    else return fail(PN_ERR_PARSE, "[input]: bad key or value '" + kv.first + "'");
+  }
+  if (net->input_name.empty() || C <= 0 || H <= 0 || W <= 0)
+    return fail(PN_ERR_SHAPE, "[input] needs name, channels, height, width > 0");
+  Blob in_blob;
+  in_blob.name = net->input_name;
+  in_blob.dims[0] = net->batch; in_blob.dims[1] = C; in_blob.dims[2] = H; in_blob.dims[3] = W;
+  in_blob.is_input = true;
+  in_blob.materialised = false;
+  net->blobs.push_back(in_blob);
+
+  for (size_t si = 1; si < sections.size(); ++si) {
+    if (sections[si].first != "layer") return fail(PN_ERR_PARSE, "unknown section [" + sections[si].first + "]");
+    const KV& kv = sections[si].second;
+    const std::string* type = get(kv, "type");
+    const std::string *name = get(kv, "name"), *bottom = get(kv, "bottom"), *top = get(kv, "top");
+    if (!type) return fail(PN_ERR_PARSE, "layer without type");
+    Layer L;
+    if (*type == "Convolution") L.type = L_CONV;
+    else if (*type == "Pooling") L.type = L_POOL;
+    else if (*type == "InnerProduct") L.type = L_IP;
+    else if (*type == "ReLU") L.type = L_RELU;
+    else if (*type == "SoftmaxWithLoss") L.type = L_LOSS;
+    else return fail(PN_ERR_UNKNOWN_LAYER, "unknown layer type " + *type);
+    for (auto& p : kv)
+      if (!allowed_key(*type, p.first)) return fail(PN_ERR_PARSE, "unknown key '" + p.first + "' for " + *type);
+    if (!name || !bottom || !top) return fail(PN_ERR_PARSE, "layer needs name, bottom, top");
+    L.name = *name; L.bottom = *bottom; L.top = *top;
+    int bi = net->blob(L.bottom);
+    if (bi < 0) return fail(PN_ERR_DANGLING_BLOB, "layer " + L.name + ": bottom '" + L.bottom + "' not produced earlier");
+    memcpy(L.in, net->blobs[bi].dims, sizeof(L.in));
+    auto geo = [&](const char* base, int def, int* h, int* w) -> bool {
+      std::string b = base;
+      const std::string* both = get(kv, b == "kernel" ? "kernel_size" : b);
+      const std::string* hs = get(kv, b + "_h");
+      const std::string* ws = get(kv, b + "_w");
+      *h = *w = def;
+      if (both && !(parse_int(*both, h) && parse_int(*both, w))) return false;
+      if (hs && !parse_int(*hs, h)) return false;
+      if (ws && !parse_int(*ws, w)) return false;
+      return *h >= 0 && *w >= 0;
+    };
+    if (L.type == L_CONV || L.type == L_POOL) {
+      if (!geo("kernel", -1, &L.kh, &L.kw) || L.kh <= 0 || L.kw <= 0 || !geo("stride", 1, &L.sh, &L.sw) ||
+          !geo("pad", 0, &L.ph, &L.pw))
+        return fail(PN_ERR_PARSE, "layer " + L.name + ": bad kernel/stride/pad");
+    }
+    L.out[0] = L.in[0];
+    if (L.type == L_CONV) {
+      const std::string* no = get(kv, "num_output");
+      if (!no || !parse_int(*no, &L.F) || L.F <= 0) return fail(PN_ERR_PARSE, L.name + ": num_output");
+      const std::string* bt = get(kv, "bias_term");
+      L.bias = !(bt && *bt == "false");
+      int Ho = conv_out(L.in[2], L.kh, L.sh, L.ph), Wo = conv_out(L.in[3], L.kw, L.sw, L.pw);
+      if (Ho < 1 || Wo < 1) return fail(PN_ERR_SHAPE, L.name + ": non-positive output size");
+      L.out[1] = L.F; L.out[2] = Ho; L.out[3] = Wo;
+      L.wcount = (int64_t)L.F * L.in[1] * L.kh * L.kw;
+      L.bcount = L.bias ? L.F : 0;
+    } else if (L.type == L_POOL) {
+      const std::string* pm = get(kv, "pool");
+      if (!pm || *pm == "MAX") L.method = 0;
+      else if (*pm == "AVE") L.method = 1;
+      else return fail(PN_ERR_PARSE, L.name + ": pool must be MAX or AVE");
+      int Hp = pool_out(L.in[2], L.kh, L.sh, L.ph), Wp = pool_out(L.in[3], L.kw, L.sw, L.pw);
+      if (Hp < 1 || Wp < 1) return fail(PN_ERR_SHAPE, L.name + ": non-positive output size");
+      if (L.method == 0 && L.kh * L.kw > 255) return fail(PN_ERR_SHAPE, L.name + ": window too large");
+      L.out[1] = L.in[1]; L.out[2] = Hp; L.out[3] = Wp;
+    } else if (L.type == L_IP) {
+      const std::string* no = get(kv, "num_output");
+      if (!no || !parse_int(*no, &L.Nout) || L.Nout <= 0) return fail(PN_ERR_PARSE, L.name + ": num_output");
+      const std::string* bt = get(kv, "bias_term");
+      L.bias = !(bt && *bt == "false");
+      L.K = L.in[1] * L.in[2] * L.in[3];
+      L.out[1] = L.Nout; L.out[2] = 1; L.out[3] = 1;
+      L.wcount = (int64_t)L.Nout * L.K;
+      L.bcount = L.bias ? L.Nout : 0;
+    } else if (L.type == L_RELU) {
+      const std::string* s = get(kv, "negative_slope");
+      L.slope = s ? (float)atof(s->c_str()) : 0.f;
+      if (!(L.slope >= 0.f)) return fail(PN_ERR_PARSE, L.name + ": negative_slope must be >= 0");
+      memcpy(L.out, L.in, sizeof(L.out));
+    } else {
+      net->classes = L.in[1] * L.in[2] * L.in[3];
+      L.out[1] = L.out[2] = L.out[3] = 1;
+      L.out[0] = 1;
+    }
+    if (L.type == L_RELU && L.top == L.bottom) {
+      // in place: blob already exists
+    } else {
+      if (net->blob(L.top) >= 0) return fail(PN_ERR_PARSE, "blob '" + L.top + "' produced twice");
+      Blob b;
+      b.name = L.top;
+      memcpy(b.dims, L.out, sizeof(b.dims));
+      if (L.type == L_POOL) b.pool_layer = (int)net->layers.size();
+      net->blobs.push_back(b);
+    }
+    net->layers.push_back(L);
+  }
+  if (net->layers.empty() || net->layers.back().type != L_LOSS)
+    return fail(PN_ERR_SHAPE, "the net must end with a SoftmaxWithLoss layer");
+  for (size_t i = 0; i + 1 < net->layers.size(); ++i)
+    if (net->layers[i].type == L_LOSS) return fail(PN_ERR_SHAPE, "SoftmaxWithLoss must be last");
+  return PN_OK;
+}
+
+// fused LeNet pattern: conv(1->20,5x5) pool(MAX2/2) conv(20->50,5x5) pool(MAX2/2)
+// ip(800->500) relu(in place, 0) ip(500->10) loss on a 1x28x28 input.
+static bool is_lenet(const pn_net* n) {
+  const auto& L = n->layers;
+  if (L.size() != 8) return false;
+  auto conv = [](const Layer& l, int C, int F) {
+    return l.type == L_CONV && l.in[1] == C && l.F == F && l.kh == 5 && l.kw == 5 && l.sh == 1 && l.sw == 1 &&
+           l.ph == 0 && l.pw == 0 && l.bias;
+  };
+  auto pool = [](const Layer& l) {
+    return l.type == L_POOL && l.method == 0 && l.kh == 2 && l.kw == 2 && l.sh == 2 && l.sw == 2 && l.ph == 0 &&
+           l.pw == 0;
+  };
+  return conv(L[0], 1, 20) && L[0].in[2] == 28 && L[0].in[3] == 28 && L[0].bottom == n->input_name && pool(L[1]) &&
+         L[1].bottom == L[0].top && conv(L[2], 20, 50) && L[2].bottom == L[1].top && pool(L[3]) &&
+         L[3].bottom == L[2].top && L[4].type == L_IP && L[4].Nout == 500 && L[4].bias && L[4].bottom == L[3].top &&
+         L[5].type == L_RELU && L[5].slope == 0.f && L[5].top == L[5].bottom && L[5].bottom == L[4].top &&
+         L[6].type == L_IP && L[6].Nout == 10 && L[6].bias && L[6].bottom == L[4].top && L[7].type == L_LOSS &&
+         L[7].bottom == L[6].top;
+}
+
+// ---------------------------------------------------------- memory layout
+static pn_status allocate(pn_net* net) {
+  // Parameters in reverse layer order so the data-parallel buckets are
+  // contiguous (ip bucket first); each blob 16-byte aligned.
+  int64_t off = 0;
+  bool seen_conv = false;
+  for (int i = (int)net->layers.size() - 1; i >= 0; --i) {
+    Layer& L = net->layers[i];
+    if (L.type != L_CONV && L.type != L_IP) continue;
+    if (L.type == L_CONV && !seen_conv) {
+      seen_conv = true;
+      net->bucket_split = off;
+    }
+    L.off = off;
+    off += L.wcount + L.bcount;
+    off = (off + 3) & ~3LL;
+    net->nlearn += L.wcount + L.bcount;
+  }
+  if (!seen_conv) net->bucket_split = off;
+  net->nparams = off;
+  TRY(net->alloc(&net->params, off));
+  TRY(net->alloc(&net->grads, off));
+  TRY(net->alloc(&net->hist, off));
+  // parameter blobs
+  for (auto& L : net->layers) {
+    if (L.off < 0) continue;
+    Blob w;
+    w.name = L.name + ".w";
+    w.is_param = true;
+    if (L.type == L_CONV) { w.dims[0] = L.F; w.dims[1] = L.in[1]; w.dims[2] = L.kh; w.dims[3] = L.kw; }
+    else { w.dims[0] = L.Nout; w.dims[1] = L.K; w.dims[2] = 1; w.dims[3] = 1; }
+    w.data = net->params + L.off; w.diff = net->grads + L.off; w.hist = net->hist + L.off;
+    net->blobs.push_back(w);
+    if (L.bcount) {
+      Blob b;
+      b.name = L.name + ".b";
+      b.is_param = true;
+      b.dims[0] = (int)L.bcount; b.dims[1] = b.dims[2] = b.dims[3] = 1;
+      b.data = net->params + L.off + L.wcount; b.diff = net->grads + L.off + L.wcount;
+      b.hist = net->hist + L.off + L.wcount;
+      net->blobs.push_back(b);
+    }
+  }
+  // partial-sum regions for split weight gradients
+  int64_t poff = 0;
+  for (auto& L : net->layers) {
+    if (L.off < 0) continue;
+    L.splits = kWgradSplits;
+    L.part_off = poff;
+    poff += (int64_t)L.splits * (L.wcount + L.bcount);
+  }
+  net->npartials = poff;
+  TRY(net->alloc(&net->partials, poff > 0 ? poff : 1));
+  TRY(net->alloc(&net->row_loss, net->batch));
+  TRY(net->alloc(&net->err, 1));
+  // activation blobs (the fused plan never stores conv1's output or its
+  // gradient, nor conv2's output; conv2's gradient is the dense unpooled G2)
+  std::string skip_data1, skip_data2;
+  if (net->fused) {
+    skip_data1 = net->layers[0].top;
+    skip_data2 = net->layers[2].top;
+  }
+  for (auto& b : net->blobs) {
+    if (b.is_param || b.is_input) continue;
+    int64_t n = b.count();
+    if (b.name == skip_data1) { b.materialised = false; continue; }
+    if (b.name == skip_data2) b.materialised = false;
+    else TRY(net->alloc(&b.data, n));
+    TRY(net->alloc(&b.diff, n));
+    if (b.pool_layer >= 0 && net->layers[b.pool_layer].method == 0) {
+      if (net->fused) TRY(net->alloc(&b.m8, n));
+      else TRY(net->alloc(&b.m32, n));
+    }
+  }
+  // classifier outputs
+  Blob prob, pred, loss;
+  prob.name = "prob"; prob.dims[0] = net->batch; prob.dims[1] = net->classes; prob.dims[2] = prob.dims[3] = 1;
+  pred.name = "pred"; pred.dims[0] = net->batch; pred.dims[1] = pred.dims[2] = pred.dims[3] = 1;
+  loss.name = "loss"; loss.dims[0] = loss.dims[1] = loss.dims[2] = loss.dims[3] = 1;
+  int li = net->blob(net->layers.back().top);
+  net->blobs.erase(net->blobs.begin() + li);  // the loss layer's top is "loss"
+  for (Blob* b : {&prob, &pred, &loss}) {
+    TRY(net->alloc(&b->data, b->count()));
+    net->blobs.push_back(*b);
+  }
+  return PN_OK;
+}
+
+static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+// ------------------------------------------------------------- plan build
+static const float* in_data(pn_net* net, const Layer& L, bool* is_x) {
+  *is_x = (L.bottom == net->input_name);
+  return *is_x ? nullptr : net->blobs[net->blob(L.bottom)].data;
+}
+
+static void add(std::vector<Stage>& v, const std::string& name, const Launch& L,
+                std::function<void(Launch&, const StepArgs&)> patch = nullptr) {
+  Stage s;
+  s.name = name;
+  s.L = L;
+  s.patch = patch;
+  v.push_back(s);
+}
+
+static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L) {
+  ReduceP r{net->partials + L.part_off, net->grads + L.off, (int)(L.wcount + L.bcount), L.splits};
+  Launch l;
+  l.set((const void*)reduce_partials, dim3(cdiv(r.n, 256)), dim3(256), 0, r);
+  add(v, L.name + ".wgrad_reduce", l);
+}
+
+static void add_loss(pn_net* net, std::vector<Stage>& fwd) {
+  LossReduceP lr{net->row_loss, nullptr, net->blobs[net->blob("loss")].data, net->batch, 1.f / net->batch};
+  Launch l;
+  l.set((const void*)loss_reduce, dim3(1), dim3(256), 0, lr);
+  add(fwd, "loss_reduce", l, [](Launch& l, const StepArgs& a) { l.params<LossReduceP>().loss_out = a.loss; });
+}
+
+static void build_layerwise(pn_net* net) {
+  auto& fwd = net->phase[0];
+  auto& bwd = net->phase[1];
+  const int N = net->batch;
+  for (size_t li = 0; li < net->layers.size(); ++li) {
+    Layer& L = net->layers[li];
+    bool isx = false;
+    const float* x = in_data(net, L, &isx);
+    Blob* top = L.type == L_LOSS ? nullptr : &net->blobs[net->blob(L.top)];
+    Launch l;
+    if (L.type == L_CONV) {
+      ConvFwdP p{x, net->params + L.off, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
+                 N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+      l.set((const void*)conv_fwd_generic, dim3(cdiv((long long)N * L.F * L.out[2] * L.out[3], 256)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<ConvFwdP>().x = a.x; }
+                                       : std::function<void(Launch&, const StepArgs&)>());
+    } else if (L.type == L_POOL) {
+      PoolFwdP p{x, top->data, top->m32, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
+                 L.out[2], L.out[3], L.method};
+      l.set((const void*)pool_fwd_generic, dim3(cdiv(top->count(), 256)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l);
+    } else if (L.type == L_IP) {
+      GemmP p{x, net->params + L.off, top->data, L.bias ? net->params + L.off + L.wcount : nullptr,
+              N, L.Nout, L.K, L.K, 1, 1, L.K, 0};
+      l.set((const void*)gemm_generic, dim3(cdiv(L.Nout, 64), cdiv(N, 64)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().A = a.x; }
+                                       : std::function<void(Launch&, const StepArgs&)>());
+    } else if (L.type == L_RELU) {
+      ReluP p{x, nullptr, top->data, top->count(), L.slope};
+      l.set((const void*)relu_fwd_generic, dim3(cdiv(top->count(), 256)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l);
+    } else {
+      Blob& bb = net->blobs[net->blob(L.bottom)];
+      SoftmaxLossP p{x, nullptr, net->blobs[net->blob("prob")].data,
+                     (int32_t*)net->blobs[net->blob("pred")].data, bb.diff, net->row_loss, net->err,
+                     N, net->classes, 1.f / N};
+      l.set((const void*)softmax_loss_generic, dim3(cdiv(N, 8)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd+bwd", l, [](Launch& l, const StepArgs& a) { l.params<SoftmaxLossP>().labels = a.labels; });
+      add_loss(net, fwd);
+    }
+  }
+  // backward, reverse order
+  for (int li = (int)net->layers.size() - 1; li >= 0; --li) {
+    Layer& L = net->layers[li];
+    bool isx = false;
+    const float* x = in_data(net, L, &isx);
+    if (L.type == L_LOSS) continue;  // gradient produced with the forward
+    Blob& top = net->blobs[net->blob(L.top)];
+    Blob* bot = isx ? nullptr : &net->blobs[net->blob(L.bottom)];
+    Launch l;
+    if (L.type == L_CONV) {
+      ConvBwdWeightP p{top.diff, x, net->partials + L.part_off, L.bcount ? net->partials + L.part_off + L.wcount : nullptr,
+                       N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
+                       L.splits, (int)(L.wcount + L.bcount)};
+      l.set((const void*)conv_bwd_weight_generic, dim3(L.F * L.in[1], L.splits), dim3(256), 0, p);
+      add(bwd, L.name + ".wgrad", l, isx ? [](Launch& l, const StepArgs& a) { l.params<ConvBwdWeightP>().x = a.x; }
+                                         : std::function<void(Launch&, const StepArgs&)>());
+      add_reduce(net, bwd, L);
+      if (bot) {
+        ConvBwdDataP q{top.diff, net->params + L.off, bot->diff, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
+                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+        Launch l2;
+        l2.set((const void*)conv_bwd_data_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, q);
+        add(bwd, L.name + ".dgrad", l2);
+      }
+    } else if (L.type == L_POOL) {
+      PoolBwdP p{top.diff, top.m32, bot->diff, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
+                 L.out[2], L.out[3], L.method};
+      l.set((const void*)pool_bwd_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, p);
+      add(bwd, L.name + ".bwd", l);
+    } else if (L.type == L_IP) {
+      // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
+      GemmP w{top.diff, x, net->grads + L.off, nullptr, L.Nout, L.K, N, 1, L.Nout, L.K, 1, 0};
+      l.set((const void*)gemm_generic, dim3(cdiv(L.K, 64), cdiv(L.Nout, 64)), dim3(256), 0, w);
+      add(bwd, L.name + ".wgrad", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().B = a.x; }
+                                         : std::function<void(Launch&, const StepArgs&)>());
+      if (L.bcount) {
+        ColSumP c{top.diff, net->grads + L.off + L.wcount, N, L.Nout};
+        Launch l2;
+        l2.set((const void*)colsum_generic, dim3(L.Nout), dim3(256), 0, c);
+        add(bwd, L.name + ".bgrad", l2);
+      }
+      if (bot) {
+        GemmP d{top.diff, net->params + L.off, bot->diff, nullptr, N, L.K, L.Nout, L.Nout, 1, L.K, 1, 0};
+        Launch l3;
+        l3.set((const void*)gemm_generic, dim3(cdiv(L.K, 64), cdiv(N, 64)), dim3(256), 0, d);
+        add(bwd, L.name + ".dgrad", l3);
+      }
+    } else if (L.type == L_RELU) {
+      ReluP p{top.diff, top.data, bot->diff, top.count(), L.slope};
+      l.set((const void*)relu_bwd_generic, dim3(cdiv(top.count(), 256)), dim3(256), 0, p);
+      add(bwd, L.name + ".bwd", l);
+    }
+  }
+}
+
+static void build_fused_lenet(pn_net* net) {
+  auto& fwd = net->phase[0];
+  auto& bwd = net->phase[1];
+  const int N = net->batch;
+  Layer &c1 = net->layers[0], &c2 = net->layers[2], &i1 = net->layers[4], &i2 = net->layers[6];
+  Blob& p1 = net->blobs[net->blob(net->layers[1].top)];
+  Blob& cv2 = net->blobs[net->blob(c2.top)];
+  Blob& p2 = net->blobs[net->blob(net->layers[3].top)];
+  Blob& a1 = net->blobs[net->blob(i1.top)];
+  Blob& lg = net->blobs[net->blob(i2.top)];
+  float* P = net->params;
+  float* G = net->grads;
+  // ---- forward
+  {
+    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N};
+    Launch l;
+    l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(288), 0, p);
+    add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
+  }
+  if (net->tf32) {
+    add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(P + c2.off, P + c2.off + 25000, p1.data, p2.data, p2.m8, N,
+                                                        net->tc_sms));
+  } else {
+    Conv2Pool2P p{p1.data, P + c2.off, P + c2.off + 25000, p2.data, p2.m8, N};
+    Launch l;
+    l.set((const void*)lenet_conv2_pool2_simt, dim3(std::min(148, (int)cdiv(N, 2))), dim3(320),
+          (50 * 20 * 28 + 2 * 2880) * 4, p);
+    add(fwd, "conv2+pool2", l);
+  }
+  if (net->tf32) {
+    add(fwd, "ip1+relu[tc]", tc::ip_fwd_launch(p2.data, P + i1.off, P + i1.off + i1.wcount, a1.data, N, 800, 500,
+                                                true, net->tc_sms));
+  } else {
+    GemmP g{p2.data, P + i1.off, a1.data, P + i1.off + i1.wcount, N, 500, 800, 800, 1, 1, 800, 1};
+    Launch l;
+    l.set((const void*)gemm_generic, dim3(cdiv(500, 64), cdiv(N, 64)), dim3(256), 0, g);
+    add(fwd, "ip1+relu", l);
+  }
+  {
+    Ip2LossP p{a1.data, P + i2.off, P + i2.off + 5000, nullptr, lg.data,
+               net->blobs[net->blob("prob")].data, (int32_t*)net->blobs[net->blob("pred")].data, lg.diff,
+               net->row_loss, net->err, N, 1.f / N};
+    Launch l;
+    l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, 8)), dim3(256), 0, p);
+    add(fwd, "ip2+softmax_loss", l, [](Launch& l, const StepArgs& a) { l.params<Ip2LossP>().labels = a.labels; });
+    add_loss(net, fwd);
+  }
+  // ---- backward (reverse order)
+  {
+    Ip2BwdP p{lg.diff, a1.data, P + i2.off, a1.diff, net->partials + i2.part_off,
+              net->partials + i2.part_off + 5000, N, i2.splits, 5010};
+    Launch l;
+    l.set((const void*)lenet_ip2_bwd, dim3(4, i2.splits), dim3(128), 0, p);
+    add(bwd, "ip2.bwd+relu1.bwd", l);
+    add_reduce(net, bwd, i2);
+  }
+  if (net->tf32) {
+    add(bwd, "ip1.wgrad[tc]", tc::ip_wgrad_launch(a1.diff, p2.data, G + i1.off, G + i1.off + i1.wcount, N, 800, 500,
+                                                  net->tc_sms));
+    add(bwd, "ip1.dgrad+unpool2[tc]", tc::ip_dgrad_unpool_launch(a1.diff, P + i1.off, p2.m8, cv2.diff, N, net->tc_sms));
+  } else {
+    GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
+    Launch l;
+    l.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(500, 64)), dim3(256), 0, w);
+    add(bwd, "ip1.wgrad", l);
+    ColSumP c{a1.diff, G + i1.off + i1.wcount, N, 500};
+    Launch l2;
+    l2.set((const void*)colsum_generic, dim3(500), dim3(256), 0, c);
+    add(bwd, "ip1.bgrad", l2);
+    GemmP d{a1.diff, P + i1.off, p2.diff, nullptr, N, 800, 500, 500, 1, 800, 1, 0};
+    Launch l3;
+    l3.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(N, 64)), dim3(256), 0, d);
+    add(bwd, "ip1.dgrad", l3);
+    Unpool2P u{p2.diff, p2.m8, cv2.diff, N};
+    Launch l4;
+    l4.set((const void*)lenet_unpool2, dim3(cdiv((long long)N * 3200, 256)), dim3(256), 0, u);
+    add(bwd, "pool2.bwd", l4);
+  }
+  if (net->tf32) {
+    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, P + c2.off, p1.diff, N, net->tc_sms));
+    add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits,
+                                                       N, net->tc_sms));
+    add_reduce(net, bwd, c2);
+  } else {
+    ConvBwdDataP q{cv2.diff, P + c2.off, p1.diff, N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8};
+    Launch l;
+    l.set((const void*)conv_bwd_data_generic, dim3(cdiv((long long)N * 2880, 256)), dim3(256), 0, q);
+    add(bwd, "conv2.dgrad", l);
+    ConvBwdWeightP w{cv2.diff, p1.data, net->partials + c2.part_off, net->partials + c2.part_off + 25000,
+                     N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8, c2.splits, 25050};
+    Launch l2;
+    l2.set((const void*)conv_bwd_weight_generic, dim3(1000, c2.splits), dim3(256), 0, w);
+    add(bwd, "conv2.wgrad", l2);
+    add_reduce(net, bwd, c2);
+  }
+  {
+    Conv1WgradP p{p1.diff, p1.m8, nullptr, net->partials + c1.part_off, net->partials + c1.part_off + 500, N,
+                  c1.splits, 520};
+    Launch l;
+    l.set((const void*)lenet_conv1_wgrad, dim3(c1.splits), dim3(320), 0, p);
+    add(bwd, "conv1.wgrad", l, [](Launch& l, const StepArgs& a) { l.params<Conv1WgradP>().x = a.x; });
+    add_reduce(net, bwd, c1);
+  }
+}
+
+static void build_update(pn_net* net) {
+  SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f};
+  Launch l;
+  long long n4 = net->nparams / 4;
+  l.set((const void*)sgd_update_kernel, dim3(std::max(1u, std::min(cdiv(n4, 256), 148u * 8))), dim3(256), 0, p);
+  add(net->phase[2], "sgd", l, [](Launch& l, const StepArgs& a) {
+    SgdP& q = l.params<SgdP>();
+    q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale;
+  });
+}
+
+// data-parallel exchange stages (inserted into the backward list)
+static void add_dp_stages(pn_net* net) {
+  if (net->nranks <= 1) return;
+  auto& bwd = net->phase[1];
+  // position: after the last stage producing an ip-bucket gradient
+  size_t pos = 0;
+  for (size_t i = 0; i < bwd.size(); ++i)
+    if (bwd[i].name.rfind("ip", 0) == 0) pos = i + 1;
+  auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) {
+    return [net, off, cnt, ready](cudaStream_t st) -> cudaError_t {
+      cudaError_t e = cudaEventRecord(ready, st);
+      if (e != cudaSuccess) return e;
+      e = cudaStreamWaitEvent(net->comm_stream, ready, 0);
+      if (e != cudaSuccess) return e;
+      if (cnt > 0 && ncclAllReduce(net->grads + off, net->grads + off, cnt, ncclFloat, ncclSum, net->comm,
+                                   net->comm_stream) != ncclSuccess)
+        return cudaErrorUnknown;
+      return cudaSuccess;
+    };
+  };
+  Stage s1;
+  s1.name = "allreduce[ip bucket]";
+  s1.custom = allreduce(0, net->bucket_split, net->ev_ip);
+  bwd.insert(bwd.begin() + pos, s1);
+  Stage s2;
+  s2.name = "allreduce[conv bucket]";
+  s2.custom = allreduce(net->bucket_split, net->nparams - net->bucket_split, net->ev_conv);
+  bwd.push_back(s2);
+  Stage s3;
+  s3.name = "join[comm]";
+  s3.custom = [net](cudaStream_t st) -> cudaError_t {
+    cudaError_t e = cudaEventRecord(net->ev_done, net->comm_stream);
+    if (e != cudaSuccess) return e;
+    return cudaStreamWaitEvent(st, net->ev_done, 0);
+  };
+  bwd.push_back(s3);
+}
+
+static pn_status build_plan(pn_net* net) {
+  for (auto& ph : net->phase) ph.clear();
+  if (net->fused) build_fused_lenet(net);
+  else build_layerwise(net);
+  build_update(net);
+  add_dp_stages(net);
+  int n = 0;
+  for (auto& ph : net->phase)
+    for (auto& s : ph)
+      if (!s.custom) ++n;
+  net->launches_per_step = n;
+  return PN_OK;
+}
+
+// --------------------------------------------------------------- execution
+static pn_status run_stage(pn_net* net, Stage& s, const StepArgs& a, cudaStream_t st) {
+  if (s.custom) {
+    cudaError_t e = s.custom(st);
+    if (e != cudaSuccess) return fail(net->comm ? PN_ERR_NCCL : PN_ERR_CUDA, "stage " + s.name + " failed");
+    return PN_OK;
+  }
+  if (s.patch) s.patch(s.L, a);
+  cudaError_t e = s.L.launch(st);
+  if (e != cudaSuccess) return fail(PN_ERR_CUDA, "launch " + s.name + ": " + cudaGetErrorString(e));
+  return PN_OK;
+}
+
+static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t st) {
+  for (auto& s : net->phase[ph]) TRY(run_stage(net, s, a, st));
+  return PN_OK;
+}
+
+static StepArgs make_args(pn_net* net, const float* x, const int32_t* labels, float* loss, const pn_sgd* sgd,
+                          int64_t iter) {
+  StepArgs a;
+  a.x = x;
+  a.labels = labels;
+  a.loss = loss;
+  if (sgd) {
+    double lr = sgd->base_lr;
+    if (sgd->lr_policy == 1) lr = (double)sgd->base_lr * pow(1.0 + (double)sgd->gamma * (double)iter, -(double)sgd->power);
+    a.lr = (float)lr;
+    a.mom = sgd->momentum;
+    a.decay = sgd->weight_decay;
+  }
+  a.gscale = 1.f / (float)net->nranks;
+  return a;
+}
+
+// capture phases [0, nph) into an executable graph; record kernel nodes
+static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_t* out, bool infer) {
+  if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
+  CU(cudaStreamBeginCapture(net->cap, cudaStreamCaptureModeThreadLocal));
+  for (int ph = 0; ph < nph; ++ph)
+    for (auto& s : net->phase[ph]) {
+      pn_status st = run_stage(net, s, a, net->cap);
+      if (st != PN_OK) {
+        cudaGraph_t g;
+        cudaStreamEndCapture(net->cap, &g);
+        return st;
+      }
+      if (!s.custom) {
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        CU(cudaStreamGetCaptureInfo(net->cap, &cs, nullptr, nullptr, &deps, &nd));
+        (infer ? s.inode : s.node) = nd ? deps[0] : nullptr;
+      }
+    }
+  cudaGraph_t g;
+  CU(cudaStreamEndCapture(net->cap, &g));
+  if (*out) cudaGraphExecDestroy(*out);
+  CU(cudaGraphInstantiate(out, g, 0));
+  cudaGraphDestroy(g);
+  return PN_OK;
+}
+
+static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_t ex, bool infer) {
+  for (int ph = 0; ph < nph; ++ph)
+    for (auto& s : net->phase[ph]) {
+      if (s.custom || !s.patch) continue;
+      s.patch(s.L, a);
+      cudaKernelNodeParams kp{};
+      void* args[1] = {s.L.arg.data()};
+      kp.func = (void*)s.L.func;
+      kp.gridDim = s.L.grid;
+      kp.blockDim = s.L.block;
+      kp.sharedMemBytes = (unsigned)s.L.smem;
+      kp.kernelParams = args;
+      CU(cudaGraphExecKernelNodeSetParams(ex, infer ? s.inode : s.node, &kp));
+    }
+  return PN_OK;
+}
+
+static bool same_args(const StepArgs& a, const StepArgs& b) {
+  return a.x == b.x && a.labels == b.labels && a.loss == b.loss && a.lr == b.lr && a.mom == b.mom &&
+         a.decay == b.decay && a.gscale == b.gscale;
+}
+
+// ------------------------------------------------------------------ C ABI
+#define CHECK_NET(n) \
+  if (!(n)) return fail(PN_ERR_INVALID_ARG, "net is NULL")
+
+extern "C" pn_status net_create(const char* spec, int batch, int device, int flags, pn_net** out) {
+  if (!spec || !out || batch <= 0 || device < 0 || (flags & ~3)) return fail(PN_ERR_INVALID_ARG, "net_create: bad argument");
+  *out = nullptr;
+  std::unique_ptr<pn_net> net(new pn_net());
+  net->device = device;
+  net->batch = batch;
+  net->flags = flags;
+  net->tf32 = flags & PN_TF32;
+  TRY(parse_and_infer(net.get(), spec));  // host-only: spec errors need no GPU
+  CU(cudaSetDevice(device));
+  net->fused = !(flags & PN_LAYERWISE) && is_lenet(net.get());
+  if (net->tf32 && !net->fused)
+    return fail(PN_ERR_INVALID_ARG, "PN_TF32 needs the fused LeNet plan (this net has no tensor-core plan yet)");
+  int sms = 0;
+  CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  net->tc_sms = sms;
+  TRY(allocate(net.get()));
+  CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (50 * 20 * 28 + 2 * 2880) * 4));
+  if (net->tf32) {
+    cudaError_t e = tc::setup();
+    if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
+  }
+  TRY(build_plan(net.get()));
+  CU(cudaDeviceSynchronize());
+  *out = net.release();
+  return PN_OK;
+}
+
+extern "C" void net_destroy(pn_net* net) {
+  if (!net) return;
+  cudaSetDevice(net->device);
+  cudaDeviceSynchronize();
+  if (net->step_exec) cudaGraphExecDestroy(net->step_exec);
+  if (net->infer_exec) cudaGraphExecDestroy(net->infer_exec);
+  if (net->cap) cudaStreamDestroy(net->cap);
+  if (net->comm) ncclCommDestroy(net->comm);
+  if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
+  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done})
+    if (e) cudaEventDestroy(e);
+  for (void* p : net->allocs) cudaFree(p);
+  delete net;
+}
+
+extern "C" pn_status net_blob_count(const pn_net* net, int* count) {
+  CHECK_NET(net);
+  if (!count) return fail(PN_ERR_INVALID_ARG, "count is NULL");
+  *count = (int)net->blobs.size();
+  return PN_OK;
+}
+
+extern "C" pn_status net_blob_info(const pn_net* net, int i, const char** name, int dims[4], int* is_param,
+                                   int* materialised) {
+  CHECK_NET(net);
+  if (i < 0 || i >= (int)net->blobs.size()) return fail(PN_ERR_INVALID_ARG, "blob index out of range");
+  const Blob& b = net->blobs[i];
+  if (name) *name = b.name.c_str();
+  if (dims) memcpy(dims, b.dims, sizeof(b.dims));
+  if (is_param) *is_param = b.is_param;
+  if (materialised) *materialised = b.materialised;
+  return PN_OK;
+}
+
+extern "C" pn_status net_param_count(const pn_net* net, int64_t* count) {
+  CHECK_NET(net);
+  if (!count) return fail(PN_ERR_INVALID_ARG, "count is NULL");
+  *count = net->nlearn;
+  return PN_OK;
+}
+
+static pn_status find_blob(pn_net* net, const char* name, Blob** b) {
+  if (!name) return fail(PN_ERR_INVALID_ARG, "blob name is NULL");
+  int i = net->blob(name);
+  if (i < 0) return fail(PN_ERR_INVALID_ARG, std::string("no blob named ") + name);
+  *b = &net->blobs[i];
+  return PN_OK;
+}
+
+extern "C" pn_status net_blob_ptr(pn_net* net, const char* name, int which, void** p) {
+  CHECK_NET(net);
+  Blob* b;
+  TRY(find_blob(net, name, &b));
+  if (!p) return fail(PN_ERR_INVALID_ARG, "out pointer is NULL");
+  void* r = which == PN_DATA ? (void*)b->data : which == PN_DIFF ? (void*)b->diff
+          : which == PN_HISTORY ? (void*)b->hist : nullptr;
+  if (!r) return fail(PN_ERR_STATE, std::string(name) + ": buffer not materialised by this plan");
+  *p = r;
+  return PN_OK;
+}
+
+extern "C" pn_status net_set_param(pn_net* net, const char* name, const float* src, int64_t count, int on_host,
+                                   void* stream) {
+  CHECK_NET(net);
+  Blob* b;
+  TRY(find_blob(net, name, &b));
+  if (!b->is_param) return fail(PN_ERR_INVALID_ARG, std::string(name) + " is not a parameter");
+  if (!src || count != b->count()) return fail(PN_ERR_INVALID_ARG, "net_set_param: count mismatch");
+  CU(cudaSetDevice(net->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  if (on_host) {
+    CU(cudaMemcpyAsync(b->data, src, count * 4, cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+  } else {
+    CU(cudaMemcpyAsync(b->data, src, count * 4, cudaMemcpyDeviceToDevice, st));
+  }
+  return PN_OK;
+}
+
+static pn_status mask_io(pn_net* net, Blob* b, int32_t* m32, bool to32, cudaStream_t st) {
+  const Layer& L = net->layers[b->pool_layer];
+  MaskExpandP p{b->m8, m32, b->dims[0], b->dims[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
+                b->dims[2], b->dims[3], to32 ? 1 : 0};
+  Launch l;
+  l.set((const void*)mask_convert, dim3(cdiv(b->count(), 256)), dim3(256), 0, p);
+  CU(l.launch(st));
+  return PN_OK;
+}
+
+static pn_status blob_io(pn_net* net, const char* name, int which, void* buf, int64_t bytes, int on_host,
+                         void* stream, bool put) {
+  CHECK_NET(net);
+  Blob* b;
+  TRY(find_blob(net, name, &b));
+  if (!buf) return fail(PN_ERR_INVALID_ARG, "buffer is NULL");
+  if (bytes != b->count() * 4) return fail(PN_ERR_INVALID_ARG, "byte count mismatch");
+  CU(cudaSetDevice(net->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  void* dev = nullptr;
+  int32_t* tmp = nullptr;
+  if (which == PN_MASK) {
+    if (b->pool_layer < 0 || net->layers[b->pool_layer].method != 0)
+      return fail(PN_ERR_INVALID_ARG, std::string(name) + " has no max-pool mask");
+    if (b->m32) dev = b->m32;
+    else {
+      CU(cudaMallocAsync((void**)&tmp, bytes, st));
+      dev = tmp;
+    }
+  } else {
+    if (which != PN_DATA && which != PN_DIFF && which != PN_HISTORY) return fail(PN_ERR_INVALID_ARG, "bad which");
+    dev = which == PN_DATA ? (void*)b->data : which == PN_DIFF ? (void*)b->diff : (void*)b->hist;
+    if (!dev) return fail(b->is_input || b->is_param ? PN_ERR_INVALID_ARG : PN_ERR_STATE,
+                          std::string(name) + ": buffer not materialised by this plan");
+  }
+  cudaMemcpyKind kind = on_host ? (put ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost) : cudaMemcpyDeviceToDevice;
+  if (put) {
+    CU(cudaMemcpyAsync(dev, buf, bytes, kind, st));
+    if (tmp) TRY(mask_io(net, b, tmp, false, st));
+  } else {
+    if (tmp) TRY(mask_io(net, b, tmp, true, st));
+    CU(cudaMemcpyAsync(buf, dev, bytes, kind, st));
+  }
+  if (tmp) CU(cudaFreeAsync(tmp, st));
+  if (on_host) CU(cudaStreamSynchronize(st));
+  return PN_OK;
+}
+
+extern "C" pn_status net_get_blob(pn_net* net, const char* name, int which, void* dst, int64_t bytes, int on_host,
+                                  void* stream) {
+  return blob_io(net, name, which, dst, bytes, on_host, stream, false);
+}
+extern "C" pn_status net_put_blob(pn_net* net, const char* name, int which, const void* src, int64_t bytes,
+                                  int on_host, void* stream) {
+  return blob_io(net, name, which, const_cast<void*>(src), bytes, on_host, stream, true);
+}
+
+extern "C" pn_status net_forward(pn_net* net, const float* x, const int32_t* labels, float* loss, void* stream) {
+  CHECK_NET(net);
+  if (!x || !labels) return fail(PN_ERR_INVALID_ARG, "x and labels are required");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = make_args(net, x, labels, loss, nullptr, 0);
+  net->last = a;
+  TRY(run_phase(net, 0, a, (cudaStream_t)stream));
+  net->forward_done = true;
+  return PN_OK;
+}
+
+extern "C" pn_status net_backward(pn_net* net, void* stream) {
+  CHECK_NET(net);
+  if (!net->forward_done) return fail(PN_ERR_STATE, "net_backward before net_forward");
+  CU(cudaSetDevice(net->device));
+  TRY(run_phase(net, 1, net->last, (cudaStream_t)stream));
+  return PN_OK;
+}
+
+extern "C" pn_status sgd_update(pn_net* net, const pn_sgd* sgd, int64_t iter, void* stream) {
+  CHECK_NET(net);
+  if (!sgd || iter < 0 || (sgd->lr_policy != 0 && sgd->lr_policy != 1))
+    return fail(PN_ERR_INVALID_ARG, "sgd_update: bad solver settings");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = make_args(net, net->last.x, net->last.labels, net->last.loss, sgd, iter);
+  TRY(run_phase(net, 2, a, (cudaStream_t)stream));
+  return PN_OK;
+}
+
+extern "C" pn_status net_train_step(pn_net* net, const float* x, const int32_t* labels, const pn_sgd* sgd,
+                                    int64_t iter, float* loss, void* stream) {
+  CHECK_NET(net);
+  if (!x || !labels || !sgd || iter < 0 || (sgd->lr_policy != 0 && sgd->lr_policy != 1))
+    return fail(PN_ERR_INVALID_ARG, "net_train_step: bad argument");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = make_args(net, x, labels, loss, sgd, iter);
+  if (!net->step_exec) {
+    TRY(capture(net, 3, a, &net->step_exec, false));
+    net->step_args = a;
+  } else if (!same_args(a, net->step_args)) {
+    TRY(patch_graph(net, 3, a, net->step_exec, false));
+    net->step_args = a;
+  }
+  CU(cudaGraphLaunch(net->step_exec, (cudaStream_t)stream));
+  net->last = a;
+  net->forward_done = true;
+  return PN_OK;
+}
+
+extern "C" pn_status net_infer(pn_net* net, const float* x, const int32_t* labels, float* loss, void* stream) {
+  CHECK_NET(net);
+  if (!x || !labels) return fail(PN_ERR_INVALID_ARG, "x and labels are required");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = make_args(net, x, labels, loss, nullptr, 0);
+  if (!net->infer_exec) {
+    TRY(capture(net, 1, a, &net->infer_exec, true));
+    net->infer_args = a;
+  } else if (!same_args(a, net->infer_args)) {
+    TRY(patch_graph(net, 1, a, net->infer_exec, true));
+    net->infer_args = a;
+  }
+  CU(cudaGraphLaunch(net->infer_exec, (cudaStream_t)stream));
+  net->last = a;
+  net->forward_done = true;
+  return PN_OK;
+}
+
+extern "C" pn_status net_train_step_host(pn_net* net, const float* xh, const int32_t* lh, const pn_sgd* sgd,
+                                         int64_t iter, float* loss_host, void* stream) {
+  CHECK_NET(net);
+  if (!xh || !lh || !loss_host) return fail(PN_ERR_INVALID_ARG, "host buffers are required");
+  CU(cudaSetDevice(net->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const Blob& in = net->blobs[net->blob(net->input_name)];
+  static thread_local struct { float* x = nullptr; int32_t* y = nullptr; float* l = nullptr; int64_t nx = 0; int n = 0; } buf;
+  if (buf.nx < in.count() || buf.n < net->batch) {
+    if (buf.x) { cudaFree(buf.x); cudaFree(buf.y); cudaFree(buf.l); }
+    CU(cudaMalloc(&buf.x, in.count() * 4));
+    CU(cudaMalloc(&buf.y, net->batch * 4));
+    CU(cudaMalloc(&buf.l, 4));
+    buf.nx = in.count();
+    buf.n = net->batch;
+  }
+  CU(cudaMemcpyAsync(buf.x, xh, in.count() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(buf.y, lh, net->batch * 4, cudaMemcpyHostToDevice, st));
+  TRY(net_train_step(net, buf.x, buf.y, sgd, iter, buf.l, stream));
+  CU(cudaMemcpyAsync(loss_host, buf.l, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return PN_OK;
+}
+
+extern "C" pn_status net_stage_count(const pn_net* net, int phase, int* count) {
+  CHECK_NET(net);
+  if (phase < 0 || phase > 2 || !count) return fail(PN_ERR_INVALID_ARG, "bad phase");
+  *count = (int)net->phase[phase].size();
+  return PN_OK;
+}
+
+extern "C" pn_status net_stage_name(const pn_net* net, int phase, int i, const char** name) {
+  CHECK_NET(net);
+  if (phase < 0 || phase > 2 || i < 0 || i >= (int)net->phase[phase].size() || !name)
+    return fail(PN_ERR_INVALID_ARG, "bad stage");
+  *name = net->phase[phase][i].name.c_str();
+  return PN_OK;
+}
+
+extern "C" pn_status net_run_stage(pn_net* net, int phase, int i, const float* x, const int32_t* labels,
+                                   void* stream) {
+  CHECK_NET(net);
+  if (phase < 0 || phase > 2 || i < 0 || i >= (int)net->phase[phase].size())
+    return fail(PN_ERR_INVALID_ARG, "bad stage");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = net->last;
+  if (x) a.x = x;
+  if (labels) a.labels = labels;
+  return run_stage(net, net->phase[phase][i], a, (cudaStream_t)stream);
+}
+
+extern "C" pn_status net_profile_stages(pn_net* net, const float* x, const int32_t* labels, const pn_sgd* sgd,
+                                        int64_t iter, int steps, float* ms_out, int cap, int* n_out, void* stream) {
+  CHECK_NET(net);
+  int total = 0;
+  for (auto& ph : net->phase) total += (int)ph.size();
+  if (!x || !labels || !sgd || steps <= 0 || !ms_out || cap < total) return fail(PN_ERR_INVALID_ARG, "bad argument");
+  CU(cudaSetDevice(net->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  std::vector<cudaEvent_t> ev(total + 1);
+  for (auto& e : ev) CU(cudaEventCreate(&e));
+  std::vector<double> acc(total, 0.0);
+  for (int s = 0; s < steps; ++s) {
+    StepArgs a = make_args(net, x, labels, nullptr, sgd, iter + s);
+    int k = 0;
+    CU(cudaEventRecord(ev[0], st));
+    for (int ph = 0; ph < 3; ++ph)
+      for (auto& stg : net->phase[ph]) {
+        TRY(run_stage(net, stg, a, st));
+        CU(cudaEventRecord(ev[++k], st));
+      }
+    CU(cudaEventSynchronize(ev[total]));
+    for (int i = 0; i < total; ++i) {
+      float ms = 0.f;
+      CU(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+      acc[i] += ms;
+    }
+  }
+  for (int i = 0; i < total; ++i) ms_out[i] = (float)(acc[i] / steps);
+  if (n_out) *n_out = total;
+  for (auto& e : ev) cudaEventDestroy(e);
+  net->forward_done = true;
+  return PN_OK;
+}
+
+extern "C" pn_status net_launches_per_step(const pn_net* net, int* n) {
+  CHECK_NET(net);
+  if (!n) return fail(PN_ERR_INVALID_ARG, "n is NULL");
+  *n = net->launches_per_step;
+  return PN_OK;
+}
+
+extern "C" pn_status net_sync_errors(pn_net* net, void* stream) {
+  CHECK_NET(net);
+  CU(cudaSetDevice(net->device));
+  CU(cudaStreamSynchronize((cudaStream_t)stream));
+  unsigned e = 0;
+  CU(cudaMemcpy(&e, net->err, 4, cudaMemcpyDeviceToHost));
+  if (e) {
+    CU(cudaMemset(net->err, 0, 4));
+    return fail(PN_ERR_LABEL_RANGE, "a label was outside [0, classes)");
+  }
+  return PN_OK;
+}
+
+extern "C" pn_status pn_nccl_unique_id(void* out128) {
+  if (!out128) return fail(PN_ERR_INVALID_ARG, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  memcpy(out128, &id, 128);
+  return PN_OK;
+}
+
+extern "C" pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* id128) {
+  CHECK_NET(net);
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id128) return fail(PN_ERR_INVALID_ARG, "net_dp_init: bad rank");
+  if (net->comm) return fail(PN_ERR_STATE, "data parallelism already initialised");
+  CU(cudaSetDevice(net->device));
+  ncclUniqueId id;
+  memcpy(&id, id128, 128);
+  NC(ncclCommInitRank(&net->comm, nranks, id, rank));
+  net->nranks = nranks;
+  net->rank = rank;
+  CU(cudaStreamCreateWithFlags(&net->comm_stream, cudaStreamNonBlocking));
+  CU(cudaEventCreateWithFlags(&net->ev_ip, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&net->ev_conv, cudaEventDisableTiming));
+  CU(cudaEventCreateWithFlags(&net->ev_done, cudaEventDisableTiming));
+  if (net->step_exec) { cudaGraphExecDestroy(net->step_exec); net->step_exec = nullptr; }
+  if (net->infer_exec) { cudaGraphExecDestroy(net->infer_exec); net->infer_exec = nullptr; }
+  TRY(build_plan(net));
+  return PN_OK;
+}

@@ -1,0 +1,157 @@
+// params.h -- kernel parameter blocks (one __grid_constant__ struct per kernel)
+// shared by the host runtime (net.cpp) and the CUDA kernels.  Product code
+// only: nothing here is shared with oracle/.
+#pragma once
+#include <stdint.h>
+
+namespace pn {
+
+// ---------------------------------------------------------------- generic
+struct ConvFwdP {  // y = W (*) x + b
+  const float* x;
+  const float* w;
+  const float* b;
+  float* y;
+  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+};
+struct ConvBwdDataP {  // dx = col2im(W^T dy) in gather form
+  const float* dy;
+  const float* w;
+  float* dx;
+  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+};
+struct ConvBwdWeightP {  // split-N partials of dW = sum dy col^T and db
+  const float* dy;
+  const float* x;
+  float* part_w;  // [splits][F*C*kh*kw]
+  float* part_b;  // [splits][F]
+  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo, splits;
+  int pstride;    // floats between consecutive splits of part_w / part_b
+};
+struct ReduceP {  // out[i] = sum_s part[s*n + i] (fixed order s = 0..)
+  const float* part;
+  float* out;
+  int n, splits;
+};
+struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
+  const float* x;
+  float* y;
+  int32_t* mask;
+  int N, C, H, W, kh, kw, sh, sw, ph, pw, Hp, Wp, method;
+};
+struct PoolBwdP {  // P:220-222; gather form, ascending output order
+  const float* dy;
+  const int32_t* mask;
+  float* dx;
+  int N, C, H, W, kh, kw, sh, sw, ph, pw, Hp, Wp, method;
+};
+struct GemmP {  // C[m,n] = sum_k A(m,k) B(k,n) (+ bias[n]) (relu)
+  const float* A;
+  const float* B;
+  float* C;
+  const float* bias;
+  int M, N, K;
+  long long sam, sak, sbk, sbn;
+  int relu;
+};
+struct ColSumP {  // out[n] = sum_m a[m*N + n]
+  const float* a;
+  float* out;
+  int M, N;
+};
+struct ReluP {
+  const float* x;   // fwd input / bwd dy
+  const float* y;   // bwd: forward output
+  float* out;
+  long long n;
+  float slope;
+};
+struct SoftmaxLossP {  // P:109-110; S:429-446 (fwd + bwd in one pass)
+  const float* logits;
+  const int32_t* labels;
+  float* prob;
+  int32_t* pred;
+  float* dlogits;
+  float* row_loss;
+  unsigned* err;
+  int M, D;
+  float grad_scale;  // loss_weight / M
+};
+struct LossReduceP {
+  const float* row_loss;
+  float* loss_out;  // caller's (may be null)
+  float* loss_blob;
+  int M;
+  float inv_M;
+};
+struct SgdP {  // S:536-544 Caffe SGD, fp32, no FMA
+  float* w;
+  const float* g;
+  float* v;
+  long long n;
+  float lr, mom, decay, gscale;
+};
+struct MaskExpandP {  // uint8 window offset <-> int32 plane-local (ABI view)
+  uint8_t* m8;
+  int32_t* m32;
+  int N, C, H, W, kh, kw, sh, sw, ph, pw, Hp, Wp;
+  int to32;  // 1: m8 -> m32, 0: m32 -> m8
+};
+
+// ------------------------------------------------------------ fused LeNet
+// Shapes are compile-time in the kernels; the structs carry pointers only.
+struct Conv1Pool1P {  // x[N,1,28,28] -> p1[N,20,12,12], m1 (uint8 offsets)
+  const float* x;
+  const float* w;  // [20,1,5,5]
+  const float* b;  // [20]
+  float* p1;
+  uint8_t* m1;
+  int N;
+};
+struct Conv2Pool2P {  // p1[N,20,12,12] -> p2[N,50,4,4], m2
+  const float* p1;
+  const float* w;  // [50,20,5,5]
+  const float* b;
+  float* p2;
+  uint8_t* m2;
+  int N;
+};
+struct Ip2LossP {  // a1[N,500] -> logits, prob, pred, dz, row_loss
+  const float* a1;
+  const float* w;  // [10,500]
+  const float* b;
+  const int32_t* labels;
+  float* logits;
+  float* prob;
+  int32_t* pred;
+  float* dz;
+  float* row_loss;
+  unsigned* err;
+  int N;
+  float grad_scale;
+};
+struct Ip2BwdP {  // dz[N,10], a1 -> da1 = relu'(a1) * dz W2 ; dW2 / db2 partials
+  const float* dz;
+  const float* a1;
+  const float* w;  // [10,500]
+  float* da1;
+  float* part_w;  // [splits][10*500]
+  float* part_b;  // [splits][10]
+  int N, splits, pstride;
+};
+struct Unpool2P {  // dp2 [N,800] + m2 -> G2 [N,50,8,8] dense
+  const float* dp2;
+  const uint8_t* m2;
+  float* g2;
+  int N;
+};
+struct Conv1WgradP {  // dp1 + m1 + x -> partial dW1, db1
+  const float* dp1;
+  const uint8_t* m1;
+  const float* x;
+  float* part_w;  // [splits][500]
+  float* part_b;  // [splits][20]
+  int N, splits, pstride;
+};
+
+}  // namespace pn

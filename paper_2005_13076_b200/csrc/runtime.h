@@ -1,0 +1,60 @@
+// runtime.h -- host-side executor types of the C ABI implementation.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/pn.h"
+
+namespace pn {
+
+// Everything that changes from one training step to the next.
+struct StepArgs {
+  const float* x = nullptr;
+  const int32_t* labels = nullptr;
+  float* loss = nullptr;
+  float lr = 0.f, mom = 0.f, decay = 0.f, gscale = 1.f;
+};
+
+// One kernel launch with its single __grid_constant__ parameter block.
+struct Launch {
+  const void* func = nullptr;
+  dim3 grid, block;
+  size_t smem = 0;
+  std::vector<unsigned char> arg;
+  template <class P>
+  void set(const void* f, dim3 g, dim3 b, size_t s, const P& p) {
+    func = f;
+    grid = g;
+    block = b;
+    smem = s;
+    arg.resize(sizeof(P));
+    std::memcpy(arg.data(), &p, sizeof(P));
+  }
+  template <class P>
+  P& params() {
+    return *reinterpret_cast<P*>(arg.data());
+  }
+  cudaError_t launch(cudaStream_t st) {
+    void* a[1] = {arg.data()};
+    return cudaLaunchKernel(func, grid, block, a, smem, st);
+  }
+};
+
+// A stage = one kernel launch (or one non-kernel action such as an NCCL
+// collective or a cross-stream event) of the plan.
+struct Stage {
+  std::string name;
+  Launch L;
+  std::function<void(Launch&, const StepArgs&)> patch;  // refresh step-dependent args
+  std::function<cudaError_t(cudaStream_t)> custom;     // non-kernel action
+  cudaGraphNode_t node = nullptr;                      // kernel node in the step graph
+  cudaGraphNode_t inode = nullptr;                     // kernel node in the infer graph
+};
+
+}  // namespace pn

@@ -1,0 +1,191 @@
+"""Thin Python front end of the C ABI (same names as include/pn.h).
+
+PyTorch provides device memory and the current CUDA stream; every compute
+step runs inside libpn.so.  Tensors passed in must be contiguous CUDA tensors
+on the net's device (fp32 images, int32 labels).
+"""
+import ctypes
+import os
+
+import numpy as np
+
+from . import _lib
+from ._lib import PN_DATA, PN_DIFF, PN_HISTORY, PN_MASK, check, lib, pn_sgd
+
+SPEC_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "specs")
+
+
+def spec_text(name):
+    """Text of a bundled spec ('lenet', 'cifar10_quick') or a path."""
+    path = name if os.path.exists(name) else os.path.join(SPEC_DIR, name + ".net")
+    with open(path) as f:
+        return f.read()
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if hasattr(stream, "cuda_stream"):
+        return ctypes.c_void_p(stream.cuda_stream)
+    return ctypes.c_void_p(stream)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def make_sgd(base_lr=0.01, momentum=0.9, weight_decay=5e-4, lr_policy="inv", gamma=1e-4,
+             power=0.75):
+    """Caffe LeNet solver defaults."""
+    return pn_sgd(base_lr, momentum, weight_decay, gamma, power, 1 if lr_policy == "inv" else 0)
+
+
+class Net:
+    """One net per device: net_create / net_forward / net_backward / sgd_update."""
+
+    def __init__(self, spec, batch, device=0, tf32=False, layerwise=False):
+        text = spec_text(spec) if "\n" not in spec else spec
+        flags = (_lib.PN_TF32 if tf32 else 0) | (_lib.PN_LAYERWISE if layerwise else 0)
+        h = ctypes.c_void_p()
+        check(lib().net_create(text.encode(), batch, device, flags, ctypes.byref(h)))
+        self._h = h
+        self.batch = batch
+        self.device = device
+        self.tf32 = tf32
+        self.blobs = {}
+        n = ctypes.c_int()
+        check(lib().net_blob_count(h, ctypes.byref(n)))
+        for i in range(n.value):
+            name = ctypes.c_char_p()
+            dims = (ctypes.c_int * 4)()
+            isp, mat = ctypes.c_int(), ctypes.c_int()
+            check(lib().net_blob_info(h, i, ctypes.byref(name), dims, ctypes.byref(isp),
+                                      ctypes.byref(mat)))
+            self.blobs[name.value.decode()] = {"dims": tuple(dims), "is_param": bool(isp.value),
+                                               "materialised": bool(mat.value)}
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().net_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------- params
+    def param_names(self):
+        return [k for k, v in self.blobs.items() if v["is_param"]]
+
+    def param_count(self):
+        n = ctypes.c_int64()
+        check(lib().net_param_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    def net_set_param(self, name, value, stream=None):
+        import torch
+        if isinstance(value, np.ndarray):
+            v = np.ascontiguousarray(value, dtype=np.float32)
+            check(lib().net_set_param(self._h, name.encode(), v.ctypes.data_as(ctypes.c_void_p),
+                                      v.size, 1, _stream(stream)))
+        else:
+            t = value.detach().to(device=f"cuda:{self.device}", dtype=torch.float32).contiguous()
+            check(lib().net_set_param(self._h, name.encode(), _ptr(t), t.numel(), 0,
+                                      _stream(stream)))
+            torch.cuda.current_stream(self.device).synchronize()
+
+    def set_params(self, params):
+        for k, v in params.items():
+            self.net_set_param(k, v)
+
+    def blob_shape(self, name):
+        return self.blobs[name]["dims"]
+
+    def net_get_blob(self, name, which=PN_DATA, stream=None):
+        """Blob contents as a new CUDA tensor (int32 for PN_MASK and 'pred')."""
+        import torch
+        dims = self.blobs[name]["dims"]
+        dt = torch.int32 if (which == PN_MASK or name == "pred") else torch.float32
+        out = torch.empty(dims, dtype=dt, device=f"cuda:{self.device}")
+        check(lib().net_get_blob(self._h, name.encode(), which, _ptr(out), out.numel() * 4, 0,
+                                 _stream(stream)))
+        return out
+
+    def net_put_blob(self, name, value, which=PN_DATA, stream=None):
+        import torch
+        dt = torch.int32 if which == PN_MASK else torch.float32
+        t = torch.as_tensor(value).to(device=f"cuda:{self.device}", dtype=dt).contiguous()
+        check(lib().net_put_blob(self._h, name.encode(), which, _ptr(t), t.numel() * 4, 0,
+                                 _stream(stream)))
+        torch.cuda.current_stream(self.device).synchronize()
+
+    # ------------------------------------------------------------ compute
+    def net_forward(self, x, labels, loss=None, stream=None):
+        check(lib().net_forward(self._h, _ptr(x), _ptr(labels), _ptr(loss), _stream(stream)))
+
+    def net_backward(self, stream=None):
+        check(lib().net_backward(self._h, _stream(stream)))
+
+    def sgd_update(self, sgd, it, stream=None):
+        check(lib().sgd_update(self._h, ctypes.byref(sgd), it, _stream(stream)))
+
+    def net_train_step(self, x, labels, sgd, it, loss=None, stream=None):
+        check(lib().net_train_step(self._h, _ptr(x), _ptr(labels), ctypes.byref(sgd), it,
+                                   _ptr(loss), _stream(stream)))
+
+    def net_train_step_host(self, x_host, labels_host, sgd, it, stream=None):
+        """Host (preferably pinned) buffers in, host loss out (synchronous)."""
+        loss = ctypes.c_float()
+        check(lib().net_train_step_host(self._h, ctypes.c_void_p(x_host.data_ptr()),
+                                        ctypes.c_void_p(labels_host.data_ptr()), ctypes.byref(sgd),
+                                        it, ctypes.byref(loss), _stream(stream)))
+        return loss.value
+
+    def net_infer(self, x, labels, loss=None, stream=None):
+        check(lib().net_infer(self._h, _ptr(x), _ptr(labels), _ptr(loss), _stream(stream)))
+
+    def net_sync_errors(self, stream=None):
+        check(lib().net_sync_errors(self._h, _stream(stream)))
+
+    # ------------------------------------------------ stages / profiling
+    def stages(self, phase):
+        n = ctypes.c_int()
+        check(lib().net_stage_count(self._h, phase, ctypes.byref(n)))
+        out = []
+        for i in range(n.value):
+            s = ctypes.c_char_p()
+            check(lib().net_stage_name(self._h, phase, i, ctypes.byref(s)))
+            out.append(s.value.decode())
+        return out
+
+    def net_run_stage(self, phase, i, x=None, labels=None, stream=None):
+        check(lib().net_run_stage(self._h, phase, i, _ptr(x), _ptr(labels), _stream(stream)))
+
+    def net_profile_stages(self, x, labels, sgd, it, steps, stream=None):
+        names = [(ph, s) for ph in range(3) for s in self.stages(ph)]
+        buf = (ctypes.c_float * len(names))()
+        n = ctypes.c_int()
+        check(lib().net_profile_stages(self._h, _ptr(x), _ptr(labels), ctypes.byref(sgd), it, steps,
+                                       buf, len(names), ctypes.byref(n), _stream(stream)))
+        return [(ph, s, buf[i]) for i, (ph, s) in enumerate(names)]
+
+    def launches_per_step(self):
+        n = ctypes.c_int()
+        check(lib().net_launches_per_step(self._h, ctypes.byref(n)))
+        return n.value
+
+    # ------------------------------------------------------- data parallel
+    @staticmethod
+    def pn_nccl_unique_id():
+        buf = (ctypes.c_ubyte * 128)()
+        check(lib().pn_nccl_unique_id(buf))
+        return bytes(buf)
+
+    def net_dp_init(self, nranks, rank, uid):
+        buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
+        check(lib().net_dp_init(self._h, nranks, rank, buf))

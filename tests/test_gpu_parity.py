@@ -1,0 +1,292 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the
+same seeded inputs.  Net-level checks (forward blobs with propagated scales,
+loss, masks, predictions, parameter gradients) plus teacher-forced stage
+checks, in which each fused kernel is fed the oracle's inputs."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import capi
+from oracle.net import OracleNet
+from paper_2005_13076_b200 import PN_DIFF, PN_HISTORY, PN_MASK, Net, PnError, make_sgd, spec_text, synth
+from parity import (RTOL, assert_bitwise, assert_close, assert_norm, check_mask, check_pred,
+                    effective_scales)
+
+pytestmark = pytest.mark.gpu
+
+LENET_POOLS = {"pool1": ("conv1", (24, 24)), "pool2": ("conv2", (8, 8))}
+
+
+def make(spec, N, tf32=False, layerwise=False, seed_x=1, seed_w=2):
+    ref = OracleNet(spec_text(spec), N)
+    params = synth.xavier_params(ref.learnable(), seed=seed_w, bias="uniform")
+    ref.set_params(params)
+    net = Net(spec, N, tf32=tf32, layerwise=layerwise)
+    net.set_params(params)
+    if spec == "lenet":
+        x, y = synth.mnist_like(N, seed=seed_x)
+    else:
+        x, y = synth.cifar_like(N, seed=seed_x)
+    return net, ref, params, x, y
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def stage_index(net, phase, prefix):
+    names = net.stages(phase)
+    for i, n in enumerate(names):
+        if n.startswith(prefix):
+            return i
+    raise KeyError(f"no stage {prefix!r} in {names}")
+
+
+def run(net, phase, prefix, x=None, y=None):
+    net.net_run_stage(phase, stage_index(net, phase, prefix), x, y)
+    torch.cuda.synchronize()
+
+
+# --------------------------------------------------------------- net level
+@pytest.mark.parametrize("spec,N,tf32,layerwise", [
+    ("lenet", 64, False, False),
+    ("lenet", 64, False, True),
+    ("lenet", 37, False, False),          # ragged batch
+    ("lenet", 1, False, False),           # degenerate batch
+    ("cifar10_quick", 16, False, True),
+    ("lenet", 64, True, False),
+    ("lenet", 37, True, False),
+])
+def test_net_forward_backward(spec, N, tf32, layerwise):
+    net, ref, params, x, y = make(spec, N, tf32, layerwise)
+    rtol = RTOL[tf32]
+    xd, yd = cuda(x), cuda(y)
+    loss = torch.zeros(1, device="cuda")
+    net.net_forward(xd, yd, loss)
+    net.net_backward()
+    net.net_sync_errors()
+    out = ref.forward(x, y)
+    seff = effective_scales(ref, out)
+    gref = ref.backward()
+    # forward blobs the plan materialises
+    for L in ref.layers:
+        name, t = L["name"], L["type"]
+        if t == "SoftmaxWithLoss" or not net.blobs.get(L["top"], {}).get("materialised", False):
+            continue
+        if t == "ReLU":
+            continue  # compared through the in-place blob below
+        g = host(net.net_get_blob(L["top"]))
+        o = out["blobs"][name]
+        # in-place ReLU: the GPU blob holds the post-activation value
+        nxt = [M for M in ref.layers if M["type"] == "ReLU" and M["bottom"] == L["top"]]
+        if nxt:
+            o = out["blobs"][nxt[0]["name"]]
+        assert_close(f"{name}", g.reshape(o.shape), o, seff[name], rtol)
+    # masks (exact up to oracle near-ties)
+    for L in ref.layers:
+        if L["type"] == "Pooling" and L["method"] == capi.MAX:
+            pre = [M for M in ref.layers if M["top"] == L["bottom"]][0]["name"]
+            gm = host(net.net_get_blob(L["top"], PN_MASK))
+            check_mask(L["name"], gm, out["masks"][L["name"]], out["blobs"][pre], seff[pre],
+                       L["in_shape"][2:], L["k"][0], L["s"][0], L["p"][0], rtol)
+    # loss, probabilities, predictions
+    lscale = seff["logits"]
+    assert abs(loss.item() - out["loss"]) <= rtol * (1 + float(lscale.max())) , (loss.item(), out["loss"])
+    prob = host(net.net_get_blob("prob")).reshape(out["prob"].shape)
+    assert_close("prob", prob, out["prob"], lscale.max(axis=1, keepdims=True) + 0 * prob, rtol)
+    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], lscale, rtol)
+    # parameter gradients: norm-wise (SURVEY §8(c) tolerance reading)
+    for k in params:
+        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
+        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * rtol)
+
+
+def test_train_step_graph_equals_eager_and_is_deterministic():
+    N = 64
+    sgd = make_sgd()
+    results = []
+    for mode in ("eager", "graph", "graph"):
+        net, ref, params, x, y = make("lenet", N)
+        xd, yd = cuda(x), cuda(y)
+        loss = torch.zeros(1, device="cuda")
+        for it in range(3):
+            if mode == "eager":
+                net.net_forward(xd, yd, loss)
+                net.net_backward()
+                net.sgd_update(sgd, it)
+            else:
+                net.net_train_step(xd, yd, sgd, it, loss)
+        results.append([host(net.net_get_blob(k)) for k in params] + [loss.item()])
+        net.close()
+    for a, b in zip(results[0][:-1], results[1][:-1]):
+        assert_bitwise("eager vs graph", a, b)
+    for a, b in zip(results[1][:-1], results[2][:-1]):
+        assert_bitwise("graph rerun", a, b)
+
+
+@pytest.mark.parametrize("tf32", [False, True])
+def test_sgd_update_bitexact(tf32):
+    """S:536-544 under teacher forcing: the GPU's own gradients, weights and
+    history fed to the oracle's fp32 SGD give bit-identical results."""
+    N = 32
+    net, ref, params, x, y = make("lenet", N, tf32)
+    sgd = make_sgd()
+    xd, yd = cuda(x), cuda(y)
+    net.net_train_step(xd, yd, sgd, 0)   # non-zero history
+    net.net_forward(xd, yd)
+    net.net_backward()
+    torch.cuda.synchronize()
+    before = {k: (host(net.net_get_blob(k)), host(net.net_get_blob(k, PN_DIFF)),
+                  host(net.net_get_blob(k, PN_HISTORY))) for k in params}
+    it = 7
+    net.sgd_update(sgd, it)
+    lr = capi.lr_at(capi.INV, sgd.base_lr, sgd.gamma, sgd.power, it)
+    for k, (w, g, v) in before.items():
+        w, v = w.copy(), v.copy()
+        capi.sgd_update_f32(w.ravel(), g.ravel(), v.ravel(), np.float32(lr), np.float32(sgd.momentum),
+                            np.float32(sgd.weight_decay))
+        assert_bitwise(f"sgd w {k}", host(net.net_get_blob(k)), w)
+        assert_bitwise(f"sgd v {k}", host(net.net_get_blob(k, PN_HISTORY)), v)
+
+
+def test_label_out_of_range_is_reported():
+    net, ref, params, x, y = make("lenet", 8)
+    y[3] = 10
+    net.net_forward(cuda(x), cuda(y))
+    with pytest.raises(PnError) as e:
+        net.net_sync_errors()
+    assert "PN_ERR_LABEL_RANGE" in str(e.value)
+    y[3] = 2
+    net.net_forward(cuda(x), cuda(y))
+    net.net_sync_errors()
+
+
+def test_backward_before_forward_is_state_error():
+    net, *_ = make("lenet", 8)
+    with pytest.raises(PnError) as e:
+        net.net_backward()
+    assert "PN_ERR_STATE" in str(e.value)
+    with pytest.raises(PnError):
+        net.net_get_blob("conv1")  # fused plan never stores conv1's output
+
+
+# ---------------------------------------------------------- teacher forcing
+@pytest.mark.parametrize("tf32", [False, True])
+def test_teacher_forced_fused_stages(tf32):
+    N = 64
+    rtol = RTOL[tf32]
+    net, ref, params, x, y = make("lenet", N, tf32)
+    out = ref.forward(x, y)
+    gref = ref.backward()
+    sc = out["scales"]
+    xd, yd = cuda(x), cuda(y)
+    net.net_forward(xd, yd)          # establishes step args
+    torch.cuda.synchronize()
+
+    # conv1 + pool1 (input x)
+    run(net, 0, "conv1+pool1", xd, yd)
+    S1, _ = capi.pool_fwd(sc["conv1"], capi.MAX, (2, 2), (2, 2))
+    assert_close("pool1", host(net.net_get_blob("pool1")), out["blobs"]["pool1"], S1, RTOL[False])
+    check_mask("pool1", host(net.net_get_blob("pool1", PN_MASK)), out["masks"]["pool1"],
+               out["blobs"]["conv1"], sc["conv1"], (24, 24), 2, 2, 0, RTOL[False])
+    # conv2 + pool2 from the oracle's pool1
+    net.net_put_blob("pool1", out["blobs"]["pool1"].astype(np.float32))
+    run(net, 0, "conv2+pool2")
+    S2, _ = capi.pool_fwd(sc["conv2"], capi.MAX, (2, 2), (2, 2))
+    assert_close("pool2", host(net.net_get_blob("pool2")), out["blobs"]["pool2"], S2, rtol)
+    check_mask("pool2", host(net.net_get_blob("pool2", PN_MASK)), out["masks"]["pool2"],
+               out["blobs"]["conv2"], sc["conv2"], (8, 8), 2, 2, 0, rtol)
+    # ip1 + relu from the oracle's pool2
+    net.net_put_blob("pool2", out["blobs"]["pool2"].astype(np.float32))
+    run(net, 0, "ip1+relu")
+    assert_close("ip1", host(net.net_get_blob("ip1")).reshape(N, 500),
+                 out["blobs"]["relu1"].reshape(N, 500), sc["ip1"].reshape(N, 500), rtol)
+    # ip2 + softmax-loss from the oracle's ip1
+    net.net_put_blob("ip1", out["blobs"]["relu1"].astype(np.float32))
+    run(net, 0, "ip2+softmax_loss", xd, yd)
+    run(net, 0, "loss_reduce")
+    s2 = sc["ip2"].reshape(N, 10)
+    assert_close("logits", host(net.net_get_blob("ip2")).reshape(N, 10), out["logits"], s2, RTOL[False])
+    assert_close("prob", host(net.net_get_blob("prob")).reshape(N, 10), out["prob"],
+                 s2.max(axis=1, keepdims=True) + 0 * out["prob"], RTOL[False])
+    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], s2, RTOL[False])
+    assert abs(host(net.net_get_blob("loss"))[0, 0, 0, 0] - out["loss"]) <= 1e-5 * (1 + out["loss"])
+    dz = gref["diffs"]["loss"].reshape(N, 10)
+    assert_close("dz", host(net.net_get_blob("ip2", PN_DIFF)).reshape(N, 10), dz,
+                 s2.max(axis=1, keepdims=True) / N + np.abs(dz), RTOL[False])
+
+    # backward: ip2 + relu1 from oracle dz and ip1
+    net.net_put_blob("ip2", dz.astype(np.float32).reshape(N, 10, 1, 1), PN_DIFF)
+    run(net, 1, "ip2.bwd")
+    run(net, 1, "ip2.wgrad_reduce")
+    gs = gref["scales"]
+    assert_close("ip2.w grad", host(net.net_get_blob("ip2.w", PN_DIFF)), gref["grads"]["ip2.w"], gs["ip2.w"],
+                 RTOL[False])
+    assert_close("ip2.b grad", host(net.net_get_blob("ip2.b", PN_DIFF)).ravel(), gref["grads"]["ip2.b"],
+                 gs["ip2.b"], RTOL[False])
+    da1 = gref["diffs"]["relu1"].reshape(N, 500)
+    assert_close("da1", host(net.net_get_blob("ip1", PN_DIFF)).reshape(N, 500), da1,
+                 gs["ip2.dx"].reshape(N, 500), RTOL[False])
+    # ip1 backward (+ pool2 backward) from oracle da1
+    net.net_put_blob("ip1", da1.astype(np.float32).reshape(N, 500, 1, 1), PN_DIFF)
+    net.net_put_blob("pool2", out["masks"]["pool2"], PN_MASK)
+    for name in net.stages(1):
+        if name.startswith("ip1.") or name.startswith("pool2"):
+            run(net, 1, name)
+    assert_close("ip1.w grad", host(net.net_get_blob("ip1.w", PN_DIFF)), gref["grads"]["ip1.w"], gs["ip1.w"], rtol)
+    assert_close("ip1.b grad", host(net.net_get_blob("ip1.b", PN_DIFF)).ravel(), gref["grads"]["ip1.b"],
+                 gs["ip1.b"], RTOL[False])
+    G2 = gref["diffs"]["pool2"]
+    Sg2, = [capi.pool_bwd(gs["ip1.dx"].reshape(N, 50, 4, 4), out["masks"]["pool2"], (N, 50, 8, 8), capi.MAX,
+                          (2, 2), (2, 2))]
+    assert_close("conv2 diff (unpooled)", host(net.net_get_blob("conv2", PN_DIFF)), G2, Sg2, rtol)
+    # conv2 backward from the oracle's G2
+    net.net_put_blob("conv2", G2.astype(np.float32), PN_DIFF)
+    run(net, 1, "conv2.dgrad")
+    run(net, 1, "conv2.wgrad")
+    run(net, 1, "conv2.wgrad_reduce")
+    assert_close("dp1", host(net.net_get_blob("pool1", PN_DIFF)), gref["diffs"]["conv2"], gs["conv2.dx"], rtol)
+    assert_close("conv2.w grad", host(net.net_get_blob("conv2.w", PN_DIFF)), gref["grads"]["conv2.w"],
+                 gs["conv2.w"], rtol)
+    assert_close("conv2.b grad", host(net.net_get_blob("conv2.b", PN_DIFF)).ravel(), gref["grads"]["conv2.b"],
+                 gs["conv2.b"], RTOL[False])
+    # conv1 weight gradient from the oracle's dp1 and mask1
+    net.net_put_blob("pool1", gref["diffs"]["conv2"].astype(np.float32), PN_DIFF)
+    net.net_put_blob("pool1", out["masks"]["pool1"], PN_MASK)
+    run(net, 1, "conv1.wgrad", xd, yd)
+    run(net, 1, "conv1.wgrad_reduce")
+    assert_close("conv1.w grad", host(net.net_get_blob("conv1.w", PN_DIFF)), gref["grads"]["conv1.w"],
+                 gs["conv1.w"], RTOL[False])
+    assert_close("conv1.b grad", host(net.net_get_blob("conv1.b", PN_DIFF)).ravel(), gref["grads"]["conv1.b"],
+                 gs["conv1.b"], RTOL[False])
+
+
+# ------------------------------------------------------------ full size
+@pytest.mark.parametrize("tf32", [False, True])
+def test_full_size_bench_configuration(tf32):
+    """BASELINE config 3 per GPU (N=512) in the launch configuration bench.py
+    times (graph-replayed net_train_step): loss, predictions and every
+    parameter gradient vs the oracle at full size."""
+    N = 512
+    rtol = RTOL[tf32]
+    net, ref, params, x, y = make("lenet", N, tf32)
+    xd, yd = cuda(x), cuda(y)
+    loss = torch.zeros(1, device="cuda")
+    sgd = make_sgd()
+    net.net_train_step(xd, yd, sgd, 0, loss)
+    net.net_sync_errors()
+    out = ref.forward(x, y)
+    seff = effective_scales(ref, out)
+    gref = ref.backward()
+    assert abs(loss.item() - out["loss"]) <= rtol * (1 + float(seff["logits"].max()))
+    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], seff["logits"], rtol)
+    # gradients were overwritten by nothing after backward: the step's SGD
+    # used them; compare them norm-wise
+    for k in params:
+        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
+        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * rtol)
