@@ -230,7 +230,7 @@ def main():
     xs, ys = synth.mnist_like_fast(BATCH * DATASET_BATCHES, seed=100 + rank)
     X = torch.from_numpy(xs).cuda().view(DATASET_BATCHES, BATCH, 1, 28, 28)
     Y = torch.from_numpy(ys).cuda().view(DATASET_BATCHES, BATCH)
-    loss = torch.zeros(1, device="cuda")
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
     sgd = make_sgd()
     stream = torch.cuda.current_stream()
 

@@ -167,6 +167,7 @@ struct pn_net {
 
   cudaStream_t cap = nullptr;  // capture stream
   cudaGraphExec_t step_exec = nullptr, infer_exec = nullptr;
+  cudaGraph_t step_graph = nullptr, infer_graph = nullptr;
   StepArgs step_args, infer_args;  // args baked into the executable graphs
   int launches_per_step = 0;
 
@@ -792,7 +793,10 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_
   CU(cudaStreamEndCapture(net->cap, &g));
   if (*out) cudaGraphExecDestroy(*out);
   CU(cudaGraphInstantiate(out, g, 0));
-  cudaGraphDestroy(g);
+  // keep the graph: its node handles address the exec's nodes when patching
+  cudaGraph_t& keep = infer ? net->infer_graph : net->step_graph;
+  if (keep) cudaGraphDestroy(keep);
+  keep = g;
   return PN_OK;
 }
 
@@ -857,6 +861,8 @@ extern "C" void net_destroy(pn_net* net) {
   cudaDeviceSynchronize();
   if (net->step_exec) cudaGraphExecDestroy(net->step_exec);
   if (net->infer_exec) cudaGraphExecDestroy(net->infer_exec);
+  if (net->step_graph) cudaGraphDestroy(net->step_graph);
+  if (net->infer_graph) cudaGraphDestroy(net->infer_graph);
   if (net->cap) cudaStreamDestroy(net->cap);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);

@@ -31,9 +31,15 @@ def _stream(stream):
     return ctypes.c_void_p(stream)
 
 
-def _ptr(t):
+def _ptr(t, dtype=None):
     if t is None:
         return None
+    if dtype is not None:
+        import torch
+        want = {"f32": torch.float32, "i32": torch.int32}[dtype]
+        if t.dtype != want or not t.is_cuda or not t.is_contiguous():
+            raise TypeError(f"expected a contiguous CUDA {want} tensor, got {t.dtype} "
+                            f"on {t.device} (contiguous={t.is_contiguous()})")
     return ctypes.c_void_p(t.data_ptr())
 
 
@@ -126,7 +132,8 @@ class Net:
 
     # ------------------------------------------------------------ compute
     def net_forward(self, x, labels, loss=None, stream=None):
-        check(lib().net_forward(self._h, _ptr(x), _ptr(labels), _ptr(loss), _stream(stream)))
+        check(lib().net_forward(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), _ptr(loss, 'f32'),
+                                _stream(stream)))
 
     def net_backward(self, stream=None):
         check(lib().net_backward(self._h, _stream(stream)))
@@ -135,8 +142,8 @@ class Net:
         check(lib().sgd_update(self._h, ctypes.byref(sgd), it, _stream(stream)))
 
     def net_train_step(self, x, labels, sgd, it, loss=None, stream=None):
-        check(lib().net_train_step(self._h, _ptr(x), _ptr(labels), ctypes.byref(sgd), it,
-                                   _ptr(loss), _stream(stream)))
+        check(lib().net_train_step(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), ctypes.byref(sgd),
+                                   it, _ptr(loss, 'f32'), _stream(stream)))
 
     def net_train_step_host(self, x_host, labels_host, sgd, it, stream=None):
         """Host (preferably pinned) buffers in, host loss out (synchronous)."""
@@ -147,7 +154,8 @@ class Net:
         return loss.value
 
     def net_infer(self, x, labels, loss=None, stream=None):
-        check(lib().net_infer(self._h, _ptr(x), _ptr(labels), _ptr(loss), _stream(stream)))
+        check(lib().net_infer(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), _ptr(loss, 'f32'),
+                              _stream(stream)))
 
     def net_sync_errors(self, stream=None):
         check(lib().net_sync_errors(self._h, _stream(stream)))
@@ -164,13 +172,15 @@ class Net:
         return out
 
     def net_run_stage(self, phase, i, x=None, labels=None, stream=None):
-        check(lib().net_run_stage(self._h, phase, i, _ptr(x), _ptr(labels), _stream(stream)))
+        check(lib().net_run_stage(self._h, phase, i, _ptr(x, 'f32'), _ptr(labels, 'i32'),
+                                  _stream(stream)))
 
     def net_profile_stages(self, x, labels, sgd, it, steps, stream=None):
         names = [(ph, s) for ph in range(3) for s in self.stages(ph)]
         buf = (ctypes.c_float * len(names))()
         n = ctypes.c_int()
-        check(lib().net_profile_stages(self._h, _ptr(x), _ptr(labels), ctypes.byref(sgd), it, steps,
+        check(lib().net_profile_stages(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), ctypes.byref(sgd),
+                                       it, steps,
                                        buf, len(names), ctypes.byref(n), _stream(stream)))
         return [(ph, s, buf[i]) for i, (ph, s) in enumerate(names)]
 

@@ -17,13 +17,16 @@ RTOL = {False: 1e-5, True: 2e-3}
 
 
 def ratio(gpu, ref, scale, rtol, atol=1e-30):
-    gpu = np.asarray(gpu, np.float64)
     ref = np.asarray(ref, np.float64)
+    gpu = np.asarray(gpu, np.float64).reshape(ref.shape)
     bound = rtol * np.asarray(scale, np.float64) + atol
     return np.abs(gpu - ref) / bound
 
 
 def assert_close(name, gpu, ref, scale, rtol, atol=1e-30):
+    ref = np.asarray(ref)
+    gpu = np.asarray(gpu).reshape(ref.shape)
+    scale = np.broadcast_to(np.asarray(scale), ref.shape)
     r = ratio(gpu, ref, scale, rtol, atol)
     worst = float(r.max()) if r.size else 0.0
     if worst > 1.0:

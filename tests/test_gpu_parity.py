@@ -66,7 +66,7 @@ def test_net_forward_backward(spec, N, tf32, layerwise):
     net, ref, params, x, y = make(spec, N, tf32, layerwise)
     rtol = RTOL[tf32]
     xd, yd = cuda(x), cuda(y)
-    loss = torch.zeros(1, device="cuda")
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
     net.net_forward(xd, yd, loss)
     net.net_backward()
     net.net_sync_errors()
@@ -113,7 +113,7 @@ def test_train_step_graph_equals_eager_and_is_deterministic():
     for mode in ("eager", "graph", "graph"):
         net, ref, params, x, y = make("lenet", N)
         xd, yd = cuda(x), cuda(y)
-        loss = torch.zeros(1, device="cuda")
+        loss = torch.zeros(1, device="cuda", dtype=torch.float32)
         for it in range(3):
             if mode == "eager":
                 net.net_forward(xd, yd, loss)
@@ -276,7 +276,7 @@ def test_full_size_bench_configuration(tf32):
     rtol = RTOL[tf32]
     net, ref, params, x, y = make("lenet", N, tf32)
     xd, yd = cuda(x), cuda(y)
-    loss = torch.zeros(1, device="cuda")
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
     sgd = make_sgd()
     net.net_train_step(xd, yd, sgd, 0, loss)
     net.net_sync_errors()

@@ -16,7 +16,6 @@ import torch.nn.functional as Fn
 from conftest import golden
 from oracle import capi
 
-torch.set_default_dtype(torch.float64)
 
 
 def rel_err(a, b, scale):
@@ -24,7 +23,7 @@ def rel_err(a, b, scale):
 
 
 def t64(a):
-    return torch.tensor(np.asarray(a, dtype=np.float64))
+    return torch.tensor(np.asarray(a, dtype=np.float64), dtype=torch.float64)
 
 
 # ----------------------------------------------------------------- geometry
@@ -51,7 +50,7 @@ def test_pool_ceil_sizes():
     assert capi.pool_out_size(8, 3, 2, 0) == 4
     # torch's ceil_mode agrees on these sizes (independent library)
     for n, k, s, p in [(32, 3, 2, 0), (7, 3, 2, 1), (6, 2, 2, 1), (5, 3, 3, 1), (13, 3, 2, 0)]:
-        t = Fn.max_pool2d(torch.zeros(1, 1, n, n), k, s, p, ceil_mode=True)
+        t = Fn.max_pool2d(torch.zeros(1, 1, n, n, dtype=torch.float64), k, s, p, ceil_mode=True)
         assert capi.pool_out_size(n, k, s, p) == t.shape[-1], (n, k, s, p)
 
 
