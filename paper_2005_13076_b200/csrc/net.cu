@@ -158,6 +158,7 @@ struct pn_net {
   float* partials = nullptr;
   int64_t npartials = 0;
   float* row_loss = nullptr;
+  float* w2d = nullptr;  // TF32 repack of conv2 weights for the data gradient
   unsigned* err = nullptr;
   std::vector<void*> allocs;
 
@@ -398,13 +399,16 @@ static pn_status allocate(pn_net* net) {
   int64_t poff = 0;
   for (auto& L : net->layers) {
     if (L.off < 0) continue;
-    L.splits = kWgradSplits;
+    // conv1's fused weight gradient is a light SIMT kernel: give it more
+    // CTAs (4 images each at batch 512)
+    L.splits = (net->fused && &L == &net->layers[0]) ? 4 * kWgradSplits : kWgradSplits;
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
   }
   net->npartials = poff;
   TRY(net->alloc(&net->partials, poff > 0 ? poff : 1));
   TRY(net->alloc(&net->row_loss, net->batch));
+  if (net->tf32) TRY(net->alloc(&net->w2d, 32 * 1280));
   TRY(net->alloc(&net->err, 1));
   // activation blobs (the fused plan never stores conv1's output or its
   // gradient, nor conv2's output; conv2's gradient is the dense unpooled G2)
@@ -645,7 +649,8 @@ static void build_fused_lenet(pn_net* net) {
     add(bwd, "pool2.bwd", l4);
   }
   if (net->tf32) {
-    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, P + c2.off, p1.diff, N, net->tc_sms));
+    add(bwd, "conv2.wpack[tc]", tc::pack_w2d_launch(P + c2.off, net->w2d));
+    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->w2d, p1.diff, N, net->tc_sms));
     add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits,
                                                        N, net->tc_sms));
     add_reduce(net, bwd, c2);

@@ -1,24 +1,26 @@
 // tc.cu -- tcgen05 TF32 implicit-GEMM kernels for the GEMM-shaped LeNet
 // layers.
 //
-// Engine (one CTA = one 128-row output tile, 4 warps):
-//   * every thread is a producer: it gathers its share of the A (128 x 32)
-//     and B (BN x 32) K-chunk straight from global memory -- the implicit
-//     im2col / col2im index math of the layer -- rounds each value to TF32
-//     with cvt.rna (round to nearest), and stores 16-byte
-//     core-matrix rows into shared memory in the UMMA canonical K-major
-//     no-swizzle layout (8 rows x 16 B core matrices; LBO = 128 B between
-//     the two K halves of one MMA, SBO = 1024 B between 8-row groups);
-//   * one elected thread issues tcgen05.mma.cta_group::1.kind::tf32
-//     (M = 128, N = BN, K = 8) x 4 per chunk, accumulating in TMEM, and
-//     tcgen05.commit's the chunk's stage back to the producers (mbarrier);
-//   * a 3-stage smem ring lets the gather of chunk k+1.. overlap the MMAs
-//     of chunk k;
-//   * the epilogue reads TMEM with tcgen05.ld 32x32b (thread = tile row)
-//     and applies the layer's fused tail: bias + 2x2 max-pool + origin mask
-//     (conv2), bias + ReLU (ip1), max-pool backward scatter (ip1 dgrad),
-//     plain stores (conv2 dgrad), split-K partial stores + bias gradient
-//     (conv2 / ip1 weight gradients).
+// Engine (one CTA = one 128-row output tile, 8 warps, all producers):
+//   * operands are assembled per 32-wide K chunk in a shared-memory ring in
+//     the UMMA canonical K-major no-swizzle layout (core matrix = 8 rows x
+//     4 K (16 B); LBO = 128 B between the K halves of one MMA, SBO = 1024 B
+//     between 8-row groups).  MN-major TF32 descriptors were measured to
+//     produce zeros on this part (tools/umma_probe.cu), so transposed global
+//     operands are gathered into K-major rows as well;
+//   * copy-type operand units move global -> shared with cp.async (16-byte
+//     rows, or 4 x 4-byte scalars for transposed operands), issued
+//     LOOKAHEAD chunks ahead of the chunk being consumed; the issuing thread
+//     later rounds its own units to TF32 in place (cvt.rna: round to
+//     nearest) -- pre-rounded packed weights skip that;
+//     gather-type units (implicit im2col) are built from activations the CTA
+//     staged in shared memory;
+//   * one thread issues tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN,
+//     K=8) x 4 per chunk into a TMEM accumulator and tcgen05.commit's the
+//     stage back to the producers through an mbarrier;
+//   * the epilogue reads TMEM with tcgen05.ld 32x32b (thread = tile row;
+//     warps 4-7 take the upper half of the columns) and applies the layer's
+//     fused tail.
 #include <cstdint>
 
 #include "tc.h"
@@ -26,10 +28,11 @@
 namespace pn {
 namespace tc {
 
-constexpr int BM = 128;     // tile rows = UMMA M
-constexpr int BK = 32;      // K elements per chunk (4 MMAs of K = 8)
-constexpr int STAGES = 3;
-constexpr int THREADS = 128;
+constexpr int BM = 128;  // tile rows = UMMA M
+constexpr int BK = 32;   // K elements per chunk (4 MMAs of K = 8)
+constexpr int THREADS = 256;
+
+enum Mode { COPY16 = 0, COPY16_PRE = 1, COPY4 = 2, GATHER = 3 };
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -98,45 +101,153 @@ __device__ __forceinline__ uint32_t to_tf32(float x) {
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
 }
+__device__ __forceinline__ float tf32f(float x) { return __uint_as_float(to_tf32(x)); }
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(to_tf32(v.x)), "r"(to_tf32(v.y)),
                "r"(to_tf32(v.z)), "r"(to_tf32(v.w))
                : "memory");
 }
-// UMMA shared-memory descriptor, K-major, no swizzle (sm_100 "version" 1).
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp4(uint32_t dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// UMMA shared-memory descriptor, no swizzle, sm_100 version 1.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
-  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);       // start address
-  d |= (uint64_t)(128 >> 4) << 16;               // LBO: next 16-B K chunk
-  d |= (uint64_t)(1024 >> 4) << 32;              // SBO: next 8-row group
-  d |= (uint64_t)1 << 46;                        // descriptor version (sm_100)
-  return d;                                      // layout type 0 = SWIZZLE_NONE
+  d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
 }
 // Instruction descriptor: kind::tf32, D = F32, A = B = TF32, both K-major.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-__device__ __forceinline__ uint32_t core_off(int r, int kc) {  // byte offset of (row, 16-B K chunk)
+// K-major: byte offset of (row r, 16-B K chunk kc) inside a [rows x 32] chunk
+__device__ __forceinline__ uint32_t kmaj_off(int r, int kc) {
   return (uint32_t)((r >> 3) * 1024 + kc * 128 + (r & 7) * 16);
 }
+__device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
+__device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // ------------------------------------------------------------------ engine
+// Op interface:
+//   BN, TMEM_COLS, STAGES, A_MODE, B_MODE, STAGE_BYTES, SYNC_AFTER_WAIT
+//   Op(params, staging_smem, ring_smem)        decodes the tile
+//   int num_k_chunks()
+//   void stage(tid)                            one-time staging (engine syncs after)
+//   void issue_extra(chunk, tid)               extra cp.async work for a chunk (may be empty)
+//   COPY16/_PRE: const float* a_src(r, k, &valid)    16-byte source of A(r, k..k+3)
+//   COPY4:       const float* a_src4(r, k, t, &valid) source of A(r, k+t)
+//   GATHER:      float4 a(r, k)                    built from staged smem
+//   (B likewise with b_src / b_src4 / b)
+//   void a_raw(r, k, float4) / b_raw(c, k, float4)   raw copied values (bias sums)
+//   void epilogue(row, c0, v[16])              columns c0..c0+15
+//   void finish(tid)                           after epilogue + __syncthreads
+template <class Op>
+__device__ __forceinline__ void issue_chunk(Op& op, uint32_t As, uint32_t Bs, int k0, int tid) {
+  constexpr int BN = Op::BN;
+  if (Op::A_MODE != GATHER) {
+#pragma unroll
+    for (int q = 0; q < BM * (BK / 4) / THREADS; ++q) {
+      const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
+      const uint32_t dst = As + kmaj_off(r, kc);
+      if (Op::A_MODE == COPY4) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          bool v;
+          const float* s = op.a_src4(r, k0 + kc * 4, t, v);
+          cp4(dst + 4 * t, s, v);
+        }
+      } else {
+        bool v;
+        const float* s = op.a_src(r, k0 + kc * 4, v);
+        cp16(dst, s, v);
+      }
+    }
+  }
+  if (Op::B_MODE != GATHER) {
+    for (int u = tid; u < BN * (BK / 4); u += THREADS) {
+      const int c = u % BN, kc = u / BN;
+      const uint32_t dst = Bs + kmaj_off(c, kc);
+      if (Op::B_MODE == COPY4) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          bool v;
+          const float* s = op.b_src4(c, k0 + kc * 4, t, v);
+          cp4(dst + 4 * t, s, v);
+        }
+      } else {
+        bool v;
+        const float* s = op.b_src(c, k0 + kc * 4, v);
+        cp16(dst, s, v);
+      }
+    }
+  }
+}
+
+template <class Op>
+__device__ __forceinline__ void produce_chunk(Op& op, uint32_t As, uint32_t Bs, int k0, int tid) {
+  constexpr int BN = Op::BN;
+#pragma unroll
+  for (int q = 0; q < BM * (BK / 4) / THREADS; ++q) {
+    const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
+    const uint32_t dst = As + kmaj_off(r, kc);
+    if (Op::A_MODE == GATHER) {
+      sts128(dst, op.a(r, k0 + kc * 4));
+    } else if (Op::A_MODE != COPY16_PRE) {
+      const float4 v = lds128(dst);
+      op.a_raw(r, k0 + kc * 4, v);
+      sts128(dst, v);
+    }
+  }
+  for (int u = tid; u < BN * (BK / 4); u += THREADS) {
+    const int c = u % BN, kc = u / BN;
+    const uint32_t dst = Bs + kmaj_off(c, kc);
+    if (Op::B_MODE == GATHER) {
+      sts128(dst, op.b(c, k0 + kc * 4));
+    } else if (Op::B_MODE != COPY16_PRE) {
+      const float4 v = lds128(dst);
+      op.b_raw(c, k0 + kc * 4, v);
+      sts128(dst, v);
+    }
+  }
+}
+
 template <class Op>
 __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typename Op::Params prm) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  __shared__ uint64_t bars[STAGES + 1];
+  constexpr int S = Op::STAGES;
+  constexpr int L = S - 2 > 0 ? S - 2 : 1;  // cp.async lookahead (chunks)
+  __shared__ uint64_t bars[S + 1];
   __shared__ uint32_t tmem_base;
   constexpr int BN = Op::BN;
   constexpr int A_BYTES = BM * BK * 4;
   constexpr int B_BYTES = BN * BK * 4;
   constexpr int STAGE = A_BYTES + B_BYTES;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  Op op(prm);
+  Op op(prm, smem + S * STAGE, smem);
   if (tid == 0) {
-    for (int s = 0; s <= STAGES; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s <= S; ++s) mbar_init(&bars[s], 1);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&tmem_base, Op::TMEM_COLS);
+  op.stage(tid);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -144,64 +255,97 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
   const uint32_t sbase = smem_u32(smem);
   constexpr uint32_t idesc = make_idesc(BM, BN);
   const int nk = op.num_k_chunks();
+  // prologue: chunks 0 .. L-1 in flight
+#pragma unroll 1
+  for (int c = 0; c < L; ++c) {
+    if (c < nk) {
+      op.issue_extra(c, tid);
+      issue_chunk(op, sbase + (c % S) * STAGE, sbase + (c % S) * STAGE + A_BYTES, c * BK, tid);
+    }
+    cp_commit();
+  }
+#pragma unroll 1
   for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % STAGES, fill = kb / STAGES;
-    if (fill > 0) mbar_wait(&bars[s], (fill - 1) & 1);
+    const int s = kb % S;
+    const int c = kb + L;
+    if (c < nk) {
+      const int s2 = c % S;
+      if (c >= S) mbar_wait(&bars[s2], ((c / S) - 1) & 1);
+      op.issue_extra(c, tid);
+      issue_chunk(op, sbase + s2 * STAGE, sbase + s2 * STAGE + A_BYTES, c * BK, tid);
+    }
+    cp_commit();
+    cp_wait<L>();
+    if (Op::SYNC_AFTER_WAIT) __syncthreads();
     const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
-    const int k0 = kb * BK;
-#pragma unroll 2
-    for (int u = tid; u < BM * (BK / 4); u += THREADS) {
-      const int r = u & (BM - 1), kc = u >> 7;
-      sts128(As + core_off(r, kc), op.a4(r, k0 + kc * 4));
-    }
-#pragma unroll 2
-    for (int u = tid; u < BN * (BK / 4); u += THREADS) {
-      const int c = u % BN, kc = u / BN;
-      sts128(Bs + core_off(c, kc), op.b4(c, k0 + kc * 4));
-    }
+    produce_chunk(op, As, Bs, kb * BK, tid);
     fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
       tc_fence_after();
 #pragma unroll
       for (int k = 0; k < BK / 8; ++k)
-        mma_tf32(tbase, make_desc(As + k * 256), make_desc(Bs + k * 256), idesc, (kb | k) != 0);
+        mma_tf32(tbase, make_desc(As + k * 256, 128, 1024), make_desc(Bs + k * 256, 128, 1024), idesc,
+                 (kb | k) != 0);
       mma_commit(&bars[s]);
-      if (kb == nk - 1) mma_commit(&bars[STAGES]);
+      if (kb == nk - 1) mma_commit(&bars[S]);
     }
   }
-  const int row = warp * 32 + lane;
+  cp_wait<0>();
+  // epilogue: warps 0-3 columns [0, BN/2), warps 4-7 [BN/2, BN) (BN >= 32),
+  // or warps 0-3 only for BN = 16
+  const int row = (warp & 3) * 32 + lane;
+  constexpr int HALF = BN >= 32 ? BN / 2 : BN;
+  const bool active = BN >= 32 || warp < 4;
+  const int cbeg = (BN >= 32 && warp >= 4) ? HALF : 0;
   if (nk > 0) {
-    mbar_wait(&bars[STAGES], 0);
+    mbar_wait(&bars[S], 0);
     tc_fence_after();
+    if (active) {
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-      float v[16];
-      tmem_ld16(tbase + ((uint32_t)(warp * 32) << 16) + c0, v);
-      op.epilogue(row, c0, v, lane);
+      for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
+        op.epilogue(row, c0, v);
+      }
     }
-  } else {  // empty K range (e.g. a weight-gradient split with no images)
+  } else if (active) {  // empty K range (a weight-gradient split with no images)
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
       float v[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      op.epilogue(row, c0, v, lane);
+      op.epilogue(row, c0, v);
     }
   }
-  op.finish(row);
   tc_fence_before();
   __syncthreads();
+  op.finish(tid);
   if (warp == 0) tmem_dealloc(tbase, Op::TMEM_COLS);
 }
 
-__device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
-__device__ __forceinline__ float ld(const float* p) { return __ldg(p); }
+// common no-op hooks
+struct OpBase {
+  static constexpr bool SYNC_AFTER_WAIT = false;
+  __device__ void stage(int) {}
+  __device__ void issue_extra(int, int) {}
+  __device__ void a_raw(int, int, float4) {}
+  __device__ void b_raw(int, int, float4) {}
+  __device__ void finish(int) {}
+  __device__ float4 a(int, int) const { return zero4(); }
+  __device__ float4 b(int, int) const { return zero4(); }
+  __device__ const float* a_src(int, int, bool& v) const { v = false; return nullptr; }
+  __device__ const float* b_src(int, int, bool& v) const { v = false; return nullptr; }
+  __device__ const float* a_src4(int, int, int, bool& v) const { v = false; return nullptr; }
+  __device__ const float* b_src4(int, int, int, bool& v) const { v = false; return nullptr; }
+};
 
 // ------------------------------------------- conv2 + bias + pool2 (+mask)
 // rows r = (image n = 2*tile + r/64, position p = ho*8+wo), cols f (50 of 64),
-// K = (c,i,j) 500 (+12 zero pad).  A(r,k) = p1[n,c,ho+i,wo+j], B(f,k) = W2[f,k].
-struct Conv2Fwd {
+// K = (c,i,j) 500 (+12 zero pad).  A(r,k) = p1[n,c,ho+i,wo+j] gathered from
+// the two staged images through a k -> c*144+i*12+j table; B(f,k) = W2[f,k]
+// copied with cp.async.
+struct Conv2Fwd : OpBase {
   struct Params {
     const float* p1;
     const float* w;
@@ -210,24 +354,40 @@ struct Conv2Fwd {
     uint8_t* m2;
     int N;
   };
-  static constexpr int BN = 64, TMEM_COLS = 64;
+  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
+  static constexpr int A_MODE = GATHER, B_MODE = COPY16;
+  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 512 * 4;
   const Params& p;
-  int n0;
-  __device__ Conv2Fwd(const Params& q) : p(q), n0(blockIdx.x * 2) {}
+  float* img;
+  int* koff;
+  int n0, rowoff;
+  __device__ Conv2Fwd(const Params& q, uint8_t* st, uint8_t*)
+      : p(q), img((float*)st), koff((int*)(st + 2 * 2880 * 4)) {
+    n0 = blockIdx.x * 2;
+    const int r = threadIdx.x & 127, pos = r & 63;
+    rowoff = (r >> 6) * 2880 + (pos >> 3) * 12 + (pos & 7);
+  }
   __device__ int num_k_chunks() const { return 16; }
-  __device__ float a1(int r, int k) const {
-    const int n = n0 + (r >> 6);
-    if (k >= 500 || n >= p.N) return 0.f;
-    const int pos = r & 63, ho = pos >> 3, wo = pos & 7;
-    const int c = k / 25, rem = k - c * 25, i = rem / 5, j = rem - i * 5;
-    return ld(p.p1 + (size_t)n * 2880 + c * 144 + (ho + i) * 12 + wo + j);
+  __device__ void stage(int tid) {
+    const int cnt = min(2, p.N - n0) * 2880;
+    const float4* src = reinterpret_cast<const float4*>(p.p1 + (size_t)n0 * 2880);
+    for (int i = tid; i < 2 * 720; i += THREADS)
+      reinterpret_cast<float4*>(img)[i] = (i * 4 < cnt) ? __ldg(src + i) : zero4();
+    for (int k = tid; k < 512; k += THREADS) {
+      const int c = k / 25, rem = k - c * 25, i = rem / 5, j = rem - i * 5;
+      koff[k] = k < 500 ? c * 144 + i * 12 + j : -1;
+    }
   }
-  __device__ float4 a4(int r, int k) const { return f4(a1(r, k), a1(r, k + 1), a1(r, k + 2), a1(r, k + 3)); }
-  __device__ float4 b4(int f, int k) const {
-    if (f >= 50 || k >= 500) return f4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(p.w + f * 500 + k));  // 500*4 B rows, k % 4 == 0
+  __device__ float g(int k) const {
+    const int o = koff[k];
+    return o >= 0 ? img[rowoff + o] : 0.f;
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int lane) const {
+  __device__ float4 a(int, int k) const { return f4(g(k), g(k + 1), g(k + 2), g(k + 3)); }
+  __device__ const float* b_src(int f, int k, bool& v) const {
+    v = f < 50 && k < 500;
+    return v ? p.w + f * 500 + k : p.w;
+  }
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int n = n0 + (row >> 6), pos = row & 63, ho = pos >> 3, wo = pos & 7;
     const int off = (ho & 1) * 2 + (wo & 1);
 #pragma unroll
@@ -249,12 +409,11 @@ struct Conv2Fwd {
       }
     }
   }
-  __device__ void finish(int) const {}
 };
 
 // ------------------------------------------------------ ip fwd + bias + relu
-// rows n, cols o (BN 64 per CTA column tile), K = 800.
-struct IpFwd {
+// y[n,o] = relu(sum_k x[n,k] W[o,k] + b[o]); rows n, cols o (BN 16), K = 800.
+struct IpFwd : OpBase {
   struct Params {
     const float* x;
     const float* w;
@@ -262,45 +421,47 @@ struct IpFwd {
     float* y;
     int M, K, Nout, relu;
   };
-  static constexpr int BN = 64, TMEM_COLS = 64;
+  static constexpr int BN = 16, TMEM_COLS = 32, STAGES = 4;
+  static constexpr int A_MODE = COPY16, B_MODE = COPY16;
+  static constexpr int STAGE_BYTES = 0;
   const Params& p;
   int m0, o0;
-  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * BM), o0(blockIdx.x * BN) {}
+  __device__ IpFwd(const Params& q, uint8_t*, uint8_t*) : p(q), m0(blockIdx.y * BM), o0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
-  __device__ float4 a4(int r, int k) const {
+  __device__ const float* a_src(int r, int k, bool& v) const {
     const int m = m0 + r;
-    if (m >= p.M || k >= p.K) return f4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(p.x + (size_t)m * p.K + k));
+    v = m < p.M && k < p.K;
+    return v ? p.x + (size_t)m * p.K + k : p.x;
   }
-  __device__ float4 b4(int c, int k) const {
+  __device__ const float* b_src(int c, int k, bool& v) const {
     const int o = o0 + c;
-    if (o >= p.Nout || k >= p.K) return f4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(p.w + (size_t)o * p.K + k));
+    v = o < p.Nout && k < p.K;
+    return v ? p.w + (size_t)o * p.K + k : p.w;
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int) const {
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int m = m0 + row;
     if (m >= p.M) return;
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {
       const int o = o0 + c0 + j;
       if (o >= p.Nout) break;
-      float4 r;
-      r.x = v[j] + __ldg(p.b + o);
-      r.y = v[j + 1] + __ldg(p.b + o + 1);
-      r.z = v[j + 2] + __ldg(p.b + o + 2);
-      r.w = v[j + 3] + __ldg(p.b + o + 3);
+      float4 r = f4(v[j] + __ldg(p.b + o), v[j + 1] + __ldg(p.b + o + 1), v[j + 2] + __ldg(p.b + o + 2),
+                    v[j + 3] + __ldg(p.b + o + 3));
       if (p.relu) {
         r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
       }
       *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
     }
   }
-  __device__ void finish(int) const {}
 };
 
 // --------------------------------------------- ip weight gradient (+ bias)
-// dW[o,k] = sum_n dy[n,o] x[n,k]: rows o, cols k (BN 160), K = n (batch).
-struct IpWgrad {
+// dW[o,k] = sum_n dy[n,o] x[n,k]: rows o, cols k (BN 32), K = n (batch).
+// Both operands are transposed in global memory: 4-byte cp.async per element
+// (a warp covers 32 consecutive rows: coalesced).  db[o] = sum_n dy[n,o]
+// (fp32, unrounded) from the raw A values in column tile 0; thread tid always
+// owns row o0 + (tid & 127), K sub-chunks tid >> 7 and 2 + (tid >> 7).
+struct IpWgrad : OpBase {
   struct Params {
     const float* dy;
     const float* x;
@@ -308,26 +469,28 @@ struct IpWgrad {
     float* db;
     int M, K, Nout;
   };
-  static constexpr int BN = 160, TMEM_COLS = 256;
+  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 4;
+  static constexpr int A_MODE = COPY4, B_MODE = COPY4;
+  static constexpr int STAGE_BYTES = THREADS * 4;
   const Params& p;
+  float* red;
   int o0, k0;
-  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
+  float bacc;
+  __device__ IpWgrad(const Params& q, uint8_t* st, uint8_t*)
+      : p(q), red((float*)st), o0(blockIdx.y * BM), k0(blockIdx.x * BN), bacc(0.f) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
-  __device__ float4 a4(int r, int n) const {
+  __device__ const float* a_src4(int r, int n, int t, bool& v) const {
     const int o = o0 + r;
-    float v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = (o < p.Nout && n + t < p.M) ? ld(p.dy + (size_t)(n + t) * p.Nout + o) : 0.f;
-    return f4(v[0], v[1], v[2], v[3]);
+    v = o < p.Nout && n + t < p.M;
+    return v ? p.dy + (size_t)(n + t) * p.Nout + o : p.dy;
   }
-  __device__ float4 b4(int c, int n) const {
+  __device__ const float* b_src4(int c, int n, int t, bool& v) const {
     const int k = k0 + c;
-    float v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) v[t] = (k < p.K && n + t < p.M) ? ld(p.x + (size_t)(n + t) * p.K + k) : 0.f;
-    return f4(v[0], v[1], v[2], v[3]);
+    v = k < p.K && n + t < p.M;
+    return v ? p.x + (size_t)(n + t) * p.K + k : p.x;
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int) const {
+  __device__ void a_raw(int, int, float4 v) { bacc += (v.x + v.y) + (v.z + v.w); }
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int o = o0 + row;
     if (o >= p.Nout) return;
 #pragma unroll
@@ -337,44 +500,43 @@ struct IpWgrad {
       *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k) = f4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
   }
-  __device__ void finish(int row) const {  // db[o] = sum_n dy[n,o], fp32, ascending n
-    const int o = o0 + row;
-    if (blockIdx.x != 0 || o >= p.Nout || !p.db) return;
-    float acc = 0.f;
-    for (int n = 0; n < p.M; ++n) acc += ld(p.dy + (size_t)n * p.Nout + o);
-    p.db[o] = acc;
+  __device__ void finish(int tid) {
+    red[tid] = bacc;
+    __syncthreads();
+    if (blockIdx.x == 0 && p.db && tid < 128 && o0 + tid < p.Nout) p.db[o0 + tid] = red[tid] + red[tid + 128];
   }
 };
 
 // ------------------------------- ip1 data gradient + pool2 backward (LeNet)
-// dp2[n,k] = sum_o dy[n,o] W1[o,k]; rows n, cols k (BN 160 = 10 filters x 16),
-// K = o (500).  Epilogue scatters each dp2 value to its pool2 origin in the
-// dense conv2 gradient G2[n,f,8,8] (zeros elsewhere).
-struct IpDgradUnpool {
+// dp2[n,k] = sum_o dy[n,o] W1[o,k]; rows n, cols k (BN 32 = 2 filters x 16),
+// K = o (500).  B(k, o) = W1[o][k] is read transposed (4-byte cp.async).
+// Epilogue scatters each dp2 value to its pool2 origin in the dense conv2
+// gradient G2[n,f,8,8] (zeros elsewhere).
+struct IpDgradUnpool : OpBase {
   struct Params {
-    const float* dy;   // [N,500]
-    const float* w;    // [500,800]
-    const uint8_t* m2; // [N,800]
-    float* g2;         // [N,50,8,8]
+    const float* dy;    // [N,500]
+    const float* w;     // [500,800]
+    const uint8_t* m2;  // [N,800]
+    float* g2;          // [N,50,8,8]
     int N;
   };
-  static constexpr int BN = 160, TMEM_COLS = 256;
+  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 4;
+  static constexpr int A_MODE = COPY16, B_MODE = COPY4;
+  static constexpr int STAGE_BYTES = 0;
   const Params& p;
   int m0, k0;
-  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
+  __device__ IpDgradUnpool(const Params& q, uint8_t*, uint8_t*) : p(q), m0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
-  __device__ float4 a4(int r, int o) const {
+  __device__ const float* a_src(int r, int o, bool& v) const {
     const int n = m0 + r;
-    if (n >= p.N || o >= 500) return f4(0.f, 0.f, 0.f, 0.f);
-    return __ldg(reinterpret_cast<const float4*>(p.dy + (size_t)n * 500 + o));
+    v = n < p.N && o < 500;
+    return v ? p.dy + (size_t)n * 500 + o : p.dy;
   }
-  __device__ float4 b4(int c, int o) const {
-    const int k = k0 + c;
-    if (o >= 500) return f4(0.f, 0.f, 0.f, 0.f);
-    return f4(ld(p.w + (size_t)o * 800 + k), ld(p.w + (size_t)(o + 1) * 800 + k), ld(p.w + (size_t)(o + 2) * 800 + k),
-              ld(p.w + (size_t)(o + 3) * 800 + k));
+  __device__ const float* b_src4(int c, int o, int t, bool& v) const {
+    v = o + t < 500;
+    return v ? p.w + (size_t)(o + t) * 800 + k0 + c : p.w;
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int) const {
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int n = m0 + row;
     if (n >= p.N) return;
     const int f = (k0 + c0) >> 4;  // the 16 columns are filter f's 4x4 pooled outputs
@@ -396,94 +558,126 @@ struct IpDgradUnpool {
       *reinterpret_cast<float4*>(g + h * 8 + 4) = f4(o8[4], o8[5], o8[6], o8[7]);
     }
   }
-  __device__ void finish(int) const {}
 };
 
 // ------------------------------------------------- conv2 data gradient
-// dp1[n,c,h,w] = sum_{f,i,j} W2[f,c,i,j] G2[n,f,h-i,w-j] (col2im of W^T G,
-// gather form).  rows r = n*144 + h*12 + w, cols c (20 of 32),
-// K = (f,i,j) 1250 (+30 pad).
-struct Conv2Dgrad {
+// dp1 = col2im(W2^T G2), computed as the GEMM
+//   C[(c,i,j), (n,p)] = sum_f W2[f,c,i,j] G2[n,f,p]
+// with rows = 5 input channels x 25 taps (+3 zero rows) per M tile (4 tiles),
+// cols = 2 images x 64 positions (N = 128), K = f (50 of 64), followed by the
+// col2im gather dp1[n,c,h,w] = sum_{i,j} C[(c,i,j), (n, h-i, w-j)] done from
+// shared memory (C staged over the drained operand ring).  A = W2^T packed
+// TF32 once per backward (pack_w2t); B(p, f) = G2[n,f,p] (4-byte cp.async).
+struct Conv2Dgrad : OpBase {
   struct Params {
     const float* g2;
-    const float* w;
+    const float* w2t;  // [4][128][64] TF32, zero padded
     float* dp1;
     int N;
   };
-  static constexpr int BN = 32, TMEM_COLS = 32;
+  static constexpr int BN = 128, TMEM_COLS = 128, STAGES = 2;
+  static constexpr int A_MODE = COPY16_PRE, B_MODE = COPY4;
+  static constexpr int STAGE_BYTES = 0;
   const Params& p;
-  int r0;
-  __device__ Conv2Dgrad(const Params& q) : p(q), r0(blockIdx.x * BM) {}
-  __device__ int num_k_chunks() const { return 40; }
-  __device__ float a1(int n, int h, int w, int k) const {
-    if (k >= 1250) return 0.f;
-    const int f = k / 25, rem = k - f * 25, i = rem / 5, j = rem - i * 5;
-    const int ho = h - i, wo = w - j;
-    if ((unsigned)ho >= 8u || (unsigned)wo >= 8u) return 0.f;
-    return ld(p.g2 + (size_t)n * 3200 + f * 64 + ho * 8 + wo);
+  float* cs;  // [128 rows][128 cols], over the ring after the MMAs
+  int m, n0;
+  __device__ Conv2Dgrad(const Params& q, uint8_t*, uint8_t* ring)
+      : p(q), cs((float*)ring), m(blockIdx.x), n0(blockIdx.y * 2) {}
+  __device__ int num_k_chunks() const { return 2; }
+  __device__ const float* a_src(int r, int f, bool& v) const {
+    v = true;
+    return p.w2t + ((size_t)m * 128 + r) * 64 + f;
   }
-  __device__ float4 a4(int r, int k) const {
-    const int gr = r0 + r;
-    if (gr >= p.N * 144) return f4(0.f, 0.f, 0.f, 0.f);
-    const int n = gr / 144, hw = gr - n * 144, h = hw / 12, w = hw - h * 12;
-    return f4(a1(n, h, w, k), a1(n, h, w, k + 1), a1(n, h, w, k + 2), a1(n, h, w, k + 3));
+  __device__ const float* b_src4(int c, int f, int t, bool& v) const {
+    const int n = n0 + (c >> 6);
+    v = n < p.N && f + t < 50;
+    return v ? p.g2 + (size_t)n * 3200 + (f + t) * 64 + (c & 63) : p.g2;
   }
-  __device__ float b1(int c, int k) const {
-    if (k >= 1250) return 0.f;
-    const int f = k / 25, rem = k - f * 25;
-    return ld(p.w + f * 500 + c * 25 + rem);
-  }
-  __device__ float4 b4(int c, int k) const {
-    if (c >= 20) return f4(0.f, 0.f, 0.f, 0.f);
-    return f4(b1(c, k), b1(c, k + 1), b1(c, k + 2), b1(c, k + 3));
-  }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int) const {
-    const int gr = r0 + row;
-    if (gr >= p.N * 144) return;
-    const int n = gr / 144, hw = gr - n * 144;
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
+    float4* dst = reinterpret_cast<float4*>(cs + row * 128 + c0);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int c = c0 + j;
-      if (c >= 20) break;
-      p.dp1[(size_t)n * 2880 + c * 144 + hw] = v[j];
+    for (int j = 0; j < 4; ++j) dst[j] = f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+  __device__ void finish(int tid) {
+    // 2 images x 5 channels x 144 outputs
+    for (int o = tid; o < 2 * 5 * 144; o += THREADS) {
+      const int img = o / 720, rem = o - img * 720, cl = rem / 144, hw = rem - cl * 144;
+      const int n = n0 + img;
+      if (n >= p.N) continue;
+      const int h = hw / 12, w = hw - h * 12;
+      const float* base = cs + (cl * 25) * 128 + img * 64;
+      float acc = 0.f;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const int ho = h - i;
+        if ((unsigned)ho >= 8u) continue;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const int wo = w - j;
+          if ((unsigned)wo >= 8u) continue;
+          acc += base[(i * 5 + j) * 128 + ho * 8 + wo];
+        }
+      }
+      p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
     }
   }
-  __device__ void finish(int) const {}
 };
 
 // ------------------------------------------------ conv2 weight gradient
 // dW2[f,(c,i,j)] = sum_{n,p} G2[n,f,p] p1[n,c,ho+i,wo+j]; rows (c,i,j) 500 of
-// 512 (4 tiles), cols f (50 of 64), K = (n in split, p).  Writes split
-// partials [split][f*500 + k]; bias partial db2[f] = sum G2 (row tile 0).
-struct Conv2Wgrad {
+// 512 (4 tiles), cols f (50 of 64), K = (n in this split, p): 2 chunks per
+// image.  Images are cp.async'ed into a 2-slot smem ring one image ahead;
+// A gathered from the staged image, B = G2 rows (16-byte cp.async).  Writes
+// split partials [split][f*500 + k] and the bias partial db2[f] = sum G2
+// (fp32, from the raw B values; thread tid always owns B row f = tid % 64).
+struct Conv2Wgrad : OpBase {
   struct Params {
     const float* g2;
     const float* p1;
     float* part;
     int N, splits, pstride;
   };
-  static constexpr int BN = 64, TMEM_COLS = 64;
+  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
+  static constexpr int A_MODE = GATHER, B_MODE = COPY16;
+  static constexpr bool SYNC_AFTER_WAIT = true;
+  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + THREADS * 4;
   const Params& p;
-  int kw0, n0, n1;
-  __device__ Conv2Wgrad(const Params& q) : p(q), kw0(blockIdx.x * BM) {
+  float* img;
+  float* red;
+  int kw0, n0, n1, rowoff;
+  bool rvalid;
+  float bacc;
+  __device__ Conv2Wgrad(const Params& q, uint8_t* st, uint8_t*)
+      : p(q), img((float*)st), red((float*)(st + 2 * 2880 * 4)) {
+    kw0 = blockIdx.x * BM;
     n0 = (int)((long long)q.N * blockIdx.y / q.splits);
     n1 = (int)((long long)q.N * (blockIdx.y + 1) / q.splits);
-  }
-  __device__ int num_k_chunks() const { return (n1 - n0) * 2; }  // 64 positions = 2 chunks per image
-  __device__ float4 a4(int r, int kk) const {
-    const int kw = kw0 + r;
-    if (kw >= 500) return f4(0.f, 0.f, 0.f, 0.f);
-    const int n = n0 + (kk >> 6), pos = kk & 63, ho = pos >> 3, wo = pos & 7;
+    const int kw = kw0 + (threadIdx.x & 127);
+    rvalid = kw < 500;
     const int c = kw / 25, rem = kw - c * 25, i = rem / 5, j = rem - i * 5;
-    const float* src = p.p1 + (size_t)n * 2880 + c * 144 + (ho + i) * 12 + wo + j;
-    return f4(ld(src), ld(src + 1), ld(src + 2), ld(src + 3));
+    rowoff = c * 144 + i * 12 + j;
+    bacc = 0.f;
   }
-  __device__ float4 b4(int f, int kk) const {
-    if (f >= 50) return f4(0.f, 0.f, 0.f, 0.f);
-    const int n = n0 + (kk >> 6), pos = kk & 63;
-    return __ldg(reinterpret_cast<const float4*>(p.g2 + (size_t)n * 3200 + f * 64 + pos));
+  __device__ int num_k_chunks() const { return (n1 - n0) * 2; }
+  __device__ void issue_extra(int c, int tid) {
+    if (c & 1) return;
+    const int im = c >> 1;
+    const float* src = p.p1 + (size_t)(n0 + im) * 2880;
+    const uint32_t dst = smem_u32(img + (im & 1) * 2880);
+    for (int i = tid; i < 720; i += THREADS) cp16(dst + i * 16, src + i * 4, true);
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16], int) const {
+  __device__ float4 a(int, int k) const {
+    if (!rvalid) return zero4();
+    const int im = k >> 6, pos = k & 63, ho = pos >> 3, wo = pos & 7;
+    const float* s = img + (im & 1) * 2880 + rowoff + ho * 12 + wo;
+    return f4(s[0], s[1], s[2], s[3]);
+  }
+  __device__ const float* b_src(int f, int k, bool& v) const {
+    v = f < 50;
+    return v ? p.g2 + (size_t)(n0 + (k >> 6)) * 3200 + f * 64 + (k & 63) : p.g2;
+  }
+  __device__ void b_raw(int, int, float4 v) { bacc += (v.x + v.y) + (v.z + v.w); }
+  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int kw = kw0 + row;
     if (kw >= 500) return;
     float* dst = p.part + (size_t)blockIdx.y * p.pstride;
@@ -494,21 +688,38 @@ struct Conv2Wgrad {
       dst[f * 500 + kw] = v[j];
     }
   }
-  __device__ void finish(int row) const {  // bias partial: fp32, ascending (n, p)
-    if (blockIdx.x != 0 || row >= 50) return;
-    float acc = 0.f;
-    for (int n = n0; n < n1; ++n) {
-      const float* g = p.g2 + (size_t)n * 3200 + row * 64;
-      for (int q = 0; q < 64; ++q) acc += ld(g + q);
-    }
-    p.part[(size_t)blockIdx.y * p.pstride + 25000 + row] = acc;
+  __device__ void finish(int tid) {
+    red[tid] = bacc;
+    __syncthreads();
+    if (blockIdx.x == 0 && tid < 50)
+      p.part[(size_t)blockIdx.y * p.pstride + 25000 + tid] =
+          (red[tid] + red[tid + 64]) + (red[tid + 128] + red[tid + 192]);
   }
 };
+
+// --------------------------------------------------------- weight repack
+// W2 [f][c][i][j] -> W2t [m (4)][r (128)][f (64)], r = (c - 5m)*25 + i*5 + j,
+// TF32-rounded, zero padded (conv2 data-gradient A operand; once per backward).
+struct PackW2tP {
+  const float* w2;
+  float* w2t;
+};
+__global__ void pack_w2t(const __grid_constant__ PackW2tP p) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 4 * 128 * 64) return;
+  const int f = idx & 63, r = (idx >> 6) & 127, m = idx >> 13;
+  float v = 0.f;
+  if (f < 50 && r < 125) {
+    const int c = 5 * m + r / 25, tap = r % 25;
+    v = p.w2[f * 500 + c * 25 + tap];
+  }
+  p.w2t[idx] = tf32f(v);
+}
 
 // ------------------------------------------------------------ host side
 template <class Op>
 static constexpr size_t smem_bytes() {
-  return (size_t)STAGES * (BM * BK * 4 + Op::BN * BK * 4);
+  return (size_t)Op::STAGES * (BM * BK * 4 + Op::BN * BK * 4) + Op::STAGE_BYTES;
 }
 
 template <class Op>
@@ -561,11 +772,17 @@ Launch ip_dgrad_unpool_launch(const float* dy, const float* w, const uint8_t* m2
   return l;
 }
 
-Launch conv2_dgrad_launch(const float* g2, const float* w, float* dp1, int N, int) {
+Launch pack_w2d_launch(const float* w2, float* w2t) {
   Launch l;
-  Conv2Dgrad::Params p{g2, w, dp1, N};
-  l.set((const void*)tc_gemm<Conv2Dgrad>, dim3(cdiv((long long)N * 144, BM)), dim3(THREADS),
-        smem_bytes<Conv2Dgrad>(), p);
+  PackW2tP p{w2, w2t};
+  l.set((const void*)pack_w2t, dim3(cdiv(4 * 128 * 64, 256)), dim3(256), 0, p);
+  return l;
+}
+
+Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int) {
+  Launch l;
+  Conv2Dgrad::Params p{g2, w2t, dp1, N};
+  l.set((const void*)tc_gemm<Conv2Dgrad>, dim3(4, cdiv(N, 2)), dim3(THREADS), smem_bytes<Conv2Dgrad>(), p);
   return l;
 }
 

@@ -17,7 +17,8 @@ Launch ip_fwd_launch(const float* x, const float* w, const float* b, float* y, i
                      int sms);
 Launch ip_wgrad_launch(const float* dy, const float* x, float* dw, float* db, int M, int K, int Nout, int sms);
 Launch ip_dgrad_unpool_launch(const float* dy, const float* w, const uint8_t* m2, float* g2, int N, int sms);
-Launch conv2_dgrad_launch(const float* g2, const float* w, float* dp1, int N, int sms);
+Launch pack_w2d_launch(const float* w2, float* w2d);  // W2 -> [c][(f,i,j)] TF32
+Launch conv2_dgrad_launch(const float* g2, const float* w2d, float* dp1, int N, int sms);
 Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N, int sms);
 }  // namespace tc
 }  // namespace pn
