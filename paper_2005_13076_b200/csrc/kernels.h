@@ -18,6 +18,7 @@ __global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p);
 __global__ void loss_reduce(const __grid_constant__ LossReduceP p);
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p);
 __global__ void mask_convert(const __grid_constant__ MaskExpandP p);
+__global__ void tf32_copy(const __grid_constant__ Tf32CopyP p);
 
 // fused LeNet kernels (kernels_lenet.cu)
 __global__ void lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p);

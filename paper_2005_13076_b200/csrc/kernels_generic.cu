@@ -145,7 +145,7 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   float acc = 0.f;
-  for (int s = 0; s < p.splits; ++s) acc += p.part[(long long)s * p.n + i];
+  for (int s = 0; s < p.splits; ++s) acc += p.part[(long long)s * p.stride + i];
   p.out[i] = acc;
 }
 
@@ -406,4 +406,18 @@ __global__ void mask_convert(const __grid_constant__ MaskExpandP p) {
   }
 }
 
+}  // namespace pn
+
+namespace pn {
+// TF32-rounded (nearest, ties away) copies of a blob for the tensor-core
+// plan's operand buffers; used when a caller overwrites a blob (net_put_blob)
+// so the internal operand copies stay consistent with it.
+__global__ void tf32_copy(const __grid_constant__ Tf32CopyP p) {
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long long)p.R * p.C) return;
+  const int r = (int)(idx / p.C), c = (int)(idx % p.C);
+  const float v = __uint_as_float((__float_as_uint(p.src[idx]) + 0x1000u) & 0xFFFFE000u);
+  if (p.dst) p.dst[idx] = v;
+  if (p.dstT) p.dstT[(long long)c * p.ldt + r] = v;
+}
 }  // namespace pn

@@ -66,7 +66,8 @@ __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__
       if (c10 > best) { best = c10; off = 2; }
       if (c11 > best) { best = c11; off = 3; }
       const long long o = ((long long)n * 20 + f) * 144 + q;
-      p.p1[o] = best;
+      // TF32 plan: round to nearest, ties away (the conv2 operand rounding)
+      p.p1[o] = p.round_tf32 ? __uint_as_float((__float_as_uint(best) + 0x1000u) & 0xFFFFE000u) : best;
       p.m1[o] = (uint8_t)off;
     }
   }
@@ -226,7 +227,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     w2[o] = valid ? __ldg(p.w + o * 500 + k) : 0.f;
     acc[o] = 0.f;
   }
-  float bacc = 0.f;
+  float bacc = 0.f, b1acc = 0.f;
   for (int mb = m0; mb < m1; mb += 64) {
     const int cnt = min(64, m1 - mb);
     __syncthreads();
@@ -243,7 +244,14 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
           g = fmaf(d, w2[o], g);
           acc[o] = fmaf(d, a, acc[o]);
         }
-        p.da1[(long long)m * 500 + k] = a > 0.f ? g : 0.f;
+        const float da = a > 0.f ? g : 0.f;
+        p.da1[(long long)m * 500 + k] = da;
+        if (p.da1r) {
+          const float r = __uint_as_float((__float_as_uint(da) + 0x1000u) & 0xFFFFE000u);  // TF32 (RNA)
+          p.da1r[(long long)m * 500 + k] = r;
+          p.da1rT[(long long)k * p.npad + m] = r;
+          b1acc += da;
+        }
       }
       if (blockIdx.x == 0 && threadIdx.x < 10) bacc += dzs[mm][threadIdx.x];
     }
@@ -251,6 +259,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
   if (valid) {
 #pragma unroll
     for (int o = 0; o < 10; ++o) p.part_w[(long long)s * p.pstride + o * 500 + k] = acc[o];
+    if (p.part_b1) p.part_b1[(long long)s * 500 + k] = b1acc;  // db1 = sum_m da1[m,k]
   }
   if (blockIdx.x == 0 && threadIdx.x < 10) p.part_b[(long long)s * p.pstride + threadIdx.x] = bacc;
 }

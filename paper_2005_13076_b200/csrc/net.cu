@@ -158,7 +158,14 @@ struct pn_net {
   float* partials = nullptr;
   int64_t npartials = 0;
   float* row_loss = nullptr;
-  float* w2d = nullptr;  // TF32 repack of conv2 weights for the data gradient
+  tc::PackP pack{};      // TF32 weight copies for the tensor-core plan
+  // TF32 plan operand copies (see tc.cu): transposes padded to npad columns
+  int npad = 0;
+  float* p2T = nullptr;       // [800][npad]
+  float* da1r = nullptr;      // [N][500]
+  float* da1rT = nullptr;     // [500][npad]
+  float* part_b1 = nullptr;   // [splits][500]  ip1 bias-gradient partials
+  float* part_db2 = nullptr;  // [rowtiles][50] conv2 bias-gradient partials
   unsigned* err = nullptr;
   std::vector<void*> allocs;
 
@@ -408,7 +415,18 @@ static pn_status allocate(pn_net* net) {
   net->npartials = poff;
   TRY(net->alloc(&net->partials, poff > 0 ? poff : 1));
   TRY(net->alloc(&net->row_loss, net->batch));
-  if (net->tf32) TRY(net->alloc(&net->w2d, 32 * 1280));
+  if (net->tf32) {
+    TRY(net->alloc(&net->pack.w1f, tc::kW1fFloats));
+    TRY(net->alloc(&net->pack.w1t, tc::kW1tFloats));
+    TRY(net->alloc(&net->pack.w2f, tc::kW2fFloats));
+    TRY(net->alloc(&net->pack.w2t, tc::kW2tFloats));
+    net->npad = (net->batch + 3) & ~3;  // TMA row pitch must be a multiple of 16 B
+    TRY(net->alloc(&net->p2T, (size_t)800 * net->npad));
+    TRY(net->alloc(&net->da1r, (size_t)net->batch * 500));
+    TRY(net->alloc(&net->da1rT, (size_t)500 * net->npad));
+    TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
+    TRY(net->alloc(&net->part_db2, (size_t)((net->batch + 127) / 128) * 50));
+  }
   TRY(net->alloc(&net->err, 1));
   // activation blobs (the fused plan never stores conv1's output or its
   // gradient, nor conv2's output; conv2's gradient is the dense unpooled G2)
@@ -460,11 +478,21 @@ static void add(std::vector<Stage>& v, const std::string& name, const Launch& L,
   v.push_back(s);
 }
 
-static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L) {
-  ReduceP r{net->partials + L.part_off, net->grads + L.off, (int)(L.wcount + L.bcount), L.splits};
+// grads[w (and b)] = sum over the layer's split partials (fixed order)
+static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L, bool with_bias = true) {
+  const int stride = (int)(L.wcount + L.bcount);
+  ReduceP r{net->partials + L.part_off, net->grads + L.off, with_bias ? stride : (int)L.wcount, L.splits, stride};
   Launch l;
   l.set((const void*)reduce_partials, dim3(cdiv(r.n, 256)), dim3(256), 0, r);
   add(v, L.name + ".wgrad_reduce", l);
+}
+
+static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const float* part, float* out, int n,
+                           int splits) {
+  ReduceP r{part, out, n, splits, n};
+  Launch l;
+  l.set((const void*)reduce_partials, dim3(cdiv(n, 256)), dim3(256), 0, r);
+  add(v, name, l);
 }
 
 static void add_loss(pn_net* net, std::vector<Stage>& fwd) {
@@ -583,15 +611,23 @@ static void build_fused_lenet(pn_net* net) {
   float* P = net->params;
   float* G = net->grads;
   // ---- forward
+  if (net->tf32) {  // TF32 weight copies for this step's contractions
+    net->pack.w1 = P + i1.off;
+    net->pack.w2 = P + c2.off;
+    add(fwd, "wpack[tc]", tc::pack_weights_launch(net->pack));
+    add(fwd, "w1t[tc]", tc::transpose_w1_launch(net->pack));
+  }
   {
-    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N};
+    // TF32 plan: pool1 is consumed only by conv2's contractions, so it is
+    // stored TF32-rounded; the mask is taken before rounding
+    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0};
     Launch l;
     l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(288), 0, p);
     add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
   }
   if (net->tf32) {
-    add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(P + c2.off, P + c2.off + 25000, p1.data, p2.data, p2.m8, N,
-                                                        net->tc_sms));
+    add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(net->pack.w2f, P + c2.off + 25000, p1.data, p2.data, net->p2T,
+                                                        p2.m8, N, net->npad));
   } else {
     Conv2Pool2P p{p1.data, P + c2.off, P + c2.off + 25000, p2.data, p2.m8, N};
     Launch l;
@@ -600,8 +636,7 @@ static void build_fused_lenet(pn_net* net) {
     add(fwd, "conv2+pool2", l);
   }
   if (net->tf32) {
-    add(fwd, "ip1+relu[tc]", tc::ip_fwd_launch(p2.data, P + i1.off, P + i1.off + i1.wcount, a1.data, N, 800, 500,
-                                                true, net->tc_sms));
+    add(fwd, "ip1+relu[tc]", tc::ip1_fwd_launch(p2.data, net->pack.w1f, P + i1.off + i1.wcount, a1.data, N));
   } else {
     GemmP g{p2.data, P + i1.off, a1.data, P + i1.off + i1.wcount, N, 500, 800, 800, 1, 1, 800, 1};
     Launch l;
@@ -620,16 +655,19 @@ static void build_fused_lenet(pn_net* net) {
   // ---- backward (reverse order)
   {
     Ip2BwdP p{lg.diff, a1.data, P + i2.off, a1.diff, net->partials + i2.part_off,
-              net->partials + i2.part_off + 5000, N, i2.splits, 5010};
+              net->partials + i2.part_off + 5000, N, i2.splits, 5010,
+              net->da1r, net->da1rT, net->part_b1, net->npad};
     Launch l;
     l.set((const void*)lenet_ip2_bwd, dim3(4, i2.splits), dim3(128), 0, p);
     add(bwd, "ip2.bwd+relu1.bwd", l);
     add_reduce(net, bwd, i2);
   }
   if (net->tf32) {
-    add(bwd, "ip1.wgrad[tc]", tc::ip_wgrad_launch(a1.diff, p2.data, G + i1.off, G + i1.off + i1.wcount, N, 800, 500,
-                                                  net->tc_sms));
-    add(bwd, "ip1.dgrad+unpool2[tc]", tc::ip_dgrad_unpool_launch(a1.diff, P + i1.off, p2.m8, cv2.diff, N, net->tc_sms));
+    add_reduce_raw(bwd, "ip1.bgrad_reduce", net->part_b1, G + i1.off + i1.wcount, 500, i2.splits);
+    add(bwd, "ip1.wgrad[tc]", tc::ip1_wgrad_launch(net->da1rT, net->p2T, G + i1.off, N, net->npad));
+    add(bwd, "ip1.dgrad+unpool2[tc]",
+        tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
+    add_reduce_raw(bwd, "conv2.bgrad_reduce", net->part_db2, G + c2.off + 25000, 50, (N + 127) / 128);
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
     Launch l;
@@ -649,11 +687,9 @@ static void build_fused_lenet(pn_net* net) {
     add(bwd, "pool2.bwd", l4);
   }
   if (net->tf32) {
-    add(bwd, "conv2.wpack[tc]", tc::pack_w2d_launch(P + c2.off, net->w2d));
-    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->w2d, p1.diff, N, net->tc_sms));
-    add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits,
-                                                       N, net->tc_sms));
-    add_reduce(net, bwd, c2);
+    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->pack.w2t, p1.diff, N));
+    add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits, N));
+    add_reduce(net, bwd, c2, /*with_bias=*/false);  // conv2.b came from the ip1 dgrad epilogue
   } else {
     ConvBwdDataP q{cv2.diff, P + c2.off, p1.diff, N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8};
     Launch l;
@@ -855,6 +891,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }
   TRY(build_plan(net.get()));
+  if (net->tf32 && !tc::tensor_maps_ok()) return fail(PN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   CU(cudaDeviceSynchronize());
   *out = net.release();
   return PN_OK;
@@ -980,6 +1017,19 @@ static pn_status blob_io(pn_net* net, const char* name, int which, void* buf, in
   if (put) {
     CU(cudaMemcpyAsync(dev, buf, bytes, kind, st));
     if (tmp) TRY(mask_io(net, b, tmp, false, st));
+    if (net->tf32 && net->fused) {
+      // keep the tensor-core operand copies of an overwritten blob in sync
+      Tf32CopyP c{nullptr, nullptr, nullptr, 0, 0, 0};
+      if (b->name == net->layers[3].top && which == PN_DATA)
+        c = Tf32CopyP{b->data, nullptr, net->p2T, net->batch, 800, net->npad};
+      else if (b->name == net->layers[4].top && which == PN_DIFF)
+        c = Tf32CopyP{b->diff, net->da1r, net->da1rT, net->batch, 500, net->npad};
+      if (c.src) {
+        Launch l;
+        l.set((const void*)tf32_copy, dim3(cdiv((long long)c.R * c.C, 256)), dim3(256), 0, c);
+        CU(l.launch(st));
+      }
+    }
   } else {
     if (tmp) TRY(mask_io(net, b, tmp, true, st));
     CU(cudaMemcpyAsync(buf, dev, bytes, kind, st));

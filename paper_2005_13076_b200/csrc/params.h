@@ -28,10 +28,10 @@ struct ConvBwdWeightP {  // split-N partials of dW = sum dy col^T and db
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo, splits;
   int pstride;    // floats between consecutive splits of part_w / part_b
 };
-struct ReduceP {  // out[i] = sum_s part[s*n + i] (fixed order s = 0..)
+struct ReduceP {  // out[i] = sum_s part[s*stride + i], i < n (fixed order s = 0..)
   const float* part;
   float* out;
-  int n, splits;
+  int n, splits, stride;
 };
 struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   const float* x;
@@ -91,6 +91,12 @@ struct SgdP {  // S:536-544 Caffe SGD, fp32, no FMA
   long long n;
   float lr, mom, decay, gscale;
 };
+struct Tf32CopyP {  // src [R][C] -> TF32-rounded copies: dst [R][C] and/or dstT [C][ldt]
+  const float* src;
+  float* dst;
+  float* dstT;
+  int R, C, ldt;
+};
 struct MaskExpandP {  // uint8 window offset <-> int32 plane-local (ABI view)
   uint8_t* m8;
   int32_t* m32;
@@ -107,6 +113,7 @@ struct Conv1Pool1P {  // x[N,1,28,28] -> p1[N,20,12,12], m1 (uint8 offsets)
   float* p1;
   uint8_t* m1;
   int N;
+  int round_tf32;  // store p1 rounded to TF32 (RNA) for the tensor-core plan
 };
 struct Conv2Pool2P {  // p1[N,20,12,12] -> p2[N,50,4,4], m2
   const float* p1;
@@ -138,6 +145,12 @@ struct Ip2BwdP {  // dz[N,10], a1 -> da1 = relu'(a1) * dz W2 ; dW2 / db2 partial
   float* part_w;  // [splits][10*500]
   float* part_b;  // [splits][10]
   int N, splits, pstride;
+  // TF32 plan only (null otherwise): TF32-rounded copies of da1 for the ip1
+  // contractions ([N][500] and transposed [500][npad]) and db1 partials
+  float* da1r;
+  float* da1rT;
+  float* part_b1;  // [splits][500]
+  int npad;
 };
 struct Unpool2P {  // dp2 [N,800] + m2 -> G2 [N,50,8,8] dense
   const float* dp2;

@@ -1,27 +1,31 @@
 // tc.cu -- tcgen05 TF32 implicit-GEMM kernels for the GEMM-shaped LeNet
 // layers.
 //
-// Engine (one CTA = one 128-row output tile, 8 warps, all producers):
-//   * operands are assembled per 32-wide K chunk in a shared-memory ring in
-//     the UMMA canonical K-major no-swizzle layout (core matrix = 8 rows x
-//     4 K (16 B); LBO = 128 B between the K halves of one MMA, SBO = 1024 B
-//     between 8-row groups).  MN-major TF32 descriptors were measured to
-//     produce zeros on this part (tools/umma_probe.cu), so transposed global
-//     operands are gathered into K-major rows as well;
-//   * copy-type operand units move global -> shared with cp.async (16-byte
-//     rows, or 4 x 4-byte scalars for transposed operands), issued
-//     LOOKAHEAD chunks ahead of the chunk being consumed; the issuing thread
-//     later rounds its own units to TF32 in place (cvt.rna: round to
-//     nearest) -- pre-rounded packed weights skip that;
-//     gather-type units (implicit im2col) are built from activations the CTA
-//     staged in shared memory;
+// Engine (one CTA = one 128-row output tile, 8 warps):
+//   * every operand K-chunk (rows x 32 fp32) lives in a shared-memory ring in
+//     the UMMA canonical K-major SWIZZLE_128B layout (row = 128 B, 16-B chunk
+//     index XOR row%8, 8-row atoms of 1024 B; descriptor SBO = 1024 B, K step
+//     of 8 = +32 B).  MN-major TF32 descriptors were measured to produce zeros
+//     on this part (tools/umma_probe.cu), so every operand is K-major;
+//   * dense operands are moved by TMA (cp.async.bulk.tensor 2D/3D with
+//     128B swizzle, one elected thread, mbarrier complete_tx), LOOKAHEAD
+//     chunks ahead of the MMA.  They are already TF32 in global memory:
+//     packed weight copies (pack_weights) and activations stored rounded to
+//     nearest by their producing kernels -- the tensor
+//     core therefore never truncates;
+//   * implicit-im2col operands are gathered by all threads from activations
+//     staged in shared memory with cp.async.bulk, written with the same
+//     swizzle, then fence.proxy.async + __syncthreads;
 //   * one thread issues tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN,
 //     K=8) x 4 per chunk into a TMEM accumulator and tcgen05.commit's the
-//     stage back to the producers through an mbarrier;
+//     stage back (mbarrier);
 //   * the epilogue reads TMEM with tcgen05.ld 32x32b (thread = tile row;
 //     warps 4-7 take the upper half of the columns) and applies the layer's
 //     fused tail.
+#include <cuda.h>
+
 #include <cstdint>
+#include <cstring>
 
 #include "tc.h"
 
@@ -29,26 +33,27 @@ namespace pn {
 namespace tc {
 
 constexpr int BM = 128;  // tile rows = UMMA M
-constexpr int BK = 32;   // K elements per chunk (4 MMAs of K = 8)
+constexpr int BK = 32;   // K elements per chunk (4 MMAs of K = 8) = one 128-B swizzle row
 constexpr int THREADS = 256;
-
-enum Mode { COPY16 = 0, COPY16_PRE = 1, COPY4 = 2, GATHER = 3 };
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_barrier_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -80,9 +85,8 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
 }
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
@@ -96,155 +100,118 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
+// Round to TF32, nearest with ties away from zero (= cvt.rna.tf32.f32 for
+// finite inputs; ptxas expands cvt.rna into a branchy sequence, this is two
+// integer ops).
+__device__ __forceinline__ float tf32f(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
-__device__ __forceinline__ float tf32f(float x) { return __uint_as_float(to_tf32(x)); }
 __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
-  asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "r"(to_tf32(v.x)), "r"(to_tf32(v.y)),
-               "r"(to_tf32(v.z)), "r"(to_tf32(v.w))
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
-__device__ __forceinline__ float4 lds128(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+// explicit shared-space accesses (32-bit addresses; the generic path the
+// compiler falls back to for pointers carried through structs is far slower)
+__device__ __forceinline__ float ldsf(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
   return v;
 }
-__device__ __forceinline__ void cp16(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(valid ? 16 : 0)
+__device__ __forceinline__ int4 lds_i4(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void stsf(uint32_t addr, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
+}
+__device__ __forceinline__ void sts_i32(uint32_t addr, int v) {
+  asm volatile("st.shared.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+// TMA: 2D / 3D tile loads (async proxy, completion on an mbarrier)
+__device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma3d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+// 1D bulk copy global -> shared (bytes % 16 == 0, both 16-B aligned)
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
                : "memory");
 }
-__device__ __forceinline__ void cp4(uint32_t dst, const void* src, bool valid) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src), "r"(valid ? 4 : 0)
-               : "memory");
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-// UMMA shared-memory descriptor, no swizzle, sm_100 version 1.
-__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor: K-major, SWIZZLE_128B, SBO = 1024 B, sm_100 version 1.
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr & 0x3FFFF) >> 4);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8-row atom stride
+  d |= (uint64_t)1 << 46;                  // version
+  d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
   return d;
 }
 // Instruction descriptor: kind::tf32, D = F32, A = B = TF32, both K-major.
 __host__ __device__ constexpr uint32_t make_idesc(int M, int N) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
-// K-major: byte offset of (row r, 16-B K chunk kc) inside a [rows x 32] chunk
-__device__ __forceinline__ uint32_t kmaj_off(int r, int kc) {
-  return (uint32_t)((r >> 3) * 1024 + kc * 128 + (r & 7) * 16);
+// byte offset of (row r, 16-B chunk kc) in a [rows x 32] SWIZZLE_128B chunk
+__device__ __forceinline__ uint32_t sw_off(int r, int kc) {
+  return (uint32_t)(r * 128 + ((kc ^ (r & 7)) << 4));
 }
 __device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // ------------------------------------------------------------------ engine
 // Op interface:
-//   BN, TMEM_COLS, STAGES, A_MODE, B_MODE, STAGE_BYTES, SYNC_AFTER_WAIT
-//   Op(params, staging_smem, ring_smem)        decodes the tile
-//   int num_k_chunks()
-//   void stage(tid)                            one-time staging (engine syncs after)
-//   void issue_extra(chunk, tid)               extra cp.async work for a chunk (may be empty)
-//   COPY16/_PRE: const float* a_src(r, k, &valid)    16-byte source of A(r, k..k+3)
-//   COPY4:       const float* a_src4(r, k, t, &valid) source of A(r, k+t)
-//   GATHER:      float4 a(r, k)                    built from staged smem
-//   (B likewise with b_src / b_src4 / b)
-//   void a_raw(r, k, float4) / b_raw(c, k, float4)   raw copied values (bias sums)
-//   void epilogue(row, c0, v[16])              columns c0..c0+15
-//   void finish(tid)                           after epilogue + __syncthreads
-template <class Op>
-__device__ __forceinline__ void issue_chunk(Op& op, uint32_t As, uint32_t Bs, int k0, int tid) {
-  constexpr int BN = Op::BN;
-  if (Op::A_MODE != GATHER) {
-#pragma unroll
-    for (int q = 0; q < BM * (BK / 4) / THREADS; ++q) {
-      const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
-      const uint32_t dst = As + kmaj_off(r, kc);
-      if (Op::A_MODE == COPY4) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          bool v;
-          const float* s = op.a_src4(r, k0 + kc * 4, t, v);
-          cp4(dst + 4 * t, s, v);
-        }
-      } else {
-        bool v;
-        const float* s = op.a_src(r, k0 + kc * 4, v);
-        cp16(dst, s, v);
-      }
-    }
-  }
-  if (Op::B_MODE != GATHER) {
-    for (int u = tid; u < BN * (BK / 4); u += THREADS) {
-      const int c = u % BN, kc = u / BN;
-      const uint32_t dst = Bs + kmaj_off(c, kc);
-      if (Op::B_MODE == COPY4) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          bool v;
-          const float* s = op.b_src4(c, k0 + kc * 4, t, v);
-          cp4(dst + 4 * t, s, v);
-        }
-      } else {
-        bool v;
-        const float* s = op.b_src(c, k0 + kc * 4, v);
-        cp16(dst, s, v);
-      }
-    }
-  }
-}
-
-template <class Op>
-__device__ __forceinline__ void produce_chunk(Op& op, uint32_t As, uint32_t Bs, int k0, int tid) {
-  constexpr int BN = Op::BN;
-#pragma unroll
-  for (int q = 0; q < BM * (BK / 4) / THREADS; ++q) {
-    const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
-    const uint32_t dst = As + kmaj_off(r, kc);
-    if (Op::A_MODE == GATHER) {
-      sts128(dst, op.a(r, k0 + kc * 4));
-    } else if (Op::A_MODE != COPY16_PRE) {
-      const float4 v = lds128(dst);
-      op.a_raw(r, k0 + kc * 4, v);
-      sts128(dst, v);
-    }
-  }
-  for (int u = tid; u < BN * (BK / 4); u += THREADS) {
-    const int c = u % BN, kc = u / BN;
-    const uint32_t dst = Bs + kmaj_off(c, kc);
-    if (Op::B_MODE == GATHER) {
-      sts128(dst, op.b(c, k0 + kc * 4));
-    } else if (Op::B_MODE != COPY16_PRE) {
-      const float4 v = lds128(dst);
-      op.b_raw(c, k0 + kc * 4, v);
-      sts128(dst, v);
-    }
-  }
-}
-
+//   BN, TMEM_COLS, STAGES, A_TMA, B_TMA (else gathered), STAGE_BYTES
+//   Op(params, staging_smem, ring_smem)   decodes the tile
+//   int  num_k_chunks()
+//   void stage(tid)                       one-time generic staging (engine syncs)
+//   void issue(chunk, As, Bs, bar)        thread 0: TMA / bulk copies for a chunk
+//   uint32_t tx_bytes(chunk)              bytes those copies complete on `bar`
+//   void before_gather(chunk, tid)        all threads, before gathering a chunk
+//   float4 a(r, k) / b(c, k)              gathered (already TF32) values
+//   void epilogue(row, c0, v[16]);  void finish(tid)
 template <class Op>
 __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typename Op::Params prm) {
-  extern __shared__ __align__(1024) uint8_t smem[];
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // 1024-B alignment for the swizzle atoms (dynamic smem base is only 16-B aligned)
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int S = Op::STAGES;
-  constexpr int L = S - 2 > 0 ? S - 2 : 1;  // cp.async lookahead (chunks)
-  __shared__ uint64_t bars[S + 1];
-  __shared__ uint32_t tmem_base;
   constexpr int BN = Op::BN;
   constexpr int A_BYTES = BM * BK * 4;
   constexpr int B_BYTES = BN * BK * 4;
   constexpr int STAGE = A_BYTES + B_BYTES;
+  constexpr bool GATHER = !Op::A_TMA || !Op::B_TMA;
+  // TMA lookahead (chunks).  With gathers, thread 0 also produces, so it
+  // must only wait for the MMA two chunks back when it refills a stage.
+  constexpr int L = GATHER ? (S > 2 ? S - 2 : 1) : S - 1;
+  __shared__ __align__(8) uint64_t full[S], empty[S], done;
+  __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Op op(prm, smem + S * STAGE, smem);
   if (tid == 0) {
-    for (int s = 0; s <= S; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    mbar_init(smem_u32(&done), 1);
+    op.init_barriers();
     fence_barrier_init();
+    op.prefetch();
   }
   if (warp == 0) tmem_alloc(&tmem_base, Op::TMEM_COLS);
   op.stage(tid);
@@ -255,43 +222,64 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
   const uint32_t sbase = smem_u32(smem);
   constexpr uint32_t idesc = make_idesc(BM, BN);
   const int nk = op.num_k_chunks();
-  // prologue: chunks 0 .. L-1 in flight
+  auto issue = [&](int c) {
+    const int s = c % S;
+    if (c >= S) mbar_wait(smem_u32(&empty[s]), ((c / S) - 1) & 1);
+    const uint32_t bar = smem_u32(&full[s]);
+    mbar_expect_tx(bar, op.tx_bytes(c));
+    op.issue(c, sbase + s * STAGE, sbase + s * STAGE + A_BYTES, bar);
+  };
+  if (tid == 0)
+    for (int c = 0; c < L && c < nk; ++c) issue(c);
+  if (GATHER) {
 #pragma unroll 1
-  for (int c = 0; c < L; ++c) {
-    if (c < nk) {
-      op.issue_extra(c, tid);
-      issue_chunk(op, sbase + (c % S) * STAGE, sbase + (c % S) * STAGE + A_BYTES, c * BK, tid);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      if (tid == 0 && kb + L < nk) issue(kb + L);
+      op.before_gather(kb, tid);
+      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
+      const int k0 = kb * BK;
+      if (!Op::A_TMA) {
+#pragma unroll
+        for (int q = 0; q < BM * 8 / THREADS; ++q) {
+          const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
+          sts128(As + sw_off(r, kc), op.a(r, k0 + kc * 4));
+        }
+      }
+      if (!Op::B_TMA) {
+        for (int u = tid; u < BN * 8; u += THREADS) {
+          const int c = u % BN, kc = u / BN;
+          sts128(Bs + sw_off(c, kc), op.b(c, k0 + kc * 4));
+        }
+      }
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        mbar_wait(smem_u32(&full[s]), (kb / S) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k)
+          mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (kb | k) != 0);
+        mma_commit(smem_u32(&empty[s]));
+        if (kb == nk - 1) mma_commit(smem_u32(&done));
+      }
     }
-    cp_commit();
-  }
+  } else if (tid == 0) {  // TMA-only: one thread streams copies and MMAs
 #pragma unroll 1
-  for (int kb = 0; kb < nk; ++kb) {
-    const int s = kb % S;
-    const int c = kb + L;
-    if (c < nk) {
-      const int s2 = c % S;
-      if (c >= S) mbar_wait(&bars[s2], ((c / S) - 1) & 1);
-      op.issue_extra(c, tid);
-      issue_chunk(op, sbase + s2 * STAGE, sbase + s2 * STAGE + A_BYTES, c * BK, tid);
-    }
-    cp_commit();
-    cp_wait<L>();
-    if (Op::SYNC_AFTER_WAIT) __syncthreads();
-    const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
-    produce_chunk(op, As, Bs, kb * BK, tid);
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      if (kb + L < nk) issue(kb + L);
+      mbar_wait(smem_u32(&full[s]), (kb / S) & 1);
       tc_fence_after();
+      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
 #pragma unroll
       for (int k = 0; k < BK / 8; ++k)
-        mma_tf32(tbase, make_desc(As + k * 256, 128, 1024), make_desc(Bs + k * 256, 128, 1024), idesc,
-                 (kb | k) != 0);
-      mma_commit(&bars[s]);
-      if (kb == nk - 1) mma_commit(&bars[S]);
+        mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (kb | k) != 0);
+      mma_commit(smem_u32(&empty[s]));
+      if (kb == nk - 1) mma_commit(smem_u32(&done));
     }
   }
-  cp_wait<0>();
+  __syncwarp();
   // epilogue: warps 0-3 columns [0, BN/2), warps 4-7 [BN/2, BN) (BN >= 32),
   // or warps 0-3 only for BN = 16
   const int row = (warp & 3) * 32 + lane;
@@ -299,7 +287,8 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
   const bool active = BN >= 32 || warp < 4;
   const int cbeg = (BN >= 32 && warp >= 4) ? HALF : 0;
   if (nk > 0) {
-    mbar_wait(&bars[S], 0);
+    mbar_wait(smem_u32(&done), 0);
+    __syncwarp();
     tc_fence_after();
     if (active) {
 #pragma unroll 1
@@ -326,66 +315,75 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
 
 // common no-op hooks
 struct OpBase {
-  static constexpr bool SYNC_AFTER_WAIT = false;
+  __device__ void init_barriers() {}
+  __device__ void prefetch() {}
   __device__ void stage(int) {}
-  __device__ void issue_extra(int, int) {}
-  __device__ void a_raw(int, int, float4) {}
-  __device__ void b_raw(int, int, float4) {}
-  __device__ void finish(int) {}
+  __device__ void before_gather(int, int) {}
   __device__ float4 a(int, int) const { return zero4(); }
   __device__ float4 b(int, int) const { return zero4(); }
-  __device__ const float* a_src(int, int, bool& v) const { v = false; return nullptr; }
-  __device__ const float* b_src(int, int, bool& v) const { v = false; return nullptr; }
-  __device__ const float* a_src4(int, int, int, bool& v) const { v = false; return nullptr; }
-  __device__ const float* b_src4(int, int, int, bool& v) const { v = false; return nullptr; }
+  __device__ void finish(int) {}
 };
 
 // ------------------------------------------- conv2 + bias + pool2 (+mask)
 // rows r = (image n = 2*tile + r/64, position p = ho*8+wo), cols f (50 of 64),
 // K = (c,i,j) 500 (+12 zero pad).  A(r,k) = p1[n,c,ho+i,wo+j] gathered from
-// the two staged images through a k -> c*144+i*12+j table; B(f,k) = W2[f,k]
-// copied with cp.async.
+// the two images (stored TF32 by conv1+pool1) bulk-copied into shared memory,
+// through a k -> c*144+i*12+j table; B(f,k) = W2f[f,k] by TMA.  The pooled
+// output p2 is stored TF32-rounded (its only consumers are the ip1
+// contractions), plus its transpose p2T[k][n] for the ip1 weight gradient.
 struct Conv2Fwd : OpBase {
   struct Params {
+    CUtensorMap tb;  // W2f [64][512]
     const float* p1;
-    const float* w;
     const float* b;
     float* p2;
+    float* p2T;  // [800][npad]
     uint8_t* m2;
-    int N;
+    int N, npad;
   };
-  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
-  static constexpr int A_MODE = GATHER, B_MODE = COPY16;
-  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 512 * 4;
+  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 3;
+  static constexpr bool A_TMA = false, B_TMA = true;
+  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 512 * 4 + 16;
   const Params& p;
-  float* img;
-  int* koff;
-  int n0, rowoff;
-  __device__ Conv2Fwd(const Params& q, uint8_t* st, uint8_t*)
-      : p(q), img((float*)st), koff((int*)(st + 2 * 2880 * 4)) {
+  uint32_t img_s, koff_s, ibar_s;  // shared-space addresses
+  uint32_t row_s;                  // this thread's row base inside the images
+  int n0;
+  __device__ Conv2Fwd(const Params& q, uint8_t* st, uint8_t*) : p(q) {
+    img_s = smem_u32(st);
+    koff_s = img_s + 2 * 2880 * 4;
+    ibar_s = koff_s + 2048;
     n0 = blockIdx.x * 2;
     const int r = threadIdx.x & 127, pos = r & 63;
-    rowoff = (r >> 6) * 2880 + (pos >> 3) * 12 + (pos & 7);
+    row_s = img_s + 4 * ((r >> 6) * 2880 + (pos >> 3) * 12 + (pos & 7));
   }
   __device__ int num_k_chunks() const { return 16; }
+  __device__ void init_barriers() { mbar_init(ibar_s, 1); }
+  __device__ void prefetch() { prefetch_tmap(&p.tb); }
   __device__ void stage(int tid) {
-    const int cnt = min(2, p.N - n0) * 2880;
-    const float4* src = reinterpret_cast<const float4*>(p.p1 + (size_t)n0 * 2880);
-    for (int i = tid; i < 2 * 720; i += THREADS)
-      reinterpret_cast<float4*>(img)[i] = (i * 4 < cnt) ? __ldg(src + i) : zero4();
+    const int cnt = min(2, p.N - n0);
+    if (tid == 0) {
+      mbar_expect_tx(ibar_s, cnt * 2880 * 4);
+      bulk_g2s(img_s, p.p1 + (size_t)n0 * 2880, cnt * 2880 * 4, ibar_s);
+    }
+    if (cnt < 2)
+      for (int i = tid; i < 2880; i += THREADS) stsf(img_s + 4 * (2880 + i), 0.f);
     for (int k = tid; k < 512; k += THREADS) {
       const int c = k / 25, rem = k - c * 25, i = rem / 5, j = rem - i * 5;
-      koff[k] = k < 500 ? c * 144 + i * 12 + j : -1;
+      sts_i32(koff_s + 4 * k, k < 500 ? 4 * (c * 144 + i * 12 + j) : -4);  // byte offsets; -4 = padding
     }
   }
-  __device__ float g(int k) const {
-    const int o = koff[k];
-    return o >= 0 ? img[rowoff + o] : 0.f;
+  __device__ void before_gather(int kb, int) {
+    if (kb == 0) mbar_wait(ibar_s, 0);
   }
-  __device__ float4 a(int, int k) const { return f4(g(k), g(k + 1), g(k + 2), g(k + 3)); }
-  __device__ const float* b_src(int f, int k, bool& v) const {
-    v = f < 50 && k < 500;
-    return v ? p.w + f * 500 + k : p.w;
+  __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
+  __device__ void issue(int c, uint32_t, uint32_t Bs, uint32_t bar) { tma2d(Bs, &p.tb, c * BK, 0, bar); }
+  __device__ float g(int o) const {  // the padding taps (o < 0) read a harmless in-CTA word, then select 0
+    const float v = ldsf(row_s + o);
+    return o >= 0 ? v : 0.f;
+  }
+  __device__ float4 a(int, int k) const {
+    const int4 o = lds_i4(koff_s + 4 * k);  // warp-uniform: broadcast
+    return f4(g(o.x), g(o.y), g(o.z), g(o.w));
   }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int n = n0 + (row >> 6), pos = row & 63, ho = pos >> 3, wo = pos & 7;
@@ -403,9 +401,11 @@ struct Conv2Fwd : OpBase {
         if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
       }
       if (off == 0 && n < p.N) {
-        const size_t o = ((size_t)n * 50 + f) * 16 + (ho >> 1) * 4 + (wo >> 1);
-        p.p2[o] = best;
-        p.m2[o] = (uint8_t)arg;
+        const int k = f * 16 + (ho >> 1) * 4 + (wo >> 1);
+        const float r = tf32f(best);
+        p.p2[(size_t)n * 800 + k] = r;
+        p.p2T[(size_t)k * p.npad + n] = r;
+        p.m2[(size_t)n * 800 + k] = (uint8_t)arg;
       }
     }
   }
@@ -413,30 +413,26 @@ struct Conv2Fwd : OpBase {
 
 // ------------------------------------------------------ ip fwd + bias + relu
 // y[n,o] = relu(sum_k x[n,k] W[o,k] + b[o]); rows n, cols o (BN 16), K = 800.
+// A = p2 (TF32) and B = W1f by TMA.
 struct IpFwd : OpBase {
   struct Params {
-    const float* x;
-    const float* w;
+    CUtensorMap ta, tb;
     const float* b;
     float* y;
     int M, K, Nout, relu;
   };
-  static constexpr int BN = 16, TMEM_COLS = 32, STAGES = 4;
-  static constexpr int A_MODE = COPY16, B_MODE = COPY16;
+  static constexpr int BN = 16, TMEM_COLS = 32, STAGES = 6;
+  static constexpr bool A_TMA = true, B_TMA = true;
   static constexpr int STAGE_BYTES = 0;
   const Params& p;
   int m0, o0;
   __device__ IpFwd(const Params& q, uint8_t*, uint8_t*) : p(q), m0(blockIdx.y * BM), o0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
-  __device__ const float* a_src(int r, int k, bool& v) const {
-    const int m = m0 + r;
-    v = m < p.M && k < p.K;
-    return v ? p.x + (size_t)m * p.K + k : p.x;
-  }
-  __device__ const float* b_src(int c, int k, bool& v) const {
-    const int o = o0 + c;
-    v = o < p.Nout && k < p.K;
-    return v ? p.w + (size_t)o * p.K + k : p.w;
+  __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
+  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
+  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
+    tma2d(As, &p.ta, c * BK, m0, bar);
+    tma2d(Bs, &p.tb, c * BK, o0, bar);
   }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int m = m0 + row;
@@ -455,41 +451,29 @@ struct IpFwd : OpBase {
   }
 };
 
-// --------------------------------------------- ip weight gradient (+ bias)
+// --------------------------------------------------------- ip weight gradient
 // dW[o,k] = sum_n dy[n,o] x[n,k]: rows o, cols k (BN 32), K = n (batch).
-// Both operands are transposed in global memory: 4-byte cp.async per element
-// (a warp covers 32 consecutive rows: coalesced).  db[o] = sum_n dy[n,o]
-// (fp32, unrounded) from the raw A values in column tile 0; thread tid always
-// owns row o0 + (tid & 127), K sub-chunks tid >> 7 and 2 + (tid >> 7).
+// A = dy^T (da1T [500][npad], TF32) and B = x^T (p2T [800][npad], TF32) by
+// TMA.  The bias gradient comes from the ip2 backward kernel (exact fp32).
 struct IpWgrad : OpBase {
   struct Params {
-    const float* dy;
-    const float* x;
+    CUtensorMap ta, tb;
     float* dw;
-    float* db;
     int M, K, Nout;
   };
-  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 4;
-  static constexpr int A_MODE = COPY4, B_MODE = COPY4;
-  static constexpr int STAGE_BYTES = THREADS * 4;
+  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 6;
+  static constexpr bool A_TMA = true, B_TMA = true;
+  static constexpr int STAGE_BYTES = 0;
   const Params& p;
-  float* red;
   int o0, k0;
-  float bacc;
-  __device__ IpWgrad(const Params& q, uint8_t* st, uint8_t*)
-      : p(q), red((float*)st), o0(blockIdx.y * BM), k0(blockIdx.x * BN), bacc(0.f) {}
+  __device__ IpWgrad(const Params& q, uint8_t*, uint8_t*) : p(q), o0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
-  __device__ const float* a_src4(int r, int n, int t, bool& v) const {
-    const int o = o0 + r;
-    v = o < p.Nout && n + t < p.M;
-    return v ? p.dy + (size_t)(n + t) * p.Nout + o : p.dy;
+  __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
+  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
+  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
+    tma2d(As, &p.ta, c * BK, o0, bar);
+    tma2d(Bs, &p.tb, c * BK, k0, bar);
   }
-  __device__ const float* b_src4(int c, int n, int t, bool& v) const {
-    const int k = k0 + c;
-    v = k < p.K && n + t < p.M;
-    return v ? p.x + (size_t)(n + t) * p.K + k : p.x;
-  }
-  __device__ void a_raw(int, int, float4 v) { bacc += (v.x + v.y) + (v.z + v.w); }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int o = o0 + row;
     if (o >= p.Nout) return;
@@ -500,44 +484,44 @@ struct IpWgrad : OpBase {
       *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k) = f4(v[j], v[j + 1], v[j + 2], v[j + 3]);
     }
   }
-  __device__ void finish(int tid) {
-    red[tid] = bacc;
-    __syncthreads();
-    if (blockIdx.x == 0 && p.db && tid < 128 && o0 + tid < p.Nout) p.db[o0 + tid] = red[tid] + red[tid + 128];
-  }
 };
 
 // ------------------------------- ip1 data gradient + pool2 backward (LeNet)
 // dp2[n,k] = sum_o dy[n,o] W1[o,k]; rows n, cols k (BN 32 = 2 filters x 16),
-// K = o (500).  B(k, o) = W1[o][k] is read transposed (4-byte cp.async).
+// K = o (500).  A = da1 (TF32 copy [N][500]), B = W1t [800][512] by TMA.
 // Epilogue scatters each dp2 value to its pool2 origin in the dense conv2
-// gradient G2[n,f,8,8] (zeros elsewhere).
+// gradient G2[n,f,8,8] (zeros elsewhere), stored TF32-rounded
+// (its only consumers are conv2's contractions), and sums the exact dp2 per
+// filter over the tile's rows for the conv2 bias gradient.
 struct IpDgradUnpool : OpBase {
   struct Params {
-    const float* dy;    // [N,500]
-    const float* w;     // [500,800]
+    CUtensorMap ta, tb;
     const uint8_t* m2;  // [N,800]
     float* g2;          // [N,50,8,8]
+    float* part_db2;    // [rowtiles][50]
     int N;
   };
-  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 4;
-  static constexpr int A_MODE = COPY16, B_MODE = COPY4;
-  static constexpr int STAGE_BYTES = 0;
+  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 6;
+  static constexpr bool A_TMA = true, B_TMA = true;
+  static constexpr int STAGE_BYTES = 2 * 128 * 4;
   const Params& p;
+  float* red;  // [2 filters][128 rows]
   int m0, k0;
-  __device__ IpDgradUnpool(const Params& q, uint8_t*, uint8_t*) : p(q), m0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
+  __device__ IpDgradUnpool(const Params& q, uint8_t* st, uint8_t*)
+      : p(q), red((float*)st), m0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
-  __device__ const float* a_src(int r, int o, bool& v) const {
-    const int n = m0 + r;
-    v = n < p.N && o < 500;
-    return v ? p.dy + (size_t)n * 500 + o : p.dy;
-  }
-  __device__ const float* b_src4(int c, int o, int t, bool& v) const {
-    v = o + t < 500;
-    return v ? p.w + (size_t)(o + t) * 800 + k0 + c : p.w;
+  __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
+  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
+  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
+    tma2d(As, &p.ta, c * BK, m0, bar);
+    tma2d(Bs, &p.tb, c * BK, k0, bar);
   }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int n = m0 + row;
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) s += v[q];
+    red[(c0 >> 4) * 128 + row] = n < p.N ? s : 0.f;
     if (n >= p.N) return;
     const int f = (k0 + c0) >> 4;  // the 16 columns are filter f's 4x4 pooled outputs
     const uint8_t* m = p.m2 + (size_t)n * 800 + f * 16;
@@ -552,10 +536,17 @@ struct IpDgradUnpool : OpBase {
       for (int w = 0; w < 8; ++w) {
         const int q = (h >> 1) * 4 + (w >> 1);
         const int off = (mw[q >> 2] >> (8 * (q & 3))) & 0xff;
-        o8[w] = (off == ((h & 1) * 2 + (w & 1))) ? v[q] : 0.f;
+        o8[w] = (off == ((h & 1) * 2 + (w & 1))) ? tf32f(v[q]) : 0.f;
       }
       *reinterpret_cast<float4*>(g + h * 8) = f4(o8[0], o8[1], o8[2], o8[3]);
       *reinterpret_cast<float4*>(g + h * 8 + 4) = f4(o8[4], o8[5], o8[6], o8[7]);
+    }
+  }
+  __device__ void finish(int tid) {
+    if (tid < 2) {  // fixed-order sum over the tile's 128 rows
+      float s = 0.f;
+      for (int r = 0; r < 128; ++r) s += red[tid * 128 + r];
+      p.part_db2[(size_t)blockIdx.y * 50 + (k0 >> 4) + tid] = s;
     }
   }
 };
@@ -566,37 +557,58 @@ struct IpDgradUnpool : OpBase {
 // with rows = 5 input channels x 25 taps (+3 zero rows) per M tile (4 tiles),
 // cols = 2 images x 64 positions (N = 128), K = f (50 of 64), followed by the
 // col2im gather dp1[n,c,h,w] = sum_{i,j} C[(c,i,j), (n, h-i, w-j)] done from
-// shared memory (C staged over the drained operand ring).  A = W2^T packed
-// TF32 once per backward (pack_w2t); B(p, f) = G2[n,f,p] (4-byte cp.async).
+// shared memory (C staged over the drained operand ring).  A = W2t by TMA;
+// B(p, f) = G2[n,f,p] gathered (transposed) from the two images of G2
+// bulk-copied into shared memory (G2 is stored TF32).
 struct Conv2Dgrad : OpBase {
   struct Params {
+    CUtensorMap ta;  // W2t [512][64]
     const float* g2;
-    const float* w2t;  // [4][128][64] TF32, zero padded
     float* dp1;
     int N;
   };
   static constexpr int BN = 128, TMEM_COLS = 128, STAGES = 2;
-  static constexpr int A_MODE = COPY16_PRE, B_MODE = COPY4;
-  static constexpr int STAGE_BYTES = 0;
+  static constexpr bool A_TMA = true, B_TMA = false;
+  static constexpr int STAGE_BYTES = 2 * 3200 * 4 + 16;
   const Params& p;
-  float* cs;  // [128 rows][128 cols], over the ring after the MMAs
+  uint32_t cs_s;  // [128 rows][128 cols] fp32, over the ring after the MMAs
+  uint32_t g2_s, gbar_s;
   int m, n0;
-  __device__ Conv2Dgrad(const Params& q, uint8_t*, uint8_t* ring)
-      : p(q), cs((float*)ring), m(blockIdx.x), n0(blockIdx.y * 2) {}
+  __device__ Conv2Dgrad(const Params& q, uint8_t* st, uint8_t* ring)
+      : p(q), cs_s(smem_u32(ring)), g2_s(smem_u32(st)), gbar_s(smem_u32(st) + 2 * 3200 * 4), m(blockIdx.x),
+        n0(blockIdx.y * 2) {}
   __device__ int num_k_chunks() const { return 2; }
-  __device__ const float* a_src(int r, int f, bool& v) const {
-    v = true;
-    return p.w2t + ((size_t)m * 128 + r) * 64 + f;
+  __device__ void init_barriers() { mbar_init(gbar_s, 1); }
+  __device__ void prefetch() { prefetch_tmap(&p.ta); }
+  __device__ void stage(int tid) {
+    const int cnt = min(2, p.N - n0);
+    if (tid == 0) {
+      mbar_expect_tx(gbar_s, cnt * 3200 * 4);
+      bulk_g2s(g2_s, p.g2 + (size_t)n0 * 3200, cnt * 3200 * 4, gbar_s);
+    }
+    if (cnt < 2)
+      for (int i = tid; i < 3200; i += THREADS) stsf(g2_s + 4 * (3200 + i), 0.f);
   }
-  __device__ const float* b_src4(int c, int f, int t, bool& v) const {
-    const int n = n0 + (c >> 6);
-    v = n < p.N && f + t < 50;
-    return v ? p.g2 + (size_t)n * 3200 + (f + t) * 64 + (c & 63) : p.g2;
+  __device__ void before_gather(int kb, int) {
+    if (kb == 0) mbar_wait(gbar_s, 0);
+  }
+  __device__ uint32_t tx_bytes(int) const { return BM * BK * 4; }
+  __device__ void issue(int c, uint32_t As, uint32_t, uint32_t bar) { tma2d(As, &p.ta, c * BK, m * 128, bar); }
+  __device__ float4 b(int c, int f) const {  // B(p, f..f+3) = G2[img, f.., p]; f >= 50 -> 0
+    const uint32_t s = g2_s + 4 * ((c >> 6) * 3200 + (c & 63));
+    float v[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int ff = f + t < 50 ? f + t : 0;  // keep the address in range, select after
+      const float x = ldsf(s + 4 * 64 * ff);
+      v[t] = f + t < 50 ? x : 0.f;
+    }
+    return f4(v[0], v[1], v[2], v[3]);
   }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    float4* dst = reinterpret_cast<float4*>(cs + row * 128 + c0);
+    const uint32_t dst = cs_s + 4 * (row * 128 + c0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) dst[j] = f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+    for (int j = 0; j < 4; ++j) sts128(dst + 16 * j, f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
   }
   __device__ void finish(int tid) {
     // 2 images x 5 channels x 144 outputs
@@ -605,7 +617,7 @@ struct Conv2Dgrad : OpBase {
       const int n = n0 + img;
       if (n >= p.N) continue;
       const int h = hw / 12, w = hw - h * 12;
-      const float* base = cs + (cl * 25) * 128 + img * 64;
+      const uint32_t base = cs_s + 4 * ((cl * 25) * 128 + img * 64);
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < 5; ++i) {
@@ -615,7 +627,7 @@ struct Conv2Dgrad : OpBase {
         for (int j = 0; j < 5; ++j) {
           const int wo = w - j;
           if ((unsigned)wo >= 8u) continue;
-          acc += base[(i * 5 + j) * 128 + ho * 8 + wo];
+          acc += ldsf(base + 4 * ((i * 5 + j) * 128 + ho * 8 + wo));
         }
       }
       p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
@@ -626,57 +638,60 @@ struct Conv2Dgrad : OpBase {
 // ------------------------------------------------ conv2 weight gradient
 // dW2[f,(c,i,j)] = sum_{n,p} G2[n,f,p] p1[n,c,ho+i,wo+j]; rows (c,i,j) 500 of
 // 512 (4 tiles), cols f (50 of 64), K = (n in this split, p): 2 chunks per
-// image.  Images are cp.async'ed into a 2-slot smem ring one image ahead;
-// A gathered from the staged image, B = G2 rows (16-byte cp.async).  Writes
-// split partials [split][f*500 + k] and the bias partial db2[f] = sum G2
-// (fp32, from the raw B values; thread tid always owns B row f = tid % 64).
+// image.  Images (TF32) are bulk-copied into a 2-slot ring one image ahead
+// and A is gathered from them; B = G2 rows f (TF32) by TMA (3D map
+// {p, f, n}).  Writes split partials [split][f*500 + k].
 struct Conv2Wgrad : OpBase {
   struct Params {
-    const float* g2;
+    CUtensorMap tb;  // G2 as {64 p, 50 f, N n}
     const float* p1;
     float* part;
     int N, splits, pstride;
   };
   static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
-  static constexpr int A_MODE = GATHER, B_MODE = COPY16;
-  static constexpr bool SYNC_AFTER_WAIT = true;
-  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + THREADS * 4;
+  static constexpr bool A_TMA = false, B_TMA = true;
+  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 32;
   const Params& p;
-  float* img;
-  float* red;
-  int kw0, n0, n1, rowoff;
+  uint32_t img_s, ibar_s;  // 2 image slots, 2 barriers
+  uint32_t row_s;          // this thread's row (c,i,j) base inside a slot
+  int kw0, n0, n1;
   bool rvalid;
-  float bacc;
-  __device__ Conv2Wgrad(const Params& q, uint8_t* st, uint8_t*)
-      : p(q), img((float*)st), red((float*)(st + 2 * 2880 * 4)) {
+  __device__ Conv2Wgrad(const Params& q, uint8_t* st, uint8_t*) : p(q) {
+    img_s = smem_u32(st);
+    ibar_s = img_s + 2 * 2880 * 4;
     kw0 = blockIdx.x * BM;
     n0 = (int)((long long)q.N * blockIdx.y / q.splits);
     n1 = (int)((long long)q.N * (blockIdx.y + 1) / q.splits);
     const int kw = kw0 + (threadIdx.x & 127);
     rvalid = kw < 500;
     const int c = kw / 25, rem = kw - c * 25, i = rem / 5, j = rem - i * 5;
-    rowoff = c * 144 + i * 12 + j;
-    bacc = 0.f;
+    row_s = img_s + 4 * (c * 144 + i * 12 + j);
   }
   __device__ int num_k_chunks() const { return (n1 - n0) * 2; }
-  __device__ void issue_extra(int c, int tid) {
-    if (c & 1) return;
-    const int im = c >> 1;
-    const float* src = p.p1 + (size_t)(n0 + im) * 2880;
-    const uint32_t dst = smem_u32(img + (im & 1) * 2880);
-    for (int i = tid; i < 720; i += THREADS) cp16(dst + i * 16, src + i * 4, true);
+  __device__ void init_barriers() {
+    mbar_init(ibar_s, 1);
+    mbar_init(ibar_s + 8, 1);
+  }
+  __device__ void prefetch() { prefetch_tmap(&p.tb); }
+  __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
+  __device__ void issue(int c, uint32_t, uint32_t Bs, uint32_t bar) {
+    tma3d(Bs, &p.tb, (c & 1) * BK, 0, n0 + (c >> 1), bar);
+    if ((c & 1) == 0) {  // next image into its ring slot
+      const int im = c >> 1;
+      const uint32_t ib = ibar_s + 8 * (im & 1);
+      mbar_expect_tx(ib, 2880 * 4);
+      bulk_g2s(img_s + (im & 1) * 2880 * 4, p.p1 + (size_t)(n0 + im) * 2880, 2880 * 4, ib);
+    }
+  }
+  __device__ void before_gather(int kb, int) {
+    if ((kb & 1) == 0) mbar_wait(ibar_s + 8 * ((kb >> 1) & 1), (kb >> 2) & 1);
   }
   __device__ float4 a(int, int k) const {
     if (!rvalid) return zero4();
     const int im = k >> 6, pos = k & 63, ho = pos >> 3, wo = pos & 7;
-    const float* s = img + (im & 1) * 2880 + rowoff + ho * 12 + wo;
-    return f4(s[0], s[1], s[2], s[3]);
+    const uint32_t s = row_s + 4 * ((im & 1) * 2880 + ho * 12 + wo);
+    return f4(ldsf(s), ldsf(s + 4), ldsf(s + 8), ldsf(s + 12));
   }
-  __device__ const float* b_src(int f, int k, bool& v) const {
-    v = f < 50;
-    return v ? p.g2 + (size_t)(n0 + (k >> 6)) * 3200 + f * 64 + (k & 63) : p.g2;
-  }
-  __device__ void b_raw(int, int, float4 v) { bacc += (v.x + v.y) + (v.z + v.w); }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
     const int kw = kw0 + row;
     if (kw >= 500) return;
@@ -688,38 +703,99 @@ struct Conv2Wgrad : OpBase {
       dst[f * 500 + kw] = v[j];
     }
   }
-  __device__ void finish(int tid) {
-    red[tid] = bacc;
-    __syncthreads();
-    if (blockIdx.x == 0 && tid < 50)
-      p.part[(size_t)blockIdx.y * p.pstride + 25000 + tid] =
-          (red[tid] + red[tid + 64]) + (red[tid + 128] + red[tid + 192]);
-  }
 };
 
-// --------------------------------------------------------- weight repack
-// W2 [f][c][i][j] -> W2t [m (4)][r (128)][f (64)], r = (c - 5m)*25 + i*5 + j,
-// TF32-rounded, zero padded (conv2 data-gradient A operand; once per backward).
-struct PackW2tP {
-  const float* w2;
-  float* w2t;
-};
-__global__ void pack_w2t(const __grid_constant__ PackW2tP p) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= 4 * 128 * 64) return;
-  const int f = idx & 63, r = (idx >> 6) & 127, m = idx >> 13;
-  float v = 0.f;
-  if (f < 50 && r < 125) {
-    const int c = 5 * m + r / 25, tap = r % 25;
-    v = p.w2[f * 500 + c * 25 + tap];
+// --------------------------------------------------------- weight packing
+// Once per forward (weights change only in SGD), TF32-rounded copies of the
+// weights in the layouts the GEMMs consume, zero padded:
+//   W1f [500][800]  = W1                      (ip1 fwd B)
+//   W2f [64][512]   = W2 [f][(c,i,j)]         (conv2 fwd B)
+//   W2t [4][128][64]: W2t[m][r][f] = W2[f, 5m + r/25, tap r%25]  (conv2 dgrad A)
+//   W1t [800][512]  = W1^T                    (ip1 dgrad B; tiled transpose)
+constexpr int W1F_N = 500 * 800, W2F_N = 64 * 512, W2T_N = 4 * 128 * 64;
+__global__ void pack_weights(const __grid_constant__ PackP p) {
+  int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx < W1F_N) {
+    p.w1f[idx] = tf32f(p.w1[idx]);
+    return;
   }
-  p.w2t[idx] = tf32f(v);
+  idx -= W1F_N;
+  if (idx < W2F_N) {
+    const int f = idx >> 9, k = idx & 511;
+    p.w2f[idx] = (f < 50 && k < 500) ? tf32f(p.w2[f * 500 + k]) : 0.f;
+    return;
+  }
+  idx -= W2F_N;
+  if (idx < W2T_N) {
+    const int f = idx & 63, r = (idx >> 6) & 127, m = idx >> 13;
+    float v = 0.f;
+    if (f < 50 && r < 125) v = p.w2[f * 500 + (5 * m + r / 25) * 25 + r % 25];
+    p.w2t[idx] = tf32f(v);
+  }
+}
+// W1t[k][o] = W1[o][k] (o < 500), 32x32 tiles through shared memory
+__global__ void transpose_w1(const __grid_constant__ PackP p) {
+  __shared__ float t[32][33];
+  const int k0 = blockIdx.x * 32, o0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  for (int y = ty; y < 32; y += 8) {
+    const int o = o0 + y;
+    t[y][tx] = o < 500 ? p.w1[(size_t)o * 800 + k0 + tx] : 0.f;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) p.w1t[(size_t)(k0 + y) * 512 + o0 + tx] = tf32f(t[tx][y]);
 }
 
 // ------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  }
+  return fn;
+}
+static bool g_tmap_ok = true;
+// row-major fp32 [rows][cols] (row pitch `pitch` floats): box {32 cols, box_rows}, 128B swizzle
+static CUtensorMap tmap2d(const float* base, uint64_t rows, uint64_t cols, uint64_t pitch, uint32_t box_rows) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  EncodeTiledFn fn = encode_fn();
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  if (!fn || fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    g_tmap_ok = false;
+  return m;
+}
+// G2 [N][50][64] as {64 p, 50 f, N n}: box {32, 64, 1}, 128B swizzle
+static CUtensorMap tmap_g2(const float* base, uint64_t N) {
+  CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  EncodeTiledFn fn = encode_fn();
+  cuuint64_t dims[3] = {64, 50, N};
+  cuuint64_t strides[2] = {64 * 4, 3200 * 4};
+  cuuint32_t box[3] = {32, 64, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (!fn || fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    g_tmap_ok = false;
+  return m;
+}
+
 template <class Op>
-static constexpr size_t smem_bytes() {
-  return (size_t)Op::STAGES * (BM * BK * 4 + Op::BN * BK * 4) + Op::STAGE_BYTES;
+static constexpr size_t smem_bytes() {  // + 1 KB slack for the 1024-B alignment
+  return (size_t)Op::STAGES * (BM * BK * 4 + Op::BN * BK * 4) + Op::STAGE_BYTES + 1024;
 }
 
 template <class Op>
@@ -729,6 +805,7 @@ static cudaError_t opt_in() {
 }
 
 cudaError_t setup() {
+  if (!encode_fn()) return cudaErrorNotSupported;
   cudaError_t e;
   if ((e = opt_in<Conv2Fwd>()) != cudaSuccess) return e;
   if ((e = opt_in<IpFwd>()) != cudaSuccess) return e;
@@ -739,56 +816,65 @@ cudaError_t setup() {
   return cudaSuccess;
 }
 
+bool tensor_maps_ok() { return g_tmap_ok; }
+
 static unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
-Launch conv2_pool2_launch(const float* w, const float* b, const float* p1, float* p2, uint8_t* m2, int N, int) {
+Launch pack_weights_launch(const PackP& p) {
   Launch l;
-  Conv2Fwd::Params p{p1, w, b, p2, m2, N};
+  l.set((const void*)pack_weights, dim3(cdiv(W1F_N + W2F_N + W2T_N, 256)), dim3(256), 0, p);
+  return l;
+}
+
+Launch transpose_w1_launch(const PackP& p) {
+  Launch l;
+  l.set((const void*)transpose_w1, dim3(800 / 32, 512 / 32), dim3(256), 0, p);
+  return l;
+}
+
+Launch conv2_pool2_launch(const float* w2f, const float* b, const float* p1, float* p2, float* p2T, uint8_t* m2,
+                          int N, int npad) {
+  Launch l;
+  Conv2Fwd::Params p{tmap2d(w2f, 64, 512, 512, 64), p1, b, p2, p2T, m2, N, npad};
   l.set((const void*)tc_gemm<Conv2Fwd>, dim3(cdiv(N, 2)), dim3(THREADS), smem_bytes<Conv2Fwd>(), p);
   return l;
 }
 
-Launch ip_fwd_launch(const float* x, const float* w, const float* b, float* y, int M, int K, int Nout, bool relu,
-                     int) {
+Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N) {
   Launch l;
-  IpFwd::Params p{x, w, b, y, M, K, Nout, relu ? 1 : 0};
-  l.set((const void*)tc_gemm<IpFwd>, dim3(cdiv(Nout, IpFwd::BN), cdiv(M, BM)), dim3(THREADS), smem_bytes<IpFwd>(), p);
+  IpFwd::Params p{tmap2d(p2, N, 800, 800, BM), tmap2d(w1f, 500, 800, 800, IpFwd::BN), b, y, N, 800, 500, 1};
+  l.set((const void*)tc_gemm<IpFwd>, dim3(cdiv(500, IpFwd::BN), cdiv(N, BM)), dim3(THREADS), smem_bytes<IpFwd>(), p);
   return l;
 }
 
-Launch ip_wgrad_launch(const float* dy, const float* x, float* dw, float* db, int M, int K, int Nout, int) {
+Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad) {
   Launch l;
-  IpWgrad::Params p{dy, x, dw, db, M, K, Nout};
-  l.set((const void*)tc_gemm<IpWgrad>, dim3(cdiv(K, IpWgrad::BN), cdiv(Nout, BM)), dim3(THREADS),
+  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, BM), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
+  l.set((const void*)tc_gemm<IpWgrad>, dim3(cdiv(800, IpWgrad::BN), cdiv(500, BM)), dim3(THREADS),
         smem_bytes<IpWgrad>(), p);
   return l;
 }
 
-Launch ip_dgrad_unpool_launch(const float* dy, const float* w, const uint8_t* m2, float* g2, int N, int) {
+Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
+                               int N) {
   Launch l;
-  IpDgradUnpool::Params p{dy, w, m2, g2, N};
+  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, BM), tmap2d(w1t, 800, 512, 512, IpDgradUnpool::BN), m2, g2,
+                          part_db2, N};
   l.set((const void*)tc_gemm<IpDgradUnpool>, dim3(800 / IpDgradUnpool::BN, cdiv(N, BM)), dim3(THREADS),
         smem_bytes<IpDgradUnpool>(), p);
   return l;
 }
 
-Launch pack_w2d_launch(const float* w2, float* w2t) {
+Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N) {
   Launch l;
-  PackW2tP p{w2, w2t};
-  l.set((const void*)pack_w2t, dim3(cdiv(4 * 128 * 64, 256)), dim3(256), 0, p);
-  return l;
-}
-
-Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int) {
-  Launch l;
-  Conv2Dgrad::Params p{g2, w2t, dp1, N};
+  Conv2Dgrad::Params p{tmap2d(w2t, 512, 64, 64, BM), g2, dp1, N};
   l.set((const void*)tc_gemm<Conv2Dgrad>, dim3(4, cdiv(N, 2)), dim3(THREADS), smem_bytes<Conv2Dgrad>(), p);
   return l;
 }
 
-Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N, int) {
+Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N) {
   Launch l;
-  Conv2Wgrad::Params p{g2, p1, part, N, splits, 25050};
+  Conv2Wgrad::Params p{tmap_g2(g2, N), p1, part, N, splits, 25050};
   l.set((const void*)tc_gemm<Conv2Wgrad>, dim3(4, splits), dim3(THREADS), smem_bytes<Conv2Wgrad>(), p);
   return l;
 }

@@ -1,9 +1,9 @@
 // tc.h -- tcgen05 (5th-gen tensor core) TF32 kernels for the GEMM-shaped
 // LeNet layers: conv2 (+bias+pool2+mask), ip1 (+bias+relu), ip1 weight and
 // data gradients (the latter fused with pool2's backward), conv2 data and
-// weight gradients.  Accumulators live in TMEM; operands are staged in shared
-// memory in the UMMA canonical K-major layout by producer warps (implicit
-// im2col gather with round-to-nearest TF32 conversion).
+// weight gradients, and the per-step TF32 weight packing they consume.
+// Dense operands are fed by TMA from TF32 copies in global memory; the
+// tensor maps are encoded at plan-build time (library-owned buffers).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -11,14 +11,28 @@
 
 namespace pn {
 namespace tc {
-cudaError_t setup();  // opt-in shared memory sizes etc.
-Launch conv2_pool2_launch(const float* w, const float* b, const float* p1, float* p2, uint8_t* m2, int N, int sms);
-Launch ip_fwd_launch(const float* x, const float* w, const float* b, float* y, int M, int K, int Nout, bool relu,
-                     int sms);
-Launch ip_wgrad_launch(const float* dy, const float* x, float* dw, float* db, int M, int K, int Nout, int sms);
-Launch ip_dgrad_unpool_launch(const float* dy, const float* w, const uint8_t* m2, float* g2, int N, int sms);
-Launch pack_w2d_launch(const float* w2, float* w2d);  // W2 -> [c][(f,i,j)] TF32
-Launch conv2_dgrad_launch(const float* g2, const float* w2d, float* dp1, int N, int sms);
-Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N, int sms);
+// Packed TF32 weight copies (see tc.cu "weight packing")
+struct PackP {
+  const float* w1;  // [500][800]
+  const float* w2;  // [50][500]
+  float* w1f;       // [500][800]
+  float* w1t;       // [800][512]
+  float* w2f;       // [64][512]
+  float* w2t;       // [4][128][64]
+};
+constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2fFloats = 64 * 512, kW2tFloats = 4 * 128 * 64;
+
+cudaError_t setup();    // driver entry point + opt-in shared memory sizes
+bool tensor_maps_ok();  // false if any cuTensorMapEncodeTiled call failed
+Launch pack_weights_launch(const PackP& p);
+Launch transpose_w1_launch(const PackP& p);
+Launch conv2_pool2_launch(const float* w2f, const float* b, const float* p1, float* p2, float* p2T, uint8_t* m2,
+                          int N, int npad);
+Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N);
+Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
+Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
+                               int N);
+Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N);
+Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N);
 }  // namespace tc
 }  // namespace pn
