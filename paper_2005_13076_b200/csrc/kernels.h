@@ -8,6 +8,7 @@ __global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p);
 __global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p);
 __global__ void conv_bwd_weight_generic(const __grid_constant__ ConvBwdWeightP p);
 __global__ void reduce_partials(const __grid_constant__ ReduceP p);
+__global__ void reduce_partials_multi(const __grid_constant__ ReduceMultiP p);
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p);
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
 __global__ void gemm_generic(const __grid_constant__ GemmP p);

@@ -149,6 +149,31 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
   p.out[i] = acc;
 }
 
+// All split-partial reductions of a gradient bucket in one launch.  Block =
+// 8 warps x 32 consecutive outputs of one segment: warp w sums splits
+// w, w+8, ... (coalesced 128-B rows, ascending), then warp 0 adds the 8 warp
+// sums in order -- a fixed order, so reruns are bitwise identical.
+// p.total = number of 32-output blocks over all segments.
+__global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_constant__ ReduceMultiP p) {
+  __shared__ float sm[8][33];
+  int b = blockIdx.x, k = 0;
+  while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
+  const ReduceP& s = p.seg[k];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = b * 32 + lane;
+  float acc = 0.f;
+  if (i < s.n)
+    for (int j = w; j < s.splits; j += 8) acc += s.part[(long long)j * s.stride + i];
+  sm[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && i < s.n) {
+    float r = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) r += sm[q][lane];
+    s.out[i] = r;
+  }
+}
+
 // ------------------------------------------------------------------ pooling
 // P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
 // a row-major scan (strict >) and stores its plane-local index h*W+w.

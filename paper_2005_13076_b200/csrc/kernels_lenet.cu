@@ -281,34 +281,48 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // ---------------------------------------------------- conv1 weight gradient
 // dW1[f,i,j] = sum_n sum_q dp1[n,f,q] * x[n, h_q + i, w_q + j] where (h_q,w_q)
 // is the conv1 position pool1 routed gradient q to (P:220-222 composed with
-// S:351); db1[f] = sum dp1.  grid = splits over images, block = 320 threads
-// (20 filters x 16 lanes), images staged in smem.
+// S:351); db1[f] = sum dp1.  grid = splits over images (<= 4 images per
+// block), block = 320 threads (20 filters x 16 lanes), images staged in smem;
+// every (gradient, origin) pair of the block is loaded up front so the 36
+// global loads per thread are in flight together.
+constexpr int CW_IMGS = 4;
 __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
-  __shared__ float xs[4][784];
+  __shared__ float xs[CW_IMGS][784];
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
+  const int cnt = min(CW_IMGS, n1 - n0);
   const int f = threadIdx.x / 16, l = threadIdx.x % 16;
+  float g[CW_IMGS * 9];
+  int off[CW_IMGS * 9];
+#pragma unroll
+  for (int im = 0; im < CW_IMGS; ++im)
+#pragma unroll
+    for (int t = 0; t < 9; ++t) {
+      const bool v = im < cnt;
+      const long long idx = ((long long)(n0 + (v ? im : 0)) * 20 + f) * 144 + l + 16 * t;
+      g[im * 9 + t] = v ? __ldg(p.dp1 + idx) : 0.f;
+      off[im * 9 + t] = v ? (int)__ldg(p.m1 + idx) : 0;
+    }
+  for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x) xs[i / 784][i % 784] = __ldg(p.x + (long long)n0 * 784 + i);
+  __syncthreads();
   float acc[25], bacc = 0.f;
 #pragma unroll
   for (int t = 0; t < 25; ++t) acc[t] = 0.f;
-  for (int nb = n0; nb < n1; nb += 4) {
-    const int cnt = min(4, n1 - nb);
-    __syncthreads();
-    for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x) xs[i / 784][i % 784] = __ldg(p.x + (long long)nb * 784 + i);
-    __syncthreads();
-    for (int im = 0; im < cnt; ++im) {
-      const long long base = ((long long)(nb + im) * 20 + f) * 144;
-      for (int q = l; q < 144; q += 16) {
-        const float g = __ldg(p.dp1 + base + q);
-        const int off = p.m1[base + q];
-        const int h = 2 * (q / 12) + (off >> 1), w = 2 * (q % 12) + (off & 1);
-        bacc += g;
-        const float* xp = &xs[im][h * 28 + w];
 #pragma unroll
-        for (int i = 0; i < 5; ++i)
+  for (int im = 0; im < CW_IMGS; ++im) {
+    if (im >= cnt) break;
 #pragma unroll
-          for (int j = 0; j < 5; ++j) acc[i * 5 + j] = fmaf(g, xp[i * 28 + j], acc[i * 5 + j]);
-      }
+    for (int t = 0; t < 9; ++t) {
+      const int q = l + 16 * t;
+      const float gv = g[im * 9 + t];
+      const int o = off[im * 9 + t];
+      const int h = 2 * (q / 12) + (o >> 1), w = 2 * (q % 12) + (o & 1);
+      bacc += gv;
+      const float* xp = &xs[im][h * 28 + w];
+#pragma unroll
+      for (int i = 0; i < 5; ++i)
+#pragma unroll
+        for (int j = 0; j < 5; ++j) acc[i * 5 + j] = fmaf(gv, xp[i * 28 + j], acc[i * 5 + j]);
     }
   }
 #pragma unroll

@@ -408,7 +408,7 @@ static pn_status allocate(pn_net* net) {
     if (L.off < 0) continue;
     // conv1's fused weight gradient is a light SIMT kernel: give it more
     // CTAs (4 images each at batch 512)
-    L.splits = (net->fused && &L == &net->layers[0]) ? 4 * kWgradSplits : kWgradSplits;
+    L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 3) / 4 : kWgradSplits;
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
   }
@@ -492,6 +492,19 @@ static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const
   ReduceP r{part, out, n, splits, n};
   Launch l;
   l.set((const void*)reduce_partials, dim3(cdiv(n, 256)), dim3(256), 0, r);
+  add(v, name, l);
+}
+
+static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs) {
+  ReduceMultiP m{};
+  m.nseg = (int)segs.size();
+  m.total = 0;
+  for (size_t i = 0; i < segs.size() && i < 6; ++i) {
+    m.seg[i] = segs[i];
+    m.total += (segs[i].n + 31) / 32;  // 32-output blocks
+  }
+  Launch l;
+  l.set((const void*)reduce_partials_multi, dim3(m.total), dim3(256), 0, m);
   add(v, name, l);
 }
 
@@ -652,7 +665,14 @@ static void build_fused_lenet(pn_net* net) {
     add(fwd, "ip2+softmax_loss", l, [](Launch& l, const StepArgs& a) { l.params<Ip2LossP>().labels = a.labels; });
     add_loss(net, fwd);
   }
-  // ---- backward (reverse order)
+  // ---- backward (reverse order).  Split-partial reductions are merged per
+  // gradient bucket: one launch for the ip bucket (ready before the NCCL ip
+  // allreduce), one for the conv bucket at the end.
+  auto seg = [](const float* part, float* out, int n, int splits, int stride) {
+    return ReduceP{part, out, n, splits, stride};
+  };
+  std::vector<ReduceP> ip_segs, conv_segs;
+  ip_segs.push_back(seg(net->partials + i2.part_off, G + i2.off, 5010, i2.splits, 5010));
   {
     Ip2BwdP p{lg.diff, a1.data, P + i2.off, a1.diff, net->partials + i2.part_off,
               net->partials + i2.part_off + 5000, N, i2.splits, 5010,
@@ -660,14 +680,14 @@ static void build_fused_lenet(pn_net* net) {
     Launch l;
     l.set((const void*)lenet_ip2_bwd, dim3(4, i2.splits), dim3(128), 0, p);
     add(bwd, "ip2.bwd+relu1.bwd", l);
-    add_reduce(net, bwd, i2);
   }
   if (net->tf32) {
-    add_reduce_raw(bwd, "ip1.bgrad_reduce", net->part_b1, G + i1.off + i1.wcount, 500, i2.splits);
+    ip_segs.push_back(seg(net->part_b1, G + i1.off + i1.wcount, 500, i2.splits, 500));
     add(bwd, "ip1.wgrad[tc]", tc::ip1_wgrad_launch(net->da1rT, net->p2T, G + i1.off, N, net->npad));
+    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs);
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
-    add_reduce_raw(bwd, "conv2.bgrad_reduce", net->part_db2, G + c2.off + 25000, 50, (N + 127) / 128);
+    conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, (N + 127) / 128, 50));
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
     Launch l;
@@ -677,6 +697,7 @@ static void build_fused_lenet(pn_net* net) {
     Launch l2;
     l2.set((const void*)colsum_generic, dim3(500), dim3(256), 0, c);
     add(bwd, "ip1.bgrad", l2);
+    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs);
     GemmP d{a1.diff, P + i1.off, p2.diff, nullptr, N, 800, 500, 500, 1, 800, 1, 0};
     Launch l3;
     l3.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(N, 64)), dim3(256), 0, d);
@@ -689,7 +710,8 @@ static void build_fused_lenet(pn_net* net) {
   if (net->tf32) {
     add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->pack.w2t, p1.diff, N));
     add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits, N));
-    add_reduce(net, bwd, c2, /*with_bias=*/false);  // conv2.b came from the ip1 dgrad epilogue
+    // conv2.b comes from the ip1 dgrad epilogue's partials
+    conv_segs.push_back(seg(net->partials + c2.part_off, G + c2.off, 25000, c2.splits, 25050));
   } else {
     ConvBwdDataP q{cv2.diff, P + c2.off, p1.diff, N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8};
     Launch l;
@@ -700,7 +722,7 @@ static void build_fused_lenet(pn_net* net) {
     Launch l2;
     l2.set((const void*)conv_bwd_weight_generic, dim3(1000, c2.splits), dim3(256), 0, w);
     add(bwd, "conv2.wgrad", l2);
-    add_reduce(net, bwd, c2);
+    conv_segs.push_back(seg(net->partials + c2.part_off, G + c2.off, 25050, c2.splits, 25050));
   }
   {
     Conv1WgradP p{p1.diff, p1.m8, nullptr, net->partials + c1.part_off, net->partials + c1.part_off + 500, N,
@@ -708,8 +730,9 @@ static void build_fused_lenet(pn_net* net) {
     Launch l;
     l.set((const void*)lenet_conv1_wgrad, dim3(c1.splits), dim3(320), 0, p);
     add(bwd, "conv1.wgrad", l, [](Launch& l, const StepArgs& a) { l.params<Conv1WgradP>().x = a.x; });
-    add_reduce(net, bwd, c1);
+    conv_segs.push_back(seg(net->partials + c1.part_off, G + c1.off, 520, c1.splits, 520));
   }
+  add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
 }
 
 static void build_update(pn_net* net) {
@@ -731,6 +754,8 @@ static void add_dp_stages(pn_net* net) {
   size_t pos = 0;
   for (size_t i = 0; i < bwd.size(); ++i)
     if (bwd[i].name.rfind("ip", 0) == 0) pos = i + 1;
+  for (size_t i = 0; i < bwd.size(); ++i)  // fused plans: right after the ip bucket is final
+    if (bwd[i].name == "ip.bucket_reduce") pos = i + 1;
   auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) {
     return [net, off, cnt, ready](cudaStream_t st) -> cudaError_t {
       cudaError_t e = cudaEventRecord(ready, st);

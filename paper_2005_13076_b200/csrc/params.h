@@ -33,6 +33,10 @@ struct ReduceP {  // out[i] = sum_s part[s*stride + i], i < n (fixed order s = 0
   float* out;
   int n, splits, stride;
 };
+struct ReduceMultiP {  // several ReduceP segments in one launch
+  ReduceP seg[6];
+  int nseg, total;
+};
 struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   const float* x;
   float* y;

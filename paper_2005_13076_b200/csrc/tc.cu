@@ -34,7 +34,7 @@ namespace tc {
 
 constexpr int BM = 128;  // tile rows = UMMA M
 constexpr int BK = 32;   // K elements per chunk (4 MMAs of K = 8) = one 128-B swizzle row
-constexpr int THREADS = 256;
+constexpr int THREADS = 192;  // 6 warps: producer, MMA, 4 gather/epilogue
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -175,16 +175,26 @@ __device__ __forceinline__ float4 f4(float a, float b, float c, float d) { retur
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
 // ------------------------------------------------------------------ engine
+// Warp-specialized (6 warps): warp 0 lane 0 = TMA producer, warp 1 lane 0 =
+// MMA issuer, warps 2-5 = gatherers (implicit-im2col operands) and, after
+// the K loop, the epilogue (warp w reads TMEM lane quadrant w % 4).  The
+// producer and gatherers run up to STAGES chunks ahead of the MMA; all hand
+// offs are mbarriers (full: TMA bytes landed, gath: 128 gatherer arrivals
+// after fence.proxy.async, empty: tcgen05.commit of the chunk's MMAs).
+//
 // Op interface:
 //   BN, TMEM_COLS, STAGES, A_TMA, B_TMA (else gathered), STAGE_BYTES
 //   Op(params, staging_smem, ring_smem)   decodes the tile
 //   int  num_k_chunks()
-//   void stage(tid)                       one-time generic staging (engine syncs)
-//   void issue(chunk, As, Bs, bar)        thread 0: TMA / bulk copies for a chunk
+//   void stage(tid)                       one-time generic staging (all threads; engine syncs)
+//   void issue(chunk, As, Bs, bar)        producer: TMA / bulk copies for a chunk
 //   uint32_t tx_bytes(chunk)              bytes those copies complete on `bar`
-//   void before_gather(chunk, tid)        all threads, before gathering a chunk
+//   void before_gather(chunk)             gatherers, before gathering a chunk
 //   float4 a(r, k) / b(c, k)              gathered (already TF32) values
 //   void epilogue(row, c0, v[16]);  void finish(tid)
+constexpr int GATHER_T0 = 64;  // first gatherer thread
+__device__ __forceinline__ int gtid() { return (int)threadIdx.x - GATHER_T0; }
+
 template <class Op>
 __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typename Op::Params prm) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -196,10 +206,8 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
   constexpr int B_BYTES = BN * BK * 4;
   constexpr int STAGE = A_BYTES + B_BYTES;
   constexpr bool GATHER = !Op::A_TMA || !Op::B_TMA;
-  // TMA lookahead (chunks).  With gathers, thread 0 also produces, so it
-  // must only wait for the MMA two chunks back when it refills a stage.
-  constexpr int L = GATHER ? (S > 2 ? S - 2 : 1) : S - 1;
-  __shared__ __align__(8) uint64_t full[S], empty[S], done;
+  constexpr int NG = THREADS - GATHER_T0;  // 128 gatherer threads
+  __shared__ __align__(8) uint64_t full[S], empty[S], gath[S], done;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   Op op(prm, smem + S * STAGE, smem);
@@ -207,6 +215,7 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
     for (int s = 0; s < S; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&empty[s]), 1);
+      mbar_init(smem_u32(&gath[s]), NG);
     }
     mbar_init(smem_u32(&done), 1);
     op.init_barriers();
@@ -222,54 +231,23 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
   const uint32_t sbase = smem_u32(smem);
   constexpr uint32_t idesc = make_idesc(BM, BN);
   const int nk = op.num_k_chunks();
-  auto issue = [&](int c) {
-    const int s = c % S;
-    if (c >= S) mbar_wait(smem_u32(&empty[s]), ((c / S) - 1) & 1);
-    const uint32_t bar = smem_u32(&full[s]);
-    mbar_expect_tx(bar, op.tx_bytes(c));
-    op.issue(c, sbase + s * STAGE, sbase + s * STAGE + A_BYTES, bar);
-  };
-  if (tid == 0)
-    for (int c = 0; c < L && c < nk; ++c) issue(c);
-  if (GATHER) {
+  if (tid == 0) {
+    // ---- TMA producer
 #pragma unroll 1
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % S;
-      if (tid == 0 && kb + L < nk) issue(kb + L);
-      op.before_gather(kb, tid);
-      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
-      const int k0 = kb * BK;
-      if (!Op::A_TMA) {
-#pragma unroll
-        for (int q = 0; q < BM * 8 / THREADS; ++q) {
-          const int u = tid + q * THREADS, r = u & (BM - 1), kc = u >> 7;
-          sts128(As + sw_off(r, kc), op.a(r, k0 + kc * 4));
-        }
-      }
-      if (!Op::B_TMA) {
-        for (int u = tid; u < BN * 8; u += THREADS) {
-          const int c = u % BN, kc = u / BN;
-          sts128(Bs + sw_off(c, kc), op.b(c, k0 + kc * 4));
-        }
-      }
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {
-        mbar_wait(smem_u32(&full[s]), (kb / S) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int k = 0; k < BK / 8; ++k)
-          mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (kb | k) != 0);
-        mma_commit(smem_u32(&empty[s]));
-        if (kb == nk - 1) mma_commit(smem_u32(&done));
-      }
+    for (int c = 0; c < nk; ++c) {
+      const int s = c % S;
+      if (c >= S) mbar_wait(smem_u32(&empty[s]), ((c / S) - 1) & 1);
+      const uint32_t bar = smem_u32(&full[s]);
+      mbar_expect_tx(bar, op.tx_bytes(c));
+      op.issue(c, sbase + s * STAGE, sbase + s * STAGE + A_BYTES, bar);
     }
-  } else if (tid == 0) {  // TMA-only: one thread streams copies and MMAs
+  } else if (tid == 32) {
+    // ---- MMA issuer
 #pragma unroll 1
     for (int kb = 0; kb < nk; ++kb) {
       const int s = kb % S;
-      if (kb + L < nk) issue(kb + L);
       mbar_wait(smem_u32(&full[s]), (kb / S) & 1);
+      if (GATHER) mbar_wait(smem_u32(&gath[s]), (kb / S) & 1);
       tc_fence_after();
       const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
 #pragma unroll
@@ -278,33 +256,55 @@ __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typen
       mma_commit(smem_u32(&empty[s]));
       if (kb == nk - 1) mma_commit(smem_u32(&done));
     }
+  } else if (GATHER && tid >= GATHER_T0) {
+    // ---- gatherers
+    const int g = gtid();
+#pragma unroll 1
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % S;
+      if (kb >= S) mbar_wait(smem_u32(&empty[s]), ((kb / S) - 1) & 1);
+      op.before_gather(kb);
+      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
+      const int k0 = kb * BK;
+      if (!Op::A_TMA) {
+#pragma unroll
+        for (int q = 0; q < BM * 8 / NG; ++q) {
+          const int u = g + q * NG, r = u & (BM - 1), kc = u >> 7;
+          sts128(As + sw_off(r, kc), op.a(r, k0 + kc * 4));
+        }
+      }
+      if (!Op::B_TMA) {
+        for (int u = g; u < BN * 8; u += NG) {
+          const int c = u % BN, kc = u / BN;
+          sts128(Bs + sw_off(c, kc), op.b(c, k0 + kc * 4));
+        }
+      }
+      fence_proxy_async();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gath[s])) : "memory");
+    }
   }
   __syncwarp();
-  // epilogue: warps 0-3 columns [0, BN/2), warps 4-7 [BN/2, BN) (BN >= 32),
-  // or warps 0-3 only for BN = 16
-  const int row = (warp & 3) * 32 + lane;
-  constexpr int HALF = BN >= 32 ? BN / 2 : BN;
-  const bool active = BN >= 32 || warp < 4;
-  const int cbeg = (BN >= 32 && warp >= 4) ? HALF : 0;
-  if (nk > 0) {
-    mbar_wait(smem_u32(&done), 0);
-    __syncwarp();
-    tc_fence_after();
-    if (active) {
+  // ---- epilogue: warps 2-5, thread = TMEM lane (tile row), all columns
+  if (warp >= 2) {
+    const int row = (warp & 3) * 32 + lane;
+    if (nk > 0) {
+      mbar_wait(smem_u32(&done), 0);
+      __syncwarp();
+      tc_fence_after();
 #pragma unroll 1
-      for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
+      for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         tmem_ld16(tbase + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
         op.epilogue(row, c0, v);
       }
-    }
-  } else if (active) {  // empty K range (a weight-gradient split with no images)
+    } else {  // empty K range (a weight-gradient split with no images)
 #pragma unroll 1
-    for (int c0 = cbeg; c0 < cbeg + HALF; c0 += 16) {
-      float v[16];
+      for (int c0 = 0; c0 < BN; c0 += 16) {
+        float v[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] = 0.f;
-      op.epilogue(row, c0, v);
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        op.epilogue(row, c0, v);
+      }
     }
   }
   tc_fence_before();
@@ -318,7 +318,7 @@ struct OpBase {
   __device__ void init_barriers() {}
   __device__ void prefetch() {}
   __device__ void stage(int) {}
-  __device__ void before_gather(int, int) {}
+  __device__ void before_gather(int) {}
   __device__ float4 a(int, int) const { return zero4(); }
   __device__ float4 b(int, int) const { return zero4(); }
   __device__ void finish(int) {}
@@ -353,7 +353,7 @@ struct Conv2Fwd : OpBase {
     koff_s = img_s + 2 * 2880 * 4;
     ibar_s = koff_s + 2048;
     n0 = blockIdx.x * 2;
-    const int r = threadIdx.x & 127, pos = r & 63;
+    const int r = gtid() & 127, pos = r & 63;
     row_s = img_s + 4 * ((r >> 6) * 2880 + (pos >> 3) * 12 + (pos & 7));
   }
   __device__ int num_k_chunks() const { return 16; }
@@ -372,7 +372,7 @@ struct Conv2Fwd : OpBase {
       sts_i32(koff_s + 4 * k, k < 500 ? 4 * (c * 144 + i * 12 + j) : -4);  // byte offsets; -4 = padding
     }
   }
-  __device__ void before_gather(int kb, int) {
+  __device__ void before_gather(int kb) {
     if (kb == 0) mbar_wait(ibar_s, 0);
   }
   __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
@@ -589,7 +589,7 @@ struct Conv2Dgrad : OpBase {
     if (cnt < 2)
       for (int i = tid; i < 3200; i += THREADS) stsf(g2_s + 4 * (3200 + i), 0.f);
   }
-  __device__ void before_gather(int kb, int) {
+  __device__ void before_gather(int kb) {
     if (kb == 0) mbar_wait(gbar_s, 0);
   }
   __device__ uint32_t tx_bytes(int) const { return BM * BK * 4; }
@@ -605,10 +605,15 @@ struct Conv2Dgrad : OpBase {
     }
     return f4(v[0], v[1], v[2], v[3]);
   }
+  // C tile in smem with the 16-B chunk index XOR-swizzled by row % 8 (the
+  // epilogue's 32 lanes are 32 rows: unswizzled they would hit one bank group)
+  __device__ uint32_t cs_addr(int row, int col) const {
+    return cs_s + row * 512 + ((((col >> 2) ^ (row & 7))) << 4) + ((col & 3) << 2);
+  }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const uint32_t dst = cs_s + 4 * (row * 128 + c0);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) sts128(dst + 16 * j, f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+    for (int j = 0; j < 4; ++j)
+      sts128(cs_addr(row, c0 + 4 * j), f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
   }
   __device__ void finish(int tid) {
     // 2 images x 5 channels x 144 outputs
@@ -617,7 +622,6 @@ struct Conv2Dgrad : OpBase {
       const int n = n0 + img;
       if (n >= p.N) continue;
       const int h = hw / 12, w = hw - h * 12;
-      const uint32_t base = cs_s + 4 * ((cl * 25) * 128 + img * 64);
       float acc = 0.f;
 #pragma unroll
       for (int i = 0; i < 5; ++i) {
@@ -627,7 +631,7 @@ struct Conv2Dgrad : OpBase {
         for (int j = 0; j < 5; ++j) {
           const int wo = w - j;
           if ((unsigned)wo >= 8u) continue;
-          acc += ldsf(base + 4 * ((i * 5 + j) * 128 + ho * 8 + wo));
+          acc += ldsf(cs_addr(cl * 25 + i * 5 + j, img * 64 + ho * 8 + wo));
         }
       }
       p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
@@ -650,46 +654,49 @@ struct Conv2Wgrad : OpBase {
   };
   static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
   static constexpr bool A_TMA = false, B_TMA = true;
-  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 32;
+  // image ring: the producer may run STAGES chunks ahead of the MMA while the
+  // gatherers still read the image of the oldest unfinished chunk
+  static constexpr int SLOTS = STAGES / 2 + 1;
+  static constexpr int STAGE_BYTES = SLOTS * 2880 * 4 + SLOTS * 8;
   const Params& p;
-  uint32_t img_s, ibar_s;  // 2 image slots, 2 barriers
+  uint32_t img_s, ibar_s;  // SLOTS image slots, SLOTS barriers
   uint32_t row_s;          // this thread's row (c,i,j) base inside a slot
   int kw0, n0, n1;
   bool rvalid;
   __device__ Conv2Wgrad(const Params& q, uint8_t* st, uint8_t*) : p(q) {
     img_s = smem_u32(st);
-    ibar_s = img_s + 2 * 2880 * 4;
+    ibar_s = img_s + SLOTS * 2880 * 4;
     kw0 = blockIdx.x * BM;
     n0 = (int)((long long)q.N * blockIdx.y / q.splits);
     n1 = (int)((long long)q.N * (blockIdx.y + 1) / q.splits);
-    const int kw = kw0 + (threadIdx.x & 127);
+    const int kw = kw0 + (gtid() & 127);
     rvalid = kw < 500;
     const int c = kw / 25, rem = kw - c * 25, i = rem / 5, j = rem - i * 5;
     row_s = img_s + 4 * (c * 144 + i * 12 + j);
   }
   __device__ int num_k_chunks() const { return (n1 - n0) * 2; }
   __device__ void init_barriers() {
-    mbar_init(ibar_s, 1);
-    mbar_init(ibar_s + 8, 1);
+    for (int i = 0; i < SLOTS; ++i) mbar_init(ibar_s + 8 * i, 1);
   }
   __device__ void prefetch() { prefetch_tmap(&p.tb); }
   __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
   __device__ void issue(int c, uint32_t, uint32_t Bs, uint32_t bar) {
     tma3d(Bs, &p.tb, (c & 1) * BK, 0, n0 + (c >> 1), bar);
     if ((c & 1) == 0) {  // next image into its ring slot
-      const int im = c >> 1;
-      const uint32_t ib = ibar_s + 8 * (im & 1);
+      const int im = c >> 1, slot = im % SLOTS;
+      const uint32_t ib = ibar_s + 8 * slot;
       mbar_expect_tx(ib, 2880 * 4);
-      bulk_g2s(img_s + (im & 1) * 2880 * 4, p.p1 + (size_t)(n0 + im) * 2880, 2880 * 4, ib);
+      bulk_g2s(img_s + slot * 2880 * 4, p.p1 + (size_t)(n0 + im) * 2880, 2880 * 4, ib);
     }
   }
-  __device__ void before_gather(int kb, int) {
-    if ((kb & 1) == 0) mbar_wait(ibar_s + 8 * ((kb >> 1) & 1), (kb >> 2) & 1);
+  __device__ void before_gather(int kb) {
+    const int im = kb >> 1;
+    if ((kb & 1) == 0) mbar_wait(ibar_s + 8 * (im % SLOTS), (im / SLOTS) & 1);
   }
   __device__ float4 a(int, int k) const {
     if (!rvalid) return zero4();
     const int im = k >> 6, pos = k & 63, ho = pos >> 3, wo = pos & 7;
-    const uint32_t s = row_s + 4 * ((im & 1) * 2880 + ho * 12 + wo);
+    const uint32_t s = row_s + 4 * ((im % SLOTS) * 2880 + ho * 12 + wo);
     return f4(ldsf(s), ldsf(s + 4), ldsf(s + 8), ldsf(s + 12));
   }
   __device__ void epilogue(int row, int c0, const float (&v)[16]) const {

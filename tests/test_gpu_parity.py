@@ -225,7 +225,7 @@ def test_teacher_forced_fused_stages(tf32):
     # backward: ip2 + relu1 from oracle dz and ip1
     net.net_put_blob("ip2", dz.astype(np.float32).reshape(N, 10, 1, 1), PN_DIFF)
     run(net, 1, "ip2.bwd")
-    run(net, 1, "ip2.wgrad_reduce")
+    run(net, 1, "ip.bucket_reduce")
     gs = gref["scales"]
     assert_close("ip2.w grad", host(net.net_get_blob("ip2.w", PN_DIFF)), gref["grads"]["ip2.w"], gs["ip2.w"],
                  RTOL[False])
@@ -249,9 +249,10 @@ def test_teacher_forced_fused_stages(tf32):
     assert_close("conv2 diff (unpooled)", host(net.net_get_blob("conv2", PN_DIFF)), G2, Sg2, rtol)
     # conv2 backward from the oracle's G2
     net.net_put_blob("conv2", G2.astype(np.float32), PN_DIFF)
-    for name in net.stages(1):       # (TF32 plan: weight repack, dgrad, wgrad, reduce)
+    for name in net.stages(1):
         if name.startswith("conv2."):
             run(net, 1, name)
+    run(net, 1, "conv.bucket_reduce")
     assert_close("dp1", host(net.net_get_blob("pool1", PN_DIFF)), gref["diffs"]["conv2"], gs["conv2.dx"], rtol)
     assert_close("conv2.w grad", host(net.net_get_blob("conv2.w", PN_DIFF)), gref["grads"]["conv2.w"],
                  gs["conv2.w"], rtol)
@@ -268,7 +269,7 @@ def test_teacher_forced_fused_stages(tf32):
     net.net_put_blob("pool1", gref["diffs"]["conv2"].astype(np.float32), PN_DIFF)
     net.net_put_blob("pool1", out["masks"]["pool1"], PN_MASK)
     run(net, 1, "conv1.wgrad", xd, yd)
-    run(net, 1, "conv1.wgrad_reduce")
+    run(net, 1, "conv.bucket_reduce")
     assert_close("conv1.w grad", host(net.net_get_blob("conv1.w", PN_DIFF)), gref["grads"]["conv1.w"],
                  gs["conv1.w"], RTOL[False])
     assert_close("conv1.b grad", host(net.net_get_blob("conv1.b", PN_DIFF)).ravel(), gref["grads"]["conv1.b"],
