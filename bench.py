@@ -208,6 +208,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2005_13076_b200 import Net, make_sgd, synth
+    from paper_2005_13076_b200.dp import dp_bootstrap, max_over_ranks
 
     world, rank, local = dist_setup(args)
     torch.cuda.set_device(local)
@@ -220,11 +221,7 @@ def main():
                                  seed=2, bias="zero")
     net.set_params(params)
     if world > 1:
-        uid = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            uid.copy_(torch.frombuffer(bytearray(Net.pn_nccl_unique_id()), dtype=torch.uint8))
-        dist.broadcast(uid, 0)
-        net.net_dp_init(world, rank, bytes(uid.cpu().numpy().tobytes()))
+        dp_bootstrap(net, dist)   # library-owned NCCL communicator (id via the torch PG)
 
     # resident synthetic dataset (> L2), distinct per rank
     xs, ys = synth.mnist_like_fast(BATCH * DATASET_BATCHES, seed=100 + rank)
@@ -256,9 +253,7 @@ def main():
     ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     if world > 1:
-        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dist)
         dist.barrier()
     net.net_sync_errors()
     final_loss = loss.item()
@@ -283,9 +278,7 @@ def main():
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+        ms_e2e = max_over_ranks(ms_e2e, dist)
     e2e = {"value": world * BATCH * e2e_steps / (ms_e2e / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": BATCH * 784 * 4 + BATCH * 4, "d2h_bytes_per_step": 4,
            "steps": e2e_steps}

@@ -300,3 +300,27 @@ def test_full_size_bench_configuration(tf32):
     for k in params:
         g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
         assert_norm(f"grad {k}", g, gref["grads"][k], 10 * rtol)
+
+
+# --------------------------------------------------------- data parallel
+@pytest.mark.parametrize("tf32", [False, True])
+def test_dp_single_rank_communicator_matches_local_step(tf32):
+    """The library-owned NCCL path (unique id, comm stream, bucketed allreduce
+    captured in the step graph) on a 1-rank communicator must reproduce the
+    local step bitwise (sum over one rank, scale 1/1)."""
+    N = 64
+    sgd = make_sgd()
+    res = []
+    for dp in (False, True):
+        net, ref, params, x, y = make("lenet", N, tf32)
+        if dp:
+            net.net_dp_init(1, 0, Net.pn_nccl_unique_id())
+            assert any(s.startswith("allreduce") for s in net.stages(1))
+        xd, yd = cuda(x), cuda(y)
+        for it in range(2):
+            net.net_train_step(xd, yd, sgd, it)
+        net.net_sync_errors()
+        res.append([host(net.net_get_blob(k)) for k in params])
+        net.close()
+    for a, b in zip(*res):
+        assert_bitwise("dp(1) vs local", a, b)
