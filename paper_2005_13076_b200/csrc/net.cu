@@ -748,7 +748,7 @@ static void build_update(pn_net* net) {
 
 // data-parallel exchange stages (inserted into the backward list)
 static void add_dp_stages(pn_net* net) {
-  if (net->nranks <= 1) return;
+  if (!net->comm) return;  // (a 1-rank communicator still runs the full exchange path)
   auto& bwd = net->phase[1];
   // position: after the last stage producing an ip-bucket gradient
   size_t pos = 0;
