@@ -708,7 +708,7 @@ static void build_fused_lenet(pn_net* net) {
     add(bwd, "pool2.bwd", l4);
   }
   if (net->tf32) {
-    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->pack.w2t, p1.diff, N));
+    add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->pack.w2t, p1.diff, N, net->tc_sms));
     add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits, N));
     // conv2.b comes from the ip1 dgrad epilogue's partials
     conv_segs.push_back(seg(net->partials + c2.part_off, G + c2.off, 25000, c2.splits, 25050));

@@ -24,6 +24,7 @@
 //     fused tail.
 #include <cuda.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 
@@ -712,6 +713,175 @@ struct Conv2Wgrad : OpBase {
   }
 };
 
+// ------------------------------ conv2 data gradient, persistent pipeline
+// Same mathematics as Conv2Dgrad (C = W2^T G2, then col2im), reorganised so
+// one CTA per SM streams many image pairs through a pipeline:
+//   warp 0      producer: W2t tile once (TMA), G2 pairs (bulk copy, 2 buffers)
+//   warp 1      MMA: 8 x tcgen05.mma (M=128 rows (c,i,j), N=128 (2 images x
+//               64 positions), K=64 f) per pair into one of 2 TMEM accumulators
+//   warps 2-5   B builders: transposed gather G2[n,f,p] -> B(p, f) (SW128)
+//   warps 6-13  epilogue: TMEM -> smem C (XOR-swizzled), then the col2im
+//               gather dp1[n,c,h,w] = sum_{i,j} C[(c,i,j), (n, h-i, w-j)]
+// so the B build of pair t+1, the MMA of pair t+1 and the col2im of pair t
+// overlap.  grid = (4 row tiles m, G groups); group g takes pairs g, g+G, ...
+namespace dg {
+constexpr int WARPS = 14, THREADS_D = WARPS * 32;
+constexpr int A_BYTES = 2 * 128 * 128;        // 2 K-chunks x 128 rows x 128 B
+constexpr int B_BYTES = 2 * 128 * 128;        // per buffer
+constexpr int G_BYTES = 2 * 3200 * 4;         // per buffer (2 images)
+constexpr int CP = 132;                       // C pitch (floats)
+constexpr int C_BYTES = 128 * CP * 4 + 1024;  // + slack for predicated-off col2im taps
+constexpr int SMEM = A_BYTES + 2 * B_BYTES + 2 * G_BYTES + C_BYTES + 1024;
+struct Params {
+  CUtensorMap ta;  // W2t [512][64]
+  const float* g2;
+  float* dp1;
+  int N, groups;
+};
+}  // namespace dg
+
+__global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const __grid_constant__ dg::Params p) {
+  using namespace dg;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t A_s = smem_u32(smem), B_s = A_s + A_BYTES, G_s = B_s + 2 * B_BYTES, C_s = G_s + 2 * G_BYTES;
+  __shared__ __align__(8) uint64_t afull, gfull[2], gfree[2], bfull[2], bfree[2], accfull[2], accfree[2];
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = blockIdx.x, g = blockIdx.y;
+  const int npairs = (p.N + 1) / 2;
+  const int mine = g < npairs ? (npairs - g + p.groups - 1) / p.groups : 0;  // pairs g, g+G, ...
+  if (tid == 0) {
+    mbar_init(smem_u32(&afull), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&gfull[b]), 1);
+      mbar_init(smem_u32(&gfree[b]), 128);
+      mbar_init(smem_u32(&bfull[b]), 128);
+      mbar_init(smem_u32(&bfree[b]), 1);
+      mbar_init(smem_u32(&accfull[b]), 1);
+      mbar_init(smem_u32(&accfree[b]), 256);
+    }
+    fence_barrier_init();
+    prefetch_tmap(&p.ta);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  // C tile [128 rows][CP] fp32 (pitch 132: the 32 lanes' 16-B stores of 32
+  // different rows land on distinct bank groups)
+  auto cs_addr = [&](int row, int col) -> uint32_t { return C_s + 4 * (row * CP + col); };
+  if (tid == 0) {
+    // ---- producer
+    mbar_expect_tx(smem_u32(&afull), A_BYTES);
+    tma2d(A_s, &p.ta, 0, m * 128, smem_u32(&afull));
+    tma2d(A_s + 128 * 128, &p.ta, 32, m * 128, smem_u32(&afull));
+#pragma unroll 1
+    for (int i = 0; i < mine; ++i) {
+      const int b = i & 1, n0 = 2 * (g + i * p.groups), cnt = min(2, p.N - n0);
+      if (i >= 2) mbar_wait(smem_u32(&gfree[b]), ((i >> 1) - 1) & 1);
+      mbar_expect_tx(smem_u32(&gfull[b]), cnt * 3200 * 4);
+      bulk_g2s(G_s + b * G_BYTES, p.g2 + (size_t)n0 * 3200, cnt * 3200 * 4, smem_u32(&gfull[b]));
+    }
+  } else if (tid == 32) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, 128);
+    mbar_wait(smem_u32(&afull), 0);
+#pragma unroll 1
+    for (int i = 0; i < mine; ++i) {
+      const int b = i & 1;
+      mbar_wait(smem_u32(&bfull[b]), (i >> 1) & 1);
+      if (i >= 2) mbar_wait(smem_u32(&accfree[b]), ((i >> 1) - 1) & 1);
+      tc_fence_after();
+      const uint32_t Bb = B_s + b * B_BYTES;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_tf32(tbase + b * 128, make_desc(A_s + kc * 16384 + k * 32), make_desc(Bb + kc * 16384 + k * 32), idesc,
+                   (kc | k) != 0);
+      mma_commit(smem_u32(&bfree[b]));
+      mma_commit(smem_u32(&accfull[b]));
+    }
+  } else if (warp >= 2 && warp < 6) {
+    // ---- B builders: B(row = img*64 + pos, f) = G2[n0+img, f, pos], f >= 50 -> 0
+    const int t = tid - 64;                       // 0..127 = B row
+    const int img = t >> 6, pos = t & 63;
+#pragma unroll 1
+    for (int i = 0; i < mine; ++i) {
+      const int b = i & 1, n0 = 2 * (g + i * p.groups);
+      const bool valid = n0 + img < p.N;
+      mbar_wait(smem_u32(&gfull[b]), (i >> 1) & 1);
+      if (i >= 2) mbar_wait(smem_u32(&bfree[b]), ((i >> 1) - 1) & 1);
+      const uint32_t src = G_s + b * G_BYTES + 4 * (img * 3200 + pos);
+      const uint32_t Bb = B_s + b * B_BYTES;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {  // 16 units of 4 f: f = 4u
+        float v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int f = 4 * u + q;
+          const float x = ldsf(src + 4 * 64 * (f < 50 ? f : 0));
+          v[q] = (f < 50 && valid) ? x : 0.f;
+        }
+        sts128(Bb + (u >> 3) * 16384 + sw_off(t, u & 7), f4(v[0], v[1], v[2], v[3]));
+      }
+      fence_proxy_async();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gfree[b])) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bfull[b])) : "memory");
+    }
+  } else if (warp >= 6) {
+    // ---- epilogue: 8 warps, quadrant = warp % 4, column half = (warp - 6) / 4
+    const int et = tid - 192;  // 0..255
+    const int quad = warp & 3, half = (warp - 6) >> 2, row = quad * 32 + lane;
+#pragma unroll 1
+    for (int i = 0; i < mine; ++i) {
+      const int b = i & 1, n0 = 2 * (g + i * p.groups);
+      mbar_wait(smem_u32(&accfull[b]), (i >> 1) & 1);
+      __syncwarp();
+      tc_fence_after();
+#pragma unroll 1
+      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
+        float v[16];
+        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 128 + c0, v);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          sts128(cs_addr(row, c0 + 4 * j), f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+      }
+      tc_fence_before();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[b])) : "memory");
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // C complete
+      // col2im: element (row (cl,i,j), col im*64 + (h-i)*8 + (w-j)) sits at
+      // base(cl, im, h, w) + tap offset (i, j) with a compile-time offset per
+      // tap; out-of-window taps are predicated off (their address stays in smem)
+      for (int o = et; o < 2 * 5 * 144; o += 256) {
+        const int im = o / 720, rem = o - im * 720, cl = rem / 144, hw = rem - cl * 144;
+        const int n = n0 + im;
+        if (n >= p.N) continue;
+        const int h = hw / 12, w = hw - h * 12;
+        const uint32_t base = C_s + 4 * (cl * 25 * CP + im * 64 + h * 8 + w);
+        float acc = 0.f;
+#pragma unroll
+        for (int ii = 0; ii < 5; ++ii) {
+          const bool hv = (unsigned)(h - ii) < 8u;
+#pragma unroll
+          for (int jj = 0; jj < 5; ++jj) {
+            const bool v = hv && (unsigned)(w - jj) < 8u;
+            const float x = ldsf(base + 4 * (ii * (5 * CP - 8) + jj * (CP - 1)));
+            acc += v ? x : 0.f;
+          }
+        }
+        p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // C free for the next pair
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
 // --------------------------------------------------------- weight packing
 // Once per forward (weights change only in SGD), TF32-rounded copies of the
 // weights in the layouts the GEMMs consume, zero padded:
@@ -820,6 +990,9 @@ cudaError_t setup() {
   if ((e = opt_in<IpDgradUnpool>()) != cudaSuccess) return e;
   if ((e = opt_in<Conv2Dgrad>()) != cudaSuccess) return e;
   if ((e = opt_in<Conv2Wgrad>()) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute((const void*)conv2_dgrad_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dg::SMEM)) != cudaSuccess)
+    return e;
   return cudaSuccess;
 }
 
@@ -872,10 +1045,12 @@ Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_
   return l;
 }
 
-Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N) {
+Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms) {
   Launch l;
-  Conv2Dgrad::Params p{tmap2d(w2t, 512, 64, 64, BM), g2, dp1, N};
-  l.set((const void*)tc_gemm<Conv2Dgrad>, dim3(4, cdiv(N, 2)), dim3(THREADS), smem_bytes<Conv2Dgrad>(), p);
+  // persistent: one CTA per SM, 4 row tiles x groups of image pairs
+  const int pairs = (N + 1) / 2, groups = std::max(1, std::min(pairs, sms / 4));
+  dg::Params p{tmap2d(w2t, 512, 64, 64, BM), g2, dp1, N, groups};
+  l.set((const void*)conv2_dgrad_persistent, dim3(4, groups), dim3(dg::THREADS_D), dg::SMEM, p);
   return l;
 }
 

@@ -32,7 +32,7 @@ Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* 
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N);
-Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N);
+Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms);
 Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N);
 }  // namespace tc
 }  // namespace pn
