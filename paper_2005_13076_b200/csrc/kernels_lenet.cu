@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__
     for (int a = 0; a < 6; ++a)
 #pragma unroll
       for (int b = 0; b < 6; ++b) patch[a][b] = xs[im][(2 * ph + a) * 28 + 2 * pw + b];
+    float pooled[4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) {
       const int f = 4 * g + t;
@@ -67,9 +68,13 @@ __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__
       if (c11 > best) { best = c11; off = 3; }
       const long long o = ((long long)n * 20 + f) * 144 + q;
       // TF32 plan: round to nearest, ties away (the conv2 operand rounding)
-      p.p1[o] = p.round_tf32 ? __uint_as_float((__float_as_uint(best) + 0x1000u) & 0xFFFFE000u) : best;
+      pooled[t] = p.round_tf32 ? __uint_as_float((__float_as_uint(best) + 0x1000u) & 0xFFFFE000u) : best;
+      p.p1[o] = pooled[t];
       p.m1[o] = (uint8_t)off;
     }
+    if (p.p1c)  // [pair][cc = g][h = ph][n = im][w = pw][4 c]: the block's 2 images are one pair
+      reinterpret_cast<float4*>(p.p1c)[(size_t)blockIdx.x * 1440 + (g * 12 + ph) * 24 + im * 12 + pw] =
+          make_float4(pooled[0], pooled[1], pooled[2], pooled[3]);
   }
 }
 

@@ -162,6 +162,7 @@ struct pn_net {
   // TF32 plan operand copies (see tc.cu): transposes padded to npad columns
   int npad = 0;
   float* p2T = nullptr;       // [800][npad]
+  float* p1c = nullptr;       // pool1 in the conv2 tap-GEMM layout (tc.h)
   float* da1r = nullptr;      // [N][500]
   float* da1rT = nullptr;     // [500][npad]
   float* part_b1 = nullptr;   // [splits][500]  ip1 bias-gradient partials
@@ -418,10 +419,11 @@ static pn_status allocate(pn_net* net) {
   if (net->tf32) {
     TRY(net->alloc(&net->pack.w1f, tc::kW1fFloats));
     TRY(net->alloc(&net->pack.w1t, tc::kW1tFloats));
-    TRY(net->alloc(&net->pack.w2f, tc::kW2fFloats));
+    TRY(net->alloc(&net->pack.w2c, tc::kW2cFloats));
     TRY(net->alloc(&net->pack.w2t, tc::kW2tFloats));
     net->npad = (net->batch + 3) & ~3;  // TMA row pitch must be a multiple of 16 B
     TRY(net->alloc(&net->p2T, (size_t)800 * net->npad));
+    TRY(net->alloc(&net->p1c, (size_t)((net->batch + 1) / 2) * tc::kP1cPairFloats));
     TRY(net->alloc(&net->da1r, (size_t)net->batch * 500));
     TRY(net->alloc(&net->da1rT, (size_t)500 * net->npad));
     TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
@@ -633,14 +635,14 @@ static void build_fused_lenet(pn_net* net) {
   {
     // TF32 plan: pool1 is consumed only by conv2's contractions, so it is
     // stored TF32-rounded; the mask is taken before rounding
-    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0};
+    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c};
     Launch l;
     l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(288), 0, p);
     add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
   }
   if (net->tf32) {
-    add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(net->pack.w2f, P + c2.off + 25000, p1.data, p2.data, net->p2T,
-                                                        p2.m8, N, net->npad));
+    add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(net->pack.w2c, P + c2.off + 25000, net->p1c, p2.data,
+                                                        net->p2T, p2.m8, N, net->npad, net->tc_sms));
   } else {
     Conv2Pool2P p{p1.data, P + c2.off, P + c2.off + 25000, p2.data, p2.m8, N};
     Launch l;
@@ -1054,6 +1056,7 @@ static pn_status blob_io(pn_net* net, const char* name, int which, void* buf, in
         l.set((const void*)tf32_copy, dim3(cdiv((long long)c.R * c.C, 256)), dim3(256), 0, c);
         CU(l.launch(st));
       }
+      if (b->name == net->layers[1].top && which == PN_DATA) CU(tc::pack_p1c_launch(b->data, net->p1c, net->batch).launch(st));
     }
   } else {
     if (tmp) TRY(mask_io(net, b, tmp, true, st));

@@ -118,6 +118,13 @@ __device__ __forceinline__ float ldsf(uint32_t addr) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
   return v;
 }
+// same without the memory clobber: ordered after earlier volatile asm (barriers)
+// but free to overlap with global stores
+__device__ __forceinline__ float ldsf_nc(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ int4 lds_i4(uint32_t addr) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
@@ -325,93 +332,6 @@ struct OpBase {
   __device__ void finish(int) {}
 };
 
-// ------------------------------------------- conv2 + bias + pool2 (+mask)
-// rows r = (image n = 2*tile + r/64, position p = ho*8+wo), cols f (50 of 64),
-// K = (c,i,j) 500 (+12 zero pad).  A(r,k) = p1[n,c,ho+i,wo+j] gathered from
-// the two images (stored TF32 by conv1+pool1) bulk-copied into shared memory,
-// through a k -> c*144+i*12+j table; B(f,k) = W2f[f,k] by TMA.  The pooled
-// output p2 is stored TF32-rounded (its only consumers are the ip1
-// contractions), plus its transpose p2T[k][n] for the ip1 weight gradient.
-struct Conv2Fwd : OpBase {
-  struct Params {
-    CUtensorMap tb;  // W2f [64][512]
-    const float* p1;
-    const float* b;
-    float* p2;
-    float* p2T;  // [800][npad]
-    uint8_t* m2;
-    int N, npad;
-  };
-  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 3;
-  static constexpr bool A_TMA = false, B_TMA = true;
-  static constexpr int STAGE_BYTES = 2 * 2880 * 4 + 512 * 4 + 16;
-  const Params& p;
-  uint32_t img_s, koff_s, ibar_s;  // shared-space addresses
-  uint32_t row_s;                  // this thread's row base inside the images
-  int n0;
-  __device__ Conv2Fwd(const Params& q, uint8_t* st, uint8_t*) : p(q) {
-    img_s = smem_u32(st);
-    koff_s = img_s + 2 * 2880 * 4;
-    ibar_s = koff_s + 2048;
-    n0 = blockIdx.x * 2;
-    const int r = gtid() & 127, pos = r & 63;
-    row_s = img_s + 4 * ((r >> 6) * 2880 + (pos >> 3) * 12 + (pos & 7));
-  }
-  __device__ int num_k_chunks() const { return 16; }
-  __device__ void init_barriers() { mbar_init(ibar_s, 1); }
-  __device__ void prefetch() { prefetch_tmap(&p.tb); }
-  __device__ void stage(int tid) {
-    const int cnt = min(2, p.N - n0);
-    if (tid == 0) {
-      mbar_expect_tx(ibar_s, cnt * 2880 * 4);
-      bulk_g2s(img_s, p.p1 + (size_t)n0 * 2880, cnt * 2880 * 4, ibar_s);
-    }
-    if (cnt < 2)
-      for (int i = tid; i < 2880; i += THREADS) stsf(img_s + 4 * (2880 + i), 0.f);
-    for (int k = tid; k < 512; k += THREADS) {
-      const int c = k / 25, rem = k - c * 25, i = rem / 5, j = rem - i * 5;
-      sts_i32(koff_s + 4 * k, k < 500 ? 4 * (c * 144 + i * 12 + j) : -4);  // byte offsets; -4 = padding
-    }
-  }
-  __device__ void before_gather(int kb) {
-    if (kb == 0) mbar_wait(ibar_s, 0);
-  }
-  __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
-  __device__ void issue(int c, uint32_t, uint32_t Bs, uint32_t bar) { tma2d(Bs, &p.tb, c * BK, 0, bar); }
-  __device__ float g(int o) const {  // the padding taps (o < 0) read a harmless in-CTA word, then select 0
-    const float v = ldsf(row_s + o);
-    return o >= 0 ? v : 0.f;
-  }
-  __device__ float4 a(int, int k) const {
-    const int4 o = lds_i4(koff_s + 4 * k);  // warp-uniform: broadcast
-    return f4(g(o.x), g(o.y), g(o.z), g(o.w));
-  }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const int n = n0 + (row >> 6), pos = row & 63, ho = pos >> 3, wo = pos & 7;
-    const int off = (ho & 1) * 2 + (wo & 1);
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int f = c0 + j;
-      if (f >= 50) break;
-      float best = v[j] + __ldg(p.b + f);
-      int arg = off;
-#pragma unroll
-      for (int x = 1; x <= 8; x <<= 3) {  // xor 1 (wo pair), xor 8 (ho pair)
-        const float ov = __shfl_xor_sync(0xffffffffu, best, x);
-        const int oa = __shfl_xor_sync(0xffffffffu, arg, x);
-        if (ov > best || (ov == best && oa < arg)) { best = ov; arg = oa; }
-      }
-      if (off == 0 && n < p.N) {
-        const int k = f * 16 + (ho >> 1) * 4 + (wo >> 1);
-        const float r = tf32f(best);
-        p.p2[(size_t)n * 800 + k] = r;
-        p.p2T[(size_t)k * p.npad + n] = r;
-        p.m2[(size_t)n * 800 + k] = (uint8_t)arg;
-      }
-    }
-  }
-};
-
 // ------------------------------------------------------ ip fwd + bias + relu
 // y[n,o] = relu(sum_k x[n,k] W[o,k] + b[o]); rows n, cols o (BN 16), K = 800.
 // A = p2 (TF32) and B = W1f by TMA.
@@ -552,94 +472,6 @@ struct IpDgradUnpool : OpBase {
   }
 };
 
-// ------------------------------------------------- conv2 data gradient
-// dp1 = col2im(W2^T G2), computed as the GEMM
-//   C[(c,i,j), (n,p)] = sum_f W2[f,c,i,j] G2[n,f,p]
-// with rows = 5 input channels x 25 taps (+3 zero rows) per M tile (4 tiles),
-// cols = 2 images x 64 positions (N = 128), K = f (50 of 64), followed by the
-// col2im gather dp1[n,c,h,w] = sum_{i,j} C[(c,i,j), (n, h-i, w-j)] done from
-// shared memory (C staged over the drained operand ring).  A = W2t by TMA;
-// B(p, f) = G2[n,f,p] gathered (transposed) from the two images of G2
-// bulk-copied into shared memory (G2 is stored TF32).
-struct Conv2Dgrad : OpBase {
-  struct Params {
-    CUtensorMap ta;  // W2t [512][64]
-    const float* g2;
-    float* dp1;
-    int N;
-  };
-  static constexpr int BN = 128, TMEM_COLS = 128, STAGES = 2;
-  static constexpr bool A_TMA = true, B_TMA = false;
-  static constexpr int STAGE_BYTES = 2 * 3200 * 4 + 16;
-  const Params& p;
-  uint32_t cs_s;  // [128 rows][128 cols] fp32, over the ring after the MMAs
-  uint32_t g2_s, gbar_s;
-  int m, n0;
-  __device__ Conv2Dgrad(const Params& q, uint8_t* st, uint8_t* ring)
-      : p(q), cs_s(smem_u32(ring)), g2_s(smem_u32(st)), gbar_s(smem_u32(st) + 2 * 3200 * 4), m(blockIdx.x),
-        n0(blockIdx.y * 2) {}
-  __device__ int num_k_chunks() const { return 2; }
-  __device__ void init_barriers() { mbar_init(gbar_s, 1); }
-  __device__ void prefetch() { prefetch_tmap(&p.ta); }
-  __device__ void stage(int tid) {
-    const int cnt = min(2, p.N - n0);
-    if (tid == 0) {
-      mbar_expect_tx(gbar_s, cnt * 3200 * 4);
-      bulk_g2s(g2_s, p.g2 + (size_t)n0 * 3200, cnt * 3200 * 4, gbar_s);
-    }
-    if (cnt < 2)
-      for (int i = tid; i < 3200; i += THREADS) stsf(g2_s + 4 * (3200 + i), 0.f);
-  }
-  __device__ void before_gather(int kb) {
-    if (kb == 0) mbar_wait(gbar_s, 0);
-  }
-  __device__ uint32_t tx_bytes(int) const { return BM * BK * 4; }
-  __device__ void issue(int c, uint32_t As, uint32_t, uint32_t bar) { tma2d(As, &p.ta, c * BK, m * 128, bar); }
-  __device__ float4 b(int c, int f) const {  // B(p, f..f+3) = G2[img, f.., p]; f >= 50 -> 0
-    const uint32_t s = g2_s + 4 * ((c >> 6) * 3200 + (c & 63));
-    float v[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int ff = f + t < 50 ? f + t : 0;  // keep the address in range, select after
-      const float x = ldsf(s + 4 * 64 * ff);
-      v[t] = f + t < 50 ? x : 0.f;
-    }
-    return f4(v[0], v[1], v[2], v[3]);
-  }
-  // C tile in smem with the 16-B chunk index XOR-swizzled by row % 8 (the
-  // epilogue's 32 lanes are 32 rows: unswizzled they would hit one bank group)
-  __device__ uint32_t cs_addr(int row, int col) const {
-    return cs_s + row * 512 + ((((col >> 2) ^ (row & 7))) << 4) + ((col & 3) << 2);
-  }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-      sts128(cs_addr(row, c0 + 4 * j), f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-  }
-  __device__ void finish(int tid) {
-    // 2 images x 5 channels x 144 outputs
-    for (int o = tid; o < 2 * 5 * 144; o += THREADS) {
-      const int img = o / 720, rem = o - img * 720, cl = rem / 144, hw = rem - cl * 144;
-      const int n = n0 + img;
-      if (n >= p.N) continue;
-      const int h = hw / 12, w = hw - h * 12;
-      float acc = 0.f;
-#pragma unroll
-      for (int i = 0; i < 5; ++i) {
-        const int ho = h - i;
-        if ((unsigned)ho >= 8u) continue;
-#pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          const int wo = w - j;
-          if ((unsigned)wo >= 8u) continue;
-          acc += ldsf(cs_addr(cl * 25 + i * 5 + j, img * 64 + ho * 8 + wo));
-        }
-      }
-      p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
-    }
-  }
-};
-
 // ------------------------------------------------ conv2 weight gradient
 // dW2[f,(c,i,j)] = sum_{n,p} G2[n,f,p] p1[n,c,ho+i,wo+j]; rows (c,i,j) 500 of
 // 512 (4 tiles), cols f (50 of 64), K = (n in this split, p): 2 chunks per
@@ -713,9 +545,232 @@ struct Conv2Wgrad : OpBase {
   }
 };
 
+// ------------------------- conv2 + bias + pool2 (+mask), persistent tap GEMM
+// conv2 as 25 tap GEMMs accumulated in TMEM, with NO im2col:
+//   D[(ho,n,wo), f] = sum_{i,j} sum_c p1[n,c,ho+i,wo+j] W2[f,c,i,j]
+// The pooled layer-1 output of an image pair is stored (by conv1+pool1, TF32)
+// as p1c[pair][cc 5][h 12][n 2][w 12][4 c]: 4-channel planes of 16-B pixels.
+// In the UMMA K-major no-swizzle layout (core matrix = 8 rows x 16 B,
+// LBO = K-direction core-matrix stride, SBO = 8-row-group stride) the A
+// operand of tap (i,j) is then just a descriptor into that staged pair:
+//   rows r = (ho, n, wo) (8-row group = (ho, n), SBO = 192 B = one (h, n) row
+//   of 12 pixels), K = 24 channels (5 stored planes + 1 zero plane,
+//   LBO = 4608 B = one plane), start = pair + (i*24 + j)*16 B.
+// B = all 25 taps of W2 resident in shared memory as w2c[tap][cc 5][f 50][4 c]
+// (exactly W2's 25000 values, 100 KB, loaded once per CTA): rows f at 16 B
+// (SBO 128), planes at LBO = 800 B.  The N = 64 MMA also reads rows 50..63
+// (the next plane's first rows: finite values into ignored columns) and a 6th
+// plane (the next tap's first plane, or a zero pad) against A's zero plane.
+// Per pair: 25 taps x 3 MMAs (M=128, N=64, K=8).
+// Persistent, pairs split evenly over the CTAs: warp 0 = bulk-copy producer
+// (weights in 5 pieces, then a 3-stage pair ring), warp 1 = MMA issuer (2
+// TMEM accumulators), warps 2-5 = epilogue: TMEM -> smem tile C[row][f] (bank
+// skewed), then one thread per pooled (f, ph, pw) for both images: bias,
+// 2x2 max with the first-max mask, TF32 p2, its transpose p2T, the mask.
+namespace cf {
+constexpr int PLANE = 12 * 2 * 12 * 16;        // [h][n][w][4 c] of one pair = 4608 B
+constexpr int A_BYTES = 6 * PLANE;             // 24 channels per stage
+constexpr int A_GLOBAL = 5 * PLANE;            // 20 channels stored per pair
+constexpr int TAP_BYTES = 5 * 800;             // [cc 5][f 50][4 c]
+constexpr int B_BYTES = 99 * 1024;             // 25 taps + >= 1024 B zero pad
+constexpr int C_PITCH = 50;                    // floats per C row (+ skew below)
+constexpr int C_BYTES = 25 * 1024 + 1024;      // 128 x 50 floats + max skew
+constexpr int STAGES = 3;
+constexpr int THREADS_F = 192;
+constexpr int SMEM = B_BYTES + STAGES * A_BYTES + C_BYTES + 1024;
+static_assert(25 * TAP_BYTES + 1024 <= B_BYTES, "B pad");
+struct Params {
+  const float* w2c;
+  const float* p1c;
+  const float* b;
+  float* p2;
+  float* p2T;  // [800][npad]
+  uint8_t* m2;
+  int N, npad, per_cta;  // pairs [blockIdx.x * per_cta, + per_cta)
+};
+// C tile address of (row r, col f): rows of 50 floats, skewed by the pooled
+// row ph = r / 32 so that both the row-per-lane 8-B stores and the pooling
+// reads (lanes = 2 f x 4 ph x 4 pw) are bank-conflict free
+__device__ __forceinline__ uint32_t c_addr(uint32_t C_s, int r, int f) {
+  const int ph = r >> 5;
+  return C_s + 4 * (r * C_PITCH + f + 2 * (ph & 1) + 16 * (ph >> 1));
+}
+}  // namespace cf
+
+// UMMA shared-memory descriptor: K-major, no swizzle, sm_100 version 1.
+__device__ __forceinline__ uint64_t make_desc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46);
+}
+
+// dev-only timeline stamps (tools/tc_trace.cu builds with -DPN_TRACE)
+#ifdef PN_TRACE
+__device__ unsigned long long g_trace[148 * 16];
+__device__ __forceinline__ void stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_trace[blockIdx.x * 16 + k] = t;
+}
+#else
+__device__ __forceinline__ void stamp(int) {}
+#endif
+
+__global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const __grid_constant__ cf::Params p) {
+  using namespace cf;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t B_s = smem_u32(smem), A_s = B_s + B_BYTES, C_s = A_s + STAGES * A_BYTES;
+  __shared__ __align__(8) uint64_t wbar[5], full[STAGES], empty[STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float bias_s[50];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int npairs = (p.N + 1) / 2;
+  const int pair0 = blockIdx.x * p.per_cta;
+  if (tid < 50) bias_s[tid] = p.b[tid];
+  const int mine = max(0, min(p.per_cta, npairs - pair0));
+  if (tid == 0) stamp(0);
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(smem_u32(&wbar[i]), 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&empty[s]), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, 128);
+  // zero channel plane 5 of every stage and the pad after the last tap (the
+  // copies never write them); generic stores -> async proxy before the MMAs
+  for (int i = tid; i < STAGES * (PLANE / 16); i += THREADS_F)
+    sts128(A_s + (i / (PLANE / 16)) * A_BYTES + 5 * PLANE + (i % (PLANE / 16)) * 16, zero4());
+  for (int i = tid; i < (B_BYTES - 25 * TAP_BYTES) / 16; i += THREADS_F)
+    sts128(B_s + 25 * TAP_BYTES + 16 * i, zero4());
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    // ---- producer: the first pair, the weights in 5 pieces (taps of one
+    // kernel row each), then the remaining pairs
+#pragma unroll 1
+    for (int it = 0; it < mine; ++it) {
+      const int s = it % STAGES;
+      if (it >= STAGES) mbar_wait(smem_u32(&empty[s]), ((it / STAGES) - 1) & 1);
+      mbar_expect_tx(smem_u32(&full[s]), A_GLOBAL);
+      bulk_g2s(A_s + s * A_BYTES, (const uint8_t*)p.p1c + (size_t)(pair0 + it) * A_GLOBAL, A_GLOBAL,
+               smem_u32(&full[s]));
+      if (it == 0)
+        for (int i = 0; i < 5; ++i) {
+          mbar_expect_tx(smem_u32(&wbar[i]), 5 * TAP_BYTES);
+          bulk_g2s(B_s + i * 5 * TAP_BYTES, (const uint8_t*)p.w2c + i * 5 * TAP_BYTES, 5 * TAP_BYTES,
+                   smem_u32(&wbar[i]));
+        }
+    }
+  } else if (tid == 32) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, 64);
+#pragma unroll 1
+    for (int it = 0; it < mine; ++it) {
+      const int s = it % STAGES, b = it & 1;
+      mbar_wait(smem_u32(&full[s]), (it / STAGES) & 1);
+      if (it >= 2) mbar_wait(smem_u32(&tempty[b]), ((it >> 1) - 1) & 1);
+      tc_fence_after();
+      if (it < 4) stamp(1 + it);  // pair landed
+      const uint32_t d = tbase + b * 64;
+      // descriptors of tap (0,0), k step 0; every other MMA adds a
+      // compile-time offset to the 14-bit start-address field (no carry:
+      // shared addresses < 256 KB)
+      const uint64_t ad0 = make_desc_ns(A_s + s * A_BYTES, PLANE, 192), bd0 = make_desc_ns(B_s, 800, 128);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        if (it == 0) {
+          mbar_wait(smem_u32(&wbar[i]), 0);
+          tc_fence_after();
+          if (i == 0) stamp(14);  // first weight piece landed
+          if (i == 4) stamp(5);   // weights landed
+        }
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+#pragma unroll
+          for (int ks = 0; ks < 3; ++ks)
+            mma_tf32(d, ad0 + (uint64_t)(((i * 24 + j) * 16 + ks * 2 * PLANE) >> 4),
+                     bd0 + (uint64_t)(((i * 5 + j) * TAP_BYTES + ks * 1600) >> 4), idesc, (i | j | ks) != 0);
+      }
+      mma_commit(smem_u32(&empty[s]));
+      mma_commit(smem_u32(&tfull[b]));
+    }
+  } else if (warp >= 2) {
+    // ---- epilogue (128 threads): TMEM lane quadrant q = warp % 4 = rows 32q..
+    const int quad = warp & 3, row = quad * 32 + lane, et = tid - 64;
+#pragma unroll 1
+    for (int it = 0; it < mine; ++it) {
+      const int b = it & 1, pair = pair0 + it;
+      mbar_wait(smem_u32(&tfull[b]), (it >> 1) & 1);
+      if (warp == 2 && lane == 0 && it < 4) stamp(6 + it);  // accumulator ready
+      __syncwarp();
+      tc_fence_after();
+      float v[64];
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16)
+        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 64 + c0, *reinterpret_cast<float(*)[16]>(v + c0));
+      tc_fence_before();
+      if (warp == 2 && lane == 0 && it == 0) stamp(11);
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // C free (previous pair pooled)
+#pragma unroll
+      for (int f = 0; f < 50; f += 2)
+        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(c_addr(C_s, row, f)), "f"(v[f]), "f"(v[f + 1])
+                     : "memory");
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // C complete
+      if (warp == 2 && lane == 0 && it == 0) stamp(12);
+      const int n0 = 2 * pair;
+#pragma unroll
+      for (int q = 0; q < 7; ++q) {  // 800 pooled (f, ph, pw) over 128 threads
+        const int k = et + 128 * q;
+        if (k >= 800) break;
+        const int f = k >> 4, ph = (k >> 2) & 3, pw = k & 3;
+        const float bias = bias_s[f];
+        float out[2];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) {
+          const int r = ph * 32 + n * 8 + pw * 2;  // window rows r, r+1, r+16, r+17
+          const float v00 = ldsf_nc(c_addr(C_s, r, f)) + bias, v01 = ldsf_nc(c_addr(C_s, r + 1, f)) + bias;
+          const float v10 = ldsf_nc(c_addr(C_s, r + 16, f)) + bias, v11 = ldsf_nc(c_addr(C_s, r + 17, f)) + bias;
+          float best = v00;
+          int arg = 0;  // first maximum in window order (0,0),(0,1),(1,0),(1,1)
+          if (v01 > best) { best = v01; arg = 1; }
+          if (v10 > best) { best = v10; arg = 2; }
+          if (v11 > best) { best = v11; arg = 3; }
+          out[n] = tf32f(best);
+          if (n0 + n < p.N) {
+            p.p2[(size_t)(n0 + n) * 800 + k] = out[n];
+            p.m2[(size_t)(n0 + n) * 800 + k] = (uint8_t)arg;
+          }
+        }
+        if (n0 + 1 < p.N)
+          *reinterpret_cast<float2*>(p.p2T + (size_t)k * p.npad + n0) = make_float2(out[0], out[1]);
+        else
+          p.p2T[(size_t)k * p.npad + n0] = out[0];
+      }
+      if (warp == 2 && lane == 0 && it == 0) stamp(13);
+    }
+    if (warp == 2 && lane == 0) stamp(15);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) stamp(10);
+  if (warp == 0) tmem_dealloc(tbase, 128);
+}
+
 // ------------------------------ conv2 data gradient, persistent pipeline
-// Same mathematics as Conv2Dgrad (C = W2^T G2, then col2im), reorganised so
-// one CTA per SM streams many image pairs through a pipeline:
+// dp1 = col2im(W2^T G2) as the GEMM
+//   C[(c,i,j), (n,p)] = sum_f W2[f,c,i,j] G2[n,f,p]
+// followed by the col2im gather, organised so one CTA per SM streams many
+// image pairs through a pipeline:
 //   warp 0      producer: W2t tile once (TMA), G2 pairs (bulk copy, 2 buffers)
 //   warp 1      MMA: 8 x tcgen05.mma (M=128 rows (c,i,j), N=128 (2 images x
 //               64 positions), K=64 f) per pair into one of 2 TMEM accumulators
@@ -886,10 +941,10 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
 // Once per forward (weights change only in SGD), TF32-rounded copies of the
 // weights in the layouts the GEMMs consume, zero padded:
 //   W1f [500][800]  = W1                      (ip1 fwd B)
-//   W2f [64][512]   = W2 [f][(c,i,j)]         (conv2 fwd B)
+//   W2c [25 taps][5 cc][50 f][4 c] = W2[f, 4cc + c, tap]   (conv2 fwd B)
 //   W2t [4][128][64]: W2t[m][r][f] = W2[f, 5m + r/25, tap r%25]  (conv2 dgrad A)
 //   W1t [800][512]  = W1^T                    (ip1 dgrad B; tiled transpose)
-constexpr int W1F_N = 500 * 800, W2F_N = 64 * 512, W2T_N = 4 * 128 * 64;
+constexpr int W1F_N = 500 * 800, W2C_N = 25 * 5 * 50 * 4, W2T_N = 4 * 128 * 64;
 __global__ void pack_weights(const __grid_constant__ PackP p) {
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx < W1F_N) {
@@ -897,18 +952,41 @@ __global__ void pack_weights(const __grid_constant__ PackP p) {
     return;
   }
   idx -= W1F_N;
-  if (idx < W2F_N) {
-    const int f = idx >> 9, k = idx & 511;
-    p.w2f[idx] = (f < 50 && k < 500) ? tf32f(p.w2[f * 500 + k]) : 0.f;
+  if (idx < W2C_N) {
+    const int c4 = idx & 3, f = (idx >> 2) % 50, cc = (idx / 200) % 5, tap = idx / 1000;
+    p.w2c[idx] = tf32f(p.w2[f * 500 + (cc * 4 + c4) * 25 + tap]);
     return;
   }
-  idx -= W2F_N;
+  idx -= W2C_N;
   if (idx < W2T_N) {
     const int f = idx & 63, r = (idx >> 6) & 127, m = idx >> 13;
     float v = 0.f;
     if (f < 50 && r < 125) v = p.w2[f * 500 + (5 * m + r / 25) * 25 + r % 25];
     p.w2t[idx] = tf32f(v);
   }
+}
+// p1c (conv2 forward operand, see conv2_fwd_persistent) from an NCHW pool1
+// blob, TF32-rounded: used when pool1 is overwritten through the ABI (the
+// forward pass writes p1c directly from conv1+pool1).
+struct PackP1cArgs {
+  const float* p1;
+  float* p1c;
+  int N;
+};
+__global__ void pack_p1c_k(const __grid_constant__ PackP1cArgs a) {
+  const float* p1 = a.p1;
+  float* p1c = a.p1c;
+  const int N = a.N;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // one 4-channel pixel
+  const long long npairs = (N + 1) / 2;
+  if (idx >= npairs * 5 * 288) return;
+  const int pair = (int)(idx / 1440), rem = (int)(idx % 1440);
+  const int cc = rem / 288, hnw = rem % 288, h = hnw / 24, nw = hnw % 24, nin = nw / 12, w = nw % 12;
+  const int n = 2 * pair + nin;
+  float v[4] = {0.f, 0.f, 0.f, 0.f};
+  if (n < N)
+    for (int t = 0; t < 4; ++t) v[t] = tf32f(p1[((size_t)n * 20 + cc * 4 + t) * 144 + h * 12 + w]);
+  reinterpret_cast<float4*>(p1c)[idx] = make_float4(v[0], v[1], v[2], v[3]);
 }
 // W1t[k][o] = W1[o][k] (o < 500), 32x32 tiles through shared memory
 __global__ void transpose_w1(const __grid_constant__ PackP p) {
@@ -984,14 +1062,15 @@ static cudaError_t opt_in() {
 cudaError_t setup() {
   if (!encode_fn()) return cudaErrorNotSupported;
   cudaError_t e;
-  if ((e = opt_in<Conv2Fwd>()) != cudaSuccess) return e;
   if ((e = opt_in<IpFwd>()) != cudaSuccess) return e;
   if ((e = opt_in<IpWgrad>()) != cudaSuccess) return e;
   if ((e = opt_in<IpDgradUnpool>()) != cudaSuccess) return e;
-  if ((e = opt_in<Conv2Dgrad>()) != cudaSuccess) return e;
   if ((e = opt_in<Conv2Wgrad>()) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute((const void*)conv2_dgrad_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 dg::SMEM)) != cudaSuccess)
+    return e;
+  if ((e = cudaFuncSetAttribute((const void*)conv2_fwd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                cf::SMEM)) != cudaSuccess)
     return e;
   return cudaSuccess;
 }
@@ -1002,7 +1081,7 @@ static unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) /
 
 Launch pack_weights_launch(const PackP& p) {
   Launch l;
-  l.set((const void*)pack_weights, dim3(cdiv(W1F_N + W2F_N + W2T_N, 256)), dim3(256), 0, p);
+  l.set((const void*)pack_weights, dim3(cdiv(W1F_N + W2C_N + W2T_N, 256)), dim3(256), 0, p);
   return l;
 }
 
@@ -1012,11 +1091,22 @@ Launch transpose_w1_launch(const PackP& p) {
   return l;
 }
 
-Launch conv2_pool2_launch(const float* w2f, const float* b, const float* p1, float* p2, float* p2T, uint8_t* m2,
-                          int N, int npad) {
+Launch conv2_pool2_launch(const float* w2c, const float* b, const float* p1c, float* p2, float* p2T, uint8_t* m2,
+                          int N, int npad, int sms) {
   Launch l;
-  Conv2Fwd::Params p{tmap2d(w2f, 64, 512, 512, 64), p1, b, p2, p2T, m2, N, npad};
-  l.set((const void*)tc_gemm<Conv2Fwd>, dim3(cdiv(N, 2)), dim3(THREADS), smem_bytes<Conv2Fwd>(), p);
+  // pairs split evenly: ceil(pairs / sms) per CTA, as few CTAs as that needs
+  // (every CTA loads the 100 KB of weights once)
+  const int pairs = (N + 1) / 2, per = std::max(1, (pairs + sms - 1) / sms);
+  cf::Params p{w2c, p1c, b, p2, p2T, m2, N, npad, per};
+  l.set((const void*)conv2_fwd_persistent, dim3(std::max(1, (pairs + per - 1) / per)), dim3(cf::THREADS_F), cf::SMEM,
+        p);
+  return l;
+}
+
+Launch pack_p1c_launch(const float* p1, float* p1c, int N) {
+  Launch l;
+  PackP1cArgs a{p1, p1c, N};
+  l.set((const void*)pack_p1c_k, dim3(cdiv((long long)((N + 1) / 2) * 1440, 256)), dim3(256), 0, a);
   return l;
 }
 

@@ -17,17 +17,20 @@ struct PackP {
   const float* w2;  // [50][500]
   float* w1f;       // [500][800]
   float* w1t;       // [800][512]
-  float* w2f;       // [64][512]
+  float* w2c;       // [25 taps][5][50][4] (conv2 fwd B)
   float* w2t;       // [4][128][64]
 };
-constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2fFloats = 64 * 512, kW2tFloats = 4 * 128 * 64;
+constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2cFloats = 25000, kW2tFloats = 4 * 128 * 64;
 
 cudaError_t setup();    // driver entry point + opt-in shared memory sizes
 bool tensor_maps_ok();  // false if any cuTensorMapEncodeTiled call failed
 Launch pack_weights_launch(const PackP& p);
 Launch transpose_w1_launch(const PackP& p);
-Launch conv2_pool2_launch(const float* w2f, const float* b, const float* p1, float* p2, float* p2T, uint8_t* m2,
-                          int N, int npad);
+// conv2 forward operand layout p1c: per image pair [5 cc][12 h][2 n][12 w][4 c] floats
+constexpr int kP1cPairFloats = 5 * 12 * 2 * 12 * 4;
+Launch conv2_pool2_launch(const float* w2c, const float* b, const float* p1c, float* p2, float* p2T, uint8_t* m2,
+                          int N, int npad, int sms);
+Launch pack_p1c_launch(const float* p1, float* p1c, int N);
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N);
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,

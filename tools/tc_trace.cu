@@ -1,0 +1,66 @@
+// tc_trace.cu -- dev harness: time conv2_fwd_persistent alone on random data
+// and dump per-CTA timeline stamps (tc.cu stamp()).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DPN_TRACE -I paper_2005_13076_b200/csrc \
+//        -o tools/tc_trace tools/tc_trace.cu -lcuda
+#include "../paper_2005_13076_b200/csrc/tc.cu"
+
+#include <cstdio>
+#include <vector>
+
+using namespace pn;
+using namespace pn::tc;
+
+int main(int argc, char** argv) {
+  const int N = argc > 1 ? atoi(argv[1]) : 512;
+  const int npairs = (N + 1) / 2, npad = (N + 3) & ~3;
+  float *w2c, *p1c, *b, *p2, *p2T;
+  uint8_t* m2;
+  cudaMalloc(&w2c, kW2cFloats * 4);
+  cudaMalloc(&p1c, (size_t)npairs * kP1cPairFloats * 4);
+  cudaMalloc(&b, 64 * 4);
+  cudaMalloc(&p2, (size_t)N * 800 * 4);
+  cudaMalloc(&p2T, (size_t)800 * npad * 4);
+  cudaMalloc(&m2, (size_t)N * 800);
+  cudaMemset(w2c, 0, kW2cFloats * 4);
+  cudaMemset(p1c, 0, (size_t)npairs * kP1cPairFloats * 4);
+  cudaMemset(b, 0, 256);
+  if (setup() != cudaSuccess) { printf("setup failed\n"); return 1; }
+  Launch l = conv2_pool2_launch(w2c, b, p1c, p2, p2T, m2, N, npad, 148);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  for (int i = 0; i < 5; ++i) l.launch(st);
+  if (argc > 2) {  // single cold-ish launch for the trace: evict L2 with a 256 MB memset first
+    void* big;
+    cudaMalloc(&big, 256 << 20);
+    cudaMemsetAsync(big, 0, 256 << 20, st);
+    l.launch(st);
+    cudaStreamSynchronize(st);
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int R = 50;
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < R; ++i) l.launch(st);
+  cudaEventRecord(e1, st);
+  cudaStreamSynchronize(st);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("conv2_fwd_persistent N=%d: %.2f us/launch (%s)\n", N, ms * 1000 / R, cudaGetErrorString(cudaGetLastError()));
+#ifdef PN_TRACE
+  std::vector<unsigned long long> t(148 * 16);
+  cudaMemcpyFromSymbol(t.data(), g_trace, t.size() * 8);
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < 148; ++c)
+    if (t[c * 16]) t0 = std::min(t0, t[c * 16]);
+  printf("cta   start  pair0  pair1   wts0    wts   acc0   acc1  tmemld  Cdone  pooled  epiend  end   (ns from first start)\n");
+  const int ncta = l.grid.x;
+  for (int c = 0; c < ncta; c += (ncta + 9) / 10) {
+    printf("%3d", c);
+    const int ks[] = {0, 1, 2, 14, 5, 6, 7, 11, 12, 13, 15, 10};
+    for (int k : ks) printf(" %6lld", t[c * 16 + k] ? (long long)(t[c * 16 + k] - t0) : -1ll);
+    printf("\n");
+  }
+#endif
+  return 0;
+}
