@@ -1,6 +1,7 @@
 // kernels.h -- declarations of every __global__ kernel of the library.
 #pragma once
 #include "params.h"
+#include "pdl.cuh"
 
 namespace pn {
 // generic per-layer kernels (kernels_generic.cu)

@@ -38,6 +38,7 @@ __device__ __forceinline__ float block_sum(float v, float* sm) {
 // each output is the inner product of a filter with one sliding
 // window (cross-correlation, R1); bias after the sum (Listing 1).
 __global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.N * p.F * p.Ho * p.Wo;
   if (idx >= total) return;
@@ -65,6 +66,7 @@ __global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p) {
 
 // col2im(W^T dy) evaluated per input element (gather form).
 __global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.N * p.C * p.H * p.W;
   if (idx >= total) return;
@@ -97,6 +99,7 @@ __global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p) {
 // grid = (F*C, splits), block = 256.
 __global__ void __launch_bounds__(256) conv_bwd_weight_generic(
     const __grid_constant__ ConvBwdWeightP p) {
+  pdl_enter();
   __shared__ float sm[32];
   const int f = blockIdx.x / p.C, c = blockIdx.x % p.C, s = blockIdx.y;
   const int n0 = (int)((long long)p.N * s / p.splits);
@@ -142,6 +145,7 @@ __global__ void __launch_bounds__(256) conv_bwd_weight_generic(
 }
 
 __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
+  pdl_enter();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   float acc = 0.f;
@@ -155,6 +159,7 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
 // sums in order -- a fixed order, so reruns are bitwise identical.
 // p.total = number of 32-output blocks over all segments.
 __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_constant__ ReduceMultiP p) {
+  pdl_enter();
   __shared__ float sm[8][33];
   int b = blockIdx.x, k = 0;
   while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
@@ -178,6 +183,7 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
 // P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
 // a row-major scan (strict >) and stores its plane-local index h*W+w.
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.N * p.C * p.Hp * p.Wp;
   if (idx >= total) return;
@@ -216,6 +222,7 @@ __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
 // each input sums the output gradients routed to it, in ascending
 // output order (the oracle's scatter order) -- no atomics.
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.N * p.C * p.H * p.W;
   if (idx >= total) return;
@@ -250,6 +257,7 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
 // 64x64 tile, BK 16, 256 threads x (4x4) outputs; arbitrary strides so one
 // kernel serves ip fwd (x W^T), dgrad (dy W) and wgrad (dy^T x).
 __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ GemmP p) {
+  pdl_enter();
   __shared__ float As[16][64 + 4];
   __shared__ float Bs[16][64 + 4];
   const int tid = threadIdx.x;
@@ -303,6 +311,7 @@ __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ Gemm
 
 // db[n] = sum_m dy[m, n] (InnerProduct bias gradient)
 __global__ void __launch_bounds__(256) colsum_generic(const __grid_constant__ ColSumP p) {
+  pdl_enter();
   __shared__ float sm[32];
   const int n = blockIdx.x;
   float acc = 0.f;
@@ -313,6 +322,7 @@ __global__ void __launch_bounds__(256) colsum_generic(const __grid_constant__ Co
 
 // --------------------------------------------------------------------- ReLU
 __global__ void relu_fwd_generic(const __grid_constant__ ReluP p) {
+  pdl_enter();
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   float v = p.x[i];
@@ -321,6 +331,7 @@ __global__ void relu_fwd_generic(const __grid_constant__ ReluP p) {
 
 // dX = dY * (y > 0 ? 1 : slope), y = in-place forward output (R8)
 __global__ void relu_bwd_generic(const __grid_constant__ ReluP p) {
+  pdl_enter();
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
   float g = p.x[i];
@@ -331,6 +342,7 @@ __global__ void relu_bwd_generic(const __grid_constant__ ReluP p) {
 // One warp per sample: stable softmax, per-row loss term, lowest-index
 // argmax, and the loss gradient (p - onehot) * loss_weight / M.
 __global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= p.M) return;
@@ -368,6 +380,7 @@ __global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p) {
 
 // loss = (1/M) sum_i row_loss[i], fixed-order block reduction (one block)
 __global__ void __launch_bounds__(256) loss_reduce(const __grid_constant__ LossReduceP p) {
+  pdl_enter();
   __shared__ float sm[32];
   float acc = 0.f;
   for (int i = threadIdx.x; i < p.M; i += blockDim.x) acc += p.row_loss[i];
@@ -390,6 +403,7 @@ __device__ __forceinline__ void sgd_one(float& w, float d, float& v, float lr, f
 }
 
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
+  pdl_enter();
   long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long n4 = p.n / 4;
   for (; i4 < n4; i4 += (long long)gridDim.x * blockDim.x) {
@@ -416,6 +430,7 @@ __global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
 // The fused plan stores the max-pool origin as a uint8 offset inside the
 // (clipped) window: (h - hs)*kw + (w - ws).  The ABI view is int32 h*W + w.
 __global__ void mask_convert(const __grid_constant__ MaskExpandP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long total = (long long)p.N * p.C * p.Hp * p.Wp;
   if (idx >= total) return;
@@ -438,6 +453,7 @@ namespace pn {
 // plan's operand buffers; used when a caller overwrites a blob (net_put_blob)
 // so the internal operand copies stay consistent with it.
 __global__ void tf32_copy(const __grid_constant__ Tf32CopyP p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (long long)p.R * p.C) return;
   const int r = (int)(idx / p.C), c = (int)(idx % p.C);

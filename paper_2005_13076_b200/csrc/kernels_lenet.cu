@@ -20,6 +20,7 @@ namespace pn {
 // values of 25 MACs).  Ties: first of (0,0),(0,1),(1,0),(1,1).
 constexpr int C1_IMGS = 2;
 __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+  pdl_enter();
   __shared__ float xs[C1_IMGS][28 * 28];
   __shared__ __align__(16) float ws[20][28];
   __shared__ float bs[20];
@@ -86,6 +87,7 @@ constexpr int C2_IMGS = 2;
 constexpr int C2_THREADS = 320;
 __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
     const __grid_constant__ Conv2Pool2P p) {
+  pdl_enter();
   extern __shared__ __align__(16) float smem[];
   float* ws = smem;                    // [50][20][28]
   float* xs = smem + 50 * 20 * 28;     // [2][20][144]
@@ -163,6 +165,7 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
 // stable softmax, per-row loss term, lowest-index argmax and the loss
 // gradient dz = (p - onehot) * loss_weight / M.
 __global__ void __launch_bounds__(256) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
+  pdl_enter();
   __shared__ __align__(16) float ws[10 * 500];
   __shared__ float bs[10];
   for (int i = threadIdx.x; i < 5000; i += blockDim.x) ws[i] = __ldg(p.w + i);
@@ -221,6 +224,7 @@ __global__ void __launch_bounds__(256) lenet_ip2_loss(const __grid_constant__ Ip
 // da1[m,k] = (a1[m,k] > 0) * sum_o dz[m,o] W2[o,k]   (S:387 + S:405)
 // partial dW2[o,k] = sum_{m in split} dz[m,o] a1[m,k];  partial db2[o].
 __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p) {
+  pdl_enter();
   const int k = blockIdx.x * 128 + threadIdx.x;
   const int s = blockIdx.y;
   const int m0 = (int)((long long)p.N * s / p.splits), m1 = (int)((long long)p.N * (s + 1) / p.splits);
@@ -272,6 +276,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
 // dp2 [N, 50*16] + mask -> dense conv2 output gradient G2 [N,50,8,8]
 // (max-pool backward: each gradient goes to its stored origin).
 __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
+  pdl_enter();
   long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;  // over N*50*64
   if (idx >= (long long)p.N * 3200) return;
   const int pos = idx % 64;
@@ -292,6 +297,7 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // global loads per thread are in flight together.
 constexpr int CW_IMGS = 4;
 __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
+  pdl_enter();
   __shared__ float xs[CW_IMGS][784];
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);

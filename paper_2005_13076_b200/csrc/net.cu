@@ -410,6 +410,8 @@ static pn_status allocate(pn_net* net) {
     // conv1's fused weight gradient is a light SIMT kernel: give it more
     // CTAs (4 images each at batch 512)
     L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 3) / 4 : kWgradSplits;
+    // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
+    if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
   }

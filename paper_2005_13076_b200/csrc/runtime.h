@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -40,9 +41,27 @@ struct Launch {
   P& params() {
     return *reinterpret_cast<P*>(arg.data());
   }
+  // every launch allows programmatic dependent launch (pdl.cuh) unless PN_PDL=0
+  static bool pdl() {
+    static const bool on = [] {
+      const char* e = getenv("PN_PDL");
+      return !(e && e[0] == '0');
+    }();
+    return on;
+  }
   cudaError_t launch(cudaStream_t st) {
     void* a[1] = {arg.data()};
-    return cudaLaunchKernel(func, grid, block, a, smem, st);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl() ? 1 : 0;
+    return cudaLaunchKernelExC(&cfg, func, a);
   }
 };
 

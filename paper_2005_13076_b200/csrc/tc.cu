@@ -28,6 +28,7 @@
 #include <cstdint>
 #include <cstring>
 
+#include "pdl.cuh"
 #include "tc.h"
 
 namespace pn {
@@ -205,6 +206,7 @@ __device__ __forceinline__ int gtid() { return (int)threadIdx.x - GATHER_T0; }
 
 template <class Op>
 __global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typename Op::Params prm) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the swizzle atoms (dynamic smem base is only 16-B aligned)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -472,79 +474,6 @@ struct IpDgradUnpool : OpBase {
   }
 };
 
-// ------------------------------------------------ conv2 weight gradient
-// dW2[f,(c,i,j)] = sum_{n,p} G2[n,f,p] p1[n,c,ho+i,wo+j]; rows (c,i,j) 500 of
-// 512 (4 tiles), cols f (50 of 64), K = (n in this split, p): 2 chunks per
-// image.  Images (TF32) are bulk-copied into a 2-slot ring one image ahead
-// and A is gathered from them; B = G2 rows f (TF32) by TMA (3D map
-// {p, f, n}).  Writes split partials [split][f*500 + k].
-struct Conv2Wgrad : OpBase {
-  struct Params {
-    CUtensorMap tb;  // G2 as {64 p, 50 f, N n}
-    const float* p1;
-    float* part;
-    int N, splits, pstride;
-  };
-  static constexpr int BN = 64, TMEM_COLS = 64, STAGES = 4;
-  static constexpr bool A_TMA = false, B_TMA = true;
-  // image ring: the producer may run STAGES chunks ahead of the MMA while the
-  // gatherers still read the image of the oldest unfinished chunk
-  static constexpr int SLOTS = STAGES / 2 + 1;
-  static constexpr int STAGE_BYTES = SLOTS * 2880 * 4 + SLOTS * 8;
-  const Params& p;
-  uint32_t img_s, ibar_s;  // SLOTS image slots, SLOTS barriers
-  uint32_t row_s;          // this thread's row (c,i,j) base inside a slot
-  int kw0, n0, n1;
-  bool rvalid;
-  __device__ Conv2Wgrad(const Params& q, uint8_t* st, uint8_t*) : p(q) {
-    img_s = smem_u32(st);
-    ibar_s = img_s + SLOTS * 2880 * 4;
-    kw0 = blockIdx.x * BM;
-    n0 = (int)((long long)q.N * blockIdx.y / q.splits);
-    n1 = (int)((long long)q.N * (blockIdx.y + 1) / q.splits);
-    const int kw = kw0 + (gtid() & 127);
-    rvalid = kw < 500;
-    const int c = kw / 25, rem = kw - c * 25, i = rem / 5, j = rem - i * 5;
-    row_s = img_s + 4 * (c * 144 + i * 12 + j);
-  }
-  __device__ int num_k_chunks() const { return (n1 - n0) * 2; }
-  __device__ void init_barriers() {
-    for (int i = 0; i < SLOTS; ++i) mbar_init(ibar_s + 8 * i, 1);
-  }
-  __device__ void prefetch() { prefetch_tmap(&p.tb); }
-  __device__ uint32_t tx_bytes(int) const { return BN * BK * 4; }
-  __device__ void issue(int c, uint32_t, uint32_t Bs, uint32_t bar) {
-    tma3d(Bs, &p.tb, (c & 1) * BK, 0, n0 + (c >> 1), bar);
-    if ((c & 1) == 0) {  // next image into its ring slot
-      const int im = c >> 1, slot = im % SLOTS;
-      const uint32_t ib = ibar_s + 8 * slot;
-      mbar_expect_tx(ib, 2880 * 4);
-      bulk_g2s(img_s + slot * 2880 * 4, p.p1 + (size_t)(n0 + im) * 2880, 2880 * 4, ib);
-    }
-  }
-  __device__ void before_gather(int kb) {
-    const int im = kb >> 1;
-    if ((kb & 1) == 0) mbar_wait(ibar_s + 8 * (im % SLOTS), (im / SLOTS) & 1);
-  }
-  __device__ float4 a(int, int k) const {
-    if (!rvalid) return zero4();
-    const int im = k >> 6, pos = k & 63, ho = pos >> 3, wo = pos & 7;
-    const uint32_t s = row_s + 4 * ((im % SLOTS) * 2880 + ho * 12 + wo);
-    return f4(ldsf(s), ldsf(s + 4), ldsf(s + 8), ldsf(s + 12));
-  }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const int kw = kw0 + row;
-    if (kw >= 500) return;
-    float* dst = p.part + (size_t)blockIdx.y * p.pstride;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const int f = c0 + j;
-      if (f >= 50) break;
-      dst[f * 500 + kw] = v[j];
-    }
-  }
-};
-
 // ------------------------- conv2 + bias + pool2 (+mask), persistent tap GEMM
 // conv2 as 25 tap GEMMs accumulated in TMEM, with NO im2col:
 //   D[(ho,n,wo), f] = sum_{i,j} sum_c p1[n,c,ho+i,wo+j] W2[f,c,i,j]
@@ -654,8 +583,16 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   if (tid == 0) {
-    // ---- producer: the first pair, the weights in 5 pieces (taps of one
-    // kernel row each), then the remaining pairs
+    // ---- producer: the weights in 5 pieces (taps of one kernel row each;
+    // packed two launches back, so readable before the PDL wait), then -- once
+    // conv1+pool1 has completed -- the pairs
+    if (mine > 0)
+      for (int i = 0; i < 5; ++i) {
+        mbar_expect_tx(smem_u32(&wbar[i]), 5 * TAP_BYTES);
+        bulk_g2s(B_s + i * 5 * TAP_BYTES, (const uint8_t*)p.w2c + i * 5 * TAP_BYTES, 5 * TAP_BYTES,
+                 smem_u32(&wbar[i]));
+      }
+    pdl_enter();
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
       const int s = it % STAGES;
@@ -663,12 +600,6 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
       mbar_expect_tx(smem_u32(&full[s]), A_GLOBAL);
       bulk_g2s(A_s + s * A_BYTES, (const uint8_t*)p.p1c + (size_t)(pair0 + it) * A_GLOBAL, A_GLOBAL,
                smem_u32(&full[s]));
-      if (it == 0)
-        for (int i = 0; i < 5; ++i) {
-          mbar_expect_tx(smem_u32(&wbar[i]), 5 * TAP_BYTES);
-          bulk_g2s(B_s + i * 5 * TAP_BYTES, (const uint8_t*)p.w2c + i * 5 * TAP_BYTES, 5 * TAP_BYTES,
-                   smem_u32(&wbar[i]));
-        }
     }
   } else if (tid == 32) {
     // ---- MMA issuer
@@ -796,6 +727,7 @@ struct Params {
 }  // namespace dg
 
 __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const __grid_constant__ dg::Params p) {
+  pdl_enter();
   using namespace dg;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -937,6 +869,178 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
   if (warp == 0) tmem_dealloc(tbase, 256);
 }
 
+// ------------------------------------- conv2 weight gradient, persistent
+// dW2[f,(c,i,j)] = sum_{n,p} G2[n,f,p] p1[n,c,ho+i,wo+j] as the GEMM
+//   D[(c,i,j), f] = sum_K A[(c,i,j), K] G2[f, K],  K = (image n, position p)
+// rows (c,i,j) 500 in 4 tiles of 128, N = 64 (f 50 + TMA zero fill), split
+// over images: grid (4 row tiles, S image ranges), one CTA per SM.  The
+// sliding window runs along the contraction (K-major only for TF32), so A is
+// materialised per image -- but from registers: one thread per (c, i, ho)
+// loads the input row p1[n,c,ho+i,0..11] (3 x 16 B) and writes the 5 j-shifted
+// 8-wide windows (10 x 16 B) into the SW128 K-major A tile.
+//   warp 0      producer: per image, the tile's <= 6 input channels (bulk
+//               copy) and G2[n] (TMA 3D, 2 x {32 p, 64 f}), 3-slot ring
+//   warp 1      MMA: 8 x tcgen05.mma (M=128, N=64, K=8) per image, one TMEM
+//               accumulator over the CTA's images
+//   warps 2-9   A builders (2 A buffers); warps 2-5 then drain TMEM into the
+//               split's partial sums part[split][f*500 + (c,i,j)]
+namespace wg {
+constexpr int WARPS = 10, THREADS_W = WARPS * 32, NB = 256;  // A builder threads
+constexpr int A_BYTES = 2 * 128 * 128;   // 2 K-chunks (32 positions each) x 128 rows x 128 B
+constexpr int G_BYTES = 2 * 64 * 128;    // 2 K-chunks x 64 f rows x 128 B
+constexpr int P_BYTES = 6 * 144 * 4;     // <= 6 input channels of one image
+constexpr int SLOTS = 3;
+constexpr int SMEM = 2 * A_BYTES + SLOTS * G_BYTES + SLOTS * P_BYTES + 1024;
+struct Params {
+  CUtensorMap tg;  // G2 as {64 p, 50 f, N n}
+  const float* p1;
+  float* part;
+  int N, splits, pstride;
+};
+}  // namespace wg
+
+__global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const __grid_constant__ wg::Params p) {
+  using namespace wg;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t A_s = smem_u32(smem), G_s = A_s + 2 * A_BYTES, P_s = G_s + SLOTS * G_BYTES;
+  __shared__ __align__(8) uint64_t full[SLOTS], sfree[SLOTS], afull[2], afree[2], done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int m = blockIdx.x, split = blockIdx.y;
+  const int n0 = (int)((long long)p.N * split / p.splits), n1 = (int)((long long)p.N * (split + 1) / p.splits);
+  const int nimg = n1 - n0;
+  // (c,i) pairs and input channels this row tile touches
+  const int R0 = 128 * m, P_lo = R0 / 5, P_hi = min(R0 + 127, 499) / 5, NP = P_hi - P_lo + 1;
+  const int c_lo = P_lo / 5, nch = P_hi / 5 - c_lo + 1;
+  if (tid == 0) {
+    for (int s = 0; s < SLOTS; ++s) {
+      mbar_init(smem_u32(&full[s]), 1);
+      mbar_init(smem_u32(&sfree[s]), NB + 1);  // builders done with P + MMA done with G
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&afull[b]), NB);
+      mbar_init(smem_u32(&afree[b]), 1);
+    }
+    mbar_init(smem_u32(&done), 1);
+    fence_barrier_init();
+    prefetch_tmap(&p.tg);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, 64);
+  // rows no builder writes (tile 3 beyond row 499) stay zero
+  for (int i = tid; i < 2 * A_BYTES / 16; i += THREADS_W) sts128(A_s + 16 * i, zero4());
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  if (tid == 0) {
+    // ---- producer (G2 and p1 come from the two preceding launches' producers:
+    // wait for the immediate predecessor first)
+    pdl_enter();
+    const uint32_t bytes = nch * 576 + G_BYTES;
+#pragma unroll 1
+    for (int t = 0; t < nimg; ++t) {
+      const int s = t % SLOTS, n = n0 + t;
+      if (t >= SLOTS) mbar_wait(smem_u32(&sfree[s]), ((t / SLOTS) - 1) & 1);
+      const uint32_t bar = smem_u32(&full[s]);
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(P_s + s * P_BYTES, p.p1 + (size_t)n * 2880 + c_lo * 144, nch * 576, bar);
+      tma3d(G_s + s * G_BYTES, &p.tg, 0, 0, n, bar);
+      tma3d(G_s + s * G_BYTES + 64 * 128, &p.tg, 32, 0, n, bar);
+    }
+  } else if (tid == 32) {
+    // ---- MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, 64);
+#pragma unroll 1
+    for (int t = 0; t < nimg; ++t) {
+      const int s = t % SLOTS, b = t & 1;
+      mbar_wait(smem_u32(&full[s]), (t / SLOTS) & 1);
+      mbar_wait(smem_u32(&afull[b]), (t >> 1) & 1);
+      tc_fence_after();
+      const uint32_t Ab = A_s + b * A_BYTES, Gb = G_s + s * G_BYTES;
+#pragma unroll
+      for (int kc = 0; kc < 2; ++kc)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          mma_tf32(tbase, make_desc(Ab + kc * 16384 + k * 32), make_desc(Gb + kc * 8192 + k * 32), idesc,
+                   (t | kc | k) != 0);
+      mma_commit(smem_u32(&afree[b]));
+      mma_commit(smem_u32(&sfree[s]));
+    }
+    mma_commit(smem_u32(&done));
+  } else if (warp >= 2) {
+    // ---- A builders: item g = (pair P_lo + g % NP, ho = g / NP); lanes with
+    // consecutive pairs write rows 5 apart (distinct swizzle phases)
+    const int g = tid - 64;
+    const bool active = g < NP * 8;
+    const int P = P_lo + g % NP, ho = g / NP, c = P / 5, i = P - 5 * (P / 5);
+    const uint32_t src_off = 4 * ((c - c_lo) * 144 + (ho + i) * 12);
+    const int r0 = 5 * P - R0;  // tile row of j = 0
+    const uint32_t dst_off = (ho >> 2) * 16384;
+    const int q0 = (ho & 3) * 2;
+#pragma unroll 1
+    for (int t = 0; t < nimg; ++t) {
+      const int s = t % SLOTS, b = t & 1;
+      mbar_wait(smem_u32(&full[s]), (t / SLOTS) & 1);
+      if (t >= 2) mbar_wait(smem_u32(&afree[b]), ((t >> 1) - 1) & 1);
+      if (active) {
+        float x[12];
+        const uint32_t src = P_s + s * P_BYTES + src_off;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+          const int4 v = lds_i4(src + 16 * u);
+          x[4 * u] = __int_as_float(v.x);
+          x[4 * u + 1] = __int_as_float(v.y);
+          x[4 * u + 2] = __int_as_float(v.z);
+          x[4 * u + 3] = __int_as_float(v.w);
+        }
+        const uint32_t Ab = A_s + b * A_BYTES + dst_off;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const int r = r0 + j;
+          if (r >= 0 && r < 128 && 5 * P + j < 500) {
+            sts128(Ab + sw_off(r, q0), f4(x[j], x[j + 1], x[j + 2], x[j + 3]));
+            sts128(Ab + sw_off(r, q0 + 1), f4(x[j + 4], x[j + 5], x[j + 6], x[j + 7]));
+          }
+        }
+      }
+      fence_proxy_async();
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sfree[s])) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&afull[b])) : "memory");
+    }
+    // ---- epilogue (warps 2-5): TMEM lane quadrant warp % 4 -> rows; the
+    // split's partial dW2[f][(c,i,j)] (coalesced over rows)
+    if (warp < 6) {
+      const int quad = warp & 3, row = quad * 32 + lane, R = R0 + row;
+      float* dst = p.part + (size_t)split * p.pstride;
+      if (nimg > 0) {
+        mbar_wait(smem_u32(&done), 0);
+        __syncwarp();
+        tc_fence_after();
+      }
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+        float v[16];
+        if (nimg > 0) {
+          tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + c0, v);
+        } else {
+#pragma unroll
+          for (int u = 0; u < 16; ++u) v[u] = 0.f;
+        }
+        if (R < 500) {
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            if (c0 + u < 50) dst[(c0 + u) * 500 + R] = v[u];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 64);
+}
+
 // --------------------------------------------------------- weight packing
 // Once per forward (weights change only in SGD), TF32-rounded copies of the
 // weights in the layouts the GEMMs consume, zero padded:
@@ -946,6 +1050,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
 //   W1t [800][512]  = W1^T                    (ip1 dgrad B; tiled transpose)
 constexpr int W1F_N = 500 * 800, W2C_N = 25 * 5 * 50 * 4, W2T_N = 4 * 128 * 64;
 __global__ void pack_weights(const __grid_constant__ PackP p) {
+  pdl_enter();
   int idx = blockIdx.x * blockDim.x + threadIdx.x;
   if (idx < W1F_N) {
     p.w1f[idx] = tf32f(p.w1[idx]);
@@ -974,6 +1079,7 @@ struct PackP1cArgs {
   int N;
 };
 __global__ void pack_p1c_k(const __grid_constant__ PackP1cArgs a) {
+  pdl_enter();
   const float* p1 = a.p1;
   float* p1c = a.p1c;
   const int N = a.N;
@@ -990,6 +1096,7 @@ __global__ void pack_p1c_k(const __grid_constant__ PackP1cArgs a) {
 }
 // W1t[k][o] = W1[o][k] (o < 500), 32x32 tiles through shared memory
 __global__ void transpose_w1(const __grid_constant__ PackP p) {
+  pdl_enter();
   __shared__ float t[32][33];
   const int k0 = blockIdx.x * 32, o0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
@@ -1065,7 +1172,9 @@ cudaError_t setup() {
   if ((e = opt_in<IpFwd>()) != cudaSuccess) return e;
   if ((e = opt_in<IpWgrad>()) != cudaSuccess) return e;
   if ((e = opt_in<IpDgradUnpool>()) != cudaSuccess) return e;
-  if ((e = opt_in<Conv2Wgrad>()) != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute((const void*)conv2_wgrad_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                wg::SMEM)) != cudaSuccess)
+    return e;
   if ((e = cudaFuncSetAttribute((const void*)conv2_dgrad_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 dg::SMEM)) != cudaSuccess)
     return e;
@@ -1146,8 +1255,8 @@ Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, 
 
 Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N) {
   Launch l;
-  Conv2Wgrad::Params p{tmap_g2(g2, N), p1, part, N, splits, 25050};
-  l.set((const void*)tc_gemm<Conv2Wgrad>, dim3(4, splits), dim3(THREADS), smem_bytes<Conv2Wgrad>(), p);
+  wg::Params p{tmap_g2(g2, N), p1, part, N, splits, 25050};
+  l.set((const void*)conv2_wgrad_persistent, dim3(4, splits), dim3(wg::THREADS_W), wg::SMEM, p);
   return l;
 }
 

@@ -14,7 +14,8 @@ for r in rows:
 seen = {}
 for k, v in out:
     seen.setdefault(k, []).append(v)
-steps = max(len(v) for v in seen.values())
+# one SGD update per step
+steps = next((len(v) for k, v in seen.items() if 'sgd_update' in k), max(len(v) for v in seen.values()))
 tot = 0.0
 for k, v in sorted(seen.items(), key=lambda kv: -sorted(kv[1])[len(kv[1]) // 2] * len(kv[1])):
     m = sorted(v)[len(v) // 2]
