@@ -20,7 +20,8 @@ namespace pn {
 // values of 25 MACs).  Ties: first of (0,0),(0,1),(1,0),(1,1).
 constexpr int C1_IMGS = 2;
 __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
-  pdl_enter();
+  // inputs (the batch) and weights (previous step's SGD) are complete at
+  // launch (pdl.cuh): stage them before waiting on the predecessor
   __shared__ float xs[C1_IMGS][28 * 28];
   __shared__ __align__(16) float ws[20][28];
   __shared__ float bs[20];
@@ -34,6 +35,7 @@ __global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__
     ws[f][t] = t < 25 ? __ldg(p.w + f * 25 + t) : 0.f;
   }
   if (threadIdx.x < 20) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
+  pdl_enter();
   __syncthreads();
   for (int it = threadIdx.x; it < C1_IMGS * 720; it += blockDim.x) {
     const int im = it / 720, r = it % 720, g = r / 144, q = r % 144;
@@ -161,27 +163,41 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
 }
 
 // ------------------------------------------------- ip2 + softmax-with-loss
-// Warp per sample: logits = a1 . W2^T + b2 (W2 staged in smem), then the
+// Warp per sample (4 per block): logits = a1 . W2^T + b2 (W2 staged in smem
+// before the PDL wait: it was written by the previous step's SGD), then the
 // stable softmax, per-row loss term, lowest-index argmax and the loss
-// gradient dz = (p - onehot) * loss_weight / M.
-__global__ void __launch_bounds__(256) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
-  pdl_enter();
+// gradient dz = (p - onehot) * loss_weight / M.  The row's 125
+// float4 of a1 are all loaded up front (4 per lane).
+__global__ void __launch_bounds__(128) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
   __shared__ __align__(16) float ws[10 * 500];
   __shared__ float bs[10];
   for (int i = threadIdx.x; i < 5000; i += blockDim.x) ws[i] = __ldg(p.w + i);
   if (threadIdx.x < 10) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
-  __syncthreads();
+  pdl_enter();
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  float4 av[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const int q = lane + 32 * t;
+    av[t] = (row < p.N && q < 125) ? __ldg(reinterpret_cast<const float4*>(p.a1 + (long long)row * 500) + q)
+                                   : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __syncthreads();
   if (row >= p.N) return;
-  const float* a = p.a1 + (long long)row * 500;
   float acc[10];
 #pragma unroll
   for (int o = 0; o < 10; ++o) acc[o] = 0.f;
-  for (int k = lane; k < 500; k += 32) {
-    const float av = __ldg(a + k);
 #pragma unroll
-    for (int o = 0; o < 10; ++o) acc[o] = fmaf(av, ws[o * 500 + k], acc[o]);
+  for (int t = 0; t < 4; ++t) {
+    const int q = lane + 32 * t;
+    if (q < 125) {
+#pragma unroll
+      for (int o = 0; o < 10; ++o) {
+        const float4 w = reinterpret_cast<const float4*>(ws + o * 500)[q];
+        acc[o] = fmaf(av[t].x, w.x, fmaf(av[t].y, w.y, fmaf(av[t].z, w.z, fmaf(av[t].w, w.w, acc[o]))));
+      }
+    }
   }
 #pragma unroll
   for (int o = 0; o < 10; ++o) {
@@ -223,12 +239,13 @@ __global__ void __launch_bounds__(256) lenet_ip2_loss(const __grid_constant__ Ip
 // grid (4 column chunks of 128, splits over samples).  Thread = column k:
 // da1[m,k] = (a1[m,k] > 0) * sum_o dz[m,o] W2[o,k]   (S:387 + S:405)
 // partial dW2[o,k] = sum_{m in split} dz[m,o] a1[m,k];  partial db2[o].
+// Rows go in chunks of 16 with all 16 a1 loads issued together; the TF32
+// transpose da1rT[k][m..m+15] is written as 4 x 16 B per thread.
 __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p) {
-  pdl_enter();
   const int k = blockIdx.x * 128 + threadIdx.x;
   const int s = blockIdx.y;
   const int m0 = (int)((long long)p.N * s / p.splits), m1 = (int)((long long)p.N * (s + 1) / p.splits);
-  __shared__ float dzs[64][10];
+  __shared__ float dzs[16][10];
   float w2[10], acc[10];
   const bool valid = k < 500;
 #pragma unroll
@@ -236,33 +253,50 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     w2[o] = valid ? __ldg(p.w + o * 500 + k) : 0.f;
     acc[o] = 0.f;
   }
+  pdl_enter();
   float bacc = 0.f, b1acc = 0.f;
-  for (int mb = m0; mb < m1; mb += 64) {
-    const int cnt = min(64, m1 - mb);
+  for (int mb = m0; mb < m1; mb += 16) {
+    const int cnt = min(16, m1 - mb);
     __syncthreads();
     for (int i = threadIdx.x; i < cnt * 10; i += 128) dzs[i / 10][i % 10] = p.dz[(long long)mb * 10 + i];
-    __syncthreads();
-    for (int mm = 0; mm < cnt; ++mm) {
-      const int m = mb + mm;
-      if (valid) {
-        const float a = p.a1[(long long)m * 500 + k];
-        float g = 0.f;
+    float a[16];
 #pragma unroll
-        for (int o = 0; o < 10; ++o) {
-          const float d = dzs[mm][o];
-          g = fmaf(d, w2[o], g);
-          acc[o] = fmaf(d, a, acc[o]);
+    for (int mm = 0; mm < 16; ++mm) a[mm] = (valid && mm < cnt) ? p.a1[(long long)(mb + mm) * 500 + k] : 0.f;
+    __syncthreads();
+    float r[16];
+#pragma unroll
+    for (int mm = 0; mm < 16; ++mm) {
+      r[mm] = 0.f;
+      if (mm < cnt) {
+        if (valid) {
+          const int m = mb + mm;
+          float g = 0.f;
+#pragma unroll
+          for (int o = 0; o < 10; ++o) {
+            const float d = dzs[mm][o];
+            g = fmaf(d, w2[o], g);
+            acc[o] = fmaf(d, a[mm], acc[o]);
+          }
+          const float da = a[mm] > 0.f ? g : 0.f;
+          p.da1[(long long)m * 500 + k] = da;
+          if (p.da1r) {
+            r[mm] = __uint_as_float((__float_as_uint(da) + 0x1000u) & 0xFFFFE000u);  // TF32 (RNA)
+            p.da1r[(long long)m * 500 + k] = r[mm];
+            b1acc += da;
+          }
         }
-        const float da = a > 0.f ? g : 0.f;
-        p.da1[(long long)m * 500 + k] = da;
-        if (p.da1r) {
-          const float r = __uint_as_float((__float_as_uint(da) + 0x1000u) & 0xFFFFE000u);  // TF32 (RNA)
-          p.da1r[(long long)m * 500 + k] = r;
-          p.da1rT[(long long)k * p.npad + m] = r;
-          b1acc += da;
-        }
+        if (blockIdx.x == 0 && threadIdx.x < 10) bacc += dzs[mm][threadIdx.x];
       }
-      if (blockIdx.x == 0 && threadIdx.x < 10) bacc += dzs[mm][threadIdx.x];
+    }
+    if (p.da1rT && valid) {
+      float* dst = p.da1rT + (long long)k * p.npad + mb;
+      if (cnt == 16 && (mb & 3) == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          reinterpret_cast<float4*>(dst)[q] = make_float4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+      } else {
+        for (int mm = 0; mm < cnt; ++mm) dst[mm] = r[mm];
+      }
     }
   }
   if (valid) {

@@ -665,7 +665,7 @@ static void build_fused_lenet(pn_net* net) {
                net->blobs[net->blob("prob")].data, (int32_t*)net->blobs[net->blob("pred")].data, lg.diff,
                net->row_loss, net->err, N, 1.f / N};
     Launch l;
-    l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, 8)), dim3(256), 0, p);
+    l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, 4)), dim3(128), 0, p);
     add(fwd, "ip2+softmax_loss", l, [](Launch& l, const StepArgs& a) { l.params<Ip2LossP>().labels = a.labels; });
     add_loss(net, fwd);
   }

@@ -538,7 +538,7 @@ __device__ unsigned long long g_trace[148 * 16];
 __device__ __forceinline__ void stamp(int k) {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_trace[blockIdx.x * 16 + k] = t;
+  g_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + k] = t;
 }
 #else
 __device__ __forceinline__ void stamp(int) {}
@@ -934,6 +934,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
+  if (tid == 0) stamp(0);
   if (tid == 0) {
     // ---- producer (G2 and p1 come from the two preceding launches' producers:
     // wait for the immediate predecessor first)
@@ -956,7 +957,9 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
     for (int t = 0; t < nimg; ++t) {
       const int s = t % SLOTS, b = t & 1;
       mbar_wait(smem_u32(&full[s]), (t / SLOTS) & 1);
+      if (t < 4) stamp(1 + t);  // image t landed
       mbar_wait(smem_u32(&afull[b]), (t >> 1) & 1);
+      if (t < 4) stamp(5 + t);  // A tile t built
       tc_fence_after();
       const uint32_t Ab = A_s + b * A_BYTES, Gb = G_s + s * G_BYTES;
 #pragma unroll
@@ -1016,6 +1019,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
       float* dst = p.part + (size_t)split * p.pstride;
       if (nimg > 0) {
         mbar_wait(smem_u32(&done), 0);
+        if (warp == 2 && lane == 0) stamp(9);  // accumulation done
         __syncwarp();
         tc_fence_after();
       }
@@ -1036,6 +1040,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
       }
     }
   }
+  if (warp == 2 && lane == 0) stamp(10);  // partials written
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tbase, 64);
