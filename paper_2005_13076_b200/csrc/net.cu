@@ -429,7 +429,7 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->da1r, (size_t)net->batch * 500));
     TRY(net->alloc(&net->da1rT, (size_t)500 * net->npad));
     TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
-    TRY(net->alloc(&net->part_db2, (size_t)((net->batch + 127) / 128) * 50));
+    TRY(net->alloc(&net->part_db2, (size_t)tc::db2_partials(net->batch) * 50));
   }
   TRY(net->alloc(&net->err, 1));
   // activation blobs (the fused plan never stores conv1's output or its
@@ -691,7 +691,7 @@ static void build_fused_lenet(pn_net* net) {
     add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs);
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
-    conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, (N + 127) / 128, 50));
+    conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
     Launch l;

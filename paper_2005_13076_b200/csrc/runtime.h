@@ -26,6 +26,7 @@ struct StepArgs {
 struct Launch {
   const void* func = nullptr;
   dim3 grid, block;
+  dim3 cluster{1, 1, 1};  // thread-block cluster dims (1 = none)
   size_t smem = 0;
   std::vector<unsigned char> arg;
   template <class P>
@@ -56,11 +57,20 @@ struct Launch {
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    unsigned n = 0;
+    if (pdl()) {
+      at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[n++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (cluster.x * cluster.y * cluster.z > 1) {
+      at[n].id = cudaLaunchAttributeClusterDimension;
+      at[n].val.clusterDim.x = cluster.x;
+      at[n].val.clusterDim.y = cluster.y;
+      at[n++].val.clusterDim.z = cluster.z;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl() ? 1 : 0;
+    cfg.numAttrs = n;
     return cudaLaunchKernelExC(&cfg, func, a);
   }
 };

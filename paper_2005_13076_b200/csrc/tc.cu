@@ -36,7 +36,6 @@ namespace tc {
 
 constexpr int BM = 128;  // tile rows = UMMA M
 constexpr int BK = 32;   // K elements per chunk (4 MMAs of K = 8) = one 128-B swizzle row
-constexpr int THREADS = 192;  // 6 warps: producer, MMA, 4 gather/epilogue
 
 // ------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -183,270 +182,273 @@ __device__ __forceinline__ uint32_t sw_off(int r, int kc) {
 __device__ __forceinline__ float4 f4(float a, float b, float c, float d) { return make_float4(a, b, c, d); }
 __device__ __forceinline__ float4 zero4() { return make_float4(0.f, 0.f, 0.f, 0.f); }
 
-// ------------------------------------------------------------------ engine
-// Warp-specialized (6 warps): warp 0 lane 0 = TMA producer, warp 1 lane 0 =
-// MMA issuer, warps 2-5 = gatherers (implicit-im2col operands) and, after
-// the K loop, the epilogue (warp w reads TMEM lane quadrant w % 4).  The
-// producer and gatherers run up to STAGES chunks ahead of the MMA; all hand
-// offs are mbarriers (full: TMA bytes landed, gath: 128 gatherer arrivals
-// after fence.proxy.async, empty: tcgen05.commit of the chunk's MMAs).
-//
-// Op interface:
-//   BN, TMEM_COLS, STAGES, A_TMA, B_TMA (else gathered), STAGE_BYTES
-//   Op(params, staging_smem, ring_smem)   decodes the tile
-//   int  num_k_chunks()
-//   void stage(tid)                       one-time generic staging (all threads; engine syncs)
-//   void issue(chunk, As, Bs, bar)        producer: TMA / bulk copies for a chunk
-//   uint32_t tx_bytes(chunk)              bytes those copies complete on `bar`
-//   void before_gather(chunk)             gatherers, before gathering a chunk
-//   float4 a(r, k) / b(c, k)              gathered (already TF32) values
-//   void epilogue(row, c0, v[16]);  void finish(tid)
-constexpr int GATHER_T0 = 64;  // first gatherer thread
-__device__ __forceinline__ int gtid() { return (int)threadIdx.x - GATHER_T0; }
+// dev-only timeline stamps (tools/tc_trace.cu builds with -DPN_TRACE)
+#ifdef PN_TRACE
+__device__ unsigned long long g_trace[148 * 16];
+__device__ __forceinline__ void stamp(int k) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  const int cta = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (cta < 148) g_trace[cta * 16 + k] = t;
+}
+#else
+__device__ __forceinline__ void stamp(int) {}
+#endif
+
+// ================================================= ip1 GEMMs: cluster split-K
+// C[M,N] = A[M,K] B[N,K]^T (both K-major TF32 by TMA, SW128) with the K range
+// split over a thread-block cluster of S CTAs on one 128 x BN tile:
+//   warp 0      TMA producer: the CTA's K slice through a 3-stage ring --
+//               operands produced two or more launches back are requested
+//               before the PDL wait, the rest after it
+//   warp 1      MMA: 4 x tcgen05.mma (M=128, N=BN, K=8) per chunk into TMEM
+//   warps 2-5   TMEM -> shared-memory partial tile C (pitch BN+4)
+// then (cluster barrier) CTA r sums rows [128r/S, 128(r+1)/S) of the S
+// partial tiles through distributed shared memory (ld.shared::cluster, float4
+// units over all threads, fixed order s = 0..S-1: deterministic, no partials
+// in global memory) into a local buffer R, and (second cluster barrier)
+// applies the layer's epilogue from R (bias+ReLU / store / pool2 backward).
+namespace ipk {
+// STAGES-deep ring (97 KB of shared memory: two CTAs per SM, so clusters of
+// up to 8 fit all tiles in one wave -- at one CTA per SM a GPC holds too few)
+constexpr int THREADS = 192, STAGES = 3;
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float4 ld_cluster4(uint32_t local_addr, uint32_t rank) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local_addr), "r"(rank));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+}  // namespace ipk
 
 template <class Op>
-__global__ void __launch_bounds__(THREADS) tc_gemm(const __grid_constant__ typename Op::Params prm) {
-  pdl_enter();
+__global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_constant__ typename Op::Params prm) {
+  using namespace ipk;
+  constexpr int BN = Op::BN, PITCH = BN + 4, UC = Op::UNIT_COLS;
+  static_assert(4 * (128 * PITCH + (128 / Op::S + 1) * BN) <= ipk::STAGES * (128 * 128 + BN * 128), "C + R fit the ring");
+  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-B alignment for the swizzle atoms (dynamic smem base is only 16-B aligned)
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  constexpr int S = Op::STAGES;
-  constexpr int BN = Op::BN;
-  constexpr int A_BYTES = BM * BK * 4;
-  constexpr int B_BYTES = BN * BK * 4;
-  constexpr int STAGE = A_BYTES + B_BYTES;
-  constexpr bool GATHER = !Op::A_TMA || !Op::B_TMA;
-  constexpr int NG = THREADS - GATHER_T0;  // 128 gatherer threads
-  __shared__ __align__(8) uint64_t full[S], empty[S], gath[S], done;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
   __shared__ uint32_t tmem_base;
+  __shared__ float red[Op::RED_FLOATS + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  Op op(prm, smem + S * STAGE, smem);
+  constexpr uint32_t S = Op::S;
+  const uint32_t rank = cluster_rank();
+  Op op(prm);
+  const int nk = op.num_k_chunks(), c0 = (int)(rank * nk / S), my = (int)((rank + 1) * nk / S) - c0;
+  const uint32_t sbase = smem_u32(smem);
   if (tid == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), 1);
-      mbar_init(smem_u32(&gath[s]), NG);
+    for (int c = 0; c < STAGES; ++c) {
+      mbar_init(smem_u32(&full[c]), 1);
+      mbar_init(smem_u32(&empty[c]), 1);
     }
     mbar_init(smem_u32(&done), 1);
-    op.init_barriers();
     fence_barrier_init();
     op.prefetch();
   }
   if (warp == 0) tmem_alloc(&tmem_base, Op::TMEM_COLS);
-  op.stage(tid);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
-  const uint32_t sbase = smem_u32(smem);
-  constexpr uint32_t idesc = make_idesc(BM, BN);
-  const int nk = op.num_k_chunks();
+  if (tid == 0) stamp(0);
   if (tid == 0) {
-    // ---- TMA producer
-#pragma unroll 1
-    for (int c = 0; c < nk; ++c) {
-      const int s = c % S;
-      if (c >= S) mbar_wait(smem_u32(&empty[s]), ((c / S) - 1) & 1);
-      const uint32_t bar = smem_u32(&full[s]);
-      mbar_expect_tx(bar, op.tx_bytes(c));
-      op.issue(c, sbase + s * STAGE, sbase + s * STAGE + A_BYTES, bar);
+    const int pre = min(my, STAGES);
+    for (int c = 0; c < pre; ++c) {
+      const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
+      mbar_expect_tx(bar, STAGE);
+      if (Op::A_EARLY) op.issue_a(c0 + c, As, bar);
+      if (Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+    }
+    pdl_enter();
+    stamp(1);
+    for (int c = 0; c < pre; ++c) {
+      const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
+      if (!Op::A_EARLY) op.issue_a(c0 + c, As, bar);
+      if (!Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+    }
+    for (int c = STAGES; c < my; ++c) {
+      const int st = c % STAGES;
+      mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
+      const uint32_t As = sbase + st * STAGE, bar = smem_u32(&full[st]);
+      mbar_expect_tx(bar, STAGE);
+      op.issue_a(c0 + c, As, bar);
+      op.issue_b(c0 + c, As + A_BYTES, bar);
     }
   } else if (tid == 32) {
-    // ---- MMA issuer
-#pragma unroll 1
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % S;
-      mbar_wait(smem_u32(&full[s]), (kb / S) & 1);
-      if (GATHER) mbar_wait(smem_u32(&gath[s]), (kb / S) & 1);
+    constexpr uint32_t idesc = make_idesc(128, BN);
+    for (int c = 0; c < my; ++c) {
+      const int st = c % STAGES;
+      mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
       tc_fence_after();
-      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
+      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
 #pragma unroll
-      for (int k = 0; k < BK / 8; ++k)
-        mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (kb | k) != 0);
-      mma_commit(smem_u32(&empty[s]));
-      if (kb == nk - 1) mma_commit(smem_u32(&done));
+      for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+      mma_commit(smem_u32(&empty[st]));
     }
-  } else if (GATHER && tid >= GATHER_T0) {
-    // ---- gatherers
-    const int g = gtid();
-#pragma unroll 1
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % S;
-      if (kb >= S) mbar_wait(smem_u32(&empty[s]), ((kb / S) - 1) & 1);
-      op.before_gather(kb);
-      const uint32_t As = sbase + s * STAGE, Bs = As + A_BYTES;
-      const int k0 = kb * BK;
-      if (!Op::A_TMA) {
-#pragma unroll
-        for (int q = 0; q < BM * 8 / NG; ++q) {
-          const int u = g + q * NG, r = u & (BM - 1), kc = u >> 7;
-          sts128(As + sw_off(r, kc), op.a(r, k0 + kc * 4));
-        }
-      }
-      if (!Op::B_TMA) {
-        for (int u = g; u < BN * 8; u += NG) {
-          const int c = u % BN, kc = u / BN;
-          sts128(Bs + sw_off(c, kc), op.b(c, k0 + kc * 4));
-        }
-      }
-      fence_proxy_async();
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gath[s])) : "memory");
-    }
-  }
-  __syncwarp();
-  // ---- epilogue: warps 2-5, thread = TMEM lane (tile row), all columns
-  if (warp >= 2) {
-    const int row = (warp & 3) * 32 + lane;
-    if (nk > 0) {
+    if (my > 0) mma_commit(smem_u32(&done));
+  } else if (warp >= 2) {
+    // TMEM -> C[row][PITCH] over the drained operand ring (all MMAs retired)
+    const int quad = warp & 3, row = quad * 32 + lane;
+    if (my > 0) {
       mbar_wait(smem_u32(&done), 0);
+      if (warp == 2 && lane == 0) stamp(2);
       __syncwarp();
       tc_fence_after();
+    }
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + ((uint32_t)((warp & 3) * 32) << 16) + c0, v);
-        op.epilogue(row, c0, v);
-      }
-    } else {  // empty K range (a weight-gradient split with no images)
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
+    for (int cc = 0; cc < BN; cc += 16) {
+      float v[16];
+      if (my > 0) {
+        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
+      } else {  // an empty K slice (tiny batch): a zero partial
 #pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        op.epilogue(row, c0, v);
+        for (int j = 0; j < 16; ++j) v[j] = 0.f;
       }
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) sts128(sbase + 4 * (row * PITCH + cc + j), f4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     }
   }
   tc_fence_before();
+  cluster_sync();  // every partial tile of the cluster is complete
+  if (tid == 0) stamp(3);
+  // ---- phase A: this CTA's rows [r0, r1) summed over the S partial tiles in a
+  // fixed order (s = 0..S-1), float4 units spread over all threads, into R
+  const int r0 = (int)(rank * 128 / S), r1 = (int)((rank + 1) * 128 / S);
+  const uint32_t R_s = sbase + 4 * (128 * PITCH);  // [ceil(128/S)][BN], after C (still in the ring)
+  for (int u = tid; u < (r1 - r0) * (BN / 4); u += THREADS) {
+    const int rr = u / (BN / 4), col = (u % (BN / 4)) * 4;
+    const uint32_t addr = sbase + 4 * ((r0 + rr) * PITCH + col);
+    float4 t[S];
+#pragma unroll
+    for (uint32_t s2 = 0; s2 < S; ++s2) t[s2] = ld_cluster4(addr, s2);
+    float4 acc = t[0];
+#pragma unroll
+    for (uint32_t s2 = 1; s2 < S; ++s2) {
+      acc.x += t[s2].x; acc.y += t[s2].y; acc.z += t[s2].z; acc.w += t[s2].w;
+    }
+    sts128(R_s + 4 * (rr * BN + col), acc);
+  }
+  cluster_sync();  // all remote reads of this cluster's C tiles are done; R complete
+  // ---- phase B: the layer's epilogue on the reduced rows (local shared memory)
+  for (int u = tid; u < (r1 - r0) * (BN / UC); u += THREADS) {
+    const int rr = u / (BN / UC), col = (u % (BN / UC)) * UC;
+    float v[UC];
+#pragma unroll
+    for (int q = 0; q < UC; q += 4) {
+      const int4 t = lds_i4(R_s + 4 * (rr * BN + col + q));
+      v[q] = __int_as_float(t.x); v[q + 1] = __int_as_float(t.y);
+      v[q + 2] = __int_as_float(t.z); v[q + 3] = __int_as_float(t.w);
+    }
+    op.store(r0 + rr, col, v, red, r0);
+  }
   __syncthreads();
-  op.finish(tid);
+  if (tid == 0) stamp(4);
+  op.finish(tid, red, r0, r1, rank);
+  if (tid == 0) stamp(5);
   if (warp == 0) tmem_dealloc(tbase, Op::TMEM_COLS);
 }
 
-// common no-op hooks
-struct OpBase {
-  __device__ void init_barriers() {}
-  __device__ void prefetch() {}
-  __device__ void stage(int) {}
-  __device__ void before_gather(int) {}
-  __device__ float4 a(int, int) const { return zero4(); }
-  __device__ float4 b(int, int) const { return zero4(); }
-  __device__ void finish(int) {}
-};
-
-// ------------------------------------------------------ ip fwd + bias + relu
-// y[n,o] = relu(sum_k x[n,k] W[o,k] + b[o]); rows n, cols o (BN 16), K = 800.
-// A = p2 (TF32) and B = W1f by TMA.
-struct IpFwd : OpBase {
+// y[n,o] = relu(sum_k p2[n,k] W1[o,k] + b[o]): rows n (4 tiles), cols o (BN
+// 128, 4 tiles), K = 800 (25 chunks) over S = 8.  A = p2 (TF32, from conv2 --
+// the immediate predecessor), B = W1f (packed at the start of the step).
+struct IpFwd {
   struct Params {
     CUtensorMap ta, tb;
     const float* b;
     float* y;
-    int M, K, Nout, relu;
+    int M, K, Nout;
   };
-  static constexpr int BN = 16, TMEM_COLS = 32, STAGES = 6;
-  static constexpr bool A_TMA = true, B_TMA = true;
-  static constexpr int STAGE_BYTES = 0;
+  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 8;
+  static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int m0, o0;
-  __device__ IpFwd(const Params& q, uint8_t*, uint8_t*) : p(q), m0(blockIdx.y * BM), o0(blockIdx.x * BN) {}
+  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.z * 128), o0(blockIdx.y * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
-  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
-    tma2d(As, &p.ta, c * BK, m0, bar);
-    tma2d(Bs, &p.tb, c * BK, o0, bar);
+  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
+  __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, o0, bar); }
+  __device__ void store(int row, int col, const float (&v)[4], float*, int) const {
+    const int m = m0 + row, o = o0 + col;
+    if (m >= p.M || o >= p.Nout) return;  // Nout % 4 == 0
+    float4 r = f4(v[0] + __ldg(p.b + o), v[1] + __ldg(p.b + o + 1), v[2] + __ldg(p.b + o + 2), v[3] + __ldg(p.b + o + 3));
+    r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
+    *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const int m = m0 + row;
-    if (m >= p.M) return;
-#pragma unroll
-    for (int j = 0; j < 16; j += 4) {
-      const int o = o0 + c0 + j;
-      if (o >= p.Nout) break;
-      float4 r = f4(v[j] + __ldg(p.b + o), v[j + 1] + __ldg(p.b + o + 1), v[j + 2] + __ldg(p.b + o + 2),
-                    v[j + 3] + __ldg(p.b + o + 3));
-      if (p.relu) {
-        r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
-      }
-      *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
-    }
-  }
+  __device__ void finish(int, float*, int, int, uint32_t) const {}
 };
 
-// --------------------------------------------------------- ip weight gradient
-// dW[o,k] = sum_n dy[n,o] x[n,k]: rows o, cols k (BN 32), K = n (batch).
-// A = dy^T (da1T [500][npad], TF32) and B = x^T (p2T [800][npad], TF32) by
-// TMA.  The bias gradient comes from the ip2 backward kernel (exact fp32).
-struct IpWgrad : OpBase {
+// dW1[o,k] = sum_n da1[n,o] p2[n,k]: rows o (4 tiles), cols k (BN 128, 7
+// tiles), K = batch over S = 5.  A = da1^T (da1rT [500][npad], TF32, from
+// ip2 backward = the immediate predecessor), B = p2^T (p2T, from conv2).
+// The bias gradient comes from the ip2 backward kernel (exact fp32).
+struct IpWgrad {
   struct Params {
     CUtensorMap ta, tb;
     float* dw;
-    int M, K, Nout;
+    int M, K, Nout;  // M = batch (contraction), K = 800 (cols), Nout = 500 (rows)
   };
-  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 6;
-  static constexpr bool A_TMA = true, B_TMA = true;
-  static constexpr int STAGE_BYTES = 0;
+  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 5;
+  static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int o0, k0;
-  __device__ IpWgrad(const Params& q, uint8_t*, uint8_t*) : p(q), o0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
+  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
-  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
-    tma2d(As, &p.ta, c * BK, o0, bar);
-    tma2d(Bs, &p.tb, c * BK, k0, bar);
+  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, o0, bar); }
+  __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
+  __device__ void store(int row, int col, const float (&v)[4], float*, int) const {
+    const int o = o0 + row, k = k0 + col;
+    if (o >= p.Nout || k >= p.K) return;
+    *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k) = f4(v[0], v[1], v[2], v[3]);
   }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const int o = o0 + row;
-    if (o >= p.Nout) return;
-#pragma unroll
-    for (int j = 0; j < 16; j += 4) {
-      const int k = k0 + c0 + j;
-      if (k >= p.K) break;
-      *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k) = f4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-    }
-  }
+  __device__ void finish(int, float*, int, int, uint32_t) const {}
 };
 
-// ------------------------------- ip1 data gradient + pool2 backward (LeNet)
-// dp2[n,k] = sum_o dy[n,o] W1[o,k]; rows n, cols k (BN 32 = 2 filters x 16),
-// K = o (500).  A = da1 (TF32 copy [N][500]), B = W1t [800][512] by TMA.
-// Epilogue scatters each dp2 value to its pool2 origin in the dense conv2
-// gradient G2[n,f,8,8] (zeros elsewhere), stored TF32-rounded
-// (its only consumers are conv2's contractions), and sums the exact dp2 per
-// filter over the tile's rows for the conv2 bias gradient.
-struct IpDgradUnpool : OpBase {
+// dp2[n,k] = sum_o da1[n,o] W1[o,k]: rows n (4 tiles), cols k (BN 128 = 8
+// filters x 16 pooled outputs, 7 tiles), K = o (500 -> 512) over S = 5.  A =
+// da1 (TF32 copy [N][500]), B = W1t [800][512] -- neither comes from the
+// immediate predecessor (the ip bucket reduce), so all loads precede the PDL
+// wait.  Epilogue (unit = one filter's 16 columns of a row): scatter each
+// dp2 value to its pool2 origin in the dense conv2 gradient G2[n,f,8,8]
+// (zeros elsewhere), stored TF32-rounded (its only consumers are
+// conv2's contractions), and the exact dp2 sum per filter over the reducer's
+// rows for the conv2 bias gradient: part_db2[(row tile * S + rank)][f].
+struct IpDgradUnpool {
   struct Params {
     CUtensorMap ta, tb;
     const uint8_t* m2;  // [N,800]
     float* g2;          // [N,50,8,8]
-    float* part_db2;    // [rowtiles][50]
+    float* part_db2;    // [row tiles * S][50]
     int N;
   };
-  static constexpr int BN = 32, TMEM_COLS = 32, STAGES = 6;
-  static constexpr bool A_TMA = true, B_TMA = true;
-  static constexpr int STAGE_BYTES = 2 * 128 * 4;
+  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 16, S = 5;
+  static constexpr int RED_FLOATS = 8 * 32;  // [filter in tile][reducer row]
+  static constexpr bool A_EARLY = true, B_EARLY = true;
   const Params& p;
-  float* red;  // [2 filters][128 rows]
   int m0, k0;
-  __device__ IpDgradUnpool(const Params& q, uint8_t* st, uint8_t*)
-      : p(q), red((float*)st), m0(blockIdx.y * BM), k0(blockIdx.x * BN) {}
+  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ uint32_t tx_bytes(int) const { return (BM + BN) * BK * 4; }
-  __device__ void issue(int c, uint32_t As, uint32_t Bs, uint32_t bar) {
-    tma2d(As, &p.ta, c * BK, m0, bar);
-    tma2d(Bs, &p.tb, c * BK, k0, bar);
-  }
-  __device__ void epilogue(int row, int c0, const float (&v)[16]) const {
-    const int n = m0 + row;
-    float s = 0.f;
+  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
+  __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
+  __device__ void store(int row, int col, const float (&v)[16], float* red, int r0) const {
+    const int n = m0 + row, f = (k0 + col) >> 4;
+    float sum = 0.f;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) s += v[q];
-    red[(c0 >> 4) * 128 + row] = n < p.N ? s : 0.f;
-    if (n >= p.N) return;
-    const int f = (k0 + c0) >> 4;  // the 16 columns are filter f's 4x4 pooled outputs
+    for (int q = 0; q < 16; ++q) sum += v[q];
+    red[(col >> 4) * 32 + (row - r0)] = n < p.N ? sum : 0.f;
+    if (n >= p.N || f >= 50) return;
     const uint8_t* m = p.m2 + (size_t)n * 800 + f * 16;
     float* g = p.g2 + ((size_t)n * 50 + f) * 64;
     uint32_t mw[4];
@@ -465,11 +467,12 @@ struct IpDgradUnpool : OpBase {
       *reinterpret_cast<float4*>(g + h * 8 + 4) = f4(o8[4], o8[5], o8[6], o8[7]);
     }
   }
-  __device__ void finish(int tid) {
-    if (tid < 2) {  // fixed-order sum over the tile's 128 rows
+  __device__ void finish(int tid, const float* red, int r0, int r1, uint32_t rank) const {
+    const int f = (k0 >> 4) + tid;
+    if (tid < 8 && f < 50) {  // fixed-order sum over the reducer's rows
       float s = 0.f;
-      for (int r = 0; r < 128; ++r) s += red[tid * 128 + r];
-      p.part_db2[(size_t)blockIdx.y * 50 + (k0 >> 4) + tid] = s;
+      for (int r = 0; r < r1 - r0; ++r) s += red[tid * 32 + r];
+      p.part_db2[((size_t)blockIdx.z * S + rank) * 50 + f] = s;
     }
   }
 };
@@ -532,17 +535,6 @@ __device__ __forceinline__ uint64_t make_desc_ns(uint32_t saddr, uint32_t lbo, u
          ((uint64_t)1 << 46);
 }
 
-// dev-only timeline stamps (tools/tc_trace.cu builds with -DPN_TRACE)
-#ifdef PN_TRACE
-__device__ unsigned long long g_trace[148 * 16];
-__device__ __forceinline__ void stamp(int k) {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_trace[(blockIdx.y * gridDim.x + blockIdx.x) * 16 + k] = t;
-}
-#else
-__device__ __forceinline__ void stamp(int) {}
-#endif
 
 __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const __grid_constant__ cf::Params p) {
   using namespace cf;
@@ -1161,14 +1153,12 @@ static CUtensorMap tmap_g2(const float* base, uint64_t N) {
 }
 
 template <class Op>
-static constexpr size_t smem_bytes() {  // + 1 KB slack for the 1024-B alignment
-  return (size_t)Op::STAGES * (BM * BK * 4 + Op::BN * BK * 4) + Op::STAGE_BYTES + 1024;
+static constexpr size_t ip_smem() {  // whole K slice + 1 KB alignment slack
+  return (size_t)ipk::STAGES * (128 * 128 + Op::BN * 128) + 1024;
 }
-
 template <class Op>
 static cudaError_t opt_in() {
-  return cudaFuncSetAttribute((const void*)tc_gemm<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem_bytes<Op>());
+  return cudaFuncSetAttribute((const void*)ip_splitk<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ip_smem<Op>());
 }
 
 cudaError_t setup() {
@@ -1226,28 +1216,34 @@ Launch pack_p1c_launch(const float* p1, float* p1c, int N) {
 
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N) {
   Launch l;
-  IpFwd::Params p{tmap2d(p2, N, 800, 800, BM), tmap2d(w1f, 500, 800, 800, IpFwd::BN), b, y, N, 800, 500, 1};
-  l.set((const void*)tc_gemm<IpFwd>, dim3(cdiv(500, IpFwd::BN), cdiv(N, BM)), dim3(THREADS), smem_bytes<IpFwd>(), p);
+  IpFwd::Params p{tmap2d(p2, N, 800, 800, 128), tmap2d(w1f, 500, 800, 800, IpFwd::BN), b, y, N, 800, 500};
+  l.set((const void*)ip_splitk<IpFwd>, dim3(IpFwd::S, cdiv(500, IpFwd::BN), cdiv(N, 128)), dim3(ipk::THREADS),
+        ip_smem<IpFwd>(), p);
+  l.cluster = dim3(IpFwd::S, 1, 1);
   return l;
 }
 
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad) {
   Launch l;
-  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, BM), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
-  l.set((const void*)tc_gemm<IpWgrad>, dim3(cdiv(800, IpWgrad::BN), cdiv(500, BM)), dim3(THREADS),
-        smem_bytes<IpWgrad>(), p);
+  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
+  l.set((const void*)ip_splitk<IpWgrad>, dim3(IpWgrad::S, cdiv(800, IpWgrad::BN), cdiv(500, 128)),
+        dim3(ipk::THREADS), ip_smem<IpWgrad>(), p);
+  l.cluster = dim3(IpWgrad::S, 1, 1);
   return l;
 }
 
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N) {
   Launch l;
-  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, BM), tmap2d(w1t, 800, 512, 512, IpDgradUnpool::BN), m2, g2,
+  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, 128), tmap2d(w1t, 800, 512, 512, IpDgradUnpool::BN), m2, g2,
                           part_db2, N};
-  l.set((const void*)tc_gemm<IpDgradUnpool>, dim3(800 / IpDgradUnpool::BN, cdiv(N, BM)), dim3(THREADS),
-        smem_bytes<IpDgradUnpool>(), p);
+  l.set((const void*)ip_splitk<IpDgradUnpool>, dim3(IpDgradUnpool::S, cdiv(800, IpDgradUnpool::BN), cdiv(N, 128)),
+        dim3(ipk::THREADS), ip_smem<IpDgradUnpool>(), p);
+  l.cluster = dim3(IpDgradUnpool::S, 1, 1);
   return l;
 }
+
+int db2_partials(int N) { return (int)cdiv(N, 128) * IpDgradUnpool::S; }
 
 Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms) {
   Launch l;

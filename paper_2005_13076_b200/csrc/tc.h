@@ -31,10 +31,12 @@ constexpr int kP1cPairFloats = 5 * 12 * 2 * 12 * 4;
 Launch conv2_pool2_launch(const float* w2c, const float* b, const float* p1c, float* p2, float* p2T, uint8_t* m2,
                           int N, int npad, int sms);
 Launch pack_p1c_launch(const float* p1, float* p1c, int N);
+// the three ip1 GEMMs split K over a thread-block cluster (reduction in DSMEM)
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N);
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N);
+int db2_partials(int N);  // conv2 bias-gradient partial rows written by ip1_dgrad_unpool
 Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms);
 Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N);
 }  // namespace tc

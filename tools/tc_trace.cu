@@ -10,8 +10,82 @@
 using namespace pn;
 using namespace pn::tc;
 
+static void dump(const char* hdr, const int* ks, int nk, int ncta) {
+  std::vector<unsigned long long> t(148 * 16);
+  cudaMemcpyFromSymbol(t.data(), g_trace, t.size() * 8);
+  unsigned long long t0 = ~0ull;
+  for (int c = 0; c < 148; ++c)
+    if (t[c * 16]) t0 = std::min(t0, t[c * 16]);
+  printf("%s\n", hdr);
+  for (int c = 0; c < ncta; c += (ncta + 9) / 10) {
+    printf("%3d", c);
+    for (int i = 0; i < nk; ++i) printf(" %6lld", t[c * 16 + ks[i]] ? (long long)(t[c * 16 + ks[i]] - t0) : -1ll);
+    printf("\n");
+  }
+}
+
+static float time_launch(Launch& l, cudaStream_t st, int R) {
+  for (int i = 0; i < 5; ++i) l.launch(st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < R; ++i) l.launch(st);
+  cudaEventRecord(e1, st);
+  cudaStreamSynchronize(st);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  return ms * 1000 / R;
+}
+
+static int wgrad_main(int N) {
+  float *g2, *p1, *part;
+  const int splits = 37;
+  cudaMalloc(&g2, (size_t)N * 3200 * 4);
+  cudaMalloc(&p1, (size_t)N * 2880 * 4);
+  cudaMalloc(&part, (size_t)splits * 25050 * 4);
+  cudaMemset(g2, 0, (size_t)N * 3200 * 4);
+  cudaMemset(p1, 0, (size_t)N * 2880 * 4);
+  if (setup() != cudaSuccess) { printf("setup failed\n"); return 1; }
+  Launch l = conv2_wgrad_launch(g2, p1, part, splits, N);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  printf("conv2_wgrad_persistent N=%d: %.2f us/launch (%s)\n", N, time_launch(l, st, 50), cudaGetErrorString(cudaGetLastError()));
+  const int ks[] = {0, 1, 2, 3, 5, 6, 7, 8, 9, 10};
+  dump("cta  start  img0  img1  img2  A0  A1  A2  A3  done  end", ks, 10, 148);
+  return 0;
+}
+
+static int ip_main(int N, char which) {
+  const int npad = (N + 3) & ~3;
+  float *a, *b, *c, *bias, *part;
+  uint8_t* m2;
+  cudaMalloc(&a, (size_t)800 * npad * 4 + (size_t)N * 800 * 4);
+  cudaMalloc(&b, (size_t)800 * 800 * 4);
+  cudaMalloc(&c, (size_t)N * 3200 * 4);
+  cudaMalloc(&bias, 4096);
+  cudaMalloc(&part, 64 * 50 * 4);
+  cudaMalloc(&m2, (size_t)N * 800);
+  cudaMemset(a, 0, (size_t)800 * npad * 4 + (size_t)N * 800 * 4);
+  cudaMemset(b, 0, (size_t)800 * 800 * 4);
+  cudaMemset(m2, 0, (size_t)N * 800);
+  if (setup() != cudaSuccess) { printf("setup failed\n"); return 1; }
+  Launch l = which == 'f' ? ip1_fwd_launch(a, b, bias, c, N)
+             : which == 'g' ? ip1_wgrad_launch(a, b, c, N, npad)
+                            : ip1_dgrad_unpool_launch(a, b, m2, c, part, N);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  printf("ip_splitk<%c> N=%d grid %d x %d x %d: %.2f us/launch (%s)\n", which, N, l.grid.x, l.grid.y, l.grid.z,
+         time_launch(l, st, 50), cudaGetErrorString(cudaGetLastError()));
+  const int ks[] = {0, 1, 2, 3, 4, 5};
+  dump("cta  start  waited  accum  sync1  reduced  end", ks, 6, 140);
+  return 0;
+}
+
 int main(int argc, char** argv) {
   const int N = argc > 1 ? atoi(argv[1]) : 512;
+  if (argc > 2 && argv[2][0] == 'w') return wgrad_main(N);
+  if (argc > 2 && (argv[2][0] == 'f' || argv[2][0] == 'g' || argv[2][0] == 'd')) return ip_main(N, argv[2][0]);
   const int npairs = (N + 1) / 2, npad = (N + 3) & ~3;
   float *w2c, *p1c, *b, *p2, *p2T;
   uint8_t* m2;
