@@ -159,7 +159,7 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
 // sums in order -- a fixed order, so reruns are bitwise identical.
 // p.total = number of 32-output blocks over all segments.
 __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_constant__ ReduceMultiP p) {
-  pdl_enter();
+  if (!p.late) pdl_enter();
   __shared__ float sm[8][33];
   int b = blockIdx.x, k = 0;
   while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
@@ -177,6 +177,7 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
     for (int q = 0; q < 8; ++q) r += sm[q][lane];
     s.out[i] = r;
   }
+  if (p.late) pdl_enter();
 }
 
 // ------------------------------------------------------------------ pooling

@@ -15,69 +15,89 @@
 namespace pn {
 
 // ------------------------------------------------------------ conv1 + pool1
-// Block: 2 images, 288 threads; item = (image, filter group of 4, pooled
-// position q of 144) -> 4 pooled outputs per item (each = max of 4 conv
-// values of 25 MACs).  Ties: first of (0,0),(0,1),(1,0),(1,1).
+// Block = one image pair, 320 threads: warp w owns filters (2w, 2w+1) with
+// their 25 weights held in registers as (w_2w, w_2w+1) pairs; lane l takes
+// pooled positions q = l, l+32, ... of both images.  Per pooled position the
+// four conv values of the 2x2 window (25 MACs each, tap order i-major, bias
+// added after the sum: S:297 with P:136) are computed for both filters at
+// once with packed fp32 FMAs (FFMA2: fma.rn.f32x2, two independent
+// round-to-nearest FMAs -- the same arithmetic as scalar fmaf), the input
+// patch streamed row by row from shared memory.  Ties: first of
+// (0,0),(0,1),(1,0),(1,1).
+__device__ __forceinline__ unsigned long long pk2(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void fma2(unsigned long long& d, float a, unsigned long long b) {
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(d) : "l"(pk2(a, a)), "l"(b));
+}
+__device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
+__device__ __forceinline__ float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
+
 constexpr int C1_IMGS = 2;
-__global__ void __launch_bounds__(288) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+__global__ void __launch_bounds__(320) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
   // inputs (the batch) and weights (previous step's SGD) are complete at
   // launch (pdl.cuh): stage them before waiting on the predecessor
   __shared__ float xs[C1_IMGS][28 * 28];
-  __shared__ __align__(16) float ws[20][28];
-  __shared__ float bs[20];
   const int n0 = blockIdx.x * C1_IMGS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int f0 = 2 * warp;
   for (int i = threadIdx.x; i < C1_IMGS * 784; i += blockDim.x) {
-    int im = i / 784, e = i % 784;
+    const int im = i / 784, e = i % 784;
     xs[im][e] = (n0 + im < p.N) ? __ldg(p.x + (long long)(n0 + im) * 784 + e) : 0.f;
   }
-  for (int i = threadIdx.x; i < 20 * 28; i += blockDim.x) {
-    int f = i / 28, t = i % 28;
-    ws[f][t] = t < 25 ? __ldg(p.w + f * 25 + t) : 0.f;
-  }
-  if (threadIdx.x < 20) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
+  unsigned long long wp[25];
+#pragma unroll
+  for (int t = 0; t < 25; ++t) wp[t] = pk2(__ldg(p.w + f0 * 25 + t), __ldg(p.w + (f0 + 1) * 25 + t));
+  const float b0 = __ldg(p.b + f0), b1 = __ldg(p.b + f0 + 1);
   pdl_enter();
   __syncthreads();
-  for (int it = threadIdx.x; it < C1_IMGS * 720; it += blockDim.x) {
-    const int im = it / 720, r = it % 720, g = r / 144, q = r % 144;
+#pragma unroll 1
+  for (int it = lane; it < C1_IMGS * 144; it += 32) {
+    const int im = it / 144, q = it - im * 144;
     const int n = n0 + im;
     if (n >= p.N) break;
-    const int ph = q / 12, pw = q % 12;
-    float patch[6][6];
+    const int ph = q / 12, pw = q - ph * 12;
+    const float* xp = &xs[im][(2 * ph) * 28 + 2 * pw];
+    unsigned long long acc[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+    float r0[6], r1[6];
 #pragma unroll
-    for (int a = 0; a < 6; ++a)
+    for (int c = 0; c < 6; ++c) r0[c] = xp[c];
 #pragma unroll
-      for (int b = 0; b < 6; ++b) patch[a][b] = xs[im][(2 * ph + a) * 28 + 2 * pw + b];
-    float pooled[4];
+    for (int i = 0; i < 5; ++i) {
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int f = 4 * g + t;
-      float c00 = 0.f, c01 = 0.f, c10 = 0.f, c11 = 0.f;
+      for (int c = 0; c < 6; ++c) r1[c] = xp[(i + 1) * 28 + c];
 #pragma unroll
-      for (int i = 0; i < 5; ++i)
+      for (int j = 0; j < 5; ++j) {
+        fma2(acc[0][0], r0[j], wp[i * 5 + j]);
+        fma2(acc[0][1], r0[j + 1], wp[i * 5 + j]);
+        fma2(acc[1][0], r1[j], wp[i * 5 + j]);
+        fma2(acc[1][1], r1[j + 1], wp[i * 5 + j]);
+      }
 #pragma unroll
-        for (int j = 0; j < 5; ++j) {
-          const float wv = ws[f][i * 5 + j];
-          c00 = fmaf(wv, patch[i][j], c00);
-          c01 = fmaf(wv, patch[i][j + 1], c01);
-          c10 = fmaf(wv, patch[i + 1][j], c10);
-          c11 = fmaf(wv, patch[i + 1][j + 1], c11);
-        }
-      const float bb = bs[f];
-      c00 += bb; c01 += bb; c10 += bb; c11 += bb;
+      for (int c = 0; c < 6; ++c) r0[c] = r1[c];
+    }
+    float v[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {  // filter f0 + h
+      const float bb = h ? b1 : b0;
+      const float c00 = (h ? hi32(acc[0][0]) : lo32(acc[0][0])) + bb, c01 = (h ? hi32(acc[0][1]) : lo32(acc[0][1])) + bb;
+      const float c10 = (h ? hi32(acc[1][0]) : lo32(acc[1][0])) + bb, c11 = (h ? hi32(acc[1][1]) : lo32(acc[1][1])) + bb;
       float best = c00;
       int off = 0;
       if (c01 > best) { best = c01; off = 1; }
       if (c10 > best) { best = c10; off = 2; }
       if (c11 > best) { best = c11; off = 3; }
-      const long long o = ((long long)n * 20 + f) * 144 + q;
       // TF32 plan: round to nearest, ties away (the conv2 operand rounding)
-      pooled[t] = p.round_tf32 ? __uint_as_float((__float_as_uint(best) + 0x1000u) & 0xFFFFE000u) : best;
-      p.p1[o] = pooled[t];
+      v[h] = p.round_tf32 ? __uint_as_float((__float_as_uint(best) + 0x1000u) & 0xFFFFE000u) : best;
+      const long long o = ((long long)n * 20 + f0 + h) * 144 + q;
+      p.p1[o] = v[h];
       p.m1[o] = (uint8_t)off;
     }
-    if (p.p1c)  // [pair][cc = g][h = ph][n = im][w = pw][4 c]: the block's 2 images are one pair
-      reinterpret_cast<float4*>(p.p1c)[(size_t)blockIdx.x * 1440 + (g * 12 + ph) * 24 + im * 12 + pw] =
-          make_float4(pooled[0], pooled[1], pooled[2], pooled[3]);
+    if (p.p1c)  // [pair][cc][h][n][w][4 c]: this thread's two channels are adjacent
+      *reinterpret_cast<float2*>(p.p1c + ((size_t)blockIdx.x * 1440 + ((f0 >> 2) * 12 + ph) * 24 + im * 12 + pw) * 4 +
+                                 (f0 & 3)) = make_float2(v[0], v[1]);
   }
 }
 
@@ -253,7 +273,8 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     w2[o] = valid ? __ldg(p.w + o * 500 + k) : 0.f;
     acc[o] = 0.f;
   }
-  pdl_enter();
+  // dz comes from ip2+loss two launches back, a1 from further back: nothing
+  // is read from the predecessor (the loss reduction), so wait only at the end
   float bacc = 0.f, b1acc = 0.f;
   for (int mb = m0; mb < m1; mb += 16) {
     const int cnt = min(16, m1 - mb);
@@ -305,6 +326,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     if (p.part_b1) p.part_b1[(long long)s * 500 + k] = b1acc;  // db1 = sum_m da1[m,k]
   }
   if (blockIdx.x == 0 && threadIdx.x < 10) p.part_b[(long long)s * p.pstride + threadIdx.x] = bacc;
+  pdl_enter();
 }
 
 // dp2 [N, 50*16] + mask -> dense conv2 output gradient G2 [N,50,8,8]
@@ -325,13 +347,15 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // ---------------------------------------------------- conv1 weight gradient
 // dW1[f,i,j] = sum_n sum_q dp1[n,f,q] * x[n, h_q + i, w_q + j] where (h_q,w_q)
 // is the conv1 position pool1 routed gradient q to (P:220-222 composed with
-// S:351); db1[f] = sum dp1.  grid = splits over images (<= 4 images per
+// S:351); db1[f] = sum dp1.  grid = splits over images (<= 2 images per
 // block), block = 320 threads (20 filters x 16 lanes), images staged in smem;
 // every (gradient, origin) pair of the block is loaded up front so the 36
 // global loads per thread are in flight together.
-constexpr int CW_IMGS = 4;
+// dp1 comes from conv2's data gradient two launches back (the predecessor,
+// conv2's weight gradient, produces nothing read here): the kernel runs
+// alongside it and waits only at the end (pdl.cuh).
+constexpr int CW_IMGS = 2;
 __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
-  pdl_enter();
   __shared__ float xs[CW_IMGS][784];
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
@@ -382,6 +406,7 @@ __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__
     for (int t = 0; t < 25; ++t) p.part_w[(long long)s * p.pstride + f * 25 + t] = acc[t];
     p.part_b[(long long)s * p.pstride + f] = bacc;
   }
+  pdl_enter();
 }
 
 }  // namespace pn

@@ -408,8 +408,8 @@ static pn_status allocate(pn_net* net) {
   for (auto& L : net->layers) {
     if (L.off < 0) continue;
     // conv1's fused weight gradient is a light SIMT kernel: give it more
-    // CTAs (4 images each at batch 512)
-    L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 3) / 4 : kWgradSplits;
+    // CTAs (2 images each)
+    L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 1) / 2 : kWgradSplits;
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
     L.part_off = poff;
@@ -499,8 +499,10 @@ static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const
   add(v, name, l);
 }
 
-static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs) {
+static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs,
+                             bool late = false) {
   ReduceMultiP m{};
+  m.late = late ? 1 : 0;
   m.nseg = (int)segs.size();
   m.total = 0;
   for (size_t i = 0; i < segs.size() && i < 6; ++i) {
@@ -639,7 +641,7 @@ static void build_fused_lenet(pn_net* net) {
     // stored TF32-rounded; the mask is taken before rounding
     Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c};
     Launch l;
-    l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(288), 0, p);
+    l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(320), 0, p);
     add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
   }
   if (net->tf32) {
@@ -688,7 +690,8 @@ static void build_fused_lenet(pn_net* net) {
   if (net->tf32) {
     ip_segs.push_back(seg(net->part_b1, G + i1.off + i1.wcount, 500, i2.splits, 500));
     add(bwd, "ip1.wgrad[tc]", tc::ip1_wgrad_launch(net->da1rT, net->p2T, G + i1.off, N, net->npad));
-    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs);
+    // the ip partials come from ip2's backward, two launches back (pdl.cuh)
+    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
     conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
@@ -701,7 +704,7 @@ static void build_fused_lenet(pn_net* net) {
     Launch l2;
     l2.set((const void*)colsum_generic, dim3(500), dim3(256), 0, c);
     add(bwd, "ip1.bgrad", l2);
-    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs);
+    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
     GemmP d{a1.diff, P + i1.off, p2.diff, nullptr, N, 800, 500, 500, 1, 800, 1, 0};
     Launch l3;
     l3.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(N, 64)), dim3(256), 0, d);

@@ -36,6 +36,7 @@ struct ReduceP {  // out[i] = sum_s part[s*stride + i], i < n (fixed order s = 0
 struct ReduceMultiP {  // several ReduceP segments in one launch
   ReduceP seg[6];
   int nseg, total;
+  int late;  // inputs come from >= 2 launches back: wait on the predecessor only at the end (pdl.cuh)
 };
 struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   const float* x;
