@@ -15,15 +15,16 @@
 namespace pn {
 
 // ------------------------------------------------------------ conv1 + pool1
-// Block = one image pair, 320 threads: warp w owns filters (2w, 2w+1) with
-// their 25 weights held in registers as (w_2w, w_2w+1) pairs; lane l takes
-// pooled positions q = l, l+32, ... of both images.  Per pooled position the
-// four conv values of the 2x2 window (25 MACs each, tap order i-major, bias
-// added after the sum: S:297 with P:136) are computed for both filters at
-// once with packed fp32 FMAs (FFMA2: fma.rn.f32x2, two independent
-// round-to-nearest FMAs -- the same arithmetic as scalar fmaf), the input
-// patch streamed row by row from shared memory.  Ties: first of
-// (0,0),(0,1),(1,0),(1,1).
+// Items = (image, pooled position q) over the whole batch, split evenly over
+// a grid of 2 blocks per SM (each block stages the <= 3 images its contiguous
+// item range touches).  Block = 320 threads: warp w owns filters (2w, 2w+1)
+// with their 25 weights held in registers as (w_2w, w_2w+1) pairs; lane l
+// takes items l, l+32, ...  Per item the four conv values of the 2x2 pool
+// window (25 MACs each, tap order i-major, bias added after the sum: S:297
+// with P:136) are computed for both filters at once with packed fp32 FMAs
+// (FFMA2 = fma.rn.f32x2: two independent round-to-nearest FMAs, the same
+// arithmetic as scalar fmaf), the input patch streamed row by row from
+// shared memory one row ahead.  Ties: first of (0,0),(0,1),(1,0),(1,1).
 __device__ __forceinline__ unsigned long long pk2(float a, float b) {
   unsigned long long r;
   asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
@@ -35,39 +36,46 @@ __device__ __forceinline__ void fma2(unsigned long long& d, float a, unsigned lo
 __device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
 __device__ __forceinline__ float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
 
-constexpr int C1_IMGS = 2;
-__global__ void __launch_bounds__(320) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
-  // inputs (the batch) and weights (previous step's SGD) are complete at
-  // launch (pdl.cuh): stage them before waiting on the predecessor
-  __shared__ float xs[C1_IMGS][28 * 28];
-  const int n0 = blockIdx.x * C1_IMGS;
+constexpr int C1_MAXIMG = 4;  // images a block's item range can touch
+__global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+  // everything read here (the batch, conv1's weights from the previous
+  // step's SGD) is complete at launch and the predecessor (the TF32 weight
+  // packing) touches none of it: run alongside it, wait only at the end
+  // (pdl.cuh)
+  __shared__ float xs[C1_MAXIMG][28 * 28];
+  const int i0 = blockIdx.x * p.per_block, i1 = min(i0 + p.per_block, p.N * 144);
+  if (i0 >= i1) {
+    pdl_enter();
+    return;
+  }
+  const int nlo = i0 / 144, nimg = (i1 - 1) / 144 - nlo + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f0 = 2 * warp;
-  for (int i = threadIdx.x; i < C1_IMGS * 784; i += blockDim.x) {
-    const int im = i / 784, e = i % 784;
-    xs[im][e] = (n0 + im < p.N) ? __ldg(p.x + (long long)(n0 + im) * 784 + e) : 0.f;
-  }
+  for (int i = threadIdx.x; i < nimg * 784; i += blockDim.x)
+    xs[i / 784][i % 784] = __ldg(p.x + (long long)nlo * 784 + i);
   unsigned long long wp[25];
 #pragma unroll
   for (int t = 0; t < 25; ++t) wp[t] = pk2(__ldg(p.w + f0 * 25 + t), __ldg(p.w + (f0 + 1) * 25 + t));
   const float b0 = __ldg(p.b + f0), b1 = __ldg(p.b + f0 + 1);
-  pdl_enter();
   __syncthreads();
 #pragma unroll 1
-  for (int it = lane; it < C1_IMGS * 144; it += 32) {
-    const int im = it / 144, q = it - im * 144;
-    const int n = n0 + im;
-    if (n >= p.N) break;
+  for (int it = i0 + lane; it < i1; it += 32) {
+    const int n = it / 144, q = it - n * 144, im = n - nlo;
     const int ph = q / 12, pw = q - ph * 12;
     const float* xp = &xs[im][(2 * ph) * 28 + 2 * pw];
     unsigned long long acc[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
-    float r0[6], r1[6];
+    float r0[6], r1[6], r2[6];
 #pragma unroll
-    for (int c = 0; c < 6; ++c) r0[c] = xp[c];
+    for (int c = 0; c < 6; ++c) {
+      r0[c] = xp[c];
+      r1[c] = xp[28 + c];
+    }
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
+      if (i < 4) {
 #pragma unroll
-      for (int c = 0; c < 6; ++c) r1[c] = xp[(i + 1) * 28 + c];
+        for (int c = 0; c < 6; ++c) r2[c] = xp[(i + 2) * 28 + c];
+      }
 #pragma unroll
       for (int j = 0; j < 5; ++j) {
         fma2(acc[0][0], r0[j], wp[i * 5 + j]);
@@ -76,7 +84,10 @@ __global__ void __launch_bounds__(320) lenet_conv1_pool1(const __grid_constant__
         fma2(acc[1][1], r1[j + 1], wp[i * 5 + j]);
       }
 #pragma unroll
-      for (int c = 0; c < 6; ++c) r0[c] = r1[c];
+      for (int c = 0; c < 6; ++c) {
+        r0[c] = r1[c];
+        r1[c] = r2[c];
+      }
     }
     float v[2];
 #pragma unroll
@@ -96,9 +107,10 @@ __global__ void __launch_bounds__(320) lenet_conv1_pool1(const __grid_constant__
       p.m1[o] = (uint8_t)off;
     }
     if (p.p1c)  // [pair][cc][h][n][w][4 c]: this thread's two channels are adjacent
-      *reinterpret_cast<float2*>(p.p1c + ((size_t)blockIdx.x * 1440 + ((f0 >> 2) * 12 + ph) * 24 + im * 12 + pw) * 4 +
+      *reinterpret_cast<float2*>(p.p1c + ((size_t)(n >> 1) * 1440 + ((f0 >> 2) * 12 + ph) * 24 + (n & 1) * 12 + pw) * 4 +
                                  (f0 & 3)) = make_float2(v[0], v[1]);
   }
+  pdl_enter();
 }
 
 // ------------------------------------------------------------ conv2 + pool2

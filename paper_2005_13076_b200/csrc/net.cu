@@ -633,15 +633,18 @@ static void build_fused_lenet(pn_net* net) {
   if (net->tf32) {  // TF32 weight copies for this step's contractions
     net->pack.w1 = P + i1.off;
     net->pack.w2 = P + c2.off;
-    add(fwd, "wpack[tc]", tc::pack_weights_launch(net->pack));
-    add(fwd, "w1t[tc]", tc::transpose_w1_launch(net->pack));
+    add(fwd, "wpack[tc]", tc::pack_weights_launch(net->pack));  // overlaps conv1+pool1 (late wait)
   }
   {
     // TF32 plan: pool1 is consumed only by conv2's contractions, so it is
     // stored TF32-rounded; the mask is taken before rounding
-    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c};
+    // items (image, pooled position) split evenly over 2 blocks per SM
+    // (at least one block per image pair: a block's range then touches <= 3 images)
+    const int blocks = std::max(std::max(1, std::min(2 * net->tc_sms, N * 144 / 32)), (N + 1) / 2);
+    const int per = (int)cdiv((long long)N * 144, blocks);
+    Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c, per};
     Launch l;
-    l.set((const void*)lenet_conv1_pool1, dim3(cdiv(N, 2)), dim3(320), 0, p);
+    l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(320), 0, p);
     add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
   }
   if (net->tf32) {
@@ -808,20 +811,26 @@ static pn_status build_plan(pn_net* net) {
 }
 
 // --------------------------------------------------------------- execution
-static pn_status run_stage(pn_net* net, Stage& s, const StepArgs& a, cudaStream_t st) {
+// pdl_ok: this stage directly follows its planned predecessor kernel
+static pn_status run_stage(pn_net* net, Stage& s, const StepArgs& a, cudaStream_t st, bool pdl_ok = false) {
   if (s.custom) {
     cudaError_t e = s.custom(st);
     if (e != cudaSuccess) return fail(net->comm ? PN_ERR_NCCL : PN_ERR_CUDA, "stage " + s.name + " failed");
     return PN_OK;
   }
   if (s.patch) s.patch(s.L, a);
-  cudaError_t e = s.L.launch(st);
+  cudaError_t e = s.L.launch(st, pdl_ok);
   if (e != cudaSuccess) return fail(PN_ERR_CUDA, "launch " + s.name + ": " + cudaGetErrorString(e));
   return PN_OK;
 }
 
+// a phase run eagerly: its first kernel follows whatever the caller enqueued
 static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t st) {
-  for (auto& s : net->phase[ph]) TRY(run_stage(net, s, a, st));
+  bool prev_kernel = false;
+  for (auto& s : net->phase[ph]) {
+    TRY(run_stage(net, s, a, st, prev_kernel));
+    prev_kernel = !s.custom;
+  }
   return PN_OK;
 }
 
@@ -846,9 +855,11 @@ static StepArgs make_args(pn_net* net, const float* x, const int32_t* labels, fl
 static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_t* out, bool infer) {
   if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
   CU(cudaStreamBeginCapture(net->cap, cudaStreamCaptureModeThreadLocal));
+  bool prev_kernel = false;  // the captured step is one fixed sequence across phases
   for (int ph = 0; ph < nph; ++ph)
     for (auto& s : net->phase[ph]) {
-      pn_status st = run_stage(net, s, a, net->cap);
+      pn_status st = run_stage(net, s, a, net->cap, prev_kernel);
+      prev_kernel = !s.custom;
       if (st != PN_OK) {
         cudaGraph_t g;
         cudaStreamEndCapture(net->cap, &g);

@@ -120,6 +120,7 @@ struct Conv1Pool1P {  // x[N,1,28,28] -> p1[N,20,12,12], m1 (uint8 offsets)
   int N;
   int round_tf32;  // store p1 rounded to TF32 (RNA) for the tensor-core plan
   float* p1c;      // optional: TF32 copy in the conv2 tap-GEMM layout (tc.h kP1cPairFloats per pair)
+  int per_block;   // pooled (image, position) items per block (grid = ceil(N*144 / per_block))
 };
 struct Conv2Pool2P {  // p1[N,20,12,12] -> p2[N,50,4,4], m2
   const float* p1;

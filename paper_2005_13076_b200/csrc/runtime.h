@@ -42,7 +42,7 @@ struct Launch {
   P& params() {
     return *reinterpret_cast<P*>(arg.data());
   }
-  // every launch allows programmatic dependent launch (pdl.cuh) unless PN_PDL=0
+  // planned launches allow programmatic dependent launch (pdl.cuh) unless PN_PDL=0
   static bool pdl() {
     static const bool on = [] {
       const char* e = getenv("PN_PDL");
@@ -50,7 +50,10 @@ struct Launch {
     }();
     return on;
   }
-  cudaError_t launch(cudaStream_t st) {
+  // pdl_ok: the previous operation on `st` is the planned predecessor kernel
+  // (inside a phase / a captured step); stand-alone launches stay fully
+  // stream-ordered (the kernels' griddepcontrol instructions are then no-ops)
+  cudaError_t launch(cudaStream_t st, bool pdl_ok = false) {
     void* a[1] = {arg.data()};
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
@@ -59,7 +62,7 @@ struct Launch {
     cfg.stream = st;
     cudaLaunchAttribute at[2];
     unsigned n = 0;
-    if (pdl()) {
+    if (pdl_ok && pdl()) {
       at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[n++].val.programmaticStreamSerializationAllowed = 1;
     }

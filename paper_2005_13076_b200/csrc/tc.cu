@@ -1045,15 +1045,28 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
 //   W2c [25 taps][5 cc][50 f][4 c] = W2[f, 4cc + c, tap]   (conv2 fwd B)
 //   W2t [4][128][64]: W2t[m][r][f] = W2[f, 5m + r/25, tap r%25]  (conv2 dgrad A)
 //   W1t [800][512]  = W1^T                    (ip1 dgrad B; tiled transpose)
-constexpr int W1F_N = 500 * 800, W2C_N = 25 * 5 * 50 * 4, W2T_N = 4 * 128 * 64;
+constexpr int W2C_N = 25 * 5 * 50 * 4, W2T_N = 4 * 128 * 64;
+constexpr int W1_TILES = (800 / 32) * (512 / 32);  // 32 x 32 tiles of W1 (o padded to 512)
+// One launch: blocks [0, W1_TILES) copy + transpose a 32 x 32 tile of W1
+// through shared memory (W1f rows and W1t rows both coalesced); the rest pack
+// W2c and W2t element-wise.
 __global__ void pack_weights(const __grid_constant__ PackP p) {
   pdl_enter();
-  int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx < W1F_N) {
-    p.w1f[idx] = tf32f(p.w1[idx]);
+  if (blockIdx.x < W1_TILES) {
+    __shared__ float t[32][33];
+    const int k0 = (blockIdx.x % 25) * 32, o0 = (blockIdx.x / 25) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+    for (int y = ty; y < 32; y += 8) {
+      const int o = o0 + y;
+      const float v = o < 500 ? tf32f(p.w1[(size_t)o * 800 + k0 + tx]) : 0.f;
+      t[y][tx] = v;
+      if (o < 500) p.w1f[(size_t)o * 800 + k0 + tx] = v;
+    }
+    __syncthreads();
+    for (int y = ty; y < 32; y += 8) p.w1t[(size_t)(k0 + y) * 512 + o0 + tx] = t[tx][y];
     return;
   }
-  idx -= W1F_N;
+  int idx = (blockIdx.x - W1_TILES) * blockDim.x + threadIdx.x;
   if (idx < W2C_N) {
     const int c4 = idx & 3, f = (idx >> 2) % 50, cc = (idx / 200) % 5, tap = idx / 1000;
     p.w2c[idx] = tf32f(p.w2[f * 500 + (cc * 4 + c4) * 25 + tap]);
@@ -1090,19 +1103,6 @@ __global__ void pack_p1c_k(const __grid_constant__ PackP1cArgs a) {
   if (n < N)
     for (int t = 0; t < 4; ++t) v[t] = tf32f(p1[((size_t)n * 20 + cc * 4 + t) * 144 + h * 12 + w]);
   reinterpret_cast<float4*>(p1c)[idx] = make_float4(v[0], v[1], v[2], v[3]);
-}
-// W1t[k][o] = W1[o][k] (o < 500), 32x32 tiles through shared memory
-__global__ void transpose_w1(const __grid_constant__ PackP p) {
-  pdl_enter();
-  __shared__ float t[32][33];
-  const int k0 = blockIdx.x * 32, o0 = blockIdx.y * 32;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
-  for (int y = ty; y < 32; y += 8) {
-    const int o = o0 + y;
-    t[y][tx] = o < 500 ? p.w1[(size_t)o * 800 + k0 + tx] : 0.f;
-  }
-  __syncthreads();
-  for (int y = ty; y < 32; y += 8) p.w1t[(size_t)(k0 + y) * 512 + o0 + tx] = tf32f(t[tx][y]);
 }
 
 // ------------------------------------------------------------ host side
@@ -1185,13 +1185,7 @@ static unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) /
 
 Launch pack_weights_launch(const PackP& p) {
   Launch l;
-  l.set((const void*)pack_weights, dim3(cdiv(W1F_N + W2C_N + W2T_N, 256)), dim3(256), 0, p);
-  return l;
-}
-
-Launch transpose_w1_launch(const PackP& p) {
-  Launch l;
-  l.set((const void*)transpose_w1, dim3(800 / 32, 512 / 32), dim3(256), 0, p);
+  l.set((const void*)pack_weights, dim3(W1_TILES + cdiv(W2C_N + W2T_N, 256)), dim3(256), 0, p);
   return l;
 }
 

@@ -25,7 +25,6 @@ constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2cFloats = 25000
 cudaError_t setup();    // driver entry point + opt-in shared memory sizes
 bool tensor_maps_ok();  // false if any cuTensorMapEncodeTiled call failed
 Launch pack_weights_launch(const PackP& p);
-Launch transpose_w1_launch(const PackP& p);
 // conv2 forward operand layout p1c: per image pair [5 cc][12 h][2 n][12 w][4 c] floats
 constexpr int kP1cPairFloats = 5 * 12 * 2 * 12 * 4;
 Launch conv2_pool2_launch(const float* w2c, const float* b, const float* p1c, float* p2, float* p2T, uint8_t* m2,
