@@ -19,11 +19,11 @@ PROF = "profiles"
 os.makedirs(PROF, exist_ok=True)
 
 # stage names of the TF32 plan (bench.py's roofline table uses them)
-STAGE_OF = {"Conv2Fwd": "conv2+pool2[tc]", "IpFwd": "ip1+relu[tc]", "IpWgrad": "ip1.wgrad[tc]",
-            "IpDgradUnpool": "ip1.dgrad+unpool2[tc]", "Conv2Dgrad": "conv2.dgrad[tc]",
-            "Conv2Wgrad": "conv2.wgrad[tc]", "lenet_conv1_wgrad": "conv1.wgrad",
-            "lenet_conv1_pool1": "conv1+pool1", "lenet_ip2_loss": "ip2+softmax_loss",
-            "lenet_ip2_bwd": "ip2.bwd+relu1.bwd"}
+STAGE_OF = {"conv2_fwd_persistent": "conv2+pool2[tc]", "ip_splitk": "ip1+relu[tc]",
+            "conv2_dgrad_persistent": "conv2.dgrad[tc]", "conv2_wgrad_persistent": "conv2.wgrad[tc]",
+            "lenet_conv1_wgrad": "conv1.wgrad", "lenet_conv1_pool1": "conv1+pool1",
+            "lenet_ip2_loss": "ip2+softmax_loss", "lenet_ip2_bwd": "ip2.bwd+relu1.bwd",
+            "pack_weights": "wpack[tc]", "sgd_update_kernel": "sgd"}
 
 
 def launches(path):
