@@ -28,6 +28,23 @@ DATASET_BATCHES = 128
 METRIC = "LeNet train images/sec (device-timed) at 1/2/4/8 B200; % of layer roofline"
 UNIT = "images/s"
 
+# BASELINE.json configs timed by this script: config 3 (the headline, default)
+# and, with --workload, config 4 (cifar10_quick) and config 5 (AlexNet conv
+# trunk, the conv sweep).  Each cycles a resident dataset larger than L2.
+WORKLOADS = {
+    "lenet": {"spec": "lenet", "batch": 512, "nb": 128,
+              "desc": "LeNet train step (fwd+bwd+SGD momentum), batch 512 per GPU, synthetic MNIST-shaped input "
+                      "(BASELINE config 3)", "metric": METRIC},
+    "cifar10_quick": {"spec": "cifar10_quick", "batch": 256, "nb": 48,
+                      "desc": "Caffe cifar10_quick train step (fwd+bwd+SGD momentum), batch 256 per GPU, "
+                              "synthetic CIFAR-shaped input (BASELINE config 4)",
+                      "metric": "cifar10_quick train images/sec (device-timed); % of layer roofline"},
+    "alexnet_conv": {"spec": "alexnet_conv", "batch": 128, "nb": 2,
+                     "desc": "AlexNet conv trunk (conv1-5 ungrouped + ReLU + max pools + 10-way ip + loss) train "
+                             "step, batch 128, synthetic ImageNet-shaped 3x227x227 input (BASELINE config 5 sweep)",
+                     "metric": "AlexNet conv trunk train images/sec (device-timed); conv tensor-pipe utilisation"},
+}
+
 
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -65,6 +82,82 @@ def stage_work(name, N):
     if base.endswith(".wgrad_reduce"):
         return (0, 0)
     return table.get(base)
+
+
+def parse_layers(text):
+    """[input] + [layer] sections of a spec (key = value lines) -> list of dicts
+    with shapes inferred (plumbing for the roofline table; no layer math)."""
+    secs, cur = [], None
+    for line in text.splitlines():
+        line = line.split("#", 1)[0].strip()
+        if not line:
+            continue
+        if line.startswith("["):
+            cur = {"_kind": line.strip("[]")}
+            secs.append(cur)
+        elif "=" in line and cur is not None:
+            k, v = (t.strip() for t in line.split("=", 1))
+            cur[k] = v
+    inp = secs[0]
+    shapes = {inp["name"]: (int(inp["channels"]), int(inp["height"]), int(inp["width"]))}
+    out = []
+    for L in secs[1:]:
+        C, H, W = shapes[L["bottom"]]
+        t, k, st, p = L["type"], int(L.get("kernel_size", 1)), int(L.get("stride", 1)), int(L.get("pad", 0))
+        d = {"name": L["name"], "type": t, "in": (C, H, W)}
+        if t == "Convolution":
+            F = int(L["num_output"])
+            Ho, Wo = (H + 2 * p - k) // st + 1, (W + 2 * p - k) // st + 1
+            d.update(out=(F, Ho, Wo), params=F * C * k * k + F, macs=F * C * k * k * Ho * Wo)
+        elif t == "Pooling":
+            Ho = -(-(H + 2 * p - k) // st) + 1
+            Wo = -(-(W + 2 * p - k) // st) + 1
+            d.update(out=(C, Ho, Wo), max=L.get("pool", "MAX") == "MAX")
+        elif t == "InnerProduct":
+            No = int(L["num_output"])
+            d.update(out=(No, 1, 1), params=No * C * H * W + No, macs=No * C * H * W)
+        else:
+            d.update(out=(C, H, W))
+        shapes[L["top"]] = d["out"]
+        out.append(d)
+    return out
+
+
+def layer_stage_work(layers, name, N):
+    """Algorithmic (flops, bytes) of one stage of the layerwise plan at batch N:
+    compulsory fp32 reads + writes of the stage (weights once, masks int32)."""
+    base = name.split("[")[0]
+    lname, _, op = base.rpartition(".")
+    by = {L["name"]: L for L in layers}
+    if base == "loss_reduce":
+        return (0, N * 4 + 4)
+    if base == "sgd":
+        return (0, sum(L.get("params", 0) for L in layers) * 20)
+    L = by.get(lname)
+    if L is None:
+        return None
+    cin = N * L["in"][0] * L["in"][1] * L["in"][2] * 4
+    cout = N * L["out"][0] * L["out"][1] * L["out"][2] * 4
+    P = L.get("params", 0) * 4
+    if L["type"] in ("Convolution", "InnerProduct"):
+        fl = 2 * N * L["macs"]
+        if op == "fwd":
+            return (fl, cin + cout + P)
+        if op in ("wgrad", "dgrad"):
+            return (fl, cin + cout + P)
+        if op == "bgrad":
+            return (0, cout + P)
+        if op.startswith("wpack"):
+            return (0, 2 * P)
+        if op == "wgrad_reduce":
+            return (0, 2 * P)
+    if L["type"] == "Pooling":
+        return (0, cin + cout + (cout if L["max"] else 0))
+    if L["type"] == "ReLU":
+        return (0, 2 * cin if op == "fwd" else 3 * cin)
+    if L["type"] == "SoftmaxWithLoss":
+        return (0, cin * 3 + N * 8)
+    return None
 
 
 class Clocks:
@@ -124,44 +217,57 @@ def dist_setup(args):
     return world, rank, local
 
 
-def cpu_baseline(steps=8, batch=64):
-    """The oracle as it stands, single-threaded, on a bounded sample."""
-    import numpy as np  # noqa: F401
+# oracle sample per workload: (batch per oracle step, steps) -- about 5-30 s of CPU
+ORACLE_SAMPLE = {"lenet": (64, 8), "cifar10_quick": (4, 4), "alexnet_conv": (1, 1)}
+
+
+def _oracle_setup(workload, batch):
     from oracle.net import OracleNet
     from paper_2005_13076_b200 import spec_text, synth
-    ref = OracleNet(spec_text("lenet"), batch)
+    ref = OracleNet(spec_text(WORKLOADS[workload]["spec"]), batch)
     ref.set_params(synth.xavier_params(ref.learnable(), seed=2, bias="zero"))
+    gen = {"lenet": lambda n, s: synth.mnist_like(n, seed=11, first=s * n),
+           "cifar10_quick": lambda n, s: synth.cifar_like(n, seed=11, first=s * n),
+           "alexnet_conv": lambda n, s: synth.imagenet_like_fast(n, seed=11 + s)}[workload]
+    return ref, gen
+
+
+def cpu_baseline(workload="lenet"):
+    """The oracle as it stands, single-threaded, on a bounded sample."""
+    batch, steps = ORACLE_SAMPLE[workload]
+    ref, gen = _oracle_setup(workload, batch)
     hist = {}
     t0 = time.perf_counter()
     for s in range(steps):
-        x, y = synth.mnist_like(batch, seed=11, first=s * batch)
+        x, y = gen(batch, s)
         ref.forward(x, y)
         g = ref.backward()
         ref.sgd_step(g["grads"], 0.01, 0.9, 5e-4, hist)
     dt = time.perf_counter() - t0
     return {"value": steps * batch / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": f"{steps} oracle steps x batch {batch} (fwd+bwd+sgd, fp64-accumulate C oracle) of the "
-                      f"LeNet batch-{BATCH} workload; {dt:.1f} s"}
+                      f"{workload} batch-{WORKLOADS[workload]['batch']} workload; {dt:.1f} s"}
 
 
 def run_reference(args):
+    """This tier's reference arm: the CPU oracle timed as it stands on the
+    host cores, on the same workload/config/metric as our arm (a bounded
+    sample per step: batch-b oracle steps, b per ORACLE_SAMPLE)."""
     world, rank, _ = dist_setup(args)
     if rank != 0:
         return 0
-    from oracle.net import OracleNet
-    from paper_2005_13076_b200 import spec_text, synth
-    batch = 8
-    ref = OracleNet(spec_text("lenet"), batch)
-    ref.set_params(synth.xavier_params(ref.learnable(), seed=2, bias="zero"))
+    WL = WORKLOADS[args.workload]
+    batch = {"lenet": 8, "cifar10_quick": 2, "alexnet_conv": 1}[args.workload]
+    ref, gen = _oracle_setup(args.workload, batch)
     hist = {}
 
     def step(s):
-        x, y = synth.mnist_like(batch, seed=11, first=s * batch)
+        x, y = gen(batch, s)
         ref.forward(x, y)
         g = ref.backward()
         ref.sgd_step(g["grads"], 0.01, 0.9, 5e-4, hist)
 
-    for s in range(args.warmup):
+    for s in range(min(args.warmup, 3)):
         step(s)
     budget = 150.0
     t0 = time.perf_counter()
@@ -173,15 +279,15 @@ def run_reference(args):
             break
     dt = time.perf_counter() - t0
     v = done * batch / dt
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": WL["metric"], "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": done, "warmup": args.warmup, "ms_per_step": 1e3 * dt / done,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": f"LeNet train step (fwd+bwd+SGD), batch {BATCH} workload sampled as "
-                                   f"batch-{batch} oracle steps", "global_batch": batch,
-                       "parallelism": "single-thread CPU oracle"},
+            "config": {"workload": WL["desc"], "global_batch": WL["batch"] * args.gpus,
+                       "per_gpu_batch": WL["batch"], "parallelism": f"dp{args.gpus}"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{done} steps x batch {batch}, {dt:.1f} s"},
+                             "sample": f"{done} single-threaded oracle steps x batch {batch} (a bounded sample "
+                                       f"of the batch-{WL['batch']} step), {dt:.1f} s"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     if done < args.steps:
         line["note"] = f"stopped after {budget:.0f} s time budget ({done} of {args.steps} steps)"
@@ -192,14 +298,21 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20000)
-    ap.add_argument("--warmup", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=None, help="default: 20000 (lenet), 2000 (cifar10_quick), "
+                    "40 (alexnet_conv)")
+    ap.add_argument("--warmup", type=int, default=None, help="default: 200 / 50 / 5")
+    ap.add_argument("--workload", default="lenet", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    dflt = {"lenet": (20000, 200), "cifar10_quick": (2000, 50), "alexnet_conv": (40, 5)}[args.workload]
+    if args.steps is None:
+        args.steps = dflt[0]
+    if args.warmup is None:
+        args.warmup = dflt[1]
     if args.impl == "reference":
         return run_reference(args)
 
@@ -207,7 +320,7 @@ def main():
     import torch
     import torch.distributed as dist
 
-    from paper_2005_13076_b200 import Net, make_sgd, synth
+    from paper_2005_13076_b200 import Net, make_sgd, spec_text, synth
     from paper_2005_13076_b200.dp import dp_bootstrap, max_over_ranks
 
     world, rank, local = dist_setup(args)
@@ -215,25 +328,34 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     tf32 = args.precision == "tf32"
-    net = Net("lenet", BATCH, device=local, tf32=tf32)
-    params = synth.xavier_params([("conv1", "", (20, 1, 5, 5), 20), ("conv2", "", (50, 20, 5, 5), 50),
-                                  ("ip1", "", (500, 800), 500), ("ip2", "", (10, 500), 10)],
-                                 seed=2, bias="zero")
+    WL = WORKLOADS[args.workload]
+    BATCH, NB = WL["batch"], WL["nb"]
+    layers = parse_layers(spec_text(WL["spec"]))
+    net = Net(WL["spec"], BATCH, device=local, tf32=tf32)
+    learn = []
+    for L in layers:
+        if "params" in L:
+            wd = net.blob_shape(L["name"] + ".w")
+            learn.append((L["name"], L["type"], tuple(d for d in wd if d > 0), int(net.blob_shape(L["name"] + ".b")[0])))
+    params = synth.xavier_params(learn, seed=2, bias="zero")
     net.set_params(params)
     if world > 1:
         dp_bootstrap(net, dist)   # library-owned NCCL communicator (id via the torch PG)
 
     # resident synthetic dataset (> L2), distinct per rank
-    xs, ys = synth.mnist_like_fast(BATCH * DATASET_BATCHES, seed=100 + rank)
-    X = torch.from_numpy(xs).cuda().view(DATASET_BATCHES, BATCH, 1, 28, 28)
-    Y = torch.from_numpy(ys).cuda().view(DATASET_BATCHES, BATCH)
+    gen = {"lenet": synth.mnist_like_fast, "cifar10_quick": synth.cifar_like_fast,
+           "alexnet_conv": synth.imagenet_like_fast}[args.workload]
+    xs, ys = gen(BATCH * NB, seed=100 + rank)
+    X = torch.from_numpy(xs).cuda().view(NB, BATCH, *xs.shape[1:])
+    Y = torch.from_numpy(ys).cuda().view(NB, BATCH)
+    img_floats = int(np.prod(xs.shape[1:]))
     loss = torch.zeros(1, device="cuda", dtype=torch.float32)
     sgd = make_sgd()
     stream = torch.cuda.current_stream()
 
     it = 0
     for _ in range(max(args.warmup, 3)):
-        net.net_train_step(X[it % DATASET_BATCHES], Y[it % DATASET_BATCHES], sgd, it, loss)
+        net.net_train_step(X[it % NB], Y[it % NB], sgd, it, loss)
         it += 1
     net.net_sync_errors()
 
@@ -246,7 +368,7 @@ def main():
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        net.net_train_step(X[it % DATASET_BATCHES], Y[it % DATASET_BATCHES], sgd, it, loss)
+        net.net_train_step(X[it % NB], Y[it % NB], sgd, it, loss)
         it += 1
     e1.record(stream)
     torch.cuda.synchronize()
@@ -280,7 +402,7 @@ def main():
     if world > 1:
         ms_e2e = max_over_ranks(ms_e2e, dist)
     e2e = {"value": world * BATCH * e2e_steps / (ms_e2e / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": BATCH * 784 * 4 + BATCH * 4, "d2h_bytes_per_step": 4,
+           "h2d_bytes_per_step": BATCH * img_floats * 4 + BATCH * 4, "d2h_bytes_per_step": 4,
            "steps": e2e_steps}
 
     # per-stage timing (CUDA events on the launching stream, eager steps)
@@ -290,7 +412,7 @@ def main():
     fp32_peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
     rows = []
     for ph, name, t_ms in prof:
-        w = stage_work(name, BATCH)
+        w = stage_work(name, BATCH) if args.workload == "lenet" else layer_stage_work(layers, name, BATCH)
         rows.append({"phase": ph, "stage": name, "ms": t_ms,
                      "flops": w[0] if w else None, "bytes": w[1] if w else None})
     dom = max(rows, key=lambda r: r["ms"])
@@ -312,7 +434,8 @@ def main():
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f)
-        roof["traffic"] = tr.get(args.precision, {}).get(dom["stage"])
+        roof["traffic"] = tr.get(args.precision if args.workload == "lenet" else f"{args.workload}_{args.precision}",
+                                 {}).get(dom["stage"])
     roof["peak_source"] = (f"{pk['src']} MEASURED_PEAKS.json: " +
                            ("TF32 = sustained bf16 x 1.1/2.25" if roof["bound"] == "tensor" else
                             "HBM copy GB/s" if roof["bound"] == "hbm" else
@@ -326,15 +449,14 @@ def main():
         step_roof_s += max((r["flops"] or 0) / (p * 1e12), (r["bytes"] or 0) / (pk["hbm"] * 1e9))
     step_s = ms / 1e3 / args.steps
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": WL["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "tf32" if tf32 else "f32",
         "data": "synthetic",
-        "config": {"workload": f"LeNet train step (fwd+bwd+SGD momentum), batch {BATCH} per GPU, "
-                               "synthetic MNIST-shaped input (BASELINE config 3)",
+        "config": {"workload": WL["desc"],
                    "global_batch": BATCH * world, "per_gpu_batch": BATCH,
-                   "parallelism": f"dp{world}", "l2": f"inputs larger than L2: {DATASET_BATCHES} resident "
-                   f"batches ({DATASET_BATCHES * BATCH * 784 * 4 / 1e6:.0f} MB) cycled",
+                   "parallelism": f"dp{world}", "l2": f"inputs larger than L2: {NB} resident "
+                   f"batches ({NB * BATCH * img_floats * 4 / 1e6:.0f} MB) cycled",
                    "final_loss": final_loss},
         "e2e": e2e,
         "gpu_launches": net.launches_per_step() * args.steps,
@@ -344,8 +466,14 @@ def main():
         "stages_ms": {f"{r['phase']}:{r['stage']}": round(r["ms"], 5) for r in rows},
         "clocks": clk,
     }
+    if args.workload != "lenet":
+        # tensor-pipe sweep of the convolution stages (BASELINE config 5)
+        line["conv_sweep"] = {r["stage"]: {"us": round(r["ms"] * 1e3, 2),
+                                           "tflops": round(r["flops"] / (r["ms"] / 1e3) / 1e12, 2),
+                                           "frac_tf32_peak": round(r["flops"] / (r["ms"] / 1e3) / 1e12 / tf32_peak, 4)}
+                              for r in rows if r["flops"] and "[tc]" in r["stage"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline()
+        line["cpu_baseline"] = cpu_baseline(args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
     net.close()

@@ -20,6 +20,7 @@
 #include "kernels.h"
 #include "runtime.h"
 #include "tc.h"
+#include "tc_conv.h"
 
 using namespace pn;
 
@@ -67,6 +68,12 @@ struct Layer {
   int64_t wcount = 0, bcount = 0, off = -1;  // offset of w in the flat buffers, b follows w
   int64_t part_off = -1;                     // partial-sum region (split wgrads)
   int splits = 0;
+  // layerwise TF32 plan (tc_conv.cu): packed B images of the forward and
+  // data-gradient contractions
+  float* bfwd = nullptr;
+  float* bdg = nullptr;
+  int fwd_rows = 0, fwd_nk = 0, dg_rows = 0, dg_nk = 0;
+  bool tc_conv = false, tc_dgrad = false;
 };
 
 struct Blob {
@@ -412,6 +419,9 @@ static pn_status allocate(pn_net* net) {
     L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 1) / 2 : kWgradSplits;
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
+    if (L.tc_conv)
+      L.splits = tcc::wgrad_splits(net->batch, L.out[2], L.out[3], L.F, (int)(L.wcount / L.F), L.bias ? 1 : 0,
+                                   net->tc_sms);
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
   }
@@ -430,6 +440,10 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->da1rT, (size_t)500 * net->npad));
     TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
     TRY(net->alloc(&net->part_db2, (size_t)tc::db2_partials(net->batch) * 50));
+  }
+  for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images
+    if (L.tc_conv) TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
+    if (L.tc_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
   }
   TRY(net->alloc(&net->err, 1));
   // activation blobs (the fused plan never stores conv1's output or its
@@ -531,7 +545,21 @@ static void build_layerwise(pn_net* net) {
     const float* x = in_data(net, L, &isx);
     Blob* top = L.type == L_LOSS ? nullptr : &net->blobs[net->blob(L.top)];
     Launch l;
-    if (L.type == L_CONV) {
+    if (L.type == L_CONV && L.tc_conv) {
+      // TF32 images of W for this step's forward and data-gradient contractions
+      ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
+      add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
+      if (L.tc_dgrad) {
+        ConvPackP pd{net->params + L.off, L.bdg, L.F, L.in[1], L.kh, L.kw, L.dg_rows, L.dg_nk, 1};
+        add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_launch(pd));
+      }
+      ConvTcP p{x, L.bfwd, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
+                N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
+                L.in[1] * L.kh * L.kw, L.fwd_nk, L.fwd_rows, 0};
+      add(fwd, L.name + ".fwd[tc]", tcc::conv_fwd_launch(p),
+          isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcP>().x = a.x; }
+              : std::function<void(Launch&, const StepArgs&)>());
+    } else if (L.type == L_CONV) {
       ConvFwdP p{x, net->params + L.off, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
                  N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
       l.set((const void*)conv_fwd_generic, dim3(cdiv((long long)N * L.F * L.out[2] * L.out[3], 256)), dim3(256), 0, p);
@@ -571,7 +599,27 @@ static void build_layerwise(pn_net* net) {
     Blob& top = net->blobs[net->blob(L.top)];
     Blob* bot = isx ? nullptr : &net->blobs[net->blob(L.bottom)];
     Launch l;
-    if (L.type == L_CONV) {
+    if (L.type == L_CONV && L.tc_conv) {
+      const int K = L.in[1] * L.kh * L.kw;
+      ConvTcWgradP w{top.diff, x, net->partials + L.part_off, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
+                     L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3], K, L.bias ? 1 : 0, L.splits,
+                     (int)(L.wcount + L.bcount)};
+      add(bwd, L.name + ".wgrad[tc]", tcc::conv_wgrad_launch(w),
+          isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcWgradP>().x = a.x; }
+              : std::function<void(Launch&, const StepArgs&)>());
+      add_reduce(net, bwd, L);
+      if (bot && L.tc_dgrad) {  // dx = W'(*)G: stride 1, pad kh-1-p, output H x W
+        ConvTcP q{top.diff, L.bdg, nullptr, bot->diff, N, L.F, L.out[2], L.out[3], L.in[1], L.kh, L.kw, 1, 1,
+                  L.kh - 1 - L.ph, L.kw - 1 - L.pw, L.in[2], L.in[3], L.F * L.kh * L.kw, L.dg_nk, L.dg_rows, 0};
+        add(bwd, L.name + ".dgrad[tc]", tcc::conv_fwd_launch(q));
+      } else if (bot) {
+        ConvBwdDataP q{top.diff, net->params + L.off, bot->diff, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
+                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+        Launch l2;
+        l2.set((const void*)conv_bwd_data_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, q);
+        add(bwd, L.name + ".dgrad", l2);
+      }
+    } else if (L.type == L_CONV) {
       ConvBwdWeightP p{top.diff, x, net->partials + L.part_off, L.bcount ? net->partials + L.part_off + L.wcount : nullptr,
                        N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
                        L.splits, (int)(L.wcount + L.bcount)};
@@ -921,16 +969,32 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
   TRY(parse_and_infer(net.get(), spec));  // host-only: spec errors need no GPU
   CU(cudaSetDevice(device));
   net->fused = !(flags & PN_LAYERWISE) && is_lenet(net.get());
-  if (net->tf32 && !net->fused)
-    return fail(PN_ERR_INVALID_ARG, "PN_TF32 needs the fused LeNet plan (this net has no tensor-core plan yet)");
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   net->tc_sms = sms;
+  int max_nk = 1;
+  if (net->tf32 && !net->fused) {
+    // layerwise TF32 plan: every convolution on the general tcgen05 kernels
+    // (tc_conv.cu); the data gradient needs stride 1 and pad < kernel (else
+    // the generic fp32 kernel computes it)
+    for (auto& L : net->layers) {
+      if (L.type != L_CONV) continue;
+      L.tc_conv = true;
+      L.fwd_rows = tcc::fwd_rows_pad(L.F);
+      L.fwd_nk = (L.in[1] * L.kh * L.kw + 31) / 32;
+      L.tc_dgrad = L.bottom != net->input_name && L.sh == 1 && L.sw == 1 && L.ph < L.kh && L.pw < L.kw;
+      if (L.tc_dgrad) {
+        L.dg_rows = tcc::fwd_rows_pad(L.in[1]);
+        L.dg_nk = (L.F * L.kh * L.kw + 31) / 32;
+      }
+      max_nk = std::max(max_nk, std::max(L.fwd_nk, L.dg_nk));
+    }
+  }
   TRY(allocate(net.get()));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (50 * 20 * 28 + 2 * 2880) * 4));
   if (net->tf32) {
-    cudaError_t e = tc::setup();
+    cudaError_t e = net->fused ? tc::setup() : tcc::setup(max_nk);
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }
   TRY(build_plan(net.get()));

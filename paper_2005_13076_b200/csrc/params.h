@@ -174,4 +174,28 @@ struct Conv1WgradP {  // dp1 + m1 + x -> partial dW1, db1
   int N, splits, pstride;
 };
 
+
+// --------------------------------------------- general tensor-core conv (tc_conv.cu)
+struct ConvTcP {  // y = W (*) x (+ b) (relu), implicit GEMM on tcgen05
+  const float* x;    // gathered activation NCHW [N][C][H][W]
+  const float* bpk;  // packed TF32 B image [nk][Fpad][32] (pack_conv_weights)
+  const float* bias; // [F] or nullptr
+  float* y;          // [N][F][Ho][Wo]
+  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  int K, nk, Fpad;   // K = C*kh*kw, nk = ceil(K/32), Fpad = rows of the B image
+  int relu;
+};
+struct ConvTcWgradP {  // split-m partials of dW = G^T col (+ db as the ones column)
+  const float* g;  // top diff [N][F][Ho][Wo]
+  const float* x;  // bottom data [N][C][H][W]
+  float* part;     // [splits][pstride]: w at f*K + k, b at F*K + f
+  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  int K, bias_col, splits, pstride;
+};
+struct ConvPackP {  // TF32 B image of the forward (mode 0) / data-gradient (mode 1) contraction
+  const float* w;   // [F][C][kh][kw]
+  float* out;       // [nk][rows][32] SW128
+  int F, C, kh, kw, rows, nk, mode;
+};
+
 }  // namespace pn

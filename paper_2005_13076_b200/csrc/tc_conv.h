@@ -1,0 +1,20 @@
+// tc_conv.h -- host entry points of the general tcgen05 TF32 convolution
+// (tc_conv.cu): forward, data gradient (as a flipped-filter stride-1
+// convolution), split-m weight gradient, and the per-step TF32 weight packing.
+#pragma once
+#include <cuda_runtime.h>
+
+#include "params.h"
+#include "runtime.h"
+
+namespace pn {
+namespace tcc {
+cudaError_t setup(int max_nk);  // opt-in shared memory for K up to max_nk*32
+int fwd_rows_pad(int F);        // rows of the packed B image for an output of F channels
+size_t fwd_smem_bytes(int F, int nk);
+Launch conv_fwd_launch(const ConvTcP& p);
+int wgrad_splits(int N, int Ho, int Wo, int F, int K, int bias, int sms);
+Launch conv_wgrad_launch(const ConvTcWgradP& p);
+Launch pack_launch(const ConvPackP& p);
+}  // namespace tcc
+}  // namespace pn

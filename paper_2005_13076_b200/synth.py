@@ -93,3 +93,21 @@ def normal(shape, seed, scale=1.0):
 
 def labels(n, d, seed):
     return rng(seed).integers(0, d, size=n).astype(np.int32)
+
+
+def cifar_like_fast(n, seed=1):
+    """CIFAR-shaped batch with cifar_like's distribution drawn in one call
+    (bench datasets; image i differs from cifar_like's)."""
+    g = rng([seed, 1 << 29])
+    x = g.integers(0, 256, size=(n, 3, 32, 32), dtype=np.uint8).astype(np.float32) / np.float32(256.0)
+    x -= _cifar_mean(seed)
+    return x, g.integers(0, 10, size=n).astype(np.int32)
+
+
+def imagenet_like_fast(n, seed=1, hw=227):
+    """ImageNet-shaped batch (n,3,hw,hw) for the AlexNet conv trunk: bytes
+    U{0..255}/256 minus 0.5 (a mean-subtracted image scale), labels U{0..9}."""
+    g = rng([seed, 1 << 28])
+    x = g.integers(0, 256, size=(n, 3, hw, hw), dtype=np.uint8).astype(np.float32) / np.float32(256.0)
+    x -= np.float32(0.5)
+    return x, g.integers(0, 10, size=n).astype(np.int32)

@@ -1,0 +1,174 @@
+"""GPU parity of the general tcgen05 TF32 convolution (tc_conv.cu) that runs
+every conv layer of the layerwise TF32 plan (cifar10_quick = SURVEY §8(a)
+row a19; AlexNet-shaped geometries = BASELINE config 5), against the CPU
+oracle on the same seeded inputs.
+
+Teacher forcing: each conv stage is fed the oracle's own input blob (bottom
+data for the forward, top diff + bottom data for the gradients), so the
+comparison isolates the kernel; the bound per element is rtol * S with S the
+oracle's sum of |terms| (SURVEY §8(c) tolerance reading), rtol = 2e-3 (TF32).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle.net import OracleNet
+from paper_2005_13076_b200 import PN_DIFF, Net, spec_text, synth
+from parity import RTOL, assert_close, assert_norm
+
+pytestmark = pytest.mark.gpu
+
+
+def conv_spec(C, H, W, convs, classes=10):
+    """input C x H x W -> conv chain (name, F, k, s, p[, pool k s]) -> ip(classes) -> loss."""
+    lines = ["[input]", "name = data", f"channels = {C}", f"height = {H}", f"width = {W}", ""]
+    bottom = "data"
+    for c in convs:
+        name, F, k, s, p = c[:5]
+        lines += ["[layer]", f"name = {name}", "type = Convolution", f"bottom = {bottom}", f"top = {name}",
+                  f"num_output = {F}", f"kernel_size = {k}", f"stride = {s}", f"pad = {p}", ""]
+        lines += ["[layer]", f"name = {name}_relu", "type = ReLU", f"bottom = {name}", f"top = {name}", ""]
+        bottom = name
+        if len(c) > 5:
+            pk, ps = c[5]
+            lines += ["[layer]", f"name = {name}_pool", "type = Pooling", f"bottom = {bottom}",
+                      f"top = {name}_pool", "pool = MAX", f"kernel_size = {pk}", f"stride = {ps}", ""]
+            bottom = f"{name}_pool"
+    lines += ["[layer]", "name = fc", "type = InnerProduct", f"bottom = {bottom}", "top = fc",
+              f"num_output = {classes}", "", "[layer]", "name = loss", "type = SoftmaxWithLoss",
+              "bottom = fc", "top = loss", ""]
+    return "\n".join(lines)
+
+
+# AlexNet geometry (Caffe bvlc_alexnet, ungrouped) on a
+# reduced input so the single-threaded oracle finishes in seconds: the layer
+# shapes (11x11 s4, 5x5 p2, 3x3 p1, F = 96/256/384/384/256) are the real ones.
+ALEX_SMALL = conv_spec(3, 67, 67, [("conv1", 96, 11, 4, 0, (3, 2)), ("conv2", 256, 5, 1, 2, (3, 2)),
+                                   ("conv3", 384, 3, 1, 1), ("conv4", 384, 3, 1, 1), ("conv5", 256, 3, 1, 1)])
+# ragged channel counts / kernels / paddings: F tiles with zero padding, two
+# row tiles in the weight gradient (F > 128), several column tiles (F > 256)
+ODD = conv_spec(5, 13, 11, [("ca", 7, 3, 2, 1), ("cb", 33, 4, 1, 2), ("cc", 130, 1, 1, 0), ("cd", 300, 3, 1, 1)])
+
+CASES = {"cifar10_quick": (lambda: spec_text("cifar10_quick"), 8),
+         "alexnet_small": (lambda: ALEX_SMALL, 2),
+         "odd": (lambda: ODD, 3)}
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def inputs(ref, N, seed=1):
+    """Byte-valued images centred at 0 (CIFAR-like recipe, any shape) and labels."""
+    rng = np.random.default_rng(seed)
+    x = rng.integers(0, 256, size=(N,) + tuple(ref.shapes[ref.input_name][1:])) / 256.0 - 0.5
+    return x.astype(np.float32), rng.integers(0, 10, size=N).astype(np.int32)
+
+
+def run_stage(net, phase, name, xd=None, yd=None):
+    names = net.stages(phase)
+    net.net_run_stage(phase, names.index(name), xd, yd)
+
+
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_conv_tc_teacher_forced(case):
+    make_spec, N = CASES[case]
+    spec = make_spec()
+    ref = OracleNet(spec, N)
+    params = synth.xavier_params(ref.learnable(), seed=2, bias="uniform")
+    ref.set_params(params)
+    net = Net(spec, N, tf32=True)
+    net.set_params(params)
+    if case == "cifar10_quick":
+        x, y = synth.cifar_like(N, seed=1)
+    else:
+        x, y = inputs(ref, N)
+    out = ref.forward(x, y)
+    gref = ref.backward()
+    xd, yd = cuda(x), cuda(y)
+    net.net_forward(xd, yd)
+    net.net_backward()
+    torch.cuda.synchronize()
+    rtol = RTOL[True]
+    fwd, bwd = net.stages(0), net.stages(1)
+    convs = [L for L in ref.layers if L["type"] == "Convolution"]
+    assert convs
+    for L in convs:
+        name = L["name"]
+        assert f"{name}.fwd[tc]" in fwd, fwd
+        for st in fwd:
+            if st.startswith(name + ".wpack"):
+                run_stage(net, 0, st)
+        # forward from the oracle's bottom
+        if L["bottom"] != ref.input_name:
+            net.net_put_blob(L["bottom"], out["blobs"][bottom_layer(ref, L)].astype(np.float32))
+        run_stage(net, 0, f"{name}.fwd[tc]", xd, yd)
+        S = out["scales"][name]
+        assert_close(f"{name} fwd", host(net.net_get_blob(L["top"])), out["blobs"][name], S, rtol)
+        # gradients from the oracle's top diff
+        G = top_diff(ref, gref, L)
+        net.net_put_blob(L["top"], G.astype(np.float32), PN_DIFF)
+        run_stage(net, 1, f"{name}.wgrad[tc]", xd, yd)
+        run_stage(net, 1, f"{name}.wgrad_reduce")
+        gs = gref["scales"]
+        assert_close(f"{name}.w grad", host(net.net_get_blob(name + ".w", PN_DIFF)), gref["grads"][name + ".w"],
+                     gs[name + ".w"], rtol)
+        assert_close(f"{name}.b grad", host(net.net_get_blob(name + ".b", PN_DIFF)).ravel(),
+                     gref["grads"][name + ".b"], gs[name + ".b"], rtol)
+        if L["bottom"] != ref.input_name:
+            assert f"{name}.dgrad[tc]" in bwd, bwd
+            run_stage(net, 1, f"{name}.dgrad[tc]")
+            assert_close(f"{name} dgrad", host(net.net_get_blob(L["bottom"], PN_DIFF)), gref["diffs"][name],
+                         gs[name + ".dx"], rtol)
+    net.close()
+
+
+def bottom_layer(ref, L):
+    """Name of the oracle layer whose output is L's bottom (last writer)."""
+    prev = [M for M in ref.layers[:ref.layers.index(L)] if M["top"] == L["bottom"]]
+    return prev[-1]["name"]
+
+
+def top_diff(ref, gref, L):
+    """Gradient w.r.t. L's output: the diff the next consumer of L's top received."""
+    nxt = [M for M in ref.layers[ref.layers.index(L) + 1:] if M["bottom"] == L["top"]]
+    return gref["diffs"][nxt[0]["name"]]
+
+
+@pytest.mark.parametrize("case,N", [("cifar10_quick", 16), ("cifar10_quick", 37), ("alexnet_small", 2)])
+def test_conv_tc_net_level(case, N):
+    """Whole layerwise TF32 step (forward, backward) vs the oracle: loss and
+    every parameter gradient (norm-wise)."""
+    spec = CASES[case][0]()
+    ref = OracleNet(spec, N)
+    params = synth.xavier_params(ref.learnable(), seed=2, bias="uniform")
+    ref.set_params(params)
+    net = Net(spec, N, tf32=True)
+    net.set_params(params)
+    if case == "cifar10_quick":
+        x, y = synth.cifar_like(N, seed=3)
+    else:
+        x, y = inputs(ref, N, seed=3)
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
+    net.net_forward(cuda(x), cuda(y), loss)
+    net.net_backward()
+    net.net_sync_errors()
+    out = ref.forward(x, y)
+    gref = ref.backward()
+    assert abs(loss.item() - out["loss"]) <= 2e-3 * (1 + abs(out["loss"])), (loss.item(), out["loss"])
+    # Every parameter gradient depends on the whole chain: the forward runs
+    # through the TF32 convolutions below the layer, the backward through those
+    # above it, and their rounding also flips discrete decisions (ReLU signs,
+    # max-pool near-ties routing a gradient to another pixel).  The norm-wise
+    # bound therefore scales with the number of TF32 conv layers in the chain;
+    # the element-wise kernel bound is asserted by the teacher-forced test.
+    nconv = sum(1 for L in ref.layers if L["type"] == "Convolution")
+    for k in params:
+        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
+        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * RTOL[True] * nconv)
+    net.close()

@@ -59,6 +59,8 @@ def run(net, phase, prefix, x=None, y=None):
     ("lenet", 37, False, False),          # ragged batch
     ("lenet", 1, False, False),           # degenerate batch
     ("cifar10_quick", 16, False, True),
+    ("cifar10_quick", 16, True, True),    # general tcgen05 conv (tc_conv.cu)
+    ("lenet", 64, True, True),            # LeNet through the general TF32 plan
     ("lenet", 64, True, False),
     ("lenet", 37, True, False),
 ])
