@@ -69,6 +69,8 @@ def stage_work(name, N):
         "loss_reduce": (0, N * 4 + 4),
         "ip2.bwd+relu1.bwd": (4 * 500 * 10 * N, N * (10 * 4 + 500 * 4 * 2) + WI2 + 32 * 5010 * 4),
         "ip1.wgrad": (2 * 500 * 800 * N, N * (500 * 4 + 800 * 4) + WI1),
+        # + the ip bucket's split partials (ip2 w/b: 32 x 5010, ip1 b: 32 x 500) read once, grads written
+        "ip1.wgrad+ip.bucket_reduce": (2 * 500 * 800 * N, N * (500 * 4 + 800 * 4) + WI1 + 33 * 5510 * 4),
         "ip1.bgrad": (0, N * 500 * 4 + 2000),
         "ip1.dgrad": (2 * 500 * 800 * N, N * (500 * 4 + 800 * 4) + WI1),
         "ip1.dgrad+unpool2": (2 * 500 * 800 * N, N * (500 * 4 + 800 + 3200 * 4) + WI1),
@@ -128,6 +130,7 @@ def layer_stage_work(layers, name, N):
     compulsory fp32 reads + writes of the stage (weights once, masks int32)."""
     base = name.split("[")[0]
     lname, _, op = base.rpartition(".")
+    op = op.split("+")[0]  # "fwd+relu": the fused ReLU adds no algorithmic traffic
     by = {L["name"]: L for L in layers}
     if base == "loss_reduce":
         return (0, N * 4 + 4)

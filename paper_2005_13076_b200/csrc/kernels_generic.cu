@@ -183,75 +183,90 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
 // ------------------------------------------------------------------ pooling
 // P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
 // a row-major scan (strict >) and stores its plane-local index h*W+w.
+// exact a / d for 0 <= a < 2^24, d >= 1 (float estimate + one-step correction)
+__device__ __forceinline__ int qdiv(int a, int d) {
+  int q = __float2int_rz(__fmul_rn((float)a + 0.5f, __frcp_rn((float)d)));
+  q -= (q * d > a);
+  q += ((q + 1) * d <= a);
+  return q;
+}
+
+// grid (positions of a plane / 256, planes): one output per thread, no
+// 64-bit or long integer division on the per-element path
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
   pdl_enter();
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)p.N * p.C * p.Hp * p.Wp;
-  if (idx >= total) return;
-  int b = idx % p.Wp;
-  int a = (idx / p.Wp) % p.Hp;
-  long long nc = idx / ((long long)p.Wp * p.Hp);
-  const float* xp = p.x + nc * p.H * p.W;
+  const int HWp = p.Hp * p.Wp, planes = p.N * p.C;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= HWp) return;
+  const int a = qdiv(r, p.Wp), b = r - a * p.Wp;
   int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
   int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
-  int size = (he - hs) * (we - ws);
+  const int size = (he - hs) * (we - ws);
   hs = max(hs, 0);
   ws = max(ws, 0);
   he = min(he, p.H);
   we = min(we, p.W);
-  if (p.method == 0) {
-    float best = xp[hs * p.W + ws];
-    int arg = hs * p.W + ws;
-    for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) {
-        float v = xp[h * p.W + w];
-        if (v > best) {
-          best = v;
-          arg = h * p.W + w;
+  for (int nc = blockIdx.y; nc < planes; nc += gridDim.y) {
+    const float* xp = p.x + (size_t)nc * p.H * p.W;
+    const size_t idx = (size_t)nc * HWp + r;
+    if (p.method == 0) {
+      float best = __ldg(xp + hs * p.W + ws);
+      int arg = hs * p.W + ws;
+      for (int h = hs; h < he; ++h)
+        for (int w = ws; w < we; ++w) {
+          float v = __ldg(xp + h * p.W + w);
+          if (v > best) {
+            best = v;
+            arg = h * p.W + w;
+          }
         }
-      }
-    p.y[idx] = best;
-    p.mask[idx] = arg;
-  } else {
-    float acc = 0.f;
-    for (int h = hs; h < he; ++h)
-      for (int w = ws; w < we; ++w) acc += xp[h * p.W + w];
-    p.y[idx] = __fdiv_rn(acc, (float)size);
+      p.y[idx] = best;
+      p.mask[idx] = arg;
+    } else {
+      float acc = 0.f;
+      for (int h = hs; h < he; ++h)
+        for (int w = ws; w < we; ++w) acc += __ldg(xp + h * p.W + w);
+      p.y[idx] = __fdiv_rn(acc, (float)size);
+    }
   }
 }
 
 // each input sums the output gradients routed to it, in ascending
-// output order (the oracle's scatter order) -- no atomics.
+// output order (the oracle's scatter order) -- no atomics.  With relu_y the
+// in-place ReLU below the pool is back-propagated here too: its
+// backward stage disappears.
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
   pdl_enter();
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)p.N * p.C * p.H * p.W;
-  if (idx >= total) return;
-  int w = idx % p.W;
-  int h = (idx / p.W) % p.H;
-  long long nc = idx / ((long long)p.W * p.H);
-  int a0 = (h + p.ph < p.kh) ? 0 : (h + p.ph - p.kh) / p.sh + 1;
-  int a1 = min((h + p.ph) / p.sh, p.Hp - 1);
-  int b0 = (w + p.pw < p.kw) ? 0 : (w + p.pw - p.kw) / p.sw + 1;
-  int b1 = min((w + p.pw) / p.sw, p.Wp - 1);
-  const float* dyp = p.dy + nc * p.Hp * p.Wp;
-  float acc = 0.f;
-  if (p.method == 0) {
-    const int32_t* mp = p.mask + nc * p.Hp * p.Wp;
-    int me = h * p.W + w;
-    for (int a = a0; a <= a1; ++a)
-      for (int b = b0; b <= b1; ++b)
-        if (mp[a * p.Wp + b] == me) acc += dyp[a * p.Wp + b];
-  } else {
-    for (int a = a0; a <= a1; ++a)
-      for (int b = b0; b <= b1; ++b) {
-        int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
-        int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
-        int size = (he - hs) * (we - ws);
-        acc += __fdiv_rn(dyp[a * p.Wp + b], (float)size);
-      }
+  const int HW = p.H * p.W, planes = p.N * p.C;
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= HW) return;
+  const int h = qdiv(r, p.W), w = r - h * p.W;
+  const int a0 = (h + p.ph < p.kh) ? 0 : qdiv(h + p.ph - p.kh, p.sh) + 1;
+  const int a1 = min(qdiv(h + p.ph, p.sh), p.Hp - 1);
+  const int b0 = (w + p.pw < p.kw) ? 0 : qdiv(w + p.pw - p.kw, p.sw) + 1;
+  const int b1 = min(qdiv(w + p.pw, p.sw), p.Wp - 1);
+  for (int nc = blockIdx.y; nc < planes; nc += gridDim.y) {
+    const float* dyp = p.dy + (size_t)nc * p.Hp * p.Wp;
+    const size_t idx = (size_t)nc * HW + r;
+    float acc = 0.f;
+    if (p.method == 0) {
+      const int32_t* mp = p.mask + (size_t)nc * p.Hp * p.Wp;
+      const int me = h * p.W + w;
+      for (int a = a0; a <= a1; ++a)
+        for (int b = b0; b <= b1; ++b)
+          if (__ldg(mp + a * p.Wp + b) == me) acc += __ldg(dyp + a * p.Wp + b);
+    } else {
+      for (int a = a0; a <= a1; ++a)
+        for (int b = b0; b <= b1; ++b) {
+          int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
+          int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+          int size = (he - hs) * (we - ws);
+          acc += __fdiv_rn(__ldg(dyp + a * p.Wp + b), (float)size);
+        }
+    }
+    if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) acc = 0.f;
+    p.dx[idx] = acc;
   }
-  p.dx[idx] = acc;
 }
 
 // -------------------------------------------------------------------- GEMM
@@ -310,6 +325,75 @@ __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ Gemm
   }
 }
 
+// Inner-product forward for few outputs and long K (cifar10_quick ip1/ip2,
+// the AlexNet trunk's classifier): block = 4 rows x 8 outputs, its
+// 8 warps split K (float4 lanes), warp-shuffle then fixed-order cross-warp
+// sums (deterministic), bias + optional ReLU in the epilogue.
+__global__ void __launch_bounds__(256) ip_fwd_rows(const __grid_constant__ IpRowsP p) {
+  pdl_enter();
+  __shared__ float red[8][4][8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 4, o0 = blockIdx.y * 8;
+  const int k0 = (int)((long long)p.K * warp / 8), k1 = (int)((long long)p.K * (warp + 1) / 8);
+  float acc[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int o = 0; o < 8; ++o) acc[r][o] = 0.f;
+  const bool vec = (p.K & 3) == 0 && (k0 & 3) == 0 && (k1 & 3) == 0;
+  if (vec) {
+    for (int k = k0 + 4 * lane; k < k1; k += 128) {
+      float4 xv[4], wv[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        xv[r] = m0 + r < p.M ? __ldg(reinterpret_cast<const float4*>(p.x + (long long)(m0 + r) * p.K + k))
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int o = 0; o < 8; ++o)
+        wv[o] = o0 + o < p.Nout ? __ldg(reinterpret_cast<const float4*>(p.w + (long long)(o0 + o) * p.K + k))
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int o = 0; o < 8; ++o)
+          acc[r][o] = fmaf(xv[r].w, wv[o].w, fmaf(xv[r].z, wv[o].z, fmaf(xv[r].y, wv[o].y, fmaf(xv[r].x, wv[o].x, acc[r][o]))));
+    }
+  } else {
+    for (int k = k0 + lane; k < k1; k += 32) {
+      float xv[4], wv[8];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) xv[r] = m0 + r < p.M ? __ldg(p.x + (long long)(m0 + r) * p.K + k) : 0.f;
+#pragma unroll
+      for (int o = 0; o < 8; ++o) wv[o] = o0 + o < p.Nout ? __ldg(p.w + (long long)(o0 + o) * p.K + k) : 0.f;
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int o = 0; o < 8; ++o) acc[r][o] = fmaf(xv[r], wv[o], acc[r][o]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int o = 0; o < 8; ++o) {
+      float v = acc[r][o];
+#pragma unroll
+      for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+      if (lane == 0) red[warp][r][o] = v;
+    }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int r = threadIdx.x >> 3, o = threadIdx.x & 7, m = m0 + r, oo = o0 + o;
+    if (m < p.M && oo < p.Nout) {
+      float v = red[0][r][o];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) v += red[w][r][o];
+      if (p.b) v += __ldg(p.b + oo);
+      if (p.relu) v = v > 0.f ? v : 0.f;
+      p.y[(long long)m * p.Nout + oo] = v;
+    }
+  }
+}
+
 // db[n] = sum_m dy[m, n] (InnerProduct bias gradient)
 __global__ void __launch_bounds__(256) colsum_generic(const __grid_constant__ ColSumP p) {
   pdl_enter();
@@ -322,21 +406,41 @@ __global__ void __launch_bounds__(256) colsum_generic(const __grid_constant__ Co
 }
 
 // --------------------------------------------------------------------- ReLU
+// float4 lanes (blob pointers are 256-B aligned; the tail is scalar)
 __global__ void relu_fwd_generic(const __grid_constant__ ReluP p) {
   pdl_enter();
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  float v = p.x[i];
-  p.out[i] = v > 0.f ? v : __fmul_rn(p.slope, v);
+  const long long n4 = p.n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 v = reinterpret_cast<const float4*>(p.x)[i];  // may alias out (in place)
+    v.x = v.x > 0.f ? v.x : __fmul_rn(p.slope, v.x);
+    v.y = v.y > 0.f ? v.y : __fmul_rn(p.slope, v.y);
+    v.z = v.z > 0.f ? v.z : __fmul_rn(p.slope, v.z);
+    v.w = v.w > 0.f ? v.w : __fmul_rn(p.slope, v.w);
+    reinterpret_cast<float4*>(p.out)[i] = v;
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    float v = p.x[i];
+    p.out[i] = v > 0.f ? v : __fmul_rn(p.slope, v);
+  }
 }
-
-// dX = dY * (y > 0 ? 1 : slope), y = in-place forward output (R8)
 __global__ void relu_bwd_generic(const __grid_constant__ ReluP p) {
   pdl_enter();
-  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= p.n) return;
-  float g = p.x[i];
-  p.out[i] = p.y[i] > 0.f ? g : __fmul_rn(g, p.slope);
+  const long long n4 = p.n >> 2;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    float4 g = reinterpret_cast<const float4*>(p.x)[i];  // may alias out (in place)
+    const float4 y = reinterpret_cast<const float4*>(p.y)[i];
+    g.x = y.x > 0.f ? g.x : __fmul_rn(g.x, p.slope);
+    g.y = y.y > 0.f ? g.y : __fmul_rn(g.y, p.slope);
+    g.z = y.z > 0.f ? g.z : __fmul_rn(g.z, p.slope);
+    g.w = y.w > 0.f ? g.w : __fmul_rn(g.w, p.slope);
+    reinterpret_cast<float4*>(p.out)[i] = g;
+  }
+  for (long long i = 4 * n4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    float g = p.x[i];
+    p.out[i] = p.y[i] > 0.f ? g : __fmul_rn(g, p.slope);
+  }
 }
 
 // ----------------------------------------------------------- softmax + loss

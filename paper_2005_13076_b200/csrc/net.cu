@@ -74,6 +74,7 @@ struct Layer {
   float* bdg = nullptr;
   int fwd_rows = 0, fwd_nk = 0, dg_rows = 0, dg_nk = 0;
   bool tc_conv = false, tc_dgrad = false;
+  tcc::WgTmaPlan wg{};  // weight gradient over materialised operands (tc_conv.cu)
 };
 
 struct Blob {
@@ -194,6 +195,10 @@ struct pn_net {
   cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
   int64_t bucket_split = 0;  // params [0, split) = ip bucket, [split, n) = conv bucket
   int tc_sms = 148;
+  bool tmap_failed = false;
+  // layerwise TF32 plan: shared workspaces of the weight-gradient operands
+  float* col_ws = nullptr;  // colT [kpad][pitch]
+  float* gm_ws = nullptr;   // Gm   [fpad][pitch]
 
   int blob(const std::string& n) const {
     for (size_t i = 0; i < blobs.size(); ++i)
@@ -419,9 +424,11 @@ static pn_status allocate(pn_net* net) {
     L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 1) / 2 : kWgradSplits;
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
-    if (L.tc_conv)
-      L.splits = tcc::wgrad_splits(net->batch, L.out[2], L.out[3], L.F, (int)(L.wcount / L.F), L.bias ? 1 : 0,
-                                   net->tc_sms);
+    if (L.tc_conv) {
+      L.wg = tcc::wgrad_tma_plan(net->batch, L.out[2], L.out[3], L.F, (int)(L.wcount / L.F), L.bias ? 1 : 0,
+                                 net->tc_sms);
+      L.splits = L.wg.splits;
+    }
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
   }
@@ -441,9 +448,18 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
     TRY(net->alloc(&net->part_db2, (size_t)tc::db2_partials(net->batch) * 50));
   }
-  for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images
+  size_t col_n = 0, gm_n = 0;
+  for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images, wgrad workspaces
     if (L.tc_conv) TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
     if (L.tc_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
+    if (L.tc_conv) {
+      col_n = std::max(col_n, (size_t)L.wg.kpad * L.wg.pitch);
+      gm_n = std::max(gm_n, (size_t)L.wg.fpad * L.wg.pitch);
+    }
+  }
+  if (col_n) {
+    TRY(net->alloc(&net->col_ws, col_n));
+    TRY(net->alloc(&net->gm_ws, gm_n));
   }
   TRY(net->alloc(&net->err, 1));
   // activation blobs (the fused plan never stores conv1's output or its
@@ -539,12 +555,22 @@ static void build_layerwise(pn_net* net) {
   auto& fwd = net->phase[0];
   auto& bwd = net->phase[1];
   const int N = net->batch;
+  // TF32 plan: an in-place ReLU (slope 0) right after a convolution runs in
+  // the convolution's epilogue (its forward stage disappears; its backward,
+  // which reads the output sign, stays)
+  std::vector<bool> relu_in_conv(net->layers.size(), false);
+  for (size_t li = 0; li + 1 < net->layers.size(); ++li) {
+    const Layer &L = net->layers[li], &R = net->layers[li + 1];
+    if (L.type == L_CONV && L.tc_conv && R.type == L_RELU && R.bottom == L.top && R.top == L.top && R.slope == 0.f)
+      relu_in_conv[li + 1] = true;
+  }
   for (size_t li = 0; li < net->layers.size(); ++li) {
     Layer& L = net->layers[li];
     bool isx = false;
     const float* x = in_data(net, L, &isx);
     Blob* top = L.type == L_LOSS ? nullptr : &net->blobs[net->blob(L.top)];
     Launch l;
+    if (relu_in_conv[li]) continue;
     if (L.type == L_CONV && L.tc_conv) {
       // TF32 images of W for this step's forward and data-gradient contractions
       ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
@@ -555,8 +581,8 @@ static void build_layerwise(pn_net* net) {
       }
       ConvTcP p{x, L.bfwd, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
                 N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
-                L.in[1] * L.kh * L.kw, L.fwd_nk, L.fwd_rows, 0};
-      add(fwd, L.name + ".fwd[tc]", tcc::conv_fwd_launch(p),
+                L.in[1] * L.kh * L.kw, L.fwd_nk, L.fwd_rows, li + 1 < net->layers.size() && relu_in_conv[li + 1]};
+      add(fwd, L.name + (p.relu ? ".fwd+relu[tc]" : ".fwd[tc]"), tcc::conv_fwd_launch(p),
           isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcP>().x = a.x; }
               : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_CONV) {
@@ -568,8 +594,16 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_POOL) {
       PoolFwdP p{x, top->data, top->m32, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
                  L.out[2], L.out[3], L.method};
-      l.set((const void*)pool_fwd_generic, dim3(cdiv(top->count(), 256)), dim3(256), 0, p);
+      l.set((const void*)pool_fwd_generic, dim3(cdiv(L.out[2] * L.out[3], 256), std::min(N * L.in[1], 65535)),
+            dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l);
+    } else if (L.type == L_IP && (long long)cdiv(L.Nout, 64) * cdiv(N, 64) < net->tc_sms) {
+      // few output tiles: split-K rows kernel instead of the 64x64-tile GEMM
+      IpRowsP p{x, net->params + L.off, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
+                N, L.K, L.Nout, 0};
+      l.set((const void*)ip_fwd_rows, dim3(cdiv(N, 4), cdiv(L.Nout, 8)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<IpRowsP>().x = a.x; }
+                                       : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_IP) {
       GemmP p{x, net->params + L.off, top->data, L.bias ? net->params + L.off + L.wcount : nullptr,
               N, L.Nout, L.K, L.K, 1, 1, L.K, 0};
@@ -578,7 +612,8 @@ static void build_layerwise(pn_net* net) {
                                        : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_RELU) {
       ReluP p{x, nullptr, top->data, top->count(), L.slope};
-      l.set((const void*)relu_fwd_generic, dim3(cdiv(top->count(), 256)), dim3(256), 0, p);
+      l.set((const void*)relu_fwd_generic, dim3(std::max(1u, std::min(cdiv(top->count() / 4, 256), 8u * net->tc_sms))),
+            dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l);
     } else {
       Blob& bb = net->blobs[net->blob(L.bottom)];
@@ -590,28 +625,49 @@ static void build_layerwise(pn_net* net) {
       add_loss(net, fwd);
     }
   }
+  // An in-place ReLU (slope 0) whose output feeds a pooling layer or a TF32
+  // convolution's data gradient is back-propagated inside that consumer's
+  // backward kernel (dx *= (y > 0)): its backward stage disappears.
+  std::vector<bool> relu_bwd_fused(net->layers.size(), false);
+  for (size_t li = 0; li + 1 < net->layers.size(); ++li) {
+    const Layer &R = net->layers[li], &C = net->layers[li + 1];
+    if (R.type == L_RELU && R.top == R.bottom && R.slope == 0.f && R.bottom != net->input_name &&
+        C.bottom == R.top && (C.type == L_POOL || (C.type == L_CONV && C.tc_dgrad)))
+      relu_bwd_fused[li] = true;
+  }
   // backward, reverse order
   for (int li = (int)net->layers.size() - 1; li >= 0; --li) {
     Layer& L = net->layers[li];
     bool isx = false;
     const float* x = in_data(net, L, &isx);
     if (L.type == L_LOSS) continue;  // gradient produced with the forward
+    if (relu_bwd_fused[li]) continue;
+    const float* relu_y = (li > 0 && relu_bwd_fused[li - 1]) ? net->blobs[net->blob(L.bottom)].data : nullptr;
     Blob& top = net->blobs[net->blob(L.top)];
     Blob* bot = isx ? nullptr : &net->blobs[net->blob(L.bottom)];
     Launch l;
     if (L.type == L_CONV && L.tc_conv) {
-      const int K = L.in[1] * L.kh * L.kw;
-      ConvTcWgradP w{top.diff, x, net->partials + L.part_off, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
-                     L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3], K, L.bias ? 1 : 0, L.splits,
-                     (int)(L.wcount + L.bcount)};
-      add(bwd, L.name + ".wgrad[tc]", tcc::conv_wgrad_launch(w),
-          isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcWgradP>().x = a.x; }
+      // weight gradient: colT = im2col(x)^T and Gm = G as [F][m] (TF32), then the
+      // TMA-fed GEMM into split partials, then their fixed-order sum
+      const int K = L.in[1] * L.kh * L.kw, M = N * L.out[2] * L.out[3];
+      Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
+                  L.out[3], K, K + (L.bias ? 1 : 0), L.wg.pitch};
+      add(bwd, L.name + ".wgrad.im2col[tc]", tcc::im2col_t_launch(ic),
+          isx ? [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; }
               : std::function<void(Launch&, const StepArgs&)>());
+      GmP gp{top.diff, net->gm_ws, N, L.F, L.out[2] * L.out[3], L.wg.pitch};
+      add(bwd, L.name + ".wgrad.gm[tc]", tcc::gm_launch(gp));
+      Launch lw;
+      if (!tcc::wgrad_tma_launch(L.wg, net->col_ws, net->gm_ws, net->partials + L.part_off, M, K, L.F,
+                                 L.bias ? 1 : 0, (int)(L.wcount + L.bcount), &lw))
+        net->tmap_failed = true;
+      add(bwd, L.name + ".wgrad[tc]", lw);
       add_reduce(net, bwd, L);
       if (bot && L.tc_dgrad) {  // dx = W'(*)G: stride 1, pad kh-1-p, output H x W
         ConvTcP q{top.diff, L.bdg, nullptr, bot->diff, N, L.F, L.out[2], L.out[3], L.in[1], L.kh, L.kw, 1, 1,
-                  L.kh - 1 - L.ph, L.kw - 1 - L.pw, L.in[2], L.in[3], L.F * L.kh * L.kw, L.dg_nk, L.dg_rows, 0};
-        add(bwd, L.name + ".dgrad[tc]", tcc::conv_fwd_launch(q));
+                  L.kh - 1 - L.ph, L.kw - 1 - L.pw, L.in[2], L.in[3], L.F * L.kh * L.kw, L.dg_nk, L.dg_rows, 0,
+                  relu_y};
+        add(bwd, L.name + (relu_y ? ".dgrad+relu_bwd[tc]" : ".dgrad[tc]"), tcc::conv_fwd_launch(q));
       } else if (bot) {
         ConvBwdDataP q{top.diff, net->params + L.off, bot->diff, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
                        L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
@@ -636,9 +692,10 @@ static void build_layerwise(pn_net* net) {
       }
     } else if (L.type == L_POOL) {
       PoolBwdP p{top.diff, top.m32, bot->diff, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
-                 L.out[2], L.out[3], L.method};
-      l.set((const void*)pool_bwd_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, p);
-      add(bwd, L.name + ".bwd", l);
+                 L.out[2], L.out[3], L.method, relu_y};
+      l.set((const void*)pool_bwd_generic, dim3(cdiv(L.in[2] * L.in[3], 256), std::min(N * L.in[1], 65535)),
+            dim3(256), 0, p);
+      add(bwd, L.name + (relu_y ? ".bwd+relu_bwd" : ".bwd"), l);
     } else if (L.type == L_IP) {
       // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
       GemmP w{top.diff, x, net->grads + L.off, nullptr, L.Nout, L.K, N, 1, L.Nout, L.K, 1, 0};
@@ -659,7 +716,8 @@ static void build_layerwise(pn_net* net) {
       }
     } else if (L.type == L_RELU) {
       ReluP p{top.diff, top.data, bot->diff, top.count(), L.slope};
-      l.set((const void*)relu_bwd_generic, dim3(cdiv(top.count(), 256)), dim3(256), 0, p);
+      l.set((const void*)relu_bwd_generic, dim3(std::max(1u, std::min(cdiv(top.count() / 4, 256), 8u * net->tc_sms))),
+            dim3(256), 0, p);
       add(bwd, L.name + ".bwd", l);
     }
   }
@@ -813,7 +871,7 @@ static void add_dp_stages(pn_net* net) {
   for (size_t i = 0; i < bwd.size(); ++i)
     if (bwd[i].name.rfind("ip", 0) == 0) pos = i + 1;
   for (size_t i = 0; i < bwd.size(); ++i)  // fused plans: right after the ip bucket is final
-    if (bwd[i].name == "ip.bucket_reduce") pos = i + 1;
+    if (bwd[i].name.find("ip.bucket_reduce") != std::string::npos) pos = i + 1;
   auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) {
     return [net, off, cnt, ready](cudaStream_t st) -> cudaError_t {
       cudaError_t e = cudaEventRecord(ready, st);
@@ -998,7 +1056,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }
   TRY(build_plan(net.get()));
-  if (net->tf32 && !tc::tensor_maps_ok()) return fail(PN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  if (net->tf32 && (!tc::tensor_maps_ok() || net->tmap_failed)) return fail(PN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   CU(cudaDeviceSynchronize());
   *out = net.release();
   return PN_OK;

@@ -49,6 +49,7 @@ struct PoolBwdP {  // P:220-222; gather form, ascending output order
   const int32_t* mask;
   float* dx;
   int N, C, H, W, kh, kw, sh, sw, ph, pw, Hp, Wp, method;
+  const float* relu_y;  // non-null: the bottom is an in-place ReLU (slope 0) output -> dx *= (relu_y > 0)
 };
 struct GemmP {  // C[m,n] = sum_k A(m,k) B(k,n) (+ bias[n]) (relu)
   const float* A;
@@ -184,6 +185,7 @@ struct ConvTcP {  // y = W (*) x (+ b) (relu), implicit GEMM on tcgen05 (P:118-1
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
   int K, nk, Fpad;   // K = C*kh*kw, nk = ceil(K/32), Fpad = rows of the B image
   int relu;
+  const float* relu_y;  // data gradient: y of the in-place ReLU (slope 0) below -> out *= (relu_y > 0)
 };
 struct ConvTcWgradP {  // split-m partials of dW = G^T col (+ db as the ones column)
   const float* g;  // top diff [N][F][Ho][Wo]
@@ -192,10 +194,28 @@ struct ConvTcWgradP {  // split-m partials of dW = G^T col (+ db as the ones col
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
   int K, bias_col, splits, pstride;
 };
+struct Im2colTP {  // colT[k][m] = tf32(col[m][k]) (k < K), 1 (k == K: bias row)
+  const float* x;
+  float* col;  // [rows][pitch]
+  int N, C, H, W, kh, kw, sh, sw, ph, pw, Ho, Wo, K, Kb, pitch;
+};
+struct GmP {  // gm[f][n*HoWo + pos] = tf32(g[n][f][pos])
+  const float* g;
+  float* gm;  // [rows][pitch]
+  int N, F, HoWo, pitch;
+};
 struct ConvPackP {  // TF32 B image of the forward (mode 0) / data-gradient (mode 1) contraction
   const float* w;   // [F][C][kh][kw]
   float* out;       // [nk][rows][32] SW128
   int F, C, kh, kw, rows, nk, mode;
+};
+
+struct IpRowsP {  // y[m,o] = sum_k x[m,k] W[o,k] + b[o] (relu): split-K rows kernel for skinny outputs
+  const float* x;   // [M][K]
+  const float* w;   // [Nout][K]
+  const float* b;   // [Nout] or nullptr
+  float* y;         // [M][Nout]
+  int M, K, Nout, relu;
 };
 
 }  // namespace pn

@@ -2,6 +2,7 @@
 // (tc_conv.cu): forward, data gradient (as a flipped-filter stride-1
 // convolution), split-m weight gradient, and the per-step TF32 weight packing.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "params.h"
@@ -16,5 +17,22 @@ Launch conv_fwd_launch(const ConvTcP& p);
 int wgrad_splits(int N, int Ho, int Wo, int F, int K, int bias, int sms);
 Launch conv_wgrad_launch(const ConvTcWgradP& p);
 Launch pack_launch(const ConvPackP& p);
+
+// weight gradient over materialised TF32 operands (colT, Gm), TMA-fed
+struct ConvWgTmaP {
+  CUtensorMap ta;  // colT [Kpad][pitch]: box {32 m, 128 k}
+  CUtensorMap tb;  // Gm   [Fpad][pitch]: box {32 m, BN f}
+  float* part;     // [splits][pstride]: w at f*K + k, b at F*K + f
+  int M, K, F, bias, splits, pstride;
+};
+struct WgTmaPlan {
+  int bn, kpad, fpad, pitch, splits;
+};
+WgTmaPlan wgrad_tma_plan(int N, int Ho, int Wo, int F, int K, int bias, int sms);
+Launch im2col_t_launch(const Im2colTP& p);
+Launch gm_launch(const GmP& p);
+// false if the tensor-map encoding failed
+bool wgrad_tma_launch(const WgTmaPlan& w, const float* col, const float* gm, float* part, int M, int K, int F,
+                      int bias, int pstride, Launch* out);
 }  // namespace tcc
 }  // namespace pn

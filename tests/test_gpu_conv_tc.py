@@ -100,30 +100,43 @@ def test_conv_tc_teacher_forced(case):
     assert convs
     for L in convs:
         name = L["name"]
-        assert f"{name}.fwd[tc]" in fwd, fwd
+        fst = [st for st in fwd if st.startswith(name + ".fwd")]
+        assert fst and fst[0].endswith("[tc]"), fwd
+        fused_relu = "+relu" in fst[0]   # in-place ReLU (slope 0) applied in the conv epilogue
         for st in fwd:
             if st.startswith(name + ".wpack"):
                 run_stage(net, 0, st)
         # forward from the oracle's bottom
         if L["bottom"] != ref.input_name:
             net.net_put_blob(L["bottom"], out["blobs"][bottom_layer(ref, L)].astype(np.float32))
-        run_stage(net, 0, f"{name}.fwd[tc]", xd, yd)
+        run_stage(net, 0, fst[0], xd, yd)
         S = out["scales"][name]
-        assert_close(f"{name} fwd", host(net.net_get_blob(L["top"])), out["blobs"][name], S, rtol)
+        want = out["blobs"][name]
+        if fused_relu:
+            want = out["blobs"][[M for M in ref.layers if M["type"] == "ReLU" and M["bottom"] == L["top"]][0]["name"]]
+        assert_close(f"{name} fwd", host(net.net_get_blob(L["top"])), want, S, rtol)
         # gradients from the oracle's top diff
         G = top_diff(ref, gref, L)
         net.net_put_blob(L["top"], G.astype(np.float32), PN_DIFF)
-        run_stage(net, 1, f"{name}.wgrad[tc]", xd, yd)
-        run_stage(net, 1, f"{name}.wgrad_reduce")
+        wst = [st for st in bwd if st.startswith(name + ".wgrad")]  # operand staging, GEMM, partial sum
+        assert f"{name}.wgrad[tc]" in wst and wst[-1] == f"{name}.wgrad_reduce", wst
+        for st in wst:
+            run_stage(net, 1, st, xd, yd)
         gs = gref["scales"]
         assert_close(f"{name}.w grad", host(net.net_get_blob(name + ".w", PN_DIFF)), gref["grads"][name + ".w"],
                      gs[name + ".w"], rtol)
         assert_close(f"{name}.b grad", host(net.net_get_blob(name + ".b", PN_DIFF)).ravel(),
                      gref["grads"][name + ".b"], gs[name + ".b"], rtol)
         if L["bottom"] != ref.input_name:
-            assert f"{name}.dgrad[tc]" in bwd, bwd
-            run_stage(net, 1, f"{name}.dgrad[tc]")
-            assert_close(f"{name} dgrad", host(net.net_get_blob(L["bottom"], PN_DIFF)), gref["diffs"][name],
+            dst = [st for st in bwd if st.startswith(name + ".dgrad")]
+            assert dst and dst[0].endswith("[tc]"), bwd
+            run_stage(net, 1, dst[0])
+            want = gref["diffs"][name]
+            if "+relu_bwd" in dst[0]:
+                # the in-place ReLU below is back-propagated in the dgrad epilogue
+                relu = [M for M in ref.layers if M["type"] == "ReLU" and M["top"] == L["bottom"]][-1]
+                want = gref["diffs"][relu["name"]]
+            assert_close(f"{name} dgrad", host(net.net_get_blob(L["bottom"], PN_DIFF)), want,
                          gs[name + ".dx"], rtol)
     net.close()
 
