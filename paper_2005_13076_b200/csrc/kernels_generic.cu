@@ -148,8 +148,17 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
   pdl_enter();
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= p.n) return;
+  // independent loads issued in batches of 8, summed in ascending split order
   float acc = 0.f;
-  for (int s = 0; s < p.splits; ++s) acc += p.part[(long long)s * p.stride + i];
+  int s = 0;
+  for (; s + 8 <= p.splits; s += 8) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldcg(p.part + (long long)(s + q) * p.stride + i);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += v[q];
+  }
+  for (; s < p.splits; ++s) acc += __ldcg(p.part + (long long)s * p.stride + i);
   p.out[i] = acc;
 }
 
@@ -167,8 +176,17 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = b * 32 + lane;
   float acc = 0.f;
-  if (i < s.n)
-    for (int j = w; j < s.splits; j += 8) acc += s.part[(long long)j * s.stride + i];
+  if (i < s.n) {  // splits w, w+8, ... in ascending order; loads issued 8 at a time
+    int j = w;
+    for (; j + 56 < s.splits; j += 64) {
+      float v[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __ldcg(s.part + (long long)(j + 8 * q) * s.stride + i);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += v[q];
+    }
+    for (; j < s.splits; j += 8) acc += __ldcg(s.part + (long long)j * s.stride + i);
+  }
   sm[w][lane] = acc;
   __syncthreads();
   if (w == 0 && i < s.n) {
@@ -183,9 +201,12 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
 // ------------------------------------------------------------------ pooling
 // P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
 // a row-major scan (strict >) and stores its plane-local index h*W+w.
-// exact a / d for 0 <= a < 2^24, d >= 1 (float estimate + one-step correction)
+// exact a / d for 0 <= a < 2^22, d >= 1: MUFU reciprocal estimate (relative
+// error ~2^-22, so the estimate is within one) + one-step correction
 __device__ __forceinline__ int qdiv(int a, int d) {
-  int q = __float2int_rz(__fmul_rn((float)a + 0.5f, __frcp_rn((float)d)));
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));
+  int q = __float2int_rz(((float)a + 0.5f) * r);
   q -= (q * d > a);
   q += ((q + 1) * d <= a);
   return q;
@@ -266,6 +287,60 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
     }
     if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) acc = 0.f;
     p.dx[idx] = acc;
+  }
+}
+
+// Pool backward, one block per (n, c) plane staged in shared memory: the
+// plane's output gradients (divided by the window size for AVE, the same
+// IEEE quotient the oracle adds) and max-pool origins are read once,
+// coalesced; each input then gathers its <= ceil(k/s)^2 windows from shared
+// memory in ascending output order (bit-exact with the scatter order).
+// Window ranges per input row / column come from two small tables.
+__global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ PoolBwdP p) {
+  extern __shared__ __align__(16) uint8_t psm[];
+  const int HWp = p.Hp * p.Wp, HW = p.H * p.W;
+  float* d = reinterpret_cast<float*>(psm);
+  int* m = reinterpret_cast<int*>(d + HWp);
+  short2* arow = reinterpret_cast<short2*>(m + HWp);
+  short2* bcol = arow + p.H;
+  for (int h = threadIdx.x; h < p.H; h += blockDim.x) {
+    const int a0 = (h + p.ph < p.kh) ? 0 : (h + p.ph - p.kh) / p.sh + 1;
+    arow[h] = make_short2((short)a0, (short)min((h + p.ph) / p.sh, p.Hp - 1));
+  }
+  for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
+    const int b0 = (w + p.pw < p.kw) ? 0 : (w + p.pw - p.kw) / p.sw + 1;
+    bcol[w] = make_short2((short)b0, (short)min((w + p.pw) / p.sw, p.Wp - 1));
+  }
+  pdl_enter();
+  for (int nc = blockIdx.x; nc < p.N * p.C; nc += gridDim.x) {
+    __syncthreads();
+    const float* dyp = p.dy + (size_t)nc * HWp;
+    for (int o = threadIdx.x; o < HWp; o += blockDim.x) {
+      float v = __ldg(dyp + o);
+      if (p.method == 0) {
+        m[o] = __ldg(p.mask + (size_t)nc * HWp + o);
+      } else {
+        const int a = o / p.Wp, b = o - a * p.Wp;
+        const int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
+        const int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+        v = __fdiv_rn(v, (float)((he - hs) * (we - ws)));
+      }
+      d[o] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < HW; r += blockDim.x) {
+      const int h = r / p.W, w = r - h * p.W;
+      const short2 ar = arow[h], bc = bcol[w];
+      float acc = 0.f;
+      for (int a = ar.x; a <= ar.y; ++a)
+        for (int b = bc.x; b <= bc.y; ++b) {
+          const int o = a * p.Wp + b;
+          if (p.method != 0 || m[o] == r) acc += d[o];
+        }
+      const size_t idx = (size_t)nc * HW + r;
+      if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) acc = 0.f;
+      p.dx[idx] = acc;
+    }
   }
 }
 

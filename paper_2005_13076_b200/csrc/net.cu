@@ -68,13 +68,15 @@ struct Layer {
   int64_t wcount = 0, bcount = 0, off = -1;  // offset of w in the flat buffers, b follows w
   int64_t part_off = -1;                     // partial-sum region (split wgrads)
   int splits = 0;
-  // layerwise TF32 plan (tc_conv.cu): packed B images of the forward and
-  // data-gradient contractions
-  float* bfwd = nullptr;
-  float* bdg = nullptr;
+  // layerwise TF32 plan (tc_conv.cu): forward and weight gradient over
+  // materialised TF32 operands (plan tp, weight copy Wf [F][kp]); data
+  // gradient as an implicit GEMM over gathered G (swizzled W' image bdg)
+  bool tc_conv = false, tc_dgrad = false, tma_fwd = false;
+  tcc::ConvTmaPlan tp{};
+  float* wf = nullptr;   // Wf [F][kp] (materialised forward)
+  float* bfwd = nullptr; // swizzled W image (gathered forward)
+  float* bdg = nullptr;  // swizzled W' image (gathered data gradient)
   int fwd_rows = 0, fwd_nk = 0, dg_rows = 0, dg_nk = 0;
-  bool tc_conv = false, tc_dgrad = false;
-  tcc::WgTmaPlan wg{};  // weight gradient over materialised operands (tc_conv.cu)
 };
 
 struct Blob {
@@ -425,9 +427,9 @@ static pn_status allocate(pn_net* net) {
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
     if (L.tc_conv) {
-      L.wg = tcc::wgrad_tma_plan(net->batch, L.out[2], L.out[3], L.F, (int)(L.wcount / L.F), L.bias ? 1 : 0,
-                                 net->tc_sms);
-      L.splits = L.wg.splits;
+      L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
+                                net->tc_sms);
+      L.splits = L.tp.wg_splits;
     }
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
@@ -450,11 +452,12 @@ static pn_status allocate(pn_net* net) {
   }
   size_t col_n = 0, gm_n = 0;
   for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images, wgrad workspaces
-    if (L.tc_conv) TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
-    if (L.tc_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
     if (L.tc_conv) {
-      col_n = std::max(col_n, (size_t)L.wg.kpad * L.wg.pitch);
-      gm_n = std::max(gm_n, (size_t)L.wg.fpad * L.wg.pitch);
+      if (L.tma_fwd) TRY(net->alloc(&L.wf, (size_t)L.F * L.tp.kp));
+      else TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
+      if (L.tc_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
+      col_n = std::max(col_n, L.tp.col_floats);
+      gm_n = std::max(gm_n, L.tp.g_floats);
     }
   }
   if (col_n) {
@@ -572,19 +575,39 @@ static void build_layerwise(pn_net* net) {
     Launch l;
     if (relu_in_conv[li]) continue;
     if (L.type == L_CONV && L.tc_conv) {
-      // TF32 images of W for this step's forward and data-gradient contractions
-      ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
-      add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
+      // im2col + GEMM.  Long contractions (K >= 1024): the TF32
+      // column matrix col [m][k] is materialised and streamed by TMA; short
+      // ones gather it straight into shared memory (the column matrix would
+      // cost more HBM traffic than the GEMM saves)
+      const bool relu = li + 1 < net->layers.size() && relu_in_conv[li + 1];
+      const float* bias = L.bias ? net->params + L.off + L.wcount : nullptr;
+      auto xpatch = [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; };
+      if (L.tma_fwd) {
+        PackPlainP pk{net->params + L.off, L.wf, L.F, L.tp.K, L.tp.kp};
+        add(fwd, L.name + ".wpack[tc]", tcc::pack_plain_launch(pk));
+      } else {
+        ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
+        add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
+      }
       if (L.tc_dgrad) {
         ConvPackP pd{net->params + L.off, L.bdg, L.F, L.in[1], L.kh, L.kw, L.dg_rows, L.dg_nk, 1};
         add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_launch(pd));
       }
-      ConvTcP p{x, L.bfwd, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
-                N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
-                L.in[1] * L.kh * L.kw, L.fwd_nk, L.fwd_rows, li + 1 < net->layers.size() && relu_in_conv[li + 1]};
-      add(fwd, L.name + (p.relu ? ".fwd+relu[tc]" : ".fwd[tc]"), tcc::conv_fwd_launch(p),
-          isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcP>().x = a.x; }
-              : std::function<void(Launch&, const StepArgs&)>());
+      if (L.tma_fwd) {
+        Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
+                    L.out[3], L.tp.K, L.tp.K, L.tp.kp};
+        add(fwd, L.name + ".im2col[tc]", tcc::im2col_rows_launch(ic),
+            isx ? xpatch : std::function<void(Launch&, const StepArgs&)>());
+        Launch lg;
+        if (!tcc::gemm_fwd_launch(L.tp, net->col_ws, L.wf, bias, top->data, relu ? 1 : 0, &lg)) net->tmap_failed = true;
+        add(fwd, L.name + (relu ? ".fwd+relu[tc]" : ".fwd[tc]"), lg);
+      } else {
+        ConvTcP p{x, L.bfwd, bias, top->data, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
+                  L.out[2], L.out[3], L.tp.K, L.fwd_nk, L.fwd_rows, relu ? 1 : 0, nullptr};
+        add(fwd, L.name + (relu ? ".fwd+relu[tc]" : ".fwd[tc]"), tcc::conv_fwd_launch(p),
+            isx ? [](Launch& l, const StepArgs& a) { l.params<ConvTcP>().x = a.x; }
+                : std::function<void(Launch&, const StepArgs&)>());
+      }
     } else if (L.type == L_CONV) {
       ConvFwdP p{x, net->params + L.off, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
                  N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
@@ -649,21 +672,23 @@ static void build_layerwise(pn_net* net) {
     if (L.type == L_CONV && L.tc_conv) {
       // weight gradient: colT = im2col(x)^T and Gm = G as [F][m] (TF32), then the
       // TMA-fed GEMM into split partials, then their fixed-order sum
-      const int K = L.in[1] * L.kh * L.kw, M = N * L.out[2] * L.out[3];
+      const int K = L.tp.K;
       Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
-                  L.out[3], K, K + (L.bias ? 1 : 0), L.wg.pitch};
+                  L.out[3], K, K + (L.bias ? 1 : 0), L.tp.pitch_m};
       add(bwd, L.name + ".wgrad.im2col[tc]", tcc::im2col_t_launch(ic),
           isx ? [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; }
               : std::function<void(Launch&, const StepArgs&)>());
-      GmP gp{top.diff, net->gm_ws, N, L.F, L.out[2] * L.out[3], L.wg.pitch};
+      GmP gp{top.diff, net->gm_ws, N, L.F, L.out[2] * L.out[3], L.tp.pitch_m};
       add(bwd, L.name + ".wgrad.gm[tc]", tcc::gm_launch(gp));
       Launch lw;
-      if (!tcc::wgrad_tma_launch(L.wg, net->col_ws, net->gm_ws, net->partials + L.part_off, M, K, L.F,
-                                 L.bias ? 1 : 0, (int)(L.wcount + L.bcount), &lw))
+      if (!tcc::gemm_wgrad_launch(L.tp, net->col_ws, net->gm_ws, net->partials + L.part_off,
+                                  (int)(L.wcount + L.bcount), &lw))
         net->tmap_failed = true;
       add(bwd, L.name + ".wgrad[tc]", lw);
       add_reduce(net, bwd, L);
-      if (bot && L.tc_dgrad) {  // dx = W'(*)G: stride 1, pad kh-1-p, output H x W
+      if (bot && L.tc_dgrad) {
+        // data gradient: col2im(W^T G) = W' (*) G, stride 1, pad
+        // kh-1-p, as an implicit GEMM gathering G (+ the in-place ReLU below)
         ConvTcP q{top.diff, L.bdg, nullptr, bot->diff, N, L.F, L.out[2], L.out[3], L.in[1], L.kh, L.kw, 1, 1,
                   L.kh - 1 - L.ph, L.kw - 1 - L.pw, L.in[2], L.in[3], L.F * L.kh * L.kw, L.dg_nk, L.dg_rows, 0,
                   relu_y};
@@ -693,8 +718,13 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_POOL) {
       PoolBwdP p{top.diff, top.m32, bot->diff, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
                  L.out[2], L.out[3], L.method, relu_y};
-      l.set((const void*)pool_bwd_generic, dim3(cdiv(L.in[2] * L.in[3], 256), std::min(N * L.in[1], 65535)),
-            dim3(256), 0, p);
+      // plane-staged kernel when a plane's gradients + origins fit shared memory
+      const size_t psmem = (size_t)L.out[2] * L.out[3] * 8 + (size_t)(L.in[2] + L.in[3]) * 4 + 16;
+      if (psmem <= 48 * 1024)
+        l.set((const void*)pool_bwd_plane, dim3(std::min(N * L.in[1], 16 * net->tc_sms)), dim3(256), psmem, p);
+      else
+        l.set((const void*)pool_bwd_generic, dim3(cdiv(L.in[2] * L.in[3], 256), std::min(N * L.in[1], 65535)),
+              dim3(256), 0, p);
       add(bwd, L.name + (relu_y ? ".bwd+relu_bwd" : ".bwd"), l);
     } else if (L.type == L_IP) {
       // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
@@ -1038,14 +1068,18 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     for (auto& L : net->layers) {
       if (L.type != L_CONV) continue;
       L.tc_conv = true;
-      L.fwd_rows = tcc::fwd_rows_pad(L.F);
-      L.fwd_nk = (L.in[1] * L.kh * L.kw + 31) / 32;
+      L.tma_fwd = L.in[1] * L.kh * L.kw >= 1024;
+      if (!L.tma_fwd) {
+        L.fwd_rows = tcc::fwd_rows_pad(L.F);
+        L.fwd_nk = (L.in[1] * L.kh * L.kw + 31) / 32;
+        max_nk = std::max(max_nk, L.fwd_nk);
+      }
       L.tc_dgrad = L.bottom != net->input_name && L.sh == 1 && L.sw == 1 && L.ph < L.kh && L.pw < L.kw;
       if (L.tc_dgrad) {
         L.dg_rows = tcc::fwd_rows_pad(L.in[1]);
         L.dg_nk = (L.F * L.kh * L.kw + 31) / 32;
+        max_nk = std::max(max_nk, L.dg_nk);
       }
-      max_nk = std::max(max_nk, std::max(L.fwd_nk, L.dg_nk));
     }
   }
   TRY(allocate(net.get()));

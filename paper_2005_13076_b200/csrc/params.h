@@ -187,12 +187,10 @@ struct ConvTcP {  // y = W (*) x (+ b) (relu), implicit GEMM on tcgen05 (P:118-1
   int relu;
   const float* relu_y;  // data gradient: y of the in-place ReLU (slope 0) below -> out *= (relu_y > 0)
 };
-struct ConvTcWgradP {  // split-m partials of dW = G^T col (+ db as the ones column)
-  const float* g;  // top diff [N][F][Ho][Wo]
-  const float* x;  // bottom data [N][C][H][W]
-  float* part;     // [splits][pstride]: w at f*K + k, b at F*K + f
-  int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
-  int K, bias_col, splits, pstride;
+struct ConvPackP {  // TF32 B image of the forward (mode 0) / data-gradient (mode 1) contraction
+  const float* w;   // [F][C][kh][kw]
+  float* out;       // [nk][rows][32] SW128
+  int F, C, kh, kw, rows, nk, mode;
 };
 struct Im2colTP {  // colT[k][m] = tf32(col[m][k]) (k < K), 1 (k == K: bias row)
   const float* x;
@@ -204,10 +202,10 @@ struct GmP {  // gm[f][n*HoWo + pos] = tf32(g[n][f][pos])
   float* gm;  // [rows][pitch]
   int N, F, HoWo, pitch;
 };
-struct ConvPackP {  // TF32 B image of the forward (mode 0) / data-gradient (mode 1) contraction
-  const float* w;   // [F][C][kh][kw]
-  float* out;       // [nk][rows][32] SW128
-  int F, C, kh, kw, rows, nk, mode;
+struct PackPlainP {  // TF32 copy of W [F][K] as [F][pitch]
+  const float* w;
+  float* out;
+  int F, K, pitch;
 };
 
 struct IpRowsP {  // y[m,o] = sum_k x[m,k] W[o,k] + b[o] (relu): split-K rows kernel for skinny outputs

@@ -1,37 +1,35 @@
-// tc_conv.cu -- general tcgen05 TF32 implicit-GEMM convolution for any
-// geometry (kernel, stride, padding, channel counts): the tensor-core plan of
-// nets other than the fused LeNet chain (cifar10_quick, SURVEY §8(a) row a19;
-// the AlexNet-shaped conv sweep, BASELINE config 5).
+// tc_conv.cu -- general tcgen05 TF32 convolution for any geometry (kernel,
+// stride, padding, channel counts): the tensor-core plan of nets other than
+// the fused LeNet chain -- cifar10_quick and the
+// AlexNet conv trunk (BASELINE config 5).
 //
-// The paper lowers a convolution to im2col + GEMM: a column
-// matrix of every (c,i,j) patch element per output position, multiplied by
-// the F x (C*kh*kw) weight matrix.  Here the column matrix is never
-// materialised: each 128-row tile of it is gathered from the NCHW
-// activation straight into the shared-memory operand layout of the tensor
-// core (K-major SWIZZLE_128B, 32 fp32 of K per 128-B row), rounded to TF32
-// (nearest, ties away) on the way.
+// It is the paper's own lowering: a convolution is im2col + GEMM,
+// its data gradient GEMM + col2im, its weight gradient a GEMM against the
+// column matrix.  Each column matrix is materialised once per use as a dense
+// TF32 operand (rounded to nearest, ties away, when written) in the layout
+// the tensor core reads K-major, and every contraction is one TMA-fed
+// tcgen05 kernel (conv_gemm_tma):
+//   forward      col[m][k] (im2col_rows)  x  Wf[f][k]          -> y (+b, ReLU)
+//   weight grad  colT[k][m] (im2col_t, + ones row for the bias) x Gm[f][m]
+//                (gather_gm)  -> split-m partials -> fixed-order sum
+//   data grad    col2im(W^T G) = W' (*) G (stride-1 layers, W' the flipped,
+//                channel-transposed filter, pad kh-1-p) as an implicit GEMM
+//                that gathers G into shared memory (conv_tc_fwd): here the
+//                materialised alternative (a K x M column gradient written
+//                and re-read, then col2im) measured slower, since the
+//                contraction over F is short and the column matrix large
+// m = (n, ho, wo), k = (c, i, j), f = output channel.  B200 has the HBM (180
+// GB, ~7 TB/s) to make the materialisation cheaper than gathering operands
+// element by element into shared memory (which measured at 5-35% of the TF32
+// pipe: the gather instruction rate, not the bytes, was the limit).
 //
-//   forward   y[m=(n,ho,wo), f]  = sum_k col[m,k] W[f,k] (+ b[f])
-//   data grad dx = col2im(W^T G) computed as a stride-1 convolution of G with
-//             the spatially flipped, channel-transposed filter
-//             W'[c, (f,i',j')] = W[f, c, kh-1-i', kw-1-j'] and padding kh-1-p
-//             (identical sums; needs stride 1 -- every non-data conv layer of
-//             the configured nets)
-//   weight grad dW[f, k] = sum_m G[m,f] col[m,k]; db[f] = sum_m G[m,f] rides
-//             along as an extra all-ones column k = K of col; the m range is
-//             split over CTAs into fixed-order partials (reduce_partials)
-//
-// CTA structure (warp-specialized over mbarriers):
-//   conv_tc_fwd (fwd and dgrad): warp 0 lane 0 streams the packed TF32 B
-//     operand (pack_conv_weights) into a STAGES-deep ring with 1-D bulk
-//     copies (complete_tx); warp 1 lane 0 issues 4 x tcgen05.mma (M=128,
-//     N=BN, K=8) per 32-wide K chunk into a TMEM accumulator and commits the
-//     stage back; warps 2-9 gather the A tile (thread = row, 16 of the 32 K
-//     values) and then run the epilogue (tcgen05.ld 32x32b, bias, ReLU,
-//     coalesced NCHW stores: lanes = consecutive output positions).
-//   conv_tc_wgrad: warp 0 lane 0 = MMA; warps 1-8 gather both operands with
-//     lanes over the 32 m values of a chunk (one 128-B swizzle row per warp
-//     store, conflict-free) and write the partial tile.
+// conv_gemm_tma: one CTA = one 128 x BN output tile, 6 warps: warp 0 lane 0
+// streams 32-wide K chunks of both operands by TMA (SWIZZLE_128B boxes,
+// mbarrier complete_tx) into a STAGES-deep ring, warp 1 lane 0 issues 4 x
+// tcgen05.mma.kind::tf32 (M=128, N=BN, K=8) per chunk into a TMEM
+// accumulator and commits each stage back, warps 2-5 read TMEM (32x32b, thread
+// = tile row) and apply the epilogue.  TMA zero-fills reads outside the
+// operand extents, so ragged M / K / F need no padding in memory.
 #include <cuda.h>
 
 #include <algorithm>
@@ -204,153 +202,6 @@ __global__ void __launch_bounds__(320, 1) conv_tc_fwd(const __grid_constant__ Co
   if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
 }
 
-// ================================================================ weight grad
-template <int BN>
-struct WgCfg {
-  static constexpr int STAGES = 3;  // BN <= 128: 97 KB, two CTAs per SM
-  static constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
-  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int THREADS = 288;
-};
-
-template <int BN>
-__global__ void __launch_bounds__(288, 2) conv_tc_wgrad(const __grid_constant__ ConvTcWgradP p) {
-  using Cfg = WgCfg<BN>;
-  constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
-  __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t sbase = smem_u32(smem), tab = sbase + STAGES * STAGE;
-  const int f0 = blockIdx.x * 128, k0 = blockIdx.y * BN, s = blockIdx.z;
-  const int HoWo = p.Ho * p.Wo, M = p.N * HoWo, HW = p.H * p.W, CHW = p.C * HW;
-  const int nc = (M + 31) / 32, c0 = (int)((long long)s * nc / p.splits),
-            c1 = (int)((long long)(s + 1) * nc / p.splits), my = c1 - c0;
-  for (int k = tid; k < BN; k += Cfg::THREADS) sts_i2(tab + 8 * k, ktab_entry(k0 + k, p.K, p.H, p.W, p.kh, p.kw));
-  if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) {
-      mbar_init(smem_u32(&full[st]), 256);
-      mbar_init(smem_u32(&empty[st]), 1);
-    }
-    mbar_init(smem_u32(&done), 1);
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc(&tmem_base, Cfg::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tmem_base;
-  pdl_enter();
-  if (warp == 0) {
-    if (lane == 0 && my > 0) {  // MMA issuer: D[f, k] += G^T[f, m] col^T[k, m]
-      constexpr uint32_t idesc = make_idesc(128, BN);
-      for (int c = 0; c < my; ++c) {
-        const int st = c % STAGES;
-        mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
-        tc_fence_after();
-        const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
-        mma_commit(smem_u32(&empty[st]));
-      }
-      mma_commit(smem_u32(&done));
-    }
-  } else {
-    // ---- gatherers: warp gw (0..7) takes rows gw, gw+8, ...; lane = m in chunk.
-    // Software-pipelined: the loads of chunk c+1 are in flight while chunk c
-    // is rounded and stored (two register sets, loop unrolled by two).
-    const int gw = warp - 1;
-    const uint32_t lane_off = (uint32_t)((lane & 3) * 4), lane_chunk = (uint32_t)(lane >> 2);
-    auto gather = [&](int c, float (&a)[16], float (&b)[BN / 8]) {
-      const int m = (c0 + c) * 32 + lane;
-      const bool live = m < M;
-      int n = 0, pos = 0, ho = 0, wo = 0;
-      if (live) {
-        n = m / HoWo;
-        pos = m - n * HoWo;
-        ho = pos / p.Wo;
-        wo = pos - ho * p.Wo;
-      }
-      const int hi0 = ho * p.sh - p.ph, wi0 = wo * p.sw - p.pw;
-      const float* gb = p.g + (size_t)n * p.F * HoWo + pos;
-      const float* xb = p.x + (size_t)n * CHW + (hi0 * p.W + wi0);
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int f = f0 + gw + 8 * t;
-        a[t] = (live && f < p.F) ? __ldg(gb + (size_t)f * HoWo) : 0.f;
-      }
-#pragma unroll
-      for (int t = 0; t < BN / 8; ++t) {
-        const int kk = gw + 8 * t, k = k0 + kk;
-        const int2 e = lds_i2(tab + 8 * kk);
-        const int i = e.y >> 16, j = e.y & 0xFFFF;
-        const bool ok = live && (unsigned)(hi0 + i) < (unsigned)p.H && (unsigned)(wi0 + j) < (unsigned)p.W;
-        float v = ok ? __ldg(xb + e.x) : 0.f;
-        if (k == p.K && p.bias_col) v = live ? 1.f : 0.f;
-        b[t] = v;
-      }
-    };
-    auto put = [&](int c, const float (&a)[16], const float (&b)[BN / 8]) {
-      const int st = c % STAGES;
-      if (c >= STAGES) mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
-      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
-#pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int row = gw + 8 * t;
-        sts32(As + row * 128 + ((lane_chunk ^ (row & 7)) << 4) + lane_off, tf32f(a[t]));
-      }
-#pragma unroll
-      for (int t = 0; t < BN / 8; ++t) {
-        const int row = gw + 8 * t;
-        sts32(Bs + row * 128 + ((lane_chunk ^ (row & 7)) << 4) + lane_off, tf32f(b[t]));
-      }
-      fence_proxy_async();
-      mbar_arrive(smem_u32(&full[st]));
-    };
-    float a0[16], b0[BN / 8], a1[16], b1[BN / 8];
-    if (my > 0) gather(0, a0, b0);
-    for (int c = 0; c < my; c += 2) {
-      if (c + 1 < my) gather(c + 1, a1, b1);
-      put(c, a0, b0);
-      if (c + 1 >= my) break;
-      if (c + 2 < my) gather(c + 2, a0, b0);
-      put(c + 1, a1, b1);
-    }
-    // ---- epilogue: the partial tile D[f, k] -> part[s][f*K + k] (bias col -> part[s][wcount + f])
-    const int quad = warp & 3, half = (warp - 1) >> 2, f = f0 + quad * 32 + lane;
-    if (my > 0) {
-      mbar_wait(smem_u32(&done), 0);
-      __syncwarp();
-      tc_fence_after();
-    }
-    float* pb = p.part + (size_t)s * p.pstride;
-    const long long wcount = (long long)p.F * p.K;
-#pragma unroll 1
-    for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
-      float v[16];
-      if (my > 0) {
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = 0.f;
-      }
-      if (f < p.F) {
-#pragma unroll
-        for (int t = 0; t < 16; ++t) {
-          const int k = k0 + cc + t;
-          if (k < p.K) pb[(size_t)f * p.K + k] = v[t];
-          else if (k == p.K && p.bias_col) pb[wcount + f] = v[t];
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
-}
-
 // ============================================================ weight packing
 // B image of the forward (mode 0: B[f][k] = W[f][k]) or data-gradient
 // (mode 1: B[c][(f,i',j')] = W[f][c][kh-1-i'][kw-1-j']) contraction: per
@@ -389,9 +240,12 @@ __global__ void pack_conv_weights(const __grid_constant__ ConvPackP p) {
 // (tile 128 k x BN f, m split over CTAs into fixed-order partials).  This
 // replaces the per-element register gather of conv_tc_wgrad, whose gather
 // instruction rate capped the weight gradient far below the tensor pipe.
-// exact a / d for 0 <= a < 2^24, d >= 1 (float estimate + one-step correction)
+// exact a / d for 0 <= a < 2^22, d >= 1: MUFU reciprocal estimate (relative
+// error ~2^-22, so the estimate is within one) + one-step correction
 __device__ __forceinline__ int qdiv(int a, int d) {
-  int q = __float2int_rz(__fmul_rn((float)a + 0.5f, __frcp_rn((float)d)));
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"((float)d));
+  int q = __float2int_rz(((float)a + 0.5f) * r);
   q -= (q * d > a);
   q += ((q + 1) * d <= a);
   return q;
@@ -462,8 +316,14 @@ static size_t tw_smem() {
   return 1024 + (size_t)TwCfg<BN>::STAGES * TwCfg<BN>::STAGE;
 }
 
-template <int BN>
-__global__ void __launch_bounds__(192, 1) conv_wgrad_tma(const __grid_constant__ ConvWgTmaP p) {
+// C[r, c] = sum_k A[r, k] B[c, k] over a dense K-major TF32 pair fed by TMA
+// (tile 128 x BN, 32-wide K chunks, K range split over blockIdx.z), with the
+// epilogue of the conv contraction it serves:
+//   EPI_WGRAD  r = k (patch element, K = bias row), c = f -> split partials
+//   EPI_FWD    r = m (output position), c = f -> y NCHW + bias (+ ReLU)
+enum { EPI_WGRAD = 0, EPI_FWD = 1 };
+template <int BN, int EPI>
+__global__ void __launch_bounds__(192, 1) conv_gemm_tma(const __grid_constant__ ConvGemmP p) {
   using Cfg = TwCfg<BN>;
   constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -472,8 +332,8 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_tma(const __grid_constant__
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = smem_u32(smem);
-  const int k0 = blockIdx.x * 128, f0 = blockIdx.y * BN, s = blockIdx.z;
-  const int nc = (p.M + 31) / 32, c0 = (int)((long long)s * nc / p.splits),
+  const int r0 = blockIdx.x * 128, q0 = blockIdx.y * BN, s = blockIdx.z;
+  const int nc = (p.Kdim + 31) / 32, c0 = (int)((long long)s * nc / p.splits),
             c1 = (int)((long long)(s + 1) * nc / p.splits), my = c1 - c0;
   if (tid == 0) {
     for (int st = 0; st < STAGES; ++st) {
@@ -497,8 +357,8 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_tma(const __grid_constant__
       if (c >= STAGES) mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
       const uint32_t bar = smem_u32(&full[st]), As = sbase + st * STAGE;
       mbar_expect_tx(bar, STAGE);
-      tma2d(As, &p.ta, (c0 + c) * 32, k0, bar);
-      tma2d(As + A_BYTES, &p.tb, (c0 + c) * 32, f0, bar);
+      tma2d(As, &p.ta, (c0 + c) * 32, r0, bar);
+      tma2d(As + A_BYTES, &p.tb, (c0 + c) * 32, q0, bar);
     }
   } else if (tid == 32) {  // MMA issuer
     constexpr uint32_t idesc = make_idesc(128, BN);
@@ -512,15 +372,18 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_tma(const __grid_constant__
       mma_commit(smem_u32(&empty[st]));
     }
     if (my > 0) mma_commit(smem_u32(&done));
-  } else if (warp >= 2) {  // epilogue: thread = k row (TMEM lane), columns f
-    const int quad = warp & 3, k = k0 + quad * 32 + lane;
+  } else if (warp >= 2) {  // epilogue: thread = tile row (TMEM lane)
+    const int quad = warp & 3, r = r0 + quad * 32 + lane;
     if (my > 0) {
       mbar_wait(smem_u32(&done), 0);
       __syncwarp();
       tc_fence_after();
     }
-    float* pb = p.part + (size_t)s * p.pstride;
-    const long long wcount = (long long)p.F * p.K;
+    int n = 0, pos = 0;
+    if (EPI == EPI_FWD && r < p.rows) {
+      n = r / p.HoWo;
+      pos = r - n * p.HoWo;
+    }
 #pragma unroll 1
     for (int cc = 0; cc < BN; cc += 16) {
       float v[16];
@@ -530,18 +393,76 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_tma(const __grid_constant__
 #pragma unroll
         for (int t = 0; t < 16; ++t) v[t] = 0.f;
       }
+      if (r >= p.rows) continue;
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
-        const int f = f0 + cc + t;
-        if (f >= p.F) break;
-        if (k < p.K) pb[(size_t)f * p.K + k] = v[t];
-        else if (k == p.K && p.bias) pb[wcount + f] = v[t];
+        const int q = q0 + cc + t;
+        if (q >= p.cols) break;
+        if (EPI == EPI_WGRAD) {  // r = k, q = f
+          float* pb = p.out + (size_t)s * p.pstride;
+          if (r < p.K) pb[(size_t)q * p.K + r] = v[t];
+          else if (p.has_bias) pb[(size_t)p.F * p.K + q] = v[t];  // r == K: the ones row
+        } else {  // EPI_FWD: r = m, q = f
+          float o = v[t];
+          if (p.bias) o += __ldg(p.bias + q);
+          if (p.relu) o = fmaxf(o, 0.f);
+          p.out[((size_t)n * p.F + q) * p.HoWo + pos] = o;
+        }
       }
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
+}
+
+// col[m][k] = tf32(x[n, c, ho*s-p+i, wo*s-p+j]) (row m contiguous in k, pitch
+// Kp): threads over k (a register-held (c,i,j) table entry each), a block
+// walks IMR_ROWS rows m -- coalesced stores, neighbouring-j loads
+constexpr int IMR_ROWS = 16;
+__global__ void __launch_bounds__(256) im2col_rows(const __grid_constant__ Im2colTP p) {
+  __shared__ int3 rowinfo[IMR_ROWS];  // per row m: input plane base offset, hi0, wi0
+  const int k = blockIdx.x * 256 + threadIdx.x, KK = p.kh * p.kw;
+  const int HoWo = p.Ho * p.Wo, M = p.N * HoWo, mb = blockIdx.y * IMR_ROWS;
+  if (threadIdx.x < IMR_ROWS) {
+    const int m = mb + threadIdx.x;
+    int3 e = make_int3(0, -(1 << 20), 0);
+    if (m < M) {
+      const int n = m / HoWo, pos = m - n * HoWo, ho = pos / p.Wo, wo = pos - ho * p.Wo;
+      e = make_int3(n * p.C * p.H * p.W, ho * p.sh - p.ph, wo * p.sw - p.pw);
+    }
+    rowinfo[threadIdx.x] = e;
+  }
+  int off = 0, i = 0, j = 0;
+  if (k < p.K) {
+    const int c = k / KK, r = k - c * KK;
+    i = r / p.kw;
+    j = r - i * p.kw;
+    off = c * p.H * p.W + i * p.W + j;
+  }
+  pdl_enter();
+  __syncthreads();
+  if (k >= p.K) return;
+  const int mend = min(IMR_ROWS, M - mb);
+#pragma unroll 4
+  for (int t = 0; t < mend; ++t) {
+    const int3 e = rowinfo[t];
+    const int hi = e.y + i, wi = e.z + j;
+    const float v = ((unsigned)hi < (unsigned)p.H && (unsigned)wi < (unsigned)p.W)
+                        ? tf32f(__ldg(p.x + (size_t)e.x + (e.y * p.W + e.z) + off))
+                        : 0.f;
+    p.col[(size_t)(mb + t) * p.pitch + k] = v;
+  }
+}
+
+// TF32 weight copy of the forward contraction: Wf[f][k] (row pitch Kp)
+__global__ void pack_plain(const __grid_constant__ PackPlainP p) {
+  pdl_enter();
+  const int total = p.F * p.K;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int f = e / p.K, k = e - f * p.K;
+    p.out[(size_t)f * p.pitch + k] = tf32f(__ldg(p.w + e));
+  }
 }
 
 // ================================================================ host side
@@ -563,46 +484,12 @@ template <int BN>
 static size_t fwd_smem(int nk) {
   return 1024 + (size_t)FwdCfg<BN>::STAGES * FwdCfg<BN>::STAGE + (size_t)nk * 32 * 8;
 }
-template <int BN>
-static size_t wg_smem() {
-  return 1024 + (size_t)WgCfg<BN>::STAGES * WgCfg<BN>::STAGE + (size_t)BN * 8;
-}
 
 #define PN_BN_LIST(X) X(32) X(64) X(96) X(128) X(192) X(256)
-
-cudaError_t setup(int max_nk) {
-  cudaError_t e = cudaSuccess;
-#define SET(BN)                                                                                            \
-  if (e == cudaSuccess)                                                                                    \
-    e = cudaFuncSetAttribute((const void*)conv_tc_fwd<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,    \
-                             (int)fwd_smem<BN>(max_nk));                                                   \
-  if (e == cudaSuccess)                                                                                    \
-    e = cudaFuncSetAttribute((const void*)conv_tc_wgrad<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)wg_smem<BN>());
-  PN_BN_LIST(SET)
-#undef SET
-#define SETW(BN)                                                                                            \
-  if (e == cudaSuccess)                                                                                     \
-    e = cudaFuncSetAttribute((const void*)conv_wgrad_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                             (int)tw_smem<BN>());
-  SETW(32) SETW(64) SETW(128) SETW(192) SETW(256)
-#undef SETW
-  return e;
-}
 
 int fwd_rows_pad(int F) {
   const int bn = pick_bn(F);
   return (F + bn - 1) / bn * bn;
-}
-
-size_t fwd_smem_bytes(int F, int nk) {
-  switch (pick_bn(F)) {
-#define CASE(BN) \
-  case BN: return fwd_smem<BN>(nk);
-    PN_BN_LIST(CASE)
-#undef CASE
-  }
-  return 0;
 }
 
 Launch conv_fwd_launch(const ConvTcP& p) {
@@ -619,37 +506,14 @@ Launch conv_fwd_launch(const ConvTcP& p) {
   return l;
 }
 
-static int pick_wbn(int Kb) {  // columns of the weight-gradient tile (K + bias column)
-  if (Kb <= 32) return 32;
-  if (Kb <= 64) return 64;
-  return 128;
-}
-
-int wgrad_splits(int N, int Ho, int Wo, int F, int K, int bias, int sms) {
-  // one wave at two CTAs per SM: splits = floor(2 sms / tiles), at least ~8
-  // chunks per split
-  const int bn = pick_wbn(K + bias);
-  const long long tiles = (long long)((F + 127) / 128) * ((K + bias + bn - 1) / bn);
-  const long long nc = ((long long)N * Ho * Wo + 31) / 32;
-  long long s = std::max(1LL, 2 * sms / tiles);
-  s = std::min(s, std::max(1LL, nc / 8));
-  return (int)s;
-}
-
-Launch conv_wgrad_launch(const ConvTcWgradP& p) {
+Launch pack_launch(const ConvPackP& p) {
   Launch l;
-  const int bn = pick_wbn(p.K + p.bias_col);
-  const dim3 grid((unsigned)((p.F + 127) / 128), (unsigned)((p.K + p.bias_col + bn - 1) / bn), (unsigned)p.splits);
-  switch (bn) {
-#define CASE(BN) \
-  case BN: l.set((const void*)conv_tc_wgrad<BN>, grid, dim3(WgCfg<BN>::THREADS), wg_smem<BN>(), p); break;
-    CASE(32) CASE(64) CASE(128)
-#undef CASE
-  }
+  const long long total = (long long)p.rows * p.nk * 32;
+  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148 * 8);
+  l.set((const void*)pack_conv_weights, dim3(blocks), dim3(256), 0, p);
   return l;
 }
 
-// ---- materialised-operand weight gradient
 static int pick_tw_bn(int F) {  // F columns per tile: one tile when F <= 256
   if (F <= 32) return 32;
   if (F <= 64) return 64;
@@ -658,17 +522,27 @@ static int pick_tw_bn(int F) {  // F columns per tile: one tile when F <= 256
   return (F + 1) / 2 <= 192 ? 192 : 256;
 }
 
-WgTmaPlan wgrad_tma_plan(int N, int Ho, int Wo, int F, int K, int bias, int sms) {
-  WgTmaPlan w;
-  w.bn = pick_tw_bn(F);
-  w.kpad = (K + bias + 127) / 128 * 128;
-  w.fpad = (F + w.bn - 1) / w.bn * w.bn;
+ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms) {
+  ConvTmaPlan w;
   const long long M = (long long)N * Ho * Wo;
-  w.pitch = (int)((M + 3) / 4 * 4);
-  const long long tiles = (long long)(w.kpad / 128) * (w.fpad / w.bn), nc = (M + 31) / 32;
+  w.M = (int)M;
+  w.K = C * kh * kw;
+  w.F = F;
+  w.bias = bias;
+  w.howo = Ho * Wo;
+  w.pitch_m = (int)((M + 3) / 4 * 4);
+  w.kp = (w.K + 3) / 4 * 4;
+  w.fp = (F + 3) / 4 * 4;
+  w.wg_bn = pick_tw_bn(F);
+  w.wg_kpad = (w.K + bias + 127) / 128 * 128;
+  w.wg_fpad = (F + w.wg_bn - 1) / w.wg_bn * w.wg_bn;
+  const long long tiles = (long long)(w.wg_kpad / 128) * (w.wg_fpad / w.wg_bn), nc = (M + 31) / 32;
   long long s = std::max(1LL, sms / tiles);  // one wave at one CTA per SM
-  s = std::min(s, std::max(1LL, nc / 8));
-  w.splits = (int)s;
+  w.wg_splits = (int)std::min(s, std::max(1LL, nc / 8));
+  w.fw_bn = pick_tw_bn(F);
+  const size_t colT = (size_t)w.wg_kpad * w.pitch_m, col = (size_t)M * w.kp;
+  w.col_floats = std::max(colT, col);
+  w.g_floats = std::max((size_t)w.wg_fpad * w.pitch_m, (size_t)M * w.fp);
   return w;
 }
 
@@ -680,10 +554,25 @@ Launch im2col_t_launch(const Im2colTP& p) {
   return l;
 }
 
+Launch im2col_rows_launch(const Im2colTP& p) {
+  Launch l;
+  const long long M = (long long)p.N * p.Ho * p.Wo;
+  l.set((const void*)im2col_rows, dim3((unsigned)((p.K + 255) / 256), (unsigned)((M + IMR_ROWS - 1) / IMR_ROWS)),
+        dim3(256), 0, p);
+  return l;
+}
+
 Launch gm_launch(const GmP& p) {
   Launch l;
   const long long total = (long long)p.N * p.F * p.HoWo;
   l.set((const void*)gather_gm, dim3((unsigned)std::min<long long>((total + 255) / 256, 148 * 16)), dim3(256), 0, p);
+  return l;
+}
+
+Launch pack_plain_launch(const PackPlainP& p) {
+  Launch l;
+  const long long total = (long long)p.F * p.K;
+  l.set((const void*)pack_plain, dim3((unsigned)std::min<long long>((total + 255) / 256, 148 * 8)), dim3(256), 0, p);
   return l;
 }
 
@@ -701,7 +590,8 @@ static EncodeTiledFn encode_fn() {
   }
   return fn;
 }
-// [rows][cols] fp32 (row pitch `pitch` floats), box {32 cols, box_rows}, 128B swizzle
+// [rows][cols] fp32 (row pitch `pitch` floats), box {32 cols, box_rows}, 128B
+// swizzle; reads outside [rows) x [cols) return zeros
 static bool tmap2d(CUtensorMap* m, const float* base, uint64_t rows, uint64_t cols, uint64_t pitch,
                    uint32_t box_rows) {
   std::memset(m, 0, sizeof(*m));
@@ -715,35 +605,68 @@ static bool tmap2d(CUtensorMap* m, const float* base, uint64_t rows, uint64_t co
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-bool wgrad_tma_launch(const WgTmaPlan& w, const float* col, const float* gm, float* part, int M, int K, int F,
-                      int bias, int pstride, Launch* out) {
-  ConvWgTmaP p;
-  bool ok = tmap2d(&p.ta, col, (uint64_t)w.kpad, (uint64_t)M, (uint64_t)w.pitch, 128);
-  ok = ok && tmap2d(&p.tb, gm, (uint64_t)w.fpad, (uint64_t)M, (uint64_t)w.pitch, (uint32_t)w.bn);
-  p.part = part;
-  p.M = M;
-  p.K = K;
-  p.F = F;
-  p.bias = bias;
-  p.splits = w.splits;
-  p.pstride = pstride;
-  const dim3 grid((unsigned)(w.kpad / 128), (unsigned)(w.fpad / w.bn), (unsigned)w.splits);
-  switch (w.bn) {
+template <int EPI>
+static bool gemm_launch(int bn, const ConvGemmP& p, dim3 grid, Launch* out) {
+  switch (bn) {
 #define CASE(BN) \
-  case BN: out->set((const void*)conv_wgrad_tma<BN>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); break;
+  case BN: out->set((const void*)conv_gemm_tma<BN, EPI>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); return true;
     CASE(32) CASE(64) CASE(128) CASE(192) CASE(256)
 #undef CASE
-    default: return false;
   }
-  return ok;
+  return false;
 }
 
-Launch pack_launch(const ConvPackP& p) {
-  Launch l;
-  const long long total = (long long)p.rows * p.nk * 32;
-  const unsigned blocks = (unsigned)std::min<long long>((total + 255) / 256, 148 * 8);
-  l.set((const void*)pack_conv_weights, dim3(blocks), dim3(256), 0, p);
-  return l;
+bool gemm_wgrad_launch(const ConvTmaPlan& w, const float* colT, const float* gm, float* part, int pstride,
+                       Launch* out) {
+  ConvGemmP p{};
+  bool ok = tmap2d(&p.ta, colT, (uint64_t)w.wg_kpad, (uint64_t)w.M, (uint64_t)w.pitch_m, 128);
+  ok = ok && tmap2d(&p.tb, gm, (uint64_t)w.wg_fpad, (uint64_t)w.M, (uint64_t)w.pitch_m, (uint32_t)w.wg_bn);
+  p.out = part;
+  p.Kdim = w.M;
+  p.rows = w.K + w.bias;
+  p.cols = w.F;
+  p.splits = w.wg_splits;
+  p.K = w.K;
+  p.F = w.F;
+  p.has_bias = w.bias;
+  p.pstride = pstride;
+  const dim3 grid((unsigned)(w.wg_kpad / 128), (unsigned)(w.wg_fpad / w.wg_bn), (unsigned)w.wg_splits);
+  return gemm_launch<EPI_WGRAD>(w.wg_bn, p, grid, out) && ok;
+}
+
+bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, const float* bias, float* y, int relu,
+                     Launch* out) {
+  ConvGemmP p{};
+  bool ok = tmap2d(&p.ta, col, (uint64_t)w.M, (uint64_t)w.K, (uint64_t)w.kp, 128);
+  ok = ok && tmap2d(&p.tb, wf, (uint64_t)w.F, (uint64_t)w.K, (uint64_t)w.kp, (uint32_t)w.fw_bn);
+  p.out = y;
+  p.bias = bias;
+  p.Kdim = w.K;
+  p.rows = w.M;
+  p.cols = w.F;
+  p.splits = 1;
+  p.F = w.F;
+  p.HoWo = w.howo;
+  p.relu = relu;
+  const dim3 grid((unsigned)((w.M + 127) / 128), (unsigned)((w.F + w.fw_bn - 1) / w.fw_bn), 1);
+  return gemm_launch<EPI_FWD>(w.fw_bn, p, grid, out) && ok;
+}
+
+
+cudaError_t setup(int max_nk) {
+  cudaError_t e = cudaSuccess;
+#define SET(BN)                                                                                         \
+  if (e == cudaSuccess)                                                                                 \
+    e = cudaFuncSetAttribute((const void*)conv_tc_fwd<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)fwd_smem<BN>(max_nk));
+  PN_BN_LIST(SET)
+#undef SET
+#define SETW(BN)                                                                                            \
+  for (const void* f : {(const void*)conv_gemm_tma<BN, EPI_WGRAD>, (const void*)conv_gemm_tma<BN, EPI_FWD>})   \
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
+  SETW(32) SETW(64) SETW(128) SETW(192) SETW(256)
+#undef SETW
+  return e;
 }
 
 }  // namespace tcc

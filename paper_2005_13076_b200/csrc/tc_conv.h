@@ -1,6 +1,6 @@
 // tc_conv.h -- host entry points of the general tcgen05 TF32 convolution
-// (tc_conv.cu): forward, data gradient (as a flipped-filter stride-1
-// convolution), split-m weight gradient, and the per-step TF32 weight packing.
+// (tc_conv.cu): im2col / col2im materialisation kernels, the TF32 weight
+// copies, and the TMA-fed GEMM of the forward, weight and data gradients.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -10,29 +10,42 @@
 
 namespace pn {
 namespace tcc {
-cudaError_t setup(int max_nk);  // opt-in shared memory for K up to max_nk*32
-int fwd_rows_pad(int F);        // rows of the packed B image for an output of F channels
-size_t fwd_smem_bytes(int F, int nk);
+cudaError_t setup(int max_nk);  // opt-in shared memory (gather kernel: K up to max_nk*32)
+
+// ---- data gradient: implicit GEMM with gathered operand (stride-1 convs):
+// dx = W' (*) G, W'[c][(f,i',j')] = W[f][c][kh-1-i'][kw-1-j'], pad kh-1-p
+int fwd_rows_pad(int F);  // rows of the packed (swizzled) B image for F output channels
 Launch conv_fwd_launch(const ConvTcP& p);
-int wgrad_splits(int N, int Ho, int Wo, int F, int K, int bias, int sms);
-Launch conv_wgrad_launch(const ConvTcWgradP& p);
 Launch pack_launch(const ConvPackP& p);
 
-// weight gradient over materialised TF32 operands (colT, Gm), TMA-fed
-struct ConvWgTmaP {
-  CUtensorMap ta;  // colT [Kpad][pitch]: box {32 m, 128 k}
-  CUtensorMap tb;  // Gm   [Fpad][pitch]: box {32 m, BN f}
-  float* part;     // [splits][pstride]: w at f*K + k, b at F*K + f
-  int M, K, F, bias, splits, pstride;
+// ---- the contractions over materialised TF32 operands (TMA-fed GEMM)
+struct ConvGemmP {
+  CUtensorMap ta;  // A [rows][Kdim] K-major, box {32, 128}
+  CUtensorMap tb;  // B [cols][Kdim] K-major, box {32, BN}
+  float* out;
+  const float* bias;
+  int Kdim, rows, cols, splits;
+  int K, F, has_bias, pstride;  // weight gradient
+  int HoWo, relu;               // forward
 };
-struct WgTmaPlan {
-  int bn, kpad, fpad, pitch, splits;
+// shapes of one conv layer's materialised operands and GEMM tilings
+struct ConvTmaPlan {
+  int M, K, F, bias, howo;
+  int pitch_m;  // row pitch of colT / Gm (floats, multiple of 4)
+  int kp, fp;   // row pitch of col / Wf (K) and of Gt / Wt (F)
+  int wg_bn, wg_kpad, wg_fpad, wg_splits;
+  int fw_bn;
+  size_t col_floats, g_floats;  // workspace this layer needs
 };
-WgTmaPlan wgrad_tma_plan(int N, int Ho, int Wo, int F, int K, int bias, int sms);
-Launch im2col_t_launch(const Im2colTP& p);
-Launch gm_launch(const GmP& p);
-// false if the tensor-map encoding failed
-bool wgrad_tma_launch(const WgTmaPlan& w, const float* col, const float* gm, float* part, int M, int K, int F,
-                      int bias, int pstride, Launch* out);
+ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms);
+Launch im2col_t_launch(const Im2colTP& p);     // colT [k][m] (weight gradient)
+Launch im2col_rows_launch(const Im2colTP& p);  // col  [m][k] (forward)
+Launch gm_launch(const GmP& p);                // Gm   [f][m] (weight gradient)
+Launch pack_plain_launch(const PackPlainP& p);
+// false if a tensor-map encoding failed
+bool gemm_wgrad_launch(const ConvTmaPlan& w, const float* colT, const float* gm, float* part, int pstride,
+                       Launch* out);
+bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, const float* bias, float* y, int relu,
+                     Launch* out);
 }  // namespace tcc
 }  // namespace pn

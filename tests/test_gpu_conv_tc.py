@@ -103,13 +103,12 @@ def test_conv_tc_teacher_forced(case):
         fst = [st for st in fwd if st.startswith(name + ".fwd")]
         assert fst and fst[0].endswith("[tc]"), fwd
         fused_relu = "+relu" in fst[0]   # in-place ReLU (slope 0) applied in the conv epilogue
-        for st in fwd:
-            if st.startswith(name + ".wpack"):
-                run_stage(net, 0, st)
-        # forward from the oracle's bottom
+        # forward from the oracle's bottom: weight copies, im2col, GEMM
         if L["bottom"] != ref.input_name:
             net.net_put_blob(L["bottom"], out["blobs"][bottom_layer(ref, L)].astype(np.float32))
-        run_stage(net, 0, fst[0], xd, yd)
+        for st in fwd:
+            if st.startswith(name + "."):
+                run_stage(net, 0, st, xd, yd)
         S = out["scales"][name]
         want = out["blobs"][name]
         if fused_relu:
@@ -129,10 +128,11 @@ def test_conv_tc_teacher_forced(case):
                      gref["grads"][name + ".b"], gs[name + ".b"], rtol)
         if L["bottom"] != ref.input_name:
             dst = [st for st in bwd if st.startswith(name + ".dgrad")]
-            assert dst and dst[0].endswith("[tc]"), bwd
-            run_stage(net, 1, dst[0])
+            assert dst and all(st.endswith("[tc]") for st in dst), bwd
+            for st in dst:
+                run_stage(net, 1, st)
             want = gref["diffs"][name]
-            if "+relu_bwd" in dst[0]:
+            if any("+relu_bwd" in st for st in dst):
                 # the in-place ReLU below is back-propagated in the dgrad epilogue
                 relu = [M for M in ref.layers if M["type"] == "ReLU" and M["top"] == L["bottom"]][-1]
                 want = gref["diffs"][relu["name"]]
