@@ -127,15 +127,16 @@ def parse_layers(text):
 
 def layer_stage_work(layers, name, N):
     """Algorithmic (flops, bytes) of one stage of the layerwise plan at batch N:
-    compulsory fp32 reads + writes of the stage (weights once, masks int32)."""
+    compulsory fp32 reads + writes of the stage (weights once, masks int32).
+    Stage names are "<layer>.<op>[+fused][tag]" (layer names have no dots)."""
     base = name.split("[")[0]
-    lname, _, op = base.rpartition(".")
-    op = op.split("+")[0]  # "fwd+relu": the fused ReLU adds no algorithmic traffic
-    by = {L["name"]: L for L in layers}
     if base == "loss_reduce":
         return (0, N * 4 + 4)
     if base == "sgd":
         return (0, sum(L.get("params", 0) for L in layers) * 20)
+    lname, _, op = base.partition(".")
+    op = ".".join(t.split("+")[0] for t in op.split("."))  # "fwd+relu": fused ReLU adds no traffic
+    by = {L["name"]: L for L in layers}
     L = by.get(lname)
     if L is None:
         return None
@@ -144,18 +145,20 @@ def layer_stage_work(layers, name, N):
     P = L.get("params", 0) * 4
     if L["type"] in ("Convolution", "InnerProduct"):
         fl = 2 * N * L["macs"]
-        if op == "fwd":
-            return (fl, cin + cout + P)
-        if op in ("wgrad", "dgrad"):
-            return (fl, cin + cout + P)
-        if op == "bgrad":
-            return (0, cout + P)
-        if op.startswith("wpack"):
-            return (0, 2 * P)
-        if op == "wgrad_reduce":
-            return (0, 2 * P)
+        K = (L["params"] - L["out"][0]) // L["out"][0]  # weights per output channel = C*kh*kw (or K)
+        M = N * L["out"][1] * L["out"][2]
+        table = {
+            "fwd": (fl, cin + cout + P), "wgrad": (fl, cin + cout + P), "dgrad": (fl, cin + cout + P),
+            "bgrad": (0, cout + P), "wpack": (0, 2 * P), "wpack_dgrad": (0, 2 * P), "wgrad_reduce": (0, 2 * P),
+            "nhwc": (0, 2 * cin), "dgrad.nhwc": (0, 2 * cout), "wgrad.gm": (0, 2 * cout),
+            "im2col": (0, cin + M * K * 4), "wgrad.im2col": (0, cin + M * (K + 1) * 4),
+        }
+        w = table.get(op)
+        if w and "+relu_bwd" in name:  # the ReLU output read by the fused backward
+            w = (w[0], w[1] + cin)
+        return w
     if L["type"] == "Pooling":
-        return (0, cin + cout + (cout if L["max"] else 0))
+        return (0, cin + cout + (cout if L["max"] else 0) + (cin if "+relu_bwd" in name else 0))
     if L["type"] == "ReLU":
         return (0, 2 * cin if op == "fwd" else 3 * cin)
     if L["type"] == "SoftmaxWithLoss":

@@ -72,6 +72,10 @@ struct Layer {
   // materialised TF32 operands (plan tp, weight copy Wf [F][kp]); data
   // gradient as an implicit GEMM over gathered G (swizzled W' image bdg)
   bool tc_conv = false, tc_dgrad = false, tma_fwd = false;
+  bool tap_fwd = false, tap_dgrad = false;  // stride-1 tap GEMM over NHWC (tc_conv.cu)
+  int cp_in = 0, cp_out = 0;                // NHWC channel pitches of x and of G
+  float* wtap_f = nullptr;                  // [T][F][cp_in]
+  float* wtap_d = nullptr;                  // [T][C][cp_out]
   tcc::ConvTmaPlan tp{};
   float* wf = nullptr;   // Wf [F][kp] (materialised forward)
   float* bfwd = nullptr; // swizzled W image (gathered forward)
@@ -453,9 +457,14 @@ static pn_status allocate(pn_net* net) {
   size_t col_n = 0, gm_n = 0;
   for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images, wgrad workspaces
     if (L.tc_conv) {
-      if (L.tma_fwd) TRY(net->alloc(&L.wf, (size_t)L.F * L.tp.kp));
+      const size_t T = (size_t)L.kh * L.kw;
+      if (L.tap_fwd) TRY(net->alloc(&L.wtap_f, T * L.F * L.cp_in));
+      else if (L.tma_fwd) TRY(net->alloc(&L.wf, (size_t)L.F * L.tp.kp));
       else TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
-      if (L.tc_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
+      if (L.tap_dgrad) TRY(net->alloc(&L.wtap_d, T * L.in[1] * L.cp_out));
+      if (L.tap_fwd) col_n = std::max(col_n, (size_t)net->batch * L.in[2] * L.in[3] * L.cp_in);
+      if (L.tap_dgrad) col_n = std::max(col_n, (size_t)net->batch * L.out[2] * L.out[3] * L.cp_out);
+      if (L.tc_dgrad && !L.tap_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
       col_n = std::max(col_n, L.tp.col_floats);
       gm_n = std::max(gm_n, L.tp.g_floats);
     }
@@ -575,25 +584,42 @@ static void build_layerwise(pn_net* net) {
     Launch l;
     if (relu_in_conv[li]) continue;
     if (L.type == L_CONV && L.tc_conv) {
-      // im2col + GEMM.  Long contractions (K >= 1024): the TF32
-      // column matrix col [m][k] is materialised and streamed by TMA; short
-      // ones gather it straight into shared memory (the column matrix would
-      // cost more HBM traffic than the GEMM saves)
+      // im2col + GEMM, engine chosen at net_create:
+      // stride-1 tap GEMM over NHWC, materialised TF32 column matrix col
+      // [m][k] streamed by TMA, or the column matrix gathered straight into
+      // shared memory
       const bool relu = li + 1 < net->layers.size() && relu_in_conv[li + 1];
       const float* bias = L.bias ? net->params + L.off + L.wcount : nullptr;
       auto xpatch = [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; };
-      if (L.tma_fwd) {
+      if (L.tap_fwd) {
+        PackTapsP pk{net->params + L.off, L.wtap_f, L.F, L.in[1], L.kh, L.kw, L.cp_in, 0};
+        add(fwd, L.name + ".wpack[tc]", tcc::pack_taps_launch(pk));
+      } else if (L.tma_fwd) {
         PackPlainP pk{net->params + L.off, L.wf, L.F, L.tp.K, L.tp.kp};
         add(fwd, L.name + ".wpack[tc]", tcc::pack_plain_launch(pk));
       } else {
         ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
         add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
       }
-      if (L.tc_dgrad) {
+      if (L.tap_dgrad) {
+        PackTapsP pd{net->params + L.off, L.wtap_d, L.F, L.in[1], L.kh, L.kw, L.cp_out, 1};
+        add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_taps_launch(pd));
+      } else if (L.tc_dgrad) {
         ConvPackP pd{net->params + L.off, L.bdg, L.F, L.in[1], L.kh, L.kw, L.dg_rows, L.dg_nk, 1};
         add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_launch(pd));
       }
-      if (L.tma_fwd) {
+      if (L.tap_fwd) {
+        // stride 1: x to NHWC (TF32), then the tap GEMM (no column matrix)
+        NhwcP nh{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.cp_in};
+        add(fwd, L.name + ".nhwc[tc]", tcc::nhwc_launch(nh),
+            isx ? [](Launch& l, const StepArgs& a) { l.params<NhwcP>().x = a.x; }
+                : std::function<void(Launch&, const StepArgs&)>());
+        Launch lt;
+        if (!tcc::tap_launch(net->col_ws, N, L.in[2], L.in[3], L.cp_in, L.wtap_f, L.F, L.cp_in, L.kh, L.kw, L.ph, L.pw,
+                             1, L.out[2], L.out[3], L.F, bias, relu ? 1 : 0, nullptr, top->data, &lt))
+          net->tmap_failed = true;
+        add(fwd, L.name + (relu ? ".fwd+relu[tc]" : ".fwd[tc]"), lt);
+      } else if (L.tma_fwd) {
         Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
                     L.out[3], L.tp.K, L.tp.K, L.tp.kp};
         add(fwd, L.name + ".im2col[tc]", tcc::im2col_rows_launch(ic),
@@ -686,7 +712,17 @@ static void build_layerwise(pn_net* net) {
         net->tmap_failed = true;
       add(bwd, L.name + ".wgrad[tc]", lw);
       add_reduce(net, bwd, L);
-      if (bot && L.tc_dgrad) {
+      if (bot && L.tap_dgrad) {
+        // data gradient: col2im(W^T G) = sum over taps of G shifted
+        // by (p - i, p - j) times W_t^T -- G to NHWC, then the tap GEMM
+        NhwcP nh{top.diff, net->col_ws, N, L.F, L.out[2], L.out[3], L.cp_out};
+        add(bwd, L.name + ".dgrad.nhwc[tc]", tcc::nhwc_launch(nh));
+        Launch lt;
+        if (!tcc::tap_launch(net->col_ws, N, L.out[2], L.out[3], L.cp_out, L.wtap_d, L.in[1], L.cp_out, L.kh, L.kw,
+                             L.ph, L.pw, -1, L.in[2], L.in[3], L.in[1], nullptr, 0, relu_y, bot->diff, &lt))
+          net->tmap_failed = true;
+        add(bwd, L.name + (relu_y ? ".dgrad+relu_bwd[tc]" : ".dgrad[tc]"), lt);
+      } else if (bot && L.tc_dgrad) {
         // data gradient: col2im(W^T G) = W' (*) G, stride 1, pad
         // kh-1-p, as an implicit GEMM gathering G (+ the in-place ReLU below)
         ConvTcP q{top.diff, L.bdg, nullptr, bot->diff, N, L.F, L.out[2], L.out[3], L.in[1], L.kh, L.kw, 1, 1,
@@ -1068,14 +1104,21 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     for (auto& L : net->layers) {
       if (L.type != L_CONV) continue;
       L.tc_conv = true;
-      L.tma_fwd = L.in[1] * L.kh * L.kw >= 1024;
-      if (!L.tma_fwd) {
+      // forward: tap GEMM for stride-1 layers with >= 16 input channels,
+      // materialised im2col for strided layers with K >= 256 (AlexNet conv1),
+      // else the gather kernel (C = 3, K = 75: cifar conv1)
+      L.tap_fwd = L.sh == 1 && L.sw == 1 && L.in[1] >= 16;
+      L.cp_in = (L.in[1] + 3) / 4 * 4;
+      L.cp_out = (L.F + 3) / 4 * 4;
+      L.tma_fwd = !L.tap_fwd && L.in[1] * L.kh * L.kw >= 256;
+      if (!L.tma_fwd && !L.tap_fwd) {
         L.fwd_rows = tcc::fwd_rows_pad(L.F);
         L.fwd_nk = (L.in[1] * L.kh * L.kw + 31) / 32;
         max_nk = std::max(max_nk, L.fwd_nk);
       }
       L.tc_dgrad = L.bottom != net->input_name && L.sh == 1 && L.sw == 1 && L.ph < L.kh && L.pw < L.kw;
-      if (L.tc_dgrad) {
+      L.tap_dgrad = L.tc_dgrad && L.F >= 16;
+      if (L.tc_dgrad && !L.tap_dgrad) {
         L.dg_rows = tcc::fwd_rows_pad(L.in[1]);
         L.dg_nk = (L.F * L.kh * L.kw + 31) / 32;
         max_nk = std::max(max_nk, L.dg_nk);

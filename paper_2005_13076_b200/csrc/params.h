@@ -192,6 +192,16 @@ struct ConvPackP {  // TF32 B image of the forward (mode 0) / data-gradient (mod
   float* out;       // [nk][rows][32] SW128
   int F, C, kh, kw, rows, nk, mode;
 };
+struct NhwcP {  // out[n][h][w][c] = tf32(x[n][c][h][w]), channels padded to cp
+  const float* x;
+  float* out;
+  int N, C, H, W, cp;
+};
+struct PackTapsP {  // per-tap TF32 weight matrices (tc_conv.cu pack_taps)
+  const float* w;   // [F][C][kh][kw]
+  float* out;       // [kh*kw][rows][ip]
+  int F, C, kh, kw, ip, mode;  // mode 0: rows f, inner c (forward); 1: rows c, inner f (data gradient)
+};
 struct Im2colTP {  // colT[k][m] = tf32(col[m][k]) (k < K), 1 (k == K: bias row)
   const float* x;
   float* col;  // [rows][pitch]

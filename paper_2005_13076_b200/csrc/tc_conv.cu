@@ -184,6 +184,15 @@ __global__ void __launch_bounds__(320, 1) conv_tc_fwd(const __grid_constant__ Co
     for (int cc = half * (BN / 2); cc < (half + 1) * (BN / 2); cc += 16) {
       float v[16];
       tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
+      if (elive && p.relu_y) {  // the ReLU outputs first: 16 independent loads, then the stores
+        float y[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          y[t] = f0 + cc + t < p.F ? __ldg(p.relu_y + (yb - p.y) + (size_t)(f0 + cc + t) * HoWo) : 0.f;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)
+          if (!(y[t] > 0.f)) v[t] = 0.f;
+      }
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
         const int f = f0 + cc + t;
@@ -191,7 +200,6 @@ __global__ void __launch_bounds__(320, 1) conv_tc_fwd(const __grid_constant__ Co
           float o = v[t];
           if (p.bias) o += __ldg(p.bias + f);
           if (p.relu) o = fmaxf(o, 0.f);
-          if (p.relu_y && !(__ldg(p.relu_y + (yb - p.y) + (size_t)f * HoWo) > 0.f)) o = 0.f;
           yb[(size_t)f * HoWo] = o;
         }
       }
@@ -465,6 +473,159 @@ __global__ void pack_plain(const __grid_constant__ PackPlainP p) {
   }
 }
 
+// ================================== stride-1 convolution as a TMA tap GEMM
+// With the activation in NHWC (channels innermost, TF32, padded to Cp), the
+// A tile of tap (i,j) for a block of 128 output positions is ONE 4-D TMA box
+// {32 channels, BW, BH, BNI images} taken at the positions shifted by the tap;
+// TMA zero-fills whatever falls outside the image -- the padding -- so the
+// convolution is sum over taps and 32-channel chunks of [128 x 32] x [32 x BN]
+// with no gather at all:
+//   forward    y[n,f,oh,ow]  = sum_{i,j,c} x[n, oh+i-p, ow+j-p, c] W[f,c,i,j]
+//   data grad  dx[n,c,h,w]   = sum_{i,j,f} G[n, h-i+p, w-j+p, f] W[f,c,i,j]
+// (the same loop with the tap offset negated: s = +1 / -1).  B_t = per-tap
+// weight matrix [out channels][in channels] (pack_taps).  Every stride, pitch
+// is a multiple of 16 B because Cp is -- unlike NCHW rows of 27 or 13 floats,
+// which TMA cannot address.
+__device__ __forceinline__ void tma4d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3,
+                                      uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(bar)
+      : "memory");
+}
+
+template <int BN>
+__global__ void __launch_bounds__(192, 1) conv_tap_tma(const __grid_constant__ ConvTapP p) {
+  using Cfg = TwCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  // output block: BNI images x BH rows x BW columns
+  int t = blockIdx.x;
+  const int tw = t % p.tiles_w;
+  t /= p.tiles_w;
+  const int th = t % p.tiles_h;
+  const int n0 = (t / p.tiles_h) * p.bni, oh0 = th * p.bh, ow0 = tw * p.bw;
+  const int q0 = blockIdx.y * BN;
+  const int nkc = (p.cp + 31) / 32, nk = p.kh * p.kw * nkc;
+  if (tid == 0) {
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(smem_u32(&full[st]), 1);
+      mbar_init(smem_u32(&empty[st]), 1);
+    }
+    mbar_init(smem_u32(&done), 1);
+    fence_barrier_init();
+    prefetch_tmap(&p.ta);
+    prefetch_tmap(&p.tb);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, Cfg::TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  pdl_enter();
+  if (tid == 0) {  // TMA producer: chunk c = (tap, 32-channel block)
+    for (int c = 0; c < nk; ++c) {
+      const int st = c % STAGES, tap = c / nkc, kc = c - tap * nkc, i = tap / p.kw, j = tap - i * p.kw;
+      if (c >= STAGES) mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
+      const uint32_t bar = smem_u32(&full[st]), As = sbase + st * STAGE;
+      mbar_expect_tx(bar, STAGE);
+      tma4d(As, &p.ta, kc * 32, ow0 + p.sgn * (j - p.pw), oh0 + p.sgn * (i - p.ph), n0, bar);
+      tma3d(As + A_BYTES, &p.tb, kc * 32, q0, tap, bar);
+    }
+  } else if (tid == 32) {  // MMA issuer
+    constexpr uint32_t idesc = make_idesc(128, BN);
+    for (int c = 0; c < nk; ++c) {
+      const int st = c % STAGES;
+      mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
+      tc_fence_after();
+      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+      mma_commit(smem_u32(&empty[st]));
+    }
+    mma_commit(smem_u32(&done));
+  } else if (warp >= 2) {  // epilogue: thread = output position of the block
+    const int quad = warp & 3, r = quad * 32 + lane;
+    const int bw = r % p.bw, rr = r / p.bw, bh = rr % p.bh, bi = rr / p.bh;
+    const int n = n0 + bi, oh = oh0 + bh, ow = ow0 + bw;
+    const bool live = n < p.N && oh < p.Ho && ow < p.Wo;
+    mbar_wait(smem_u32(&done), 0);
+    __syncwarp();
+    tc_fence_after();
+    const size_t HoWo = (size_t)p.Ho * p.Wo, base = (size_t)n * p.F * HoWo + (size_t)oh * p.Wo + ow;
+#pragma unroll 1
+    for (int cc = 0; cc < BN; cc += 16) {
+      float v[16];
+      tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
+      if (!live) continue;
+      if (p.relu_y) {  // the ReLU outputs first: 16 independent loads, then the stores
+        float y[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          y[u] = q0 + cc + u < p.F ? __ldg(p.relu_y + base + (size_t)(q0 + cc + u) * HoWo) : 0.f;
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          if (!(y[u] > 0.f)) v[u] = 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int q = q0 + cc + u;
+        if (q >= p.F) break;
+        float o = v[u];
+        if (p.bias) o += __ldg(p.bias + q);
+        if (p.relu) o = fmaxf(o, 0.f);
+        p.out[base + (size_t)q * HoWo] = o;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
+}
+
+// NCHW -> NHWC (channels padded to cp with zeros), TF32: 32 x 32 smem transposes
+__global__ void __launch_bounds__(256) to_nhwc(const __grid_constant__ NhwcP p) {
+  __shared__ float t[32][33];
+  pdl_enter();
+  const int n = blockIdx.z, s0 = blockIdx.x * 32, c0 = blockIdx.y * 32, HW = p.H * p.W;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  for (int y = ty; y < 32; y += 8) {
+    const int c = c0 + y, sp = s0 + tx;
+    t[y][tx] = (c < p.C && sp < HW) ? tf32f(__ldg(p.x + ((size_t)n * p.C + c) * HW + sp)) : 0.f;
+  }
+  __syncthreads();
+  for (int y = ty; y < 32; y += 8) {
+    const int sp = s0 + y, c = c0 + tx;
+    if (sp < HW && c < p.cp) p.out[((size_t)n * HW + sp) * p.cp + c] = t[tx][y];
+  }
+}
+
+// per-tap weight matrices, TF32: mode 0 (forward) out[t][f][c] = W[f][c][t],
+// mode 1 (data gradient) out[t][c][f] = W[f][c][t]; inner dimension padded to
+// ip with zeros (rows beyond the channel count are never read: TMA bounds)
+__global__ void pack_taps(const __grid_constant__ PackTapsP p) {
+  pdl_enter();
+  const int T = p.kh * p.kw, rows = p.mode == 0 ? p.F : p.C, inner = p.mode == 0 ? p.C : p.F;
+  const long long total = (long long)T * rows * p.ip;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    const int k = (int)(e % p.ip);
+    const long long tr = e / p.ip;
+    const int r = (int)(tr % rows), t = (int)(tr / rows);
+    float v = 0.f;
+    if (k < inner) {
+      const int f = p.mode == 0 ? r : k, c = p.mode == 0 ? k : r;
+      v = tf32f(__ldg(p.w + ((size_t)f * p.C + c) * T + t));
+    }
+    p.out[e] = v;
+  }
+}
+
 // ================================================================ host side
 static int pick_bn(int F) {
   if (F <= 32) return 32;
@@ -653,6 +814,81 @@ bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, co
 }
 
 
+// ---- tap GEMM
+static int pow2_at_least(int v, int lo) {
+  int r = lo;
+  while (r < v) r <<= 1;
+  return r;
+}
+
+bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float* wtaps, int rows, int ip, int kh,
+                int kw, int ph, int pw, int sgn, int Ho, int Wo, int F, const float* bias, int relu,
+                const float* relu_y, float* out, Launch* l) {
+  ConvTapP p{};
+  p.bw = std::min(32, pow2_at_least(Wo, 8));
+  p.bh = std::min(128 / p.bw, pow2_at_least(Ho, 1));
+  p.bni = 128 / (p.bw * p.bh);
+  p.tiles_w = (Wo + p.bw - 1) / p.bw;
+  p.tiles_h = (Ho + p.bh - 1) / p.bh;
+  const int bn = pick_tw_bn(F);
+  EncodeTiledFn fn = encode_fn();
+  bool ok = fn != nullptr;
+  {
+    cuuint64_t dims[4] = {(cuuint64_t)cp, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)cp * 4, (cuuint64_t)Win * cp * 4, (cuuint64_t)Hin * Win * cp * 4};
+    cuuint32_t box[4] = {32, (cuuint32_t)p.bw, (cuuint32_t)p.bh, (cuuint32_t)p.bni};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    ok = ok && fn(&p.ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)nhwc, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  {
+    cuuint64_t dims[3] = {(cuuint64_t)ip, (cuuint64_t)rows, (cuuint64_t)(kh * kw)};
+    cuuint64_t strides[2] = {(cuuint64_t)ip * 4, (cuuint64_t)rows * ip * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)bn, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    ok = ok && fn(&p.tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)wtaps, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  p.bias = bias;
+  p.relu_y = relu_y;
+  p.out = out;
+  p.N = N;
+  p.Ho = Ho;
+  p.Wo = Wo;
+  p.F = F;
+  p.cp = cp;
+  p.kh = kh;
+  p.kw = kw;
+  p.ph = ph;
+  p.pw = pw;
+  p.sgn = sgn;
+  p.relu = relu;
+  const dim3 grid((unsigned)(p.tiles_w * p.tiles_h * ((N + p.bni - 1) / p.bni)), (unsigned)((F + bn - 1) / bn));
+  switch (bn) {
+#define CASE(BN) \
+  case BN: l->set((const void*)conv_tap_tma<BN>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); return ok;
+    CASE(32) CASE(64) CASE(128) CASE(192) CASE(256)
+#undef CASE
+  }
+  return false;
+}
+
+Launch nhwc_launch(const NhwcP& p) {
+  Launch l;
+  l.set((const void*)to_nhwc, dim3((unsigned)((p.H * p.W + 31) / 32), (unsigned)((p.cp + 31) / 32), (unsigned)p.N),
+        dim3(256), 0, p);
+  return l;
+}
+
+Launch pack_taps_launch(const PackTapsP& p) {
+  Launch l;
+  const long long total = (long long)p.kh * p.kw * (p.mode == 0 ? p.F : p.C) * p.ip;
+  l.set((const void*)pack_taps, dim3((unsigned)std::min<long long>((total + 255) / 256, 148 * 8)), dim3(256), 0, p);
+  return l;
+}
+
 cudaError_t setup(int max_nk) {
   cudaError_t e = cudaSuccess;
 #define SET(BN)                                                                                         \
@@ -666,6 +902,11 @@ cudaError_t setup(int max_nk) {
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
   SETW(32) SETW(64) SETW(128) SETW(192) SETW(256)
 #undef SETW
+#define SETT(BN)      \
+  if (e == cudaSuccess) \
+    e = cudaFuncSetAttribute((const void*)conv_tap_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
+  SETT(32) SETT(64) SETT(128) SETT(192) SETT(256)
+#undef SETT
   return e;
 }
 

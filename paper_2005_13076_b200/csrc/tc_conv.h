@@ -47,5 +47,23 @@ bool gemm_wgrad_launch(const ConvTmaPlan& w, const float* colT, const float* gm,
                        Launch* out);
 bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, const float* bias, float* y, int relu,
                      Launch* out);
+
+// ---- stride-1 convolution as a TMA tap GEMM over NHWC (forward and data gradient)
+struct ConvTapP {
+  CUtensorMap ta;  // NHWC activation [N][H][W][cp], box {32, bw, bh, bni}
+  CUtensorMap tb;  // per-tap weights [T][rows][ip], box {32, BN, 1}
+  const float* bias;
+  const float* relu_y;
+  float* out;      // NCHW [N][F][Ho][Wo]
+  int N, Ho, Wo, F, cp, kh, kw, ph, pw, sgn;
+  int bw, bh, bni, tiles_w, tiles_h, relu;
+};
+// in: NHWC activation (N x Hin x Win x cp); out: F channels of Ho x Wo;
+// sgn = +1 forward (input at out + tap - pad), -1 data gradient (out - tap + pad)
+bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float* wtaps, int rows, int ip, int kh,
+                int kw, int ph, int pw, int sgn, int Ho, int Wo, int F, const float* bias, int relu,
+                const float* relu_y, float* out, Launch* l);
+Launch nhwc_launch(const NhwcP& p);
+Launch pack_taps_launch(const PackTapsP& p);
 }  // namespace tcc
 }  // namespace pn
