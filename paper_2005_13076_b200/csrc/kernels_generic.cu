@@ -37,59 +37,48 @@ __device__ __forceinline__ float block_sum(float v, float* sm) {
 // ---------------------------------------------------------------- conv fwd
 // each output is the inner product of a filter with one sliding
 // window (cross-correlation, R1); bias after the sum (Listing 1).
+// (32-bit index math throughout: every blob has fewer than 2^31 elements)
 __global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p) {
   pdl_enter();
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)p.N * p.F * p.Ho * p.Wo;
-  if (idx >= total) return;
-  int wo = idx % p.Wo;
-  int ho = (idx / p.Wo) % p.Ho;
-  int f = (idx / ((long long)p.Wo * p.Ho)) % p.F;
-  int n = idx / ((long long)p.Wo * p.Ho * p.F);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int HoWo = p.Ho * p.Wo;
+  if (idx >= p.N * p.F * HoWo) return;
+  const int nf = idx / HoWo, pos = idx - nf * HoWo, n = nf / p.F, f = nf - n * p.F;
+  const int ho = pos / p.Wo, wo = pos - ho * p.Wo;
+  const int h0 = ho * p.sh - p.ph, w0 = wo * p.sw - p.pw;
+  const int i0 = max(0, -h0), i1 = min(p.kh, p.H - h0), j0 = max(0, -w0), j1 = min(p.kw, p.W - w0);
   float acc = 0.f;
   for (int c = 0; c < p.C; ++c) {
-    const float* xp = p.x + ((long long)n * p.C + c) * p.H * p.W;
-    const float* wp = p.w + ((long long)f * p.C + c) * p.kh * p.kw;
-    for (int i = 0; i < p.kh; ++i) {
-      int h = ho * p.sh - p.ph + i;
-      if (h < 0 || h >= p.H) continue;
-      for (int j = 0; j < p.kw; ++j) {
-        int w = wo * p.sw - p.pw + j;
-        if (w < 0 || w >= p.W) continue;
-        acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(xp + h * p.W + w), acc);
-      }
-    }
+    const float* xp = p.x + ((size_t)n * p.C + c) * p.H * p.W + h0 * p.W + w0;
+    const float* wp = p.w + ((size_t)f * p.C + c) * p.kh * p.kw;
+    for (int i = i0; i < i1; ++i)
+      for (int j = j0; j < j1; ++j) acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(xp + i * p.W + j), acc);
   }
   if (p.b) acc += __ldg(p.b + f);
   p.y[idx] = acc;
 }
 
-// col2im(W^T dy) evaluated per input element (gather form).
+// col2im(W^T dy) evaluated per input element (gather form): the
+// output positions whose window covers (h, w) are a rectangle [ho0, ho1] x
+// [wo0, wo1] (no per-tap divisibility tests).
 __global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p) {
   pdl_enter();
-  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long total = (long long)p.N * p.C * p.H * p.W;
-  if (idx >= total) return;
-  int w = idx % p.W;
-  int h = (idx / p.W) % p.H;
-  int c = (idx / ((long long)p.W * p.H)) % p.C;
-  int n = idx / ((long long)p.W * p.H * p.C);
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int HW = p.H * p.W, HoWo = p.Ho * p.Wo;
+  if (idx >= p.N * p.C * HW) return;
+  const int nc = idx / HW, r = idx - nc * HW, n = nc / p.C, c = nc - n * p.C;
+  const int h = r / p.W, w = r - h * p.W;
+  const int th = h + p.ph, tw = w + p.pw;  // ho*sh + i = th, wo*sw + j = tw
+  const int ho0 = th >= p.kh ? (th - p.kh) / p.sh + 1 : 0, ho1 = min(th / p.sh, p.Ho - 1);
+  const int wo0 = tw >= p.kw ? (tw - p.kw) / p.sw + 1 : 0, wo1 = min(tw / p.sw, p.Wo - 1);
   float acc = 0.f;
   for (int f = 0; f < p.F; ++f) {
-    const float* dyp = p.dy + ((long long)n * p.F + f) * p.Ho * p.Wo;
-    const float* wp = p.w + ((long long)f * p.C + c) * p.kh * p.kw;
-    for (int i = 0; i < p.kh; ++i) {
-      int t = h + p.ph - i;
-      if (t < 0 || t % p.sh) continue;
-      int ho = t / p.sh;
-      if (ho >= p.Ho) continue;
-      for (int j = 0; j < p.kw; ++j) {
-        int u = w + p.pw - j;
-        if (u < 0 || u % p.sw) continue;
-        int wo = u / p.sw;
-        if (wo >= p.Wo) continue;
-        acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(dyp + ho * p.Wo + wo), acc);
-      }
+    const float* dyp = p.dy + ((size_t)n * p.F + f) * HoWo;
+    const float* wp = p.w + ((size_t)f * p.C + c) * p.kh * p.kw;
+    for (int ho = ho0; ho <= ho1; ++ho) {
+      const int i = th - ho * p.sh;
+      for (int wo = wo0; wo <= wo1; ++wo)
+        acc = fmaf(__ldg(wp + i * p.kw + (tw - wo * p.sw)), __ldg(dyp + ho * p.Wo + wo), acc);
     }
   }
   p.dx[idx] = acc;
@@ -105,29 +94,30 @@ __global__ void __launch_bounds__(256) conv_bwd_weight_generic(
   const int n0 = (int)((long long)p.N * s / p.splits);
   const int n1 = (int)((long long)p.N * (s + 1) / p.splits);
   const int P = p.Ho * p.Wo;
-  const long long cnt = (long long)(n1 - n0) * P;
+  const int cnt = (n1 - n0) * P;
   const int taps = p.kh * p.kw;
   for (int t0 = 0; t0 < taps; t0 += 16) {
     float acc[16];
+    int ti[16], tj[16];
 #pragma unroll
-    for (int q = 0; q < 16; ++q) acc[q] = 0.f;
+    for (int q = 0; q < 16; ++q) {
+      acc[q] = 0.f;
+      ti[q] = (t0 + q) / p.kw;
+      tj[q] = (t0 + q) - ti[q] * p.kw;
+    }
     float bacc = 0.f;
-    for (long long e = threadIdx.x; e < cnt; e += blockDim.x) {
-      int n = n0 + (int)(e / P);
-      int pos = (int)(e % P);
-      int ho = pos / p.Wo, wo = pos % p.Wo;
-      float g = __ldg(p.dy + ((long long)n * p.F + f) * P + pos);
+    for (int e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const int nn = e / P, pos = e - nn * P, n = n0 + nn;
+      const int ho = pos / p.Wo, wo = pos - ho * p.Wo;
+      const float g = __ldg(p.dy + ((size_t)n * p.F + f) * P + pos);
       if (t0 == 0) bacc += g;
-      const float* xp = p.x + ((long long)n * p.C + c) * p.H * p.W;
+      const int h0 = ho * p.sh - p.ph, w0 = wo * p.sw - p.pw;
+      const float* xp = p.x + ((size_t)n * p.C + c) * p.H * p.W;
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
-        int t = t0 + q;
-        if (t < taps) {
-          int i = t / p.kw, j = t % p.kw;
-          int h = ho * p.sh - p.ph + i, w = wo * p.sw - p.pw + j;
-          if (h >= 0 && h < p.H && w >= 0 && w < p.W)
-            acc[q] = fmaf(g, __ldg(xp + h * p.W + w), acc[q]);
-        }
+        const int h = h0 + ti[q], w = w0 + tj[q];
+        if (t0 + q < taps && (unsigned)h < (unsigned)p.H && (unsigned)w < (unsigned)p.W)
+          acc[q] = fmaf(g, __ldg(xp + h * p.W + w), acc[q]);
       }
     }
 #pragma unroll 1
@@ -328,18 +318,29 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
       d[o] = v;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < HW; r += blockDim.x) {
-      const int h = r / p.W, w = r - h * p.W;
-      const short2 ar = arow[h], bc = bcol[w];
-      float acc = 0.f;
-      for (int a = ar.x; a <= ar.y; ++a)
-        for (int b = bc.x; b <= bc.y; ++b) {
-          const int o = a * p.Wp + b;
-          if (p.method != 0 || m[o] == r) acc += d[o];
-        }
-      const size_t idx = (size_t)nc * HW + r;
-      if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) acc = 0.f;
-      p.dx[idx] = acc;
+    // 4 inputs per thread per pass: their ReLU-output loads are issued together
+    for (int r0 = threadIdx.x; r0 < HW; r0 += 4 * blockDim.x) {
+      float y[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * blockDim.x;
+        y[u] = (p.relu_y && r < HW) ? __ldg(p.relu_y + (size_t)nc * HW + r) : 1.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int r = r0 + u * blockDim.x;
+        if (r >= HW) break;
+        const int h = r / p.W, w = r - h * p.W;
+        const short2 ar = arow[h], bc = bcol[w];
+        float acc = 0.f;
+        for (int a = ar.x; a <= ar.y; ++a)
+          for (int b = bc.x; b <= bc.y; ++b) {
+            const int o = a * p.Wp + b;
+            if (p.method != 0 || m[o] == r) acc += d[o];
+          }
+        if (!(y[u] > 0.f)) acc = 0.f;
+        p.dx[(size_t)nc * HW + r] = acc;
+      }
     }
   }
 }

@@ -259,8 +259,9 @@ __device__ __forceinline__ int qdiv(int a, int d) {
   return q;
 }
 
-// block = 256 consecutive m x a group of IM_KROWS k rows: (n, ho, wo) once per
-// thread, (c, i, j) from a shared table, one coalesced store per element
+// block = 1024 consecutive m (4 per thread: one 16-B store per k row) x a
+// group of IM_KROWS k rows; (n, ho, wo) of the thread's 4 positions computed
+// once, (c, i, j) from a shared table
 constexpr int IM_KROWS = 16;
 __global__ void __launch_bounds__(256) im2col_t(const __grid_constant__ Im2colTP p) {
   __shared__ int2 tab[IM_KROWS];
@@ -279,24 +280,56 @@ __global__ void __launch_bounds__(256) im2col_t(const __grid_constant__ Im2colTP
   }
   pdl_enter();
   __syncthreads();
-  const int m = blockIdx.x * 256 + threadIdx.x;
-  if (m >= M) return;
-  const int n = qdiv(m, HoWo), pos = m - n * HoWo, ho = qdiv(pos, p.Wo), wo = pos - ho * p.Wo;
-  const int hi0 = ho * p.sh - p.ph, wi0 = wo * p.sw - p.pw;
-  const float* xb = p.x + (size_t)n * p.C * p.H * p.W + (hi0 * p.W + wi0);
+  // unit-stride layers: 4 consecutive m per thread (one 16-B store per k
+  // row); strided layers: one m per thread (their loads do not coalesce
+  // across the 4 positions anyway)
+  const int V = p.sw == 1 ? 4 : 1;
+  const int m0 = V * (blockIdx.x * 256 + threadIdx.x);
+  if (m0 >= M) return;
+  int hi0[4], wi0[4], xoff[4];
+  {
+    int n = qdiv(m0, HoWo), pos = m0 - n * HoWo, ho = qdiv(pos, p.Wo), wo = pos - ho * p.Wo;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      hi0[u] = ho * p.sh - p.ph;
+      wi0[u] = wo * p.sw - p.pw;
+      xoff[u] = n * p.C * p.H * p.W + hi0[u] * p.W + wi0[u];
+      if (m0 + u >= M || u >= V) hi0[u] = -(1 << 20);  // past the end / unused: zeros
+      if (++wo == p.Wo) {
+        wo = 0;
+        if (++ho == p.Ho) {
+          ho = 0;
+          ++n;
+        }
+      }
+    }
+  }
   const int kend = min(IM_KROWS, p.Kb - kb0);
-  float* dst = p.col + (size_t)kb0 * p.pitch + m;
-#pragma unroll 4
+  const bool full4 = V == 4 && m0 + 4 <= M;
+  float* dst = p.col + (size_t)kb0 * p.pitch + m0;
+#pragma unroll 2
   for (int t = 0; t < kend; ++t) {
     const int2 e = tab[t];
-    float v;
+    float v[4];
     if (e.y == -1) {
-      v = 1.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) v[u] = 1.f;
     } else {
       const int i = e.y >> 16, j = e.y & 0xFFFF;
-      v = ((unsigned)(hi0 + i) < (unsigned)p.H && (unsigned)(wi0 + j) < (unsigned)p.W) ? tf32f(__ldg(xb + e.x)) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        v[u] = (u < V && (unsigned)(hi0[u] + i) < (unsigned)p.H && (unsigned)(wi0[u] + j) < (unsigned)p.W)
+                   ? tf32f(__ldg(p.x + (xoff[u] + e.x)))
+                   : 0.f;
     }
-    dst[(size_t)t * p.pitch] = v;
+    float* d = dst + (size_t)t * p.pitch;
+    if (full4) {
+      *reinterpret_cast<float4*>(d) = make_float4(v[0], v[1], v[2], v[3]);
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (u < V && m0 + u < M) d[u] = v[u];
+    }
   }
 }
 
@@ -330,63 +363,132 @@ static size_t tw_smem() {
 //   EPI_WGRAD  r = k (patch element, K = bias row), c = f -> split partials
 //   EPI_FWD    r = m (output position), c = f -> y NCHW + bias (+ ReLU)
 enum { EPI_WGRAD = 0, EPI_FWD = 1 };
-template <int BN, int EPI>
-__global__ void __launch_bounds__(192, 1) conv_gemm_tma(const __grid_constant__ ConvGemmP p) {
+// Persistent warp-specialized TMA -> tcgen05 GEMM skeleton shared by the
+// conv contractions: grid = min(tiles, SMs), CTA b takes tiles b, b+grid, ...
+//   warp 0 lane 0  TMA producer, one K chunk per ring stage, running ahead
+//                  across tile boundaries
+//   warp 1 lane 0  MMA issuer into one of two TMEM accumulators (tile parity)
+//   warps 2-5      epilogue of tile t from its accumulator while the MMA
+//                  already fills the other one with tile t+1
+// Op supplies num_tiles(), tile(t) -> Info (coordinates and chunk count nk),
+// issue(info, chunk, A, B, bar) and epilogue(info, tmem, quad, lane).
+template <int BN, class Op>
+__global__ void __launch_bounds__(192, 1) tc_persistent(const __grid_constant__ typename Op::Params prm) {
   using Cfg = TwCfg<BN>;
-  constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE;
+  constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE, TC = Cfg::TMEM_COLS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
+  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t sbase = smem_u32(smem);
-  const int r0 = blockIdx.x * 128, q0 = blockIdx.y * BN, s = blockIdx.z;
-  const int nc = (p.Kdim + 31) / 32, c0 = (int)((long long)s * nc / p.splits),
-            c1 = (int)((long long)(s + 1) * nc / p.splits), my = c1 - c0;
+  const Op op(prm);
+  const int ntiles = op.num_tiles();
   if (tid == 0) {
     for (int st = 0; st < STAGES; ++st) {
       mbar_init(smem_u32(&full[st]), 1);
       mbar_init(smem_u32(&empty[st]), 1);
     }
-    mbar_init(smem_u32(&done), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(smem_u32(&tfull[b]), 1);
+      mbar_init(smem_u32(&tempty[b]), 128);
+    }
     fence_barrier_init();
-    prefetch_tmap(&p.ta);
-    prefetch_tmap(&p.tb);
+    op.prefetch();
   }
-  if (warp == 0) tmem_alloc(&tmem_base, Cfg::TMEM_COLS);
+  if (warp == 0) tmem_alloc(&tmem_base, 2 * TC);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   pdl_enter();
-  if (tid == 0) {  // TMA producer
-    for (int c = 0; c < my; ++c) {
-      const int st = c % STAGES;
-      if (c >= STAGES) mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
-      const uint32_t bar = smem_u32(&full[st]), As = sbase + st * STAGE;
-      mbar_expect_tx(bar, STAGE);
-      tma2d(As, &p.ta, (c0 + c) * 32, r0, bar);
-      tma2d(As + A_BYTES, &p.tb, (c0 + c) * 32, q0, bar);
+  if (tid == 0) {  // TMA producer (tile decoded once; per chunk only the box coordinates)
+    int g = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const typename Op::Info t = op.tile(tile);
+      for (int c = 0; c < t.nk; ++c, ++g) {
+        const int st = g % STAGES;
+        if (g >= STAGES) mbar_wait(smem_u32(&empty[st]), ((g / STAGES) - 1) & 1);
+        const uint32_t bar = smem_u32(&full[st]), As = sbase + st * STAGE;
+        mbar_expect_tx(bar, STAGE);
+        op.issue(t, c, As, As + A_BYTES, bar);
+      }
     }
   } else if (tid == 32) {  // MMA issuer
     constexpr uint32_t idesc = make_idesc(128, BN);
-    for (int c = 0; c < my; ++c) {
-      const int st = c % STAGES;
-      mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
+    int g = 0, it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1, nk = op.tile(tile).nk;
+      if (it >= 2) mbar_wait(smem_u32(&tempty[buf]), ((it >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
+      const uint32_t acc = tbase + buf * TC;
+      for (int c = 0; c < nk; ++c, ++g) {
+        const int st = g % STAGES;
+        mbar_wait(smem_u32(&full[st]), (g / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
-      mma_commit(smem_u32(&empty[st]));
+        for (int k = 0; k < 4; ++k) mma_tf32(acc, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+        mma_commit(smem_u32(&empty[st]));
+      }
+      mma_commit(smem_u32(&tfull[buf]));  // (every tile has nk >= 1: the accumulator is always written)
     }
-    if (my > 0) mma_commit(smem_u32(&done));
-  } else if (warp >= 2) {  // epilogue: thread = tile row (TMEM lane)
-    const int quad = warp & 3, r = r0 + quad * 32 + lane;
-    if (my > 0) {
-      mbar_wait(smem_u32(&done), 0);
+  } else if (warp >= 2) {  // epilogue
+    const int quad = warp & 3;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+      const int buf = it & 1;
+      mbar_wait(smem_u32(&tfull[buf]), (it >> 1) & 1);
       __syncwarp();
       tc_fence_after();
+      op.template epilogue<BN>(op.tile(tile), tbase + buf * TC + ((uint32_t)(quad * 32) << 16), quad, lane);
+      tc_fence_before();
+      mbar_arrive(smem_u32(&tempty[buf]));
     }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, 2 * TC);
+}
+
+// C[r, c] = sum_k A[r, k] B[c, k] over a dense K-major TF32 pair by 2-D TMA
+// (tile 128 x BN, 32-wide K chunks, K range split into `splits` tiles), with
+// the epilogue of the conv contraction it serves:
+//   EPI_WGRAD  r = k (patch element, K = bias row), c = f -> split partials
+//   EPI_FWD    r = m (output position), c = f -> y NCHW + bias (+ ReLU)
+template <int EPI>
+struct GemmOp {
+  using Params = ConvGemmP;
+  const ConvGemmP& p;
+  int rt, ct;  // row / column tiles
+  __device__ GemmOp(const ConvGemmP& q) : p(q), rt((q.rows + 127) / 128), ct(q.ctiles) {}
+  __device__ int num_tiles() const { return rt * ct * p.splits; }
+  __device__ void prefetch() const { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
+  struct Info {
+    int r0, q0, s, k0, nk;  // row / column origin, split, first K element, chunks (0: past Kdim, zeros)
+  };
+  __device__ Info tile(int t) const {
+    Info i;
+    i.r0 = (t % rt) * 128;
+    t /= rt;
+    i.q0 = (t % ct) * p.bn;
+    i.s = t / ct;
+    const int nc = (p.Kdim + 31) / 32, c0 = (int)((long long)i.s * nc / p.splits),
+              c1 = (int)((long long)(i.s + 1) * nc / p.splits);
+    // an empty split range (never planned, but safe) reads one chunk past Kdim: zeros
+    i.k0 = c1 > c0 ? c0 * 32 : nc * 32;
+    i.nk = max(1, c1 - c0);
+    return i;
+  }
+  __device__ void issue(const Info& t, int c, uint32_t As, uint32_t Bs, uint32_t bar) const {
+    const int k = t.k0 + c * 32;
+    tma2d(As, &p.ta, k, t.r0, bar);
+    tma2d(Bs, &p.tb, k, t.q0, bar);
+  }
+  template <int BN>
+  __device__ void epilogue(const Info& t, uint32_t taddr, int quad, int lane) const {
+    const int r0 = t.r0, q0 = t.q0, s = t.s;
+    const int r = r0 + quad * 32 + lane;
     int n = 0, pos = 0;
     if (EPI == EPI_FWD && r < p.rows) {
       n = r / p.HoWo;
@@ -395,13 +497,11 @@ __global__ void __launch_bounds__(192, 1) conv_gemm_tma(const __grid_constant__ 
 #pragma unroll 1
     for (int cc = 0; cc < BN; cc += 16) {
       float v[16];
-      if (my > 0) {
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 16; ++t) v[t] = 0.f;
-      }
+      tmem_ld16(taddr + cc, v);
       if (r >= p.rows) continue;
+      float bv[16];
+#pragma unroll
+      for (int t = 0; t < 16; ++t) bv[t] = (EPI == EPI_FWD && p.bias && q0 + cc + t < p.cols) ? __ldg(p.bias + q0 + cc + t) : 0.f;
 #pragma unroll
       for (int t = 0; t < 16; ++t) {
         const int q = q0 + cc + t;
@@ -411,18 +511,14 @@ __global__ void __launch_bounds__(192, 1) conv_gemm_tma(const __grid_constant__ 
           if (r < p.K) pb[(size_t)q * p.K + r] = v[t];
           else if (p.has_bias) pb[(size_t)p.F * p.K + q] = v[t];  // r == K: the ones row
         } else {  // EPI_FWD: r = m, q = f
-          float o = v[t];
-          if (p.bias) o += __ldg(p.bias + q);
+          float o = v[t] + bv[t];
           if (p.relu) o = fmaxf(o, 0.f);
           p.out[((size_t)n * p.F + q) * p.HoWo + pos] = o;
         }
       }
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
-}
+};
 
 // col[m][k] = tf32(x[n, c, ho*s-p+i, wo*s-p+j]) (row m contiguous in k, pitch
 // Kp): threads over k (a register-held (c,i,j) table entry each), a block
@@ -495,74 +591,45 @@ __device__ __forceinline__ void tma4d(uint32_t dst, const CUtensorMap* m, int c0
       : "memory");
 }
 
-template <int BN>
-__global__ void __launch_bounds__(192, 1) conv_tap_tma(const __grid_constant__ ConvTapP p) {
-  using Cfg = TwCfg<BN>;
-  constexpr int STAGES = Cfg::STAGES, A_BYTES = Cfg::A_BYTES, STAGE = Cfg::STAGE;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
-  __shared__ uint32_t tmem_base;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const uint32_t sbase = smem_u32(smem);
-  // output block: BNI images x BH rows x BW columns
-  int t = blockIdx.x;
-  const int tw = t % p.tiles_w;
-  t /= p.tiles_w;
-  const int th = t % p.tiles_h;
-  const int n0 = (t / p.tiles_h) * p.bni, oh0 = th * p.bh, ow0 = tw * p.bw;
-  const int q0 = blockIdx.y * BN;
-  const int nkc = (p.cp + 31) / 32, nk = p.kh * p.kw * nkc;
-  if (tid == 0) {
-    for (int st = 0; st < STAGES; ++st) {
-      mbar_init(smem_u32(&full[st]), 1);
-      mbar_init(smem_u32(&empty[st]), 1);
-    }
-    mbar_init(smem_u32(&done), 1);
-    fence_barrier_init();
-    prefetch_tmap(&p.ta);
-    prefetch_tmap(&p.tb);
+struct TapOp {
+  using Params = ConvTapP;
+  const ConvTapP& p;
+  int ti;  // position tiles
+  __device__ TapOp(const ConvTapP& q) : p(q), ti(q.tiles_w * q.tiles_h * ((q.N + q.bni - 1) / q.bni)) {}
+  __device__ int num_tiles() const { return ti * p.ctiles; }
+  __device__ void prefetch() const { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
+  struct Info {
+    int n0, oh0, ow0, q0, nkc, nk;
+  };
+  __device__ Info tile(int tile) const {
+    Info i;
+    i.q0 = (tile / ti) * p.bn;
+    int t = tile % ti;
+    i.ow0 = (t % p.tiles_w) * p.bw;
+    t /= p.tiles_w;
+    i.oh0 = (t % p.tiles_h) * p.bh;
+    i.n0 = (t / p.tiles_h) * p.bni;
+    i.nkc = (p.cp + 31) / 32;
+    i.nk = p.kh * p.kw * i.nkc;
+    return i;
   }
-  if (warp == 0) tmem_alloc(&tmem_base, Cfg::TMEM_COLS);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tbase = tmem_base;
-  pdl_enter();
-  if (tid == 0) {  // TMA producer: chunk c = (tap, 32-channel block)
-    for (int c = 0; c < nk; ++c) {
-      const int st = c % STAGES, tap = c / nkc, kc = c - tap * nkc, i = tap / p.kw, j = tap - i * p.kw;
-      if (c >= STAGES) mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
-      const uint32_t bar = smem_u32(&full[st]), As = sbase + st * STAGE;
-      mbar_expect_tx(bar, STAGE);
-      tma4d(As, &p.ta, kc * 32, ow0 + p.sgn * (j - p.pw), oh0 + p.sgn * (i - p.ph), n0, bar);
-      tma3d(As + A_BYTES, &p.tb, kc * 32, q0, tap, bar);
-    }
-  } else if (tid == 32) {  // MMA issuer
-    constexpr uint32_t idesc = make_idesc(128, BN);
-    for (int c = 0; c < nk; ++c) {
-      const int st = c % STAGES;
-      mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
-      tc_fence_after();
-      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
-      mma_commit(smem_u32(&empty[st]));
-    }
-    mma_commit(smem_u32(&done));
-  } else if (warp >= 2) {  // epilogue: thread = output position of the block
-    const int quad = warp & 3, r = quad * 32 + lane;
+  __device__ void issue(const Info& t, int c, uint32_t As, uint32_t Bs, uint32_t bar) const {
+    const int tap = c / t.nkc, kc = c - tap * t.nkc, i = tap / p.kw, j = tap - i * p.kw;
+    tma4d(As, &p.ta, kc * 32, t.ow0 + p.sgn * (j - p.pw), t.oh0 + p.sgn * (i - p.ph), t.n0, bar);
+    tma3d(Bs, &p.tb, kc * 32, t.q0, tap, bar);
+  }
+  template <int BN>
+  __device__ void epilogue(const Info& t, uint32_t taddr, int quad, int lane) const {
+    const int n0 = t.n0, oh0 = t.oh0, ow0 = t.ow0, q0 = t.q0;
+    const int r = quad * 32 + lane;
     const int bw = r % p.bw, rr = r / p.bw, bh = rr % p.bh, bi = rr / p.bh;
     const int n = n0 + bi, oh = oh0 + bh, ow = ow0 + bw;
     const bool live = n < p.N && oh < p.Ho && ow < p.Wo;
-    mbar_wait(smem_u32(&done), 0);
-    __syncwarp();
-    tc_fence_after();
     const size_t HoWo = (size_t)p.Ho * p.Wo, base = (size_t)n * p.F * HoWo + (size_t)oh * p.Wo + ow;
 #pragma unroll 1
     for (int cc = 0; cc < BN; cc += 16) {
       float v[16];
-      tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
+      tmem_ld16(taddr + cc, v);
       if (!live) continue;
       if (p.relu_y) {  // the ReLU outputs first: 16 independent loads, then the stores
         float y[16];
@@ -573,21 +640,20 @@ __global__ void __launch_bounds__(192, 1) conv_tap_tma(const __grid_constant__ C
         for (int u = 0; u < 16; ++u)
           if (!(y[u] > 0.f)) v[u] = 0.f;
       }
+      float bv[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) bv[u] = (p.bias && q0 + cc + u < p.F) ? __ldg(p.bias + q0 + cc + u) : 0.f;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int q = q0 + cc + u;
         if (q >= p.F) break;
-        float o = v[u];
-        if (p.bias) o += __ldg(p.bias + q);
+        float o = v[u] + bv[u];
         if (p.relu) o = fmaxf(o, 0.f);
         p.out[base + (size_t)q * HoWo] = o;
       }
     }
   }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, Cfg::TMEM_COLS);
-}
+};
 
 // NCHW -> NHWC (channels padded to cp with zeros), TF32: 32 x 32 smem transposes
 __global__ void __launch_bounds__(256) to_nhwc(const __grid_constant__ NhwcP p) {
@@ -710,7 +776,8 @@ ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, i
 Launch im2col_t_launch(const Im2colTP& p) {
   Launch l;
   const long long M = (long long)p.N * p.Ho * p.Wo;
-  l.set((const void*)im2col_t, dim3((unsigned)((M + 255) / 256), (unsigned)((p.Kb + IM_KROWS - 1) / IM_KROWS)),
+  const long long per_block = p.sw == 1 ? 1024 : 256;  // (see the kernel)
+  l.set((const void*)im2col_t, dim3((unsigned)((M + per_block - 1) / per_block), (unsigned)((p.Kb + IM_KROWS - 1) / IM_KROWS)),
         dim3(256), 0, p);
   return l;
 }
@@ -766,11 +833,19 @@ static bool tmap2d(CUtensorMap* m, const float* base, uint64_t rows, uint64_t co
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static int g_sms = 148;  // SM count of the device (setup())
+
 template <int EPI>
-static bool gemm_launch(int bn, const ConvGemmP& p, dim3 grid, Launch* out) {
+static bool gemm_launch(int bn, ConvGemmP& p, Launch* out) {
+  p.bn = bn;
+  p.ctiles = (p.cols + bn - 1) / bn;
+  const long long tiles = (long long)((p.rows + 127) / 128) * p.ctiles * p.splits;
+  const dim3 grid((unsigned)std::min<long long>(tiles, g_sms));
   switch (bn) {
-#define CASE(BN) \
-  case BN: out->set((const void*)conv_gemm_tma<BN, EPI>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); return true;
+#define CASE(BN)                                                                                              \
+  case BN:                                                                                                    \
+    out->set((const void*)tc_persistent<BN, GemmOp<EPI>>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); \
+    return true;
     CASE(32) CASE(64) CASE(128) CASE(192) CASE(256)
 #undef CASE
   }
@@ -791,8 +866,7 @@ bool gemm_wgrad_launch(const ConvTmaPlan& w, const float* colT, const float* gm,
   p.F = w.F;
   p.has_bias = w.bias;
   p.pstride = pstride;
-  const dim3 grid((unsigned)(w.wg_kpad / 128), (unsigned)(w.wg_fpad / w.wg_bn), (unsigned)w.wg_splits);
-  return gemm_launch<EPI_WGRAD>(w.wg_bn, p, grid, out) && ok;
+  return gemm_launch<EPI_WGRAD>(w.wg_bn, p, out) && ok;
 }
 
 bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, const float* bias, float* y, int relu,
@@ -809,8 +883,7 @@ bool gemm_fwd_launch(const ConvTmaPlan& w, const float* col, const float* wf, co
   p.F = w.F;
   p.HoWo = w.howo;
   p.relu = relu;
-  const dim3 grid((unsigned)((w.M + 127) / 128), (unsigned)((w.F + w.fw_bn - 1) / w.fw_bn), 1);
-  return gemm_launch<EPI_FWD>(w.fw_bn, p, grid, out) && ok;
+  return gemm_launch<EPI_FWD>(w.fw_bn, p, out) && ok;
 }
 
 
@@ -865,10 +938,13 @@ bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float*
   p.pw = pw;
   p.sgn = sgn;
   p.relu = relu;
-  const dim3 grid((unsigned)(p.tiles_w * p.tiles_h * ((N + p.bni - 1) / p.bni)), (unsigned)((F + bn - 1) / bn));
+  p.bn = bn;
+  p.ctiles = (F + bn - 1) / bn;
+  const long long tiles = (long long)p.tiles_w * p.tiles_h * ((N + p.bni - 1) / p.bni) * p.ctiles;
+  const dim3 grid((unsigned)std::min<long long>(tiles, g_sms));
   switch (bn) {
 #define CASE(BN) \
-  case BN: l->set((const void*)conv_tap_tma<BN>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); return ok;
+  case BN: l->set((const void*)tc_persistent<BN, TapOp>, grid, dim3(TwCfg<BN>::THREADS), tw_smem<BN>(), p); return ok;
     CASE(32) CASE(64) CASE(128) CASE(192) CASE(256)
 #undef CASE
   }
@@ -890,7 +966,9 @@ Launch pack_taps_launch(const PackTapsP& p) {
 }
 
 cudaError_t setup(int max_nk) {
-  cudaError_t e = cudaSuccess;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
 #define SET(BN)                                                                                         \
   if (e == cudaSuccess)                                                                                 \
     e = cudaFuncSetAttribute((const void*)conv_tc_fwd<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
@@ -898,13 +976,13 @@ cudaError_t setup(int max_nk) {
   PN_BN_LIST(SET)
 #undef SET
 #define SETW(BN)                                                                                            \
-  for (const void* f : {(const void*)conv_gemm_tma<BN, EPI_WGRAD>, (const void*)conv_gemm_tma<BN, EPI_FWD>})   \
+  for (const void* f : {(const void*)tc_persistent<BN, GemmOp<EPI_WGRAD>>, (const void*)tc_persistent<BN, GemmOp<EPI_FWD>>}) \
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
   SETW(32) SETW(64) SETW(128) SETW(192) SETW(256)
 #undef SETW
 #define SETT(BN)      \
   if (e == cudaSuccess) \
-    e = cudaFuncSetAttribute((const void*)conv_tap_tma<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
+    e = cudaFuncSetAttribute((const void*)tc_persistent<BN, TapOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
   SETT(32) SETT(64) SETT(128) SETT(192) SETT(256)
 #undef SETT
   return e;

@@ -27,6 +27,7 @@ struct ConvGemmP {
   int Kdim, rows, cols, splits;
   int K, F, has_bias, pstride;  // weight gradient
   int HoWo, relu;               // forward
+  int bn, ctiles;               // column tile width / count (set at launch)
 };
 // shapes of one conv layer's materialised operands and GEMM tilings
 struct ConvTmaPlan {
@@ -57,6 +58,7 @@ struct ConvTapP {
   float* out;      // NCHW [N][F][Ho][Wo]
   int N, Ho, Wo, F, cp, kh, kw, ph, pw, sgn;
   int bw, bh, bni, tiles_w, tiles_h, relu;
+  int bn, ctiles;  // output-channel tile width / count
 };
 // in: NHWC activation (N x Hin x Win x cp); out: F channels of Ho x Wo;
 // sgn = +1 forward (input at out + tap - pad), -1 data gradient (out - tap + pad)
