@@ -63,6 +63,9 @@ def lib():
         L.orc_relu_bwd.restype = None
         L.orc_softmax_loss_fwd.argtypes = [_dp, _ip, _i, _i, _dp, _dp, _ip]
         L.orc_softmax_loss_bwd.argtypes = [_dp, _ip, _i, _i, _d, _dp]
+        L.orc_softmax_fwd.argtypes = [_dp, _i, _i, _dp]
+        L.orc_softmax_bwd.argtypes = [_dp, _dp, _i, _i, _dp]
+        L.orc_accuracy.argtypes = [_dp, _ip, _i, _i, _i, _ip, _dp]
         L.orc_lr.argtypes = [_i, _d, _d, _d, _l]
         L.orc_lr.restype = _d
         L.orc_sgd_update_f32.argtypes = [_fp, _fp, _fp, _l, _f, _f, _f, _f]
@@ -261,6 +264,32 @@ def softmax_loss_bwd(prob, labels, loss_weight=1.0):
     _check(lib().orc_softmax_loss_bwd(_ptr(p), _ptr(lab, _ip), M, D, loss_weight, _ptr(dx)),
            "softmax_loss_bwd")
     return dx
+
+
+def softmax_fwd(x):
+    x = _d64(x)
+    M, D = x.shape
+    p = np.empty_like(x)
+    _check(lib().orc_softmax_fwd(_ptr(x), M, D, _ptr(p)), "softmax_fwd")
+    return p
+
+
+def softmax_bwd(p, dy):
+    p, dy = _d64(p), _d64(dy)
+    M, D = p.shape
+    dx = np.empty_like(p)
+    _check(lib().orc_softmax_bwd(_ptr(p), _ptr(dy), M, D, _ptr(dx)), "softmax_bwd")
+    return dx
+
+
+def accuracy(x, labels, k=1):
+    x = _d64(x)
+    M, D = x.shape
+    lab = np.ascontiguousarray(labels, dtype=np.int32)
+    correct = np.empty(M, dtype=np.int32)
+    acc = np.zeros(1)
+    _check(lib().orc_accuracy(_ptr(x), _ptr(lab, _ip), M, D, k, _ptr(correct, _ip), _ptr(acc)), "accuracy")
+    return float(acc[0]), correct
 
 
 FIXED, INV = 0, 1

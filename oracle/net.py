@@ -25,6 +25,8 @@ _KEYS = {
     "InnerProduct": {"name", "type", "bottom", "top", "num_output", "bias_term"},
     "ReLU": {"name", "type", "bottom", "top", "negative_slope"},
     "SoftmaxWithLoss": {"name", "type", "bottom", "top"},
+    "Softmax": {"name", "type", "bottom", "top"},
+    "Accuracy": {"name", "type", "bottom", "top", "top_k"},
 }
 
 
@@ -86,6 +88,7 @@ class OracleNet:
         shapes = {inp["name"]: (batch, int(inp["channels"]), int(inp["height"]),
                                 int(inp["width"]))}
         self.layers = []
+        self.accuracy_layers = []  # test-phase side outputs (forward only, off the chain)
         for s in specs:
             L = {"name": s["name"], "type": s["type"], "bottom": s["bottom"], "top": s["top"]}
             if s["bottom"] not in shapes:
@@ -126,6 +129,17 @@ class OracleNet:
             elif t == "SoftmaxWithLoss":
                 L.update(D=C * H * W)
                 shapes[s["top"]] = (1, 1, 1, 1)
+            elif t == "Softmax":
+                L.update(D=C * H * W)
+                shapes[s["top"]] = (N, C, H, W)
+            elif t == "Accuracy":
+                k = int(s.get("top_k", "1"))
+                if not 1 <= k <= C * H * W:
+                    raise ValueError("top_k out of range")
+                L.update(D=C * H * W, k=k, in_shape=(N, C, H, W))
+                shapes[s["top"]] = (1, 1, 1, 1)
+                self.accuracy_layers.append(L)
+                continue
             L["in_shape"] = (N, C, H, W)
             L["out_shape"] = shapes[s["top"]]
             self.layers.append(L)
@@ -172,6 +186,9 @@ class OracleNet:
             elif t == "ReLU":
                 y = capi.relu_fwd(xb, L["slope"])
                 self._saved.append(None)
+            elif t == "Softmax":
+                y = capi.softmax_fwd(xb.reshape(xb.shape[0], -1)).reshape(L["out_shape"])
+                self._saved.append(None)
             elif t == "SoftmaxWithLoss":
                 logits = xb.reshape(xb.shape[0], -1)
                 prob, loss, pred = capi.softmax_loss_fwd(logits, labels)
@@ -184,6 +201,13 @@ class OracleNet:
             y = f32(y)
             blobs[L["top"]] = y
             out["blobs"][L["name"]] = y
+        # test-phase accuracy on the blobs the chain produced
+        out["accuracy"], out["correct"] = {}, {}
+        for L in self.accuracy_layers:
+            xb = blobs[L["bottom"]]
+            acc, correct = capi.accuracy(xb.reshape(xb.shape[0], -1), labels, L["k"])
+            out["accuracy"][L["name"]] = acc
+            out["correct"][L["name"]] = correct
         self._blobs = blobs
         return out
 
@@ -212,6 +236,9 @@ class OracleNet:
             elif t == "ReLU":
                 y = self._blobs[L["top"]]
                 d = f32(capi.relu_bwd(d, y.reshape(d.shape), L["slope"]))
+            elif t == "Softmax":
+                pr = self._blobs[L["top"]]
+                d = f32(capi.softmax_bwd(pr.reshape(pr.shape[0], -1), d.reshape(d.shape[0], -1))).reshape(L["in_shape"])
             elif t == "Pooling":
                 xb, m = saved
                 d = f32(capi.pool_bwd(d, m, L["in_shape"], L["method"], L["k"], L["s"], L["p"]))

@@ -430,6 +430,65 @@ int orc_softmax_loss_bwd(const double* prob, const int32_t* labels, int M,
   return 0;
 }
 
+/* Standalone SoftMax ("maps any set of numbers to probabilities that
+ * will add up to 1").  Per row: m = max x, e = exp(x - m),
+ * s = sum e (ascending), p = e / s. */
+int orc_softmax_fwd(const double* x, int M, int D, double* p) {
+  if (M < 0 || D < 1) return -1;
+  for (int i = 0; i < M; ++i) {
+    const double* xr = x + (long)i * D;
+    double* pr = p + (long)i * D;
+    double m = xr[0];
+    for (int j = 1; j < D; ++j)
+      if (xr[j] > m) m = xr[j];
+    double s = 0.0;
+    for (int j = 0; j < D; ++j) {
+      pr[j] = exp(xr[j] - m);
+      s += pr[j];
+    }
+    for (int j = 0; j < D; ++j) pr[j] /= s;
+  }
+  return 0;
+}
+
+/* SoftMax backward: per row dx[i] = p[i] (dy[i] - sum_j dy[j] p[j]),
+ * the inner sum ascending in j. */
+int orc_softmax_bwd(const double* p, const double* dy, int M, int D, double* dx) {
+  if (M < 0 || D < 1) return -1;
+  for (int i = 0; i < M; ++i) {
+    const double* pr = p + (long)i * D;
+    const double* gr = dy + (long)i * D;
+    double dot = 0.0;
+    for (int j = 0; j < D; ++j) dot += gr[j] * pr[j];
+    for (int j = 0; j < D; ++j) dx[(long)i * D + j] = pr[j] * (gr[j] - dot);
+  }
+  return 0;
+}
+
+/* Accuracy ("calculates the accuracy of the network for a specific set
+ * of inputs"): the fraction of rows whose label ranks among the
+ * top k scores, ranking by descending score with ties broken by ascending
+ * class index (R10): rank(y) = #{j : x_j > x_y or (x_j == x_y and
+ * j < y)}; correct iff rank < k.  correct[i] (may be NULL) gets 0/1. */
+int orc_accuracy(const double* x, const int32_t* labels, int M, int D, int k, int32_t* correct,
+                 double* acc) {
+  if (M < 0 || D < 1 || k < 1 || k > D) return -1;
+  long hits = 0;
+  for (int i = 0; i < M; ++i) {
+    const double* xr = x + (long)i * D;
+    int y = labels[i];
+    if (y < 0 || y >= D) return -2;
+    int rank = 0;
+    for (int j = 0; j < D; ++j)
+      if (xr[j] > xr[y] || (xr[j] == xr[y] && j < y)) ++rank;
+    int ok = rank < k;
+    if (correct) correct[i] = ok;
+    hits += ok;
+  }
+  if (acc) *acc = M > 0 ? (double)hits / M : 0.0;
+  return 0;
+}
+
 /* lr = base_lr * (1 + gamma*iter)^(-power) for inv, base_lr for fixed */
 double orc_lr(int policy, double base_lr, double gamma, double power,
               long iter) {

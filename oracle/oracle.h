@@ -112,6 +112,13 @@ double orc_lr(int policy, double base_lr, double gamma, double power,
 void orc_sgd_update_f32(float* w, const float* diff, float* v, long n,
                         float lr, float mom, float decay, float grad_scale);
 
+/* Standalone SoftMax forward / backward and top-k accuracy
+ * (ties by ascending class index: DESIGN.md R10). */
+int orc_softmax_fwd(const double* x, int M, int D, double* p);
+int orc_softmax_bwd(const double* p, const double* dy, int M, int D, double* dx);
+int orc_accuracy(const double* x, const int32_t* labels, int M, int D, int k, int32_t* correct,
+                 double* acc);
+
 #ifdef __cplusplus
 }
 #endif

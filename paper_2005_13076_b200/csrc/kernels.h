@@ -19,6 +19,10 @@ __global__ void colsum_generic(const __grid_constant__ ColSumP p);
 __global__ void relu_fwd_generic(const __grid_constant__ ReluP p);
 __global__ void relu_bwd_generic(const __grid_constant__ ReluP p);
 __global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p);
+__global__ void softmax_fwd_generic(const __grid_constant__ SoftmaxP p);
+__global__ void softmax_bwd_generic(const __grid_constant__ SoftmaxP p);
+__global__ void accuracy_generic(const __grid_constant__ AccuracyP p);
+__global__ void accuracy_reduce(const __grid_constant__ AccReduceP p);
 __global__ void loss_reduce(const __grid_constant__ LossReduceP p);
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p);
 __global__ void mask_convert(const __grid_constant__ MaskExpandP p);

@@ -345,6 +345,71 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
   }
 }
 
+// ---------------------------------------------- test-phase blocks (NEXT #3)
+// Standalone SoftMax forward: warp per row, stable
+// (max-subtracted) exponentials, lane-strided sums.
+__global__ void __launch_bounds__(256) softmax_fwd_generic(const __grid_constant__ SoftmaxP p) {
+  pdl_enter();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= p.M) return;
+  const float* x = p.x + (size_t)row * p.D;
+  float* y = p.out + (size_t)row * p.D;
+  float m = -INFINITY;
+  for (int j = lane; j < p.D; j += 32) m = fmaxf(m, x[j]);
+  for (int s = 16; s > 0; s >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, s));
+  float sum = 0.f;
+  for (int j = lane; j < p.D; j += 32) sum += expf(x[j] - m);
+  for (int s = 16; s > 0; s >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, s);
+  for (int j = lane; j < p.D; j += 32) y[j] = __fdiv_rn(expf(x[j] - m), sum);
+}
+// SoftMax backward: dx = y (dy - sum_j dy_j y_j)
+__global__ void __launch_bounds__(256) softmax_bwd_generic(const __grid_constant__ SoftmaxP p) {
+  pdl_enter();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= p.M) return;
+  const float* dy = p.x + (size_t)row * p.D;
+  const float* y = p.y + (size_t)row * p.D;
+  float dot = 0.f;
+  for (int j = lane; j < p.D; j += 32) dot = fmaf(dy[j], y[j], dot);
+  for (int s = 16; s > 0; s >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, s);
+  for (int j = lane; j < p.D; j += 32) p.out[(size_t)row * p.D + j] = y[j] * (dy[j] - dot);
+}
+// Accuracy: warp per row; rank(y) = #{j : x_j > x_y or (x_j == x_y
+// and j < y)} (ties by ascending class index, R10), exact compares
+__global__ void __launch_bounds__(256) accuracy_generic(const __grid_constant__ AccuracyP p) {
+  pdl_enter();
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= p.M) return;
+  int y = p.labels[row];
+  if (y < 0 || y >= p.D) {
+    if (lane == 0) atomicOr(p.err, 1u);
+    y = 0;
+  }
+  const float* x = p.x + (size_t)row * p.D;
+  const float sy = x[y];
+  int rank = 0;
+  for (int j0 = 0; j0 < p.D; j0 += 32) {
+    const int j = j0 + lane;
+    const bool better = j < p.D && (x[j] > sy || (x[j] == sy && j < y));
+    rank += __popc(__ballot_sync(0xffffffffu, better));
+  }
+  if (lane == 0) p.flag[row] = rank < p.k ? 1 : 0;
+}
+__global__ void __launch_bounds__(256) accuracy_reduce(const __grid_constant__ AccReduceP p) {
+  pdl_enter();
+  __shared__ int sm[8];
+  int c = 0;
+  for (int i = threadIdx.x; i < p.M; i += 256) c += p.flag[i];
+  for (int s = 16; s > 0; s >>= 1) c += __shfl_xor_sync(0xffffffffu, c, s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 8; ++w) t += sm[w];
+    p.out[0] = p.M > 0 ? __fdiv_rn((float)t, (float)p.M) : 0.f;  // = fp32(hits / M)
+  }
+}
+
 // -------------------------------------------------------------------- GEMM
 // 64x64 tile, BK 16, 256 threads x (4x4) outputs; arbitrary strides so one
 // kernel serves ip fwd (x W^T), dgrad (dy W) and wgrad (dy^T x).

@@ -53,7 +53,7 @@ extern "C" const char* pn_last_error(void) { return g_err.c_str(); }
 // -------------------------------------------------------------- spec model
 namespace {
 
-enum LType { L_CONV, L_POOL, L_IP, L_RELU, L_LOSS };
+enum LType { L_CONV, L_POOL, L_IP, L_RELU, L_LOSS, L_SOFTMAX, L_ACC };
 
 struct Layer {
   LType type;
@@ -64,6 +64,7 @@ struct Layer {
   int K = 0, Nout = 0;                                        // ip
   bool bias = true;
   float slope = 0.f;
+  int top_k = 1;  // accuracy
   // parameters (conv / ip)
   int64_t wcount = 0, bcount = 0, off = -1;  // offset of w in the flat buffers, b follows w
   int64_t part_off = -1;                     // partial-sum region (split wgrads)
@@ -121,6 +122,8 @@ bool allowed_key(const std::string& type, const std::string& k) {
     return k == "num_output" || k == "bias_term";
   } else if (type == "ReLU") {
     return k == "negative_slope";
+  } else if (type == "Accuracy") {
+    return k == "top_k";
   }
   return false;
 }
@@ -160,6 +163,7 @@ struct pn_net {
   int device = 0, batch = 0, flags = 0;
   bool tf32 = false, fused = false;
   std::vector<Layer> layers;
+  std::vector<Layer> acc_layers;  // Accuracy (forward only; read the chain's blobs)
   std::vector<Blob> blobs;
   std::string input_name;
   int classes = 0;
@@ -182,6 +186,7 @@ struct pn_net {
   float* part_b1 = nullptr;   // [splits][500]  ip1 bias-gradient partials
   float* part_db2 = nullptr;  // [rowtiles][50] conv2 bias-gradient partials
   unsigned* err = nullptr;
+  int32_t* acc_flags = nullptr;  // per-row top-k hits of the Accuracy layers
   std::vector<void*> allocs;
 
   std::vector<Stage> phase[3];  // 0 fwd, 1 bwd, 2 update
@@ -275,6 +280,8 @@ static pn_status parse_and_infer(pn_net* net, const char* text) {
     else if (*type == "InnerProduct") L.type = L_IP;
     else if (*type == "ReLU") L.type = L_RELU;
     else if (*type == "SoftmaxWithLoss") L.type = L_LOSS;
+    else if (*type == "Softmax") L.type = L_SOFTMAX;
+    else if (*type == "Accuracy") L.type = L_ACC;
     else return fail(PN_ERR_UNKNOWN_LAYER, "unknown layer type " + *type);
     for (auto& p : kv)
       if (!allowed_key(*type, p.first)) return fail(PN_ERR_PARSE, "unknown key '" + p.first + "' for " + *type);
@@ -333,6 +340,15 @@ static pn_status parse_and_infer(pn_net* net, const char* text) {
       L.slope = s ? (float)atof(s->c_str()) : 0.f;
       if (!(L.slope >= 0.f)) return fail(PN_ERR_PARSE, L.name + ": negative_slope must be >= 0");
       memcpy(L.out, L.in, sizeof(L.out));
+    } else if (L.type == L_SOFTMAX) {
+      if (L.top == L.bottom) return fail(PN_ERR_PARSE, L.name + ": Softmax cannot run in place");
+      memcpy(L.out, L.in, sizeof(L.out));
+    } else if (L.type == L_ACC) {
+      const std::string* k = get(kv, "top_k");
+      const int D = L.in[1] * L.in[2] * L.in[3];
+      if (k && !parse_int(*k, &L.top_k)) return fail(PN_ERR_PARSE, L.name + ": top_k");
+      if (L.top_k < 1 || L.top_k > D) return fail(PN_ERR_SHAPE, L.name + ": top_k must be in [1, classes]");
+      L.out[0] = L.out[1] = L.out[2] = L.out[3] = 1;
     } else {
       net->classes = L.in[1] * L.in[2] * L.in[3];
       L.out[1] = L.out[2] = L.out[3] = 1;
@@ -348,7 +364,8 @@ static pn_status parse_and_infer(pn_net* net, const char* text) {
       if (L.type == L_POOL) b.pool_layer = (int)net->layers.size();
       net->blobs.push_back(b);
     }
-    net->layers.push_back(L);
+    if (L.type == L_ACC) net->acc_layers.push_back(L);  // test-phase side output, off the chain
+    else net->layers.push_back(L);
   }
   if (net->layers.empty() || net->layers.back().type != L_LOSS)
     return fail(PN_ERR_SHAPE, "the net must end with a SoftmaxWithLoss layer");
@@ -474,6 +491,7 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->gm_ws, gm_n));
   }
   TRY(net->alloc(&net->err, 1));
+  if (!net->acc_layers.empty()) TRY(net->alloc(&net->acc_flags, net->batch));
   // activation blobs (the fused plan never stores conv1's output or its
   // gradient, nor conv2's output; conv2's gradient is the dense unpooled G2)
   std::string skip_data1, skip_data2;
@@ -659,6 +677,11 @@ static void build_layerwise(pn_net* net) {
       l.set((const void*)gemm_generic, dim3(cdiv(L.Nout, 64), cdiv(N, 64)), dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().A = a.x; }
                                        : std::function<void(Launch&, const StepArgs&)>());
+    } else if (L.type == L_SOFTMAX) {
+      SoftmaxP p{x, nullptr, top->data, N, L.in[1] * L.in[2] * L.in[3]};
+      l.set((const void*)softmax_fwd_generic, dim3(cdiv(N, 8)), dim3(256), 0, p);
+      add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<SoftmaxP>().x = a.x; }
+                                       : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_RELU) {
       ReluP p{x, nullptr, top->data, top->count(), L.slope};
       l.set((const void*)relu_fwd_generic, dim3(std::max(1u, std::min(cdiv(top->count() / 4, 256), 8u * net->tc_sms))),
@@ -779,6 +802,12 @@ static void build_layerwise(pn_net* net) {
         Launch l3;
         l3.set((const void*)gemm_generic, dim3(cdiv(L.K, 64), cdiv(N, 64)), dim3(256), 0, d);
         add(bwd, L.name + ".dgrad", l3);
+      }
+    } else if (L.type == L_SOFTMAX) {
+      if (bot) {
+        SoftmaxP p{top.diff, top.data, bot->diff, N, L.in[1] * L.in[2] * L.in[3]};
+        l.set((const void*)softmax_bwd_generic, dim3(cdiv(N, 8)), dim3(256), 0, p);
+        add(bwd, L.name + ".bwd", l);
       }
     } else if (L.type == L_RELU) {
       ReluP p{top.diff, top.data, bot->diff, top.count(), L.slope};
@@ -968,10 +997,31 @@ static void add_dp_stages(pn_net* net) {
   bwd.push_back(s3);
 }
 
+// Accuracy layers (test-phase side outputs): after the forward
+// chain, in both plans, on the blobs it materialised
+static pn_status add_accuracy(pn_net* net) {
+  for (auto& L : net->acc_layers) {
+    const Blob& b = net->blobs[net->blob(L.bottom)];
+    if (!b.materialised || !b.data)
+      return fail(PN_ERR_STATE, L.name + ": bottom '" + L.bottom + "' is not materialised by this plan");
+    const int D = L.in[1] * L.in[2] * L.in[3];
+    AccuracyP a{b.data, nullptr, net->acc_flags, net->err, net->batch, D, L.top_k};
+    Launch l;
+    l.set((const void*)accuracy_generic, dim3(cdiv(net->batch, 8)), dim3(256), 0, a);
+    add(net->phase[0], L.name + ".fwd", l, [](Launch& l, const StepArgs& s) { l.params<AccuracyP>().labels = s.labels; });
+    AccReduceP r{net->acc_flags, net->blobs[net->blob(L.top)].data, net->batch};
+    Launch l2;
+    l2.set((const void*)accuracy_reduce, dim3(1), dim3(256), 0, r);
+    add(net->phase[0], L.name + ".reduce", l2);
+  }
+  return PN_OK;
+}
+
 static pn_status build_plan(pn_net* net) {
   for (auto& ph : net->phase) ph.clear();
   if (net->fused) build_fused_lenet(net);
   else build_layerwise(net);
+  TRY(add_accuracy(net));
   build_update(net);
   add_dp_stages(net);
   int n = 0;

@@ -83,6 +83,24 @@ struct SoftmaxLossP {  // P:109-110; S:429-446 (fwd + bwd in one pass)
   int M, D;
   float grad_scale;  // loss_weight / M
 };
+struct SoftmaxP {  // standalone SoftMax: fwd y = softmax(x); bwd dx = y (dy - <dy, y>)
+  const float* x;   // fwd input / bwd top diff
+  const float* y;   // bwd: forward output
+  float* out;       // fwd y / bwd bottom diff
+  int M, D;
+};
+struct AccuracyP {  // top-k accuracy: flag[i] = rank(label_i) < k
+  const float* x;
+  const int32_t* labels;
+  int32_t* flag;
+  unsigned* err;
+  int M, D, k;
+};
+struct AccReduceP {  // acc = (sum of flags) / M, IEEE division
+  const int32_t* flag;
+  float* out;
+  int M;
+};
 struct LossReduceP {
   const float* row_loss;
   float* loss_out;  // caller's (may be null)

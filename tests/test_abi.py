@@ -73,6 +73,37 @@ def test_spec_errors_are_reported(lib, mutate, status):
     assert msg
 
 
+ACC = "\n[layer]\nname = accuracy\ntype = Accuracy\nbottom = ip2\ntop = accuracy\n"
+SMX = ("[layer]\nname = prob1\ntype = Softmax\nbottom = ip1\ntop = prob1\n\n"
+       "[layer]\nname = ip2\ntype = InnerProduct\nbottom = prob1\n")
+
+
+@pytest.mark.parametrize("text,status", [
+    (lambda: lenet() + ACC + "top_k = 0\n", 5),                         # top_k outside [1, classes]
+    (lambda: lenet() + ACC + "top_k = 11\n", 5),
+    (lambda: lenet() + ACC + "k = 1\n", 2),                             # unknown key
+    (lambda: lenet() + ACC.replace("bottom = ip2", "bottom = nosuch"), 4),
+    (lambda: lenet().replace("[layer]\nname = ip2\ntype = InnerProduct\nbottom = ip1\n", SMX.replace("top = prob1", "top = ip1").replace("bottom = prob1", "bottom = ip1")), 2),  # in-place Softmax
+])
+def test_test_phase_layer_errors(lib, text, status):
+    st, msg = _create(lib, text())
+    assert st == status, (st, msg)
+
+
+def test_test_phase_layers_parse(lib):
+    """Accuracy (top_k) and a standalone Softmax are accepted; without a GPU
+    the only failure left is PN_ERR_CUDA."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    text = lenet() + ACC + "top_k = 3\n"
+    text2 = lenet().replace("[layer]\nname = ip2\ntype = InnerProduct\nbottom = ip1\n", SMX)
+    assert "type = Softmax" in text2
+    for t in (text, text2):
+        st, msg = _create(lib, t)
+        assert st == 7, (st, msg)
+
+
 def test_invalid_arguments(lib):
     h = ctypes.c_void_p()
     assert lib.net_create(None, 4, 0, 0, ctypes.byref(h)) == 1

@@ -412,3 +412,67 @@ def test_sgd_grad_scale_exact():
     capi.sgd_update_f32(w1, d, v1, 0.01, 0.9, 5e-4)
     capi.sgd_update_f32(w2, 4 * d, v2, 0.01, 0.9, 5e-4, 0.25)
     np.testing.assert_array_equal(w1, w2)
+
+
+# ------------------------------------------------ test-phase blocks (NEXT #3)
+def test_softmax_fwd_golden_and_invariants():
+    g = golden("softmax_hand.json")
+    assert np.allclose(capi.softmax_fwd(np.zeros((1, 4))), g["uniform4"], atol=1e-15)
+    for c in (-30.0, 0.0, 7.5):                                                        # S:418, any c
+        assert np.allclose(capi.softmax_fwd(np.array([[c, c + math.log(3)]])), g["two_class_probs"], atol=1e-12)
+    x = np.random.default_rng(5).normal(size=(8, 10)) * 4
+    p = capi.softmax_fwd(x)
+    assert np.all(np.abs(p.sum(1) - 1) < 1e-6)
+    assert np.allclose(capi.softmax_fwd(x + 123.0), p, atol=1e-12)                      # shift invariance
+    assert rel_err(p, torch.softmax(t64(x), 1).numpy(), 1.0) < 1e-14
+
+
+def test_softmax_bwd_closed_forms_fd_and_autograd():
+    rng = np.random.default_rng(6)
+    x = rng.normal(size=(2, 5))
+    p = capi.softmax_fwd(x)
+    assert np.all(capi.softmax_bwd(p, np.zeros_like(p)) == 0)
+    assert np.allclose(capi.softmax_bwd(p, np.full_like(p, 3.0)), 0, atol=1e-15)
+    dy = rng.normal(size=p.shape)
+    dx = capi.softmax_bwd(p, dy)
+    h = 1e-6                                                                           # S:428 central FD
+    fd = np.zeros_like(x)
+    for i in range(x.shape[0]):
+        for j in range(x.shape[1]):
+            xp, xm = x.copy(), x.copy()
+            xp[i, j] += h
+            xm[i, j] -= h
+            fd[i, j] = ((capi.softmax_fwd(xp) - capi.softmax_fwd(xm)) * dy).sum() / (2 * h)
+    assert np.max(np.abs(dx - fd)) < 1e-8
+    xt = t64(x).requires_grad_()
+    torch.softmax(xt, 1).backward(t64(dy))
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-14
+
+
+def test_accuracy_golden():
+    g = golden("accuracy_hand.json")
+    for c in g["cases"]:
+        acc, correct = capi.accuracy(np.array(c["x"], np.float64), c["labels"], c["k"])
+        assert acc == c["acc"], c["note"]
+
+
+def test_accuracy_brute_force_ranking():
+    """rank(y) by sorting on (-score, index) -- an independent formulation of
+    S:450's ranking -- on tie-heavy quantised scores."""
+    rng = np.random.default_rng(7)
+    for trial in range(20):
+        M, D = int(rng.integers(1, 20)), int(rng.integers(1, 12))
+        x = rng.integers(-2, 3, size=(M, D)).astype(np.float64)
+        y = rng.integers(0, D, size=M)
+        k = int(rng.integers(1, D + 1))
+        want = [sorted(range(D), key=lambda j: (-x[i, j], j)).index(y[i]) < k for i in range(M)]
+        acc, correct = capi.accuracy(x, y, k)
+        assert list(correct.astype(bool)) == want
+        assert acc == sum(want) / M
+
+
+def test_accuracy_errors():
+    with pytest.raises(Exception):
+        capi.accuracy(np.zeros((2, 3)), [0, 3], 1)     # label out of range (S:452)
+    with pytest.raises(Exception):
+        capi.accuracy(np.zeros((2, 3)), [0, 1], 4)     # k > D
