@@ -204,6 +204,9 @@ struct pn_net {
   ncclComm_t comm = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
+  // single-GPU step: a side stream for independent backward branches
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int64_t bucket_split = 0;  // params [0, split) = ip bucket, [split, n) = conv bucket
   int tc_sms = 148;
   bool tmap_failed = false;
@@ -818,6 +821,17 @@ static void build_layerwise(pn_net* net) {
   }
 }
 
+// fork: the side stream continues after everything enqueued so far on the main one
+static void add_fork(pn_net* net, std::vector<Stage>& v, const char* name, cudaEvent_t ev) {
+  Stage f;
+  f.name = name;
+  f.custom = [net, ev](cudaStream_t st) -> cudaError_t {
+    cudaError_t e = cudaEventRecord(ev, st);
+    return e != cudaSuccess ? e : cudaStreamWaitEvent(net->side, ev, 0);
+  };
+  v.push_back(f);
+}
+
 static void build_fused_lenet(pn_net* net) {
   auto& fwd = net->phase[0];
   auto& bwd = net->phase[1];
@@ -891,11 +905,20 @@ static void build_fused_lenet(pn_net* net) {
     l.set((const void*)lenet_ip2_bwd, dim3(4, i2.splits), dim3(128), 0, p);
     add(bwd, "ip2.bwd+relu1.bwd", l);
   }
+  // single GPU: the ip weight gradients (+ the ip bucket reduction) run on a
+  // side stream, concurrently with ip1's data gradient and the conv
+  // backward (their CTAs co-reside: 97 KB of shared memory each); joined
+  // before the solver.  With data parallelism the chain stays linear (the
+  // bucket allreduce follows the reduction on the main stream).
+  const bool fork = net->tf32 && !net->comm && net->side;
   if (net->tf32) {
     ip_segs.push_back(seg(net->part_b1, G + i1.off + i1.wcount, 500, i2.splits, 500));
+    if (fork) add_fork(net, bwd, "fork[side]", net->ev_fork);
     add(bwd, "ip1.wgrad[tc]", tc::ip1_wgrad_launch(net->da1rT, net->p2T, G + i1.off, N, net->npad));
+    if (fork) bwd.back().side = true;
     // the ip partials come from ip2's backward, two launches back (pdl.cuh)
     add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
+    if (fork) bwd.back().side = true;
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
     conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
@@ -919,6 +942,8 @@ static void build_fused_lenet(pn_net* net) {
     add(bwd, "pool2.bwd", l4);
   }
   if (net->tf32) {
+    // (a side branch for conv2's weight gradient measured slower: both conv2
+    // backward kernels are persistent over every SM and cannot co-reside)
     add(bwd, "conv2.dgrad[tc]", tc::conv2_dgrad_launch(cv2.diff, net->pack.w2t, p1.diff, N, net->tc_sms));
     add(bwd, "conv2.wgrad[tc]", tc::conv2_wgrad_launch(cv2.diff, p1.data, net->partials + c2.part_off, c2.splits, N));
     // conv2.b comes from the ip1 dgrad epilogue's partials
@@ -944,6 +969,15 @@ static void build_fused_lenet(pn_net* net) {
     conv_segs.push_back(seg(net->partials + c1.part_off, G + c1.off, 520, c1.splits, 520));
   }
   add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
+  if (fork) {  // the ip branch joins before the solver (its gradients are ready)
+    Stage j;
+    j.name = "join[side]";
+    j.custom = [net](cudaStream_t st) -> cudaError_t {
+      cudaError_t e = cudaEventRecord(net->ev_join, net->side);
+      return e != cudaSuccess ? e : cudaStreamWaitEvent(st, net->ev_join, 0);
+    };
+    bwd.push_back(j);
+  }
 }
 
 static void build_update(pn_net* net) {
@@ -1048,8 +1082,12 @@ static pn_status run_stage(pn_net* net, Stage& s, const StepArgs& a, cudaStream_
 
 // a phase run eagerly: its first kernel follows whatever the caller enqueued
 static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t st) {
-  bool prev_kernel = false;
+  bool prev_kernel = false;  // (main stream; side-stream kernels run without PDL)
   for (auto& s : net->phase[ph]) {
+    if (s.side) {
+      TRY(run_stage(net, s, a, net->side, false));
+      continue;
+    }
     TRY(run_stage(net, s, a, st, prev_kernel));
     prev_kernel = !s.custom;
   }
@@ -1080,8 +1118,9 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_
   bool prev_kernel = false;  // the captured step is one fixed sequence across phases
   for (int ph = 0; ph < nph; ++ph)
     for (auto& s : net->phase[ph]) {
-      pn_status st = run_stage(net, s, a, net->cap, prev_kernel);
-      prev_kernel = !s.custom;
+      cudaStream_t on = s.side ? net->side : net->cap;
+      pn_status st = run_stage(net, s, a, on, s.side ? false : prev_kernel);
+      if (!s.side) prev_kernel = !s.custom;
       if (st != PN_OK) {
         cudaGraph_t g;
         cudaStreamEndCapture(net->cap, &g);
@@ -1091,7 +1130,7 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_
         cudaStreamCaptureStatus cs;
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
-        CU(cudaStreamGetCaptureInfo(net->cap, &cs, nullptr, nullptr, &deps, &nd));
+        CU(cudaStreamGetCaptureInfo(on, &cs, nullptr, nullptr, &deps, &nd));
         (infer ? s.inode : s.node) = nd ? deps[0] : nullptr;
       }
     }
@@ -1182,6 +1221,11 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     cudaError_t e = net->fused ? tc::setup() : tcc::setup(max_nk);
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }
+  if (net->fused && net->tf32) {  // side stream of the single-GPU backward (build_fused_lenet)
+    CU(cudaStreamCreateWithFlags(&net->side, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&net->ev_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&net->ev_join, cudaEventDisableTiming));
+  }
   TRY(build_plan(net.get()));
   if (net->tf32 && (!tc::tensor_maps_ok() || net->tmap_failed)) return fail(PN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   CU(cudaDeviceSynchronize());
@@ -1200,8 +1244,9 @@ extern "C" void net_destroy(pn_net* net) {
   if (net->cap) cudaStreamDestroy(net->cap);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
-  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done})
+  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join})
     if (e) cudaEventDestroy(e);
+  if (net->side) cudaStreamDestroy(net->side);
   for (void* p : net->allocs) cudaFree(p);
   delete net;
 }

@@ -85,6 +85,7 @@ struct Stage {
   Launch L;
   std::function<void(Launch&, const StepArgs&)> patch;  // refresh step-dependent args
   std::function<cudaError_t(cudaStream_t)> custom;     // non-kernel action
+  bool side = false;  // in a step (graph or eager phase run): launched on the side stream, between fork and join
   cudaGraphNode_t node = nullptr;                      // kernel node in the step graph
   cudaGraphNode_t inode = nullptr;                     // kernel node in the infer graph
 };
