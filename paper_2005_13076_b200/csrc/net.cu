@@ -995,12 +995,20 @@ static void build_update(pn_net* net) {
 static void add_dp_stages(pn_net* net) {
   if (!net->comm) return;  // (a 1-rank communicator still runs the full exchange path)
   auto& bwd = net->phase[1];
-  // position: after the last stage producing an ip-bucket gradient
+  // position: after the last stage producing a gradient of the ip bucket
+  // (the inner-product layers' parameters, which lead the flat buffer):
+  // stages are named "<layer>.<op>"; the fused plan reduces the bucket in
+  // "ip.bucket_reduce"
   size_t pos = 0;
+  bool fused_reduce = false;
   for (size_t i = 0; i < bwd.size(); ++i)
-    if (bwd[i].name.rfind("ip", 0) == 0) pos = i + 1;
-  for (size_t i = 0; i < bwd.size(); ++i)  // fused plans: right after the ip bucket is final
-    if (bwd[i].name.find("ip.bucket_reduce") != std::string::npos) pos = i + 1;
+    if (bwd[i].name == "ip.bucket_reduce") {
+      pos = i + 1;
+      fused_reduce = true;
+    }
+  for (size_t i = 0; i < bwd.size() && !fused_reduce; ++i)
+    for (const Layer& L : net->layers)
+      if (L.type == L_IP && bwd[i].name.compare(0, L.name.size() + 1, L.name + ".") == 0) pos = i + 1;
   auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) {
     return [net, off, cnt, ready](cudaStream_t st) -> cudaError_t {
       cudaError_t e = cudaEventRecord(ready, st);

@@ -329,3 +329,20 @@ def test_dp_single_rank_communicator_matches_local_step(tf32):
         net.close()
     for a, b in zip(*res):
         assert_bitwise("dp(1) vs local", a, b)
+
+
+@pytest.mark.parametrize("spec,N,tf32", [("lenet", 64, True), ("lenet", 64, False), ("cifar10_quick", 8, True)])
+def test_dp_bucket_allreduce_follows_its_gradients(spec, N, tf32):
+    """The ip-bucket allreduce is placed after every stage that writes an
+    inner-product gradient (and the conv bucket's at the end): stage order of
+    the data-parallel plan, whatever the layer names."""
+    net = Net(spec, N, tf32=tf32)
+    net.net_dp_init(1, 0, Net.pn_nccl_unique_id())
+    names = net.stages(1)
+    ar = names.index("allreduce[ip bucket]")
+    ips = [L["name"] for L in OracleNet(spec_text(spec), N).layers if L["type"] == "InnerProduct"]
+    writers = [i for i, n in enumerate(names)
+               if n == "ip.bucket_reduce" or (n.split(".")[0] in ips and "wgrad" in n or n.endswith(".bgrad"))]
+    assert writers and max(writers) < ar, (names, ar)
+    assert names.index("allreduce[conv bucket]") > max(i for i, n in enumerate(names) if "wgrad" in n)
+    net.close()
