@@ -39,6 +39,11 @@ WORKLOADS = {
                       "desc": "Caffe cifar10_quick train step (fwd+bwd+SGD momentum), batch 256 per GPU, "
                               "synthetic CIFAR-shaped input (BASELINE config 4)",
                       "metric": "cifar10_quick train images/sec (device-timed); % of layer roofline"},
+    "alexnet_grouped": {"spec": "alexnet_grouped", "batch": 128, "nb": 2,
+                        "desc": "AlexNet conv trunk as Caffe defines it (conv2/4/5 grouped in two) train step, batch "
+                                "128, synthetic ImageNet-shaped 3x227x227 input (SURVEY NEXT #2)",
+                        "metric": "grouped AlexNet conv trunk train images/sec (device-timed); conv tensor-pipe "
+                                  "utilisation"},
     "alexnet_conv": {"spec": "alexnet_conv", "batch": 128, "nb": 2,
                      "desc": "AlexNet conv trunk (conv1-5 ungrouped + ReLU + max pools + 10-way ip + loss) train "
                              "step, batch 128, synthetic ImageNet-shaped 3x227x227 input (BASELINE config 5 sweep)",
@@ -108,9 +113,9 @@ def parse_layers(text):
         t, k, st, p = L["type"], int(L.get("kernel_size", 1)), int(L.get("stride", 1)), int(L.get("pad", 0))
         d = {"name": L["name"], "type": t, "in": (C, H, W)}
         if t == "Convolution":
-            F = int(L["num_output"])
+            F, G = int(L["num_output"]), int(L.get("group", 1))
             Ho, Wo = (H + 2 * p - k) // st + 1, (W + 2 * p - k) // st + 1
-            d.update(out=(F, Ho, Wo), params=F * C * k * k + F, macs=F * C * k * k * Ho * Wo)
+            d.update(out=(F, Ho, Wo), params=F * (C // G) * k * k + F, macs=F * (C // G) * k * k * Ho * Wo)
         elif t == "Pooling":
             Ho = -(-(H + 2 * p - k) // st) + 1
             Wo = -(-(W + 2 * p - k) // st) + 1
@@ -224,7 +229,7 @@ def dist_setup(args):
 
 
 # oracle sample per workload: (batch per oracle step, steps) -- about 5-30 s of CPU
-ORACLE_SAMPLE = {"lenet": (64, 8), "cifar10_quick": (4, 4), "alexnet_conv": (1, 1)}
+ORACLE_SAMPLE = {"lenet": (64, 8), "cifar10_quick": (4, 4), "alexnet_conv": (1, 1), "alexnet_grouped": (1, 1)}
 
 
 def _oracle_setup(workload, batch):
@@ -234,7 +239,8 @@ def _oracle_setup(workload, batch):
     ref.set_params(synth.xavier_params(ref.learnable(), seed=2, bias="zero"))
     gen = {"lenet": lambda n, s: synth.mnist_like(n, seed=11, first=s * n),
            "cifar10_quick": lambda n, s: synth.cifar_like(n, seed=11, first=s * n),
-           "alexnet_conv": lambda n, s: synth.imagenet_like_fast(n, seed=11 + s)}[workload]
+           "alexnet_conv": lambda n, s: synth.imagenet_like_fast(n, seed=11 + s),
+           "alexnet_grouped": lambda n, s: synth.imagenet_like_fast(n, seed=11 + s)}[workload]
     return ref, gen
 
 
@@ -263,7 +269,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     WL = WORKLOADS[args.workload]
-    batch = {"lenet": 8, "cifar10_quick": 2, "alexnet_conv": 1}[args.workload]
+    batch = {"lenet": 8, "cifar10_quick": 2, "alexnet_conv": 1, "alexnet_grouped": 1}[args.workload]
     ref, gen = _oracle_setup(args.workload, batch)
     hist = {}
 
@@ -314,7 +320,8 @@ def main():
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    dflt = {"lenet": (20000, 200), "cifar10_quick": (2000, 50), "alexnet_conv": (40, 5)}[args.workload]
+    dflt = {"lenet": (20000, 200), "cifar10_quick": (2000, 50), "alexnet_conv": (40, 5),
+            "alexnet_grouped": (40, 5)}[args.workload]
     if args.steps is None:
         args.steps = dflt[0]
     if args.warmup is None:
@@ -350,7 +357,7 @@ def main():
 
     # resident synthetic dataset (> L2), distinct per rank
     gen = {"lenet": synth.mnist_like_fast, "cifar10_quick": synth.cifar_like_fast,
-           "alexnet_conv": synth.imagenet_like_fast}[args.workload]
+           "alexnet_conv": synth.imagenet_like_fast, "alexnet_grouped": synth.imagenet_like_fast}[args.workload]
     xs, ys = gen(BATCH * NB, seed=100 + rank)
     X = torch.from_numpy(xs).cuda().view(NB, BATCH, *xs.shape[1:])
     Y = torch.from_numpy(ys).cuda().view(NB, BATCH)

@@ -19,7 +19,7 @@ _KEYS = {
     "input": {"name", "channels", "height", "width"},
     "Convolution": {"name", "type", "bottom", "top", "num_output", "kernel_size", "kernel_h",
                     "kernel_w", "stride", "stride_h", "stride_w", "pad", "pad_h", "pad_w",
-                    "bias_term"},
+                    "bias_term", "group"},
     "Pooling": {"name", "type", "bottom", "top", "pool", "kernel_size", "kernel_h", "kernel_w",
                 "stride", "stride_h", "stride_w", "pad", "pad_h", "pad_w"},
     "InnerProduct": {"name", "type", "bottom", "top", "num_output", "bias_term"},
@@ -74,6 +74,34 @@ def _hw(s, base, default):
     return int(h), int(w)
 
 
+def grouped_conv_fwd(x, w, b, G, stride, pad):
+    """Grouped convolution (Caffe `group` [outside ref]): the
+    input channels and the filters are split into G equal groups and group g's
+    filters see only group g's channels -- G independent convolutions whose
+    outputs are concatenated along channels.  Returns (y, S)."""
+    if G == 1:
+        return capi.conv_fwd(x, w, b, stride, pad, want_scale=True)
+    Cg, Fg = x.shape[1] // G, w.shape[0] // G
+    ys, Ss = [], []
+    for g in range(G):
+        y, S = capi.conv_fwd(x[:, g * Cg:(g + 1) * Cg], w[g * Fg:(g + 1) * Fg],
+                             None if b is None else b[g * Fg:(g + 1) * Fg], stride, pad, want_scale=True)
+        ys.append(y)
+        Ss.append(S)
+    return np.concatenate(ys, axis=1), np.concatenate(Ss, axis=1)
+
+
+def grouped_conv_bwd(dy, x, w, G, stride, pad, want_dx=True):
+    """Backward of grouped_conv_fwd, group by group: (dw, db, dx, Sdw, Sdb, Sdx)."""
+    if G == 1:
+        return capi.conv_bwd(dy, x, w, stride, pad, want_dx=want_dx, want_scale=True)
+    Cg, Fg = x.shape[1] // G, w.shape[0] // G
+    parts = [capi.conv_bwd(dy[:, g * Fg:(g + 1) * Fg], x[:, g * Cg:(g + 1) * Cg], w[g * Fg:(g + 1) * Fg],
+                           stride, pad, want_dx=want_dx, want_scale=True) for g in range(G)]
+    cat = lambda i, ax: None if parts[0][i] is None else np.concatenate([q[i] for q in parts], axis=ax)
+    return cat(0, 0), cat(1, 0), cat(2, 1), cat(3, 0), cat(4, 0), cat(5, 1)
+
+
 def f32(a):
     return np.asarray(a, dtype=np.float32).astype(np.float64)
 
@@ -103,9 +131,12 @@ class OracleNet:
                 Ho, Wo = capi.conv_out_size(H, kh, sh, ph), capi.conv_out_size(W, kw, sw, pw)
                 if Ho < 1 or Wo < 1:
                     raise ValueError("shape inference failure")
-                L.update(F=F, C=C, k=(kh, kw), s=(sh, sw), p=(ph, pw),
+                G = int(s.get("group", "1"))
+                if G < 1 or C % G or F % G:
+                    raise ValueError("group must divide channels and num_output")
+                L.update(F=F, C=C, k=(kh, kw), s=(sh, sw), p=(ph, pw), G=G,
                          bias=s.get("bias_term", "true") != "false",
-                         wshape=(F, C, kh, kw), blen=F)
+                         wshape=(F, C // G, kh, kw), blen=F)
                 shapes[s["top"]] = (N, F, Ho, Wo)
             elif t == "Pooling":
                 method = {"MAX": capi.MAX, "AVE": capi.AVE}[s.get("pool", "MAX")]
@@ -168,7 +199,7 @@ class OracleNet:
             if t == "Convolution":
                 w = f32(P[L["name"] + ".w"])
                 b = f32(P[L["name"] + ".b"]) if L["bias"] else None
-                y, S = capi.conv_fwd(xb, w, b, L["s"], L["p"], want_scale=True)
+                y, S = grouped_conv_fwd(xb, w, b, L["G"], L["s"], L["p"])
                 self._saved.append((xb,))
                 out["scales"][L["name"]] = S
             elif t == "Pooling":
@@ -246,8 +277,7 @@ class OracleNet:
                 (xb,) = saved
                 w = f32(P[L["name"] + ".w"])
                 first = L["bottom"] == self.input_name
-                dw, db, dx, Sdw, Sdb, Sdx = capi.conv_bwd(d, xb, w, L["s"], L["p"],
-                                                          want_dx=not first, want_scale=True)
+                dw, db, dx, Sdw, Sdb, Sdx = grouped_conv_bwd(d, xb, w, L["G"], L["s"], L["p"], want_dx=not first)
                 grads[L["name"] + ".w"], scales[L["name"] + ".w"] = dw, Sdw
                 grads[L["name"] + ".b"], scales[L["name"] + ".b"] = db, Sdb
                 if not first:

@@ -47,10 +47,11 @@ __global__ void conv_fwd_generic(const __grid_constant__ ConvFwdP p) {
   const int ho = pos / p.Wo, wo = pos - ho * p.Wo;
   const int h0 = ho * p.sh - p.ph, w0 = wo * p.sw - p.pw;
   const int i0 = max(0, -h0), i1 = min(p.kh, p.H - h0), j0 = max(0, -w0), j1 = min(p.kw, p.W - w0);
+  const int G = max(1, p.G), Cg = p.C / G, c0 = (f / (p.F / G)) * Cg;  // filter f sees its group's channels
   float acc = 0.f;
-  for (int c = 0; c < p.C; ++c) {
-    const float* xp = p.x + ((size_t)n * p.C + c) * p.H * p.W + h0 * p.W + w0;
-    const float* wp = p.w + ((size_t)f * p.C + c) * p.kh * p.kw;
+  for (int cl = 0; cl < Cg; ++cl) {
+    const float* xp = p.x + ((size_t)n * p.C + c0 + cl) * p.H * p.W + h0 * p.W + w0;
+    const float* wp = p.w + ((size_t)f * Cg + cl) * p.kh * p.kw;
     for (int i = i0; i < i1; ++i)
       for (int j = j0; j < j1; ++j) acc = fmaf(__ldg(wp + i * p.kw + j), __ldg(xp + i * p.W + j), acc);
   }
@@ -71,10 +72,11 @@ __global__ void conv_bwd_data_generic(const __grid_constant__ ConvBwdDataP p) {
   const int th = h + p.ph, tw = w + p.pw;  // ho*sh + i = th, wo*sw + j = tw
   const int ho0 = th >= p.kh ? (th - p.kh) / p.sh + 1 : 0, ho1 = min(th / p.sh, p.Ho - 1);
   const int wo0 = tw >= p.kw ? (tw - p.kw) / p.sw + 1 : 0, wo1 = min(tw / p.sw, p.Wo - 1);
+  const int G = max(1, p.G), Cg = p.C / G, Fg = p.F / G, g = c / Cg;  // channel c feeds its group's filters
   float acc = 0.f;
-  for (int f = 0; f < p.F; ++f) {
+  for (int f = g * Fg; f < (g + 1) * Fg; ++f) {
     const float* dyp = p.dy + ((size_t)n * p.F + f) * HoWo;
-    const float* wp = p.w + ((size_t)f * p.C + c) * p.kh * p.kw;
+    const float* wp = p.w + ((size_t)f * Cg + (c - g * Cg)) * p.kh * p.kw;
     for (int ho = ho0; ho <= ho1; ++ho) {
       const int i = th - ho * p.sh;
       for (int wo = wo0; wo <= wo1; ++wo)
@@ -90,7 +92,8 @@ __global__ void __launch_bounds__(256) conv_bwd_weight_generic(
     const __grid_constant__ ConvBwdWeightP p) {
   pdl_enter();
   __shared__ float sm[32];
-  const int f = blockIdx.x / p.C, c = blockIdx.x % p.C, s = blockIdx.y;
+  const int G = max(1, p.G), Cg = p.C / G;
+  const int f = blockIdx.x / Cg, cl = blockIdx.x % Cg, c = (f / (p.F / G)) * Cg + cl, s = blockIdx.y;
   const int n0 = (int)((long long)p.N * s / p.splits);
   const int n1 = (int)((long long)p.N * (s + 1) / p.splits);
   const int P = p.Ho * p.Wo;
@@ -125,9 +128,9 @@ __global__ void __launch_bounds__(256) conv_bwd_weight_generic(
       if (t0 + q >= taps) break;
       float r = block_sum<256>(acc[q], sm);
       if (threadIdx.x == 0)
-        p.part_w[(long long)s * p.pstride + ((long long)f * p.C + c) * taps + t0 + q] = r;
+        p.part_w[(long long)s * p.pstride + ((long long)f * Cg + cl) * taps + t0 + q] = r;
     }
-    if (t0 == 0 && c == 0 && p.part_b) {
+    if (t0 == 0 && cl == 0 && p.part_b) {
       float r = block_sum<256>(bacc, sm);
       if (threadIdx.x == 0) p.part_b[(long long)s * p.pstride + f] = r;
     }

@@ -60,6 +60,7 @@ struct Layer {
   std::string name, bottom, top;
   int in[4] = {0, 0, 0, 0}, out[4] = {0, 0, 0, 0};
   int F = 0, kh = 0, kw = 0, sh = 1, sw = 1, ph = 0, pw = 0;  // conv / pool
+  int G = 1;                                                  // conv groups (Caffe `group`)
   int method = 0;                                             // pool
   int K = 0, Nout = 0;                                        // ip
   bool bias = true;
@@ -111,7 +112,7 @@ bool allowed_key(const std::string& type, const std::string& k) {
   static const char* geo[] = {"kernel_size", "kernel_h", "kernel_w", "stride", "stride_h",
                               "stride_w",    "pad",      "pad_h",    "pad_w"};
   if (type == "Convolution") {
-    if (k == "num_output" || k == "bias_term") return true;
+    if (k == "num_output" || k == "bias_term" || k == "group") return true;
     for (auto g : geo)
       if (k == g) return true;
   } else if (type == "Pooling") {
@@ -317,8 +318,11 @@ static pn_status parse_and_infer(pn_net* net, const char* text) {
       L.bias = !(bt && *bt == "false");
       int Ho = conv_out(L.in[2], L.kh, L.sh, L.ph), Wo = conv_out(L.in[3], L.kw, L.sw, L.pw);
       if (Ho < 1 || Wo < 1) return fail(PN_ERR_SHAPE, L.name + ": non-positive output size");
+      const std::string* gs = get(kv, "group");
+      if (gs && (!parse_int(*gs, &L.G) || L.G < 1)) return fail(PN_ERR_PARSE, L.name + ": group");
+      if (L.in[1] % L.G || L.F % L.G) return fail(PN_ERR_SHAPE, L.name + ": group must divide channels and num_output");
       L.out[1] = L.F; L.out[2] = Ho; L.out[3] = Wo;
-      L.wcount = (int64_t)L.F * L.in[1] * L.kh * L.kw;
+      L.wcount = (int64_t)L.F * (L.in[1] / L.G) * L.kh * L.kw;
       L.bcount = L.bias ? L.F : 0;
     } else if (L.type == L_POOL) {
       const std::string* pm = get(kv, "pool");
@@ -384,7 +388,7 @@ static bool is_lenet(const pn_net* n) {
   if (L.size() != 8) return false;
   auto conv = [](const Layer& l, int C, int F) {
     return l.type == L_CONV && l.in[1] == C && l.F == F && l.kh == 5 && l.kw == 5 && l.sh == 1 && l.sw == 1 &&
-           l.ph == 0 && l.pw == 0 && l.bias;
+           l.ph == 0 && l.pw == 0 && l.bias && l.G == 1;
   };
   auto pool = [](const Layer& l) {
     return l.type == L_POOL && l.method == 0 && l.kh == 2 && l.kw == 2 && l.sh == 2 && l.sw == 2 && l.ph == 0 &&
@@ -427,7 +431,7 @@ static pn_status allocate(pn_net* net) {
     Blob w;
     w.name = L.name + ".w";
     w.is_param = true;
-    if (L.type == L_CONV) { w.dims[0] = L.F; w.dims[1] = L.in[1]; w.dims[2] = L.kh; w.dims[3] = L.kw; }
+    if (L.type == L_CONV) { w.dims[0] = L.F; w.dims[1] = L.in[1] / L.G; w.dims[2] = L.kh; w.dims[3] = L.kw; }
     else { w.dims[0] = L.Nout; w.dims[1] = L.K; w.dims[2] = 1; w.dims[3] = 1; }
     w.data = net->params + L.off; w.diff = net->grads + L.off; w.hist = net->hist + L.off;
     net->blobs.push_back(w);
@@ -452,7 +456,7 @@ static pn_status allocate(pn_net* net) {
     if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
     if (L.tc_conv) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
-                                net->tc_sms);
+                                net->tc_sms, L.G);
       L.splits = L.tp.wg_splits;
     }
     L.part_off = poff;
@@ -478,12 +482,12 @@ static pn_status allocate(pn_net* net) {
   for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images, wgrad workspaces
     if (L.tc_conv) {
       const size_t T = (size_t)L.kh * L.kw;
-      if (L.tap_fwd) TRY(net->alloc(&L.wtap_f, T * L.F * L.cp_in));
+      if (L.tap_fwd) TRY(net->alloc(&L.wtap_f, T * L.F * L.cp_in));  // inner = per-group slots
       else if (L.tma_fwd) TRY(net->alloc(&L.wf, (size_t)L.F * L.tp.kp));
       else TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
       if (L.tap_dgrad) TRY(net->alloc(&L.wtap_d, T * L.in[1] * L.cp_out));
-      if (L.tap_fwd) col_n = std::max(col_n, (size_t)net->batch * L.in[2] * L.in[3] * L.cp_in);
-      if (L.tap_dgrad) col_n = std::max(col_n, (size_t)net->batch * L.out[2] * L.out[3] * L.cp_out);
+      if (L.tap_fwd) col_n = std::max(col_n, (size_t)net->batch * L.in[2] * L.in[3] * L.cp_in * L.G);
+      if (L.tap_dgrad) col_n = std::max(col_n, (size_t)net->batch * L.out[2] * L.out[3] * L.cp_out * L.G);
       if (L.tc_dgrad && !L.tap_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
       col_n = std::max(col_n, L.tp.col_floats);
       gm_n = std::max(gm_n, L.tp.g_floats);
@@ -613,7 +617,7 @@ static void build_layerwise(pn_net* net) {
       const float* bias = L.bias ? net->params + L.off + L.wcount : nullptr;
       auto xpatch = [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; };
       if (L.tap_fwd) {
-        PackTapsP pk{net->params + L.off, L.wtap_f, L.F, L.in[1], L.kh, L.kw, L.cp_in, 0};
+        PackTapsP pk{net->params + L.off, L.wtap_f, L.F, L.in[1], L.kh, L.kw, L.cp_in, 0, L.G};
         add(fwd, L.name + ".wpack[tc]", tcc::pack_taps_launch(pk));
       } else if (L.tma_fwd) {
         PackPlainP pk{net->params + L.off, L.wf, L.F, L.tp.K, L.tp.kp};
@@ -623,7 +627,7 @@ static void build_layerwise(pn_net* net) {
         add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
       }
       if (L.tap_dgrad) {
-        PackTapsP pd{net->params + L.off, L.wtap_d, L.F, L.in[1], L.kh, L.kw, L.cp_out, 1};
+        PackTapsP pd{net->params + L.off, L.wtap_d, L.F, L.in[1], L.kh, L.kw, L.cp_out, 1, L.G};
         add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_taps_launch(pd));
       } else if (L.tc_dgrad) {
         ConvPackP pd{net->params + L.off, L.bdg, L.F, L.in[1], L.kh, L.kw, L.dg_rows, L.dg_nk, 1};
@@ -631,13 +635,14 @@ static void build_layerwise(pn_net* net) {
       }
       if (L.tap_fwd) {
         // stride 1: x to NHWC (TF32), then the tap GEMM (no column matrix)
-        NhwcP nh{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.cp_in};
+        NhwcP nh{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.cp_in * L.G, L.G, L.cp_in};
         add(fwd, L.name + ".nhwc[tc]", tcc::nhwc_launch(nh),
             isx ? [](Launch& l, const StepArgs& a) { l.params<NhwcP>().x = a.x; }
                 : std::function<void(Launch&, const StepArgs&)>());
         Launch lt;
-        if (!tcc::tap_launch(net->col_ws, N, L.in[2], L.in[3], L.cp_in, L.wtap_f, L.F, L.cp_in, L.kh, L.kw, L.ph, L.pw,
-                             1, L.out[2], L.out[3], L.F, bias, relu ? 1 : 0, nullptr, top->data, &lt))
+        if (!tcc::tap_launch(net->col_ws, N, L.in[2], L.in[3], L.cp_in * L.G, L.wtap_f, L.F, L.cp_in, L.kh, L.kw,
+                             L.ph, L.pw, 1, L.out[2], L.out[3], L.F, bias, relu ? 1 : 0, nullptr, top->data, &lt, L.G,
+                             L.cp_in))
           net->tmap_failed = true;
         add(fwd, L.name + (relu ? ".fwd+relu[tc]" : ".fwd[tc]"), lt);
       } else if (L.tma_fwd) {
@@ -657,7 +662,7 @@ static void build_layerwise(pn_net* net) {
       }
     } else if (L.type == L_CONV) {
       ConvFwdP p{x, net->params + L.off, L.bias ? net->params + L.off + L.wcount : nullptr, top->data,
-                 N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+                 N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3], L.G};
       l.set((const void*)conv_fwd_generic, dim3(cdiv((long long)N * L.F * L.out[2] * L.out[3], 256)), dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<ConvFwdP>().x = a.x; }
                                        : std::function<void(Launch&, const StepArgs&)>());
@@ -726,7 +731,7 @@ static void build_layerwise(pn_net* net) {
       // TMA-fed GEMM into split partials, then their fixed-order sum
       const int K = L.tp.K;
       Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
-                  L.out[3], K, K + (L.bias ? 1 : 0), L.tp.pitch_m};
+                  L.out[3], K, L.G * (K + (L.bias ? 1 : 0)), L.tp.pitch_m, L.G, K + (L.bias ? 1 : 0)};
       add(bwd, L.name + ".wgrad.im2col[tc]", tcc::im2col_t_launch(ic),
           isx ? [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; }
               : std::function<void(Launch&, const StepArgs&)>());
@@ -741,11 +746,12 @@ static void build_layerwise(pn_net* net) {
       if (bot && L.tap_dgrad) {
         // data gradient: col2im(W^T G) = sum over taps of G shifted
         // by (p - i, p - j) times W_t^T -- G to NHWC, then the tap GEMM
-        NhwcP nh{top.diff, net->col_ws, N, L.F, L.out[2], L.out[3], L.cp_out};
+        NhwcP nh{top.diff, net->col_ws, N, L.F, L.out[2], L.out[3], L.cp_out * L.G, L.G, L.cp_out};
         add(bwd, L.name + ".dgrad.nhwc[tc]", tcc::nhwc_launch(nh));
         Launch lt;
-        if (!tcc::tap_launch(net->col_ws, N, L.out[2], L.out[3], L.cp_out, L.wtap_d, L.in[1], L.cp_out, L.kh, L.kw,
-                             L.ph, L.pw, -1, L.in[2], L.in[3], L.in[1], nullptr, 0, relu_y, bot->diff, &lt))
+        if (!tcc::tap_launch(net->col_ws, N, L.out[2], L.out[3], L.cp_out * L.G, L.wtap_d, L.in[1], L.cp_out, L.kh,
+                             L.kw, L.ph, L.pw, -1, L.in[2], L.in[3], L.in[1], nullptr, 0, relu_y, bot->diff, &lt, L.G,
+                             L.cp_out))
           net->tmap_failed = true;
         add(bwd, L.name + (relu_y ? ".dgrad+relu_bwd[tc]" : ".dgrad[tc]"), lt);
       } else if (bot && L.tc_dgrad) {
@@ -757,7 +763,7 @@ static void build_layerwise(pn_net* net) {
         add(bwd, L.name + (relu_y ? ".dgrad+relu_bwd[tc]" : ".dgrad[tc]"), tcc::conv_fwd_launch(q));
       } else if (bot) {
         ConvBwdDataP q{top.diff, net->params + L.off, bot->diff, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
-                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3], L.G};
         Launch l2;
         l2.set((const void*)conv_bwd_data_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, q);
         add(bwd, L.name + ".dgrad", l2);
@@ -765,14 +771,14 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_CONV) {
       ConvBwdWeightP p{top.diff, x, net->partials + L.part_off, L.bcount ? net->partials + L.part_off + L.wcount : nullptr,
                        N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3],
-                       L.splits, (int)(L.wcount + L.bcount)};
-      l.set((const void*)conv_bwd_weight_generic, dim3(L.F * L.in[1], L.splits), dim3(256), 0, p);
+                       L.splits, (int)(L.wcount + L.bcount), L.G};
+      l.set((const void*)conv_bwd_weight_generic, dim3(L.F * (L.in[1] / L.G), L.splits), dim3(256), 0, p);
       add(bwd, L.name + ".wgrad", l, isx ? [](Launch& l, const StepArgs& a) { l.params<ConvBwdWeightP>().x = a.x; }
                                          : std::function<void(Launch&, const StepArgs&)>());
       add_reduce(net, bwd, L);
       if (bot) {
         ConvBwdDataP q{top.diff, net->params + L.off, bot->diff, N, L.in[1], L.in[2], L.in[3], L.F, L.kh, L.kw,
-                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3]};
+                       L.sh, L.sw, L.ph, L.pw, L.out[2], L.out[3], L.G};
         Launch l2;
         l2.set((const void*)conv_bwd_data_generic, dim3(cdiv(bot->count(), 256)), dim3(256), 0, q);
         add(bwd, L.name + ".dgrad", l2);
@@ -1200,13 +1206,19 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     // the generic fp32 kernel computes it)
     for (auto& L : net->layers) {
       if (L.type != L_CONV) continue;
+      const int Cg = L.in[1] / L.G, Fg = L.F / L.G;
+      // grouped layers run on the tap GEMM only: stride 1,
+      // >= 16 channels per group (else the generic fp32 kernels)
+      if (L.G > 1 && !(L.sh == 1 && L.sw == 1 && Cg >= 16 && Fg >= 16)) continue;
       L.tc_conv = true;
       // forward: tap GEMM for stride-1 layers with >= 16 input channels,
       // materialised im2col for strided layers with K >= 256 (AlexNet conv1),
       // else the gather kernel (C = 3, K = 75: cifar conv1)
-      L.tap_fwd = L.sh == 1 && L.sw == 1 && L.in[1] >= 16;
-      L.cp_in = (L.in[1] + 3) / 4 * 4;
-      L.cp_out = (L.F + 3) / 4 * 4;
+      L.tap_fwd = L.sh == 1 && L.sw == 1 && Cg >= 16;
+      // NHWC channel slots: per group a multiple of 32 when grouped (chunks
+      // never straddle groups), else a multiple of 4
+      L.cp_in = L.G > 1 ? (Cg + 31) / 32 * 32 : (L.in[1] + 3) / 4 * 4;
+      L.cp_out = L.G > 1 ? (Fg + 31) / 32 * 32 : (L.F + 3) / 4 * 4;
       L.tma_fwd = !L.tap_fwd && L.in[1] * L.kh * L.kw >= 256;
       if (!L.tma_fwd && !L.tap_fwd) {
         L.fwd_rows = tcc::fwd_rows_pad(L.F);
@@ -1214,7 +1226,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
         max_nk = std::max(max_nk, L.fwd_nk);
       }
       L.tc_dgrad = L.bottom != net->input_name && L.sh == 1 && L.sw == 1 && L.ph < L.kh && L.pw < L.kw;
-      L.tap_dgrad = L.tc_dgrad && L.F >= 16;
+      L.tap_dgrad = L.tc_dgrad && Fg >= 16;
       if (L.tc_dgrad && !L.tap_dgrad) {
         L.dg_rows = tcc::fwd_rows_pad(L.in[1]);
         L.dg_nk = (L.F * L.kh * L.kw + 31) / 32;

@@ -13,12 +13,14 @@ struct ConvFwdP {  // y = W (*) x + b
   const float* b;
   float* y;
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  int G;  // groups (0 or 1: none); w is [F][C/G][kh][kw]
 };
 struct ConvBwdDataP {  // dx = col2im(W^T dy) in gather form
   const float* dy;
   const float* w;
   float* dx;
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo;
+  int G;
 };
 struct ConvBwdWeightP {  // split-N partials of dW = sum dy col^T and db
   const float* dy;
@@ -27,6 +29,7 @@ struct ConvBwdWeightP {  // split-N partials of dW = sum dy col^T and db
   float* part_b;  // [splits][F]
   int N, C, H, W, F, kh, kw, sh, sw, ph, pw, Ho, Wo, splits;
   int pstride;    // floats between consecutive splits of part_w / part_b
+  int G;          // groups; grid.x = F * C/G
 };
 struct ReduceP {  // out[i] = sum_s part[s*stride + i], i < n (fixed order s = 0..)
   const float* part;
@@ -214,16 +217,19 @@ struct NhwcP {  // out[n][h][w][c] = tf32(x[n][c][h][w]), channels padded to cp
   const float* x;
   float* out;
   int N, C, H, W, cp;
+  int G, cpg;  // grouped: group g's channels at slots [g*cpg, g*cpg + C/G)
 };
 struct PackTapsP {  // per-tap TF32 weight matrices (tc_conv.cu pack_taps)
   const float* w;   // [F][C][kh][kw]
   float* out;       // [kh*kw][rows][ip]
   int F, C, kh, kw, ip, mode;  // mode 0: rows f, inner c (forward); 1: rows c, inner f (data gradient)
+  int G;                       // groups (inner index group-local)
 };
 struct Im2colTP {  // colT[k][m] = tf32(col[m][k]) (k < K), 1 (k == K: bias row)
   const float* x;
   float* col;  // [rows][pitch]
   int N, C, H, W, kh, kw, sh, sw, ph, pw, Ho, Wo, K, Kb, pitch;
+  int G, Kgb;  // grouped (colT only): Kb = G blocks of Kgb = K + bias rows, K per group
 };
 struct GmP {  // gm[f][n*HoWo + pos] = tf32(g[n][f][pos])
   const float* g;

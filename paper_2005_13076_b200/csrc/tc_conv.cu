@@ -266,14 +266,17 @@ constexpr int IM_KROWS = 16;
 __global__ void __launch_bounds__(256) im2col_t(const __grid_constant__ Im2colTP p) {
   __shared__ int2 tab[IM_KROWS];
   const int HoWo = p.Ho * p.Wo, M = p.N * HoWo, KK = p.kh * p.kw;
+  // grouped layers: Kb rows = G blocks of Kgb rows (the group's K patch rows,
+  // then its ones row); row k of block g reads channel g*(C/G) + k/KK
+  const int G = max(1, p.G), Kgb = G > 1 ? p.Kgb : p.Kb, Cg = p.C / G;
   const int kb0 = blockIdx.y * IM_KROWS;
   if (threadIdx.x < IM_KROWS) {
-    const int k = kb0 + threadIdx.x;
+    const int k = kb0 + threadIdx.x, g = k / Kgb, kl = k - g * Kgb;
     int2 e = make_int2(0, 0x7FFF << 16);
-    if (k < p.K) {
-      const int c = k / KK, r = k - c * KK, i = r / p.kw, j = r - i * p.kw;
+    if (k < p.Kb && kl < p.K) {
+      const int c = g * Cg + kl / KK, r = kl - (kl / KK) * KK, i = r / p.kw, j = r - i * p.kw;
       e = make_int2(c * p.H * p.W + i * p.W + j, (i << 16) | j);
-    } else if (k == p.K) {
+    } else if (k < p.Kb && kl == p.K) {
       e = make_int2(0, -1);  // bias row: ones
     }
     tab[threadIdx.x] = e;
@@ -462,17 +465,21 @@ struct GemmOp {
   const ConvGemmP& p;
   int rt, ct;  // row / column tiles
   __device__ GemmOp(const ConvGemmP& q) : p(q), rt((q.rows + 127) / 128), ct(q.ctiles) {}
-  __device__ int num_tiles() const { return rt * ct * p.splits; }
+  // rows / cols are per group; groups contract disjoint row and column ranges
+  __device__ int num_tiles() const { return rt * ct * max(1, p.G) * p.splits; }
   __device__ void prefetch() const { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   struct Info {
-    int r0, q0, s, k0, nk;  // row / column origin, split, first K element, chunks (0: past Kdim, zeros)
+    int r0, q0, g, s, k0, nk;  // group-local row / column origin, group, split, first K element, chunks
   };
   __device__ Info tile(int t) const {
     Info i;
     i.r0 = (t % rt) * 128;
     t /= rt;
     i.q0 = (t % ct) * p.bn;
-    i.s = t / ct;
+    t /= ct;
+    const int G = max(1, p.G);
+    i.g = t % G;
+    i.s = t / G;
     const int nc = (p.Kdim + 31) / 32, c0 = (int)((long long)i.s * nc / p.splits),
               c1 = (int)((long long)(i.s + 1) * nc / p.splits);
     // an empty split range (never planned, but safe) reads one chunk past Kdim: zeros
@@ -482,12 +489,12 @@ struct GemmOp {
   }
   __device__ void issue(const Info& t, int c, uint32_t As, uint32_t Bs, uint32_t bar) const {
     const int k = t.k0 + c * 32;
-    tma2d(As, &p.ta, k, t.r0, bar);
-    tma2d(Bs, &p.tb, k, t.q0, bar);
+    tma2d(As, &p.ta, k, t.g * p.rows + t.r0, bar);
+    tma2d(Bs, &p.tb, k, t.g * p.cols + t.q0, bar);
   }
   template <int BN>
   __device__ void epilogue(const Info& t, uint32_t taddr, int quad, int lane) const {
-    const int r0 = t.r0, q0 = t.q0, s = t.s;
+    const int r0 = t.r0, q0 = t.q0, s = t.s, t_g = t.g;
     const int r = r0 + quad * 32 + lane;
     int n = 0, pos = 0;
     if (EPI == EPI_FWD && r < p.rows) {
@@ -506,10 +513,11 @@ struct GemmOp {
       for (int t = 0; t < 16; ++t) {
         const int q = q0 + cc + t;
         if (q >= p.cols) break;
-        if (EPI == EPI_WGRAD) {  // r = k, q = f
+        if (EPI == EPI_WGRAD) {  // r = group-local k, q = group-local f
           float* pb = p.out + (size_t)s * p.pstride;
-          if (r < p.K) pb[(size_t)q * p.K + r] = v[t];
-          else if (p.has_bias) pb[(size_t)p.F * p.K + q] = v[t];  // r == K: the ones row
+          const int f = t_g * p.cols + q;
+          if (r < p.K) pb[(size_t)f * p.K + r] = v[t];
+          else if (p.has_bias) pb[(size_t)p.F * p.K + f] = v[t];  // r == K: the ones row
         } else {  // EPI_FWD: r = m, q = f
           float o = v[t] + bv[t];
           if (p.relu) o = fmaxf(o, 0.f);
@@ -596,31 +604,36 @@ struct TapOp {
   const ConvTapP& p;
   int ti;  // position tiles
   __device__ TapOp(const ConvTapP& q) : p(q), ti(q.tiles_w * q.tiles_h * ((q.N + q.bni - 1) / q.bni)) {}
-  __device__ int num_tiles() const { return ti * p.ctiles; }
+  // tiles: position tile x output-channel tile (ctiles per group) x group
+  __device__ int num_tiles() const { return ti * p.ctiles * max(1, p.G); }
   __device__ void prefetch() const { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   struct Info {
-    int n0, oh0, ow0, q0, nkc, nk;
+    int n0, oh0, ow0, q0, qend, cbase, nkc, nk;
   };
   __device__ Info tile(int tile) const {
     Info i;
-    i.q0 = (tile / ti) * p.bn;
+    const int G = max(1, p.G), qt = tile / ti, g = qt / p.ctiles;
+    i.q0 = g * p.fg + (qt - g * p.ctiles) * p.bn;  // output channels [q0, qend) of group g
+    i.qend = min(p.F, (g + 1) * p.fg);
+    i.cbase = g * p.cpg;                              // the group's input-channel slots
     int t = tile % ti;
     i.ow0 = (t % p.tiles_w) * p.bw;
     t /= p.tiles_w;
     i.oh0 = (t % p.tiles_h) * p.bh;
     i.n0 = (t / p.tiles_h) * p.bni;
-    i.nkc = (p.cp + 31) / 32;
+    i.nkc = (p.cpg + 31) / 32;
     i.nk = p.kh * p.kw * i.nkc;
+    (void)G;
     return i;
   }
   __device__ void issue(const Info& t, int c, uint32_t As, uint32_t Bs, uint32_t bar) const {
     const int tap = c / t.nkc, kc = c - tap * t.nkc, i = tap / p.kw, j = tap - i * p.kw;
-    tma4d(As, &p.ta, kc * 32, t.ow0 + p.sgn * (j - p.pw), t.oh0 + p.sgn * (i - p.ph), t.n0, bar);
+    tma4d(As, &p.ta, t.cbase + kc * 32, t.ow0 + p.sgn * (j - p.pw), t.oh0 + p.sgn * (i - p.ph), t.n0, bar);
     tma3d(Bs, &p.tb, kc * 32, t.q0, tap, bar);
   }
   template <int BN>
   __device__ void epilogue(const Info& t, uint32_t taddr, int quad, int lane) const {
-    const int n0 = t.n0, oh0 = t.oh0, ow0 = t.ow0, q0 = t.q0;
+    const int n0 = t.n0, oh0 = t.oh0, ow0 = t.ow0, q0 = t.q0, qend = t.qend;
     const int r = quad * 32 + lane;
     const int bw = r % p.bw, rr = r / p.bw, bh = rr % p.bh, bi = rr / p.bh;
     const int n = n0 + bi, oh = oh0 + bh, ow = ow0 + bw;
@@ -635,18 +648,18 @@ struct TapOp {
         float y[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u)
-          y[u] = q0 + cc + u < p.F ? __ldg(p.relu_y + base + (size_t)(q0 + cc + u) * HoWo) : 0.f;
+          y[u] = q0 + cc + u < qend ? __ldg(p.relu_y + base + (size_t)(q0 + cc + u) * HoWo) : 0.f;
 #pragma unroll
         for (int u = 0; u < 16; ++u)
           if (!(y[u] > 0.f)) v[u] = 0.f;
       }
       float bv[16];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) bv[u] = (p.bias && q0 + cc + u < p.F) ? __ldg(p.bias + q0 + cc + u) : 0.f;
+      for (int u = 0; u < 16; ++u) bv[u] = (p.bias && q0 + cc + u < qend) ? __ldg(p.bias + q0 + cc + u) : 0.f;
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         const int q = q0 + cc + u;
-        if (q >= p.F) break;
+        if (q >= qend) break;  // (columns past the group's channels belong to the next group's tile)
         float o = v[u] + bv[u];
         if (p.relu) o = fmaxf(o, 0.f);
         p.out[base + (size_t)q * HoWo] = o;
@@ -656,14 +669,19 @@ struct TapOp {
 };
 
 // NCHW -> NHWC (channels padded to cp with zeros), TF32: 32 x 32 smem transposes
+// Grouped layers (G > 1): group g's channels occupy slots [g*cpg, g*cpg + C/G)
+// of the padded channel dimension (cpg a multiple of 32, the rest zeros), so
+// no 32-channel chunk of one group reaches into the next.
 __global__ void __launch_bounds__(256) to_nhwc(const __grid_constant__ NhwcP p) {
   __shared__ float t[32][33];
   pdl_enter();
   const int n = blockIdx.z, s0 = blockIdx.x * 32, c0 = blockIdx.y * 32, HW = p.H * p.W;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int G = max(1, p.G), Cg = p.C / G, cpg = G > 1 ? p.cpg : p.cp;
   for (int y = ty; y < 32; y += 8) {
-    const int c = c0 + y, sp = s0 + tx;
-    t[y][tx] = (c < p.C && sp < HW) ? tf32f(__ldg(p.x + ((size_t)n * p.C + c) * HW + sp)) : 0.f;
+    const int slot = c0 + y, g = slot / cpg, cl = slot - g * cpg, sp = s0 + tx;
+    const int c = g * Cg + cl;
+    t[y][tx] = (g < G && cl < Cg && sp < HW) ? tf32f(__ldg(p.x + ((size_t)n * p.C + c) * HW + sp)) : 0.f;
   }
   __syncthreads();
   for (int y = ty; y < 32; y += 8) {
@@ -675,9 +693,12 @@ __global__ void __launch_bounds__(256) to_nhwc(const __grid_constant__ NhwcP p) 
 // per-tap weight matrices, TF32: mode 0 (forward) out[t][f][c] = W[f][c][t],
 // mode 1 (data gradient) out[t][c][f] = W[f][c][t]; inner dimension padded to
 // ip with zeros (rows beyond the channel count are never read: TMA bounds)
+// (grouped: W is [F][C/G][kh][kw]; the inner index is the group-local channel
+// (mode 0) or group-local filter (mode 1) of the row's group)
 __global__ void pack_taps(const __grid_constant__ PackTapsP p) {
   pdl_enter();
-  const int T = p.kh * p.kw, rows = p.mode == 0 ? p.F : p.C, inner = p.mode == 0 ? p.C : p.F;
+  const int G = max(1, p.G), Cg = p.C / G, Fg = p.F / G;
+  const int T = p.kh * p.kw, rows = p.mode == 0 ? p.F : p.C, inner = p.mode == 0 ? Cg : Fg;
   const long long total = (long long)T * rows * p.ip;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
     const int k = (int)(e % p.ip);
@@ -685,8 +706,9 @@ __global__ void pack_taps(const __grid_constant__ PackTapsP p) {
     const int r = (int)(tr % rows), t = (int)(tr / rows);
     float v = 0.f;
     if (k < inner) {
-      const int f = p.mode == 0 ? r : k, c = p.mode == 0 ? k : r;
-      v = tf32f(__ldg(p.w + ((size_t)f * p.C + c) * T + t));
+      const int g = p.mode == 0 ? r / Fg : r / Cg;
+      const int f = p.mode == 0 ? r : g * Fg + k, cl = p.mode == 0 ? k : r - g * Cg;
+      v = tf32f(__ldg(p.w + ((size_t)f * Cg + cl) * T + t));
     }
     p.out[e] = v;
   }
@@ -749,21 +771,23 @@ static int pick_tw_bn(int F) {  // F columns per tile: one tile when F <= 256
   return (F + 1) / 2 <= 192 ? 192 : 256;
 }
 
-ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms) {
+ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms, int G) {
   ConvTmaPlan w;
   const long long M = (long long)N * Ho * Wo;
   w.M = (int)M;
-  w.K = C * kh * kw;
+  w.G = std::max(1, G);
+  w.K = C / w.G * kh * kw;
   w.F = F;
   w.bias = bias;
   w.howo = Ho * Wo;
   w.pitch_m = (int)((M + 3) / 4 * 4);
   w.kp = (w.K + 3) / 4 * 4;
   w.fp = (F + 3) / 4 * 4;
-  w.wg_bn = pick_tw_bn(F);
-  w.wg_kpad = (w.K + bias + 127) / 128 * 128;
+  w.wg_bn = pick_tw_bn(F / w.G);
+  w.wg_kpad = (w.G * (w.K + bias) + 127) / 128 * 128;  // colT rows: G blocks of K + bias
   w.wg_fpad = (F + w.wg_bn - 1) / w.wg_bn * w.wg_bn;
-  const long long tiles = (long long)(w.wg_kpad / 128) * (w.wg_fpad / w.wg_bn), nc = (M + 31) / 32;
+  const long long tiles = (long long)((w.K + bias + 127) / 128) * ((F / w.G + w.wg_bn - 1) / w.wg_bn) * w.G,
+                  nc = (M + 31) / 32;
   long long s = std::max(1LL, sms / tiles);  // one wave at one CTA per SM
   w.wg_splits = (int)std::min(s, std::max(1LL, nc / 8));
   w.fw_bn = pick_tw_bn(F);
@@ -839,7 +863,7 @@ template <int EPI>
 static bool gemm_launch(int bn, ConvGemmP& p, Launch* out) {
   p.bn = bn;
   p.ctiles = (p.cols + bn - 1) / bn;
-  const long long tiles = (long long)((p.rows + 127) / 128) * p.ctiles * p.splits;
+  const long long tiles = (long long)((p.rows + 127) / 128) * p.ctiles * std::max(1, p.G) * p.splits;
   const dim3 grid((unsigned)std::min<long long>(tiles, g_sms));
   switch (bn) {
 #define CASE(BN)                                                                                              \
@@ -859,8 +883,9 @@ bool gemm_wgrad_launch(const ConvTmaPlan& w, const float* colT, const float* gm,
   ok = ok && tmap2d(&p.tb, gm, (uint64_t)w.wg_fpad, (uint64_t)w.M, (uint64_t)w.pitch_m, (uint32_t)w.wg_bn);
   p.out = part;
   p.Kdim = w.M;
-  p.rows = w.K + w.bias;
-  p.cols = w.F;
+  p.G = w.G;
+  p.rows = w.K + w.bias;  // per group
+  p.cols = w.F / w.G;
   p.splits = w.wg_splits;
   p.K = w.K;
   p.F = w.F;
@@ -896,14 +921,17 @@ static int pow2_at_least(int v, int lo) {
 
 bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float* wtaps, int rows, int ip, int kh,
                 int kw, int ph, int pw, int sgn, int Ho, int Wo, int F, const float* bias, int relu,
-                const float* relu_y, float* out, Launch* l) {
+                const float* relu_y, float* out, Launch* l, int G, int cpg) {
   ConvTapP p{};
+  p.G = std::max(1, G);
+  p.fg = F / p.G;
+  p.cpg = p.G > 1 ? cpg : cp;
   p.bw = std::min(32, pow2_at_least(Wo, 8));
   p.bh = std::min(128 / p.bw, pow2_at_least(Ho, 1));
   p.bni = 128 / (p.bw * p.bh);
   p.tiles_w = (Wo + p.bw - 1) / p.bw;
   p.tiles_h = (Ho + p.bh - 1) / p.bh;
-  const int bn = pick_tw_bn(F);
+  const int bn = pick_tw_bn(F / std::max(1, G));
   EncodeTiledFn fn = encode_fn();
   bool ok = fn != nullptr;
   {
@@ -939,8 +967,8 @@ bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float*
   p.sgn = sgn;
   p.relu = relu;
   p.bn = bn;
-  p.ctiles = (F + bn - 1) / bn;
-  const long long tiles = (long long)p.tiles_w * p.tiles_h * ((N + p.bni - 1) / p.bni) * p.ctiles;
+  p.ctiles = (p.fg + bn - 1) / bn;
+  const long long tiles = (long long)p.tiles_w * p.tiles_h * ((N + p.bni - 1) / p.bni) * p.ctiles * p.G;
   const dim3 grid((unsigned)std::min<long long>(tiles, g_sms));
   switch (bn) {
 #define CASE(BN) \

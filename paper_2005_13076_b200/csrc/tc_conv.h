@@ -27,18 +27,19 @@ struct ConvGemmP {
   int Kdim, rows, cols, splits;
   int K, F, has_bias, pstride;  // weight gradient
   int HoWo, relu;               // forward
-  int bn, ctiles;               // column tile width / count (set at launch)
+  int bn, ctiles;               // column tile width / count per group (set at launch)
+  int G;                        // groups: rows / cols above are per group
 };
 // shapes of one conv layer's materialised operands and GEMM tilings
 struct ConvTmaPlan {
-  int M, K, F, bias, howo;
+  int M, K, F, bias, howo, G;  // K = (C/G)*kh*kw (per group)
   int pitch_m;  // row pitch of colT / Gm (floats, multiple of 4)
   int kp, fp;   // row pitch of col / Wf (K) and of Gt / Wt (F)
   int wg_bn, wg_kpad, wg_fpad, wg_splits;
   int fw_bn;
   size_t col_floats, g_floats;  // workspace this layer needs
 };
-ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms);
+ConvTmaPlan conv_tma_plan(int N, int C, int kh, int kw, int F, int Ho, int Wo, int bias, int sms, int G = 1);
 Launch im2col_t_launch(const Im2colTP& p);     // colT [k][m] (weight gradient)
 Launch im2col_rows_launch(const Im2colTP& p);  // col  [m][k] (forward)
 Launch gm_launch(const GmP& p);                // Gm   [f][m] (weight gradient)
@@ -58,13 +59,16 @@ struct ConvTapP {
   float* out;      // NCHW [N][F][Ho][Wo]
   int N, Ho, Wo, F, cp, kh, kw, ph, pw, sgn;
   int bw, bh, bni, tiles_w, tiles_h, relu;
-  int bn, ctiles;  // output-channel tile width / count
+  int bn, ctiles;  // output-channel tile width / tiles per group
+  int G, fg, cpg;  // groups, output channels per group, input-channel slots per group
 };
 // in: NHWC activation (N x Hin x Win x cp); out: F channels of Ho x Wo;
 // sgn = +1 forward (input at out + tap - pad), -1 data gradient (out - tap + pad)
+// G > 1: grouped convolution -- cp = G * cpg input-channel slots, F = G * fg
+// output channels, group g's output channels read slots [g*cpg, (g+1)*cpg)
 bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float* wtaps, int rows, int ip, int kh,
                 int kw, int ph, int pw, int sgn, int Ho, int Wo, int F, const float* bias, int relu,
-                const float* relu_y, float* out, Launch* l);
+                const float* relu_y, float* out, Launch* l, int G = 1, int cpg = 0);
 Launch nhwc_launch(const NhwcP& p);
 Launch pack_taps_launch(const PackTapsP& p);
 }  // namespace tcc

@@ -66,6 +66,8 @@ def lenet():
     (lambda s: s.replace("[input]", "[inputs]"), 2),                     # PN_ERR_PARSE
     (lambda s: s.replace("kernel_size = 5", "kernel_size = five", 1), 2),
     (lambda s: s.replace("pool = MAX", "pool = MIN", 1), 2),             # P:215 "minimum": not Caffe
+    (lambda s: s.replace("num_output = 50", "num_output = 50\ngroup = 3"), 5),  # group must divide C and F
+    (lambda s: s.replace("num_output = 50", "num_output = 50\ngroup = 0"), 2),
 ])
 def test_spec_errors_are_reported(lib, mutate, status):
     st, msg = _create(lib, mutate(lenet()))

@@ -476,3 +476,44 @@ def test_accuracy_errors():
         capi.accuracy(np.zeros((2, 3)), [0, 3], 1)     # label out of range
     with pytest.raises(Exception):
         capi.accuracy(np.zeros((2, 3)), [0, 1], 4)     # k > D
+
+
+# ------------------------------------------------------- grouped convolution
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_grouped_conv_vs_torch(G):
+    """Grouped convolution (Caffe `group`): forward and all
+    three gradients against torch conv2d(groups=G) fp64 + autograd."""
+    from oracle.net import grouped_conv_bwd, grouped_conv_fwd
+    rng = np.random.default_rng(10 + G)
+    N, Cg, Fg, H, W, k, s, p = 2, 3, 2, 9, 7, 3, 2, 1
+    x = rng.normal(size=(N, G * Cg, H, W))
+    w = rng.normal(size=(G * Fg, Cg, k, k))
+    b = rng.normal(size=G * Fg)
+    y, S = grouped_conv_fwd(x, w, b, G, (s, s), (p, p))
+    xt, wt, bt = t64(x).requires_grad_(), t64(w).requires_grad_(), t64(b).requires_grad_()
+    yt = Fn.conv2d(xt, wt, bt, stride=s, padding=p, groups=G)
+    assert y.shape == tuple(yt.shape)
+    assert np.max(np.abs(y - yt.detach().numpy())) < 1e-12
+    assert np.all(S >= np.abs(y) - 1e-12)
+    dy = rng.normal(size=y.shape)
+    yt.backward(t64(dy))
+    dw, db, dx, Sdw, Sdb, Sdx = grouped_conv_bwd(dy, x, w, G, (s, s), (p, p))
+    assert np.max(np.abs(dw - wt.grad.numpy())) < 1e-11
+    assert np.max(np.abs(db - bt.grad.numpy())) < 1e-11
+    assert np.max(np.abs(dx - xt.grad.numpy())) < 1e-11
+
+
+def test_grouped_conv_is_blockwise():
+    """A grouped filter bank equals the dense one whose cross-group taps are
+    zero (the definition restated with a different operand)."""
+    from oracle.net import grouped_conv_fwd
+    rng = np.random.default_rng(3)
+    G, Cg, Fg = 2, 2, 3
+    x = rng.normal(size=(1, G * Cg, 6, 6))
+    wg = rng.normal(size=(G * Fg, Cg, 3, 3))
+    dense = np.zeros((G * Fg, G * Cg, 3, 3))
+    for g in range(G):
+        dense[g * Fg:(g + 1) * Fg, g * Cg:(g + 1) * Cg] = wg[g * Fg:(g + 1) * Fg]
+    y1, _ = grouped_conv_fwd(x, wg, None, G, (1, 1), (1, 1))
+    y2 = capi.conv_fwd(x, dense, None, (1, 1), (1, 1))
+    assert np.max(np.abs(y1 - y2)) < 1e-12
