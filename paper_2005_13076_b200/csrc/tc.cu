@@ -60,21 +60,34 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// (no memory clobber: ordered by the cluster barriers around the reduction,
+// free to be issued back to back)
 __device__ __forceinline__ float4 ld_cluster4(uint32_t local_addr, uint32_t rank) {
   uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local_addr), "r"(rank));
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local_addr), "r"(rank));
   float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
-               : "memory");
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
+}
+// the layer epilogue over units of UNIT_COLS columns of the reduced rows
+template <class Op>
+__device__ __forceinline__ void phase_b_units(const Op& op, int tid, uint32_t R_s, int RP, int r0, int r1, float* red) {
+  constexpr int UC = Op::UNIT_COLS, BN = Op::BN;
+  for (int u = tid; u < (r1 - r0) * (BN / UC); u += THREADS) {
+    const int rr = u / (BN / UC), col = (u % (BN / UC)) * UC;
+    float v[UC];
+#pragma unroll
+    for (int q = 0; q < UC; ++q) v[q] = ldsf(R_s + 4 * (rr * RP + col + q));
+    op.store(r0 + rr, col, v, red, r0);
+  }
 }
 }  // namespace ipk
 
 template <class Op>
 __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_constant__ typename Op::Params prm) {
   using namespace ipk;
-  constexpr int BN = Op::BN, PITCH = BN + 4, UC = Op::UNIT_COLS;
-  static_assert(4 * (128 * PITCH + (128 / Op::S + 1) * BN) <= ipk::STAGES * (128 * 128 + BN * 128), "C + R fit the ring");
+  constexpr int BN = Op::BN, PITCH = BN + 4;
+  static_assert(4 * (128 * PITCH + (128 / Op::S + 1) * PITCH) <= ipk::STAGES * (128 * 128 + BN * 128), "C + R fit the ring");
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -87,6 +100,11 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_consta
   Op op(prm);
   const int nk = op.num_k_chunks(), c0 = (int)(rank * nk / S), my = (int)((rank + 1) * nk / S) - c0;
   const uint32_t sbase = smem_u32(smem);
+  // rows [r0, r1) of the tile are this CTA's after the reduction; the layer's
+  // epilogue may stage what it reads for them now (inputs from >= 2 launches back)
+  const int r0 = (int)(rank * 128 / S), r1 = (int)((rank + 1) * 128 / S);
+  __shared__ __align__(16) uint8_t epi_s[Op::EPI_BYTES + 16];
+  op.stage_epilogue(tid, epi_s, r0, r1);
   if (tid == 0) {
     for (int c = 0; c < STAGES; ++c) {
       mbar_init(smem_u32(&full[c]), 1);
@@ -147,16 +165,18 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_consta
       tc_fence_after();
     }
 #pragma unroll 1
-    for (int cc = 0; cc < BN; cc += 16) {
-      float v[16];
+    for (int cc = 0; cc < BN; cc += 32) {  // two TMEM loads in flight per wait
+      float v[32];
       if (my > 0) {
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + cc, v);
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + cc, *reinterpret_cast<float(*)[16]>(v));
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + cc + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+        tmem_ld_wait();
       } else {  // an empty K slice (tiny batch): a zero partial
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 16; j += 4) sts128(sbase + 4 * (row * PITCH + cc + j), f4(v[j], v[j + 1], v[j + 2], v[j + 3]));
+      for (int j = 0; j < 32; j += 4) sts128(sbase + 4 * (row * PITCH + cc + j), f4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     }
   }
   tc_fence_before();
@@ -164,34 +184,40 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_consta
   if (tid == 0) stamp(3);
   // ---- phase A: this CTA's rows [r0, r1) summed over the S partial tiles in a
   // fixed order (s = 0..S-1), float4 units spread over all threads, into R
-  const int r0 = (int)(rank * 128 / S), r1 = (int)((rank + 1) * 128 / S);
-  const uint32_t R_s = sbase + 4 * (128 * PITCH);  // [ceil(128/S)][BN], after C (still in the ring)
-  for (int u = tid; u < (r1 - r0) * (BN / 4); u += THREADS) {
-    const int rr = u / (BN / 4), col = (u % (BN / 4)) * 4;
-    const uint32_t addr = sbase + 4 * ((r0 + rr) * PITCH + col);
-    float4 t[S];
+  // (DSMEM-bandwidth bound: ~20 B/clk per SM)
+  constexpr int RP = PITCH;
+  const uint32_t R_s = sbase + 4 * (128 * PITCH);  // [ceil(128/S)][PITCH], after C (still in the ring)
+  {
+    constexpr int MAXU = ((128 + S - 1) / S * (BN / 4) + THREADS - 1) / THREADS;
+    const int units = (r1 - r0) * (BN / 4);
+    float4 t[MAXU][S];
 #pragma unroll
-    for (uint32_t s2 = 0; s2 < S; ++s2) t[s2] = ld_cluster4(addr, s2);
-    float4 acc = t[0];
+    for (int q = 0; q < MAXU; ++q) {
+      const int u = tid + q * THREADS;
+      if (u < units) {
+        const uint32_t addr = sbase + 4 * ((r0 + u / (BN / 4)) * PITCH + (u % (BN / 4)) * 4);
 #pragma unroll
-    for (uint32_t s2 = 1; s2 < S; ++s2) {
-      acc.x += t[s2].x; acc.y += t[s2].y; acc.z += t[s2].z; acc.w += t[s2].w;
+        for (uint32_t s2 = 0; s2 < S; ++s2) t[q][s2] = ld_cluster4(addr, s2);
+      }
     }
-    sts128(R_s + 4 * (rr * BN + col), acc);
+#pragma unroll
+    for (int q = 0; q < MAXU; ++q) {
+      const int u = tid + q * THREADS;
+      if (u < units) {
+        float4 acc = t[q][0];
+#pragma unroll
+        for (uint32_t s2 = 1; s2 < S; ++s2) {
+          acc.x += t[q][s2].x; acc.y += t[q][s2].y; acc.z += t[q][s2].z; acc.w += t[q][s2].w;
+        }
+        sts128(R_s + 4 * ((u / (BN / 4)) * PITCH + (u % (BN / 4)) * 4), acc);
+      }
+    }
   }
+  if (tid == 0) stamp(6);
   cluster_sync();  // all remote reads of this cluster's C tiles are done; R complete
+  if (tid == 0) stamp(7);
   // ---- phase B: the layer's epilogue on the reduced rows (local shared memory)
-  for (int u = tid; u < (r1 - r0) * (BN / UC); u += THREADS) {
-    const int rr = u / (BN / UC), col = (u % (BN / UC)) * UC;
-    float v[UC];
-#pragma unroll
-    for (int q = 0; q < UC; q += 4) {
-      const int4 t = lds_i4(R_s + 4 * (rr * BN + col + q));
-      v[q] = __int_as_float(t.x); v[q + 1] = __int_as_float(t.y);
-      v[q + 2] = __int_as_float(t.z); v[q + 3] = __int_as_float(t.w);
-    }
-    op.store(r0 + rr, col, v, red, r0);
-  }
+  op.phase_b(tid, R_s, RP, r0, r1, red);
   __syncthreads();
   if (tid == 0) stamp(4);
   op.finish(tid, red, r0, r1, rank);
@@ -211,6 +237,11 @@ struct IpFwd {
   };
   static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 8;
   static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr int EPI_BYTES = 0;
+  __device__ void stage_epilogue(int, uint8_t*, int, int) {}
+  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
+    ipk::phase_b_units(*this, tid, R_s, RP, r0, r1, red);
+  }
   const Params& p;
   int m0, o0;
   __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.z * 128), o0(blockIdx.y * BN) {}
@@ -240,6 +271,11 @@ struct IpWgrad {
   };
   static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 5;
   static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr int EPI_BYTES = 0;
+  __device__ void stage_epilogue(int, uint8_t*, int, int) {}
+  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
+    ipk::phase_b_units(*this, tid, R_s, RP, r0, r1, red);
+  }
   const Params& p;
   int o0, k0;
   __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
@@ -275,36 +311,61 @@ struct IpDgradUnpool {
   static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 16, S = 5;
   static constexpr int RED_FLOATS = 8 * 32;  // [filter in tile][reducer row]
   static constexpr bool A_EARLY = true, B_EARLY = true;
+  // the pool2 origins of the reducer's rows: [row][8 filters x 16], staged at
+  // kernel start (written by conv2's forward, many launches back)
+  static constexpr int EPI_BYTES = (128 / S + 1) * 128;
   const Params& p;
   int m0, k0;
+  const uint8_t* ms = nullptr;
+  __device__ void stage_epilogue(int tid, uint8_t* s, int r0, int r1) {
+    ms = s;
+    const int kb = min(128, 800 - k0);  // mask bytes of this column tile per row
+    for (int u = tid; u < (r1 - r0) * 8; u += ipk::THREADS) {
+      const int rr = u >> 3, q = u & 7, n = m0 + r0 + rr;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (n < p.N && 16 * q < kb) v = __ldg(reinterpret_cast<const uint4*>(p.m2 + (size_t)n * 800 + k0) + q);
+      reinterpret_cast<uint4*>(s)[u] = v;
+    }
+  }
   __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
-  __device__ void store(int row, int col, const float (&v)[16], float* red, int r0) const {
-    const int n = m0 + row, f = (k0 + col) >> 4;
-    float sum = 0.f;
+  // 16 threads per (row n, filter f) unit, thread q = (h = q/2, w0 = 4(q%2)):
+  // the 4 outputs G2[n,f,h,w0..w0+3] (one 16-B store; a warp writes two
+  // whole 256-B planes) from the two pooled values and origins they touch;
+  // thread q = 0 also forms the unit's bias-gradient term
+  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
+    const int nr = r1 - r0;
+    // pass 1: the unit sums (bias-gradient terms), fixed order t = 0..15
+    for (int u = tid; u < nr * 8; u += ipk::THREADS) {
+      const int rr = u >> 3, fl = u & 7;
+      const uint32_t rv = R_s + 4 * (rr * RP + fl * 16);
+      float sum = 0.f;
 #pragma unroll
-    for (int q = 0; q < 16; ++q) sum += v[q];
-    red[(col >> 4) * 32 + (row - r0)] = n < p.N ? sum : 0.f;
-    if (n >= p.N || f >= 50) return;
-    const uint8_t* m = p.m2 + (size_t)n * 800 + f * 16;
-    float* g = p.g2 + ((size_t)n * 50 + f) * 64;
-    uint32_t mw[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t) mw[t] = __ldg(reinterpret_cast<const uint32_t*>(m) + t);
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-      float o8[8];
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        const int q = (h >> 1) * 4 + (w >> 1);
-        const int off = (mw[q >> 2] >> (8 * (q & 3))) & 0xff;
-        o8[w] = (off == ((h & 1) * 2 + (w & 1))) ? tf32f(v[q]) : 0.f;
+      for (int t = 0; t < 16; t += 4) {
+        const int4 x = lds_i4(rv + 4 * t);
+        sum += __int_as_float(x.x); sum += __int_as_float(x.y); sum += __int_as_float(x.z); sum += __int_as_float(x.w);
       }
-      *reinterpret_cast<float4*>(g + h * 8) = f4(o8[0], o8[1], o8[2], o8[3]);
-      *reinterpret_cast<float4*>(g + h * 8 + 4) = f4(o8[4], o8[5], o8[6], o8[7]);
+      red[fl * 32 + rr] = m0 + r0 + rr < p.N ? sum : 0.f;
+    }
+    // pass 2: the unpooled stores (independent iterations: loads of several in flight)
+    const uint32_t ms_s = smem_u32(ms);
+#pragma unroll 4
+    for (int it = tid; it < nr * 128; it += ipk::THREADS) {
+      const int q = it & 15, unit = it >> 4, rr = unit >> 3, fl = unit & 7;
+      const int n = m0 + r0 + rr, f = (k0 >> 4) + fl;
+      const int h = q >> 1, w0 = (q & 1) * 4, pq = (h >> 1) * 4 + (w0 >> 1);
+      const uint32_t rv = R_s + 4 * (rr * RP + fl * 16 + pq);
+      const float va = ldsf_nc(rv), vb = ldsf_nc(rv + 4);
+      uint32_t mab;
+      asm("ld.shared.u16 %0, [%1];" : "=r"(mab) : "r"(ms_s + rr * 128 + fl * 16 + pq));  // pq even: 2-B aligned
+      const int ma = mab & 0xff, mb = mab >> 8, hb = (h & 1) * 2;
+      if (n < p.N && f < 50)
+        *reinterpret_cast<float4*>(p.g2 + ((size_t)n * 50 + f) * 64 + h * 8 + w0) =
+            f4(ma == hb ? tf32f(va) : 0.f, ma == hb + 1 ? tf32f(va) : 0.f, mb == hb ? tf32f(vb) : 0.f,
+               mb == hb + 1 ? tf32f(vb) : 0.f);
     }
   }
   __device__ void finish(int tid, const float* red, int r0, int r1, uint32_t rank) const {
@@ -530,175 +591,191 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
 }
 
 // ------------------------------ conv2 data gradient, persistent pipeline
-// dp1 = col2im(W2^T G2) as the GEMM
-//   C[(c,i,j), (n,p)] = sum_f W2[f,c,i,j] G2[n,f,p]
-// followed by the col2im gather, organised so one CTA per SM streams many
-// image pairs through a pipeline:
-//   warp 0      producer: W2t tile once (TMA), G2 pairs (bulk copy, 2 buffers)
-//   warp 1      MMA: 8 x tcgen05.mma (M=128 rows (c,i,j), N=128 (2 images x
-//               64 positions), K=64 f) per pair into one of 2 TMEM accumulators
-//   warps 2-5   B builders: transposed gather G2[n,f,p] -> B(p, f) (SW128)
-//   warps 6-13  epilogue: TMEM -> smem C (XOR-swizzled), then the col2im
-//               gather dp1[n,c,h,w] = sum_{i,j} C[(c,i,j), (n, h-i, w-j)]
-// so the B build of pair t+1, the MMA of pair t+1 and the col2im of pair t
-// overlap.  grid = (4 row tiles m, G groups); group g takes pairs g, g+G, ...
+// dp1 = col2im(W2^T G2).  Half of col2im is folded into the
+// contraction: with M = (c, j) (100 rows), K = (i, f), N = (n, h, w),
+//   Y[(c,j), (n,h,w)] = sum_{i,f} W2[f,c,i,j] G2[n,f,h-i,w]      (h in 0..11)
+//   dp1[n,c,h,w]       = sum_j Y[(c,j), (n,h,w-j)]               (0 <= w-j < 8)
+// (the same products as col2im of W2^T G2, summed over i inside the tensor
+// core and over j in the epilogue: 5 terms per output instead of 25).
+// The B operand of kernel row i is G2 shifted by i image rows, and in the
+// UMMA K-major no-swizzle layout (core matrix = 8 rows x 16 B) a shift by one
+// image row is a shift of the descriptor start by one 8-row group: each image
+// pair is staged once as Gs[plane f/4][slot][w][4 f], slot = 4 + 12 n + h
+// (slots 0-3, 12-15, 24-27 stay zero: the out-of-image rows), so
+//   B_i = descriptor(Gs + (4 - i) * 128 B), N = 192 = (n, h 0..11, w 0..7),
+// SBO = 128 B, LBO = one plane.  A = W2 as W2d[i][plane][(c,j)][4 f] (packed
+// per step), resident: 5 taps x 7 K steps of tcgen05.mma M=128 N=192 K=8 per
+// pair.  The remaining column sum (5 terms per output) runs in the epilogue.
+//   warp 0      producer: W2d (bulk copies, once)
+//   warp 1      MMA issuer, 2 TMEM accumulators (192 columns each)
+//   warps 2-5   B builders: G2[n,f,h,w] (global/L2, coalesced along (h,w))
+//               -> Gs, 2 buffers
+//   warps 6-9   epilogue: per image row h, TMEM -> smem scratch -> the
+//               j-sum -> dp1 (NCHW)
 namespace dg {
-constexpr int WARPS = 14, THREADS_D = WARPS * 32;
-constexpr int A_BYTES = 2 * 128 * 128;        // 2 K-chunks x 128 rows x 128 B
-constexpr int B_BYTES = 2 * 128 * 128;        // per buffer
-constexpr int G_BYTES = 2 * 3200 * 4;         // per buffer (2 images)
-constexpr int CP = 132;                       // C pitch (floats)
-constexpr int C_BYTES = 128 * CP * 4 + 1024;  // + slack for predicated-off col2im taps
-constexpr int SMEM = A_BYTES + 2 * B_BYTES + 2 * G_BYTES + C_BYTES + 1024;
+constexpr int PLANES = 14;                          // 56 f (50 + zeros), 7 K steps of 8
+constexpr int AROWS = 104;                          // (c,j) rows 0..99 + 4 zero rows
+constexpr int A_PLANE = AROWS * 16;                 // 1664 B
+constexpr int A_TAP = PLANES * A_PLANE;             // 23296 B
+constexpr int A_BYTES = 5 * A_TAP + 384;            // + the rows 104..127 the M=128 MMA over-reads
+constexpr int G_PLANE = 28 * 128;                   // 28 slots x 8 w x 16 B
+constexpr int G_BYTES = PLANES * G_PLANE;           // 50176 B per buffer
+constexpr int SP = 12;                              // scratch pitch (floats): conflict-free 16-B stores
+constexpr int S_BYTES = 128 * SP * 4;               // per scratch buffer
+constexpr int WARPS = 10, THREADS_D = WARPS * 32;
+constexpr int SMEM = A_BYTES + 2 * G_BYTES + 2 * S_BYTES + 1024;
+constexpr int W2D_FLOATS = A_BYTES / 4;
 struct Params {
-  CUtensorMap ta;  // W2t [512][64]
-  const float* g2;
-  float* dp1;
-  int N, groups;
+  const float* w2d;  // packed A (W2D_FLOATS)
+  const float* g2;   // [N][50][64] TF32
+  float* dp1;        // [N][20][144]
+  int N, per_cta;    // pairs [blockIdx.x * per_cta, + per_cta)
 };
 }  // namespace dg
 
 __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const __grid_constant__ dg::Params p) {
-  pdl_enter();
   using namespace dg;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t A_s = smem_u32(smem), B_s = A_s + A_BYTES, G_s = B_s + 2 * B_BYTES, C_s = G_s + 2 * G_BYTES;
-  __shared__ __align__(8) uint64_t afull, gfull[2], gfree[2], bfull[2], bfree[2], accfull[2], accfree[2];
+  const uint32_t A_s = smem_u32(smem), G_s = A_s + A_BYTES, S_s = G_s + 2 * G_BYTES;
+  __shared__ __align__(8) uint64_t afull, gfull[2], gfree[2], accfull[2], accfree[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int m = blockIdx.x, g = blockIdx.y;
-  const int npairs = (p.N + 1) / 2;
-  const int mine = g < npairs ? (npairs - g + p.groups - 1) / p.groups : 0;  // pairs g, g+G, ...
+  const int npairs = (p.N + 1) / 2, pair0 = blockIdx.x * p.per_cta;
+  const int mine = max(0, min(p.per_cta, npairs - pair0));
   if (tid == 0) {
     mbar_init(smem_u32(&afull), 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&gfull[b]), 1);
-      mbar_init(smem_u32(&gfree[b]), 128);
-      mbar_init(smem_u32(&bfull[b]), 128);
-      mbar_init(smem_u32(&bfree[b]), 1);
+      mbar_init(smem_u32(&gfull[b]), 128);
+      mbar_init(smem_u32(&gfree[b]), 1);
       mbar_init(smem_u32(&accfull[b]), 1);
-      mbar_init(smem_u32(&accfree[b]), 256);
+      mbar_init(smem_u32(&accfree[b]), 128);
     }
     fence_barrier_init();
-    prefetch_tmap(&p.ta);
   }
-  if (warp == 0) tmem_alloc(&tmem_base, 256);
+  if (warp == 0) tmem_alloc(&tmem_base, 512);
+  // zero both G buffers once: the builders only ever write the in-image slots
+  // of planes 0..12, so the halo slots and plane 13 stay zero
+  for (int i = tid; i < 2 * G_BYTES / 16; i += THREADS_D) sts128(G_s + 16 * i, zero4());
+  fence_proxy_async();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
-  // C tile [128 rows][CP] fp32 (pitch 132: the 32 lanes' 16-B stores of 32
-  // different rows land on distinct bank groups)
-  auto cs_addr = [&](int row, int col) -> uint32_t { return C_s + 4 * (row * CP + col); };
+  if (tid == 0) stamp(0);
   if (tid == 0) {
-    // ---- producer
-    mbar_expect_tx(smem_u32(&afull), A_BYTES);
-    tma2d(A_s, &p.ta, 0, m * 128, smem_u32(&afull));
-    tma2d(A_s + 128 * 128, &p.ta, 32, m * 128, smem_u32(&afull));
-#pragma unroll 1
-    for (int i = 0; i < mine; ++i) {
-      const int b = i & 1, n0 = 2 * (g + i * p.groups), cnt = min(2, p.N - n0);
-      if (i >= 2) mbar_wait(smem_u32(&gfree[b]), ((i >> 1) - 1) & 1);
-      mbar_expect_tx(smem_u32(&gfull[b]), cnt * 3200 * 4);
-      bulk_g2s(G_s + b * G_BYTES, p.g2 + (size_t)n0 * 3200, cnt * 3200 * 4, smem_u32(&gfull[b]));
+    // ---- producer: the packed weights (written by the step's first launch,
+    // so readable before the PDL wait), then let the successor launch
+    if (mine > 0) {
+      mbar_expect_tx(smem_u32(&afull), A_BYTES);
+      for (int i = 0; i < 5; ++i) {
+        const uint32_t bytes = i < 4 ? A_TAP : A_TAP + 384;
+        bulk_g2s(A_s + i * A_TAP, (const uint8_t*)p.w2d + i * A_TAP, bytes, smem_u32(&afull));
+      }
     }
+    pdl_enter();
   } else if (tid == 32) {
     // ---- MMA issuer
-    constexpr uint32_t idesc = make_idesc(128, 128);
-    mbar_wait(smem_u32(&afull), 0);
+    constexpr uint32_t idesc = make_idesc(128, 192);
+    if (mine > 0) mbar_wait(smem_u32(&afull), 0);
+    stamp(1);
+    const uint64_t ad0 = make_desc_ns(A_s, A_PLANE, 128);
 #pragma unroll 1
-    for (int i = 0; i < mine; ++i) {
-      const int b = i & 1;
-      mbar_wait(smem_u32(&bfull[b]), (i >> 1) & 1);
-      if (i >= 2) mbar_wait(smem_u32(&accfree[b]), ((i >> 1) - 1) & 1);
+    for (int it = 0; it < mine; ++it) {
+      const int b = it & 1;
+      mbar_wait(smem_u32(&gfull[b]), (it >> 1) & 1);
+      if (it < 2) stamp(2 + 2 * it);  // pair built
+      if (it >= 2) mbar_wait(smem_u32(&accfree[b]), ((it >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t Bb = B_s + b * B_BYTES;
+      const uint64_t bd0 = make_desc_ns(G_s + b * G_BYTES, G_PLANE, 128);
 #pragma unroll
-      for (int kc = 0; kc < 2; ++kc)
+      for (int i = 0; i < 5; ++i)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          mma_tf32(tbase + b * 128, make_desc(A_s + kc * 16384 + k * 32), make_desc(Bb + kc * 16384 + k * 32), idesc,
-                   (kc | k) != 0);
-      mma_commit(smem_u32(&bfree[b]));
+        for (int ks = 0; ks < PLANES / 2; ++ks)
+          mma_tf32(tbase + b * 256, ad0 + (uint64_t)((i * A_TAP + ks * 2 * A_PLANE) >> 4),
+                   bd0 + (uint64_t)(((4 - i) * 128 + ks * 2 * G_PLANE) >> 4), idesc, (i | ks) != 0);
+      mma_commit(smem_u32(&gfree[b]));
       mma_commit(smem_u32(&accfull[b]));
+      if (it < 2) stamp(3 + 2 * it);  // MMAs issued
     }
   } else if (warp >= 2 && warp < 6) {
-    // ---- B builders: B(row = img*64 + pos, f) = G2[n0+img, f, pos], f >= 50 -> 0
-    const int t = tid - 64;                       // 0..127 = B row
-    const int img = t >> 6, pos = t & 63;
+    // ---- B builders: thread = (image n, position h*8+w); 13 planes of 4 f
+    pdl_enter();  // G2 comes from the immediate predecessor
+    if (tid == 64) stamp(11);
+    const int t = tid - 64, n = t >> 6, pos = t & 63, h = pos >> 3, w = pos & 7;
+    const uint32_t dst0 = (uint32_t)((4 + 12 * n + h) * 128 + w * 16);
 #pragma unroll 1
-    for (int i = 0; i < mine; ++i) {
-      const int b = i & 1, n0 = 2 * (g + i * p.groups);
-      const bool valid = n0 + img < p.N;
-      mbar_wait(smem_u32(&gfull[b]), (i >> 1) & 1);
-      if (i >= 2) mbar_wait(smem_u32(&bfree[b]), ((i >> 1) - 1) & 1);
-      const uint32_t src = G_s + b * G_BYTES + 4 * (img * 3200 + pos);
-      const uint32_t Bb = B_s + b * B_BYTES;
+    for (int it = 0; it < mine; ++it) {
+      const int b = it & 1, img = 2 * (pair0 + it) + n;
+      float v[52];
+      if (img < p.N) {
+        const float* g = p.g2 + (size_t)img * 3200 + pos;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {  // 16 units of 4 f: f = 4u
-        float v[4];
+        for (int f = 0; f < 50; ++f) v[f] = __ldcg(g + f * 64);
+      } else {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int f = 4 * u + q;
-          const float x = ldsf(src + 4 * 64 * (f < 50 ? f : 0));
-          v[q] = (f < 50 && valid) ? x : 0.f;
-        }
-        sts128(Bb + (u >> 3) * 16384 + sw_off(t, u & 7), f4(v[0], v[1], v[2], v[3]));
+        for (int f = 0; f < 50; ++f) v[f] = 0.f;
       }
+      v[50] = v[51] = 0.f;
+      if (it >= 2) mbar_wait(smem_u32(&gfree[b]), ((it >> 1) - 1) & 1);
+      const uint32_t dst = G_s + b * G_BYTES + dst0;
+#pragma unroll
+      for (int q = 0; q < 13; ++q) sts128(dst + q * G_PLANE, f4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
       fence_proxy_async();
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gfree[b])) : "memory");
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bfull[b])) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gfull[b])) : "memory");
     }
   } else if (warp >= 6) {
-    // ---- epilogue: 8 warps, quadrant = warp % 4, column half = (warp - 6) / 4
-    const int et = tid - 192;  // 0..255
-    const int quad = warp & 3, half = (warp - 6) >> 2, row = quad * 32 + lane;
+    // ---- epilogue: TMEM lane quadrant q = warp % 4 holds rows (c,j) 32q..;
+    // per image row h the 8 columns w of every row go through a scratch tile
+    // (double-buffered: one barrier per row), then thread -> outputs (c, w)
+    const int quad = warp & 3, row = quad * 32 + lane, et = tid - 192;
+    int step = 0;
 #pragma unroll 1
-    for (int i = 0; i < mine; ++i) {
-      const int b = i & 1, n0 = 2 * (g + i * p.groups);
-      mbar_wait(smem_u32(&accfull[b]), (i >> 1) & 1);
+    for (int it = 0; it < mine; ++it) {
+      const int b = it & 1;
+      mbar_wait(smem_u32(&accfull[b]), (it >> 1) & 1);
+      if (et == 0 && it < 2) stamp(6 + 2 * it);  // accumulator ready
       __syncwarp();
       tc_fence_after();
 #pragma unroll 1
-      for (int c0 = half * 64; c0 < half * 64 + 64; c0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 128 + c0, v);
+      for (int n = 0; n < 2; ++n) {
+        const int img = 2 * (pair0 + it) + n;
+#pragma unroll 1
+        for (int hp = 0; hp < 6; ++hp) {
+          float v[16];
+          tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 256 + (n * 12 + 2 * hp) * 8, v);
+          if (n == 1 && hp == 5) {  // every column of this accumulator is in registers
+            tc_fence_before();
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[b])) : "memory");
+          }
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          sts128(cs_addr(row, c0 + 4 * j), f4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
-      }
-      tc_fence_before();
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[b])) : "memory");
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // C complete
-      // col2im: element (row (cl,i,j), col im*64 + (h-i)*8 + (w-j)) sits at
-      // base(cl, im, h, w) + tap offset (i, j) with a compile-time offset per
-      // tap; out-of-window taps are predicated off (their address stays in smem)
-      for (int o = et; o < 2 * 5 * 144; o += 256) {
-        const int im = o / 720, rem = o - im * 720, cl = rem / 144, hw = rem - cl * 144;
-        const int n = n0 + im;
-        if (n >= p.N) continue;
-        const int h = hw / 12, w = hw - h * 12;
-        const uint32_t base = C_s + 4 * (cl * 25 * CP + im * 64 + h * 8 + w);
-        float acc = 0.f;
+          for (int hh = 0; hh < 2; ++hh, ++step) {
+            const uint32_t S = S_s + (step & 1) * S_BYTES;
+            sts128(S + 4 * (row * SP), f4(v[8 * hh], v[8 * hh + 1], v[8 * hh + 2], v[8 * hh + 3]));
+            sts128(S + 4 * (row * SP + 4), f4(v[8 * hh + 4], v[8 * hh + 5], v[8 * hh + 6], v[8 * hh + 7]));
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (img < p.N) {
+              const int h = 2 * hp + hh;
 #pragma unroll
-        for (int ii = 0; ii < 5; ++ii) {
-          const bool hv = (unsigned)(h - ii) < 8u;
+              for (int o = et; o < 240; o += 128) {
+                const int c = o / 12, w = o - 12 * c;
+                float acc = 0.f;
 #pragma unroll
-          for (int jj = 0; jj < 5; ++jj) {
-            const bool v = hv && (unsigned)(w - jj) < 8u;
-            const float x = ldsf(base + 4 * (ii * (5 * CP - 8) + jj * (CP - 1)));
-            acc += v ? x : 0.f;
+                for (int j = 0; j < 5; ++j)
+                  if ((unsigned)(w - j) < 8u) acc += ldsf(S + 4 * ((c * 5 + j) * SP + w - j));
+                p.dp1[(size_t)img * 2880 + c * 144 + h * 12 + w] = acc;
+              }
+            }
           }
         }
-        p.dp1[(size_t)n * 2880 + (5 * m + cl) * 144 + hw] = acc;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");  // C free for the next pair
+      if (et == 0 && it < 2) stamp(7 + 2 * it);  // pair stored
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tbase, 256);
+  if (tid == 0) stamp(10);
+  if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
 // ------------------------------------- conv2 weight gradient, persistent
@@ -883,13 +960,14 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
 // weights in the layouts the GEMMs consume, zero padded:
 //   W1f [500][800]  = W1                      (ip1 fwd B)
 //   W2c [25 taps][5 cc][50 f][4 c] = W2[f, 4cc + c, tap]   (conv2 fwd B)
-//   W2t [4][128][64]: W2t[m][r][f] = W2[f, 5m + r/25, tap r%25]  (conv2 dgrad A)
+//   W2d [5 i][14 planes][104 (c,j)][4 f] = W2[4 plane + q, c, i, j] (conv2 dgrad A, see dg)
 //   W1t [800][512]  = W1^T                    (ip1 dgrad B; tiled transpose)
-constexpr int W2C_N = 25 * 5 * 50 * 4, W2T_N = 4 * 128 * 64;
+constexpr int W2C_N = 25 * 5 * 50 * 4, W2T_N = dg::W2D_FLOATS;
+static_assert(W2T_N == kW2tFloats, "W2d size");
 constexpr int W1_TILES = (800 / 32) * (512 / 32);  // 32 x 32 tiles of W1 (o padded to 512)
 // One launch: blocks [0, W1_TILES) copy + transpose a 32 x 32 tile of W1
 // through shared memory (W1f rows and W1t rows both coalesced); the rest pack
-// W2c and W2t element-wise.
+// W2c and W2d element-wise.
 __global__ void pack_weights(const __grid_constant__ PackP p) {
   pdl_enter();
   if (blockIdx.x < W1_TILES) {
@@ -913,10 +991,11 @@ __global__ void pack_weights(const __grid_constant__ PackP p) {
     return;
   }
   idx -= W2C_N;
-  if (idx < W2T_N) {
-    const int f = idx & 63, r = (idx >> 6) & 127, m = idx >> 13;
+  if (idx < W2T_N) {  // W2d[i][plane][(c,j)][4 f] (conv2 dgrad A), zero rows / filters / tail pad
+    const int q = idx & 3, r = (idx >> 2) % dg::AROWS, pl = (idx / (4 * dg::AROWS)) % dg::PLANES;
+    const int i = idx / (4 * dg::AROWS * dg::PLANES), f = 4 * pl + q, c = r / 5, j = r % 5;
     float v = 0.f;
-    if (f < 50 && r < 125) v = p.w2[f * 500 + (5 * m + r / 25) * 25 + r % 25];
+    if (i < 5 && f < 50 && r < 100) v = p.w2[f * 500 + c * 25 + i * 5 + j];
     p.w2t[idx] = tf32f(v);
   }
 }
@@ -1079,12 +1158,13 @@ Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_
 
 int db2_partials(int N) { return (int)cdiv(N, 128) * IpDgradUnpool::S; }
 
-Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms) {
+Launch conv2_dgrad_launch(const float* g2, const float* w2d, float* dp1, int N, int sms) {
   Launch l;
-  // persistent: one CTA per SM, 4 row tiles x groups of image pairs
-  const int pairs = (N + 1) / 2, groups = std::max(1, std::min(pairs, sms / 4));
-  dg::Params p{tmap2d(w2t, 512, 64, 64, BM), g2, dp1, N, groups};
-  l.set((const void*)conv2_dgrad_persistent, dim3(4, groups), dim3(dg::THREADS_D), dg::SMEM, p);
+  // persistent: pairs split evenly, ceil(pairs / sms) per CTA
+  const int pairs = (N + 1) / 2, per = std::max(1, (pairs + sms - 1) / sms);
+  dg::Params p{w2d, g2, dp1, N, per};
+  l.set((const void*)conv2_dgrad_persistent, dim3(std::max(1, (pairs + per - 1) / per)), dim3(dg::THREADS_D), dg::SMEM,
+        p);
   return l;
 }
 

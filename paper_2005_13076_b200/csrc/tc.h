@@ -7,6 +7,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <cstddef>
+
 #include "runtime.h"
 
 namespace pn {
@@ -18,9 +20,9 @@ struct PackP {
   float* w1f;       // [500][800]
   float* w1t;       // [800][512]
   float* w2c;       // [25 taps][5][50][4] (conv2 fwd B)
-  float* w2t;       // [4][128][64]
+  float* w2t;       // W2d: [5 i][14 planes][104 (c,j)][4 f] + pad (conv2 dgrad A)
 };
-constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2cFloats = 25000, kW2tFloats = 4 * 128 * 64;
+constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2cFloats = 25000, kW2tFloats = 5 * 14 * 104 * 4 + 96;
 
 cudaError_t setup();    // driver entry point + opt-in shared memory sizes
 bool tensor_maps_ok();  // false if any cuTensorMapEncodeTiled call failed

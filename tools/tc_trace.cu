@@ -77,13 +77,32 @@ static int ip_main(int N, char which) {
   cudaStreamCreate(&st);
   printf("ip_splitk<%c> N=%d grid %d x %d x %d: %.2f us/launch (%s)\n", which, N, l.grid.x, l.grid.y, l.grid.z,
          time_launch(l, st, 50), cudaGetErrorString(cudaGetLastError()));
-  const int ks[] = {0, 1, 2, 3, 4, 5};
-  dump("cta  start  waited  accum  sync1  reduced  end", ks, 6, 140);
+  const int ks[] = {0, 1, 2, 3, 6, 7, 4, 5};
+  dump("cta  start  waited  accum  sync1  phaseA  sync2  stored  end", ks, 8, 140);
+  return 0;
+}
+
+static int dgrad_main(int N) {
+  float *g2, *w2d, *dp1;
+  cudaMalloc(&g2, (size_t)N * 3200 * 4);
+  cudaMalloc(&w2d, kW2tFloats * 4);
+  cudaMalloc(&dp1, (size_t)N * 2880 * 4);
+  cudaMemset(g2, 0, (size_t)N * 3200 * 4);
+  cudaMemset(w2d, 0, kW2tFloats * 4);
+  if (setup() != cudaSuccess) { printf("setup failed\n"); return 1; }
+  Launch l = conv2_dgrad_launch(g2, w2d, dp1, N, 148);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  printf("conv2_dgrad_persistent N=%d grid %d: %.2f us/launch (%s)\n", N, l.grid.x, time_launch(l, st, 50),
+         cudaGetErrorString(cudaGetLastError()));
+  const int ks[] = {0, 11, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
+  dump("cta  start pdl  A  built0 mma0 built1 mma1 acc0 st0 acc1 st1 end", ks, 12, l.grid.x);
   return 0;
 }
 
 int main(int argc, char** argv) {
   const int N = argc > 1 ? atoi(argv[1]) : 512;
+  if (argc > 2 && argv[2][0] == 'D') return dgrad_main(N);
   if (argc > 2 && argv[2][0] == 'w') return wgrad_main(N);
   if (argc > 2 && (argv[2][0] == 'f' || argv[2][0] == 'g' || argv[2][0] == 'd')) return ip_main(N, argv[2][0]);
   const int npairs = (N + 1) / 2, npad = (N + 3) & ~3;
