@@ -798,7 +798,7 @@ constexpr int WARPS = 10, THREADS_W = WARPS * 32, NB = 256;  // A builder thread
 constexpr int A_BYTES = 2 * 128 * 128;   // 2 K-chunks (32 positions each) x 128 rows x 128 B
 constexpr int G_BYTES = 2 * 64 * 128;    // 2 K-chunks x 64 f rows x 128 B
 constexpr int P_BYTES = 6 * 144 * 4;     // <= 6 input channels of one image
-constexpr int SLOTS = 3;
+constexpr int SLOTS = 6;  // images in flight
 constexpr int SMEM = 2 * A_BYTES + SLOTS * G_BYTES + SLOTS * P_BYTES + 1024;
 struct Params {
   CUtensorMap tg;  // G2 as {64 p, 50 f, N n}
