@@ -35,76 +35,37 @@
 namespace pn {
 namespace tc {
 
-// ================================================= ip1 GEMMs: cluster split-K
-// C[M,N] = A[M,K] B[N,K]^T (both K-major TF32 by TMA, SW128) with the K range
-// split over a thread-block cluster of S CTAs on one 128 x BN tile:
-//   warp 0      TMA producer: the CTA's K slice through a 3-stage ring --
-//               operands produced two or more launches back are requested
-//               before the PDL wait, the rest after it
+// ================================================= ip1 GEMMs: full-K narrow tiles
+// C[M,N] = A[M,K] B[N,K]^T (both K-major TF32 by TMA, SW128), one CTA per
+// 128 x BN tile (BN = 32) over the whole K: no split-K reduction (no partial
+// tiles, no cluster barriers), the A rows are re-read by the N/BN column
+// tiles from L2 instead.
+//   warp 0      TMA producer: a STAGES-deep ring -- operands produced two or
+//               more launches back are requested before the PDL wait, the
+//               rest after it
 //   warp 1      MMA: 4 x tcgen05.mma (M=128, N=BN, K=8) per chunk into TMEM
-//   warps 2-5   TMEM -> shared-memory partial tile C (pitch BN+4)
-// then (cluster barrier) CTA r sums rows [128r/S, 128(r+1)/S) of the S
-// partial tiles through distributed shared memory (ld.shared::cluster, float4
-// units over all threads, fixed order s = 0..S-1: deterministic, no partials
-// in global memory) into a local buffer R, and (second cluster barrier)
-// applies the layer's epilogue from R (bias+ReLU / store / pool2 backward).
+//   warps 2-5   epilogue: TMEM -> registers (thread = tile row, BN columns)
+//               -> the layer's store (bias+ReLU / dW / pool2 backward)
+// The ring is L2-latency bound: as deep as residency allows -- 10 stages
+// (200 KB) for the forward, 5 (100 KB: two CTAs per SM) for ip1's weight and
+// data gradients, which run side by side on the two streams of the backward.
 namespace ipk {
-// STAGES-deep ring (97 KB of shared memory: two CTAs per SM, so clusters of
-// up to 8 fit all tiles in one wave -- at one CTA per SM a GPC holds too few)
-constexpr int THREADS = 192, STAGES = 3;
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// (no memory clobber: ordered by the cluster barriers around the reduction,
-// free to be issued back to back)
-__device__ __forceinline__ float4 ld_cluster4(uint32_t local_addr, uint32_t rank) {
-  uint32_t a;
-  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local_addr), "r"(rank));
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
-  return v;
-}
-// the layer epilogue over units of UNIT_COLS columns of the reduced rows
-template <class Op>
-__device__ __forceinline__ void phase_b_units(const Op& op, int tid, uint32_t R_s, int RP, int r0, int r1, float* red) {
-  constexpr int UC = Op::UNIT_COLS, BN = Op::BN;
-  for (int u = tid; u < (r1 - r0) * (BN / UC); u += THREADS) {
-    const int rr = u / (BN / UC), col = (u % (BN / UC)) * UC;
-    float v[UC];
-#pragma unroll
-    for (int q = 0; q < UC; ++q) v[q] = ldsf(R_s + 4 * (rr * RP + col + q));
-    op.store(r0 + rr, col, v, red, r0);
-  }
-}
+constexpr int THREADS = 192, BN = 32;
 }  // namespace ipk
 
 template <class Op>
-__global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_constant__ typename Op::Params prm) {
+__global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant__ typename Op::Params prm) {
   using namespace ipk;
-  constexpr int BN = Op::BN, PITCH = BN + 4;
-  static_assert(4 * (128 * PITCH + (128 / Op::S + 1) * PITCH) <= ipk::STAGES * (128 * 128 + BN * 128), "C + R fit the ring");
-  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES;
+  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES, STAGES = Op::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
   __shared__ uint32_t tmem_base;
   __shared__ float red[Op::RED_FLOATS + 1];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr uint32_t S = Op::S;
-  const uint32_t rank = cluster_rank();
   Op op(prm);
-  const int nk = op.num_k_chunks(), c0 = (int)(rank * nk / S), my = (int)((rank + 1) * nk / S) - c0;
+  const int nk = op.num_k_chunks();
   const uint32_t sbase = smem_u32(smem);
-  // rows [r0, r1) of the tile are this CTA's after the reduction; the layer's
-  // epilogue may stage what it reads for them now (inputs from >= 2 launches back)
-  const int r0 = (int)(rank * 128 / S), r1 = (int)((rank + 1) * 128 / S);
-  __shared__ __align__(16) uint8_t epi_s[Op::EPI_BYTES + 16];
-  op.stage_epilogue(tid, epi_s, r0, r1);
   if (tid == 0) {
     for (int c = 0; c < STAGES; ++c) {
       mbar_init(smem_u32(&full[c]), 1);
@@ -114,38 +75,38 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_consta
     fence_barrier_init();
     op.prefetch();
   }
-  if (warp == 0) tmem_alloc(&tmem_base, Op::TMEM_COLS);
+  if (warp == 0) tmem_alloc(&tmem_base, 32);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   if (tid == 0) stamp(0);
   if (tid == 0) {
-    const int pre = min(my, STAGES);
+    const int pre = min(nk, STAGES);
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
       mbar_expect_tx(bar, STAGE);
-      if (Op::A_EARLY) op.issue_a(c0 + c, As, bar);
-      if (Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+      if (Op::A_EARLY) op.issue_a(c, As, bar);
+      if (Op::B_EARLY) op.issue_b(c, As + A_BYTES, bar);
     }
     pdl_enter();
     stamp(1);
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
-      if (!Op::A_EARLY) op.issue_a(c0 + c, As, bar);
-      if (!Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+      if (!Op::A_EARLY) op.issue_a(c, As, bar);
+      if (!Op::B_EARLY) op.issue_b(c, As + A_BYTES, bar);
     }
-    for (int c = STAGES; c < my; ++c) {
+    for (int c = STAGES; c < nk; ++c) {
       const int st = c % STAGES;
       mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
       const uint32_t As = sbase + st * STAGE, bar = smem_u32(&full[st]);
       mbar_expect_tx(bar, STAGE);
-      op.issue_a(c0 + c, As, bar);
-      op.issue_b(c0 + c, As + A_BYTES, bar);
+      op.issue_a(c, As, bar);
+      op.issue_b(c, As + A_BYTES, bar);
     }
   } else if (tid == 32) {
     constexpr uint32_t idesc = make_idesc(128, BN);
-    for (int c = 0; c < my; ++c) {
+    for (int c = 0; c < nk; ++c) {
       const int st = c % STAGES;
       mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
       tc_fence_after();
@@ -154,80 +115,30 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_splitk(const __grid_consta
       for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
       mma_commit(smem_u32(&empty[st]));
     }
-    if (my > 0) mma_commit(smem_u32(&done));
+    mma_commit(smem_u32(&done));
   } else if (warp >= 2) {
-    // TMEM -> C[row][PITCH] over the drained operand ring (all MMAs retired)
     const int quad = warp & 3, row = quad * 32 + lane;
-    if (my > 0) {
-      mbar_wait(smem_u32(&done), 0);
-      if (warp == 2 && lane == 0) stamp(2);
-      __syncwarp();
-      tc_fence_after();
-    }
-#pragma unroll 1
-    for (int cc = 0; cc < BN; cc += 32) {  // two TMEM loads in flight per wait
-      float v[32];
-      if (my > 0) {
-        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + cc, *reinterpret_cast<float(*)[16]>(v));
-        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + cc + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-        tmem_ld_wait();
-      } else {  // an empty K slice (tiny batch): a zero partial
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
-      }
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) sts128(sbase + 4 * (row * PITCH + cc + j), f4(v[j], v[j + 1], v[j + 2], v[j + 3]));
-    }
+    op.stage_epilogue(row);  // epilogue inputs from >= 2 launches back, while the MMAs run
+    mbar_wait(smem_u32(&done), 0);
+    if (warp == 2 && lane == 0) stamp(2);
+    __syncwarp();
+    tc_fence_after();
+    float v[32];
+    tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
+    tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+    tmem_ld_wait();
+    op.store(row, v, red);
   }
   tc_fence_before();
-  cluster_sync();  // every partial tile of the cluster is complete
-  if (tid == 0) stamp(3);
-  // ---- phase A: this CTA's rows [r0, r1) summed over the S partial tiles in a
-  // fixed order (s = 0..S-1), float4 units spread over all threads, into R
-  // (DSMEM-bandwidth bound: ~20 B/clk per SM)
-  constexpr int RP = PITCH;
-  const uint32_t R_s = sbase + 4 * (128 * PITCH);  // [ceil(128/S)][PITCH], after C (still in the ring)
-  {
-    constexpr int MAXU = ((128 + S - 1) / S * (BN / 4) + THREADS - 1) / THREADS;
-    const int units = (r1 - r0) * (BN / 4);
-    float4 t[MAXU][S];
-#pragma unroll
-    for (int q = 0; q < MAXU; ++q) {
-      const int u = tid + q * THREADS;
-      if (u < units) {
-        const uint32_t addr = sbase + 4 * ((r0 + u / (BN / 4)) * PITCH + (u % (BN / 4)) * 4);
-#pragma unroll
-        for (uint32_t s2 = 0; s2 < S; ++s2) t[q][s2] = ld_cluster4(addr, s2);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < MAXU; ++q) {
-      const int u = tid + q * THREADS;
-      if (u < units) {
-        float4 acc = t[q][0];
-#pragma unroll
-        for (uint32_t s2 = 1; s2 < S; ++s2) {
-          acc.x += t[q][s2].x; acc.y += t[q][s2].y; acc.z += t[q][s2].z; acc.w += t[q][s2].w;
-        }
-        sts128(R_s + 4 * ((u / (BN / 4)) * PITCH + (u % (BN / 4)) * 4), acc);
-      }
-    }
-  }
-  if (tid == 0) stamp(6);
-  cluster_sync();  // all remote reads of this cluster's C tiles are done; R complete
-  if (tid == 0) stamp(7);
-  // ---- phase B: the layer's epilogue on the reduced rows (local shared memory)
-  op.phase_b(tid, R_s, RP, r0, r1, red);
   __syncthreads();
-  if (tid == 0) stamp(4);
-  op.finish(tid, red, r0, r1, rank);
-  if (tid == 0) stamp(5);
-  if (warp == 0) tmem_dealloc(tbase, Op::TMEM_COLS);
+  if (tid == 0) stamp(3);
+  op.finish(tid, red);
+  if (warp == 0) tmem_dealloc(tbase, 32);
 }
 
-// y[n,o] = relu(sum_k p2[n,k] W1[o,k] + b[o]): rows n (4 tiles), cols o (BN
-// 128, 4 tiles), K = 800 (25 chunks) over S = 8.  A = p2 (TF32, from conv2 --
-// the immediate predecessor), B = W1f (packed at the start of the step).
+// y[n,o] = relu(sum_k p2[n,k] W1[o,k] + b[o]): rows n, cols o (16 tiles of
+// 32), K = 800 (25 chunks).  A = p2 (TF32, from conv2 -- the immediate
+// predecessor), B = W1f (packed at the start of the step).
 struct IpFwd {
   struct Params {
     CUtensorMap ta, tb;
@@ -235,145 +146,130 @@ struct IpFwd {
     float* y;
     int M, K, Nout;
   };
-  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 8;
+  static constexpr int RED_FLOATS = 0, STAGES = 10;
   static constexpr bool A_EARLY = false, B_EARLY = true;
-  static constexpr int EPI_BYTES = 0;
-  __device__ void stage_epilogue(int, uint8_t*, int, int) {}
-  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
-    ipk::phase_b_units(*this, tid, R_s, RP, r0, r1, red);
-  }
   const Params& p;
   int m0, o0;
-  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.z * 128), o0(blockIdx.y * BN) {}
+  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0(blockIdx.x * ipk::BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, o0, bar); }
-  __device__ void store(int row, int col, const float (&v)[4], float*, int) const {
-    const int m = m0 + row, o = o0 + col;
-    if (m >= p.M || o >= p.Nout) return;  // Nout % 4 == 0
-    float4 r = f4(v[0] + __ldg(p.b + o), v[1] + __ldg(p.b + o + 1), v[2] + __ldg(p.b + o + 2), v[3] + __ldg(p.b + o + 3));
-    r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
-    *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
+  __device__ void stage_epilogue(int) {}
+  __device__ void store(int row, const float (&v)[32], float*) const {
+    const int m = m0 + row;
+    if (m >= p.M) return;
+#pragma unroll
+    for (int c = 0; c < 32; c += 4) {
+      const int o = o0 + c;
+      if (o >= p.Nout) break;  // Nout % 4 == 0
+      float4 r = f4(v[c] + __ldg(p.b + o), v[c + 1] + __ldg(p.b + o + 1), v[c + 2] + __ldg(p.b + o + 2),
+                    v[c + 3] + __ldg(p.b + o + 3));
+      r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
+      *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
+    }
   }
-  __device__ void finish(int, float*, int, int, uint32_t) const {}
+  __device__ void finish(int, const float*) const {}
 };
 
-// dW1[o,k] = sum_n da1[n,o] p2[n,k]: rows o (4 tiles), cols k (BN 128, 7
-// tiles), K = batch over S = 5.  A = da1^T (da1rT [500][npad], TF32, from
-// ip2 backward = the immediate predecessor), B = p2^T (p2T, from conv2).
-// The bias gradient comes from the ip2 backward kernel (exact fp32).
+// dW1[o,k] = sum_n da1[n,o] p2[n,k]: rows o (4 tiles), cols k (25 tiles of
+// 32), K = batch.  A = da1^T (da1rT [500][npad], TF32, from ip2 backward =
+// the immediate predecessor), B = p2^T (p2T, from conv2).  The bias gradient
+// comes from the ip2 backward kernel (exact fp32).
 struct IpWgrad {
   struct Params {
     CUtensorMap ta, tb;
     float* dw;
     int M, K, Nout;  // M = batch (contraction), K = 800 (cols), Nout = 500 (rows)
   };
-  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 4, RED_FLOATS = 0, S = 5;
+  static constexpr int RED_FLOATS = 0, STAGES = 5;
   static constexpr bool A_EARLY = false, B_EARLY = true;
-  static constexpr int EPI_BYTES = 0;
-  __device__ void stage_epilogue(int, uint8_t*, int, int) {}
-  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
-    ipk::phase_b_units(*this, tid, R_s, RP, r0, r1, red);
-  }
   const Params& p;
   int o0, k0;
-  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
+  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * 128), k0(blockIdx.x * ipk::BN) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, o0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
-  __device__ void store(int row, int col, const float (&v)[4], float*, int) const {
-    const int o = o0 + row, k = k0 + col;
-    if (o >= p.Nout || k >= p.K) return;
-    *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k) = f4(v[0], v[1], v[2], v[3]);
+  __device__ void stage_epilogue(int) {}
+  __device__ void store(int row, const float (&v)[32], float*) const {
+    const int o = o0 + row;
+    if (o >= p.Nout) return;
+#pragma unroll
+    for (int c = 0; c < 32; c += 4)
+      if (k0 + c < p.K) *reinterpret_cast<float4*>(p.dw + (size_t)o * p.K + k0 + c) = f4(v[c], v[c + 1], v[c + 2], v[c + 3]);
   }
-  __device__ void finish(int, float*, int, int, uint32_t) const {}
+  __device__ void finish(int, const float*) const {}
 };
 
-// dp2[n,k] = sum_o da1[n,o] W1[o,k]: rows n (4 tiles), cols k (BN 128 = 8
-// filters x 16 pooled outputs, 7 tiles), K = o (500 -> 512) over S = 5.  A =
-// da1 (TF32 copy [N][500]), B = W1t [800][512] -- neither comes from the
-// immediate predecessor (the ip bucket reduce), so all loads precede the PDL
-// wait.  Epilogue (unit = one filter's 16 columns of a row): scatter each
-// dp2 value to its pool2 origin in the dense conv2 gradient G2[n,f,8,8]
-// (zeros elsewhere), stored TF32-rounded (its only consumers are
-// conv2's contractions), and the exact dp2 sum per filter over the reducer's
-// rows for the conv2 bias gradient: part_db2[(row tile * S + rank)][f].
+// dp2[n,k] = sum_o da1[n,o] W1[o,k]: rows n, cols k (25 tiles of 32 = 2
+// filters x 16 pooled outputs), K = o (500 -> 512).  A = da1 (TF32 copy
+// [N][500]), B = W1t [800][512] -- neither comes from the immediate
+// predecessor (the ip bucket reduce), so all loads precede the PDL wait.
+// Epilogue (thread = image n): each of its two filters' 16 dp2 values goes
+// to its pool2 origin in the dense conv2 gradient G2[n,f,8,8] (zeros
+// elsewhere), stored TF32-rounded (its only consumers are conv2's
+// contractions); the exact dp2 sum per filter over the tile's rows (fixed
+// order) is the conv2 bias-gradient partial part_db2[row tile][f].
 struct IpDgradUnpool {
   struct Params {
     CUtensorMap ta, tb;
     const uint8_t* m2;  // [N,800]
     float* g2;          // [N,50,8,8]
-    float* part_db2;    // [row tiles * S][50]
+    float* part_db2;    // [row tiles][50]
     int N;
   };
-  static constexpr int BN = 128, TMEM_COLS = 128, UNIT_COLS = 16, S = 5;
-  static constexpr int RED_FLOATS = 8 * 32;  // [filter in tile][reducer row]
+  static constexpr int RED_FLOATS = 2 * 128, STAGES = 5;  // red: [filter in tile][row]
   static constexpr bool A_EARLY = true, B_EARLY = true;
-  // the pool2 origins of the reducer's rows: [row][8 filters x 16], staged at
-  // kernel start (written by conv2's forward, many launches back)
-  static constexpr int EPI_BYTES = (128 / S + 1) * 128;
   const Params& p;
   int m0, k0;
-  const uint8_t* ms = nullptr;
-  __device__ void stage_epilogue(int tid, uint8_t* s, int r0, int r1) {
-    ms = s;
-    const int kb = min(128, 800 - k0);  // mask bytes of this column tile per row
-    for (int u = tid; u < (r1 - r0) * 8; u += ipk::THREADS) {
-      const int rr = u >> 3, q = u & 7, n = m0 + r0 + rr;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (n < p.N && 16 * q < kb) v = __ldg(reinterpret_cast<const uint4*>(p.m2 + (size_t)n * 800 + k0) + q);
-      reinterpret_cast<uint4*>(s)[u] = v;
-    }
-  }
-  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.z * 128), k0(blockIdx.y * BN) {}
+  uint4 mk[2];
+  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0(blockIdx.x * ipk::BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
-  // 16 threads per (row n, filter f) unit, thread q = (h = q/2, w0 = 4(q%2)):
-  // the 4 outputs G2[n,f,h,w0..w0+3] (one 16-B store; a warp writes two
-  // whole 256-B planes) from the two pooled values and origins they touch;
-  // thread q = 0 also forms the unit's bias-gradient term
-  __device__ void phase_b(int tid, uint32_t R_s, int RP, int r0, int r1, float* red) const {
-    const int nr = r1 - r0;
-    // pass 1: the unit sums (bias-gradient terms), fixed order t = 0..15
-    for (int u = tid; u < nr * 8; u += ipk::THREADS) {
-      const int rr = u >> 3, fl = u & 7;
-      const uint32_t rv = R_s + 4 * (rr * RP + fl * 16);
-      float sum = 0.f;
-#pragma unroll
-      for (int t = 0; t < 16; t += 4) {
-        const int4 x = lds_i4(rv + 4 * t);
-        sum += __int_as_float(x.x); sum += __int_as_float(x.y); sum += __int_as_float(x.z); sum += __int_as_float(x.w);
-      }
-      red[fl * 32 + rr] = m0 + r0 + rr < p.N ? sum : 0.f;
-    }
-    // pass 2: the unpooled stores (independent iterations: loads of several in flight)
-    const uint32_t ms_s = smem_u32(ms);
-#pragma unroll 4
-    for (int it = tid; it < nr * 128; it += ipk::THREADS) {
-      const int q = it & 15, unit = it >> 4, rr = unit >> 3, fl = unit & 7;
-      const int n = m0 + r0 + rr, f = (k0 >> 4) + fl;
-      const int h = q >> 1, w0 = (q & 1) * 4, pq = (h >> 1) * 4 + (w0 >> 1);
-      const uint32_t rv = R_s + 4 * (rr * RP + fl * 16 + pq);
-      const float va = ldsf_nc(rv), vb = ldsf_nc(rv + 4);
-      uint32_t mab;
-      asm("ld.shared.u16 %0, [%1];" : "=r"(mab) : "r"(ms_s + rr * 128 + fl * 16 + pq));  // pq even: 2-B aligned
-      const int ma = mab & 0xff, mb = mab >> 8, hb = (h & 1) * 2;
-      if (n < p.N && f < 50)
-        *reinterpret_cast<float4*>(p.g2 + ((size_t)n * 50 + f) * 64 + h * 8 + w0) =
-            f4(ma == hb ? tf32f(va) : 0.f, ma == hb + 1 ? tf32f(va) : 0.f, mb == hb ? tf32f(vb) : 0.f,
-               mb == hb + 1 ? tf32f(vb) : 0.f);
+  __device__ void stage_epilogue(int row) {  // the row's pool2 origins (conv2's forward, many launches back)
+    const int n = m0 + row;
+    mk[0] = mk[1] = make_uint4(0, 0, 0, 0);
+    if (n < p.N) {
+      const uint4* m = reinterpret_cast<const uint4*>(p.m2 + (size_t)n * 800 + k0);
+      mk[0] = __ldg(m);
+      if (k0 + 16 < 800) mk[1] = __ldg(m + 1);
     }
   }
-  __device__ void finish(int tid, const float* red, int r0, int r1, uint32_t rank) const {
+  __device__ void store(int row, const float (&v)[32], float* red) const {
+    const int n = m0 + row;
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int f = (k0 >> 4) + h2;
+      float sum = 0.f;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) sum += v[16 * h2 + q];
+      red[h2 * 128 + row] = n < p.N ? sum : 0.f;
+      if (n >= p.N || f >= 50) continue;
+      const uint32_t mw[4] = {mk[h2].x, mk[h2].y, mk[h2].z, mk[h2].w};
+      float* g = p.g2 + ((size_t)n * 50 + f) * 64;
+#pragma unroll
+      for (int h = 0; h < 8; ++h) {
+        float o8[8];
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int q = (h >> 1) * 4 + (w >> 1);
+          const int off = (mw[q >> 2] >> (8 * (q & 3))) & 0xff;
+          o8[w] = (off == ((h & 1) * 2 + (w & 1))) ? tf32f(v[16 * h2 + q]) : 0.f;
+        }
+        *reinterpret_cast<float4*>(g + h * 8) = f4(o8[0], o8[1], o8[2], o8[3]);
+        *reinterpret_cast<float4*>(g + h * 8 + 4) = f4(o8[4], o8[5], o8[6], o8[7]);
+      }
+    }
+  }
+  __device__ void finish(int tid, const float* red) const {
     const int f = (k0 >> 4) + tid;
-    if (tid < 8 && f < 50) {  // fixed-order sum over the reducer's rows
+    if (tid < 2 && f < 50) {  // fixed-order sum over the tile's rows
       float s = 0.f;
-      for (int r = 0; r < r1 - r0; ++r) s += red[tid * 32 + r];
-      p.part_db2[((size_t)blockIdx.z * S + rank) * 50 + f] = s;
+      for (int r = 0; r < 128; ++r) s += red[tid * 128 + r];
+      p.part_db2[(size_t)blockIdx.y * 50 + f] = s;
     }
   }
 };
@@ -1072,12 +968,12 @@ static CUtensorMap tmap_g2(const float* base, uint64_t N) {
 }
 
 template <class Op>
-static constexpr size_t ip_smem() {  // whole K slice + 1 KB alignment slack
-  return (size_t)ipk::STAGES * (128 * 128 + Op::BN * 128) + 1024;
+static constexpr size_t ip_smem() {  // the ring + 1 KB alignment slack
+  return (size_t)Op::STAGES * (128 * 128 + ipk::BN * 128) + 1024;
 }
 template <class Op>
 static cudaError_t opt_in() {
-  return cudaFuncSetAttribute((const void*)ip_splitk<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ip_smem<Op>());
+  return cudaFuncSetAttribute((const void*)ip_tile<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ip_smem<Op>());
 }
 
 cudaError_t setup() {
@@ -1129,34 +1025,29 @@ Launch pack_p1c_launch(const float* p1, float* p1c, int N) {
 
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N) {
   Launch l;
-  IpFwd::Params p{tmap2d(p2, N, 800, 800, 128), tmap2d(w1f, 500, 800, 800, IpFwd::BN), b, y, N, 800, 500};
-  l.set((const void*)ip_splitk<IpFwd>, dim3(IpFwd::S, cdiv(500, IpFwd::BN), cdiv(N, 128)), dim3(ipk::THREADS),
-        ip_smem<IpFwd>(), p);
-  l.cluster = dim3(IpFwd::S, 1, 1);
+  IpFwd::Params p{tmap2d(p2, N, 800, 800, 128), tmap2d(w1f, 500, 800, 800, ipk::BN), b, y, N, 800, 500};
+  l.set((const void*)ip_tile<IpFwd>, dim3(cdiv(500, ipk::BN), cdiv(N, 128)), dim3(ipk::THREADS), ip_smem<IpFwd>(), p);
   return l;
 }
 
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad) {
   Launch l;
-  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
-  l.set((const void*)ip_splitk<IpWgrad>, dim3(IpWgrad::S, cdiv(800, IpWgrad::BN), cdiv(500, 128)),
-        dim3(ipk::THREADS), ip_smem<IpWgrad>(), p);
-  l.cluster = dim3(IpWgrad::S, 1, 1);
+  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, ipk::BN), dw, N, 800, 500};
+  l.set((const void*)ip_tile<IpWgrad>, dim3(cdiv(800, ipk::BN), cdiv(500, 128)), dim3(ipk::THREADS), ip_smem<IpWgrad>(),
+        p);
   return l;
 }
 
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N) {
   Launch l;
-  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, 128), tmap2d(w1t, 800, 512, 512, IpDgradUnpool::BN), m2, g2,
-                          part_db2, N};
-  l.set((const void*)ip_splitk<IpDgradUnpool>, dim3(IpDgradUnpool::S, cdiv(800, IpDgradUnpool::BN), cdiv(N, 128)),
-        dim3(ipk::THREADS), ip_smem<IpDgradUnpool>(), p);
-  l.cluster = dim3(IpDgradUnpool::S, 1, 1);
+  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, 128), tmap2d(w1t, 800, 512, 512, ipk::BN), m2, g2, part_db2, N};
+  l.set((const void*)ip_tile<IpDgradUnpool>, dim3(cdiv(800, ipk::BN), cdiv(N, 128)), dim3(ipk::THREADS),
+        ip_smem<IpDgradUnpool>(), p);
   return l;
 }
 
-int db2_partials(int N) { return (int)cdiv(N, 128) * IpDgradUnpool::S; }
+int db2_partials(int N) { return (int)cdiv(N, 128); }
 
 Launch conv2_dgrad_launch(const float* g2, const float* w2d, float* dp1, int N, int sms) {
   Launch l;
