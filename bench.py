@@ -396,27 +396,54 @@ def main():
     value = images / (ms / 1e3)
 
     # end to end through the public API from pinned host buffers
-    xh = torch.from_numpy(xs[:BATCH].copy()).pin_memory()
-    yh = torch.from_numpy(ys[:BATCH].copy()).pin_memory()
     e2e_steps = min(args.e2e_steps, args.steps)
-    for _ in range(3):
-        net.net_train_step_host(xh, yh, sgd, it)
-        it += 1
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        net.net_train_step_host(xh, yh, sgd, it)
-        it += 1
-    e1.record(stream)
+    gen8 = {"lenet": synth.mnist_like_fast_u8, "cifar10_quick": synth.cifar_like_fast_u8}.get(args.workload)
+    if gen8 is not None:
+        # the dataset's bytes (NEXT #4): pinned host batches -> net_train_steps_u8_host
+        # (double-buffered H2D on a copy stream under the previous step, bytes
+        # normalised on the device, every step's loss read back)
+        ring = min(64, max(1, e2e_steps))
+        g8 = gen8(BATCH * ring, seed=200 + rank)
+        net.net_set_input_transform(1.0 / 256, g8[2] if len(g8) > 2 else None)
+        xh = torch.from_numpy(g8[0]).view(ring, BATCH, *g8[0].shape[1:]).pin_memory()
+        yh = torch.from_numpy(g8[1]).view(ring, BATCH).pin_memory()
+        net.net_train_steps_u8_host(xh[:3], yh[:3], sgd, it)
+        it += 3
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        done = 0
+        while done < e2e_steps:
+            k = min(ring, e2e_steps - done)
+            net.net_train_steps_u8_host(xh[:k], yh[:k], sgd, it)
+            it += k
+            done += k
+        e1.record(stream)
+        h2d = BATCH * img_floats + BATCH * 4
+        e2e_kind = "byte batches, pipelined (net_train_steps_u8_host)"
+    else:
+        xh = torch.from_numpy(xs[:BATCH].copy()).pin_memory()
+        yh = torch.from_numpy(ys[:BATCH].copy()).pin_memory()
+        for _ in range(3):
+            net.net_train_step_host(xh, yh, sgd, it)
+            it += 1
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            net.net_train_step_host(xh, yh, sgd, it)
+            it += 1
+        e1.record(stream)
+        h2d = BATCH * img_floats * 4 + BATCH * 4
+        e2e_kind = "fp32 batches, one synchronous call per step (net_train_step_host)"
     torch.cuda.synchronize()
     ms_e2e = e0.elapsed_time(e1)
     if world > 1:
         ms_e2e = max_over_ranks(ms_e2e, dist)
     e2e = {"value": world * BATCH * e2e_steps / (ms_e2e / 1e3), "unit": UNIT,
-           "h2d_bytes_per_step": BATCH * img_floats * 4 + BATCH * 4, "d2h_bytes_per_step": 4,
-           "steps": e2e_steps}
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "steps": e2e_steps, "path": e2e_kind}
 
     # per-stage timing (CUDA events on the launching stream, eager steps)
     prof = net.net_profile_stages(X[0], Y[0], sgd, it, args.profile_steps)

@@ -148,6 +148,47 @@ pn_status net_train_step_host(pn_net* net, const float* x_host,
 pn_status net_infer(pn_net* net, const float* x, const int32_t* labels,
                     float* loss, void* stream);
 
+/* Byte input (data ingestion).  Images arrive as the
+ * datasets store them, one unsigned byte per pixel, N*C*H*W; the input blob is
+ * x = fl(fl(byte * scale) - mean[c,h,w]) (S:604 MNIST: scale 1/256, no mean;
+ * S:613 CIFAR: scale 1/256 minus the per-pixel mean), two IEEE fp32
+ * roundings, no FMA.  The fused LeNet plan applies it inside conv1's own
+ * loads (no fp32 input is ever stored); other plans run one ingest kernel
+ * into a library-owned fp32 input buffer first.
+ * net_set_input_transform: scale > 0; mean_host = NULL or count = C*H*W host
+ *   floats (copied).  Default: scale 1/256, no mean.  Invalidates the captured
+ *   graphs (they are re-captured on the next step). */
+pn_status net_set_input_transform(pn_net* net, float scale,
+                                  const float* mean_host, int64_t count);
+/* net_train_step from a device byte batch x8 (N*C*H*W bytes, caller-owned,
+ * stream-ordered like net_train_step's x). */
+pn_status net_train_step_u8(pn_net* net, const uint8_t* x8,
+                            const int32_t* labels, const pn_sgd* sgd,
+                            int64_t iter, float* loss, void* stream);
+/* nsteps consecutive training steps from HOST byte batches (the end-to-end
+ * data path): batch s is x8_host[s*N*C*H*W ...], labels_host[s*N ...]
+ * (pinned memory for overlap).  Double-buffered: the host->device copy of
+ * batch s+1 runs on a library copy stream while step s computes; step s's
+ * loss is copied back to losses_host[s].  Iterations iter0 .. iter0+nsteps-1.
+ * Synchronises `stream` before returning. */
+pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host,
+                                  const int32_t* labels_host, int64_t nsteps,
+                                  const pn_sgd* sgd, int64_t iter0,
+                                  float* losses_host, void* stream);
+/* Dataset files (host only, no GPU needed).
+ * pn_idx_read: an unsigned-byte IDX file (MNIST images: 3 dims N,28,28;
+ *   labels: 1 dim N).  Fills ndims/dims (up to 4, big-endian sizes decoded);
+ *   copies the payload to dst when dst != NULL (cap bytes available).
+ *   PN_ERR_PARSE: wrong magic / data type / truncated or oversized file.
+ * pn_cifar_read: a CIFAR-10 binary batch (records: 1 label byte, 3072 pixel
+ *   bytes in CHW order).  *count = records; pixels (count*3072 bytes) and
+ *   labels (count int32) filled when non-NULL (cap records available).
+ *   PN_ERR_PARSE: size not a multiple of 3073 or a label byte > 9. */
+pn_status pn_idx_read(const char* path, uint8_t* dst, int64_t cap, int* ndims,
+                      int64_t dims[4]);
+pn_status pn_cifar_read(const char* path, uint8_t* pixels, int32_t* labels,
+                        int64_t cap, int64_t* count);
+
 /* Teacher forcing / profiling: the plan is a list of stages (one kernel
  * launch each).  Stage i of the forward (phase 0), backward (phase 1) or
  * update (phase 2) list can be run alone against the current blob contents. */

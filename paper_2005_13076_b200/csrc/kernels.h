@@ -25,6 +25,7 @@ __global__ void accuracy_generic(const __grid_constant__ AccuracyP p);
 __global__ void accuracy_reduce(const __grid_constant__ AccReduceP p);
 __global__ void loss_reduce(const __grid_constant__ LossReduceP p);
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p);
+__global__ void ingest_u8(const __grid_constant__ IngestP p);
 __global__ void mask_convert(const __grid_constant__ MaskExpandP p);
 __global__ void tf32_copy(const __grid_constant__ Tf32CopyP p);
 

@@ -641,6 +641,21 @@ __global__ void __launch_bounds__(256) loss_reduce(const __grid_constant__ LossR
   }
 }
 
+// ------------------------------------------------------------ byte ingest
+// NEXT #4 (S:604 MNIST bytes x 1/256; S:613 CIFAR bytes x 1/256 minus the
+// per-pixel mean): one fp32 rounding per operation, no FMA (matches the
+// harness's numpy float32 arithmetic bit for bit).  4 bytes per thread.
+__global__ void ingest_u8(const __grid_constant__ IngestP p) {
+  pdl_enter();
+  const long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int q = 0; q < 4; ++q) {
+    const long long i = 4 * i4 + q;
+    if (i >= p.n) return;
+    const float v = __fmul_rn((float)p.x8[i], p.scale);
+    p.y[i] = p.mean ? __fsub_rn(v, p.mean[i % p.per]) : v;
+  }
+}
+
 // ---------------------------------------------------------------------- SGD
 // S:536-544 / DESIGN.md R11: one IEEE fp32 rounding per op, no contraction.
 __device__ __forceinline__ void sgd_one(float& w, float d, float& v, float lr, float mom,

@@ -36,6 +36,15 @@ __device__ __forceinline__ void fma2(unsigned long long& d, float a, unsigned lo
 __device__ __forceinline__ float lo32(unsigned long long v) { return __uint_as_float((unsigned)v); }
 __device__ __forceinline__ float hi32(unsigned long long v) { return __uint_as_float((unsigned)(v >> 32)); }
 
+// the network input element i: the fp32 blob, or a byte normalised on load
+// (NEXT #4: x = byte * scale - mean[pixel], two IEEE roundings, no FMA)
+__device__ __forceinline__ float in_x(const float* x, const uint8_t* x8, float scale, const float* mean,
+                                      long long i) {
+  if (!x8) return __ldg(x + i);
+  const float v = __fmul_rn((float)__ldg(x8 + i), scale);
+  return mean ? __fsub_rn(v, __ldg(mean + i % 784)) : v;
+}
+
 constexpr int C1_MAXIMG = 4;  // images a block's item range can touch
 __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
   // everything read here (the batch, conv1's weights from the previous
@@ -52,7 +61,7 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constan
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f0 = 2 * warp;
   for (int i = threadIdx.x; i < nimg * 784; i += blockDim.x)
-    xs[i / 784][i % 784] = __ldg(p.x + (long long)nlo * 784 + i);
+    xs[i / 784][i % 784] = in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i);
   unsigned long long wp[25];
 #pragma unroll
   for (int t = 0; t < 25; ++t) wp[t] = pk2(__ldg(p.w + f0 * 25 + t), __ldg(p.w + (f0 + 1) * 25 + t));
@@ -384,7 +393,8 @@ __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__
       g[im * 9 + t] = v ? __ldg(p.dp1 + idx) : 0.f;
       off[im * 9 + t] = v ? (int)__ldg(p.m1 + idx) : 0;
     }
-  for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x) xs[i / 784][i % 784] = __ldg(p.x + (long long)n0 * 784 + i);
+  for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x)
+    xs[i / 784][i % 784] = in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + i);
   __syncthreads();
   float acc[25], bacc = 0.f;
 #pragma unroll

@@ -160,6 +160,25 @@ int pool_out(int in, int k, int s, int p) {
 }  // namespace
 
 // -------------------------------------------------------------------- net
+// one instantiated graph of phases [0, nph): the node of every stage (flat
+// phase-major order; null for non-kernel stages) and the parameter block it
+// was last given, so a re-patch touches only the nodes whose arguments changed
+struct GraphExec {
+  cudaGraphExec_t ex = nullptr;
+  cudaGraph_t g = nullptr;
+  std::vector<cudaGraphNode_t> nodes;
+  std::vector<std::vector<unsigned char>> args;
+  StepArgs a;
+  void drop() {
+    if (ex) cudaGraphExecDestroy(ex);
+    if (g) cudaGraphDestroy(g);
+    ex = nullptr;
+    g = nullptr;
+    nodes.clear();
+    args.clear();
+  }
+};
+
 struct pn_net {
   int device = 0, batch = 0, flags = 0;
   bool tf32 = false, fused = false;
@@ -182,6 +201,17 @@ struct pn_net {
   int npad = 0;
   float* p2T = nullptr;       // [800][npad]
   float* p1c = nullptr;       // pool1 in the conv2 tap-GEMM layout (tc.h)
+  // byte input (NEXT #4): x = byte * x_scale - x_mean[pixel]
+  float x_scale = 1.f / 256.f;
+  float* x_mean = nullptr;    // [C*H*W] device, or null
+  float* xin = nullptr;       // fp32 input written by the ingest kernel (layerwise plans)
+  uint8_t* h2d_x8[2] = {nullptr, nullptr};  // pipelined host input: device slots
+  int32_t* h2d_y[2] = {nullptr, nullptr};
+  float* h2d_loss = nullptr;  // [2]
+  float* loss_pinned = nullptr;  // host (pinned) per-step losses of the pipelined loop
+  int64_t loss_pinned_cap = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   float* da1r = nullptr;      // [N][500]
   float* da1rT = nullptr;     // [500][npad]
   float* part_b1 = nullptr;   // [splits][500]  ip1 bias-gradient partials
@@ -195,9 +225,10 @@ struct pn_net {
   StepArgs last;  // for eager stage patching
 
   cudaStream_t cap = nullptr;  // capture stream
-  cudaGraphExec_t step_exec = nullptr, infer_exec = nullptr;
-  cudaGraph_t step_graph = nullptr, infer_graph = nullptr;
-  StepArgs step_args, infer_args;  // args baked into the executable graphs
+  // captured graphs: the train step, forward-only inference, and one train
+  // step per input slot of the pipelined host loop (their arguments then
+  // differ only in the learning rate)
+  GraphExec step, infer, slot[2];
   int launches_per_step = 0;
 
   // data parallel
@@ -866,7 +897,10 @@ static void build_fused_lenet(pn_net* net) {
     Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c, per};
     Launch l;
     l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(320), 0, p);
-    add(fwd, "conv1+pool1", l, [](Launch& l, const StepArgs& a) { l.params<Conv1Pool1P>().x = a.x; });
+    add(fwd, "conv1+pool1", l, [net](Launch& l, const StepArgs& a) {
+      Conv1Pool1P& q = l.params<Conv1Pool1P>();
+      q.x = a.x, q.x8 = a.x8, q.x_scale = net->x_scale, q.x_mean = net->x_mean;
+    });
   }
   if (net->tf32) {
     add(fwd, "conv2+pool2[tc]", tc::conv2_pool2_launch(net->pack.w2c, P + c2.off + 25000, net->p1c, p2.data,
@@ -971,7 +1005,10 @@ static void build_fused_lenet(pn_net* net) {
                   c1.splits, 520};
     Launch l;
     l.set((const void*)lenet_conv1_wgrad, dim3(c1.splits), dim3(320), 0, p);
-    add(bwd, "conv1.wgrad", l, [](Launch& l, const StepArgs& a) { l.params<Conv1WgradP>().x = a.x; });
+    add(bwd, "conv1.wgrad", l, [net](Launch& l, const StepArgs& a) {
+      Conv1WgradP& q = l.params<Conv1WgradP>();
+      q.x = a.x, q.x8 = a.x8, q.x_scale = net->x_scale, q.x_mean = net->x_mean;
+    });
     conv_segs.push_back(seg(net->partials + c1.part_off, G + c1.off, 520, c1.splits, 520));
   }
   add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
@@ -1125,9 +1162,15 @@ static StepArgs make_args(pn_net* net, const float* x, const int32_t* labels, fl
   return a;
 }
 
+static bool same_args(const StepArgs& a, const StepArgs& b) {
+  return a.x == b.x && a.x8 == b.x8 && a.labels == b.labels && a.loss == b.loss && a.lr == b.lr && a.mom == b.mom &&
+         a.decay == b.decay && a.gscale == b.gscale;
+}
+
 // capture phases [0, nph) into an executable graph; record kernel nodes
-static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_t* out, bool infer) {
+static pn_status capture(pn_net* net, int nph, const StepArgs& a, GraphExec& E) {
   if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
+  E.drop();
   CU(cudaStreamBeginCapture(net->cap, cudaStreamCaptureModeThreadLocal));
   bool prev_kernel = false;  // the captured step is one fixed sequence across phases
   for (int ph = 0; ph < nph; ++ph)
@@ -1138,32 +1181,34 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_
       if (st != PN_OK) {
         cudaGraph_t g;
         cudaStreamEndCapture(net->cap, &g);
+        E.drop();
         return st;
       }
+      cudaGraphNode_t node = nullptr;
       if (!s.custom) {
         cudaStreamCaptureStatus cs;
         const cudaGraphNode_t* deps = nullptr;
         size_t nd = 0;
         CU(cudaStreamGetCaptureInfo(on, &cs, nullptr, nullptr, &deps, &nd));
-        (infer ? s.inode : s.node) = nd ? deps[0] : nullptr;
+        node = nd ? deps[0] : nullptr;
       }
+      E.nodes.push_back(node);
+      E.args.push_back(s.L.arg);
     }
-  cudaGraph_t g;
-  CU(cudaStreamEndCapture(net->cap, &g));
-  if (*out) cudaGraphExecDestroy(*out);
-  CU(cudaGraphInstantiate(out, g, 0));
-  // keep the graph: its node handles address the exec's nodes when patching
-  cudaGraph_t& keep = infer ? net->infer_graph : net->step_graph;
-  if (keep) cudaGraphDestroy(keep);
-  keep = g;
+  CU(cudaStreamEndCapture(net->cap, &E.g));
+  CU(cudaGraphInstantiate(&E.ex, E.g, 0));  // (the graph is kept: its node handles address the exec's nodes)
+  E.a = a;
   return PN_OK;
 }
 
-static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, cudaGraphExec_t ex, bool infer) {
+static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, GraphExec& E) {
+  size_t i = 0;
   for (int ph = 0; ph < nph; ++ph)
     for (auto& s : net->phase[ph]) {
+      const size_t k = i++;
       if (s.custom || !s.patch) continue;
       s.patch(s.L, a);
+      if (s.L.arg == E.args[k]) continue;  // unchanged in this exec
       cudaKernelNodeParams kp{};
       void* args[1] = {s.L.arg.data()};
       kp.func = (void*)s.L.func;
@@ -1171,15 +1216,30 @@ static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, cudaGraphE
       kp.blockDim = s.L.block;
       kp.sharedMemBytes = (unsigned)s.L.smem;
       kp.kernelParams = args;
-      CU(cudaGraphExecKernelNodeSetParams(ex, infer ? s.inode : s.node, &kp));
+      CU(cudaGraphExecKernelNodeSetParams(E.ex, E.nodes[k], &kp));
+      E.args[k] = s.L.arg;
     }
+  E.a = a;
   return PN_OK;
 }
 
-static bool same_args(const StepArgs& a, const StepArgs& b) {
-  return a.x == b.x && a.labels == b.labels && a.loss == b.loss && a.lr == b.lr && a.mom == b.mom &&
-         a.decay == b.decay && a.gscale == b.gscale;
+// launch graph E of phases [0, nph) with arguments a (capture on first use)
+static pn_status replay(pn_net* net, int nph, const StepArgs& a, GraphExec& E, cudaStream_t st) {
+  if (!E.ex) TRY(capture(net, nph, a, E));
+  else if (!same_args(a, E.a)) TRY(patch_graph(net, nph, a, E));
+  CU(cudaGraphLaunch(E.ex, st));
+  net->last = a;
+  net->forward_done = true;
+  return PN_OK;
 }
+
+static void drop_graphs(pn_net* net) {
+  net->step.drop();
+  net->infer.drop();
+  net->slot[0].drop();
+  net->slot[1].drop();
+}
+
 
 // ------------------------------------------------------------------ C ABI
 #define CHECK_NET(n) \
@@ -1257,16 +1317,16 @@ extern "C" void net_destroy(pn_net* net) {
   if (!net) return;
   cudaSetDevice(net->device);
   cudaDeviceSynchronize();
-  if (net->step_exec) cudaGraphExecDestroy(net->step_exec);
-  if (net->infer_exec) cudaGraphExecDestroy(net->infer_exec);
-  if (net->step_graph) cudaGraphDestroy(net->step_graph);
-  if (net->infer_graph) cudaGraphDestroy(net->infer_graph);
+  drop_graphs(net);
   if (net->cap) cudaStreamDestroy(net->cap);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
-  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join})
+  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join, net->ev_copied[0],
+                        net->ev_copied[1], net->ev_used[0], net->ev_used[1]})
     if (e) cudaEventDestroy(e);
   if (net->side) cudaStreamDestroy(net->side);
+  if (net->copy) cudaStreamDestroy(net->copy);
+  if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
   for (void* p : net->allocs) cudaFree(p);
   delete net;
 }
@@ -1442,17 +1502,7 @@ extern "C" pn_status net_train_step(pn_net* net, const float* x, const int32_t* 
     return fail(PN_ERR_INVALID_ARG, "net_train_step: bad argument");
   CU(cudaSetDevice(net->device));
   StepArgs a = make_args(net, x, labels, loss, sgd, iter);
-  if (!net->step_exec) {
-    TRY(capture(net, 3, a, &net->step_exec, false));
-    net->step_args = a;
-  } else if (!same_args(a, net->step_args)) {
-    TRY(patch_graph(net, 3, a, net->step_exec, false));
-    net->step_args = a;
-  }
-  CU(cudaGraphLaunch(net->step_exec, (cudaStream_t)stream));
-  net->last = a;
-  net->forward_done = true;
-  return PN_OK;
+  return replay(net, 3, a, net->step, (cudaStream_t)stream);
 }
 
 extern "C" pn_status net_infer(pn_net* net, const float* x, const int32_t* labels, float* loss, void* stream) {
@@ -1460,17 +1510,7 @@ extern "C" pn_status net_infer(pn_net* net, const float* x, const int32_t* label
   if (!x || !labels) return fail(PN_ERR_INVALID_ARG, "x and labels are required");
   CU(cudaSetDevice(net->device));
   StepArgs a = make_args(net, x, labels, loss, nullptr, 0);
-  if (!net->infer_exec) {
-    TRY(capture(net, 1, a, &net->infer_exec, true));
-    net->infer_args = a;
-  } else if (!same_args(a, net->infer_args)) {
-    TRY(patch_graph(net, 1, a, net->infer_exec, true));
-    net->infer_args = a;
-  }
-  CU(cudaGraphLaunch(net->infer_exec, (cudaStream_t)stream));
-  net->last = a;
-  net->forward_done = true;
-  return PN_OK;
+  return replay(net, 1, a, net->infer, (cudaStream_t)stream);
 }
 
 extern "C" pn_status net_train_step_host(pn_net* net, const float* xh, const int32_t* lh, const pn_sgd* sgd,
@@ -1494,6 +1534,165 @@ extern "C" pn_status net_train_step_host(pn_net* net, const float* xh, const int
   TRY(net_train_step(net, buf.x, buf.y, sgd, iter, buf.l, stream));
   CU(cudaMemcpyAsync(loss_host, buf.l, 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  return PN_OK;
+}
+
+// ------------------------------------------------ byte input (NEXT #4)
+static int64_t input_count(pn_net* net) { return net->blobs[net->blob(net->input_name)].count(); }
+
+extern "C" pn_status net_set_input_transform(pn_net* net, float scale, const float* mean_host, int64_t count) {
+  CHECK_NET(net);
+  const Blob& in = net->blobs[net->blob(net->input_name)];
+  const int64_t per = in.count() / net->batch;
+  if (!(scale > 0.f) || (mean_host && count != per))
+    return fail(PN_ERR_INVALID_ARG, "input transform: scale > 0 and a mean of C*H*W floats (or none)");
+  CU(cudaSetDevice(net->device));
+  net->x_scale = scale;
+  if (mean_host) {
+    if (!net->x_mean) TRY(net->alloc(&net->x_mean, (size_t)per));
+    CU(cudaMemcpy(net->x_mean, mean_host, per * 4, cudaMemcpyHostToDevice));
+  } else {
+    net->x_mean = nullptr;
+  }
+  // the transform is a kernel parameter of the captured graphs: re-capture
+  drop_graphs(net);
+  return PN_OK;
+}
+
+// the step's arguments for a byte batch: the fused LeNet plan normalises the
+// bytes inside conv1's own loads; any other plan gets them through the ingest
+// kernel into an fp32 input buffer first
+static pn_status byte_args(pn_net* net, const uint8_t* x8, StepArgs& a, cudaStream_t st) {
+  if (net->fused) {
+    a.x = nullptr;
+    a.x8 = x8;
+    return PN_OK;
+  }
+  const int64_t n = input_count(net);
+  if (!net->xin) TRY(net->alloc(&net->xin, (size_t)n));
+  IngestP q{x8, net->xin, n, (int)(n / net->batch), net->x_scale, net->x_mean};
+  Launch l;
+  l.set((const void*)ingest_u8, dim3(cdiv((n + 3) / 4, 256)), dim3(256), 0, q);
+  CU(l.launch(st));
+  a.x = net->xin;
+  a.x8 = nullptr;
+  return PN_OK;
+}
+
+
+extern "C" pn_status net_train_step_u8(pn_net* net, const uint8_t* x8, const int32_t* labels, const pn_sgd* sgd,
+                                       int64_t iter, float* loss, void* stream) {
+  CHECK_NET(net);
+  if (!x8 || !labels || !sgd || iter < 0 || (sgd->lr_policy != 0 && sgd->lr_policy != 1))
+    return fail(PN_ERR_INVALID_ARG, "net_train_step_u8: bad argument");
+  CU(cudaSetDevice(net->device));
+  StepArgs a = make_args(net, nullptr, labels, loss, sgd, iter);
+  TRY(byte_args(net, x8, a, (cudaStream_t)stream));
+  return replay(net, 3, a, net->step, (cudaStream_t)stream);
+}
+
+extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host, const int32_t* labels_host,
+                                             int64_t nsteps, const pn_sgd* sgd, int64_t iter0, float* losses_host,
+                                             void* stream) {
+  CHECK_NET(net);
+  if (!x8_host || !labels_host || !losses_host || !sgd || nsteps < 0 || iter0 < 0)
+    return fail(PN_ERR_INVALID_ARG, "net_train_steps_u8_host: bad argument");
+  CU(cudaSetDevice(net->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nx = input_count(net);
+  if (!net->copy) {
+    CU(cudaStreamCreateWithFlags(&net->copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CU(cudaEventCreateWithFlags(&net->ev_copied[b], cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&net->ev_used[b], cudaEventDisableTiming));
+      TRY(net->alloc(&net->h2d_x8[b], (size_t)nx));
+      TRY(net->alloc(&net->h2d_y[b], (size_t)net->batch));
+    }
+    TRY(net->alloc(&net->h2d_loss, 2));
+    // the slots start free
+    for (int b = 0; b < 2; ++b) CU(cudaEventRecord(net->ev_used[b], st));
+  }
+  if (net->loss_pinned_cap < nsteps) {  // the D2H loss reads land in pinned memory (asynchronous)
+    if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
+    net->loss_pinned = nullptr;
+    net->loss_pinned_cap = 0;
+    CU(cudaMallocHost(&net->loss_pinned, nsteps * sizeof(float)));
+    net->loss_pinned_cap = nsteps;
+  }
+  // double buffering: the copy of batch s+1 (copy stream) overlaps step s
+  for (int64_t s = 0; s < nsteps; ++s) {
+    const int b = (int)(s & 1);
+    CU(cudaStreamWaitEvent(net->copy, net->ev_used[b], 0));  // step s-2 is done with slot b
+    CU(cudaMemcpyAsync(net->h2d_x8[b], x8_host + s * nx, nx, cudaMemcpyHostToDevice, net->copy));
+    CU(cudaMemcpyAsync(net->h2d_y[b], labels_host + s * net->batch, net->batch * 4, cudaMemcpyHostToDevice,
+                       net->copy));
+    CU(cudaEventRecord(net->ev_copied[b], net->copy));
+    CU(cudaStreamWaitEvent(st, net->ev_copied[b], 0));
+    StepArgs a = make_args(net, nullptr, net->h2d_y[b], net->h2d_loss + b, sgd, iter0 + s);
+    TRY(byte_args(net, net->h2d_x8[b], a, st));
+    TRY(replay(net, 3, a, net->slot[b], st));  // slot b's own graph: only the lr changes
+    CU(cudaMemcpyAsync(net->loss_pinned + s, net->h2d_loss + b, 4, cudaMemcpyDeviceToHost, st));
+    CU(cudaEventRecord(net->ev_used[b], st));
+  }
+  CU(cudaStreamSynchronize(st));
+  std::memcpy(losses_host, net->loss_pinned, nsteps * sizeof(float));
+  return PN_OK;
+}
+
+// ------------------------------------------------ dataset files (NEXT #4)
+// MNIST IDX (big-endian magic 0x00000800 | type << 8 | ndims, then ndims
+// big-endian uint32 sizes, then the data; type 0x08 = unsigned byte) and the
+// CIFAR-10 binary batches (records of 1 label byte + 3072 pixel bytes, CHW).
+static bool read_all(const char* path, std::vector<uint8_t>& buf) {
+  FILE* f = fopen(path, "rb");
+  if (!f) return false;
+  uint8_t tmp[1 << 16];
+  size_t n;
+  while ((n = fread(tmp, 1, sizeof(tmp), f)) > 0) buf.insert(buf.end(), tmp, tmp + n);
+  fclose(f);
+  return true;
+}
+
+extern "C" pn_status pn_idx_read(const char* path, uint8_t* dst, int64_t cap, int* ndims, int64_t dims[4]) {
+  if (!path || !ndims || !dims) return fail(PN_ERR_INVALID_ARG, "pn_idx_read: NULL argument");
+  std::vector<uint8_t> b;
+  if (!read_all(path, b)) return fail(PN_ERR_INVALID_ARG, std::string("cannot read ") + path);
+  if (b.size() < 4 || b[0] != 0 || b[1] != 0 || b[2] != 0x08 || b[3] < 1 || b[3] > 4)
+    return fail(PN_ERR_PARSE, "not an unsigned-byte IDX file (magic)");
+  const int nd = b[3];
+  if (b.size() < 4 + 4 * (size_t)nd) return fail(PN_ERR_PARSE, "truncated IDX header");
+  int64_t total = 1;
+  for (int i = 0; i < nd; ++i) {
+    const uint8_t* q = &b[4 + 4 * i];
+    dims[i] = ((int64_t)q[0] << 24) | ((int64_t)q[1] << 16) | ((int64_t)q[2] << 8) | q[3];
+    total *= dims[i];
+  }
+  *ndims = nd;
+  const size_t off = 4 + 4 * (size_t)nd;
+  if (b.size() != off + (size_t)total) return fail(PN_ERR_PARSE, "IDX size does not match its header");
+  if (dst) {
+    if (cap < total) return fail(PN_ERR_INVALID_ARG, "pn_idx_read: destination too small");
+    std::memcpy(dst, b.data() + off, (size_t)total);
+  }
+  return PN_OK;
+}
+
+extern "C" pn_status pn_cifar_read(const char* path, uint8_t* pixels, int32_t* labels, int64_t cap, int64_t* count) {
+  if (!path || !count) return fail(PN_ERR_INVALID_ARG, "pn_cifar_read: NULL argument");
+  std::vector<uint8_t> b;
+  if (!read_all(path, b)) return fail(PN_ERR_INVALID_ARG, std::string("cannot read ") + path);
+  if (b.empty() || b.size() % 3073) return fail(PN_ERR_PARSE, "CIFAR-10 binary: size is not a multiple of 3073");
+  const int64_t n = (int64_t)(b.size() / 3073);
+  *count = n;
+  if (pixels || labels) {
+    if (cap < n) return fail(PN_ERR_INVALID_ARG, "pn_cifar_read: destination too small");
+    for (int64_t i = 0; i < n; ++i) {
+      const uint8_t* r = b.data() + i * 3073;
+      if (r[0] > 9) return fail(PN_ERR_PARSE, "CIFAR-10 binary: label byte > 9");
+      if (labels) labels[i] = r[0];
+      if (pixels) std::memcpy(pixels + i * 3072, r + 1, 3072);
+    }
+  }
   return PN_OK;
 }
 
@@ -1601,8 +1800,7 @@ extern "C" pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* 
   CU(cudaEventCreateWithFlags(&net->ev_ip, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&net->ev_conv, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&net->ev_done, cudaEventDisableTiming));
-  if (net->step_exec) { cudaGraphExecDestroy(net->step_exec); net->step_exec = nullptr; }
-  if (net->infer_exec) { cudaGraphExecDestroy(net->infer_exec); net->infer_exec = nullptr; }
+  drop_graphs(net);
   TRY(build_plan(net));
   return PN_OK;
 }

@@ -143,6 +143,10 @@ struct Conv1Pool1P {  // x[N,1,28,28] -> p1[N,20,12,12], m1 (uint8 offsets)
   int round_tf32;  // store p1 rounded to TF32 (RNA) for the tensor-core plan
   float* p1c;      // optional: TF32 copy in the conv2 tap-GEMM layout (tc.h kP1cPairFloats per pair)
   int per_block;   // pooled (image, position) items per block (grid = ceil(N*144 / per_block))
+  // optional byte input (NEXT #4): x = fl(fl(x8 * x_scale) - x_mean[pixel]) replaces x
+  const uint8_t* x8;
+  float x_scale;
+  const float* x_mean;  // [784] or null
 };
 struct Conv2Pool2P {  // p1[N,20,12,12] -> p2[N,50,4,4], m2
   const float* p1;
@@ -194,6 +198,17 @@ struct Conv1WgradP {  // dp1 + m1 + x -> partial dW1, db1
   float* part_w;  // [splits][500]
   float* part_b;  // [splits][20]
   int N, splits, pstride;
+  const uint8_t* x8;  // optional byte input, as Conv1Pool1P
+  float x_scale;
+  const float* x_mean;
+};
+struct IngestP {  // bytes -> fp32 input blob: y = fl(fl(x8 * scale) - mean[i % per])
+  const uint8_t* x8;
+  float* y;
+  long long n;
+  int per;
+  float scale;
+  const float* mean;  // [per] or null
 };
 
 

@@ -17,6 +17,7 @@ namespace pn {
 // Everything that changes from one training step to the next.
 struct StepArgs {
   const float* x = nullptr;
+  const uint8_t* x8 = nullptr;  // byte input (fused LeNet plan: normalised inside conv1's loads)
   const int32_t* labels = nullptr;
   float* loss = nullptr;
   float lr = 0.f, mom = 0.f, decay = 0.f, gscale = 1.f;
@@ -86,8 +87,6 @@ struct Stage {
   std::function<void(Launch&, const StepArgs&)> patch;  // refresh step-dependent args
   std::function<cudaError_t(cudaStream_t)> custom;     // non-kernel action
   bool side = false;  // in a step (graph or eager phase run): launched on the side stream, between fork and join
-  cudaGraphNode_t node = nullptr;                      // kernel node in the step graph
-  cudaGraphNode_t inode = nullptr;                     // kernel node in the infer graph
 };
 
 }  // namespace pn

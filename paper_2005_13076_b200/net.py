@@ -36,7 +36,7 @@ def _ptr(t, dtype=None):
         return None
     if dtype is not None:
         import torch
-        want = {"f32": torch.float32, "i32": torch.int32}[dtype]
+        want = {"f32": torch.float32, "i32": torch.int32, "u8": torch.uint8}[dtype]
         if t.dtype != want or not t.is_cuda or not t.is_contiguous():
             raise TypeError(f"expected a contiguous CUDA {want} tensor, got {t.dtype} "
                             f"on {t.device} (contiguous={t.is_contiguous()})")
@@ -152,6 +152,29 @@ class Net:
                                         ctypes.c_void_p(labels_host.data_ptr()), ctypes.byref(sgd),
                                         it, ctypes.byref(loss), _stream(stream)))
         return loss.value
+
+    # ---- byte input (NEXT #4)
+    def net_set_input_transform(self, scale=1.0 / 256, mean=None):
+        """x = byte * scale - mean[c,h,w] (mean: host float32 array of C*H*W, or None)."""
+        if mean is None:
+            check(lib().net_set_input_transform(self._h, scale, None, 0))
+        else:
+            m = np.ascontiguousarray(mean, dtype=np.float32).ravel()
+            check(lib().net_set_input_transform(self._h, scale, m.ctypes.data_as(ctypes.c_void_p), m.size))
+
+    def net_train_step_u8(self, x8, labels, sgd, it, loss=None, stream=None):
+        check(lib().net_train_step_u8(self._h, _ptr(x8, 'u8'), _ptr(labels, 'i32'), ctypes.byref(sgd), it,
+                                      _ptr(loss, 'f32'), _stream(stream)))
+
+    def net_train_steps_u8_host(self, x8_host, labels_host, sgd, it0, stream=None):
+        """x8_host: (steps, N, C, H, W) uint8 (pinned torch tensor preferred),
+        labels_host: (steps, N) int32.  Returns the per-step losses (numpy)."""
+        steps = x8_host.shape[0]
+        losses = np.zeros(steps, np.float32)
+        check(lib().net_train_steps_u8_host(self._h, ctypes.c_void_p(x8_host.data_ptr()),
+                                            ctypes.c_void_p(labels_host.data_ptr()), steps, ctypes.byref(sgd),
+                                            it0, losses.ctypes.data_as(ctypes.c_void_p), _stream(stream)))
+        return losses
 
     def net_infer(self, x, labels, loss=None, stream=None):
         check(lib().net_infer(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), _ptr(loss, 'f32'),

@@ -33,17 +33,24 @@ def mnist_like(n, seed=1, first=0):
     return x, y
 
 
-def mnist_like_fast(n, seed=1):
-    """Same distribution as mnist_like, drawn in one vectorised call (used for
-    the large bench datasets; image i is NOT the same as mnist_like's)."""
+def mnist_like_fast_u8(n, seed=1):
+    """mnist_like_fast's images as the bytes a dataset file stores: (n,1,28,28)
+    uint8 (x = byte/256) and labels."""
     g = rng([seed, 1 << 30])
     u = g.random((n, 16, 16))
     b = g.integers(1, 255, size=(n, 16, 16))
     b = np.where(u < 0.45, 0, np.where(u < 0.75, 255, b))
-    x = np.zeros((n, 1, 28, 28), np.float32)
-    x[:, 0, 6:22, 6:22] = b.astype(np.float32) / np.float32(256.0)
+    x8 = np.zeros((n, 1, 28, 28), np.uint8)
+    x8[:, 0, 6:22, 6:22] = b
     y = g.integers(0, 10, size=n).astype(np.int32)
-    return x, y
+    return x8, y
+
+
+def mnist_like_fast(n, seed=1):
+    """Same distribution as mnist_like, drawn in one vectorised call (used for
+    the large bench datasets; image i is NOT the same as mnist_like's)."""
+    x8, y = mnist_like_fast_u8(n, seed)
+    return x8.astype(np.float32) / np.float32(256.0), y
 
 
 def cifar_like(n, seed=1, first=0):
@@ -95,13 +102,21 @@ def labels(n, d, seed):
     return rng(seed).integers(0, d, size=n).astype(np.int32)
 
 
+def cifar_like_fast_u8(n, seed=1):
+    """cifar_like_fast's images as stored bytes: (n,3,32,32) uint8, labels, and
+    the per-pixel mean (3,32,32) float32 the input transform subtracts."""
+    g = rng([seed, 1 << 29])
+    x8 = g.integers(0, 256, size=(n, 3, 32, 32), dtype=np.uint8)
+    return x8, g.integers(0, 10, size=n).astype(np.int32), _cifar_mean(seed)
+
+
 def cifar_like_fast(n, seed=1):
     """CIFAR-shaped batch with cifar_like's distribution drawn in one call
-    (bench datasets; image i differs from cifar_like's)."""
-    g = rng([seed, 1 << 29])
-    x = g.integers(0, 256, size=(n, 3, 32, 32), dtype=np.uint8).astype(np.float32) / np.float32(256.0)
-    x -= _cifar_mean(seed)
-    return x, g.integers(0, 10, size=n).astype(np.int32)
+    (bench datasets; image i differs from cifar_like's): byte/256 - mean."""
+    x8, y, mean = cifar_like_fast_u8(n, seed)
+    x = x8.astype(np.float32) / np.float32(256.0)
+    x -= mean
+    return x, y
 
 
 def imagenet_like_fast(n, seed=1, hw=227):
