@@ -174,3 +174,65 @@ def test_pipelined_host_steps_equal_device_steps():
         np.testing.assert_array_equal(u, v)
     a.close()
     b.close()
+
+
+def learnable_mnist_u8(n, seed):
+    """A synthetic task LeNet must learn (stand-in for the MNIST sanity of
+    S:719 when the dataset is not provided): class y is a bright 6x5 block at
+    one of 10 positions (row block y // 5, column block y % 5) over byte noise
+    U{0..60}."""
+    g = np.random.default_rng(seed)
+    y = g.integers(0, 10, size=n).astype(np.int32)
+    x = g.integers(0, 61, size=(n, 1, 28, 28)).astype(np.uint8)
+    for i in range(n):
+        r, c = 4 + 10 * (y[i] // 5), 2 + 5 * (y[i] % 5)
+        x[i, 0, r:r + 6, c:c + 5] = 255
+    return x, y
+
+
+@pytest.mark.gpu
+def test_training_sanity_from_dataset_files(tmp_path):
+    """NEXT #4 end to end: IDX files -> pn_idx_read -> pipelined byte-input
+    training -> the loss falls and held-out accuracy >= 0.95 (S:719's bar),
+    on real MNIST when PN_MNIST_DIR provides it, else on the learnable
+    synthetic task written in the same IDX format."""
+    import os
+
+    import torch
+
+    from paper_2005_13076_b200 import Net, make_sgd
+    d = os.environ.get("PN_MNIST_DIR")
+    N = 64
+    if d and os.path.exists(os.path.join(d, "train-images-idx3-ubyte")):
+        xtr, ytr = data.read_mnist(os.path.join(d, "train-images-idx3-ubyte"),
+                                   os.path.join(d, "train-labels-idx1-ubyte"))
+        xte, yte = data.read_mnist(os.path.join(d, "t10k-images-idx3-ubyte"),
+                                   os.path.join(d, "t10k-labels-idx1-ubyte"))
+        steps = 1000
+    else:
+        x, y = learnable_mnist_u8(N * 300 + 512, seed=11)
+        write_idx(tmp_path / "img", x[:, 0])
+        write_idx(tmp_path / "lab", y.astype(np.uint8))
+        x, y = data.read_mnist(str(tmp_path / "img"), str(tmp_path / "lab"))
+        xtr, ytr, xte, yte = x[:-512], y[:-512], x[-512:], y[-512:]
+        steps = 300
+    net = Net("lenet", N, device=0, tf32=True)
+    net.set_params(_params("lenet"))
+    sgd = make_sgd()
+    idx = np.arange(steps * N) % len(xtr)
+    xs = torch.from_numpy(np.ascontiguousarray(xtr[idx]).reshape(steps, N, 1, 28, 28)).pin_memory()
+    ys = torch.from_numpy(np.ascontiguousarray(ytr[idx]).reshape(steps, N)).pin_memory()
+    losses = np.concatenate([net.net_train_steps_u8_host(xs[s:s + 100], ys[s:s + 100], sgd, s)
+                             for s in range(0, steps, 100)])
+    assert np.all(np.isfinite(losses))
+    assert losses[-20:].mean() < 0.25 * losses[:5].mean(), (losses[:5], losses[-20:])
+    hits = total = 0
+    loss = torch.zeros(1, device="cuda")
+    for b in range(0, (len(xte) // N) * N, N):
+        xb = torch.from_numpy(xte[b:b + N].astype(np.float32) / np.float32(256)).cuda()
+        net.net_infer(xb, torch.from_numpy(yte[b:b + N]).cuda(), loss)
+        pred = net.net_get_blob("pred").cpu().numpy().view(np.int32).ravel()[:N]
+        hits += int((pred == yte[b:b + N]).sum())
+        total += N
+    assert hits / total >= 0.95, hits / total
+    net.close()

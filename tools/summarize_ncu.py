@@ -19,7 +19,8 @@ PROF = "profiles"
 os.makedirs(PROF, exist_ok=True)
 
 # stage names of the TF32 plan (bench.py's roofline table uses them)
-STAGE_OF = {"conv2_fwd_persistent": "conv2+pool2[tc]", "ip_splitk": "ip1+relu[tc]",
+STAGE_OF = {"conv2_fwd_persistent": "conv2+pool2[tc]", "IpFwd": "ip1+relu[tc]", "IpWgrad": "ip1.wgrad[tc]",
+            "IpDgradUnpool": "ip1.dgrad+unpool2[tc]", "reduce_partials_multi": "conv.bucket_reduce",
             "conv2_dgrad_persistent": "conv2.dgrad[tc]", "conv2_wgrad_persistent": "conv2.wgrad[tc]",
             "lenet_conv1_wgrad": "conv1.wgrad", "lenet_conv1_pool1": "conv1+pool1",
             "lenet_ip2_loss": "ip2+softmax_loss", "lenet_ip2_bwd": "ip2.bwd+relu1.bwd",
