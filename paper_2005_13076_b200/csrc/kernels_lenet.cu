@@ -60,8 +60,20 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constan
   const int nlo = i0 / 144, nimg = (i1 - 1) / 144 - nlo + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f0 = 2 * warp;
-  for (int i = threadIdx.x; i < nimg * 784; i += blockDim.x)
-    xs[i / 784][i % 784] = in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i);
+  {  // every load of the staging issued before the first store (one HBM round trip)
+    constexpr int PER = (C1_MAXIMG * 784 + 319) / 320;
+    float v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + 320 * k;
+      v[k] = i < nimg * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + 320 * k;
+      if (i < nimg * 784) xs[i / 784][i % 784] = v[k];
+    }
+  }
   unsigned long long wp[25];
 #pragma unroll
   for (int t = 0; t < 25; ++t) wp[t] = pk2(__ldg(p.w + f0 * 25 + t), __ldg(p.w + (f0 + 1) * 25 + t));
@@ -212,7 +224,19 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
 __global__ void __launch_bounds__(128) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
   __shared__ __align__(16) float ws[10 * 500];
   __shared__ float bs[10];
-  for (int i = threadIdx.x; i < 5000; i += blockDim.x) ws[i] = __ldg(p.w + i);
+  {  // W2 as 1250 float4, all ten loads of a thread in flight together
+    float4 v[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const int i = threadIdx.x + 128 * k;
+      v[k] = i < 1250 ? __ldg(reinterpret_cast<const float4*>(p.w) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+#pragma unroll
+    for (int k = 0; k < 10; ++k) {
+      const int i = threadIdx.x + 128 * k;
+      if (i < 1250) reinterpret_cast<float4*>(ws)[i] = v[k];
+    }
+  }
   if (threadIdx.x < 10) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
   pdl_enter();
   const int lane = threadIdx.x & 31;
@@ -393,8 +417,20 @@ __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__
       g[im * 9 + t] = v ? __ldg(p.dp1 + idx) : 0.f;
       off[im * 9 + t] = v ? (int)__ldg(p.m1 + idx) : 0;
     }
-  for (int i = threadIdx.x; i < cnt * 784; i += blockDim.x)
-    xs[i / 784][i % 784] = in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + i);
+  {  // staging loads all in flight together
+    constexpr int PER = (CW_IMGS * 784 + 319) / 320;
+    float v[PER];
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + 320 * k;
+      v[k] = i < cnt * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + i) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + 320 * k;
+      if (i < cnt * 784) xs[i / 784][i % 784] = v[k];
+    }
+  }
   __syncthreads();
   float acc[25], bacc = 0.f;
 #pragma unroll

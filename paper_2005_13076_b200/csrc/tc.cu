@@ -921,11 +921,17 @@ __global__ void pack_weights(const __grid_constant__ PackP p) {
     __shared__ float t[32][33];
     const int k0 = (blockIdx.x % 25) * 32, o0 = (blockIdx.x / 25) * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
-    for (int y = ty; y < 32; y += 8) {
-      const int o = o0 + y;
-      const float v = o < 500 ? tf32f(p.w1[(size_t)o * 800 + k0 + tx]) : 0.f;
-      t[y][tx] = v;
-      if (o < 500) p.w1f[(size_t)o * 800 + k0 + tx] = v;
+    float v[4];  // the tile's four rows per thread loaded together
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = o0 + ty + 8 * u;
+      v[u] = o < 500 ? tf32f(p.w1[(size_t)o * 800 + k0 + tx]) : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = o0 + ty + 8 * u;
+      t[ty + 8 * u][tx] = v[u];
+      if (o < 500) p.w1f[(size_t)o * 800 + k0 + tx] = v[u];
     }
     __syncthreads();
     for (int y = ty; y < 32; y += 8) p.w1t[(size_t)(k0 + y) * 512 + o0 + tx] = t[tx][y];
