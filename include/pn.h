@@ -167,7 +167,7 @@ pn_status net_train_step_u8(pn_net* net, const uint8_t* x8,
                             int64_t iter, float* loss, void* stream);
 /* nsteps consecutive training steps from HOST byte batches (the end-to-end
  * data path): batch s is x8_host[s*N*C*H*W ...], labels_host[s*N ...]
- * (pinned memory for overlap).  Double-buffered: the host->device copy of
+ * (pinned memory for overlap).  Three device input slots: the host->device copy of
  * batch s+1 runs on a library copy stream while step s computes; step s's
  * loss is copied back to losses_host[s].  Iterations iter0 .. iter0+nsteps-1.
  * Synchronises `stream` before returning. */

@@ -205,13 +205,14 @@ struct pn_net {
   float x_scale = 1.f / 256.f;
   float* x_mean = nullptr;    // [C*H*W] device, or null
   float* xin = nullptr;       // fp32 input written by the ingest kernel (layerwise plans)
-  uint8_t* h2d_x8[2] = {nullptr, nullptr};  // pipelined host input: device slots
-  int32_t* h2d_y[2] = {nullptr, nullptr};
+  static constexpr int kSlots = 3;  // pipelined host input: device slots (copies run up to 2 steps ahead)
+  uint8_t* h2d_x8[kSlots] = {};
+  int32_t* h2d_y[kSlots] = {};
   float* h2d_loss = nullptr;  // [2]
   float* loss_pinned = nullptr;  // host (pinned) per-step losses of the pipelined loop
   int64_t loss_pinned_cap = 0;
   cudaStream_t copy = nullptr;
-  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copied[kSlots] = {}, ev_used[kSlots] = {};
   float* da1r = nullptr;      // [N][500]
   float* da1rT = nullptr;     // [500][npad]
   float* part_b1 = nullptr;   // [splits][500]  ip1 bias-gradient partials
@@ -228,7 +229,7 @@ struct pn_net {
   // captured graphs: the train step, forward-only inference, and one train
   // step per input slot of the pipelined host loop (their arguments then
   // differ only in the learning rate)
-  GraphExec step, infer, slot[2];
+  GraphExec step, infer, slot[kSlots];
   int launches_per_step = 0;
 
   // data parallel
@@ -1236,8 +1237,7 @@ static pn_status replay(pn_net* net, int nph, const StepArgs& a, GraphExec& E, c
 static void drop_graphs(pn_net* net) {
   net->step.drop();
   net->infer.drop();
-  net->slot[0].drop();
-  net->slot[1].drop();
+  for (auto& g : net->slot) g.drop();
 }
 
 
@@ -1321,9 +1321,12 @@ extern "C" void net_destroy(pn_net* net) {
   if (net->cap) cudaStreamDestroy(net->cap);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
-  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join, net->ev_copied[0],
-                        net->ev_copied[1], net->ev_used[0], net->ev_used[1]})
+  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join})
     if (e) cudaEventDestroy(e);
+  for (int b = 0; b < pn_net::kSlots; ++b) {
+    if (net->ev_copied[b]) cudaEventDestroy(net->ev_copied[b]);
+    if (net->ev_used[b]) cudaEventDestroy(net->ev_used[b]);
+  }
   if (net->side) cudaStreamDestroy(net->side);
   if (net->copy) cudaStreamDestroy(net->copy);
   if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
@@ -1602,15 +1605,15 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
   const int64_t nx = input_count(net);
   if (!net->copy) {
     CU(cudaStreamCreateWithFlags(&net->copy, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < pn_net::kSlots; ++b) {
       CU(cudaEventCreateWithFlags(&net->ev_copied[b], cudaEventDisableTiming));
       CU(cudaEventCreateWithFlags(&net->ev_used[b], cudaEventDisableTiming));
       TRY(net->alloc(&net->h2d_x8[b], (size_t)nx));
       TRY(net->alloc(&net->h2d_y[b], (size_t)net->batch));
     }
-    TRY(net->alloc(&net->h2d_loss, 2));
+    TRY(net->alloc(&net->h2d_loss, pn_net::kSlots));
     // the slots start free
-    for (int b = 0; b < 2; ++b) CU(cudaEventRecord(net->ev_used[b], st));
+    for (int b = 0; b < pn_net::kSlots; ++b) CU(cudaEventRecord(net->ev_used[b], st));
   }
   if (net->loss_pinned_cap < nsteps) {  // the D2H loss reads land in pinned memory (asynchronous)
     if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
@@ -1619,9 +1622,9 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
     CU(cudaMallocHost(&net->loss_pinned, nsteps * sizeof(float)));
     net->loss_pinned_cap = nsteps;
   }
-  // double buffering: the copy of batch s+1 (copy stream) overlaps step s
+  // kSlots input slots: the copies of the next batches (copy stream) run under step s
   for (int64_t s = 0; s < nsteps; ++s) {
-    const int b = (int)(s & 1);
+    const int b = (int)(s % pn_net::kSlots);
     CU(cudaStreamWaitEvent(net->copy, net->ev_used[b], 0));  // step s-2 is done with slot b
     CU(cudaMemcpyAsync(net->h2d_x8[b], x8_host + s * nx, nx, cudaMemcpyHostToDevice, net->copy));
     CU(cudaMemcpyAsync(net->h2d_y[b], labels_host + s * net->batch, net->batch * 4, cudaMemcpyHostToDevice,
