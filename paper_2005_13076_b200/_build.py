@@ -46,7 +46,8 @@ def needs_build():
 def _compile(src, verbose):
     obj = os.path.join(BUILD, os.path.basename(src) + ".o")
     nd = nccl_dir()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
+    extra = os.environ.get("PN_NVCC_FLAGS", "").split()  # dev A/B builds (e.g. -DCF_STAGES=2)
+    cmd = [NVCC, *ARCH, *extra, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
            "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I",
            os.path.join(nd, "include"), "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)

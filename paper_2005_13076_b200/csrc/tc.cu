@@ -51,6 +51,19 @@ namespace tc {
 // operand bytes the cost: the split halves them, and the 8-KB exchange is
 // the cheapest reduction (a 128 x 128 split-K tile over DSMEM at ~20 B/clk
 // was the bottleneck of the previous design).
+// ring depths (compile-time knobs for A/B builds, tools/ab_build.sh)
+#ifndef IPF_STAGES
+#define IPF_STAGES 4
+#endif
+#ifndef IPG_STAGES
+#define IPG_STAGES 5
+#endif
+#ifndef IPD_STAGES
+#define IPD_STAGES 5
+#endif
+#ifndef WG_SLOTS
+#define WG_SLOTS 6
+#endif
 namespace ipk {
 constexpr int THREADS = 192, BN = 32, CP = 33;  // C pitch (floats)
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -198,7 +211,7 @@ struct IpFwd {
     float* y;
     int M, K, Nout;
   };
-  static constexpr int RED_FLOATS = 0, STAGES = 4, EPI_BYTES = 0, SPLIT = 2;
+  static constexpr int RED_FLOATS = 0, STAGES = IPF_STAGES, EPI_BYTES = 0, SPLIT = 2;
   static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int m0, o0;
@@ -234,7 +247,7 @@ struct IpWgrad {
     float* dw;
     int M, K, Nout;  // M = batch (contraction), K = 800 (cols), Nout = 500 (rows)
   };
-  static constexpr int RED_FLOATS = 0, STAGES = 5, EPI_BYTES = 0, SPLIT = 1;
+  static constexpr int RED_FLOATS = 0, STAGES = IPG_STAGES, EPI_BYTES = 0, SPLIT = 1;
   static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int o0, k0;
@@ -273,7 +286,7 @@ struct IpDgradUnpool {
     float* part_db2;    // [row tiles * 2][50]
     int N;
   };
-  static constexpr int SPLIT = 1, ROWS = 128 / SPLIT, STAGES = 5;
+  static constexpr int SPLIT = 1, ROWS = 128 / SPLIT, STAGES = IPD_STAGES;
   static constexpr int RED_FLOATS = 2 * ROWS;  // red: [filter in tile][owned row]
   static constexpr int EPI_BYTES = ROWS * 32;  // the owned rows' pool2 origins [row][2 x 16]
   static constexpr bool A_EARLY = true, B_EARLY = true;
@@ -347,6 +360,9 @@ struct IpDgradUnpool {
 // TMEM accumulators), warps 2-5 = epilogue: TMEM -> smem tile C[row][f] (bank
 // skewed), then one thread per pooled (f, ph, pw) for both images: bias,
 // 2x2 max with the first-max mask, TF32 p2, its transpose p2T, the mask.
+#ifndef CF_STAGES
+#define CF_STAGES 2  // pair stages of conv2's forward (2: fits beside a conv1+pool1 block)
+#endif
 namespace cf {
 constexpr int PLANE = 12 * 2 * 12 * 16;        // [h][n][w][4 c] of one pair = 4608 B
 constexpr int A_BYTES = 6 * PLANE;             // 24 channels per stage
@@ -355,7 +371,7 @@ constexpr int TAP_BYTES = 5 * 800;             // [cc 5][f 50][4 c]
 constexpr int B_BYTES = 99 * 1024;             // 25 taps + >= 1024 B zero pad
 constexpr int C_PITCH = 50;                    // floats per C row (+ skew below)
 constexpr int C_BYTES = 25 * 1024 + 1024;      // 128 x 50 floats + max skew
-constexpr int STAGES = 3;
+constexpr int STAGES = CF_STAGES;
 constexpr int THREADS_F = 192;
 constexpr int SMEM = B_BYTES + STAGES * A_BYTES + C_BYTES + 1024;
 static_assert(25 * TAP_BYTES + 1024 <= B_BYTES, "B pad");
@@ -745,7 +761,7 @@ constexpr int WARPS = 10, THREADS_W = WARPS * 32, NB = 256;  // A builder thread
 constexpr int A_BYTES = 2 * 128 * 128;   // 2 K-chunks (32 positions each) x 128 rows x 128 B
 constexpr int G_BYTES = 2 * 64 * 128;    // 2 K-chunks x 64 f rows x 128 B
 constexpr int P_BYTES = 6 * 144 * 4;     // <= 6 input channels of one image
-constexpr int SLOTS = 6;  // images in flight
+constexpr int SLOTS = WG_SLOTS;  // images in flight
 constexpr int SMEM = 2 * A_BYTES + SLOTS * G_BYTES + SLOTS * P_BYTES + 1024;
 struct Params {
   CUtensorMap tg;  // G2 as {64 p, 50 f, N n}
