@@ -39,4 +39,10 @@ __global__ void lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p);
 
 constexpr int kGemmTile = 64;
 constexpr int kWgradSplits = 32;
+// conv1 + pool1 (SIMT): filters per thread (2 or 4; compile-time knob for A/B
+// builds) and the block size that covers conv1's 20 filters with one warp per group
+#ifndef C1_FPT
+#define C1_FPT 4
+#endif
+constexpr int C1_THREADS = 32 * (20 / C1_FPT);
 }  // namespace pn

@@ -46,7 +46,8 @@ __device__ __forceinline__ float in_x(const float* x, const uint8_t* x8, float s
 }
 
 constexpr int C1_MAXIMG = 4;  // images a block's item range can touch
-__global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+constexpr int C1_PAIRS = C1_FPT / 2;    // filter pairs per thread (one FFMA2 lane pair each)
+__global__ void __launch_bounds__(C1_THREADS, 2) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
   // everything read here (the batch, conv1's weights from the previous
   // step's SGD) is complete at launch and the predecessor (the TF32 weight
   // packing) touches none of it: run alongside it, wait only at the end
@@ -59,32 +60,39 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constan
   }
   const int nlo = i0 / 144, nimg = (i1 - 1) / 144 - nlo + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int f0 = 2 * warp;
+  const int f0 = C1_FPT * warp;  // this warp's filters f0 .. f0 + C1_FPT - 1
   {  // every load of the staging issued before the first store (one HBM round trip)
-    constexpr int PER = (C1_MAXIMG * 784 + 319) / 320;
+    constexpr int PER = (C1_MAXIMG * 784 + C1_THREADS - 1) / C1_THREADS;
     float v[PER];
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + 320 * k;
+      const int i = threadIdx.x + C1_THREADS * k;
       v[k] = i < nimg * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i) : 0.f;
     }
 #pragma unroll
     for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + 320 * k;
+      const int i = threadIdx.x + C1_THREADS * k;
       if (i < nimg * 784) xs[i / 784][i % 784] = v[k];
     }
   }
-  unsigned long long wp[25];
+  unsigned long long wp[C1_PAIRS][25];
+  float bias[C1_FPT];
 #pragma unroll
-  for (int t = 0; t < 25; ++t) wp[t] = pk2(__ldg(p.w + f0 * 25 + t), __ldg(p.w + (f0 + 1) * 25 + t));
-  const float b0 = __ldg(p.b + f0), b1 = __ldg(p.b + f0 + 1);
+  for (int g = 0; g < C1_PAIRS; ++g)
+#pragma unroll
+    for (int t = 0; t < 25; ++t)
+      wp[g][t] = pk2(__ldg(p.w + (f0 + 2 * g) * 25 + t), __ldg(p.w + (f0 + 2 * g + 1) * 25 + t));
+#pragma unroll
+  for (int h = 0; h < C1_FPT; ++h) bias[h] = __ldg(p.b + f0 + h);
   __syncthreads();
 #pragma unroll 1
   for (int it = i0 + lane; it < i1; it += 32) {
     const int n = it / 144, q = it - n * 144, im = n - nlo;
     const int ph = q / 12, pw = q - ph * 12;
     const float* xp = &xs[im][(2 * ph) * 28 + 2 * pw];
-    unsigned long long acc[2][2] = {{0ull, 0ull}, {0ull, 0ull}};
+    unsigned long long acc[C1_PAIRS][2][2];
+#pragma unroll
+    for (int g = 0; g < C1_PAIRS; ++g) acc[g][0][0] = acc[g][0][1] = acc[g][1][0] = acc[g][1][1] = 0ull;
     float r0[6], r1[6], r2[6];
 #pragma unroll
     for (int c = 0; c < 6; ++c) {
@@ -98,24 +106,30 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constan
         for (int c = 0; c < 6; ++c) r2[c] = xp[(i + 2) * 28 + c];
       }
 #pragma unroll
-      for (int j = 0; j < 5; ++j) {
-        fma2(acc[0][0], r0[j], wp[i * 5 + j]);
-        fma2(acc[0][1], r0[j + 1], wp[i * 5 + j]);
-        fma2(acc[1][0], r1[j], wp[i * 5 + j]);
-        fma2(acc[1][1], r1[j + 1], wp[i * 5 + j]);
-      }
+      for (int j = 0; j < 5; ++j)
+#pragma unroll
+        for (int g = 0; g < C1_PAIRS; ++g) {
+          fma2(acc[g][0][0], r0[j], wp[g][i * 5 + j]);
+          fma2(acc[g][0][1], r0[j + 1], wp[g][i * 5 + j]);
+          fma2(acc[g][1][0], r1[j], wp[g][i * 5 + j]);
+          fma2(acc[g][1][1], r1[j + 1], wp[g][i * 5 + j]);
+        }
 #pragma unroll
       for (int c = 0; c < 6; ++c) {
         r0[c] = r1[c];
         r1[c] = r2[c];
       }
     }
-    float v[2];
+    float v[C1_FPT];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {  // filter f0 + h
-      const float bb = h ? b1 : b0;
-      const float c00 = (h ? hi32(acc[0][0]) : lo32(acc[0][0])) + bb, c01 = (h ? hi32(acc[0][1]) : lo32(acc[0][1])) + bb;
-      const float c10 = (h ? hi32(acc[1][0]) : lo32(acc[1][0])) + bb, c11 = (h ? hi32(acc[1][1]) : lo32(acc[1][1])) + bb;
+    for (int h = 0; h < C1_FPT; ++h) {  // filter f0 + h (pair h / 2, lane pair half h % 2)
+      const int g = h >> 1;
+      const bool hi = h & 1;
+      const float bb = bias[h];
+      const float c00 = (hi ? hi32(acc[g][0][0]) : lo32(acc[g][0][0])) + bb;
+      const float c01 = (hi ? hi32(acc[g][0][1]) : lo32(acc[g][0][1])) + bb;
+      const float c10 = (hi ? hi32(acc[g][1][0]) : lo32(acc[g][1][0])) + bb;
+      const float c11 = (hi ? hi32(acc[g][1][1]) : lo32(acc[g][1][1])) + bb;
       float best = c00;
       int off = 0;
       if (c01 > best) { best = c01; off = 1; }
@@ -127,9 +141,13 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_pool1(const __grid_constan
       p.p1[o] = v[h];
       p.m1[o] = (uint8_t)off;
     }
-    if (p.p1c)  // [pair][cc][h][n][w][4 c]: this thread's two channels are adjacent
-      *reinterpret_cast<float2*>(p.p1c + ((size_t)(n >> 1) * 1440 + ((f0 >> 2) * 12 + ph) * 24 + (n & 1) * 12 + pw) * 4 +
-                                 (f0 & 3)) = make_float2(v[0], v[1]);
+    if (p.p1c) {  // [pair][cc][h][n][w][4 c]: this thread's channels are adjacent
+      float* d = p.p1c + ((size_t)(n >> 1) * 1440 + ((f0 >> 2) * 12 + ph) * 24 + (n & 1) * 12 + pw) * 4 + (f0 & 3);
+      if (C1_FPT == 4)
+        *reinterpret_cast<float4*>(d) = make_float4(v[0], v[1], v[C1_FPT > 2 ? 2 : 0], v[C1_FPT > 2 ? 3 : 1]);
+      else
+        *reinterpret_cast<float2*>(d) = make_float2(v[0], v[1]);
+    }
   }
   pdl_enter();
 }

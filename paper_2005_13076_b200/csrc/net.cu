@@ -897,7 +897,7 @@ static void build_fused_lenet(pn_net* net) {
     const int per = (int)cdiv((long long)N * 144, blocks);
     Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c, per};
     Launch l;
-    l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(320), 0, p);
+    l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(C1_THREADS), 0, p);
     add(fwd, "conv1+pool1", l, [net](Launch& l, const StepArgs& a) {
       Conv1Pool1P& q = l.params<Conv1Pool1P>();
       q.x = a.x, q.x8 = a.x8, q.x_scale = net->x_scale, q.x_mean = net->x_mean;
