@@ -445,7 +445,8 @@ def main():
     e2e = {"value": world * BATCH * e2e_steps / (ms_e2e / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "steps": e2e_steps, "path": e2e_kind}
 
-    # per-stage timing (CUDA events on the launching stream, eager steps)
+    # per-stage kernel durations (CUDA events on the launching stream around
+    # back-to-back launches of each stage: net_profile_stages)
     prof = net.net_profile_stages(X[0], Y[0], sgd, it, args.profile_steps)
     pk = peaks()
     tf32_peak = pk["bf16_sus"] * 1.1 / 2.25           # nominal TF32/BF16 ratio x measured sustained bf16

@@ -197,9 +197,13 @@ pn_status net_stage_name(const pn_net* net, int phase, int i,
                          const char** name);
 pn_status net_run_stage(pn_net* net, int phase, int i, const float* x,
                         const int32_t* labels, void* stream);
-/* Time `steps` eager training steps with CUDA events around every stage on
- * `stream`; ms_out[phase-major stage order] = mean milliseconds per launch.
- * Synchronises.  n_out: number of entries written (must be >= total stages). */
+/* Per-stage kernel durations on `stream`: one pass through the plan in order
+ * (x, labels, sgd, iter as for net_train_step); every forward / backward
+ * kernel stage is launched once, then `steps` times back to back between two
+ * CUDA events (each overwrites its outputs from inputs it does not write), so
+ * ms_out[phase-major stage order] = mean milliseconds per launch without
+ * per-launch host gaps; the solver and non-kernel stages run once.
+ * Synchronises.  n_out: number of entries written (cap >= total stages). */
 pn_status net_profile_stages(pn_net* net, const float* x,
                              const int32_t* labels, const pn_sgd* sgd,
                              int64_t iter, int steps, float* ms_out, int cap,
