@@ -393,11 +393,6 @@ __device__ __forceinline__ uint32_t c_addr(uint32_t C_s, int r, int f) {
 }
 }  // namespace cf
 
-// UMMA shared-memory descriptor: K-major, no swizzle, sm_100 version 1.
-__device__ __forceinline__ uint64_t make_desc_ns(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
-         ((uint64_t)1 << 46);
-}
 
 
 __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const __grid_constant__ cf::Params p) {
