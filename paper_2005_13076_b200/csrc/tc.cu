@@ -570,6 +570,9 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
 //               -> Gs, 2 buffers
 //   warps 6-9   epilogue: per image row h, TMEM -> smem scratch -> the
 //               j-sum -> dp1 (NCHW)
+#ifndef DG_RESTRICT
+#define DG_RESTRICT 1
+#endif
 namespace dg {
 constexpr int PLANES = 14;                          // 56 f (50 + zeros), 7 K steps of 8
 constexpr int AROWS = 104;                          // (c,j) rows 0..99 + 4 zero rows
@@ -646,12 +649,35 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
       if (it >= 2) mbar_wait(smem_u32(&accfree[b]), ((it >> 1) - 1) & 1);
       tc_fence_after();
       const uint64_t bd0 = make_desc_ns(G_s + b * G_BYTES, G_PLANE, 128);
+#if DG_RESTRICT
+      // kernel row 2 over all 12 output rows of both images (N = 192; its
+      // zero halo rows make it exact everywhere, and it initialises the
+      // accumulator), then rows 0, 1, 3, 4 only over the 8 output rows they
+      // reach, one image at a time (N = 64: B = the image's 8 real G2 rows,
+      // D columns from output row i): 27% fewer MMA cycles (floor ~ N)
+      constexpr uint32_t idesc64 = make_idesc(128, 64);
+#pragma unroll
+      for (int ks = 0; ks < PLANES / 2; ++ks)
+        mma_tf32(tbase + b * 256, ad0 + (uint64_t)((2 * A_TAP + ks * 2 * A_PLANE) >> 4),
+                 bd0 + (uint64_t)((2 * 128 + ks * 2 * G_PLANE) >> 4), idesc, ks != 0);
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        if (i == 2) continue;
+#pragma unroll
+        for (int n = 0; n < 2; ++n)
+#pragma unroll
+          for (int ks = 0; ks < PLANES / 2; ++ks)
+            mma_tf32(tbase + b * 256 + (n * 12 + i) * 8, ad0 + (uint64_t)((i * A_TAP + ks * 2 * A_PLANE) >> 4),
+                     bd0 + (uint64_t)(((4 + 12 * n) * 128 + ks * 2 * G_PLANE) >> 4), idesc64, 1u);
+      }
+#else
 #pragma unroll
       for (int i = 0; i < 5; ++i)
 #pragma unroll
         for (int ks = 0; ks < PLANES / 2; ++ks)
           mma_tf32(tbase + b * 256, ad0 + (uint64_t)((i * A_TAP + ks * 2 * A_PLANE) >> 4),
                    bd0 + (uint64_t)(((4 - i) * 128 + ks * 2 * G_PLANE) >> 4), idesc, (i | ks) != 0);
+#endif
       mma_commit(smem_u32(&gfree[b]));
       mma_commit(smem_u32(&accfull[b]));
       if (it < 2) stamp(3 + 2 * it);  // MMAs issued
