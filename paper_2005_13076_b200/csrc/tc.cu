@@ -64,8 +64,26 @@ namespace tc {
 #ifndef WG_SLOTS
 #define WG_SLOTS 6
 #endif
+#ifndef IPF_SPLIT
+#define IPF_SPLIT 4
+#endif
+#ifndef IPF_BN
+#define IPF_BN 64
+#endif
+#ifndef IPD_SPLIT
+#define IPD_SPLIT 1
+#endif
+#ifndef IPD_BN
+#define IPD_BN 32
+#endif
+#ifndef IPG_SPLIT
+#define IPG_SPLIT 1
+#endif
+#ifndef IPG_BN
+#define IPG_BN 32
+#endif
 namespace ipk {
-constexpr int THREADS = 192, BN = 32, CP = 33;  // C pitch (floats)
+constexpr int THREADS = 192;
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -86,8 +104,10 @@ __device__ __forceinline__ float ld_cluster(uint32_t local_addr, uint32_t rank) 
 template <class Op>
 __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant__ typename Op::Params prm) {
   using namespace ipk;
+  constexpr int BN = Op::BN, CPB = BN + 1;  // tile width, C pitch (floats)
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES, STAGES = Op::STAGES;
-  static_assert(128 * CP * 4 <= STAGES * STAGE, "C fits the ring");
+  static_assert(128 * CPB * 4 <= STAGES * STAGE, "C fits the ring");
+  static_assert(BN == 32 || BN == 64 || BN == 128, "tile width");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], done;
@@ -95,7 +115,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   __shared__ float red[Op::RED_FLOATS + 1];
   __shared__ __align__(16) uint8_t epi_s[Op::EPI_BYTES + 16];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int SPLIT = Op::SPLIT, ROWS = 128 / SPLIT;  // K halves over a CTA pair, or the whole K
+  constexpr int SPLIT = Op::SPLIT, ROWS = 128 / SPLIT;  // K split over a cluster of SPLIT CTAs, or the whole K
   const uint32_t rank = SPLIT > 1 ? cluster_rank() : 0u;  // cluster = (SPLIT, 1, 1): blockIdx.x = SPLIT * column + rank
   Op op(prm);
   const int nk = op.num_k_chunks(), c0 = (int)rank * nk / SPLIT, my = ((int)rank + 1) * nk / SPLIT - c0;
@@ -109,7 +129,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
     fence_barrier_init();
     op.prefetch();
   }
-  if (warp == 0) tmem_alloc(&tmem_base, 32);
+  if (warp == 0) tmem_alloc(&tmem_base, BN);
   op.stage_epilogue(tid, epi_s, (int)rank);  // epilogue inputs from >= 2 launches back
   tc_fence_before();
   __syncthreads();
@@ -154,51 +174,60 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   } else if (warp >= 2) {
     // TMEM -> C over the drained ring (all MMAs retired)
     const int quad = warp & 3, row = quad * 32 + lane;
-    float v[32];
     if (my > 0) {
       mbar_wait(smem_u32(&done), 0);
       if (warp == 2 && lane == 0) stamp(2);
       __syncwarp();
       tc_fence_after();
-      tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16), *reinterpret_cast<float(*)[16]>(v));
-      tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + 16, *reinterpret_cast<float(*)[16]>(v + 16));
-      tmem_ld_wait();
-    } else {  // an empty K half (tiny K): a zero partial
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = 0.f;
     }
 #pragma unroll
-    for (int j = 0; j < 32; ++j) stsf(sbase + 4 * (row * CP + j), v[j]);
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      float v[32];
+      if (my > 0) {
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + c0, *reinterpret_cast<float(*)[16]>(v));
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + c0 + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+        tmem_ld_wait();
+      } else {  // an empty K slice (tiny K): a zero partial
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stsf(sbase + 4 * (row * CPB + c0 + j), v[j]);
+    }
   }
   tc_fence_before();
   if (SPLIT > 1) {
-    cluster_sync();  // both partial tiles complete
+    cluster_sync();  // every partial tile of the cluster complete
     if (tid == 0) stamp(3);
-    // rows [64 rank, +64): partial of CTA 0 + partial of CTA 1, in place in the
-    // local C (the peer never reads this CTA's own rows)
-    const uint32_t peer = rank ^ 1u;
+    // rows [ROWS rank, +ROWS): the SPLIT partials summed in rank order, in
+    // place in the local C (no other CTA reads this CTA's own rows)
     for (int u = tid; u < ROWS * BN; u += THREADS) {
-      const int r = ROWS * (int)rank + (u >> 5), col = u & 31;
-      const uint32_t addr = sbase + 4 * (r * CP + col);
-      const float mine = ldsf(addr), other = ld_cluster(addr, peer);
-      stsf(addr, rank == 0 ? mine + other : other + mine);
+      const int r = ROWS * (int)rank + u / BN, col = u % BN;
+      const uint32_t addr = sbase + 4 * (r * CPB + col);
+      float t[SPLIT];
+#pragma unroll
+      for (int q = 0; q < SPLIT; ++q) t[q] = q == (int)rank ? ldsf(addr) : ld_cluster(addr, (uint32_t)q);
+      float acc = t[0];
+#pragma unroll
+      for (int q = 1; q < SPLIT; ++q) acc += t[q];
+      stsf(addr, acc);
     }
-    cluster_sync();  // the peer's reads of this CTA's C are done; local sums visible
+    cluster_sync();  // the other CTAs' reads of this CTA's C are done; local sums visible
   } else {
     __syncthreads();
   }
-  // the layer's epilogue: two threads per owned row, 16 columns each
-  for (int u = tid; u < 2 * ROWS; u += THREADS) {
+  // the layer's epilogue: BN / 16 threads per owned row, 16 columns each
+  for (int u = tid; u < (BN / 16) * ROWS; u += THREADS) {
     const int rr = u % ROWS, half = u / ROWS, r = ROWS * (int)rank + rr;
     float v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = ldsf(sbase + 4 * (r * CP + 16 * half + j));
+    for (int j = 0; j < 16; ++j) v[j] = ldsf(sbase + 4 * (r * CPB + 16 * half + j));
     op.store(r, rr, half, v, red, epi_s);
   }
   __syncthreads();
   if (tid == 0) stamp(4);
   op.finish(tid, red, (int)rank);
-  if (warp == 0) tmem_dealloc(tbase, 32);
+  if (warp == 0) tmem_dealloc(tbase, BN);
 }
 
 // y[n,o] = relu(sum_k p2[n,k] W1[o,k] + b[o]): rows n, cols o (16 tiles of
@@ -211,11 +240,11 @@ struct IpFwd {
     float* y;
     int M, K, Nout;
   };
-  static constexpr int RED_FLOATS = 0, STAGES = IPF_STAGES, EPI_BYTES = 0, SPLIT = 2;
+  static constexpr int RED_FLOATS = 0, STAGES = IPF_STAGES, EPI_BYTES = 0, SPLIT = IPF_SPLIT, BN = IPF_BN;
   static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int m0, o0;
-  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * ipk::BN) {}
+  __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
@@ -247,11 +276,11 @@ struct IpWgrad {
     float* dw;
     int M, K, Nout;  // M = batch (contraction), K = 800 (cols), Nout = 500 (rows)
   };
-  static constexpr int RED_FLOATS = 0, STAGES = IPG_STAGES, EPI_BYTES = 0, SPLIT = 1;
+  static constexpr int RED_FLOATS = 0, STAGES = IPG_STAGES, EPI_BYTES = 0, SPLIT = IPG_SPLIT, BN = IPG_BN;
   static constexpr bool A_EARLY = false, B_EARLY = true;
   const Params& p;
   int o0, k0;
-  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * ipk::BN) {}
+  __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, o0, bar); }
@@ -286,23 +315,23 @@ struct IpDgradUnpool {
     float* part_db2;    // [row tiles * 2][50]
     int N;
   };
-  static constexpr int SPLIT = 1, ROWS = 128 / SPLIT, STAGES = IPD_STAGES;
-  static constexpr int RED_FLOATS = 2 * ROWS;  // red: [filter in tile][owned row]
-  static constexpr int EPI_BYTES = ROWS * 32;  // the owned rows' pool2 origins [row][2 x 16]
+  static constexpr int SPLIT = IPD_SPLIT, ROWS = 128 / SPLIT, STAGES = IPD_STAGES, BN = IPD_BN, FT = BN / 16;
+  static constexpr int RED_FLOATS = FT * ROWS;  // red: [filter in tile][owned row]
+  static constexpr int EPI_BYTES = ROWS * BN;   // the owned rows' pool2 origins [row][FT x 16]
   static constexpr bool A_EARLY = true, B_EARLY = true;
   const Params& p;
   int m0, k0;
-  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * ipk::BN) {}
+  __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
   __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
   __device__ void stage_epilogue(int tid, uint8_t* es, int rank) {  // conv2's forward wrote them, many launches back
-    for (int u = tid; u < 2 * ROWS; u += ipk::THREADS) {
+    for (int u = tid; u < FT * ROWS; u += ipk::THREADS) {
       const int rr = u % ROWS, half = u / ROWS, n = m0 + ROWS * rank + rr;
       uint4 m = make_uint4(0, 0, 0, 0);
       if (n < p.N && k0 + 16 * half < 800) m = __ldg(reinterpret_cast<const uint4*>(p.m2 + (size_t)n * 800 + k0) + half);
-      reinterpret_cast<uint4*>(es)[rr * 2 + half] = m;
+      reinterpret_cast<uint4*>(es)[rr * FT + half] = m;
     }
   }
   __device__ void store(int row, int rr, int half, const float (&v)[16], float* red, const uint8_t* es) const {
@@ -312,7 +341,7 @@ struct IpDgradUnpool {
     for (int q = 0; q < 16; ++q) sum += v[q];
     red[half * ROWS + rr] = n < p.N ? sum : 0.f;
     if (n >= p.N || f >= 50) return;
-    const uint4 mk = reinterpret_cast<const uint4*>(es)[rr * 2 + half];
+    const uint4 mk = reinterpret_cast<const uint4*>(es)[rr * FT + half];
     const uint32_t mw[4] = {mk.x, mk.y, mk.z, mk.w};
     float* g = p.g2 + ((size_t)n * 50 + f) * 64;
 #pragma unroll
@@ -330,7 +359,7 @@ struct IpDgradUnpool {
   }
   __device__ void finish(int tid, const float* red, int rank) const {
     const int f = (k0 >> 4) + tid;
-    if (tid < 2 && f < 50) {  // fixed-order sum over the CTA's rows
+    if (tid < FT && f < 50) {  // fixed-order sum over the CTA's rows
       float s = 0.f;
       for (int r = 0; r < ROWS; ++r) s += red[tid * ROWS + r];
       p.part_db2[((size_t)blockIdx.y * SPLIT + rank) * 50 + f] = s;
@@ -1063,7 +1092,7 @@ static CUtensorMap tmap_g2(const float* base, uint64_t N) {
 
 template <class Op>
 static constexpr size_t ip_smem() {  // the ring + 1 KB alignment slack
-  return (size_t)Op::STAGES * (128 * 128 + ipk::BN * 128) + 1024;
+  return (size_t)Op::STAGES * (128 * 128 + Op::BN * 128) + 1024;
 }
 template <class Op>
 static cudaError_t opt_in() {
@@ -1119,8 +1148,8 @@ Launch pack_p1c_launch(const float* p1, float* p1c, int N) {
 
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N) {
   Launch l;
-  IpFwd::Params p{tmap2d(p2, N, 800, 800, 128), tmap2d(w1f, 500, 800, 800, ipk::BN), b, y, N, 800, 500};
-  l.set((const void*)ip_tile<IpFwd>, dim3(IpFwd::SPLIT * cdiv(500, ipk::BN), cdiv(N, 128)), dim3(ipk::THREADS),
+  IpFwd::Params p{tmap2d(p2, N, 800, 800, 128), tmap2d(w1f, 500, 800, 800, IpFwd::BN), b, y, N, 800, 500};
+  l.set((const void*)ip_tile<IpFwd>, dim3(IpFwd::SPLIT * cdiv(500, IpFwd::BN), cdiv(N, 128)), dim3(ipk::THREADS),
         ip_smem<IpFwd>(), p);
   l.cluster = dim3(IpFwd::SPLIT, 1, 1);
   return l;
@@ -1128,8 +1157,8 @@ Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* 
 
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad) {
   Launch l;
-  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, ipk::BN), dw, N, 800, 500};
-  l.set((const void*)ip_tile<IpWgrad>, dim3(IpWgrad::SPLIT * cdiv(800, ipk::BN), cdiv(500, 128)), dim3(ipk::THREADS),
+  IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
+  l.set((const void*)ip_tile<IpWgrad>, dim3(IpWgrad::SPLIT * cdiv(800, IpWgrad::BN), cdiv(500, 128)), dim3(ipk::THREADS),
         ip_smem<IpWgrad>(), p);
   l.cluster = dim3(IpWgrad::SPLIT, 1, 1);
   return l;
@@ -1138,8 +1167,9 @@ Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, i
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N) {
   Launch l;
-  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, 128), tmap2d(w1t, 800, 512, 512, ipk::BN), m2, g2, part_db2, N};
-  l.set((const void*)ip_tile<IpDgradUnpool>, dim3(IpDgradUnpool::SPLIT * cdiv(800, ipk::BN), cdiv(N, 128)),
+  IpDgradUnpool::Params p{tmap2d(da1r, N, 500, 500, 128), tmap2d(w1t, 800, 512, 512, IpDgradUnpool::BN), m2, g2,
+                          part_db2, N};
+  l.set((const void*)ip_tile<IpDgradUnpool>, dim3(IpDgradUnpool::SPLIT * cdiv(800, IpDgradUnpool::BN), cdiv(N, 128)),
         dim3(ipk::THREADS), ip_smem<IpDgradUnpool>(), p);
   l.cluster = dim3(IpDgradUnpool::SPLIT, 1, 1);
   return l;
