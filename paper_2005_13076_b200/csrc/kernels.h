@@ -38,7 +38,15 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p);
 __global__ void lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p);
 
 constexpr int kGemmTile = 64;
-constexpr int kWgradSplits = 32;
+#ifndef KWG
+#define KWG 32
+#endif
+constexpr int kWgradSplits = KWG;
+// conv1 weight gradient (fused LeNet plan): images per block
+#ifndef CW_IMGS_DEF
+#define CW_IMGS_DEF 2
+#endif
+constexpr int CW_IMGS = CW_IMGS_DEF;
 // conv1 + pool1 (SIMT): filters per thread (2 or 4; compile-time knob for A/B
 // builds) and the block size that covers conv1's 20 filters with one warp per group
 #ifndef C1_FPT

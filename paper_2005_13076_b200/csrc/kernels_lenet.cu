@@ -417,7 +417,6 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // dp1 comes from conv2's data gradient two launches back (the predecessor,
 // conv2's weight gradient, produces nothing read here): the kernel runs
 // alongside it and waits only at the end (pdl.cuh).
-constexpr int CW_IMGS = 2;
 __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
   __shared__ float xs[CW_IMGS][784];
   const int s = blockIdx.x;

@@ -22,6 +22,10 @@
 #include "tc.h"
 #include "tc_conv.h"
 
+#ifndef WG2_SPLITS
+#define WG2_SPLITS 0  // conv2 weight-gradient image splits (0: SMs / 4; compile-time knob for A/B builds)
+#endif
+
 using namespace pn;
 
 // ------------------------------------------------------------------ errors
@@ -483,9 +487,10 @@ static pn_status allocate(pn_net* net) {
     if (L.off < 0) continue;
     // conv1's fused weight gradient is a light SIMT kernel: give it more
     // CTAs (2 images each)
-    L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + 1) / 2 : kWgradSplits;
+    L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + CW_IMGS - 1) / CW_IMGS : kWgradSplits;
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
-    if (net->fused && net->tf32 && &L == &net->layers[2]) L.splits = std::max(1, std::min(net->batch, net->tc_sms / 4));
+    if (net->fused && net->tf32 && &L == &net->layers[2])  // conv2 weight gradient: one CTA per SM (4 row tiles)
+      L.splits = std::max(1, std::min(net->batch, WG2_SPLITS > 0 ? WG2_SPLITS : net->tc_sms / 4));
     if (L.tc_conv) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
                                 net->tc_sms, L.G);
