@@ -47,6 +47,14 @@ constexpr int kWgradSplits = KWG;
 #define CW_IMGS_DEF 2
 #endif
 constexpr int CW_IMGS = CW_IMGS_DEF;
+// ip2 + softmax-loss: samples (warps) per block
+#ifndef IP2_SPB
+#define IP2_SPB 4
+#endif
+// SGD blocks per SM (grid-stride over float4 groups)
+#ifndef SGD_BPS
+#define SGD_BPS 8
+#endif
 // conv1 + pool1 (SIMT): filters per thread (2 or 4; compile-time knob for A/B
 // builds) and the block size that covers conv1's 20 filters with one warp per group
 #ifndef C1_FPT

@@ -239,26 +239,27 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
 // stable softmax, per-row loss term, lowest-index argmax and the loss
 // gradient dz = (p - onehot) * loss_weight / M.  The row's 125
 // float4 of a1 are all loaded up front (4 per lane).
-__global__ void __launch_bounds__(128) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
+__global__ void __launch_bounds__(IP2_SPB * 32) lenet_ip2_loss(const __grid_constant__ Ip2LossP p) {
+  constexpr int NT = IP2_SPB * 32, PER = (1250 + NT - 1) / NT;
   __shared__ __align__(16) float ws[10 * 500];
   __shared__ float bs[10];
-  {  // W2 as 1250 float4, all ten loads of a thread in flight together
-    float4 v[10];
+  {  // W2 as 1250 float4, all loads of a thread in flight together
+    float4 v[PER];
 #pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      const int i = threadIdx.x + 128 * k;
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + NT * k;
       v[k] = i < 1250 ? __ldg(reinterpret_cast<const float4*>(p.w) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
 #pragma unroll
-    for (int k = 0; k < 10; ++k) {
-      const int i = threadIdx.x + 128 * k;
+    for (int k = 0; k < PER; ++k) {
+      const int i = threadIdx.x + NT * k;
       if (i < 1250) reinterpret_cast<float4*>(ws)[i] = v[k];
     }
   }
   if (threadIdx.x < 10) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
   pdl_enter();
   const int lane = threadIdx.x & 31;
-  const int row = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int row = blockIdx.x * IP2_SPB + (threadIdx.x >> 5);
   float4 av[4];
 #pragma unroll
   for (int t = 0; t < 4; ++t) {

@@ -931,7 +931,7 @@ static void build_fused_lenet(pn_net* net) {
                net->blobs[net->blob("prob")].data, (int32_t*)net->blobs[net->blob("pred")].data, lg.diff,
                net->row_loss, net->err, N, 1.f / N};
     Launch l;
-    l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, 4)), dim3(128), 0, p);
+    l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, IP2_SPB)), dim3(IP2_SPB * 32), 0, p);
     add(fwd, "ip2+softmax_loss", l, [](Launch& l, const StepArgs& a) { l.params<Ip2LossP>().labels = a.labels; });
     add_loss(net, fwd);
   }
@@ -1033,7 +1033,7 @@ static void build_update(pn_net* net) {
   SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f};
   Launch l;
   long long n4 = net->nparams / 4;
-  l.set((const void*)sgd_update_kernel, dim3(std::max(1u, std::min(cdiv(n4, 256), 148u * 8))), dim3(256), 0, p);
+  l.set((const void*)sgd_update_kernel, dim3(std::max(1u, std::min(cdiv(n4, 256), 148u * SGD_BPS))), dim3(256), 0, p);
   add(net->phase[2], "sgd", l, [](Launch& l, const StepArgs& a) {
     SgdP& q = l.params<SgdP>();
     q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale;
