@@ -668,23 +668,24 @@ __device__ __forceinline__ void sgd_one(float& w, float d, float& v, float lr, f
 
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
   pdl_enter();
+  const float lr = p.lr_dev ? __ldg(p.lr_dev) : p.lr;
   long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long n4 = p.n / 4;
   for (; i4 < n4; i4 += (long long)gridDim.x * blockDim.x) {
     float4 w = reinterpret_cast<float4*>(p.w)[i4];
     float4 v = reinterpret_cast<float4*>(p.v)[i4];
     float4 g = reinterpret_cast<const float4*>(p.g)[i4];
-    sgd_one(w.x, g.x, v.x, p.lr, p.mom, p.decay, p.gscale);
-    sgd_one(w.y, g.y, v.y, p.lr, p.mom, p.decay, p.gscale);
-    sgd_one(w.z, g.z, v.z, p.lr, p.mom, p.decay, p.gscale);
-    sgd_one(w.w, g.w, v.w, p.lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.x, g.x, v.x, lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.y, g.y, v.y, lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.z, g.z, v.z, lr, p.mom, p.decay, p.gscale);
+    sgd_one(w.w, g.w, v.w, lr, p.mom, p.decay, p.gscale);
     reinterpret_cast<float4*>(p.w)[i4] = w;
     reinterpret_cast<float4*>(p.v)[i4] = v;
   }
   if (blockIdx.x == 0 && threadIdx.x < (p.n & 3)) {
     long long i = n4 * 4 + threadIdx.x;
     float w = p.w[i], v = p.v[i];
-    sgd_one(w, p.g[i], v, p.lr, p.mom, p.decay, p.gscale);
+    sgd_one(w, p.g[i], v, lr, p.mom, p.decay, p.gscale);
     p.w[i] = w;
     p.v[i] = v;
   }

@@ -212,7 +212,10 @@ struct pn_net {
   static constexpr int kSlots = 3;  // pipelined host input: device slots (copies run up to 2 steps ahead)
   uint8_t* h2d_x8[kSlots] = {};
   int32_t* h2d_y[kSlots] = {};
-  float* h2d_loss = nullptr;  // [2]
+  float* h2d_loss = nullptr;  // [kSlots]
+  float* h2d_lr = nullptr;    // [kSlots]: each slot's learning rate (its graph reads it: no per-step patch)
+  float* lr_pinned = nullptr; // host (pinned) learning rates of the steps of one call
+  int64_t lr_pinned_cap = 0;
   float* loss_pinned = nullptr;  // host (pinned) per-step losses of the pipelined loop
   int64_t loss_pinned_cap = 0;
   cudaStream_t copy = nullptr;
@@ -1030,13 +1033,13 @@ static void build_fused_lenet(pn_net* net) {
 }
 
 static void build_update(pn_net* net) {
-  SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f};
+  SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f, nullptr};
   Launch l;
   long long n4 = net->nparams / 4;
   l.set((const void*)sgd_update_kernel, dim3(std::max(1u, std::min(cdiv(n4, 256), 148u * SGD_BPS))), dim3(256), 0, p);
   add(net->phase[2], "sgd", l, [](Launch& l, const StepArgs& a) {
     SgdP& q = l.params<SgdP>();
-    q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale;
+    q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale; q.lr_dev = a.lr_dev;
   });
 }
 
@@ -1169,7 +1172,7 @@ static StepArgs make_args(pn_net* net, const float* x, const int32_t* labels, fl
 }
 
 static bool same_args(const StepArgs& a, const StepArgs& b) {
-  return a.x == b.x && a.x8 == b.x8 && a.labels == b.labels && a.loss == b.loss && a.lr == b.lr && a.mom == b.mom &&
+  return a.x == b.x && a.x8 == b.x8 && a.lr_dev == b.lr_dev && a.labels == b.labels && a.loss == b.loss && a.lr == b.lr && a.mom == b.mom &&
          a.decay == b.decay && a.gscale == b.gscale;
 }
 
@@ -1335,6 +1338,7 @@ extern "C" void net_destroy(pn_net* net) {
   if (net->side) cudaStreamDestroy(net->side);
   if (net->copy) cudaStreamDestroy(net->copy);
   if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
+  if (net->lr_pinned) cudaFreeHost(net->lr_pinned);
   for (void* p : net->allocs) cudaFree(p);
   delete net;
 }
@@ -1617,11 +1621,21 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
       TRY(net->alloc(&net->h2d_y[b], (size_t)net->batch));
     }
     TRY(net->alloc(&net->h2d_loss, pn_net::kSlots));
+    TRY(net->alloc(&net->h2d_lr, pn_net::kSlots));
     // the slots start free
     for (int b = 0; b < pn_net::kSlots; ++b) CU(cudaEventRecord(net->ev_used[b], st));
   }
+  if (net->lr_pinned_cap < nsteps) {  // the steps' learning rates, staged in pinned memory
+    if (net->lr_pinned) cudaFreeHost(net->lr_pinned);
+    net->lr_pinned = nullptr;
+    net->lr_pinned_cap = 0;
+    CU(cudaMallocHost(&net->lr_pinned, nsteps * sizeof(float)));
+    net->lr_pinned_cap = nsteps;
+  }
+  for (int64_t s = 0; s < nsteps; ++s) net->lr_pinned[s] = make_args(net, nullptr, nullptr, nullptr, sgd, iter0 + s).lr;
   if (net->loss_pinned_cap < nsteps) {  // the D2H loss reads land in pinned memory (asynchronous)
     if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
+  if (net->lr_pinned) cudaFreeHost(net->lr_pinned);
     net->loss_pinned = nullptr;
     net->loss_pinned_cap = 0;
     CU(cudaMallocHost(&net->loss_pinned, nsteps * sizeof(float)));
@@ -1634,9 +1648,12 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
     CU(cudaMemcpyAsync(net->h2d_x8[b], x8_host + s * nx, nx, cudaMemcpyHostToDevice, net->copy));
     CU(cudaMemcpyAsync(net->h2d_y[b], labels_host + s * net->batch, net->batch * 4, cudaMemcpyHostToDevice,
                        net->copy));
+    CU(cudaMemcpyAsync(net->h2d_lr + b, net->lr_pinned + s, 4, cudaMemcpyHostToDevice, net->copy));
     CU(cudaEventRecord(net->ev_copied[b], net->copy));
     CU(cudaStreamWaitEvent(st, net->ev_copied[b], 0));
     StepArgs a = make_args(net, nullptr, net->h2d_y[b], net->h2d_loss + b, sgd, iter0 + s);
+    a.lr = 0.f;  // read from the slot on the device instead: slot b's graph needs no patching
+    a.lr_dev = net->h2d_lr + b;
     TRY(byte_args(net, net->h2d_x8[b], a, st));
     TRY(replay(net, 3, a, net->slot[b], st));  // slot b's own graph: only the lr changes
     CU(cudaMemcpyAsync(net->loss_pinned + s, net->h2d_loss + b, 4, cudaMemcpyDeviceToHost, st));

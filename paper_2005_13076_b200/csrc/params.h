@@ -117,6 +117,7 @@ struct SgdP {  // S:536-544 Caffe SGD, fp32, no FMA
   float* v;
   long long n;
   float lr, mom, decay, gscale;
+  const float* lr_dev;  // if set: the learning rate is read from device memory (pipelined host loop)
 };
 struct Tf32CopyP {  // src [R][C] -> TF32-rounded copies: dst [R][C] and/or dstT [C][ldt]
   const float* src;

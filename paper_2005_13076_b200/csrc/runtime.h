@@ -21,6 +21,7 @@ struct StepArgs {
   const int32_t* labels = nullptr;
   float* loss = nullptr;
   float lr = 0.f, mom = 0.f, decay = 0.f, gscale = 1.f;
+  const float* lr_dev = nullptr;  // learning rate in device memory (then lr is unused)
 };
 
 // One kernel launch with its single __grid_constant__ parameter block.
