@@ -1635,7 +1635,6 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
   for (int64_t s = 0; s < nsteps; ++s) net->lr_pinned[s] = make_args(net, nullptr, nullptr, nullptr, sgd, iter0 + s).lr;
   if (net->loss_pinned_cap < nsteps) {  // the D2H loss reads land in pinned memory (asynchronous)
     if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
-  if (net->lr_pinned) cudaFreeHost(net->lr_pinned);
     net->loss_pinned = nullptr;
     net->loss_pinned_cap = 0;
     CU(cudaMallocHost(&net->loss_pinned, nsteps * sizeof(float)));
