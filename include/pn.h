@@ -167,10 +167,13 @@ pn_status net_train_step_u8(pn_net* net, const uint8_t* x8,
                             int64_t iter, float* loss, void* stream);
 /* nsteps consecutive training steps from HOST byte batches (the end-to-end
  * data path): batch s is x8_host[s*N*C*H*W ...], labels_host[s*N ...]
- * (pinned memory for overlap).  Three device input slots: the host->device copy of
- * batch s+1 runs on a library copy stream while step s computes; step s's
- * loss is copied back to losses_host[s].  Iterations iter0 .. iter0+nsteps-1.
- * Synchronises `stream` before returning. */
+ * (pinned memory for overlap).  Three device input slots: the host->device
+ * copies (bytes, labels, the step's learning rate) of the next batches run on
+ * a library copy stream while the current step computes; in the fused LeNet
+ * plan each three consecutive steps replay as one captured graph whose loss
+ * read-backs run on a side branch; step s's loss lands in losses_host[s].
+ * Iterations iter0 .. iter0+nsteps-1.  Synchronises `stream` before
+ * returning. */
 pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host,
                                   const int32_t* labels_host, int64_t nsteps,
                                   const pn_sgd* sgd, int64_t iter0,

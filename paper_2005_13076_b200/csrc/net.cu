@@ -237,6 +237,14 @@ struct pn_net {
   // step per input slot of the pipelined host loop (their arguments then
   // differ only in the learning rate)
   GraphExec step, infer, slot[kSlots];
+  // the pipelined loop's kSlots consecutive steps as ONE graph (one host launch
+  // per kSlots steps): waits on the slots' copy events, the steps, the per-step
+  // loss read-backs (destination patched per launch) and the slot-free events
+  cudaGraphExec_t multi = nullptr;
+  cudaGraph_t multi_g = nullptr;
+  cudaGraphNode_t multi_d2h[kSlots] = {};
+  cudaStream_t aux = nullptr;  // capture-side branch of the loss read-backs
+  cudaEvent_t ev_loss[kSlots] = {}, ev_aux = nullptr;
   int launches_per_step = 0;
 
   // data parallel
@@ -1246,6 +1254,10 @@ static void drop_graphs(pn_net* net) {
   net->step.drop();
   net->infer.drop();
   for (auto& g : net->slot) g.drop();
+  if (net->multi) cudaGraphExecDestroy(net->multi);
+  if (net->multi_g) cudaGraphDestroy(net->multi_g);
+  net->multi = nullptr;
+  net->multi_g = nullptr;
 }
 
 
@@ -1337,6 +1349,10 @@ extern "C" void net_destroy(pn_net* net) {
   }
   if (net->side) cudaStreamDestroy(net->side);
   if (net->copy) cudaStreamDestroy(net->copy);
+  if (net->aux) cudaStreamDestroy(net->aux);
+  for (cudaEvent_t e : net->ev_loss)
+    if (e) cudaEventDestroy(e);
+  if (net->ev_aux) cudaEventDestroy(net->ev_aux);
   if (net->loss_pinned) cudaFreeHost(net->loss_pinned);
   if (net->lr_pinned) cudaFreeHost(net->lr_pinned);
   for (void* p : net->allocs) cudaFree(p);
@@ -1640,8 +1656,85 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
     CU(cudaMallocHost(&net->loss_pinned, nsteps * sizeof(float)));
     net->loss_pinned_cap = nsteps;
   }
-  // kSlots input slots: the copies of the next batches (copy stream) run under step s
-  for (int64_t s = 0; s < nsteps; ++s) {
+  // slot b's step arguments (fixed device pointers; the learning rate rides in h2d_lr[b])
+  auto slot_args = [&](int b, int64_t s, StepArgs& a) -> pn_status {
+    a = make_args(net, nullptr, net->h2d_y[b], net->h2d_loss + b, sgd, iter0 + s);
+    a.lr = 0.f;
+    a.lr_dev = net->h2d_lr + b;
+    return byte_args(net, net->h2d_x8[b], a, st);
+  };
+  auto issue_copies = [&](int64_t s) -> pn_status {
+    const int b = (int)(s % pn_net::kSlots);
+    CU(cudaStreamWaitEvent(net->copy, net->ev_used[b], 0));  // step s - kSlots is done with slot b
+    CU(cudaMemcpyAsync(net->h2d_x8[b], x8_host + s * nx, nx, cudaMemcpyHostToDevice, net->copy));
+    CU(cudaMemcpyAsync(net->h2d_y[b], labels_host + s * net->batch, net->batch * 4, cudaMemcpyHostToDevice,
+                       net->copy));
+    CU(cudaMemcpyAsync(net->h2d_lr + b, net->lr_pinned + s, 4, cudaMemcpyHostToDevice, net->copy));
+    CU(cudaEventRecord(net->ev_copied[b], net->copy));
+    return PN_OK;
+  };
+  int64_t s0 = 0;
+  if (net->fused && nsteps >= pn_net::kSlots && !getenv("PN_NO_MULTI")) {
+    if (!net->multi) {  // capture the kSlots-step graph once (slot arguments never change)
+      if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
+      if (!net->aux) {
+        CU(cudaStreamCreateWithFlags(&net->aux, cudaStreamNonBlocking));
+        for (auto& e : net->ev_loss) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CU(cudaEventCreateWithFlags(&net->ev_aux, cudaEventDisableTiming));
+      }
+      CU(cudaStreamBeginCapture(net->cap, cudaStreamCaptureModeThreadLocal));
+      pn_status err = PN_OK;
+      bool prev_kernel = false;
+      for (int b = 0; b < pn_net::kSlots && err == PN_OK; ++b) {
+        StepArgs a;
+        if ((err = slot_args(b, b, a)) != PN_OK) break;
+        if (cudaStreamWaitEvent(net->cap, net->ev_copied[b], cudaEventWaitExternal) != cudaSuccess) { err = PN_ERR_CUDA; break; }
+        prev_kernel = false;
+        for (int ph = 0; ph < 3 && err == PN_OK; ++ph)
+          for (auto& stg : net->phase[ph]) {
+            cudaStream_t on = stg.side ? net->side : net->cap;
+            if ((err = run_stage(net, stg, a, on, stg.side ? false : prev_kernel)) != PN_OK) break;
+            if (!stg.side) prev_kernel = !stg.custom;
+          }
+        if (err != PN_OK) break;
+        // the loss read-back on a side branch (the next step does not wait for it)
+        if (cudaEventRecord(net->ev_loss[b], net->cap) != cudaSuccess ||
+            cudaStreamWaitEvent(net->aux, net->ev_loss[b], 0) != cudaSuccess ||
+            cudaMemcpyAsync(net->loss_pinned + b, net->h2d_loss + b, 4, cudaMemcpyDeviceToHost, net->aux) != cudaSuccess) {
+          err = PN_ERR_CUDA;
+          break;
+        }
+        cudaStreamCaptureStatus cs;
+        const cudaGraphNode_t* deps = nullptr;
+        size_t nd = 0;
+        if (cudaStreamGetCaptureInfo(net->aux, &cs, nullptr, nullptr, &deps, &nd) != cudaSuccess || nd == 0) { err = PN_ERR_CUDA; break; }
+        net->multi_d2h[b] = deps[0];
+        if (cudaEventRecordWithFlags(net->ev_used[b], net->cap, cudaEventRecordExternal) != cudaSuccess) { err = PN_ERR_CUDA; break; }
+      }
+      if (err == PN_OK && (cudaEventRecord(net->ev_aux, net->aux) != cudaSuccess ||
+                           cudaStreamWaitEvent(net->cap, net->ev_aux, 0) != cudaSuccess))
+        err = PN_ERR_CUDA;  // the read-backs join before the graph ends
+      cudaGraph_t g = nullptr;
+      const cudaError_t ce = cudaStreamEndCapture(net->cap, &g);
+      if (err != PN_OK || ce != cudaSuccess) {
+        if (g) cudaGraphDestroy(g);
+        return err != PN_OK ? err : fail(PN_ERR_CUDA, "capture of the pipelined steps failed");
+      }
+      CU(cudaGraphInstantiate(&net->multi, g, 0));
+      net->multi_g = g;
+    }
+    for (; s0 + pn_net::kSlots <= nsteps; s0 += pn_net::kSlots) {
+      for (int b = 0; b < pn_net::kSlots; ++b) TRY(issue_copies(s0 + b));
+      for (int b = 0; b < pn_net::kSlots; ++b)
+        CU(cudaGraphExecMemcpyNodeSetParams1D(net->multi, net->multi_d2h[b], net->loss_pinned + s0 + b,
+                                              net->h2d_loss + b, 4, cudaMemcpyDeviceToHost));
+      CU(cudaGraphLaunch(net->multi, st));
+    }
+    net->forward_done = true;
+  }
+  // the remaining steps one graph launch each (kSlots input slots: the copies
+  // of the next batches on the copy stream run under step s)
+  for (int64_t s = s0; s < nsteps; ++s) {
     const int b = (int)(s % pn_net::kSlots);
     CU(cudaStreamWaitEvent(net->copy, net->ev_used[b], 0));  // step s-2 is done with slot b
     CU(cudaMemcpyAsync(net->h2d_x8[b], x8_host + s * nx, nx, cudaMemcpyHostToDevice, net->copy));
