@@ -1,27 +1,24 @@
-// tc.cu -- tcgen05 TF32 implicit-GEMM kernels for the GEMM-shaped LeNet
-// layers.
+// tc.cu -- tcgen05 TF32 kernels for the GEMM-shaped LeNet layers (SURVEY
+// §8(a) rows a3/a4, a5/a6, a12/a13, a14) and the per-step TF32 weight packing.
 //
-// Engine (one CTA = one 128-row output tile, 8 warps):
-//   * every operand K-chunk (rows x 32 fp32) lives in a shared-memory ring in
-//     the UMMA canonical K-major SWIZZLE_128B layout (row = 128 B, 16-B chunk
-//     index XOR row%8, 8-row atoms of 1024 B; descriptor SBO = 1024 B, K step
-//     of 8 = +32 B).  MN-major TF32 descriptors were measured to produce zeros
-//     on this part (tools/umma_probe.cu), so every operand is K-major;
-//   * dense operands are moved by TMA (cp.async.bulk.tensor 2D/3D with
-//     128B swizzle, one elected thread, mbarrier complete_tx), LOOKAHEAD
-//     chunks ahead of the MMA.  They are already TF32 in global memory:
-//     packed weight copies (pack_weights) and activations stored rounded to
-//     nearest by their producing kernels -- the tensor
-//     core therefore never truncates;
-//   * implicit-im2col operands are gathered by all threads from activations
-//     staged in shared memory with cp.async.bulk, written with the same
-//     swizzle, then fence.proxy.async + __syncthreads;
-//   * one thread issues tcgen05.mma.cta_group::1.kind::tf32 (M=128, N=BN,
-//     K=8) x 4 per chunk into a TMEM accumulator and tcgen05.commit's the
-//     stage back (mbarrier);
-//   * the epilogue reads TMEM with tcgen05.ld 32x32b (thread = tile row;
-//     warps 4-7 take the upper half of the columns) and applies the layer's
-//     fused tail.
+// Common ground (the kernels below are warp-specialised variations on it):
+//   * every operand lives in shared memory in a UMMA K-major layout: the
+//     canonical SWIZZLE_128B one (row = 128 B of K, 16-B chunk index XOR
+//     row%8, 8-row atoms of 1 KB; SBO = 1 KB, K step of 8 = +32 B) when TMA
+//     delivers it, or the no-swizzle core-matrix one (8 rows x 16 B; LBO /
+//     SBO free) when a shifted descriptor must address a tap of a staged
+//     image (conv2's forward and data gradient).  MN-major TF32 descriptors
+//     were measured to produce zeros on this part (tools/umma_probe.cu);
+//   * operands are already TF32 in memory: packed weight copies
+//     (pack_weights) and activations rounded to nearest by their producers
+//      -- the tensor core never truncates;
+//   * one elected thread issues tcgen05.mma.cta_group::1.kind::tf32 (M=128,
+//     K=8) into TMEM accumulators and tcgen05.commit's stages back through
+//     mbarriers; TMA / bulk-copy producers, gather / build warps and TMEM
+//     epilogue warps (tcgen05.ld 32x32b, thread = tile row) run beside it;
+//   * kernels launch with programmatic dependent launch (pdl.cuh): inputs
+//     from two or more launches back are requested before the dependency
+//     wait.
 #include <cuda.h>
 
 #include <algorithm>

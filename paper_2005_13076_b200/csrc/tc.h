@@ -32,7 +32,8 @@ constexpr int kP1cPairFloats = 5 * 12 * 2 * 12 * 4;
 Launch conv2_pool2_launch(const float* w2c, const float* b, const float* p1c, float* p2, float* p2T, uint8_t* m2,
                           int N, int npad, int sms);
 Launch pack_p1c_launch(const float* p1, float* p1c, int N);
-// the three ip1 GEMMs split K over a thread-block cluster (reduction in DSMEM)
+// the three ip1 GEMMs as 128-row tiles (ip_tile<Op>: per-layer tile width and K
+// split over a cluster, partials reduced in DSMEM)
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N);
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
