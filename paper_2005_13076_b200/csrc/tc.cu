@@ -61,6 +61,9 @@ namespace tc {
 #ifndef WG_SLOTS
 #define WG_SLOTS 6
 #endif
+#ifndef PACK_GRID
+#define PACK_GRID 0  // weight-pack blocks (0: one per W1 tile)
+#endif
 #ifndef IPF_SPLIT
 #define IPF_SPLIT 4
 #endif
@@ -980,16 +983,19 @@ constexpr int W1_TILES = (800 / 32) * (512 / 32);  // 32 x 32 tiles of W1 (o pad
 // W2c and W2d element-wise.
 __global__ void pack_weights(const __grid_constant__ PackP p) {
   pdl_enter();
-  if (blockIdx.x < W1_TILES) {
-    __shared__ float t[32][33];
-    const int k0 = (blockIdx.x % 25) * 32, o0 = (blockIdx.x / 25) * 32;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  __shared__ float t[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
+  // W1 tiles (grid-stride: PACK_GRID > 0 runs the pack in fewer, longer blocks)
+#pragma unroll 1
+  for (int tile = blockIdx.x; tile < W1_TILES; tile += gridDim.x) {
+    const int k0 = (tile % 25) * 32, o0 = (tile / 25) * 32;
     float v[4];  // the tile's four rows per thread loaded together
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int o = o0 + ty + 8 * u;
       v[u] = o < 500 ? tf32f(p.w1[(size_t)o * 800 + k0 + tx]) : 0.f;
     }
+    __syncthreads();  // the previous tile's transpose reads are done
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int o = o0 + ty + 8 * u;
@@ -997,22 +1003,24 @@ __global__ void pack_weights(const __grid_constant__ PackP p) {
       if (o < 500) p.w1f[(size_t)o * 800 + k0 + tx] = v[u];
     }
     __syncthreads();
-    for (int y = ty; y < 32; y += 8) p.w1t[(size_t)(k0 + y) * 512 + o0 + tx] = t[tx][y];
-    return;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p.w1t[(size_t)(k0 + ty + 8 * u) * 512 + o0 + tx] = t[tx][ty + 8 * u];
   }
-  int idx = (blockIdx.x - W1_TILES) * blockDim.x + threadIdx.x;
-  if (idx < W2C_N) {
-    const int c4 = idx & 3, f = (idx >> 2) % 50, cc = (idx / 200) % 5, tap = idx / 1000;
-    p.w2c[idx] = tf32f(p.w2[f * 500 + (cc * 4 + c4) * 25 + tap]);
-    return;
-  }
-  idx -= W2C_N;
-  if (idx < W2T_N) {  // W2d[i][plane][(c,j)][4 f] (conv2 dgrad A), zero rows / filters / tail pad
-    const int q = idx & 3, r = (idx >> 2) % dg::AROWS, pl = (idx / (4 * dg::AROWS)) % dg::PLANES;
-    const int i = idx / (4 * dg::AROWS * dg::PLANES), f = 4 * pl + q, c = r / 5, j = r % 5;
-    float v = 0.f;
-    if (i < 5 && f < 50 && r < 100) v = p.w2[f * 500 + c * 25 + i * 5 + j];
-    p.w2t[idx] = tf32f(v);
+  // W2c and W2d element-wise, over all blocks
+  const int nb = gridDim.x, bx = blockIdx.x;
+#pragma unroll 1
+  for (int idx = bx * blockDim.x + threadIdx.x; idx < W2C_N + W2T_N; idx += nb * blockDim.x) {
+    if (idx < W2C_N) {
+      const int c4 = idx & 3, f = (idx >> 2) % 50, cc = (idx / 200) % 5, tap = idx / 1000;
+      p.w2c[idx] = tf32f(p.w2[f * 500 + (cc * 4 + c4) * 25 + tap]);
+    } else {  // W2d[i][plane][(c,j)][4 f] (conv2 dgrad A), zero rows / filters / tail pad
+      const int e = idx - W2C_N;
+      const int q = e & 3, r = (e >> 2) % dg::AROWS, pl = (e / (4 * dg::AROWS)) % dg::PLANES;
+      const int i = e / (4 * dg::AROWS * dg::PLANES), f = 4 * pl + q, c = r / 5, j = r % 5;
+      float v = 0.f;
+      if (i < 5 && f < 50 && r < 100) v = p.w2[f * 500 + c * 25 + i * 5 + j];
+      p.w2t[e] = tf32f(v);
+    }
   }
 }
 // p1c (conv2 forward operand, see conv2_fwd_persistent) from an NCHW pool1
@@ -1120,7 +1128,7 @@ static unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) /
 
 Launch pack_weights_launch(const PackP& p) {
   Launch l;
-  l.set((const void*)pack_weights, dim3(W1_TILES + cdiv(W2C_N + W2T_N, 256)), dim3(256), 0, p);
+  l.set((const void*)pack_weights, dim3(PACK_GRID > 0 ? PACK_GRID : W1_TILES), dim3(256), 0, p);
   return l;
 }
 
