@@ -12,6 +12,7 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p);
 __global__ void reduce_partials_multi(const __grid_constant__ ReduceMultiP p);
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p);
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
+template <int KH, int KW, int SH, int SW>
 __global__ void pool_bwd_plane(const __grid_constant__ PoolBwdP p);
 __global__ void gemm_generic(const __grid_constant__ GemmP p);
 __global__ void ip_fwd_rows(const __grid_constant__ IpRowsP p);

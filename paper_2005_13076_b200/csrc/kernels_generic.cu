@@ -289,7 +289,9 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
 // coalesced; each input then gathers its <= ceil(k/s)^2 windows from shared
 // memory in ascending output order (bit-exact with the scatter order).
 // Window ranges per input row / column come from two small tables.
+template <int KH, int KW, int SH, int SW>  // window / stride fixed at compile time when nonzero
 __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ PoolBwdP p) {
+  const int kh = KH ? KH : p.kh, kw = KW ? KW : p.kw, sh = SH ? SH : p.sh, sw = SW ? SW : p.sw;
   extern __shared__ __align__(16) uint8_t psm[];
   const int HWp = p.Hp * p.Wp, HW = p.H * p.W;
   float* d = reinterpret_cast<float*>(psm);
@@ -297,12 +299,12 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
   short2* arow = reinterpret_cast<short2*>(m + HWp);
   short2* bcol = arow + p.H;
   for (int h = threadIdx.x; h < p.H; h += blockDim.x) {
-    const int a0 = (h + p.ph < p.kh) ? 0 : (h + p.ph - p.kh) / p.sh + 1;
-    arow[h] = make_short2((short)a0, (short)min((h + p.ph) / p.sh, p.Hp - 1));
+    const int a0 = (h + p.ph < kh) ? 0 : (h + p.ph - kh) / sh + 1;
+    arow[h] = make_short2((short)a0, (short)min((h + p.ph) / sh, p.Hp - 1));
   }
   for (int w = threadIdx.x; w < p.W; w += blockDim.x) {
-    const int b0 = (w + p.pw < p.kw) ? 0 : (w + p.pw - p.kw) / p.sw + 1;
-    bcol[w] = make_short2((short)b0, (short)min((w + p.pw) / p.sw, p.Wp - 1));
+    const int b0 = (w + p.pw < kw) ? 0 : (w + p.pw - kw) / sw + 1;
+    bcol[w] = make_short2((short)b0, (short)min((w + p.pw) / sw, p.Wp - 1));
   }
   pdl_enter();
   for (int nc = blockIdx.x; nc < p.N * p.C; nc += gridDim.x) {
@@ -314,8 +316,8 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
         m[o] = __ldg(p.mask + (size_t)nc * HWp + o);
       } else {
         const int a = o / p.Wp, b = o - a * p.Wp;
-        const int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
-        const int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+        const int hs = a * sh - p.ph, ws = b * sw - p.pw;
+        const int he = min(hs + kh, p.H + p.ph), we = min(ws + kw, p.W + p.pw);
         v = __fdiv_rn(v, (float)((he - hs) * (we - ws)));
       }
       d[o] = v;
@@ -336,17 +338,34 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
         const int h = r / p.W, w = r - h * p.W;
         const short2 ar = arow[h], bc = bcol[w];
         float acc = 0.f;
-        for (int a = ar.x; a <= ar.y; ++a)
-          for (int b = bc.x; b <= bc.y; ++b) {
-            const int o = a * p.Wp + b;
-            if (p.method != 0 || m[o] == r) acc += d[o];
-          }
+        if (KH && SH && KW && SW) {  // at most ceil(k/s) windows per dimension: unrolled, ascending
+          constexpr int NA = (KH + SH - 1) / (SH ? SH : 1), NB = (KW + SW - 1) / (SW ? SW : 1);
+#pragma unroll
+          for (int ia = 0; ia < NA; ++ia)
+#pragma unroll
+            for (int ib = 0; ib < NB; ++ib) {
+              const int a = ar.x + ia, b = bc.x + ib;
+              if (a <= ar.y && b <= bc.y) {
+                const int o = a * p.Wp + b;
+                if (p.method != 0 || m[o] == r) acc += d[o];
+              }
+            }
+        } else {
+          for (int a = ar.x; a <= ar.y; ++a)
+            for (int b = bc.x; b <= bc.y; ++b) {
+              const int o = a * p.Wp + b;
+              if (p.method != 0 || m[o] == r) acc += d[o];
+            }
+        }
         if (!(y[u] > 0.f)) acc = 0.f;
         p.dx[(size_t)nc * HW + r] = acc;
       }
     }
   }
 }
+template __global__ void pool_bwd_plane<0, 0, 0, 0>(const __grid_constant__ PoolBwdP);
+template __global__ void pool_bwd_plane<3, 3, 2, 2>(const __grid_constant__ PoolBwdP);
+template __global__ void pool_bwd_plane<2, 2, 2, 2>(const __grid_constant__ PoolBwdP);
 
 // ---------------------------------------------- test-phase blocks (NEXT #3)
 // Standalone SoftMax forward: warp per row, stable

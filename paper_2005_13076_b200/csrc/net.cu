@@ -836,11 +836,15 @@ static void build_layerwise(pn_net* net) {
                  L.out[2], L.out[3], L.method, relu_y};
       // plane-staged kernel when a plane's gradients + origins fit shared memory
       const size_t psmem = (size_t)L.out[2] * L.out[3] * 8 + (size_t)(L.in[2] + L.in[3]) * 4 + 16;
-      if (psmem <= 48 * 1024)
-        l.set((const void*)pool_bwd_plane, dim3(std::min(N * L.in[1], 16 * net->tc_sms)), dim3(256), psmem, p);
-      else
+      if (psmem <= 48 * 1024) {  // (3x3 / 2x2 stride-2 windows: compile-time geometry)
+        const void* fn = (L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2) ? (const void*)pool_bwd_plane<3, 3, 2, 2>
+                         : (L.kh == 2 && L.kw == 2 && L.sh == 2 && L.sw == 2) ? (const void*)pool_bwd_plane<2, 2, 2, 2>
+                                                                               : (const void*)pool_bwd_plane<0, 0, 0, 0>;
+        l.set(fn, dim3(std::min(N * L.in[1], 16 * net->tc_sms)), dim3(256), psmem, p);
+      } else {
         l.set((const void*)pool_bwd_generic, dim3(cdiv(L.in[2] * L.in[3], 256), std::min(N * L.in[1], 65535)),
               dim3(256), 0, p);
+      }
       add(bwd, L.name + (relu_y ? ".bwd+relu_bwd" : ".bwd"), l);
     } else if (L.type == L_IP) {
       // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
