@@ -402,7 +402,7 @@ def main():
         # the dataset's bytes (NEXT #4): pinned host batches -> net_train_steps_u8_host
         # (double-buffered H2D on a copy stream under the previous step, bytes
         # normalised on the device, every step's loss read back)
-        ring = min(64, max(1, e2e_steps))
+        ring = min(250, max(1, e2e_steps))
         g8 = gen8(BATCH * ring, seed=200 + rank)
         net.net_set_input_transform(1.0 / 256, g8[2] if len(g8) > 2 else None)
         xh = torch.from_numpy(g8[0]).view(ring, BATCH, *g8[0].shape[1:]).pin_memory()
