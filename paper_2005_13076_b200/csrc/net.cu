@@ -22,6 +22,9 @@
 #include "tc.h"
 #include "tc_conv.h"
 
+#ifndef PIPE_SLOTS
+#define PIPE_SLOTS 3  // pipelined host loop: input slots = steps per captured graph (A/B knob)
+#endif
 #ifndef WG2_SPLITS
 #define WG2_SPLITS 0  // conv2 weight-gradient image splits (0: SMs / 4; compile-time knob for A/B builds)
 #endif
@@ -209,7 +212,7 @@ struct pn_net {
   float x_scale = 1.f / 256.f;
   float* x_mean = nullptr;    // [C*H*W] device, or null
   float* xin = nullptr;       // fp32 input written by the ingest kernel (layerwise plans)
-  static constexpr int kSlots = 3;  // pipelined host input: device slots (copies run up to 2 steps ahead)
+  static constexpr int kSlots = PIPE_SLOTS;  // pipelined host input: device slots (copies run up to kSlots-1 steps ahead)
   uint8_t* h2d_x8[kSlots] = {};
   int32_t* h2d_y[kSlots] = {};
   float* h2d_loss = nullptr;  // [kSlots]
