@@ -890,6 +890,7 @@ static void add_fork(pn_net* net, std::vector<Stage>& v, const char* name, cudaE
     cudaError_t e = cudaEventRecord(ev, st);
     return e != cudaSuccess ? e : cudaStreamWaitEvent(net->side, ev, 0);
   };
+  f.transparent = FORK_PDL != 0;
   v.push_back(f);
 }
 
@@ -1164,7 +1165,7 @@ static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t 
       continue;
     }
     TRY(run_stage(net, s, a, st, prev_kernel));
-    prev_kernel = !s.custom;
+    if (!s.transparent) prev_kernel = !s.custom;
   }
   return PN_OK;
 }
@@ -1201,7 +1202,7 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, GraphExec& E) 
     for (auto& s : net->phase[ph]) {
       cudaStream_t on = s.side ? net->side : net->cap;
       pn_status st = run_stage(net, s, a, on, s.side ? false : prev_kernel);
-      if (!s.side) prev_kernel = !s.custom;
+      if (!s.side && !s.transparent) prev_kernel = !s.custom;
       if (st != PN_OK) {
         cudaGraph_t g;
         cudaStreamEndCapture(net->cap, &g);
@@ -1701,7 +1702,7 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
           for (auto& stg : net->phase[ph]) {
             cudaStream_t on = stg.side ? net->side : net->cap;
             if ((err = run_stage(net, stg, a, on, stg.side ? false : prev_kernel)) != PN_OK) break;
-            if (!stg.side) prev_kernel = !stg.custom;
+            if (!stg.side && !stg.transparent) prev_kernel = !stg.custom;
           }
         if (err != PN_OK) break;
         // the loss read-back on a side branch (the next step does not wait for it)

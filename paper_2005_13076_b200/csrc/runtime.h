@@ -15,6 +15,14 @@
 namespace pn {
 
 // Everything that changes from one training step to the next.
+// The backward fork (an event record + side-stream wait) adds no dependency to
+// the main stream, so the kernel after it launches programmatically after ip2's
+// backward; ip1's data gradient then reads its da1 operand after the wait.
+// (Shared by net.cu and tc.cu; compile-time knob for A/B builds.)
+#ifndef FORK_PDL
+#define FORK_PDL 1
+#endif
+
 struct StepArgs {
   const float* x = nullptr;
   const uint8_t* x8 = nullptr;  // byte input (fused LeNet plan: normalised inside conv1's loads)
@@ -88,6 +96,8 @@ struct Stage {
   std::function<void(Launch&, const StepArgs&)> patch;  // refresh step-dependent args
   std::function<cudaError_t(cudaStream_t)> custom;     // non-kernel action
   bool side = false;  // in a step (graph or eager phase run): launched on the side stream, between fork and join
+  bool transparent = false;  // non-kernel stage that adds no dependency to its own stream (a fork's event
+                             // record): the next kernel may still launch programmatically after the previous one
 };
 
 }  // namespace pn

@@ -318,7 +318,7 @@ struct IpDgradUnpool {
   static constexpr int SPLIT = IPD_SPLIT, ROWS = 128 / SPLIT, STAGES = IPD_STAGES, BN = IPD_BN, FT = BN / 16;
   static constexpr int RED_FLOATS = FT * ROWS;  // red: [filter in tile][owned row]
   static constexpr int EPI_BYTES = ROWS * BN;   // the owned rows' pool2 origins [row][FT x 16]
-  static constexpr bool A_EARLY = true, B_EARLY = true;
+  static constexpr bool A_EARLY = !FORK_PDL, B_EARLY = true;  // (FORK_PDL: da1r from the immediate predecessor)
   const Params& p;
   int m0, k0;
   __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
