@@ -62,4 +62,7 @@ constexpr int CW_IMGS = CW_IMGS_DEF;
 #define C1_FPT 4
 #endif
 constexpr int C1_THREADS = 32 * (20 / C1_FPT);
+#ifndef C1_MINB
+#define C1_MINB 2  // conv1 + pool1: resident blocks per SM the register budget is sized for
+#endif
 }  // namespace pn

@@ -47,7 +47,7 @@ __device__ __forceinline__ float in_x(const float* x, const uint8_t* x8, float s
 
 constexpr int C1_MAXIMG = 4;  // images a block's item range can touch
 constexpr int C1_PAIRS = C1_FPT / 2;    // filter pairs per thread (one FFMA2 lane pair each)
-__global__ void __launch_bounds__(C1_THREADS, 2) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
+__global__ void __launch_bounds__(C1_THREADS, C1_MINB) lenet_conv1_pool1(const __grid_constant__ Conv1Pool1P p) {
   // everything read here (the batch, conv1's weights from the previous
   // step's SGD) is complete at launch and the predecessor (the TF32 weight
   // packing) touches none of it: run alongside it, wait only at the end

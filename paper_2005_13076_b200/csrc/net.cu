@@ -917,7 +917,7 @@ static void build_fused_lenet(pn_net* net) {
     // stored TF32-rounded; the mask is taken before rounding
     // items (image, pooled position) split evenly over 2 blocks per SM
     // (at least one block per image pair: a block's range then touches <= 3 images)
-    const int blocks = std::max(std::max(1, std::min(2 * net->tc_sms, N * 144 / 32)), (N + 1) / 2);
+    const int blocks = std::max(std::max(1, std::min(C1_MINB * net->tc_sms, N * 144 / 32)), (N + 1) / 2);
     const int per = (int)cdiv((long long)N * 144, blocks);
     Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c, per};
     Launch l;
