@@ -55,6 +55,8 @@ def lib():
                                    _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_pool_fwd.argtypes = [_dp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _dp, _ip]
         L.orc_pool_bwd.argtypes = [_dp, _ip, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _dp]
+        L.orc_pool_fwd_f32.argtypes = [_fp, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _fp, _ip]
+        L.orc_pool_bwd_f32.argtypes = [_fp, _ip, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _i, _fp]
         L.orc_ip_fwd.argtypes = [_dp, _i, _i, _dp, _i, _dp, _dp, _dp]
         L.orc_ip_bwd.argtypes = [_dp, _dp, _dp, _i, _i, _i, _dp, _dp, _dp, _dp, _dp, _dp]
         L.orc_relu_fwd.argtypes = [_dp, _l, _d, _dp]
@@ -198,6 +200,34 @@ def pool_bwd(dy, mask, in_shape, method, kernel, stride, pad=(0, 0)):
     _check(lib().orc_pool_bwd(_ptr(dy), _ptr(mask, _ip), N, C, H, W, method, kernel[0],
                               kernel[1], stride[0], stride[1], pad[0], pad[1], _ptr(dx)),
            "pool_bwd")
+    return dx
+
+
+def pool_fwd_f32(x, method, kernel, stride, pad=(0, 0)):
+    """Caffe float-arithmetic pooling forward (oracle.c orc_pool_fwd_f32)."""
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    N, C, H, W = x.shape
+    Hp = pool_out_size(H, kernel[0], stride[0], pad[0])
+    Wp = pool_out_size(W, kernel[1], stride[1], pad[1])
+    if Hp < 1 or Wp < 1:
+        raise ValueError("pool_fwd_f32: invalid geometry")
+    y = np.empty((N, C, Hp, Wp), np.float32)
+    mask = np.empty((N, C, Hp, Wp), dtype=np.int32) if method == MAX else None
+    _check(lib().orc_pool_fwd_f32(_ptr(x, _fp), N, C, H, W, method, kernel[0], kernel[1], stride[0],
+                                  stride[1], pad[0], pad[1], _ptr(y, _fp), _ptr(mask, _ip)), "pool_fwd_f32")
+    return y, mask
+
+
+def pool_bwd_f32(dy, mask, in_shape, method, kernel, stride, pad=(0, 0)):
+    """Caffe float-arithmetic pooling backward (oracle.c orc_pool_bwd_f32)."""
+    dy = np.ascontiguousarray(dy, dtype=np.float32)
+    N, C, H, W = in_shape
+    if mask is not None:
+        mask = np.ascontiguousarray(mask, dtype=np.int32)
+    dx = np.empty((N, C, H, W), np.float32)
+    _check(lib().orc_pool_bwd_f32(_ptr(dy, _fp), _ptr(mask, _ip), N, C, H, W, method, kernel[0],
+                                  kernel[1], stride[0], stride[1], pad[0], pad[1], _ptr(dx, _fp)),
+           "pool_bwd_f32")
     return dx
 
 

@@ -305,6 +305,93 @@ int orc_pool_bwd(const double* dy, const int32_t* mask, int N, int C, int H,
   return 0;
 }
 
+/* Pooling in Caffe's float arithmetic (SURVEY.md §8(c) implementation rule
+ * "acc = float (Caffe-faithful)"; rows c4-c6 are a bit-exact contract).
+ * Same windows, scan order and output order as orc_pool_fwd / orc_pool_bwd
+ * (S:357-374); every sum is a float accumulator rounded after each
+ * addition and the AVE quotient is one IEEE float division:
+ *   fwd AVE:  acc = 0f; acc += x (h, w ascending); y = acc / (float)size
+ *   fwd MAX:  identical to orc_pool_fwd (a max selects an input: no rounding)
+ *   bwd MAX:  dx = 0f; for o ascending: dx[mask[o]] += dy[o]
+ *   bwd AVE:  q = dy[o] / (float)size; every in-window position += q, o ascending
+ * Inputs and outputs are float. */
+int orc_pool_fwd_f32(const float* x, int N, int C, int H, int W, int method,
+                     int kh, int kw, int sh, int sw, int ph, int pw, float* y,
+                     int32_t* mask) {
+  int Hp = orc_pool_out_size(H, kh, sh, ph);
+  int Wp = orc_pool_out_size(W, kw, sw, pw);
+  if (Hp < 1 || Wp < 1 || (method != 0 && method != 1)) return -1;
+  for (int n = 0; n < N; ++n)
+    for (int c = 0; c < C; ++c) {
+      const float* xp = x + ((long)n * C + c) * H * W;
+      for (int a = 0; a < Hp; ++a)
+        for (int bq = 0; bq < Wp; ++bq) {
+          int hs = a * sh - ph, ws = bq * sw - pw;
+          int he = hs + kh < H + ph ? hs + kh : H + ph;
+          int we = ws + kw < W + pw ? ws + kw : W + pw;
+          int size = (he - hs) * (we - ws);
+          if (hs < 0) hs = 0;
+          if (ws < 0) ws = 0;
+          if (he > H) he = H;
+          if (we > W) we = W;
+          long o = (((long)n * C + c) * Hp + a) * Wp + bq;
+          if (method == 0) {
+            float best = xp[(long)hs * W + ws];
+            int arg = hs * W + ws;
+            for (int h = hs; h < he; ++h)
+              for (int w = ws; w < we; ++w)
+                if (xp[(long)h * W + w] > best) {
+                  best = xp[(long)h * W + w];
+                  arg = h * W + w;
+                }
+            y[o] = best;
+            if (mask) mask[o] = arg;
+          } else {
+            float acc = 0.0f;
+            for (int h = hs; h < he; ++h)
+              for (int w = ws; w < we; ++w) acc = acc + xp[(long)h * W + w];
+            y[o] = acc / (float)size;
+          }
+        }
+    }
+  return 0;
+}
+
+int orc_pool_bwd_f32(const float* dy, const int32_t* mask, int N, int C, int H,
+                     int W, int method, int kh, int kw, int sh, int sw, int ph,
+                     int pw, float* dx) {
+  int Hp = orc_pool_out_size(H, kh, sh, ph);
+  int Wp = orc_pool_out_size(W, kw, sw, pw);
+  if (Hp < 1 || Wp < 1 || (method != 0 && method != 1)) return -1;
+  memset(dx, 0, sizeof(float) * (size_t)N * C * H * W);
+  for (int n = 0; n < N; ++n)
+    for (int c = 0; c < C; ++c) {
+      float* dxp = dx + ((long)n * C + c) * H * W;
+      for (int a = 0; a < Hp; ++a)
+        for (int bq = 0; bq < Wp; ++bq) {
+          long o = (((long)n * C + c) * Hp + a) * Wp + bq;
+          if (method == 0) {
+            int m = mask[o];
+            if (m < 0 || m >= H * W) return -1;
+            dxp[m] = dxp[m] + dy[o];
+          } else {
+            int hs = a * sh - ph, ws = bq * sw - pw;
+            int he = hs + kh < H + ph ? hs + kh : H + ph;
+            int we = ws + kw < W + pw ? ws + kw : W + pw;
+            int size = (he - hs) * (we - ws);
+            if (hs < 0) hs = 0;
+            if (ws < 0) ws = 0;
+            if (he > H) he = H;
+            if (we > W) we = W;
+            const float q = dy[o] / (float)size;
+            for (int h = hs; h < he; ++h)
+              for (int w = ws; w < we; ++w) dxp[(long)h * W + w] = dxp[(long)h * W + w] + q;
+          }
+        }
+    }
+  return 0;
+}
+
 /* InnerProduct forward (Listing 1: gemm NoTrans x Trans, then the
  * bias row add).  y[m,o] = sum_k x[m,k] w[o,k] + b[o]. */
 int orc_ip_fwd(const double* x, int M, int K, const double* w, int Nout,

@@ -79,6 +79,16 @@ int orc_pool_bwd(const double* dy, const int32_t* mask, int N, int C, int H,
                  int W, int method, int kh, int kw, int sh, int sw, int ph,
                  int pw, double* dx);
 
+/* The same pooling in Caffe's float arithmetic (float accumulators rounded
+ * after every addition, one float division for AVE; SURVEY §8(c) c4-c6
+ * bit-exact contract).  Inputs/outputs float. */
+int orc_pool_fwd_f32(const float* x, int N, int C, int H, int W, int method,
+                     int kh, int kw, int sh, int sw, int ph, int pw, float* y,
+                     int32_t* mask);
+int orc_pool_bwd_f32(const float* dy, const int32_t* mask, int N, int C, int H,
+                     int W, int method, int kh, int kw, int sh, int sw, int ph,
+                     int pw, float* dx);
+
 /* InnerProduct (Listings 1-2).  w is [Nout, K]
  * (transpose_ = false).  y = x * w^T + b. */
 int orc_ip_fwd(const double* x, int M, int K, const double* w, int Nout,

@@ -220,6 +220,9 @@ struct pn_net {
   float* lr_pinned = nullptr; // host (pinned) learning rates of the steps of one call
   int64_t lr_pinned_cap = 0;
   float* loss_pinned = nullptr;  // host (pinned) per-step losses of the pipelined loop
+  float* hs_x = nullptr;         // net_train_step_host: device staging of one batch (on this net's device)
+  int32_t* hs_y = nullptr;
+  float* hs_loss = nullptr;
   int64_t loss_pinned_cap = 0;
   cudaStream_t copy = nullptr;
   cudaEvent_t ev_copied[kSlots] = {}, ev_used[kSlots] = {};
@@ -246,6 +249,7 @@ struct pn_net {
   cudaGraphExec_t multi = nullptr;
   cudaGraph_t multi_g = nullptr;
   cudaGraphNode_t multi_d2h[kSlots] = {};
+  float multi_mom = 0.f, multi_decay = 0.f, multi_gscale = 0.f;  // solver settings baked into `multi`
   cudaStream_t aux = nullptr;  // capture-side branch of the loss read-backs
   cudaEvent_t ev_loss[kSlots] = {}, ev_aux = nullptr;
   int launches_per_step = 0;
@@ -1556,19 +1560,15 @@ extern "C" pn_status net_train_step_host(pn_net* net, const float* xh, const int
   CU(cudaSetDevice(net->device));
   cudaStream_t st = (cudaStream_t)stream;
   const Blob& in = net->blobs[net->blob(net->input_name)];
-  static thread_local struct { float* x = nullptr; int32_t* y = nullptr; float* l = nullptr; int64_t nx = 0; int n = 0; } buf;
-  if (buf.nx < in.count() || buf.n < net->batch) {
-    if (buf.x) { cudaFree(buf.x); cudaFree(buf.y); cudaFree(buf.l); }
-    CU(cudaMalloc(&buf.x, in.count() * 4));
-    CU(cudaMalloc(&buf.y, net->batch * 4));
-    CU(cudaMalloc(&buf.l, 4));
-    buf.nx = in.count();
-    buf.n = net->batch;
+  if (!net->hs_x) {  // owned by the net, on its device, freed by net_destroy
+    TRY(net->alloc(&net->hs_x, (size_t)in.count()));
+    TRY(net->alloc(&net->hs_y, (size_t)net->batch));
+    TRY(net->alloc(&net->hs_loss, 1));
   }
-  CU(cudaMemcpyAsync(buf.x, xh, in.count() * 4, cudaMemcpyHostToDevice, st));
-  CU(cudaMemcpyAsync(buf.y, lh, net->batch * 4, cudaMemcpyHostToDevice, st));
-  TRY(net_train_step(net, buf.x, buf.y, sgd, iter, buf.l, stream));
-  CU(cudaMemcpyAsync(loss_host, buf.l, 4, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(net->hs_x, xh, in.count() * 4, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(net->hs_y, lh, net->batch * 4, cudaMemcpyHostToDevice, st));
+  TRY(net_train_step(net, net->hs_x, net->hs_y, sgd, iter, net->hs_loss, stream));
+  CU(cudaMemcpyAsync(loss_host, net->hs_loss, 4, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return PN_OK;
 }
@@ -1683,6 +1683,16 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
   };
   int64_t s0 = 0;
   if (net->fused && nsteps >= pn_net::kSlots && !getenv("PN_NO_MULTI")) {
+    {  // momentum / decay / 1/G are kernel arguments of the captured steps: re-capture when they change
+      const StepArgs h = make_args(net, nullptr, nullptr, nullptr, sgd, iter0);
+      if (net->multi && (h.mom != net->multi_mom || h.decay != net->multi_decay || h.gscale != net->multi_gscale)) {
+        CU(cudaStreamSynchronize(st));
+        cudaGraphExecDestroy(net->multi);
+        cudaGraphDestroy(net->multi_g);
+        net->multi = nullptr;
+        net->multi_g = nullptr;
+      }
+    }
     if (!net->multi) {  // capture the kSlots-step graph once (slot arguments never change)
       if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
       if (!net->aux) {
@@ -1730,6 +1740,10 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
       }
       CU(cudaGraphInstantiate(&net->multi, g, 0));
       net->multi_g = g;
+      const StepArgs h = make_args(net, nullptr, nullptr, nullptr, sgd, iter0);
+      net->multi_mom = h.mom;
+      net->multi_decay = h.decay;
+      net->multi_gscale = h.gscale;
     }
     for (; s0 + pn_net::kSlots <= nsteps; s0 += pn_net::kSlots) {
       for (int b = 0; b < pn_net::kSlots; ++b) TRY(issue_copies(s0 + b));

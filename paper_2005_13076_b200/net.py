@@ -145,8 +145,24 @@ class Net:
         check(lib().net_train_step(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), ctypes.byref(sgd),
                                    it, _ptr(loss, 'f32'), _stream(stream)))
 
+    def _check_host(self, t, dtype, shape, what):
+        import torch
+        if not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != dtype or not t.is_contiguous() \
+                or tuple(t.shape) != tuple(shape):
+            raise (TypeError if not isinstance(t, torch.Tensor) or t.dtype != dtype or t.is_cuda else ValueError)(
+                f"{what}: expected a contiguous CPU {dtype} tensor of shape {tuple(shape)}, got "
+                f"{getattr(t, 'dtype', type(t))} {tuple(getattr(t, 'shape', ()))} on "
+                f"{getattr(t, 'device', 'host')} (contiguous={getattr(t, 'is_contiguous', lambda: None)()})")
+
+    def _input_chw(self):
+        name = [k for k, v in self.blobs.items() if not v["is_param"]][0]  # the input blob comes first
+        return self.blobs[name]["dims"][1:]
+
     def net_train_step_host(self, x_host, labels_host, sgd, it, stream=None):
         """Host (preferably pinned) buffers in, host loss out (synchronous)."""
+        import torch
+        self._check_host(x_host, torch.float32, (self.batch,) + tuple(self._input_chw()), "x_host")
+        self._check_host(labels_host, torch.int32, (self.batch,), "labels_host")
         loss = ctypes.c_float()
         check(lib().net_train_step_host(self._h, ctypes.c_void_p(x_host.data_ptr()),
                                         ctypes.c_void_p(labels_host.data_ptr()), ctypes.byref(sgd),
@@ -169,7 +185,10 @@ class Net:
     def net_train_steps_u8_host(self, x8_host, labels_host, sgd, it0, stream=None):
         """x8_host: (steps, N, C, H, W) uint8 (pinned torch tensor preferred),
         labels_host: (steps, N) int32.  Returns the per-step losses (numpy)."""
-        steps = x8_host.shape[0]
+        import torch
+        steps = x8_host.shape[0] if hasattr(x8_host, "shape") and len(x8_host.shape) else 0
+        self._check_host(x8_host, torch.uint8, (steps, self.batch) + tuple(self._input_chw()), "x8_host")
+        self._check_host(labels_host, torch.int32, (steps, self.batch), "labels_host")
         losses = np.zeros(steps, np.float32)
         check(lib().net_train_steps_u8_host(self._h, ctypes.c_void_p(x8_host.data_ptr()),
                                             ctypes.c_void_p(labels_host.data_ptr()), steps, ctypes.byref(sgd),

@@ -176,6 +176,63 @@ def test_pipelined_host_steps_equal_device_steps():
     b.close()
 
 
+@pytest.mark.gpu
+def test_pipelined_host_steps_follow_changed_solver_settings():
+    """Two pipelined calls with different momentum / weight decay (the
+    multi-step graph captured by the first call must not keep the first
+    call's settings) equal the same steps one device call at a time."""
+    import torch
+
+    from paper_2005_13076_b200 import Net, make_sgd
+    N, S = 64, 3
+    x8, y = synth.mnist_like_fast_u8(N * 2 * S, seed=11)
+    x8 = x8.reshape(2 * S, N, 1, 28, 28)
+    y = y.reshape(2 * S, N)
+    params = _params("lenet")
+    sgds = [make_sgd(momentum=0.9, weight_decay=5e-4), make_sgd(momentum=0.5, weight_decay=1e-3)]
+    a = Net("lenet", N, device=0, tf32=True)
+    a.set_params(params)
+    la = []
+    for c in range(2):
+        la.append(a.net_train_steps_u8_host(torch.from_numpy(x8[c * S:(c + 1) * S]).pin_memory(),
+                                            torch.from_numpy(y[c * S:(c + 1) * S]).pin_memory(), sgds[c], c * S))
+    b = Net("lenet", N, device=0, tf32=True)
+    b.set_params(params)
+    lb = []
+    loss = torch.zeros(1, device="cuda")
+    for s in range(2 * S):
+        b.net_train_step_u8(torch.from_numpy(x8[s]).cuda(), torch.from_numpy(y[s]).cuda(), sgds[s // S], s, loss)
+        lb.append(loss.item())
+    np.testing.assert_array_equal(np.concatenate(la), np.array(lb, np.float32))
+    for u, v in zip(_state(a, params), _state(b, params)):
+        np.testing.assert_array_equal(u, v)
+    a.close()
+    b.close()
+
+
+def test_host_input_validation():
+    """net_train_step_host / net_train_steps_u8_host reject host buffers of
+    the wrong dtype, shape, device or layout before the C call (the C side
+    would read past them)."""
+    import torch
+
+    from paper_2005_13076_b200.net import Net
+    fake = Net.__new__(Net)
+    fake.batch = 4
+    fake.blobs = {"data": {"dims": (4, 1, 28, 28), "is_param": False, "materialised": False}}
+    ok = torch.zeros((2, 4, 1, 28, 28), dtype=torch.uint8)
+    fake._check_host(ok, torch.uint8, (2, 4) + tuple(fake._input_chw()), "x8_host")
+    with pytest.raises(TypeError):
+        fake._check_host(ok.to(torch.int64), torch.uint8, (2, 4, 1, 28, 28), "x8_host")
+    with pytest.raises(ValueError):
+        fake._check_host(torch.zeros((2, 5, 1, 28, 28), dtype=torch.uint8), torch.uint8, (2, 4, 1, 28, 28), "x8")
+    with pytest.raises(ValueError):
+        fake._check_host(torch.zeros((2, 4, 1, 28, 56), dtype=torch.uint8)[..., ::2], torch.uint8,
+                         (2, 4, 1, 28, 28), "x8")
+    with pytest.raises(TypeError):
+        fake._check_host(np.zeros((2, 4, 1, 28, 28), np.uint8), torch.uint8, (2, 4, 1, 28, 28), "x8")
+
+
 def learnable_mnist_u8(n, seed):
     """A synthetic task LeNet must learn (stand-in for the MNIST sanity of
     S:719 when the dataset is not provided): class y is a bright 6x5 block at

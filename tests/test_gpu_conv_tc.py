@@ -14,7 +14,7 @@ import torch
 
 from oracle.net import OracleNet
 from paper_2005_13076_b200 import PN_DIFF, Net, spec_text, synth
-from parity import RTOL, assert_close, assert_norm
+from parity import RTOL, assert_close, assert_norm, report
 
 pytestmark = pytest.mark.gpu
 
@@ -188,15 +188,12 @@ def test_conv_tc_net_level(case, N):
     net.net_sync_errors()
     out = ref.forward(x, y)
     gref = ref.backward()
-    assert abs(loss.item() - out["loss"]) <= 2e-3 * (1 + abs(out["loss"])), (loss.item(), out["loss"])
-    # Every parameter gradient depends on the whole chain: the forward runs
-    # through the TF32 convolutions below the layer, the backward through those
-    # above it, and their rounding also flips discrete decisions (ReLU signs,
-    # max-pool near-ties routing a gradient to another pixel).  The norm-wise
-    # bound therefore scales with the number of TF32 conv layers in the chain;
-    # the element-wise kernel bound is asserted by the teacher-forced test.
-    nconv = sum(1 for L in ref.layers if L["type"] == "Convolution")
+    rel = abs(loss.item() - out["loss"]) / abs(out["loss"])
+    report("loss (net level)", kind="relative", rel_err=rel, bound=RTOL[True])
+    assert rel <= RTOL[True], (loss.item(), out["loss"])
+    # every parameter gradient norm-wise at rtol; the
+    # element-wise kernel bound is asserted by the teacher-forced test
     for k in params:
         g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
-        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * RTOL[True] * nconv)
+        assert_norm(f"grad {k}", g, gref["grads"][k], RTOL[True])
     net.close()

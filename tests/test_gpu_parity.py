@@ -1,7 +1,19 @@
 """GPU parity: the CUDA path (through the C ABI) vs the CPU oracle on the
-same seeded inputs.  Net-level checks (forward blobs with propagated scales,
-loss, masks, predictions, parameter gradients) plus teacher-forced stage
-checks, in which each fused kernel is fed the oracle's inputs."""
+same seeded inputs.
+
+* Net level (the GPU chain's own intermediate values): the loss by plain
+  relative error <= rtol; every materialised forward blob element-wise
+  against rtol * S of its own layer PLUS the error its GPU input actually
+  carries (measured on the materialised input blob, pushed through |W| --
+  the incoming error is measured, not a worst case); masks / predictions
+  exact except listed, capped near-ties under that same bound; parameter
+  gradients norm-wise at rtol.
+* Teacher forcing at N = 64, 300 and 512 (the bench size; at 300 and 512
+  every persistent conv2 CTA runs >= 2 image pairs, so the ring wrap, the
+  second TMEM accumulator and the mbarrier phase flips are covered): every
+  fused kernel is fed the oracle's own inputs and compared element-wise
+  against rtol * S of its layer (S = sum |terms|, R16).
+"""
 import numpy as np
 import pytest
 import torch
@@ -9,12 +21,9 @@ import torch
 from oracle import capi
 from oracle.net import OracleNet
 from paper_2005_13076_b200 import PN_DIFF, PN_HISTORY, PN_MASK, Net, PnError, make_sgd, spec_text, synth
-from parity import (RTOL, assert_bitwise, assert_close, assert_norm, check_mask, check_pred,
-                    effective_scales)
+from parity import RTOL, assert_bitwise, assert_close, assert_norm, check_mask, check_pred, report
 
 pytestmark = pytest.mark.gpu
-
-LENET_POOLS = {"pool1": ("conv1", (24, 24)), "pool2": ("conv2", (8, 8))}
 
 
 def make(spec, N, tf32=False, layerwise=False, seed_x=1, seed_w=2):
@@ -55,6 +64,64 @@ def run(net, phase, prefix, x=None, y=None):
 
 
 # --------------------------------------------------------------- net level
+def chain_bounds(ref, out, gpu, rtol):
+    """Per-blob error bounds of the GPU chain's forward values.
+
+    For a contraction layer (conv / ip): B = rtol * S(own terms) + |W| (*) D,
+    where D is the measured |gpu - oracle| of its input blob when the plan
+    materialises it (else that blob's bound).  MAX pool: the window max of the
+    pre-pool bound (valid whichever element wins); AVE pool: the window mean
+    plus its own rounding; ReLU: unchanged (1-Lipschitz).  Returns (bounds of
+    each layer's output by layer name, pre-pool bounds by pool layer name)."""
+    cur = {ref.input_name: np.zeros(ref.shapes[ref.input_name])}
+    final = {}  # oracle's final value of every blob (after in-place ReLUs)
+    for L in ref.layers:
+        if L["type"] != "SoftmaxWithLoss":
+            final[L["top"]] = out["blobs"][L["name"]]
+    bnd, pre = {}, {}
+
+    def incoming(blob):
+        if blob in gpu:
+            return np.abs(gpu[blob].reshape(final[blob].shape).astype(np.float64) - final[blob])
+        return cur[blob]
+
+    for L in ref.layers:
+        t, nm = L["type"], L["name"]
+        if t == "SoftmaxWithLoss":
+            bnd["logits"] = cur[L["bottom"]].reshape(cur[L["bottom"]].shape[0], -1)
+            continue
+        if t == "Convolution":
+            d = incoming(L["bottom"])
+            w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
+            b = rtol * out["scales"][nm]
+            if L["bottom"] != ref.input_name:
+                if L["G"] == 1:
+                    b = b + capi.conv_fwd(d, w, None, L["s"], L["p"])
+                else:
+                    from oracle.net import grouped_conv_fwd
+                    b = b + grouped_conv_fwd(d, w, None, L["G"], L["s"], L["p"])[0]
+        elif t == "InnerProduct":
+            d = incoming(L["bottom"])
+            w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
+            b = rtol * out["scales"][nm] + capi.ip_fwd(d.reshape(d.shape[0], -1), w, None).reshape(
+                out["scales"][nm].shape)
+        elif t == "Pooling":
+            d = incoming(L["bottom"])
+            pre[nm] = d
+            if L["method"] == capi.MAX:
+                b, _ = capi.pool_fwd(d, capi.MAX, L["k"], L["s"], L["p"])
+            else:
+                b, _ = capi.pool_fwd(d, capi.AVE, L["k"], L["s"], L["p"])
+                b = b + rtol * np.abs(out["blobs"][nm])
+        elif t == "ReLU":
+            b = cur[L["bottom"]]
+        else:
+            b = cur[L["bottom"]]
+        cur[L["top"]] = b
+        bnd[nm] = b
+    return bnd, pre
+
+
 @pytest.mark.parametrize("spec,N,tf32,layerwise", [
     ("lenet", 64, False, False),
     ("lenet", 64, False, True),
@@ -65,6 +132,8 @@ def run(net, phase, prefix, x=None, y=None):
     ("lenet", 64, True, True),            # LeNet through the general TF32 plan
     ("lenet", 64, True, False),
     ("lenet", 37, True, False),
+    ("lenet", 512, True, False),          # the bench configuration (eager phases)
+    ("lenet", 512, False, False),
 ])
 def test_net_forward_backward(spec, N, tf32, layerwise):
     net, ref, params, x, y = make(spec, N, tf32, layerwise)
@@ -75,39 +144,50 @@ def test_net_forward_backward(spec, N, tf32, layerwise):
     net.net_backward()
     net.net_sync_errors()
     out = ref.forward(x, y)
-    seff = effective_scales(ref, out)
     gref = ref.backward()
-    # forward blobs the plan materialises
+    # the materialised forward blobs (in-place ReLUs: the post-activation value)
+    gpu = {}
     for L in ref.layers:
-        name, t = L["name"], L["type"]
-        if t == "SoftmaxWithLoss" or not net.blobs.get(L["top"], {}).get("materialised", False):
+        top = L["top"]
+        if L["type"] == "SoftmaxWithLoss" or not net.blobs.get(top, {}).get("materialised", False):
             continue
-        if t == "ReLU":
-            continue  # compared through the in-place blob below
-        g = host(net.net_get_blob(L["top"]))
-        o = out["blobs"][name]
-        # in-place ReLU: the GPU blob holds the post-activation value
-        nxt = [M for M in ref.layers if M["type"] == "ReLU" and M["bottom"] == L["top"]]
-        if nxt:
-            o = out["blobs"][nxt[0]["name"]]
-        assert_close(f"{name}", g.reshape(o.shape), o, seff[name], rtol)
-    # masks (exact up to oracle near-ties)
+        gpu[top] = host(net.net_get_blob(top))
+    bnd, pre = chain_bounds(ref, out, gpu, rtol)
+    for L in ref.layers:
+        top = L["top"]
+        if top not in gpu or L["type"] == "ReLU":
+            continue
+        last = [M for M in ref.layers if M["top"] == top][-1]      # the blob's final writer
+        o = out["blobs"][last["name"]]
+        assert_close(f"{L['name']} (net level)", gpu[top].reshape(o.shape), o, bnd[last["name"]] / rtol, rtol)
+    # masks: exact up to listed near-ties of the pre-pool values under their bound
     for L in ref.layers:
         if L["type"] == "Pooling" and L["method"] == capi.MAX:
-            pre = [M for M in ref.layers if M["top"] == L["bottom"]][0]["name"]
+            pre_layer = [M for M in ref.layers if M["top"] == L["bottom"]][-1]["name"]
             gm = host(net.net_get_blob(L["top"], PN_MASK))
-            check_mask(L["name"], gm, out["masks"][L["name"]], out["blobs"][pre], seff[pre],
-                       L["in_shape"][2:], L["k"][0], L["s"][0], L["p"][0], rtol)
-    # loss, probabilities, predictions
-    lscale = seff["logits"]
-    assert abs(loss.item() - out["loss"]) <= rtol * (1 + float(lscale.max())) , (loss.item(), out["loss"])
+            check_mask(L["name"] + " mask (net level)", gm, out["masks"][L["name"]], out["blobs"][pre_layer],
+                       pre[L["name"]] / rtol, L["in_shape"][2:], L["k"][0], L["s"][0], L["p"][0], rtol)
+    # loss by plain relative error
+    rel = abs(loss.item() - out["loss"]) / abs(out["loss"])
+    report("loss (net level)", kind="relative", rel_err=rel, bound=rtol)
+    assert rel <= rtol, (loss.item(), out["loss"])
+    # probabilities: softmax of logits within their bound (first order)
+    blg = bnd["logits"]
     prob = host(net.net_get_blob("prob")).reshape(out["prob"].shape)
-    assert_close("prob", prob, out["prob"], lscale.max(axis=1, keepdims=True) + 0 * prob, rtol)
-    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], lscale, rtol)
-    # parameter gradients: norm-wise (SURVEY §8(c) tolerance reading)
+    p = out["prob"]
+    pb = p * (blg + (p * blg).sum(1, keepdims=True)) * 1.01 + RTOL[False] * p + 1e-30
+    assert_close("prob (net level)", prob, p, pb / rtol, rtol)
+    # predictions: exact up to near-ties of the oracle logits under the logit bound
+    pred = host(net.net_get_blob("pred")).ravel()
+    g = pred
+    tol = np.zeros(N)
+    for i in np.flatnonzero(g != out["pred"]):
+        tol[i] = blg[i, g[i]] + blg[i, out["pred"][i]]
+    check_pred(pred, out["pred"], out["logits"], tol, name="pred (net level)")
+    # parameter gradients: norm-wise at rtol
     for k in params:
-        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
-        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * rtol)
+        gg = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
+        assert_norm(f"grad {k} (net level)", gg, gref["grads"][k], rtol)
 
 
 def test_train_step_graph_equals_eager_and_is_deterministic():
@@ -180,9 +260,9 @@ def test_backward_before_forward_is_state_error():
 
 
 # ---------------------------------------------------------- teacher forcing
+@pytest.mark.parametrize("N", [64, 300, 512])
 @pytest.mark.parametrize("tf32", [False, True])
-def test_teacher_forced_fused_stages(tf32):
-    N = 64
+def test_teacher_forced_fused_stages(tf32, N):
     rtol = RTOL[tf32]
     net, ref, params, x, y = make("lenet", N, tf32)
     out = ref.forward(x, y)
@@ -198,30 +278,35 @@ def test_teacher_forced_fused_stages(tf32):
     # conv1 is fp32 SIMT in both plans; the TF32 plan stores pool1 rounded to
     # TF32 (its only consumers are conv2's contractions): rtol of that plan
     assert_close("pool1", host(net.net_get_blob("pool1")), out["blobs"]["pool1"], S1, rtol)
-    check_mask("pool1", host(net.net_get_blob("pool1", PN_MASK)), out["masks"]["pool1"],
+    check_mask("pool1 mask", host(net.net_get_blob("pool1", PN_MASK)), out["masks"]["pool1"],
                out["blobs"]["conv1"], sc["conv1"], (24, 24), 2, 2, 0, RTOL[False])
     # conv2 + pool2 from the oracle's pool1
     net.net_put_blob("pool1", out["blobs"]["pool1"].astype(np.float32))
     run(net, 0, "conv2+pool2")
     S2, _ = capi.pool_fwd(sc["conv2"], capi.MAX, (2, 2), (2, 2))
     assert_close("pool2", host(net.net_get_blob("pool2")), out["blobs"]["pool2"], S2, rtol)
-    check_mask("pool2", host(net.net_get_blob("pool2", PN_MASK)), out["masks"]["pool2"],
-               out["blobs"]["conv2"], sc["conv2"], (8, 8), 2, 2, 0, rtol)
+    check_mask("pool2 mask", host(net.net_get_blob("pool2", PN_MASK)), out["masks"]["pool2"],
+               out["blobs"]["conv2"], sc["conv2"], (8, 8), 2, 2, 0, rtol,
+               max_excused=max(1, out["masks"]["pool2"].size // 200))
     # ip1 + relu from the oracle's pool2
     net.net_put_blob("pool2", out["blobs"]["pool2"].astype(np.float32))
     run(net, 0, "ip1+relu")
-    assert_close("ip1", host(net.net_get_blob("ip1")).reshape(N, 500),
+    assert_close("ip1+relu1", host(net.net_get_blob("ip1")).reshape(N, 500),
                  out["blobs"]["relu1"].reshape(N, 500), sc["ip1"].reshape(N, 500), rtol)
     # ip2 + softmax-loss from the oracle's ip1
     net.net_put_blob("ip1", out["blobs"]["relu1"].astype(np.float32))
     run(net, 0, "ip2+softmax_loss", xd, yd)
     run(net, 0, "loss_reduce")
     s2 = sc["ip2"].reshape(N, 10)
-    assert_close("logits", host(net.net_get_blob("ip2")).reshape(N, 10), out["logits"], s2, RTOL[False])
+    lg = host(net.net_get_blob("ip2")).reshape(N, 10)
+    assert_close("logits", lg, out["logits"], s2, RTOL[False])
     assert_close("prob", host(net.net_get_blob("prob")).reshape(N, 10), out["prob"],
                  s2.max(axis=1, keepdims=True) + 0 * out["prob"], RTOL[False])
-    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], s2, RTOL[False])
-    assert abs(host(net.net_get_blob("loss"))[0, 0, 0, 0] - out["loss"]) <= 1e-5 * (1 + out["loss"])
+    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"],
+               RTOL[False] * (2 * s2.max(axis=1)), name="pred")
+    rel = abs(host(net.net_get_blob("loss"))[0, 0, 0, 0] - out["loss"]) / out["loss"]
+    report("loss", kind="relative", rel_err=rel, bound=RTOL[False])
+    assert rel <= RTOL[False]
     dz = gref["diffs"]["loss"].reshape(N, 10)
     assert_close("dz", host(net.net_get_blob("ip2", PN_DIFF)).reshape(N, 10), dz,
                  s2.max(axis=1, keepdims=True) / N + np.abs(dz), RTOL[False])
@@ -229,7 +314,6 @@ def test_teacher_forced_fused_stages(tf32):
     # backward: ip2 + relu1 from oracle dz and ip1
     net.net_put_blob("ip2", dz.astype(np.float32).reshape(N, 10, 1, 1), PN_DIFF)
     run(net, 1, "ip2.bwd")
-    # the ip bucket reduction: its own stage (fp32 plan) or inside ip1.wgrad (TF32 plan)
     run(net, 1, [n for n in net.stages(1) if "ip.bucket_reduce" in n][0])
     gs = gref["scales"]
     assert_close("ip2.w grad", host(net.net_get_blob("ip2.w", PN_DIFF)), gref["grads"]["ip2.w"], gs["ip2.w"],
@@ -237,7 +321,7 @@ def test_teacher_forced_fused_stages(tf32):
     assert_close("ip2.b grad", host(net.net_get_blob("ip2.b", PN_DIFF)).ravel(), gref["grads"]["ip2.b"],
                  gs["ip2.b"], RTOL[False])
     da1 = gref["diffs"]["relu1"].reshape(N, 500)
-    assert_close("da1", host(net.net_get_blob("ip1", PN_DIFF)).reshape(N, 500), da1,
+    assert_close("da1 (ip2 dgrad + relu1 bwd)", host(net.net_get_blob("ip1", PN_DIFF)).reshape(N, 500), da1,
                  gs["ip2.dx"].reshape(N, 500), RTOL[False])
     # ip1 backward (+ pool2 backward) from oracle da1
     net.net_put_blob("ip1", da1.astype(np.float32).reshape(N, 500, 1, 1), PN_DIFF)
@@ -249,16 +333,24 @@ def test_teacher_forced_fused_stages(tf32):
     assert_close("ip1.b grad", host(net.net_get_blob("ip1.b", PN_DIFF)).ravel(), gref["grads"]["ip1.b"],
                  gs["ip1.b"], RTOL[False])
     G2 = gref["diffs"]["pool2"]
-    Sg2, = [capi.pool_bwd(gs["ip1.dx"].reshape(N, 50, 4, 4), out["masks"]["pool2"], (N, 50, 8, 8), capi.MAX,
-                          (2, 2), (2, 2))]
-    assert_close("conv2 diff (unpooled)", host(net.net_get_blob("conv2", PN_DIFF)), G2, Sg2, rtol)
+    Sg2 = capi.pool_bwd(gs["ip1.dx"].reshape(N, 50, 4, 4), out["masks"]["pool2"], (N, 50, 8, 8), capi.MAX,
+                        (2, 2), (2, 2))
+    g2 = host(net.net_get_blob("conv2", PN_DIFF))
+    assert_close("conv2 diff (ip1 dgrad + unpool)", g2, G2, Sg2, rtol)
+    # unpooling routes each gradient to its origin only: exact zeros elsewhere
+    off = np.zeros(G2.shape, bool)
+    m2 = out["masks"]["pool2"]
+    hh, ww = np.meshgrid(np.arange(8), np.arange(8), indexing="ij")
+    off = m2[:, :, hh // 2, ww // 2] != (hh * 8 + ww)[None, None]
+    assert_bitwise("conv2 diff off-origin zeros", g2[off], np.zeros(int(off.sum()), np.float32), zero_sign=False)
     # conv2 backward from the oracle's G2
     net.net_put_blob("conv2", G2.astype(np.float32), PN_DIFF)
     for name in net.stages(1):
         if name.startswith("conv2."):
             run(net, 1, name)
     run(net, 1, "conv.bucket_reduce")
-    assert_close("dp1", host(net.net_get_blob("pool1", PN_DIFF)), gref["diffs"]["conv2"], gs["conv2.dx"], rtol)
+    assert_close("dp1 (conv2 dgrad)", host(net.net_get_blob("pool1", PN_DIFF)), gref["diffs"]["conv2"],
+                 gs["conv2.dx"], rtol)
     assert_close("conv2.w grad", host(net.net_get_blob("conv2.w", PN_DIFF)), gref["grads"]["conv2.w"],
                  gs["conv2.w"], rtol)
     if tf32:
@@ -285,8 +377,9 @@ def test_teacher_forced_fused_stages(tf32):
 @pytest.mark.parametrize("tf32", [False, True])
 def test_full_size_bench_configuration(tf32):
     """BASELINE config 3 per GPU (N=512) in the launch configuration bench.py
-    times (graph-replayed net_train_step): loss, predictions and every
-    parameter gradient vs the oracle at full size."""
+    times (graph-replayed net_train_step): loss by plain relative error,
+    predictions exact up to capped near-ties, every parameter gradient
+    norm-wise at rtol."""
     N = 512
     rtol = RTOL[tf32]
     net, ref, params, x, y = make("lenet", N, tf32)
@@ -296,15 +389,22 @@ def test_full_size_bench_configuration(tf32):
     net.net_train_step(xd, yd, sgd, 0, loss)
     net.net_sync_errors()
     out = ref.forward(x, y)
-    seff = effective_scales(ref, out)
     gref = ref.backward()
-    assert abs(loss.item() - out["loss"]) <= rtol * (1 + float(seff["logits"].max()))
-    check_pred(host(net.net_get_blob("pred")), out["pred"], out["logits"], seff["logits"], rtol)
-    # gradients were overwritten by nothing after backward: the step's SGD
-    # used them; compare them norm-wise
+    rel = abs(loss.item() - out["loss"]) / out["loss"]
+    report("loss (graph step)", kind="relative", rel_err=rel, bound=rtol)
+    assert rel <= rtol
+    gpu = {L["top"]: host(net.net_get_blob(L["top"])) for L in ref.layers
+           if L["type"] != "SoftmaxWithLoss" and net.blobs.get(L["top"], {}).get("materialised", False)}
+    bnd, _ = chain_bounds(ref, out, gpu, rtol)
+    pred = host(net.net_get_blob("pred")).ravel()
+    tol = np.zeros(N)
+    for i in np.flatnonzero(pred != out["pred"]):
+        tol[i] = bnd["logits"][i, pred[i]] + bnd["logits"][i, out["pred"][i]]
+    check_pred(pred, out["pred"], out["logits"], tol, name="pred (graph step)")
+    # the step's SGD used these gradients (nothing overwrites them after backward)
     for k in params:
         g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
-        assert_norm(f"grad {k}", g, gref["grads"][k], 10 * rtol)
+        assert_norm(f"grad {k} (graph step)", g, gref["grads"][k], rtol)
 
 
 # --------------------------------------------------------- data parallel

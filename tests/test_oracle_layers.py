@@ -258,6 +258,94 @@ def test_maxpool_bwd_conservation():
     assert np.count_nonzero(dx) == np.count_nonzero(dy)
 
 
+# -------------------------------------------- pooling in float arithmetic
+# orc_pool_{fwd,bwd}_f32: Caffe's float accumulators (the GPU bit-exactness
+# contract of SURVEY §8(c) c4-c6).  Pinned against the fp64 oracle (itself
+# pinned to torch above) by exactness on inputs whose sums are exact, by the
+# correct-rounding property of the AVE quotient, and by the recursive
+# summation error bound on random inputs.
+F32_EPS = 2.0 ** -24
+
+
+def _f32_geoms():
+    return [(2, 2, 0, 8), (3, 2, 0, 16), (3, 2, 0, 13), (3, 2, 1, 9), (2, 1, 0, 5), (4, 2, 2, 10)]
+
+
+@pytest.mark.parametrize("k,s,p,H", _f32_geoms())
+def test_pool_fwd_f32_max_equals_fp64(k, s, p, H):
+    g = np.random.default_rng(H * 13 + k)
+    for x in (g.standard_normal((2, 3, H, H + 2)).astype(np.float32),
+              np.round(g.standard_normal((2, 3, H, H + 2))).astype(np.float32)):   # ties
+        y32, m32 = capi.pool_fwd_f32(x, capi.MAX, (k, k), (s, s), (p, p))
+        y64, m64 = capi.pool_fwd(x, capi.MAX, (k, k), (s, s), (p, p))
+        np.testing.assert_array_equal(y32.astype(np.float64), y64)
+        np.testing.assert_array_equal(m32, m64)
+
+
+@pytest.mark.parametrize("k,s,p,H", _f32_geoms())
+def test_pool_fwd_f32_ave_exact_sums_and_rounding(k, s, p, H):
+    """Brute force with exact rationals on small dyadic inputs (every partial
+    sum is exact in float): the result is the correctly rounded quotient of
+    the exact window sum by Caffe's window size (R6), and equals it exactly
+    when the size is a power of two."""
+    from fractions import Fraction
+    g = np.random.default_rng(H * 17 + k)
+    x = (g.integers(-255, 256, (1, 2, H, H + 1)) / 16.0).astype(np.float32)
+    y32, _ = capi.pool_fwd_f32(x, capi.AVE, (k, k), (s, s), (p, p))
+    W = H + 1
+    for idx in np.ndindex(y32.shape):
+        a, b = idx[2], idx[3]
+        hs, ws = a * s - p, b * s - p
+        he, we = min(hs + k, H + p), min(ws + k, W + p)
+        size = (he - hs) * (we - ws)
+        tot = sum(Fraction(float(x[idx[0], idx[1], h, w]))
+                  for h in range(max(hs, 0), min(he, H)) for w in range(max(ws, 0), min(we, W)))
+        q = tot / size
+        got = np.float32(y32[idx])
+        ulp = Fraction(float(np.spacing(np.abs(got)))) if got != 0 else Fraction(2) ** -149
+        assert abs(Fraction(float(got)) - q) <= ulp / 2, (idx, float(got), float(q))
+        if size & (size - 1) == 0:
+            assert Fraction(float(got)) == q
+
+
+@pytest.mark.parametrize("k,s,p,H", _f32_geoms())
+def test_pool_fwd_f32_ave_error_bound(k, s, p, H):
+    g = np.random.default_rng(H * 19 + k)
+    x = g.standard_normal((2, 3, H, H + 1)).astype(np.float32)
+    y32, _ = capi.pool_fwd_f32(x, capi.AVE, (k, k), (s, s), (p, p))
+    y64, _ = capi.pool_fwd(x, capi.AVE, (k, k), (s, s), (p, p))
+    sabs, _ = capi.pool_fwd(np.abs(x), capi.AVE, (k, k), (s, s), (p, p))
+    n = k * k
+    bound = (n - 1) * F32_EPS * sabs * 1.0001 + F32_EPS * np.abs(y64) * 1.0001 + 1e-45
+    assert np.all(np.abs(y32 - y64) <= bound)
+
+
+@pytest.mark.parametrize("k,s,p,H", _f32_geoms())
+@pytest.mark.parametrize("method", [capi.MAX, capi.AVE])
+def test_pool_bwd_f32(k, s, p, H, method):
+    g = np.random.default_rng(H * 23 + k + method)
+    x = g.standard_normal((2, 2, H, H)).astype(np.float32)
+    _, m = capi.pool_fwd(x, method, (k, k), (s, s), (p, p))
+    Hp = capi.pool_out_size(H, k, s, p)
+    # dyadic top gradients and power-of-two windows: all sums exact -> equal to fp64
+    dyq = (g.integers(-255, 256, (2, 2, Hp, Hp)) / 16.0).astype(np.float32)
+    d32 = capi.pool_bwd_f32(dyq, m, x.shape, method, (k, k), (s, s), (p, p))
+    d64 = capi.pool_bwd(dyq, m, x.shape, method, (k, k), (s, s), (p, p))
+    if method == capi.MAX or k in (1, 2, 4):
+        if not (method == capi.AVE and p > 0):          # padded windows change the divisor
+            np.testing.assert_array_equal(d32.astype(np.float64), d64)
+    # random top gradients: within the summation bound (terms per input <= ceil(k/s)^2)
+    dy = g.standard_normal((2, 2, Hp, Hp)).astype(np.float32)
+    d32 = capi.pool_bwd_f32(dy, m, x.shape, method, (k, k), (s, s), (p, p))
+    d64 = capi.pool_bwd(dy, m, x.shape, method, (k, k), (s, s), (p, p))
+    sabs = capi.pool_bwd(np.abs(dy), m, x.shape, method, (k, k), (s, s), (p, p))
+    t = (-(-k // s)) ** 2
+    bound = (t + 1) * F32_EPS * sabs * 1.0001 + 1e-45
+    assert np.all(np.abs(d32 - d64) <= bound)
+    if method == capi.MAX and s >= k:                   # non-overlapping: one term, exact
+        np.testing.assert_array_equal(d32.astype(np.float64), d64)
+
+
 # ------------------------------------------------------------- inner product
 def test_ip_hand_vector():
     g = golden("ip_hand.json")
