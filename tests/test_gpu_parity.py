@@ -21,6 +21,7 @@ import torch
 from oracle import capi
 from oracle.net import OracleNet
 from paper_2005_13076_b200 import PN_DIFF, PN_HISTORY, PN_MASK, Net, PnError, make_sgd, spec_text, synth
+import netcheck
 from parity import RTOL, assert_bitwise, assert_close, assert_norm, check_mask, check_pred, report
 
 pytestmark = pytest.mark.gpu
@@ -64,62 +65,69 @@ def run(net, phase, prefix, x=None, y=None):
 
 
 # --------------------------------------------------------------- net level
-def chain_bounds(ref, out, gpu, rtol):
-    """Per-blob error bounds of the GPU chain's forward values.
+def gpu_forward_blobs(net, ref):
+    """The plan's materialised forward blobs (in-place ReLUs: post-activation)."""
+    return {L["top"]: host(net.net_get_blob(L["top"])) for L in ref.layers
+            if L["type"] != "SoftmaxWithLoss" and net.blobs.get(L["top"], {}).get("materialised", False)}
 
-    For a contraction layer (conv / ip): B = rtol * S(own terms) + |W| (*) D,
-    where D is the measured |gpu - oracle| of its input blob when the plan
-    materialises it (else that blob's bound).  MAX pool: the window max of the
-    pre-pool bound (valid whichever element wins); AVE pool: the window mean
-    plus its own rounding; ReLU: unchanged (1-Lipschitz).  Returns (bounds of
-    each layer's output by layer name, pre-pool bounds by pool layer name)."""
-    cur = {ref.input_name: np.zeros(ref.shapes[ref.input_name])}
-    final = {}  # oracle's final value of every blob (after in-place ReLUs)
+
+def gpu_top_diffs(net, ref):
+    """The GPU's gradient w.r.t. each conv / ip layer's output.  The fused
+    LeNet plan never stores conv1's output gradient: it is rebuilt exactly
+    (routing, no arithmetic) from the stored pooled gradient and the GPU's own
+    pool1 origins."""
+    res = {}
     for L in ref.layers:
-        if L["type"] != "SoftmaxWithLoss":
-            final[L["top"]] = out["blobs"][L["name"]]
-    bnd, pre = {}, {}
-
-    def incoming(blob):
-        if blob in gpu:
-            return np.abs(gpu[blob].reshape(final[blob].shape).astype(np.float64) - final[blob])
-        return cur[blob]
-
-    for L in ref.layers:
-        t, nm = L["type"], L["name"]
-        if t == "SoftmaxWithLoss":
-            bnd["logits"] = cur[L["bottom"]].reshape(cur[L["bottom"]].shape[0], -1)
+        if L["type"] not in ("Convolution", "InnerProduct"):
             continue
-        if t == "Convolution":
-            d = incoming(L["bottom"])
-            w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
-            b = rtol * out["scales"][nm]
-            if L["bottom"] != ref.input_name:
-                if L["G"] == 1:
-                    b = b + capi.conv_fwd(d, w, None, L["s"], L["p"])
-                else:
-                    from oracle.net import grouped_conv_fwd
-                    b = b + grouped_conv_fwd(d, w, None, L["G"], L["s"], L["p"])[0]
-        elif t == "InnerProduct":
-            d = incoming(L["bottom"])
-            w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
-            b = rtol * out["scales"][nm] + capi.ip_fwd(d.reshape(d.shape[0], -1), w, None).reshape(
-                out["scales"][nm].shape)
-        elif t == "Pooling":
-            d = incoming(L["bottom"])
-            pre[nm] = d
-            if L["method"] == capi.MAX:
-                b, _ = capi.pool_fwd(d, capi.MAX, L["k"], L["s"], L["p"])
-            else:
-                b, _ = capi.pool_fwd(d, capi.AVE, L["k"], L["s"], L["p"])
-                b = b + rtol * np.abs(out["blobs"][nm])
-        elif t == "ReLU":
-            b = cur[L["bottom"]]
+        if net.blobs[L["top"]]["materialised"] or L["bottom"] != ref.input_name:
+            res[L["name"]] = host(net.net_get_blob(L["top"], PN_DIFF))
         else:
-            b = cur[L["bottom"]]
-        cur[L["top"]] = b
-        bnd[nm] = b
-    return bnd, pre
+            P = [M for M in ref.layers if M["bottom"] == L["top"]][0]
+            dp = host(net.net_get_blob(P["top"], PN_DIFF))
+            m = host(net.net_get_blob(P["top"], PN_MASK))
+            res[L["name"]] = capi.pool_bwd(dp, m, L["out_shape"], capi.MAX, P["k"], P["s"], P["p"])
+    return res
+
+
+def check_net_level(net, ref, params, out, gref, loss_value, rtol, tag="net level"):
+    """Loss by plain relative error; forward blobs, masks, probabilities,
+    predictions and parameter gradients element-wise under the measured-
+    incoming-error bounds of tests/netcheck.py (norm-wise errors reported)."""
+    gpu = gpu_forward_blobs(net, ref)
+    bnd, pre = netcheck.forward_bounds(ref, out, gpu, rtol)
+    for L in ref.layers:
+        top = L["top"]
+        if top not in gpu or L["type"] == "ReLU":
+            continue
+        last = [M for M in ref.layers if M["top"] == top][-1]      # the blob's final writer
+        o = out["blobs"][last["name"]]
+        assert_close(f"{L['name']} ({tag})", gpu[top].reshape(o.shape), o, bnd[last["name"]] / rtol, rtol)
+    for L in ref.layers:
+        if L["type"] == "Pooling" and L["method"] == capi.MAX:
+            pre_layer = [M for M in ref.layers if M["top"] == L["bottom"]][-1]["name"]
+            gm = host(net.net_get_blob(L["top"], PN_MASK))
+            check_mask(f"{L['name']} mask ({tag})", gm, out["masks"][L["name"]], out["blobs"][pre_layer],
+                       pre[L["name"]] / rtol, L["in_shape"][2:], L["k"][0], L["s"][0], L["p"][0], rtol)
+    rel = abs(loss_value - out["loss"]) / abs(out["loss"])
+    report(f"loss ({tag})", kind="relative", rel_err=rel, bound=rtol)
+    assert rel <= rtol, (loss_value, out["loss"])
+    blg = bnd["logits"]
+    p = out["prob"]
+    prob = host(net.net_get_blob("prob")).reshape(p.shape)
+    pb = p * (blg + (p * blg).sum(1, keepdims=True)) * 1.01 + RTOL[False] * p + 1e-30
+    assert_close(f"prob ({tag})", prob, p, pb / rtol, rtol)
+    pred = host(net.net_get_blob("pred")).ravel()
+    tol = np.zeros(pred.size)
+    for i in np.flatnonzero(pred != out["pred"]):
+        tol[i] = blg[i, pred[i]] + blg[i, out["pred"][i]]
+    check_pred(pred, out["pred"], out["logits"], tol, name=f"pred ({tag})")
+    gb = netcheck.gradient_bounds(ref, out, gref, gpu, gpu_top_diffs(net, ref), rtol)
+    for k in params:
+        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
+        report(f"grad {k} ({tag})", kind="normwise(info)", rel_err=np.linalg.norm(g - gref["grads"][k]) /
+               (np.linalg.norm(gref["grads"][k]) + 1e-30))
+        assert_close(f"grad {k} ({tag})", g, gref["grads"][k], gb[k] / rtol, rtol)
 
 
 @pytest.mark.parametrize("spec,N,tf32,layerwise", [
@@ -145,49 +153,7 @@ def test_net_forward_backward(spec, N, tf32, layerwise):
     net.net_sync_errors()
     out = ref.forward(x, y)
     gref = ref.backward()
-    # the materialised forward blobs (in-place ReLUs: the post-activation value)
-    gpu = {}
-    for L in ref.layers:
-        top = L["top"]
-        if L["type"] == "SoftmaxWithLoss" or not net.blobs.get(top, {}).get("materialised", False):
-            continue
-        gpu[top] = host(net.net_get_blob(top))
-    bnd, pre = chain_bounds(ref, out, gpu, rtol)
-    for L in ref.layers:
-        top = L["top"]
-        if top not in gpu or L["type"] == "ReLU":
-            continue
-        last = [M for M in ref.layers if M["top"] == top][-1]      # the blob's final writer
-        o = out["blobs"][last["name"]]
-        assert_close(f"{L['name']} (net level)", gpu[top].reshape(o.shape), o, bnd[last["name"]] / rtol, rtol)
-    # masks: exact up to listed near-ties of the pre-pool values under their bound
-    for L in ref.layers:
-        if L["type"] == "Pooling" and L["method"] == capi.MAX:
-            pre_layer = [M for M in ref.layers if M["top"] == L["bottom"]][-1]["name"]
-            gm = host(net.net_get_blob(L["top"], PN_MASK))
-            check_mask(L["name"] + " mask (net level)", gm, out["masks"][L["name"]], out["blobs"][pre_layer],
-                       pre[L["name"]] / rtol, L["in_shape"][2:], L["k"][0], L["s"][0], L["p"][0], rtol)
-    # loss by plain relative error
-    rel = abs(loss.item() - out["loss"]) / abs(out["loss"])
-    report("loss (net level)", kind="relative", rel_err=rel, bound=rtol)
-    assert rel <= rtol, (loss.item(), out["loss"])
-    # probabilities: softmax of logits within their bound (first order)
-    blg = bnd["logits"]
-    prob = host(net.net_get_blob("prob")).reshape(out["prob"].shape)
-    p = out["prob"]
-    pb = p * (blg + (p * blg).sum(1, keepdims=True)) * 1.01 + RTOL[False] * p + 1e-30
-    assert_close("prob (net level)", prob, p, pb / rtol, rtol)
-    # predictions: exact up to near-ties of the oracle logits under the logit bound
-    pred = host(net.net_get_blob("pred")).ravel()
-    g = pred
-    tol = np.zeros(N)
-    for i in np.flatnonzero(g != out["pred"]):
-        tol[i] = blg[i, g[i]] + blg[i, out["pred"][i]]
-    check_pred(pred, out["pred"], out["logits"], tol, name="pred (net level)")
-    # parameter gradients: norm-wise at rtol
-    for k in params:
-        gg = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
-        assert_norm(f"grad {k} (net level)", gg, gref["grads"][k], rtol)
+    check_net_level(net, ref, params, out, gref, loss.item(), rtol)
 
 
 def test_train_step_graph_equals_eager_and_is_deterministic():
@@ -378,8 +344,8 @@ def test_teacher_forced_fused_stages(tf32, N):
 def test_full_size_bench_configuration(tf32):
     """BASELINE config 3 per GPU (N=512) in the launch configuration bench.py
     times (graph-replayed net_train_step): loss by plain relative error,
-    predictions exact up to capped near-ties, every parameter gradient
-    norm-wise at rtol."""
+    forward blobs, masks, predictions and every parameter gradient under the
+    net-level bounds (the step's SGD consumed exactly these gradients)."""
     N = 512
     rtol = RTOL[tf32]
     net, ref, params, x, y = make("lenet", N, tf32)
@@ -390,21 +356,7 @@ def test_full_size_bench_configuration(tf32):
     net.net_sync_errors()
     out = ref.forward(x, y)
     gref = ref.backward()
-    rel = abs(loss.item() - out["loss"]) / out["loss"]
-    report("loss (graph step)", kind="relative", rel_err=rel, bound=rtol)
-    assert rel <= rtol
-    gpu = {L["top"]: host(net.net_get_blob(L["top"])) for L in ref.layers
-           if L["type"] != "SoftmaxWithLoss" and net.blobs.get(L["top"], {}).get("materialised", False)}
-    bnd, _ = chain_bounds(ref, out, gpu, rtol)
-    pred = host(net.net_get_blob("pred")).ravel()
-    tol = np.zeros(N)
-    for i in np.flatnonzero(pred != out["pred"]):
-        tol[i] = bnd["logits"][i, pred[i]] + bnd["logits"][i, out["pred"][i]]
-    check_pred(pred, out["pred"], out["logits"], tol, name="pred (graph step)")
-    # the step's SGD used these gradients (nothing overwrites them after backward)
-    for k in params:
-        g = host(net.net_get_blob(k, PN_DIFF)).reshape(gref["grads"][k].shape)
-        assert_norm(f"grad {k} (graph step)", g, gref["grads"][k], rtol)
+    check_net_level(net, ref, params, out, gref, loss.item(), rtol, tag="graph step")
 
 
 # --------------------------------------------------------- data parallel
