@@ -9,12 +9,14 @@ materialises (|gpu - oracle| element by element), never a worst case:
 
   forward contraction   B(y)  = rtol*S(y) + |W| (*) |dX|
   MAX pool              B(y)  = window max of the pre-pool bound
-  AVE pool              B(y)  = window mean of the pre-pool bound + own rounding
+  AVE pool              B(y)  = window mean of the pre-pool bound + own rounding (rtol * |y|)
   ReLU                  B(y)  = B(x)                         (1-Lipschitz)
   weight gradient       B(dW) = rtol*S(dW) + WG(|dG|, |X|) + WG(|G| + |dG|, |dX|)
   bias gradient         B(db) = rtol*S(db) + sum |dG|
 
-with dG / dX the measured errors of the layer's top gradient and input, and
+(the propagated terms carry a factor 1 + rtol: the kernel's own bound on
+the GPU's terms, rtol * S(gpu terms), exceeds rtol * S(oracle terms) by at
+most rtol times them) with dG / dX the measured errors of the layer's top gradient and input, and
 WG the layer's own weight-gradient contraction (conv: sum over images and
 positions; inner product: dy^T x).  Where the fused LeNet plan does not store
 conv1's output gradient, the GPU's is rebuilt exactly from its stored pooled
@@ -56,18 +58,18 @@ def forward_bounds(ref, out, gpu, rtol):
             b = rtol * out["scales"][nm]
             if L["bottom"] != ref.input_name:
                 w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
-                b = b + grouped_conv_fwd(incoming(L["bottom"]), w, None, L["G"], L["s"], L["p"])[0]
+                b = b + (1 + rtol) * grouped_conv_fwd(incoming(L["bottom"]), w, None, L["G"], L["s"], L["p"])[0]
         elif t == "InnerProduct":
             d = incoming(L["bottom"])
             w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
-            b = rtol * out["scales"][nm] + capi.ip_fwd(d.reshape(d.shape[0], -1), w, None).reshape(
+            b = rtol * out["scales"][nm] + (1 + rtol) * capi.ip_fwd(d.reshape(d.shape[0], -1), w, None).reshape(
                 out["scales"][nm].shape)
         elif t == "Pooling":
             d = incoming(L["bottom"])
             pre[nm] = d
             b, _ = capi.pool_fwd(d, L["method"], L["k"], L["s"], L["p"])
-            if L["method"] == capi.AVE:
-                b = b + rtol * np.abs(out["blobs"][nm])
+            if L["method"] == capi.AVE:  # + its own fp32 rounding, relative to the GPU's value
+                b = b * (1 + rtol) + rtol * np.abs(out["blobs"][nm])
         elif t == "Softmax":
             # first order: |dp_j| <= p_j (|dz_j| + sum_k p_k |dz_k|), plus its own rounding
             d = cur[L["bottom"]].reshape(cur[L["bottom"]].shape[0], -1)
@@ -110,18 +112,20 @@ def gradient_bounds(ref, out, gref, gpu_data, gpu_top_diff, rtol):
         if t == "Convolution":
             xin = np.abs(Xo) if Xo is not None else np.abs(ref._blobs[ref.input_name])
             w = np.abs(ref.params[nm + ".w"]).astype(np.float64)
-            bw = rtol * gs[nm + ".w"] + grouped_conv_bwd(dG, xin, w, L["G"], L["s"], L["p"], want_dx=False)[0]
+            prop = grouped_conv_bwd(dG, xin, w, L["G"], L["s"], L["p"], want_dx=False)[0]
             if dX is not None:
-                bw = bw + grouped_conv_bwd(np.abs(Go) + dG, dX, w, L["G"], L["s"], L["p"], want_dx=False)[0]
-            bb = rtol * gs[nm + ".b"] + dG.sum(axis=(0, 2, 3))
+                prop = prop + grouped_conv_bwd(np.abs(Go) + dG, dX, w, L["G"], L["s"], L["p"], want_dx=False)[0]
+            bw = rtol * gs[nm + ".w"] + (1 + rtol) * prop
+            bb = rtol * gs[nm + ".b"] + (1 + rtol) * dG.sum(axis=(0, 2, 3))
         else:
             M = Go.shape[0]
             g2, dg2 = np.abs(Go).reshape(M, -1), dG.reshape(M, -1)
             xin = np.abs(Xo if Xo is not None else ref._blobs[ref.input_name]).reshape(M, -1)
-            bw = rtol * gs[nm + ".w"] + dg2.T @ xin
+            prop = dg2.T @ xin
             if dX is not None:
-                bw = bw + (g2 + dg2).T @ dX.reshape(M, -1)
-            bb = rtol * gs[nm + ".b"] + dg2.sum(axis=0)
+                prop = prop + (g2 + dg2).T @ dX.reshape(M, -1)
+            bw = rtol * gs[nm + ".w"] + (1 + rtol) * prop
+            bb = rtol * gs[nm + ".b"] + (1 + rtol) * dg2.sum(axis=0)
         res[nm + ".w"] = bw
         res[nm + ".b"] = bb
     return res
