@@ -201,11 +201,13 @@ pn_status net_stage_name(const pn_net* net, int phase, int i,
 pn_status net_run_stage(pn_net* net, int phase, int i, const float* x,
                         const int32_t* labels, void* stream);
 /* Per-stage kernel durations on `stream`: one pass through the plan in order
- * (x, labels, sgd, iter as for net_train_step); every forward / backward
- * kernel stage is launched once, then `steps` times back to back between two
- * CUDA events (each overwrites its outputs from inputs it does not write), so
- * ms_out[phase-major stage order] = mean milliseconds per launch without
- * per-launch host gaps; the solver and non-kernel stages run once.
+ * (x, labels, sgd, iter as for net_train_step); every kernel stage is
+ * launched once, then captured `steps` times back to back into a CUDA graph
+ * that is replayed between two CUDA events, so ms_out[phase-major stage
+ * order] = mean device milliseconds per launch (kernel + in-graph launch
+ * gap, no host launch rate).  Forward / backward stages overwrite their
+ * outputs from inputs they do not write; the solver stage applies `steps`
+ * updates (profiling changes the parameters).  Non-kernel stages report 0.
  * Synchronises.  n_out: number of entries written (cap >= total stages). */
 pn_status net_profile_stages(pn_net* net, const float* x,
                              const int32_t* labels, const pn_sgd* sgd,

@@ -925,8 +925,11 @@ static void build_fused_lenet(pn_net* net) {
     const int per = (int)cdiv((long long)N * 144, blocks);
     Conv1Pool1P p{nullptr, P + c1.off, P + c1.off + 500, p1.data, p1.m8, N, net->tf32 ? 1 : 0, net->p1c, per};
     Launch l;
-    l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(C1_THREADS), 0, p);
-    add(fwd, "conv1+pool1", l, [net](Launch& l, const StepArgs& a) {
+    if (net->tf32 && !getenv("PN_C1_SIMT"))  // TF32 plan: implicit GEMM on the tensor cores (tc_conv1.cu)
+      l = tc::conv1_pool1_tc_launch(p, net->tc_sms);
+    else
+      l.set((const void*)lenet_conv1_pool1, dim3(cdiv((long long)N * 144, per)), dim3(C1_THREADS), 0, p);
+    add(fwd, net->tf32 && !getenv("PN_C1_SIMT") ? "conv1+pool1[tc]" : "conv1+pool1", l, [net](Launch& l, const StepArgs& a) {
       Conv1Pool1P& q = l.params<Conv1Pool1P>();
       q.x = a.x, q.x8 = a.x8, q.x_scale = net->x_scale, q.x_mean = net->x_mean;
     });
@@ -1873,26 +1876,47 @@ extern "C" pn_status net_profile_stages(pn_net* net, const float* x, const int32
   cudaEvent_t e0, e1;
   CU(cudaEventCreate(&e0));
   CU(cudaEventCreate(&e1));
-  // one pass through the plan in order; every kernel stage of the forward and
-  // backward (idempotent: each overwrites its outputs from inputs it does not
-  // write) is launched once to warm up, then `steps` times back to back
-  // between two events -- the mean is the kernel's duration without the
-  // host-side launch gaps of one-launch-per-event timing.  The solver
-  // (state-changing) and non-kernel stages (events, collectives) run once.
+  // one pass through the plan in order.  Every kernel stage (each overwrites
+  // its outputs from inputs it does not write, so repeats are idempotent --
+  // except the solver, which then applies `steps` updates: the net's
+  // parameters are changed by profiling) is captured `steps` times back to
+  // back into one CUDA graph and replayed between two events: the mean is the
+  // kernel's device duration plus the graph's launch-to-launch gap, without
+  // the host launch rate (which bounds eager back-to-back launches on a slow
+  // host).  Non-kernel stages (events, collectives) report 0.
   StepArgs a = make_args(net, x, labels, nullptr, sgd, iter);
+  if (!net->cap) CU(cudaStreamCreateWithFlags(&net->cap, cudaStreamNonBlocking));
   int k = 0;
   for (int ph = 0; ph < 3; ++ph)
     for (auto& stg : net->phase[ph]) {
-      const bool rep = ph < 2 && !stg.custom;
-      if (rep) TRY(run_stage(net, stg, a, st));
+      if (stg.custom) {
+        ms_out[k++] = 0.f;
+        continue;
+      }
+      TRY(run_stage(net, stg, a, st));
+      CU(cudaStreamSynchronize(st));
+      cudaGraph_t g = nullptr;
+      cudaGraphExec_t ge = nullptr;
+      CU(cudaStreamBeginCapture(net->cap, cudaStreamCaptureModeThreadLocal));
+      pn_status cs = PN_OK;
+      for (int i = 0; i < steps && cs == PN_OK; ++i) cs = run_stage(net, stg, a, net->cap);
+      cudaError_t ce = cudaStreamEndCapture(net->cap, &g);
+      if (cs != PN_OK) {
+        if (g) cudaGraphDestroy(g);
+        return cs;
+      }
+      CU(ce);
+      CU(cudaGraphInstantiate(&ge, g, 0));
+      CU(cudaGraphLaunch(ge, st));  // warm
       CU(cudaEventRecord(e0, st));
-      const int r = rep ? steps : 1;
-      for (int i = 0; i < r; ++i) TRY(run_stage(net, stg, a, st));
+      CU(cudaGraphLaunch(ge, st));
       CU(cudaEventRecord(e1, st));
       CU(cudaEventSynchronize(e1));
       float ms = 0.f;
       CU(cudaEventElapsedTime(&ms, e0, e1));
-      ms_out[k++] = ms / r;
+      ms_out[k++] = ms / steps;
+      cudaGraphExecDestroy(ge);
+      cudaGraphDestroy(g);
     }
   if (n_out) *n_out = total;
   cudaEventDestroy(e0);

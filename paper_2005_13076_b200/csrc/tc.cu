@@ -1119,7 +1119,7 @@ cudaError_t setup() {
   if ((e = cudaFuncSetAttribute((const void*)conv2_fwd_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 cf::SMEM)) != cudaSuccess)
     return e;
-  return cudaSuccess;
+  return conv1_setup();
 }
 
 bool tensor_maps_ok() { return g_tmap_ok; }

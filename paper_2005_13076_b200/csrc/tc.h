@@ -9,6 +9,7 @@
 
 #include <cstddef>
 
+#include "params.h"
 #include "runtime.h"
 
 namespace pn {
@@ -41,5 +42,9 @@ Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_
 int db2_partials(int N);  // conv2 bias-gradient partial rows written by ip1_dgrad_unpool
 Launch conv2_dgrad_launch(const float* g2, const float* w2t, float* dp1, int N, int sms);
 Launch conv2_wgrad_launch(const float* g2, const float* p1, float* part, int splits, int N);
+// conv1 + pool1 on the tensor cores (tc_conv1.cu): implicit GEMM over 128-row
+// tiles of (pooled position, window slot), quad-shuffle pooling epilogue
+cudaError_t conv1_setup();
+Launch conv1_pool1_tc_launch(const Conv1Pool1P& p, int sms);
 }  // namespace tc
 }  // namespace pn

@@ -241,11 +241,13 @@ def test_teacher_forced_fused_stages(tf32, N):
     # conv1 + pool1 (input x)
     run(net, 0, "conv1+pool1", xd, yd)
     S1, _ = capi.pool_fwd(sc["conv1"], capi.MAX, (2, 2), (2, 2))
-    # conv1 is fp32 SIMT in both plans; the TF32 plan stores pool1 rounded to
-    # TF32 (its only consumers are conv2's contractions): rtol of that plan
+    # conv1 runs on the tensor cores (TF32 operands) in the TF32 plan, fp32
+    # SIMT in the fp32 plan; the TF32 plan stores pool1 rounded to TF32 (its
+    # only consumers are conv2's contractions): rtol of that plan
     assert_close("pool1", host(net.net_get_blob("pool1")), out["blobs"]["pool1"], S1, rtol)
     check_mask("pool1 mask", host(net.net_get_blob("pool1", PN_MASK)), out["masks"]["pool1"],
-               out["blobs"]["conv1"], sc["conv1"], (24, 24), 2, 2, 0, RTOL[False])
+               out["blobs"]["conv1"], sc["conv1"], (24, 24), 2, 2, 0, rtol,
+               max_excused=max(1, out["masks"]["pool1"].size // 200))
     # conv2 + pool2 from the oracle's pool1
     net.net_put_blob("pool1", out["blobs"]["pool1"].astype(np.float32))
     run(net, 0, "conv2+pool2")

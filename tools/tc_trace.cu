@@ -3,6 +3,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DPN_TRACE -I paper_2005_13076_b200/csrc \
 //        -o tools/tc_trace tools/tc_trace.cu -lcuda
 #include "../paper_2005_13076_b200/csrc/tc.cu"
+#include "../paper_2005_13076_b200/csrc/tc_conv1.cu"
 
 #include <cstdio>
 #include <vector>
@@ -100,8 +101,45 @@ static int dgrad_main(int N) {
   return 0;
 }
 
+static int conv1_main(int N) {
+  float *x, *w, *b, *p1, *p1c;
+  uint8_t* m1;
+  cudaMalloc(&x, (size_t)N * 784 * 4);
+  cudaMalloc(&w, 500 * 4);
+  cudaMalloc(&b, 20 * 4);
+  cudaMalloc(&p1, (size_t)N * 2880 * 4);
+  cudaMalloc(&p1c, (size_t)((N + 1) / 2) * kP1cPairFloats * 4);
+  cudaMalloc(&m1, (size_t)N * 2880);
+  cudaMemset(x, 0, (size_t)N * 784 * 4);
+  cudaMemset(w, 0, 2000);
+  cudaMemset(b, 0, 80);
+  if (setup() != cudaSuccess) { printf("setup failed\n"); return 1; }
+  Conv1Pool1P p{x, w, b, p1, m1, N, 1, p1c, 0, nullptr, 1.f, nullptr};
+  Launch l = conv1_pool1_tc_launch(p, 148);
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  printf("conv1_pool1_tc N=%d grid %d: %.2f us/launch (%s)\n", N, l.grid.x, time_launch(l, st, 50),
+         cudaGetErrorString(cudaGetLastError()));
+  const int ks[] = {0, 1, 2, 3, 4, 5, 6, 7, 8};
+  dump("cta  start  pro  built0  mma0  built_all  mma_all  acc0  epi_end  end", ks, 9, l.grid.x);
+  {
+    std::vector<unsigned long long> t(4096), tr(148 * 16);
+    cudaMemcpyFromSymbol(t.data(), g_trace0, t.size() * 8);
+    cudaMemcpyFromSymbol(tr.data(), g_trace, tr.size() * 8);
+    const unsigned long long t0 = tr[0];
+    printf("CTA 0 (ns from its start): bld:start loaded stored | bld:batch_go | mma:afull accfree | epi:mdone tile_ld\n");
+    for (int it = 0; it < 16; ++it) {
+      printf("%2d", it);
+      for (int k = 1000; k <= 1700; k += 100) printf(" %6lld", t[k + it] ? (long long)(t[k + it] - t0) : -1ll);
+      printf("\n");
+    }
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
   const int N = argc > 1 ? atoi(argv[1]) : 512;
+  if (argc > 2 && argv[2][0] == 'c') return conv1_main(N);
   if (argc > 2 && argv[2][0] == 'D') return dgrad_main(N);
   if (argc > 2 && argv[2][0] == 'w') return wgrad_main(N);
   if (argc > 2 && (argv[2][0] == 'f' || argv[2][0] == 'g' || argv[2][0] == 'd')) return ip_main(N, argv[2][0]);
