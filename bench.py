@@ -52,13 +52,55 @@ WORKLOADS = {
 
 
 def peaks():
+    """Roofline denominators: HBM copy GB/s and bf16 from the driver's
+    MEASURED_PEAKS.json (else the profiling guide's fallback); TF32 and FP32
+    (SGEMM) dense peaks measured with cuBLAS on this pool's B200s by
+    tools/measure_peaks.py (profiles/measured_peaks_tf32.json), burst for a
+    kernel timed alone, sustained for a kernel timed inside a long step."""
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as f:
             p = json.load(f)
-        return {"hbm": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sus": p["bf16_tflops_sustained"],
-                "sm_max_mhz": p.get("sm_max_mhz", 1965.0), "src": "measured"}
-    return {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+        pk = {"hbm": p["hbm_gbs"], "bf16": p["bf16_tflops"], "bf16_sus": p["bf16_tflops_sustained"],
+              "sm_max_mhz": p.get("sm_max_mhz", 1965.0), "src": "measured"}
+    else:
+        pk = {"hbm": 6650.0, "bf16": 1590.0, "bf16_sus": 1400.0, "sm_max_mhz": 1965.0, "src": "fallback"}
+    tpath = os.path.join(ROOT, "profiles", "measured_peaks_tf32.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            t = json.load(f)
+        pk.update(tf32=t["tf32_tflops"], tf32_sus=t["tf32_tflops_sustained"], fp32=t["fp32_tflops_sustained"],
+                  tf32_src="measured (cuBLAS TF32 8192^3, profiles/measured_peaks_tf32.json)")
+    else:  # nominal TF32/bf16 ratio x measured bf16
+        pk.update(tf32=pk["bf16"] * 1.1 / 2.25, tf32_sus=pk["bf16_sus"] * 1.1 / 2.25,
+                  fp32=148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12, tf32_src="bf16 x 1.1/2.25 (derived)")
+    return pk
+
+
+# SURVEY.md §8(d) / App. A: LeNet per-layer compulsory work per image (FLOP,
+# bytes) and per-step constant bytes (weights), unfused -- the per-layer
+# roofline the north star's "% of layer roofline" is defined on.
+LENET_LAYERS = [  # (phase, layer, flop/img, bytes/img, const bytes, contraction?)
+    ("F", "conv1", 576000, 49216, 2080, True), ("F", "pool1", 8640, 69120, 0, False),
+    ("F", "conv2", 3200000, 24320, 100200, True), ("F", "pool2", 2400, 19200, 0, False),
+    ("F", "ip1", 800000, 5200, 1602000, True), ("F", "relu1", 500, 4000, 0, False),
+    ("F", "ip2", 10000, 2040, 20040, True), ("F", "softmax+loss", 60, 88, 0, False),
+    ("B", "softmax-loss bwd", 20, 84, 0, False), ("B", "ip2 bwd", 20000, 4040, 40080, True),
+    ("B", "relu1 bwd", 500, 6000, 0, False), ("B", "ip1 bwd", 1600000, 8400, 3204000, True),
+    ("B", "pool2 bwd", 800, 19200, 0, False), ("B", "conv2 bwd", 6400000, 35840, 200400, True),
+    ("B", "pool1 bwd", 2880, 69120, 0, False), ("B", "conv1 bwd", 576000, 49216, 4160, True),
+]
+
+
+def lenet_layer_roofline(N, pk, contraction_peak):
+    """T_roof = sum over layers of max(FLOP / P_pipe, bytes / BW_HBM) + the
+    solver (431,080 params x 20 B), SURVEY §8(d)."""
+    t = 0.0
+    for _ph, _name, fl, by, cb, contr in LENET_LAYERS:
+        flops, byts = fl * N, by * N + cb
+        t += max(flops / (contraction_peak * 1e12) if contr else 0.0, byts / (pk["hbm"] * 1e9))
+    t += 431080 * 20 / (pk["hbm"] * 1e9)
+    return t
 
 
 # Algorithmic work per launch of each stage at batch N (DESIGN.md "Roofline"):
@@ -89,6 +131,31 @@ def stage_work(name, N):
     if base.endswith(".wgrad_reduce"):
         return (0, 0)
     return table.get(base)
+
+
+def stage_roofline(dom, pk, tf32):
+    """Roofline of one stage timed alone (burst peaks): achieved algorithmic
+    FLOP/s or bytes/s of its launch vs the bound that limits it."""
+    flops, byts = dom["flops"] or 0, dom["bytes"] or 0
+    is_tc = "[tc]" in dom["stage"] and tf32
+    fpeak = pk["tf32"] if is_tc else pk["fp32"]
+    t_f = flops / (fpeak * 1e12) if flops else 0.0
+    t_b = byts / (pk["hbm"] * 1e9) if byts else 0.0
+    sec = dom["ms"] / 1e3
+    if t_f >= t_b and flops:
+        roof = {"bound": "tensor" if is_tc else "alu", "achieved": flops / sec / 1e12, "peak": fpeak,
+                "unit": "TFLOP/s"}
+        src = (f"TF32 burst, {pk['tf32_src']}" if is_tc else
+               "FP32 SGEMM sustained (cuBLAS, profiles/measured_peaks_tf32.json)")
+    else:
+        roof = {"bound": "hbm", "achieved": byts / sec / 1e9, "peak": pk["hbm"], "unit": "GB/s"}
+        src = f"HBM copy GB/s, {pk['src']} MEASURED_PEAKS.json"
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel"] = dom["stage"]
+    roof["us"] = dom["ms"] * 1e3
+    roof["traffic"] = None
+    roof["peak_source"] = src
+    return roof
 
 
 def parse_layers(text):
@@ -155,8 +222,10 @@ def layer_stage_work(layers, name, N):
         table = {
             "fwd": (fl, cin + cout + P), "wgrad": (fl, cin + cout + P), "dgrad": (fl, cin + cout + P),
             "bgrad": (0, cout + P), "wpack": (0, 2 * P), "wpack_dgrad": (0, 2 * P), "wgrad_reduce": (0, 2 * P),
-            "nhwc": (0, 2 * cin), "dgrad.nhwc": (0, 2 * cout), "wgrad.gm": (0, 2 * cout),
-            "im2col": (0, cin + M * K * 4), "wgrad.im2col": (0, cin + M * (K + 1) * 4),
+            # operand materialisation (NHWC copies, im2col, Gm) is this
+            # implementation's own traffic, not the layer's algorithmic work
+            "nhwc": (0, 0), "dgrad.nhwc": (0, 0), "wgrad.gm": (0, 0),
+            "im2col": (0, 0), "wgrad.im2col": (0, 0),
         }
         w = table.get(op)
         if w and "+relu_bwd" in name:  # the ReLU output read by the fused backward
@@ -256,9 +325,58 @@ def cpu_baseline(workload="lenet"):
         g = ref.backward()
         ref.sgd_step(g["grads"], 0.01, 0.9, 5e-4, hist)
     dt = time.perf_counter() - t0
-    return {"value": steps * batch / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+    return {"value": steps * batch / dt, "unit": UNIT, "cores": 1, "cpu": cpu_model(), "kind": "oracle",
             "sample": f"{steps} oracle steps x batch {batch} (fwd+bwd+sgd, fp64-accumulate C oracle) of the "
                       f"{workload} batch-{WORKLOADS[workload]['batch']} workload; {dt:.1f} s"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_threaded(workload="lenet", seconds=8.0):
+    """The oracle batch-sharded across all host cores (the analogue of the
+    paper's PHAST std::thread CPU backend, P:41, Table 2): one thread per core,
+    each runs the single-threaded oracle's forward + backward on its shard
+    (the oracle's C calls release the GIL), then the shard gradients are
+    summed in fixed shard order and scaled by 1/shards (R13) and
+    the solver steps once.  A bounded sample: as many steps of a batch of
+    8 images per core as fit in ~`seconds`."""
+    import concurrent.futures
+    import numpy as np
+    cores = len(os.sched_getaffinity(0))
+    per = 8
+    refs = [_oracle_setup(workload, per)[0] for _ in range(cores)]
+    _, gen = _oracle_setup(workload, 1)
+    hist = {}
+    pool = concurrent.futures.ThreadPoolExecutor(max_workers=cores)
+
+    def shard(i, s):
+        x, y = gen(per, s * cores + i)
+        refs[i].forward(x, y)
+        return refs[i].backward()["grads"]
+
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds or done == 0:
+        grads = list(pool.map(lambda i: shard(i, done), range(cores)))
+        g = {k: sum(gr[k] for gr in grads) / cores for k in grads[0]}  # fixed shard order
+        refs[0].sgd_step(g, 0.01, 0.9, 5e-4, hist)
+        for r in refs[1:]:
+            r.set_params(refs[0].params)
+        done += 1
+    dt = time.perf_counter() - t0
+    pool.shutdown()
+    return {"value": done * per * cores / dt, "unit": UNIT, "cores": cores, "cpu": cpu_model(),
+            "kind": "oracle, batch-sharded over host threads",
+            "sample": f"{done} steps x {cores} shards x batch {per} (fwd+bwd+fixed-order shard sum+sgd) of the "
+                      f"{workload} workload; {dt:.1f} s"}
 
 
 def run_reference(args):
@@ -307,6 +425,70 @@ def run_reference(args):
     return 0
 
 
+def fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd):
+    """The paper-precision path (fp32 blobs, fp32-class arithmetic: the
+    PN_FP32 fused plan) on the same workload: device-timed value, end to end
+    from host bytes, and its dominant stage's roofline."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_13076_b200 import Net, synth
+    from paper_2005_13076_b200.dp import dp_bootstrap, max_over_ranks
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    net = Net("lenet", BATCH, device=local, tf32=False)
+    net.set_params(params)
+    if world > 1:
+        dp_bootstrap(net, dist)
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+    for it in range(5):
+        net.net_train_step(X[it % NB], Y[it % NB], sgd, it, loss)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = args.fp32_steps
+    e0.record(stream)
+    for it in range(steps):
+        net.net_train_step(X[it % NB], Y[it % NB], sgd, 5 + it, loss)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        ms = max_over_ranks(ms, dist)
+    rank = int(os.environ.get("RANK", "0"))
+    ring = 30
+    x8, y8 = synth.mnist_like_fast_u8(BATCH * ring, seed=300 + rank)
+    xh = torch.from_numpy(x8).view(ring, BATCH, 1, 28, 28).pin_memory()
+    yh = torch.from_numpy(y8).view(ring, BATCH).pin_memory()
+    net.net_train_steps_u8_host(xh[:3], yh[:3], sgd, 0)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    net.net_train_steps_u8_host(xh, yh, sgd, 3)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        ms_e2e = max_over_ranks(ms_e2e, dist)
+    prof = net.net_profile_stages(X[0], Y[0], sgd, 0, 5)
+    rows = [{"phase": ph, "stage": n, "ms": t, "flops": (stage_work(n, BATCH) or (None, None))[0],
+             "bytes": (stage_work(n, BATCH) or (None, None))[1]} for ph, n, t in prof]
+    dom = max(rows, key=lambda r: r["ms"])
+    step_s = ms / 1e3 / steps
+    per_layer = lenet_layer_roofline(BATCH, pk, pk["fp32"])
+    net.close()
+    return {"value": world * BATCH * steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+            "dtype": "f32", "plan": "fused LeNet, PN_FP32 (fp32 SIMT kernels, 1e-5 class)",
+            "e2e": {"value": world * BATCH * ring / (ms_e2e / 1e3), "unit": UNIT,
+                    "h2d_bytes_per_step": BATCH * 784 + BATCH * 4, "d2h_bytes_per_step": 4, "steps": ring,
+                    "path": "byte batches, pipelined (net_train_steps_u8_host)"},
+            "roofline": stage_roofline(dom, pk, False),
+            "step_roofline": {"per_layer_us": per_layer * 1e6, "measured_us": step_s * 1e6,
+                              "frac": per_layer / step_s,
+                              "definition": "SURVEY §8(d) per-layer, P = FP32 SGEMM sustained (measured)"},
+            "stages_ms": {f"{r['phase']}:{r['stage']}": round(r["ms"], 5) for r in rows}}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -319,6 +501,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-class sub-record")
+    ap.add_argument("--fp32-steps", type=int, default=300)
     args = ap.parse_args()
     dflt = {"lenet": (20000, 200), "cifar10_quick": (2000, 50), "alexnet_conv": (40, 5),
             "alexnet_grouped": (40, 5)}[args.workload]
@@ -445,50 +629,65 @@ def main():
     e2e = {"value": world * BATCH * e2e_steps / (ms_e2e / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "steps": e2e_steps, "path": e2e_kind}
 
-    # per-stage kernel durations (CUDA events on the launching stream around
-    # back-to-back launches of each stage: net_profile_stages)
+    # inference (forward-only graph, net_infer) over the same resident dataset
+    inf_steps = max(100, args.steps // 4)
+    for _ in range(10):
+        net.net_infer(X[it % NB], Y[it % NB], loss)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for k in range(inf_steps):
+        net.net_infer(X[k % NB], Y[k % NB], loss)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms_inf = e0.elapsed_time(e1)
+    if world > 1:
+        ms_inf = max_over_ranks(ms_inf, dist)
+    inference = {"value": world * BATCH * inf_steps / (ms_inf / 1e3), "unit": UNIT,
+                 "ms_per_step": ms_inf / inf_steps, "steps": inf_steps,
+                 "path": "forward-only graph (net_infer): conv/pool/ip/relu/softmax-loss, no backward or solver"}
+
+    # per-stage kernel durations: each stage captured back to back in a CUDA
+    # graph and replayed between two events on the launching stream
+    # (net_profile_stages) -- device time of a kernel timed alone, so the
+    # BURST peaks apply to it
     prof = net.net_profile_stages(X[0], Y[0], sgd, it, args.profile_steps)
     pk = peaks()
-    tf32_peak = pk["bf16_sus"] * 1.1 / 2.25           # nominal TF32/BF16 ratio x measured sustained bf16
-    fp32_peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+    tf32_peak, tf32_sus = pk["tf32"], pk["tf32_sus"]
+    fp32_peak = pk["fp32"]
     rows = []
     for ph, name, t_ms in prof:
         w = stage_work(name, BATCH) if args.workload == "lenet" else layer_stage_work(layers, name, BATCH)
         rows.append({"phase": ph, "stage": name, "ms": t_ms,
                      "flops": w[0] if w else None, "bytes": w[1] if w else None})
     dom = max(rows, key=lambda r: r["ms"])
-    flops, byts = dom["flops"] or 0, dom["bytes"] or 0
-    is_tc = "[tc]" in dom["stage"]
-    fpeak = tf32_peak if is_tc else fp32_peak
-    t_f = flops / (fpeak * 1e12) if flops else 0.0
-    t_b = byts / (pk["hbm"] * 1e9) if byts else 0.0
-    sec = dom["ms"] / 1e3
-    if t_f >= t_b:
-        roof = {"bound": "tensor" if is_tc else "alu", "achieved": flops / sec / 1e12, "peak": fpeak,
-                "unit": "TFLOP/s"}
-    else:
-        roof = {"bound": "hbm", "achieved": byts / sec / 1e9, "peak": pk["hbm"], "unit": "GB/s"}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["kernel"] = dom["stage"]
-    roof["traffic"] = None
+    roof = stage_roofline(dom, pk, tf32 if args.workload == "lenet" else True)
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
             tr = json.load(f)
         roof["traffic"] = tr.get(args.precision if args.workload == "lenet" else f"{args.workload}_{args.precision}",
                                  {}).get(dom["stage"])
-    roof["peak_source"] = (f"{pk['src']} MEASURED_PEAKS.json: " +
-                           ("TF32 = sustained bf16 x 1.1/2.25" if roof["bound"] == "tensor" else
-                            "HBM copy GB/s" if roof["bound"] == "hbm" else
-                            "148 SM x 128 FP32 lanes x 2 x sm_max_mhz"))
-    # whole-step per-layer roofline: sum of max(flop/peak, bytes/bw)
-    step_roof_s = 0.0
+    step_s = ms / 1e3 / args.steps
+    # whole step vs the roofline: SURVEY §8(d)'s per-layer definition (unfused
+    # compulsory bytes per layer, the contraction peak of the path's
+    # precision, SUSTAINED: the step runs for seconds), and the stricter
+    # fused-stage one (each launched stage's own algorithmic bytes)
+    fused_s = 0.0
     for r in rows:
         if r["flops"] is None:
             continue
-        p = tf32_peak if "[tc]" in r["stage"] else fp32_peak
-        step_roof_s += max((r["flops"] or 0) / (p * 1e12), (r["bytes"] or 0) / (pk["hbm"] * 1e9))
-    step_s = ms / 1e3 / args.steps
+        pp = tf32_sus if ("[tc]" in r["stage"] and tf32) else fp32_peak
+        fused_s += max((r["flops"] or 0) / (pp * 1e12), (r["bytes"] or 0) / (pk["hbm"] * 1e9))
+    step_roofline = {"fused_stage_us": fused_s * 1e6, "measured_us": step_s * 1e6, "frac_fused": fused_s / step_s}
+    if args.workload == "lenet":
+        per_layer = lenet_layer_roofline(BATCH, pk, tf32_sus if tf32 else fp32_peak)
+        step_roofline.update({"per_layer_us": per_layer * 1e6, "frac": per_layer / step_s,
+                              "definition": "SURVEY §8(d): sum over layers of max(FLOP/P, bytes/HBM) + SGD, unfused "
+                                            f"compulsory bytes; P = {'TF32' if tf32 else 'FP32 SGEMM'} sustained "
+                                            f"({tf32_sus if tf32 else fp32_peak:.0f} TF/s, measured), HBM "
+                                            f"{pk['hbm']:.0f} GB/s"})
     line = {
         "metric": WL["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -500,10 +699,10 @@ def main():
                    f"batches ({NB * BATCH * img_floats * 4 / 1e6:.0f} MB) cycled",
                    "final_loss": final_loss},
         "e2e": e2e,
+        "inference": inference,
         "gpu_launches": net.launches_per_step() * args.steps,
         "roofline": roof,
-        "step_roofline": {"per_layer_us": step_roof_s * 1e6, "measured_us": step_s * 1e6,
-                          "frac": step_roof_s / step_s},
+        "step_roofline": step_roofline,
         "stages_ms": {f"{r['phase']}:{r['stage']}": round(r["ms"], 5) for r in rows},
         "clocks": clk,
     }
@@ -513,8 +712,11 @@ def main():
                                            "tflops": round(r["flops"] / (r["ms"] / 1e3) / 1e12, 2),
                                            "frac_tf32_peak": round(r["flops"] / (r["ms"] / 1e3) / 1e12 / tf32_peak, 4)}
                               for r in rows if r["flops"] and "[tc]" in r["stage"]}
+    if args.workload == "lenet" and tf32 and not args.no_fp32:
+        line["fp32"] = fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
+        line["cpu_baseline_threaded"] = cpu_baseline_threaded(args.workload)
     if rank == 0:
         print(json.dumps(line), flush=True)
     net.close()

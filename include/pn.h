@@ -226,6 +226,20 @@ pn_status net_sync_errors(pn_net* net, void* stream);
 pn_status pn_nccl_unique_id(void* out128);
 pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* id128);
 
+/* TEST HOOK: data parallelism without NCCL for n <= 8 nets on ONE device
+ * (NCCL cannot place two ranks on one GPU), to check the exchange semantics
+ * of R13 (sum over ranks, 1/G in the solver) on a single-GPU box.  Create a
+ * group, then give each net its rank (net_dp_init_loopback); drive each net
+ * from its own host thread with the EAGER phases (net_forward, net_backward,
+ * sgd_update: net_train_step returns PN_ERR_STATE).  Each bucket's exchange
+ * synchronises the calling rank's stream, meets the other ranks at a host
+ * barrier, and rank 0 sums the bucket over the ranks' gradient buffers in
+ * rank order on the device.  The group must outlive its nets' exchanges;
+ * pn_loopback_destroy after every net using it is destroyed. */
+pn_status pn_loopback_create(int n, void** group);
+void pn_loopback_destroy(void* group);
+pn_status net_dp_init_loopback(pn_net* net, void* group, int rank);
+
 #ifdef __cplusplus
 }
 #endif

@@ -6,7 +6,7 @@ fallback: without libpn.so every call raises.
 """
 from ._lib import (PN_DATA, PN_DIFF, PN_FP32, PN_HISTORY, PN_LAYERWISE, PN_MASK, PN_TF32, PnError,
                    pn_sgd)
-from .net import Net, make_sgd, spec_text
+from .net import LoopbackGroup, Net, make_sgd, spec_text
 
 __all__ = ["Net", "make_sgd", "spec_text", "pn_sgd", "PnError", "PN_DATA", "PN_DIFF", "PN_MASK",
            "PN_HISTORY", "PN_FP32", "PN_TF32", "PN_LAYERWISE"]

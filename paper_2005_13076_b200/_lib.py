@@ -23,7 +23,7 @@ EXPORTS = ["net_create", "net_destroy", "pn_last_error", "net_blob_count", "net_
            "net_infer", "net_stage_count", "net_stage_name", "net_run_stage", "net_profile_stages",
            "net_launches_per_step", "net_sync_errors", "pn_nccl_unique_id", "net_dp_init",
            "net_set_input_transform", "net_train_step_u8", "net_train_steps_u8_host", "pn_idx_read",
-           "pn_cifar_read"]
+           "pn_cifar_read", "pn_loopback_create", "pn_loopback_destroy", "net_dp_init_loopback"]
 
 
 class PnError(RuntimeError):
@@ -82,6 +82,8 @@ def lib():
             "net_train_steps_u8_host": [_vp, _vp, _vp, _i64, ctypes.POINTER(pn_sgd), _i64, _vp, _vp],
             "pn_idx_read": [_cp, _vp, _i64, ctypes.POINTER(_i), ctypes.POINTER(_i64)],
             "pn_cifar_read": [_cp, _vp, _vp, _i64, ctypes.POINTER(_i64)],
+            "pn_loopback_create": [_i, ctypes.POINTER(_vp)],
+            "net_dp_init_loopback": [_vp, _vp, _i],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -89,6 +91,8 @@ def lib():
             f.restype = _i
         L.net_destroy.argtypes = [_vp]
         L.net_destroy.restype = None
+        L.pn_loopback_destroy.argtypes = [_vp]
+        L.pn_loopback_destroy.restype = None
         L.pn_last_error.argtypes = []
         L.pn_last_error.restype = _cp
         _lib = L

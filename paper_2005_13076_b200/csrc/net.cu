@@ -9,7 +9,9 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
+#include <mutex>
 #include <cstring>
 #include <memory>
 #include <sstream>
@@ -186,6 +188,31 @@ struct GraphExec {
   }
 };
 
+// Test hook: an in-process "communicator" for n nets on ONE
+// device, each driven eagerly from its own host thread.  The exchange stage
+// of rank r synchronises its stream, meets the others at a host barrier, and
+// rank 0 sums the bucket over the ranks' gradient buffers in rank order on
+// the device (the same semantics as the NCCL sum; not capturable in a graph).
+struct pn_loop {
+  int n = 0;
+  std::vector<pn_net*> nets;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  long long gen = 0;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const long long g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct pn_net {
   int device = 0, batch = 0, flags = 0;
   bool tf32 = false, fused = false;
@@ -257,6 +284,9 @@ struct pn_net {
   // data parallel
   int nranks = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  pn_loop* loop = nullptr;          // test-hook exchange (instead of comm)
+  void* nccl_grads = nullptr;       // gradient buffer from ncclMemAlloc (registered with the communicator)
+  void* nccl_reg = nullptr;         // ncclCommRegister handle
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
   // single-GPU step: a side stream for independent backward branches
@@ -977,12 +1007,12 @@ static void build_fused_lenet(pn_net* net) {
     l.set((const void*)lenet_ip2_bwd, dim3(4, i2.splits), dim3(128), 0, p);
     add(bwd, "ip2.bwd+relu1.bwd", l);
   }
-  // single GPU: the ip weight gradients (+ the ip bucket reduction) run on a
-  // side stream, concurrently with ip1's data gradient and the conv
-  // backward (their CTAs co-reside: 97 KB of shared memory each); joined
-  // before the solver.  With data parallelism the chain stays linear (the
-  // bucket allreduce follows the reduction on the main stream).
-  const bool fork = net->tf32 && !net->comm && net->side;
+  // the ip weight gradients (+ the ip bucket reduction) run on a side
+  // stream, concurrently with ip1's data gradient and the conv backward
+  // (their CTAs co-reside: 97 KB of shared memory each); joined before the
+  // solver.  With data parallelism the ip bucket's allreduce is issued from
+  // the same side branch, right after its reduction.
+  const bool fork = net->tf32 && net->side;
   if (net->tf32) {
     ip_segs.push_back(seg(net->part_b1, G + i1.off + i1.wcount, 500, i2.splits, 500));
     if (fork) add_fork(net, bwd, "fork[side]", net->ev_fork);
@@ -1067,24 +1097,53 @@ static void build_update(pn_net* net) {
 }
 
 // data-parallel exchange stages (inserted into the backward list)
+__global__ void loopback_sum(const __grid_constant__ LoopSumP p) {
+  // rank-order sum of one bucket over the ranks' buffers, written back to all
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < p.count; i += stride) {
+    float s = p.buf[0][i];
+    for (int r = 1; r < p.n; ++r) s += p.buf[r][i];
+    for (int r = 0; r < p.n; ++r) p.buf[r][i] = s;
+  }
+}
+
 static void add_dp_stages(pn_net* net) {
-  if (!net->comm) return;  // (a 1-rank communicator still runs the full exchange path)
+  if (!net->comm && !net->loop) return;  // (a 1-rank communicator still runs the full exchange path)
   auto& bwd = net->phase[1];
   // position: after the last stage producing a gradient of the ip bucket
   // (the inner-product layers' parameters, which lead the flat buffer):
   // stages are named "<layer>.<op>"; the fused plan reduces the bucket in
-  // "ip.bucket_reduce"
+  // "ip.bucket_reduce" (on the side branch when the plan forks)
   size_t pos = 0;
-  bool fused_reduce = false;
+  bool fused_reduce = false, on_side = false;
   for (size_t i = 0; i < bwd.size(); ++i)
     if (bwd[i].name == "ip.bucket_reduce") {
       pos = i + 1;
       fused_reduce = true;
+      on_side = bwd[i].side;
     }
   for (size_t i = 0; i < bwd.size() && !fused_reduce; ++i)
     for (const Layer& L : net->layers)
       if (L.type == L_IP && bwd[i].name.compare(0, L.name.size() + 1, L.name + ".") == 0) pos = i + 1;
-  auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) {
+  auto allreduce = [net](int64_t off, int64_t cnt, cudaEvent_t ready) -> std::function<cudaError_t(cudaStream_t)> {
+    if (net->loop)
+      return [net, off, cnt](cudaStream_t st) -> cudaError_t {
+        cudaError_t e = cudaStreamSynchronize(st);  // this rank's bucket is complete
+        if (e != cudaSuccess) return e;
+        net->loop->barrier();
+        if (net->rank == 0 && cnt > 0) {
+          LoopSumP q{};
+          q.n = net->loop->n;
+          q.count = cnt;
+          for (int r = 0; r < q.n; ++r) q.buf[r] = net->loop->nets[r]->grads + off;
+          Launch l;
+          l.set((const void*)loopback_sum, dim3(std::min<long long>(1184, (cnt + 255) / 256)), dim3(256), 0, q);
+          if ((e = l.launch(st)) != cudaSuccess) return e;
+          if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return e;
+        }
+        net->loop->barrier();
+        return cudaSuccess;
+      };
     return [net, off, cnt, ready](cudaStream_t st) -> cudaError_t {
       cudaError_t e = cudaEventRecord(ready, st);
       if (e != cudaSuccess) return e;
@@ -1099,19 +1158,23 @@ static void add_dp_stages(pn_net* net) {
   Stage s1;
   s1.name = "allreduce[ip bucket]";
   s1.custom = allreduce(0, net->bucket_split, net->ev_ip);
+  s1.side = on_side;
+  s1.transparent = on_side;  // (on the side branch it adds nothing to the main stream)
   bwd.insert(bwd.begin() + pos, s1);
   Stage s2;
   s2.name = "allreduce[conv bucket]";
   s2.custom = allreduce(net->bucket_split, net->nparams - net->bucket_split, net->ev_conv);
   bwd.push_back(s2);
-  Stage s3;
-  s3.name = "join[comm]";
-  s3.custom = [net](cudaStream_t st) -> cudaError_t {
-    cudaError_t e = cudaEventRecord(net->ev_done, net->comm_stream);
-    if (e != cudaSuccess) return e;
-    return cudaStreamWaitEvent(st, net->ev_done, 0);
-  };
-  bwd.push_back(s3);
+  if (net->comm) {
+    Stage s3;
+    s3.name = "join[comm]";
+    s3.custom = [net](cudaStream_t st) -> cudaError_t {
+      cudaError_t e = cudaEventRecord(net->ev_done, net->comm_stream);
+      if (e != cudaSuccess) return e;
+      return cudaStreamWaitEvent(st, net->ev_done, 0);
+    };
+    bwd.push_back(s3);
+  }
 }
 
 // Accuracy layers (test-phase side outputs): after the forward
@@ -1257,6 +1320,9 @@ static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, GraphExec&
 
 // launch graph E of phases [0, nph) with arguments a (capture on first use)
 static pn_status replay(pn_net* net, int nph, const StepArgs& a, GraphExec& E, cudaStream_t st) {
+  if (net->loop && nph >= 2)
+    return fail(PN_ERR_STATE, "a loopback data-parallel net runs its phases eagerly (net_forward / net_backward / "
+                              "sgd_update): its exchange synchronises on the host");
   if (!E.ex) TRY(capture(net, nph, a, E));
   else if (!same_args(a, E.a)) TRY(patch_graph(net, nph, a, E));
   CU(cudaGraphLaunch(E.ex, st));
@@ -1354,6 +1420,8 @@ extern "C" void net_destroy(pn_net* net) {
   cudaDeviceSynchronize();
   drop_graphs(net);
   if (net->cap) cudaStreamDestroy(net->cap);
+  if (net->comm && net->nccl_reg) ncclCommDeregister(net->comm, net->nccl_reg);
+  if (net->nccl_grads) ncclMemFree(net->nccl_grads);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
   for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join})
@@ -1954,20 +2022,70 @@ extern "C" pn_status pn_nccl_unique_id(void* out128) {
   return PN_OK;
 }
 
+// point the parameter blobs' diffs at the current gradient buffer
+static void repoint_diffs(pn_net* net) {
+  for (auto& L : net->layers) {
+    if (L.off < 0) continue;
+    int wi = net->blob(L.name + ".w"), bi = net->blob(L.name + ".b");
+    if (wi >= 0) net->blobs[wi].diff = net->grads + L.off;
+    if (bi >= 0) net->blobs[bi].diff = net->grads + L.off + L.wcount;
+  }
+}
+
 extern "C" pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* id128) {
   CHECK_NET(net);
   if (nranks < 1 || rank < 0 || rank >= nranks || !id128) return fail(PN_ERR_INVALID_ARG, "net_dp_init: bad rank");
-  if (net->comm) return fail(PN_ERR_STATE, "data parallelism already initialised");
+  if (net->comm || net->loop) return fail(PN_ERR_STATE, "data parallelism already initialised");
   CU(cudaSetDevice(net->device));
   ncclUniqueId id;
   memcpy(&id, id128, 128);
   NC(ncclCommInitRank(&net->comm, nranks, id, rank));
   net->nranks = nranks;
   net->rank = rank;
+  // the flat gradient buffer (both buckets) from NCCL's allocator and
+  // registered with the communicator, so NCCL can use NVLink SHARP (NVLS,
+  // in-switch reduction) / zero-copy paths for the bucket allreduces
+  const size_t bytes = (size_t)net->nparams * 4;
+  void* buf = nullptr;
+  NC(ncclMemAlloc(&buf, bytes));
+  CU(cudaMemset(buf, 0, bytes));
+  net->nccl_grads = buf;
+  net->grads = (float*)buf;
+  repoint_diffs(net);
+  NC(ncclCommRegister(net->comm, buf, bytes, &net->nccl_reg));
   CU(cudaStreamCreateWithFlags(&net->comm_stream, cudaStreamNonBlocking));
   CU(cudaEventCreateWithFlags(&net->ev_ip, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&net->ev_conv, cudaEventDisableTiming));
   CU(cudaEventCreateWithFlags(&net->ev_done, cudaEventDisableTiming));
+  drop_graphs(net);
+  TRY(build_plan(net));
+  return PN_OK;
+}
+
+extern "C" pn_status pn_loopback_create(int n, void** group) {
+  if (n < 1 || n > 8 || !group) return fail(PN_ERR_INVALID_ARG, "pn_loopback_create: 1 <= n <= 8");
+  pn_loop* g = new pn_loop();
+  g->n = n;
+  g->nets.assign(n, nullptr);
+  *group = g;
+  return PN_OK;
+}
+
+extern "C" void pn_loopback_destroy(void* group) { delete static_cast<pn_loop*>(group); }
+
+extern "C" pn_status net_dp_init_loopback(pn_net* net, void* group, int rank) {
+  CHECK_NET(net);
+  pn_loop* g = static_cast<pn_loop*>(group);
+  if (!g || rank < 0 || rank >= g->n) return fail(PN_ERR_INVALID_ARG, "net_dp_init_loopback: bad group or rank");
+  if (net->comm || net->loop) return fail(PN_ERR_STATE, "data parallelism already initialised");
+  for (pn_net* o : g->nets)
+    if (o && o->device != net->device) return fail(PN_ERR_INVALID_ARG, "loopback ranks must share one device");
+  if (g->nets[rank]) return fail(PN_ERR_INVALID_ARG, "loopback rank already taken");
+  CU(cudaSetDevice(net->device));
+  g->nets[rank] = net;
+  net->loop = g;
+  net->nranks = g->n;
+  net->rank = rank;
   drop_graphs(net);
   TRY(build_plan(net));
   return PN_OK;

@@ -203,6 +203,11 @@ struct Conv1WgradP {  // dp1 + m1 + x -> partial dW1, db1
   float x_scale;
   const float* x_mean;
 };
+struct LoopSumP {  // test-hook exchange: rank-order sum of one bucket over n ranks' buffers (net.cu)
+  float* buf[8];
+  int n;
+  long long count;
+};
 struct IngestP {  // bytes -> fp32 input blob: y = fl(fl(x8 * scale) - mean[i % per])
   const uint8_t* x8;
   float* y;

@@ -241,3 +241,21 @@ class Net:
     def net_dp_init(self, nranks, rank, uid):
         buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
         check(lib().net_dp_init(self._h, nranks, rank, buf))
+
+    def net_dp_init_loopback(self, group, rank):
+        """Test hook (include/pn.h): join a LoopbackGroup as `rank`."""
+        check(lib().net_dp_init_loopback(self._h, group.handle, rank))
+
+
+class LoopbackGroup:
+    """Test hook: an in-process exchange for n nets on one device (pn.h)."""
+
+    def __init__(self, n):
+        h = ctypes.c_void_p()
+        check(lib().pn_loopback_create(n, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            lib().pn_loopback_destroy(self.handle)
+            self.handle = None
