@@ -37,6 +37,9 @@ __global__ void lenet_ip2_loss(const __grid_constant__ Ip2LossP p);
 __global__ void lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p);
 __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p);
 __global__ void lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p);
+__global__ void lenet_conv2_dgrad_simt(const __grid_constant__ ConvBwdDataP p);
+__global__ void lenet_conv2_wgrad_simt(const __grid_constant__ ConvBwdWeightP p);
+constexpr int kConv2DgradSimtSmem = (50 * 20 * 5 * 8 + 2 * 50 * 16 * 8) * 4;
 
 constexpr int kGemmTile = 64;
 #ifndef KWG

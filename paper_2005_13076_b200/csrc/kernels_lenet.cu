@@ -233,6 +233,126 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
   }
 }
 
+// ------------------------------------------- conv2 backward, fp32 (SIMT)
+// The fp32 plan's conv2 data and weight gradients, in
+// fp32 FMA arithmetic (1e-5 class), specialised to LeNet's geometry (20 ->
+// 50 channels, 5x5, 12x12 -> 8x8).  Register-blocked rows so every shared
+// load feeds several FMAs (the generic gather kernels did one load per FMA).
+//
+// Data gradient (gather form of col2im(W^T G)):
+//   dp1[n,c,y,x] = sum_f sum_{i,j} W2[f,c,i,j] G2[n,f,y-i,x-j]
+// thread = (image of the pair, c, output row y): 12 accumulators; per (f, i)
+// the G2 row y-i (8 values; rows outside 0..7 are a zero halo) and the 5
+// taps W2[f,c,i,:] -> 40 FMAs.  Persistent blocks of 480 threads over image
+// pairs; W2 staged once ([f][c][i][8], taps padded), G2 per pair.
+constexpr int C2D_THREADS = 480;
+constexpr int C2D_SMEM = (50 * 20 * 5 * 8 + 2 * 50 * 16 * 8) * 4;
+__global__ void __launch_bounds__(C2D_THREADS, 1) lenet_conv2_dgrad_simt(const __grid_constant__ ConvBwdDataP p) {
+  extern __shared__ __align__(16) float c2d_smem[];
+  float* ws = c2d_smem;                    // [50 f][20 c][5 i][8]
+  float* gs = c2d_smem + 50 * 20 * 5 * 8;  // [2][50 f][16 rows: 4 zero + 8 + 4 zero][8]
+  pdl_enter();
+  for (int u = threadIdx.x; u < 50 * 20 * 5 * 8; u += C2D_THREADS) {
+    const int j = u & 7, fci = u >> 3;
+    ws[u] = j < 5 ? __ldg(p.w + fci * 5 + j) : 0.f;
+  }
+  for (int u = threadIdx.x; u < 2 * 50 * 16 * 8; u += C2D_THREADS) gs[u] = 0.f;
+  const int im = threadIdx.x / 240, t = threadIdx.x % 240, c = t / 12, y = t % 12;
+  for (int n0 = blockIdx.x * 2; n0 < p.N; n0 += gridDim.x * 2) {
+    __syncthreads();
+    for (int u = threadIdx.x; u < 2 * 3200; u += C2D_THREADS) {
+      const int ii = u / 3200, e = u % 3200, f = e >> 6, r = (e >> 3) & 7, x = e & 7;
+      gs[((ii * 50 + f) * 16 + 4 + r) * 8 + x] = (n0 + ii < p.N) ? __ldg(p.dy + (size_t)(n0 + ii) * 3200 + e) : 0.f;
+    }
+    __syncthreads();
+    float acc[12];
+#pragma unroll
+    for (int x = 0; x < 12; ++x) acc[x] = 0.f;
+    const float* gb = gs + (im * 50 * 16 + 4 + y) * 8;  // row y - i of filter f: gb + (f*16 - i)*8
+    const float* wb = ws + c * 40;                         // W2[f][c][i][:] at wb + f*800 + i*8
+#pragma unroll 1
+    for (int f = 0; f < 50; ++f) {
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        const float4 g0 = *reinterpret_cast<const float4*>(gb + (f * 16 - i) * 8);
+        const float4 g1 = *reinterpret_cast<const float4*>(gb + (f * 16 - i) * 8 + 4);
+        const float4 w0 = *reinterpret_cast<const float4*>(wb + f * 800 + i * 8);
+        const float w4 = wb[f * 800 + i * 8 + 4];
+        const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+        const float w[5] = {w0.x, w0.y, w0.z, w0.w, w4};
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+#pragma unroll
+          for (int x0 = 0; x0 < 8; ++x0) acc[x0 + j] = fmaf(w[j], g[x0], acc[x0 + j]);
+      }
+    }
+    const int n = n0 + im;
+    if (n < p.N) {
+      float4* d = reinterpret_cast<float4*>(p.dx + ((size_t)n * 20 + c) * 144 + y * 12);
+      d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+      d[2] = make_float4(acc[8], acc[9], acc[10], acc[11]);
+    }
+  }
+}
+
+// Weight gradient  dW2[f,c,i,j] = sum_n sum_{h,w<8} G2[n,f,h,w] p1[n,c,h+i,w+j],
+// db2[f] = sum G2[n,f]: one block per split (contiguous images), 512
+// threads: thread t < 500 takes filter f = t / 10 and the 10 (c, i) pairs
+// q = t % 10 + 10 k; per image and row h, the G2 row (8 values) is loaded
+// once and each pair's input row p1[c, h+i, 0..11] feeds 40 FMAs into the
+// pair's 5 accumulators.  Split partials, reduced by the conv bucket.
+constexpr int C2W_THREADS = 512;
+__global__ void __launch_bounds__(C2W_THREADS, 1) lenet_conv2_wgrad_simt(const __grid_constant__ ConvBwdWeightP p) {
+  __shared__ __align__(16) float gsm[3200];  // G2[n]: [50 f][8][8]
+  __shared__ __align__(16) float psm[2880];  // p1[n]: [20 c][12][12]
+  pdl_enter();
+  const int s = blockIdx.x;
+  const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
+  const int t = threadIdx.x, f = t / 10, q0 = t % 10;
+  const bool active = t < 500;
+  float acc[10][5], bacc = 0.f;
+#pragma unroll
+  for (int k = 0; k < 10; ++k)
+#pragma unroll
+    for (int j = 0; j < 5; ++j) acc[k][j] = 0.f;
+  for (int n = n0; n < n1; ++n) {
+    __syncthreads();
+    for (int u = t; u < 3200 / 4; u += C2W_THREADS)
+      reinterpret_cast<float4*>(gsm)[u] = __ldg(reinterpret_cast<const float4*>(p.dy + (size_t)n * 3200) + u);
+    for (int u = t; u < 2880 / 4; u += C2W_THREADS)
+      reinterpret_cast<float4*>(psm)[u] = __ldg(reinterpret_cast<const float4*>(p.x + (size_t)n * 2880) + u);
+    __syncthreads();
+    if (!active) continue;
+#pragma unroll 1
+    for (int h = 0; h < 8; ++h) {
+      const float4 g0 = *reinterpret_cast<const float4*>(gsm + f * 64 + h * 8);
+      const float4 g1 = *reinterpret_cast<const float4*>(gsm + f * 64 + h * 8 + 4);
+      const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      if (q0 == 0) bacc += ((g[0] + g[1]) + (g[2] + g[3])) + ((g[4] + g[5]) + (g[6] + g[7]));
+#pragma unroll
+      for (int k = 0; k < 10; ++k) {
+        const int q = q0 + 10 * k, c = q / 5, i = q % 5;
+        const float4* pr = reinterpret_cast<const float4*>(psm + c * 144 + (h + i) * 12);
+        const float4 a0 = pr[0], a1 = pr[1], a2 = pr[2];
+        const float a[12] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w, a2.x, a2.y, a2.z, a2.w};
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+#pragma unroll
+          for (int w = 0; w < 8; ++w) acc[k][j] = fmaf(g[w], a[w + j], acc[k][j]);
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    const int q = q0 + 10 * k, c = q / 5, i = q % 5;
+#pragma unroll
+    for (int j = 0; j < 5; ++j) p.part_w[(size_t)s * p.pstride + ((f * 20 + c) * 5 + i) * 5 + j] = acc[k][j];
+  }
+  if (q0 == 0) p.part_b[(size_t)s * p.pstride + f] = bacc;
+}
+
 // ------------------------------------------------- ip2 + softmax-with-loss
 // Warp per sample (4 per block): logits = a1 . W2^T + b2 (W2 staged in smem
 // before the PDL wait: it was written by the previous step's SGD), then the

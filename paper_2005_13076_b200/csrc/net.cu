@@ -539,6 +539,8 @@ static pn_status allocate(pn_net* net) {
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2])  // conv2 weight gradient: one CTA per SM (4 row tiles)
       L.splits = std::max(1, std::min(net->batch, WG2_SPLITS > 0 ? WG2_SPLITS : net->tc_sms / 4));
+    if (net->fused && !net->tf32 && &L == &net->layers[2])  // fp32 SIMT conv2 weight gradient: one block per SM
+      L.splits = std::max(1, std::min(net->batch, net->tc_sms));
     if (L.tc_conv) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
                                 net->tc_sms, L.G);
@@ -1053,12 +1055,13 @@ static void build_fused_lenet(pn_net* net) {
   } else {
     ConvBwdDataP q{cv2.diff, P + c2.off, p1.diff, N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8};
     Launch l;
-    l.set((const void*)conv_bwd_data_generic, dim3(cdiv((long long)N * 2880, 256)), dim3(256), 0, q);
+    l.set((const void*)lenet_conv2_dgrad_simt, dim3(std::min(net->tc_sms, (int)cdiv(N, 2))), dim3(480),
+          kConv2DgradSimtSmem, q);
     add(bwd, "conv2.dgrad", l);
     ConvBwdWeightP w{cv2.diff, p1.data, net->partials + c2.part_off, net->partials + c2.part_off + 25000,
                      N, 20, 12, 12, 50, 5, 5, 1, 1, 0, 0, 8, 8, c2.splits, 25050};
     Launch l2;
-    l2.set((const void*)conv_bwd_weight_generic, dim3(1000, c2.splits), dim3(256), 0, w);
+    l2.set((const void*)lenet_conv2_wgrad_simt, dim3(c2.splits), dim3(512), 0, w);
     add(bwd, "conv2.wgrad", l2);
     conv_segs.push_back(seg(net->partials + c2.part_off, G + c2.off, 25050, c2.splits, 25050));
   }
@@ -1398,6 +1401,8 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
   TRY(allocate(net.get()));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (50 * 20 * 28 + 2 * 2880) * 4));
+  CU(cudaFuncSetAttribute((const void*)lenet_conv2_dgrad_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          kConv2DgradSimtSmem));
   if (net->tf32) {
     cudaError_t e = net->fused ? tc::setup() : tcc::setup(max_nk);
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
