@@ -221,7 +221,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
     const int rr = u % ROWS, half = u / ROWS, r = ROWS * (int)rank + rr;
     float v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = ldsf(sbase + 4 * (r * CPB + 16 * half + j));
+    for (int j = 0; j < 16; ++j) v[j] = ldsf_nc(sbase + 4 * (r * CPB + 16 * half + j));
     op.store(r, rr, half, v, red, epi_s);
   }
   __syncthreads();
@@ -596,9 +596,13 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
 //   warp 0      producer: W2d (bulk copies, once)
 //   warp 1      MMA issuer, 2 TMEM accumulators (192 columns each)
 //   warps 2-5   B builders: G2[n,f,h,w] (global/L2, coalesced along (h,w))
-//               -> Gs, 2 buffers
-//   warps 6-9   epilogue: per image row h, TMEM -> smem scratch -> the
-//               j-sum -> dp1 (NCHW)
+//               -> Gs (one buffer)
+//   warps 6-13  epilogue, one group of 4 per image of the pair: per chunk
+//               of 4 image rows, TMEM -> smem scratch -> the j-sum -> dp1
+//               (NCHW)
+// (one G buffer: the builders hold the next pair in registers and store it
+// as soon as the MMAs have read the previous one; the freed shared memory
+// holds the second epilogue group's scratch)
 #ifndef DG_RESTRICT
 #define DG_RESTRICT 1
 #endif
@@ -610,10 +614,11 @@ constexpr int A_TAP = PLANES * A_PLANE;             // 23296 B
 constexpr int A_BYTES = 5 * A_TAP + 384;            // + the rows 104..127 the M=128 MMA over-reads
 constexpr int G_PLANE = 28 * 128;                   // 28 slots x 8 w x 16 B
 constexpr int G_BYTES = PLANES * G_PLANE;           // 50176 B per buffer
-constexpr int SP = 12;                              // scratch pitch (floats): conflict-free 16-B stores
-constexpr int S_BYTES = 128 * SP * 4;               // per scratch buffer
-constexpr int WARPS = 10, THREADS_D = WARPS * 32;
-constexpr int SMEM = A_BYTES + 2 * G_BYTES + 2 * S_BYTES + 1024;
+constexpr int RCH = 4;                              // epilogue: output rows per staged chunk
+constexpr int SP = RCH * 8 + 4;                     // scratch pitch (floats): conflict-free 16-B stores
+constexpr int S_BYTES = 128 * SP * 4;               // per epilogue group
+constexpr int WARPS = 14, THREADS_D = WARPS * 32;   // producer, MMA, 4 builders, 2 x 4 epilogue
+constexpr int SMEM = A_BYTES + G_BYTES + 2 * S_BYTES + 1024;
 constexpr int W2D_FLOATS = A_BYTES / 4;
 struct Params {
   const float* w2d;  // packed A (W2D_FLOATS)
@@ -627,26 +632,26 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
   using namespace dg;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t A_s = smem_u32(smem), G_s = A_s + A_BYTES, S_s = G_s + 2 * G_BYTES;
-  __shared__ __align__(8) uint64_t afull, gfull[2], gfree[2], accfull[2], accfree[2];
+  const uint32_t A_s = smem_u32(smem), G_s = A_s + A_BYTES, S_s = G_s + G_BYTES;
+  __shared__ __align__(8) uint64_t afull, gfull, gfree, accfull[2], accfree[2];
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int npairs = (p.N + 1) / 2, pair0 = blockIdx.x * p.per_cta;
   const int mine = max(0, min(p.per_cta, npairs - pair0));
   if (tid == 0) {
     mbar_init(smem_u32(&afull), 1);
+    mbar_init(smem_u32(&gfull), 128);
+    mbar_init(smem_u32(&gfree), 1);
     for (int b = 0; b < 2; ++b) {
-      mbar_init(smem_u32(&gfull[b]), 128);
-      mbar_init(smem_u32(&gfree[b]), 1);
       mbar_init(smem_u32(&accfull[b]), 1);
-      mbar_init(smem_u32(&accfree[b]), 128);
+      mbar_init(smem_u32(&accfree[b]), 256);
     }
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc(&tmem_base, 512);
-  // zero both G buffers once: the builders only ever write the in-image slots
+  // zero the G buffer once: the builders only ever write the in-image slots
   // of planes 0..12, so the halo slots and plane 13 stay zero
-  for (int i = tid; i < 2 * G_BYTES / 16; i += THREADS_D) sts128(G_s + 16 * i, zero4());
+  for (int i = tid; i < G_BYTES / 16; i += THREADS_D) sts128(G_s + 16 * i, zero4());
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -673,11 +678,11 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
       const int b = it & 1;
-      mbar_wait(smem_u32(&gfull[b]), (it >> 1) & 1);
+      mbar_wait(smem_u32(&gfull), it & 1);
       if (it < 2) stamp(2 + 2 * it);  // pair built
       if (it >= 2) mbar_wait(smem_u32(&accfree[b]), ((it >> 1) - 1) & 1);
       tc_fence_after();
-      const uint64_t bd0 = make_desc_ns(G_s + b * G_BYTES, G_PLANE, 128);
+      const uint64_t bd0 = make_desc_ns(G_s, G_PLANE, 128);
 #if DG_RESTRICT
       // kernel row 2 over all 12 output rows of both images (N = 192; its
       // zero halo rows make it exact everywhere, and it initialises the
@@ -707,7 +712,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
           mma_tf32(tbase + b * 256, ad0 + (uint64_t)((i * A_TAP + ks * 2 * A_PLANE) >> 4),
                    bd0 + (uint64_t)(((4 - i) * 128 + ks * 2 * G_PLANE) >> 4), idesc, (i | ks) != 0);
 #endif
-      mma_commit(smem_u32(&gfree[b]));
+      mma_commit(smem_u32(&gfree));
       mma_commit(smem_u32(&accfull[b]));
       if (it < 2) stamp(3 + 2 * it);  // MMAs issued
     }
@@ -719,7 +724,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
     const uint32_t dst0 = (uint32_t)((4 + 12 * n + h) * 128 + w * 16);
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
-      const int b = it & 1, img = 2 * (pair0 + it) + n;
+      const int img = 2 * (pair0 + it) + n;
       float v[52];
       if (img < p.N) {
         const float* g = p.g2 + (size_t)img * 3200 + pos;
@@ -730,59 +735,76 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
         for (int f = 0; f < 50; ++f) v[f] = 0.f;
       }
       v[50] = v[51] = 0.f;
-      if (it >= 2) mbar_wait(smem_u32(&gfree[b]), ((it >> 1) - 1) & 1);
-      const uint32_t dst = G_s + b * G_BYTES + dst0;
+      // one G buffer: its next pair is stored (from registers, loaded above)
+      // as soon as the previous pair's MMAs have read it
+      if (it >= 1) mbar_wait(smem_u32(&gfree), (it - 1) & 1);
+      const uint32_t dst = G_s + dst0;
 #pragma unroll
       for (int q = 0; q < 13; ++q) sts128(dst + q * G_PLANE, f4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
       fence_proxy_async();
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gfull[b])) : "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&gfull)) : "memory");
     }
   } else if (warp >= 6) {
-    // ---- epilogue: TMEM lane quadrant q = warp % 4 holds rows (c,j) 32q..;
-    // per image row h the 8 columns w of every row go through a scratch tile
-    // (double-buffered: one barrier per row), then thread -> outputs (c, w)
-    const int quad = warp & 3, row = quad * 32 + lane, et = tid - 192;
-    int step = 0;
+    // ---- epilogue: two groups of 4 warps, group g = image n of the pair
+    // (its 96 accumulator columns); TMEM lane quadrant q = warp % 4 holds
+    // rows (c,j) 32q..  Per chunk of RCH output rows: the 8 columns w of
+    // every row and chunk row go through the group's scratch tile (one
+    // barrier to publish, one before it is rewritten), then thread ->
+    // outputs (c, h, w): the 5-term column sum in fixed j order.
+    const int quad = warp & 3, row = quad * 32 + lane, g = (warp - 6) >> 2, et = (tid - 192) & 127;
+    const uint32_t S = S_s + g * S_BYTES;
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
-      const int b = it & 1;
+      const int b = it & 1, img = 2 * (pair0 + it) + g;
       mbar_wait(smem_u32(&accfull[b]), (it >> 1) & 1);
-      if (et == 0 && it < 2) stamp(6 + 2 * it);  // accumulator ready
+      if (et == 0 && g == 0 && it < 2) stamp(6 + 2 * it);  // accumulator ready
       __syncwarp();
       tc_fence_after();
 #pragma unroll 1
-      for (int n = 0; n < 2; ++n) {
-        const int img = 2 * (pair0 + it) + n;
-#pragma unroll 1
-        for (int hp = 0; hp < 6; ++hp) {
-          float v[16];
-          tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 256 + (n * 12 + 2 * hp) * 8, v);
-          if (n == 1 && hp == 5) {  // every column of this accumulator is in registers
-            tc_fence_before();
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[b])) : "memory");
+      for (int h0 = 0; h0 < 12; h0 += RCH) {
+        float v[RCH * 8];
+#pragma unroll
+        for (int u = 0; u < RCH / 2; ++u)
+          tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + b * 256 + (g * 12 + h0 + 2 * u) * 8,
+                           *reinterpret_cast<float(*)[16]>(v + 16 * u));
+        tmem_ld_wait();
+        if (h0 + RCH == 12) {  // every column of this image is in registers
+          tc_fence_before();
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&accfree[b])) : "memory");
+        }
+#pragma unroll
+        for (int u = 0; u < RCH * 2; ++u) sts128(S + 4 * (row * SP + 4 * u), f4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]));
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");
+        if (img < p.N) {
+          // all shared loads of the thread's outputs first (no memory clobber:
+          // the compiler may hoist them above the previous outputs' global
+          // stores), then the fixed-order sums
+          constexpr int NO = (RCH * 240 + 127) / 128;
+          float t[NO][5];
+#pragma unroll
+          for (int k = 0; k < NO; ++k) {
+            const int o = et + 128 * k;
+            const int hh = o / 240, r2 = o - 240 * hh, c = r2 / 12, w = r2 - 12 * c;
+#pragma unroll
+            for (int jj = 0; jj < 5; ++jj)
+              t[k][jj] = (o < RCH * 240 && (unsigned)(w - jj) < 8u)
+                             ? ldsf_nc(S + 4 * ((c * 5 + jj) * SP + hh * 8 + w - jj)) : 0.f;
           }
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh, ++step) {
-            const uint32_t S = S_s + (step & 1) * S_BYTES;
-            sts128(S + 4 * (row * SP), f4(v[8 * hh], v[8 * hh + 1], v[8 * hh + 2], v[8 * hh + 3]));
-            sts128(S + 4 * (row * SP + 4), f4(v[8 * hh + 4], v[8 * hh + 5], v[8 * hh + 6], v[8 * hh + 7]));
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (img < p.N) {
-              const int h = 2 * hp + hh;
+          for (int k = 0; k < NO; ++k) {
+            const int o = et + 128 * k;
+            if (o >= RCH * 240) break;
+            const int hh = o / 240, r2 = o - 240 * hh, c = r2 / 12, w = r2 - 12 * c;
+            float acc = 0.f;  // j ascending over the valid taps (the first valid term initialises it)
 #pragma unroll
-              for (int o = et; o < 240; o += 128) {
-                const int c = o / 12, w = o - 12 * c;
-                float acc = 0.f;
-#pragma unroll
-                for (int j = 0; j < 5; ++j)
-                  if ((unsigned)(w - j) < 8u) acc += ldsf(S + 4 * ((c * 5 + j) * SP + w - j));
-                p.dp1[(size_t)img * 2880 + c * 144 + h * 12 + w] = acc;
-              }
-            }
+            for (int jj = 0; jj < 5; ++jj)
+              if ((unsigned)(w - jj) < 8u) acc += t[k][jj];
+            p.dp1[(size_t)img * 2880 + c * 144 + (h0 + hh) * 12 + w] = acc;
           }
         }
+        asm volatile("bar.sync %0, 128;" ::"r"(1 + g) : "memory");  // the scratch is read before it is rewritten
       }
-      if (et == 0 && it < 2) stamp(7 + 2 * it);  // pair stored
+      if (et == 0 && g == 0 && it < 2) stamp(7 + 2 * it);  // pair stored
     }
   }
   tc_fence_before();

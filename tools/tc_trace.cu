@@ -98,6 +98,18 @@ static int dgrad_main(int N) {
          cudaGetErrorString(cudaGetLastError()));
   const int ks[] = {0, 11, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10};
   dump("cta  start pdl  A  built0 mma0 built1 mma1 acc0 st0 acc1 st1 end", ks, 12, l.grid.x);
+  {
+    std::vector<unsigned long long> t(4096), tr(148 * 16);
+    cudaMemcpyFromSymbol(t.data(), g_trace0, t.size() * 8);
+    cudaMemcpyFromSymbol(tr.data(), g_trace, tr.size() * 8);
+    printf("CTA 0 epilogue group 0, per (pair, chunk): ld_done staged computed reread_ok (ns from CTA start)\n");
+    for (int it = 0; it < 2; ++it)
+      for (int ch = 0; ch < 3; ++ch) {
+        printf("%d %d", it, ch);
+        for (int k = 0; k < 4; ++k) printf(" %6lld", t[1000 + it * 16 + ch * 4 + k] ? (long long)(t[1000 + it * 16 + ch * 4 + k] - tr[0]) : -1ll);
+        printf("\n");
+      }
+  }
   return 0;
 }
 
