@@ -126,6 +126,10 @@ def stage_work(name, N):
         "conv2.wgrad": (2 * 64 * 500 * 50 * N, N * (3200 * 4 + 2880 * 4) + 32 * W2),
         "conv1.wgrad": (2 * 144 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1),
         "sgd": (0, 431080 * 4 * 5),
+        # the fused solver: SGD's 20 B/param (its TF32 weight copies and the
+        # conv partials it sums are this implementation's, not the method's)
+        "solver": (0, 431080 * 4 * 5),
+        "reduce+solver": (0, 431080 * 4 * 5),
     }
     base = name.split("[")[0]
     if base.endswith(".wgrad_reduce"):
@@ -653,6 +657,9 @@ def main():
     # (net_profile_stages) -- device time of a kernel timed alone, so the
     # BURST peaks apply to it
     prof = net.net_profile_stages(X[0], Y[0], sgd, it, args.profile_steps)
+    # the stages of a whole step (net_stage_mode != 1: not the phase-alone variants)
+    in_step = {(ph, s) for ph in range(3) for s, m in zip(net.stages(ph), net.stage_modes(ph)) if m != 1}
+    prof = [r for r in prof if (r[0], r[1]) in in_step]
     pk = peaks()
     tf32_peak, tf32_sus = pk["tf32"], pk["tf32_sus"]
     fp32_peak = pk["fp32"]

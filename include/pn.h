@@ -198,6 +198,12 @@ pn_status pn_cifar_read(const char* path, uint8_t* pixels, int32_t* labels,
 pn_status net_stage_count(const pn_net* net, int phase, int* count);
 pn_status net_stage_name(const pn_net* net, int phase, int i,
                          const char** name);
+/* Whether stage i runs in a whole captured step: 0 always, 1 only when the
+ * phases run on their own (net_forward / net_backward / sgd_update /
+ * net_infer), 2 only inside a whole step (net_train_step*: e.g. the loss sum
+ * moved to the backward's side branch, the conv bucket reduced inside the
+ * solver). */
+pn_status net_stage_mode(const pn_net* net, int phase, int i, int* mode);
 pn_status net_run_stage(pn_net* net, int phase, int i, const float* x,
                         const int32_t* labels, void* stream);
 /* Per-stage kernel durations on `stream`: one pass through the plan in order
@@ -215,6 +221,14 @@ pn_status net_profile_stages(pn_net* net, const float* x,
                              int* n_out, void* stream);
 /* Number of kernels one net_train_step launches on the device. */
 pn_status net_launches_per_step(const pn_net* net, int* n);
+
+/* Dev-only: in-graph step timeline.  Only in a library built with
+ * -DPN_STEPTRACE (else PN_ERR_STATE).  Synchronises the device; when
+ * host_out is non-NULL copies the per-kernel record gathered since the last
+ * call into it (16 x 3 uint64 %globaltimer ns: first CTA entry, first return
+ * from the PDL wait, last CTA exit; kernel order as enum StKernel in
+ * csrc/pdl.cuh), then re-arms the record. */
+pn_status net_steptrace(pn_net* net, unsigned long long* host_out);
 
 /* Synchronise `stream` and surface device-side errors (label range). */
 pn_status net_sync_errors(pn_net* net, void* stream);

@@ -20,8 +20,8 @@ PN_DATA, PN_DIFF, PN_MASK, PN_HISTORY = 0, 1, 2, 3
 EXPORTS = ["net_create", "net_destroy", "pn_last_error", "net_blob_count", "net_blob_info",
            "net_param_count", "net_blob_ptr", "net_set_param", "net_get_blob", "net_put_blob",
            "net_forward", "net_backward", "sgd_update", "net_train_step", "net_train_step_host",
-           "net_infer", "net_stage_count", "net_stage_name", "net_run_stage", "net_profile_stages",
-           "net_launches_per_step", "net_sync_errors", "pn_nccl_unique_id", "net_dp_init",
+           "net_infer", "net_stage_count", "net_stage_name", "net_stage_mode", "net_run_stage", "net_profile_stages",
+           "net_launches_per_step", "net_steptrace", "net_sync_errors", "pn_nccl_unique_id", "net_dp_init",
            "net_set_input_transform", "net_train_step_u8", "net_train_steps_u8_host", "pn_idx_read",
            "pn_cifar_read", "pn_loopback_create", "pn_loopback_destroy", "net_dp_init_loopback"]
 
@@ -70,10 +70,12 @@ def lib():
             "net_infer": [_vp, _vp, _vp, _vp, _vp],
             "net_stage_count": [_vp, _i, ctypes.POINTER(_i)],
             "net_stage_name": [_vp, _i, _i, ctypes.POINTER(_cp)],
+            "net_stage_mode": [_vp, _i, _i, ctypes.POINTER(_i)],
             "net_run_stage": [_vp, _i, _i, _vp, _vp, _vp],
             "net_profile_stages": [_vp, _vp, _vp, ctypes.POINTER(pn_sgd), _i64, _i,
                                    ctypes.POINTER(ctypes.c_float), _i, ctypes.POINTER(_i), _vp],
             "net_launches_per_step": [_vp, ctypes.POINTER(_i)],
+            "net_steptrace": [_vp, _vp],
             "net_sync_errors": [_vp, _vp],
             "pn_nccl_unique_id": [_vp],
             "net_dp_init": [_vp, _i, _i, _vp],

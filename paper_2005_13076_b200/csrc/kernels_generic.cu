@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "sgd.cuh"
 
 namespace pn {
 
@@ -161,7 +162,9 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p) {
 // sums in order -- a fixed order, so reruns are bitwise identical.
 // p.total = number of 32-output blocks over all segments.
 __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_constant__ ReduceMultiP p) {
-  if (!p.late) pdl_enter();
+  const int stk = p.late ? ST_RED_IP : ST_RED_CONV;
+  ST_BEGIN(stk);
+  if (!p.late) pdl_enter_k(stk);
   __shared__ float sm[8][33];
   int b = blockIdx.x, k = 0;
   while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
@@ -188,7 +191,8 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
     for (int q = 0; q < 8; ++q) r += sm[q][lane];
     s.out[i] = r;
   }
-  if (p.late) pdl_enter();
+  if (p.late) pdl_enter_k(stk);
+  ST_END(stk);
 }
 
 // ------------------------------------------------------------------ pooling
@@ -648,7 +652,8 @@ __global__ void softmax_loss_generic(const __grid_constant__ SoftmaxLossP p) {
 
 // loss = (1/M) sum_i row_loss[i], fixed-order block reduction (one block)
 __global__ void __launch_bounds__(256) loss_reduce(const __grid_constant__ LossReduceP p) {
-  pdl_enter();
+  ST_BEGIN(ST_LOSSRED);
+  pdl_enter_k(ST_LOSSRED);
   __shared__ float sm[32];
   float acc = 0.f;
   for (int i = threadIdx.x; i < p.M; i += blockDim.x) acc += p.row_loss[i];
@@ -658,6 +663,7 @@ __global__ void __launch_bounds__(256) loss_reduce(const __grid_constant__ LossR
     p.loss_blob[0] = r;
     if (p.loss_out) p.loss_out[0] = r;
   }
+  ST_END(ST_LOSSRED);
 }
 
 // ------------------------------------------------------------ byte ingest
@@ -676,17 +682,11 @@ __global__ void ingest_u8(const __grid_constant__ IngestP p) {
 }
 
 // ---------------------------------------------------------------------- SGD
-// S:536-544 / DESIGN.md R11: one IEEE fp32 rounding per op, no contraction.
-__device__ __forceinline__ void sgd_one(float& w, float d, float& v, float lr, float mom,
-                                        float decay, float gs) {
-  float g = __fmul_rn(d, gs);
-  g = __fadd_rn(g, __fmul_rn(decay, w));
-  v = __fadd_rn(__fmul_rn(mom, v), __fmul_rn(lr, g));
-  w = __fsub_rn(w, v);
-}
+// S:536-544 / DESIGN.md R11 (sgd.cuh)
 
 __global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
-  pdl_enter();
+  ST_BEGIN(ST_SGD);
+  pdl_enter_k(ST_SGD);
   const float lr = p.lr_dev ? __ldg(p.lr_dev) : p.lr;
   long long i4 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long n4 = p.n / 4;
@@ -708,6 +708,7 @@ __global__ void sgd_update_kernel(const __grid_constant__ SgdP p) {
     p.w[i] = w;
     p.v[i] = v;
   }
+  ST_END(ST_SGD);
 }
 
 // ----------------------------------------------------- mask representation
@@ -745,4 +746,6 @@ __global__ void tf32_copy(const __grid_constant__ Tf32CopyP p) {
   if (p.dst) p.dst[idx] = v;
   if (p.dstT) p.dstT[(long long)c * p.ldt + r] = v;
 }
+PN_STEPTRACE_TU(st_set_generic)
+
 }  // namespace pn

@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(IP2_SPB * 32) lenet_ip2_loss(const __grid_cons
   constexpr int NT = IP2_SPB * 32, PER = (1250 + NT - 1) / NT;
   __shared__ __align__(16) float ws[10 * 500];
   __shared__ float bs[10];
+  ST_BEGIN(ST_IP2);
   {  // W2 as 1250 float4, all loads of a thread in flight together
     float4 v[PER];
 #pragma unroll
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(IP2_SPB * 32) lenet_ip2_loss(const __grid_cons
     }
   }
   if (threadIdx.x < 10) bs[threadIdx.x] = __ldg(p.b + threadIdx.x);
-  pdl_enter();
+  pdl_enter_k(ST_IP2);
   const int lane = threadIdx.x & 31;
   const int row = blockIdx.x * IP2_SPB + (threadIdx.x >> 5);
   float4 av[4];
@@ -437,6 +438,7 @@ __global__ void __launch_bounds__(IP2_SPB * 32) lenet_ip2_loss(const __grid_cons
     p.row_loss[row] = -logf(fmaxf(__fdiv_rn(ey, s), FLT_MIN));
     p.pred[row] = arg;
   }
+  ST_END(ST_IP2);
 }
 
 // ------------------------------------------------ ip2 backward + relu1 bwd
@@ -450,6 +452,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
   const int s = blockIdx.y;
   const int m0 = (int)((long long)p.N * s / p.splits), m1 = (int)((long long)p.N * (s + 1) / p.splits);
   __shared__ float dzs[16][10];
+  ST_BEGIN(ST_IP2B);
   float w2[10], acc[10];
   const bool valid = k < 500;
 #pragma unroll
@@ -457,8 +460,11 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     w2[o] = valid ? __ldg(p.w + o * 500 + k) : 0.f;
     acc[o] = 0.f;
   }
-  // dz comes from ip2+loss two launches back, a1 from further back: nothing
-  // is read from the predecessor (the loss reduction), so wait only at the end
+  // dz comes from ip2+loss: the immediate predecessor in a whole TF32 step
+  // (its loss sum runs on the side branch), two launches back otherwise --
+  // wait for it after the weight loads; let the successor launch at the end
+  pdl_wait();
+  if (threadIdx.x == 0) st_mark(ST_IP2B, 1);
   float bacc = 0.f, b1acc = 0.f;
   for (int mb = m0; mb < m1; mb += 16) {
     const int cnt = min(16, m1 - mb);
@@ -510,7 +516,8 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
     if (p.part_b1) p.part_b1[(long long)s * 500 + k] = b1acc;  // db1 = sum_m da1[m,k]
   }
   if (blockIdx.x == 0 && threadIdx.x < 10) p.part_b[(long long)s * p.pstride + threadIdx.x] = bacc;
-  pdl_enter();
+  pdl_trigger();
+  ST_END(ST_IP2B);
 }
 
 // dp2 [N, 50*16] + mask -> dense conv2 output gradient G2 [N,50,8,8]
@@ -540,6 +547,7 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // alongside it and waits only at the end (pdl.cuh).
 __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
   __shared__ float xs[CW_IMGS][784];
+  ST_BEGIN(ST_CONV1W);
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
   const int cnt = min(CW_IMGS, n1 - n0);
@@ -602,7 +610,10 @@ __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__
     for (int t = 0; t < 25; ++t) p.part_w[(long long)s * p.pstride + f * 25 + t] = acc[t];
     p.part_b[(long long)s * p.pstride + f] = bacc;
   }
-  pdl_enter();
+  pdl_enter_k(ST_CONV1W);
+  ST_END(ST_CONV1W);
 }
+
+PN_STEPTRACE_TU(st_set_lenet)
 
 }  // namespace pn

@@ -280,6 +280,10 @@ struct pn_net {
   cudaStream_t aux = nullptr;  // capture-side branch of the loss read-backs
   cudaEvent_t ev_loss[kSlots] = {}, ev_aux = nullptr;
   int launches_per_step = 0;
+  // TF32 fused plan: the packed weight copies (pack.w1f ...) no longer match
+  // the parameters (set through the ABI): packed before the next run
+  bool pack_dirty = true;
+  std::vector<ReduceP> conv_segs;  // the conv bucket's partial sums (the step's solver reduces them)
 
   // data parallel
   int nranks = 1, rank = 0;
@@ -291,7 +295,7 @@ struct pn_net {
   cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
   // single-GPU step: a side stream for independent backward branches
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_ipd = nullptr;
   int64_t bucket_split = 0;  // params [0, split) = ip bucket, [split, n) = conv bucket
   int tc_sms = 148;
   bool tmap_failed = false;
@@ -627,6 +631,9 @@ static const float* in_data(pn_net* net, const Layer& L, bool* is_x) {
   return *is_x ? nullptr : net->blobs[net->blob(L.bottom)].data;
 }
 
+// whether stage s runs in a captured whole step (full) or a phase run on its own
+static bool in_run(const Stage& s, bool full) { return s.mode == 0 || (s.mode == 2) == full; }
+
 static void add(std::vector<Stage>& v, const std::string& name, const Launch& L,
                 std::function<void(Launch&, const StepArgs&)> patch = nullptr) {
   Stage s;
@@ -930,6 +937,8 @@ static void add_fork(pn_net* net, std::vector<Stage>& v, const char* name, cudaE
   v.push_back(f);
 }
 
+static Stage solver_stage(pn_net* net, const std::string& name, bool ip, bool conv, const std::vector<ReduceP>* segs);
+
 static void build_fused_lenet(pn_net* net) {
   auto& fwd = net->phase[0];
   auto& bwd = net->phase[1];
@@ -943,10 +952,13 @@ static void build_fused_lenet(pn_net* net) {
   float* P = net->params;
   float* G = net->grads;
   // ---- forward
-  if (net->tf32) {  // TF32 weight copies for this step's contractions
+  // TF32 weight copies for the contractions: written by the solver of the
+  // previous step (lenet_solver), or packed once after the parameters were
+  // set through the ABI (ensure_packed)
+  const bool dp = net->comm || net->loop;
+  if (net->tf32) {
     net->pack.w1 = P + i1.off;
     net->pack.w2 = P + c2.off;
-    add(fwd, "wpack[tc]", tc::pack_weights_launch(net->pack));  // overlaps conv1+pool1 (late wait)
   }
   {
     // TF32 plan: pool1 is consumed only by conv2's contractions, so it is
@@ -992,6 +1004,9 @@ static void build_fused_lenet(pn_net* net) {
     l.set((const void*)lenet_ip2_loss, dim3(cdiv(N, IP2_SPB)), dim3(IP2_SPB * 32), 0, p);
     add(fwd, "ip2+softmax_loss", l, [](Launch& l, const StepArgs& a) { l.params<Ip2LossP>().labels = a.labels; });
     add_loss(net, fwd);
+    // in a whole TF32 step the loss sum runs on the backward's side branch
+    // (below), off the critical path: ip2's backward follows ip2+loss directly
+    if (net->tf32 && net->side) fwd.back().mode = 1;
   }
   // ---- backward (reverse order).  Split-partial reductions are merged per
   // gradient bucket: one launch for the ip bucket (ready before the NCCL ip
@@ -1022,9 +1037,24 @@ static void build_fused_lenet(pn_net* net) {
     if (fork) bwd.back().side = true;
     // the ip partials come from ip2's backward, two launches back (pdl.cuh)
     add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
-    if (fork) bwd.back().side = true;
+    if (fork) {
+      bwd.back().side = true;
+      add_loss(net, bwd);
+      bwd.back().name = "loss_reduce[side]";
+      bwd.back().side = true;
+      bwd.back().mode = 2;
+    }
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
+    if (fork && !dp) {
+      // a whole single-GPU step updates the ip layers on the side branch once
+      // ip1's data gradient (the last reader of W1t) is done: overlaps the conv backward
+      add_fork(net, bwd, "fork2[side]", net->ev_ipd);
+      bwd.back().mode = 2;
+      bwd.push_back(solver_stage(net, "ip.solver[tc]", true, false, nullptr));
+      bwd.back().side = true;
+      bwd.back().mode = 2;
+    }
     conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
@@ -1077,6 +1107,10 @@ static void build_fused_lenet(pn_net* net) {
     conv_segs.push_back(seg(net->partials + c1.part_off, G + c1.off, 520, c1.splits, 520));
   }
   add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
+  net->conv_segs = conv_segs;
+  // a whole single-GPU TF32 step reduces the conv bucket inside the solver
+  // (build_update); with data parallelism the reduced bucket is all-reduced first
+  if (net->tf32 && !dp) bwd.back().mode = 1;
   if (fork) {  // the ip branch joins before the solver (its gradients are ready)
     Stage j;
     j.name = "join[side]";
@@ -1088,7 +1122,54 @@ static void build_fused_lenet(pn_net* net) {
   }
 }
 
+// the fused TF32 solver over a part of the parameters: ip (the ip layers:
+// ip1 weight tiles + the plain ip2 / ip1-bias ranges), conv (the conv bucket
+// as reduce segments: `segs`, or its already-reduced gradients)
+static Stage solver_stage(pn_net* net, const std::string& name, bool ip, bool conv, const std::vector<ReduceP>* segs) {
+  const Layer &c1 = net->layers[0], &c2 = net->layers[2], &i1 = net->layers[4], &i2 = net->layers[6];
+  float* G = net->grads;
+  tc::SolverP p{};
+  p.w = net->params, p.g = G, p.v = net->hist;
+  p.w1_off = i1.off, p.w2_off = c2.off;
+  p.w1f = net->pack.w1f, p.w1t = net->pack.w1t, p.w2c = net->pack.w2c, p.w2t = net->pack.w2t;
+  if (ip) {
+    p.w1_tiles = 400;
+    p.plain_lo[0] = i2.off, p.plain_hi[0] = i2.off + i2.wcount + i2.bcount;
+    p.plain_lo[1] = i1.off + i1.wcount, p.plain_hi[1] = i1.off + i1.wcount + i1.bcount;
+    p.nplain = 2;
+  }
+  if (conv && segs) {
+    p.nseg = (int)segs->size();
+    for (int k = 0; k < p.nseg && k < 4; ++k) p.seg[k] = (*segs)[k];
+  } else if (conv) {  // gradients already reduced: one-split segments over the gradient blob
+    const int n2 = (int)(c2.wcount + c2.bcount), n1 = (int)(c1.wcount + c1.bcount);
+    p.seg[0] = ReduceP{G + c2.off, G + c2.off, n2, 1, n2};
+    p.seg[1] = ReduceP{G + c1.off, G + c1.off, n1, 1, n1};
+    p.nseg = 2;
+  }
+  Stage s;
+  s.name = name;
+  s.L = tc::lenet_solver_launch(p);
+  s.patch = [](Launch& l, const StepArgs& a) {
+    tc::SolverP& q = l.params<tc::SolverP>();
+    q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale; q.lr_dev = a.lr_dev;
+  };
+  return s;
+}
+
 static void build_update(pn_net* net) {
+  if (net->fused && net->tf32) {  // reduce (conv bucket) + SGD + the TF32 weight copies
+    const bool dp = net->comm || net->loop;
+    net->phase[2].push_back(solver_stage(net, "solver[tc]", true, true, nullptr));
+    if (!dp) {
+      // the whole single-GPU step: the ip part ran on the side branch (build_fused_lenet);
+      // the conv bucket's partials are summed here (reduce_partials_multi's order)
+      net->phase[2].back().mode = 1;
+      net->phase[2].push_back(solver_stage(net, "conv.reduce+solver[tc]", false, true, &net->conv_segs));
+      net->phase[2].back().mode = 2;
+    }
+    return;
+  }
   SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f, nullptr};
   Launch l;
   long long n4 = net->nparams / 4;
@@ -1210,7 +1291,7 @@ static pn_status build_plan(pn_net* net) {
   int n = 0;
   for (auto& ph : net->phase)
     for (auto& s : ph)
-      if (!s.custom) ++n;
+      if (!s.custom && in_run(s, true)) ++n;
   net->launches_per_step = n;
   return PN_OK;
 }
@@ -1229,10 +1310,14 @@ static pn_status run_stage(pn_net* net, Stage& s, const StepArgs& a, cudaStream_
   return PN_OK;
 }
 
+static pn_status ensure_packed(pn_net* net, cudaStream_t st);
+
 // a phase run eagerly: its first kernel follows whatever the caller enqueued
 static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t st) {
+  TRY(ensure_packed(net, st));
   bool prev_kernel = false;  // (main stream; side-stream kernels run without PDL)
   for (auto& s : net->phase[ph]) {
+    if (!in_run(s, false)) continue;
     if (s.side) {
       TRY(run_stage(net, s, a, net->side, false));
       continue;
@@ -1240,6 +1325,16 @@ static pn_status run_phase(pn_net* net, int ph, const StepArgs& a, cudaStream_t 
     TRY(run_stage(net, s, a, st, prev_kernel));
     if (!s.transparent) prev_kernel = !s.custom;
   }
+  return PN_OK;
+}
+
+// the TF32 weight copies after the parameters changed through the ABI (the
+// solver keeps them current from then on); stand-alone, stream-ordered
+static pn_status ensure_packed(pn_net* net, cudaStream_t st) {
+  if (!(net->fused && net->tf32) || !net->pack_dirty) return PN_OK;
+  CU(cudaSetDevice(net->device));
+  CU(tc::pack_weights_launch(net->pack).launch(st));
+  net->pack_dirty = false;
   return PN_OK;
 }
 
@@ -1273,6 +1368,7 @@ static pn_status capture(pn_net* net, int nph, const StepArgs& a, GraphExec& E) 
   bool prev_kernel = false;  // the captured step is one fixed sequence across phases
   for (int ph = 0; ph < nph; ++ph)
     for (auto& s : net->phase[ph]) {
+      if (!in_run(s, nph == 3)) continue;
       cudaStream_t on = s.side ? net->side : net->cap;
       pn_status st = run_stage(net, s, a, on, s.side ? false : prev_kernel);
       if (!s.side && !s.transparent) prev_kernel = !s.custom;
@@ -1303,6 +1399,7 @@ static pn_status patch_graph(pn_net* net, int nph, const StepArgs& a, GraphExec&
   size_t i = 0;
   for (int ph = 0; ph < nph; ++ph)
     for (auto& s : net->phase[ph]) {
+      if (!in_run(s, nph == 3)) continue;
       const size_t k = i++;
       if (s.custom || !s.patch) continue;
       s.patch(s.L, a);
@@ -1326,6 +1423,7 @@ static pn_status replay(pn_net* net, int nph, const StepArgs& a, GraphExec& E, c
   if (net->loop && nph >= 2)
     return fail(PN_ERR_STATE, "a loopback data-parallel net runs its phases eagerly (net_forward / net_backward / "
                               "sgd_update): its exchange synchronises on the host");
+  TRY(ensure_packed(net, st));
   if (!E.ex) TRY(capture(net, nph, a, E));
   else if (!same_args(a, E.a)) TRY(patch_graph(net, nph, a, E));
   CU(cudaGraphLaunch(E.ex, st));
@@ -1411,6 +1509,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     CU(cudaStreamCreateWithFlags(&net->side, cudaStreamNonBlocking));
     CU(cudaEventCreateWithFlags(&net->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&net->ev_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&net->ev_ipd, cudaEventDisableTiming));
   }
   TRY(build_plan(net.get()));
   if (net->tf32 && (!tc::tensor_maps_ok() || net->tmap_failed)) return fail(PN_ERR_CUDA, "cuTensorMapEncodeTiled failed");
@@ -1429,7 +1528,7 @@ extern "C" void net_destroy(pn_net* net) {
   if (net->nccl_grads) ncclMemFree(net->nccl_grads);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
-  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join})
+  for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join, net->ev_ipd})
     if (e) cudaEventDestroy(e);
   for (int b = 0; b < pn_net::kSlots; ++b) {
     if (net->ev_copied[b]) cudaEventDestroy(net->ev_copied[b]);
@@ -1489,6 +1588,7 @@ extern "C" pn_status net_blob_ptr(pn_net* net, const char* name, int which, void
   void* r = which == PN_DATA ? (void*)b->data : which == PN_DIFF ? (void*)b->diff
           : which == PN_HISTORY ? (void*)b->hist : nullptr;
   if (!r) return fail(PN_ERR_STATE, std::string(name) + ": buffer not materialised by this plan");
+  if (b->is_param && which == PN_DATA) net->pack_dirty = true;  // the caller may write the parameters
   *p = r;
   return PN_OK;
 }
@@ -1501,6 +1601,7 @@ extern "C" pn_status net_set_param(pn_net* net, const char* name, const float* s
   if (!b->is_param) return fail(PN_ERR_INVALID_ARG, std::string(name) + " is not a parameter");
   if (!src || count != b->count()) return fail(PN_ERR_INVALID_ARG, "net_set_param: count mismatch");
   CU(cudaSetDevice(net->device));
+  net->pack_dirty = true;
   cudaStream_t st = (cudaStream_t)stream;
   if (on_host) {
     CU(cudaMemcpyAsync(b->data, src, count * 4, cudaMemcpyHostToDevice, st));
@@ -1547,6 +1648,7 @@ static pn_status blob_io(pn_net* net, const char* name, int which, void* buf, in
                           std::string(name) + ": buffer not materialised by this plan");
   }
   cudaMemcpyKind kind = on_host ? (put ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost) : cudaMemcpyDeviceToDevice;
+  if (put && b->is_param && which == PN_DATA) net->pack_dirty = true;
   if (put) {
     CU(cudaMemcpyAsync(dev, buf, bytes, kind, st));
     if (tmp) TRY(mask_io(net, b, tmp, false, st));
@@ -1758,6 +1860,7 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
     return PN_OK;
   };
   int64_t s0 = 0;
+  TRY(ensure_packed(net, st));
   if (net->fused && nsteps >= pn_net::kSlots && !getenv("PN_NO_MULTI")) {
     {  // momentum / decay / 1/G are kernel arguments of the captured steps: re-capture when they change
       const StepArgs h = make_args(net, nullptr, nullptr, nullptr, sgd, iter0);
@@ -1786,6 +1889,7 @@ extern "C" pn_status net_train_steps_u8_host(pn_net* net, const uint8_t* x8_host
         prev_kernel = false;
         for (int ph = 0; ph < 3 && err == PN_OK; ++ph)
           for (auto& stg : net->phase[ph]) {
+            if (!in_run(stg, true)) continue;
             cudaStream_t on = stg.side ? net->side : net->cap;
             if ((err = run_stage(net, stg, a, on, stg.side ? false : prev_kernel)) != PN_OK) break;
             if (!stg.side && !stg.transparent) prev_kernel = !stg.custom;
@@ -1926,6 +2030,14 @@ extern "C" pn_status net_stage_name(const pn_net* net, int phase, int i, const c
   return PN_OK;
 }
 
+extern "C" pn_status net_stage_mode(const pn_net* net, int phase, int i, int* mode) {
+  CHECK_NET(net);
+  if (phase < 0 || phase > 2 || i < 0 || i >= (int)net->phase[phase].size() || !mode)
+    return fail(PN_ERR_INVALID_ARG, "bad stage");
+  *mode = net->phase[phase][i].mode;
+  return PN_OK;
+}
+
 extern "C" pn_status net_run_stage(pn_net* net, int phase, int i, const float* x, const int32_t* labels,
                                    void* stream) {
   CHECK_NET(net);
@@ -1935,6 +2047,7 @@ extern "C" pn_status net_run_stage(pn_net* net, int phase, int i, const float* x
   StepArgs a = net->last;
   if (x) a.x = x;
   if (labels) a.labels = labels;
+  TRY(ensure_packed(net, (cudaStream_t)stream));
   return run_stage(net, net->phase[phase][i], a, (cudaStream_t)stream);
 }
 
@@ -2003,6 +2116,41 @@ extern "C" pn_status net_launches_per_step(const pn_net* net, int* n) {
   if (!n) return fail(PN_ERR_INVALID_ARG, "n is NULL");
   *n = net->launches_per_step;
   return PN_OK;
+}
+
+// dev-only in-graph step timeline (pdl.cuh; libpn built with -DPN_STEPTRACE)
+namespace pn {
+void st_set_lenet(unsigned long long*);
+void st_set_generic(unsigned long long*);
+namespace tc {
+void st_set_tc(unsigned long long*);
+void st_set_c1(unsigned long long*);
+}  // namespace tc
+}  // namespace pn
+
+extern "C" pn_status net_steptrace(pn_net* net, unsigned long long* host_out) {
+  CHECK_NET(net);
+#ifndef PN_STEPTRACE
+  (void)host_out;
+  return fail(PN_ERR_STATE, "libpn was built without -DPN_STEPTRACE");
+#else
+  CU(cudaSetDevice(net->device));
+  static unsigned long long* buf = nullptr;
+  const size_t bytes = ST_N * 3 * sizeof(unsigned long long);
+  if (!buf) {
+    CU(cudaMalloc(&buf, bytes));
+    pn::st_set_lenet(buf);
+    pn::st_set_generic(buf);
+    pn::tc::st_set_tc(buf);
+    pn::tc::st_set_c1(buf);
+  }
+  CU(cudaDeviceSynchronize());
+  if (host_out) CU(cudaMemcpy(host_out, buf, bytes, cudaMemcpyDeviceToHost));
+  std::vector<unsigned long long> init(ST_N * 3);
+  for (int k = 0; k < ST_N; ++k) init[3 * k] = init[3 * k + 1] = ~0ull, init[3 * k + 2] = 0;
+  CU(cudaMemcpy(buf, init.data(), bytes, cudaMemcpyHostToDevice));
+  return PN_OK;
+#endif
 }
 
 extern "C" pn_status net_sync_errors(pn_net* net, void* stream) {

@@ -96,6 +96,11 @@ struct Stage {
   std::function<void(Launch&, const StepArgs&)> patch;  // refresh step-dependent args
   std::function<cudaError_t(cudaStream_t)> custom;     // non-kernel action
   bool side = false;  // in a step (graph or eager phase run): launched on the side stream, between fork and join
+  // 0: always; 1: only when phases run on their own (net_forward / net_backward /
+  // sgd_update / net_infer), skipped in a captured whole step; 2: only in a
+  // captured whole step (its replacement there, e.g. the loss sum off the
+  // critical path, the conv bucket reduced inside the solver)
+  int mode = 0;
   bool transparent = false;  // non-kernel stage that adds no dependency to its own stream (a fork's event
                              // record): the next kernel may still launch programmatically after the previous one
 };

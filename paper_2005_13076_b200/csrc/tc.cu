@@ -26,6 +26,7 @@
 #include <cstring>
 
 #include "pdl.cuh"
+#include "sgd.cuh"
 #include "tc.h"
 #include "tc_ptx.cuh"
 
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   Op op(prm);
   const int nk = op.num_k_chunks(), c0 = (int)rank * nk / SPLIT, my = ((int)rank + 1) * nk / SPLIT - c0;
   const uint32_t sbase = smem_u32(smem);
+  ST_BEGIN(Op::ST);
   if (tid == 0) {
     for (int c = 0; c < STAGES; ++c) {
       mbar_init(smem_u32(&full[c]), 1);
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
       if (Op::A_EARLY) op.issue_a(c0 + c, As, bar);
       if (Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
     }
-    pdl_enter();
+    pdl_enter_k(Op::ST);
     stamp(1);
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
@@ -227,6 +229,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   __syncthreads();
   if (tid == 0) stamp(4);
   op.finish(tid, red, (int)rank);
+  ST_END(Op::ST);
   if (warp == 0) tmem_dealloc(tbase, BN);
 }
 
@@ -242,6 +245,7 @@ struct IpFwd {
   };
   static constexpr int RED_FLOATS = 0, STAGES = IPF_STAGES, EPI_BYTES = 0, SPLIT = IPF_SPLIT, BN = IPF_BN;
   static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr int ST = ST_IPF;
   const Params& p;
   int m0, o0;
   __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * BN) {}
@@ -278,6 +282,7 @@ struct IpWgrad {
   };
   static constexpr int RED_FLOATS = 0, STAGES = IPG_STAGES, EPI_BYTES = 0, SPLIT = IPG_SPLIT, BN = IPG_BN;
   static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr int ST = ST_IPG;
   const Params& p;
   int o0, k0;
   __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
@@ -319,6 +324,7 @@ struct IpDgradUnpool {
   static constexpr int RED_FLOATS = FT * ROWS;  // red: [filter in tile][owned row]
   static constexpr int EPI_BYTES = ROWS * BN;   // the owned rows' pool2 origins [row][FT x 16]
   static constexpr bool A_EARLY = !FORK_PDL, B_EARLY = true;  // (FORK_PDL: da1r from the immediate predecessor)
+  static constexpr int ST = ST_IPD;
   const Params& p;
   int m0, k0;
   __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
@@ -435,6 +441,7 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int npairs = (p.N + 1) / 2;
   const int pair0 = blockIdx.x * p.per_cta;
+  ST_BEGIN(ST_CONV2F);
   if (tid < 50) bias_s[tid] = p.b[tid];
   const int mine = max(0, min(p.per_cta, npairs - pair0));
   if (tid == 0) stamp(0);
@@ -472,7 +479,7 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
         bulk_g2s(B_s + i * 5 * TAP_BYTES, (const uint8_t*)p.w2c + i * 5 * TAP_BYTES, 5 * TAP_BYTES,
                  smem_u32(&wbar[i]));
       }
-    pdl_enter();
+    pdl_enter_k(ST_CONV2F);
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
       const int s = it % STAGES;
@@ -574,6 +581,7 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
   tc_fence_before();
   __syncthreads();
   if (tid == 0) stamp(10);
+  ST_END(ST_CONV2F);
   if (warp == 0) tmem_dealloc(tbase, 128);
 }
 
@@ -638,6 +646,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int npairs = (p.N + 1) / 2, pair0 = blockIdx.x * p.per_cta;
   const int mine = max(0, min(p.per_cta, npairs - pair0));
+  ST_BEGIN(ST_CONV2D);
   if (tid == 0) {
     mbar_init(smem_u32(&afull), 1);
     mbar_init(smem_u32(&gfull), 128);
@@ -718,7 +727,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
     }
   } else if (warp >= 2 && warp < 6) {
     // ---- B builders: thread = (image n, position h*8+w); 13 planes of 4 f
-    pdl_enter();  // G2 comes from the immediate predecessor
+    pdl_enter_k(ST_CONV2D);  // G2 comes from the immediate predecessor
     if (tid == 64) stamp(11);
     const int t = tid - 64, n = t >> 6, pos = t & 63, h = pos >> 3, w = pos & 7;
     const uint32_t dst0 = (uint32_t)((4 + 12 * n + h) * 128 + w * 16);
@@ -810,6 +819,7 @@ __global__ void __launch_bounds__(dg::THREADS_D, 1) conv2_dgrad_persistent(const
   tc_fence_before();
   __syncthreads();
   if (tid == 0) stamp(10);
+  ST_END(ST_CONV2D);
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
@@ -854,6 +864,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   const int m = blockIdx.x, split = blockIdx.y;
   const int n0 = (int)((long long)p.N * split / p.splits), n1 = (int)((long long)p.N * (split + 1) / p.splits);
   const int nimg = n1 - n0;
+  ST_BEGIN(ST_CONV2W);
   // (c,i) pairs and input channels this row tile touches
   const int R0 = 128 * m, P_lo = R0 / 5, P_hi = min(R0 + 127, 499) / 5, NP = P_hi - P_lo + 1;
   const int c_lo = P_lo / 5, nch = P_hi / 5 - c_lo + 1;
@@ -882,7 +893,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   if (tid == 0) {
     // ---- producer (G2 and p1 come from the two preceding launches' producers:
     // wait for the immediate predecessor first)
-    pdl_enter();
+    pdl_enter_k(ST_CONV2W);
     const uint32_t bytes = nch * 576 + G_BYTES;
 #pragma unroll 1
     for (int t = 0; t < nimg; ++t) {
@@ -987,6 +998,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   if (warp == 2 && lane == 0) stamp(10);  // partials written
   tc_fence_before();
   __syncthreads();
+  ST_END(ST_CONV2W);
   if (warp == 0) tmem_dealloc(tbase, 64);
 }
 
@@ -1004,7 +1016,8 @@ constexpr int W1_TILES = (800 / 32) * (512 / 32);  // 32 x 32 tiles of W1 (o pad
 // through shared memory (W1f rows and W1t rows both coalesced); the rest pack
 // W2c and W2d element-wise.
 __global__ void pack_weights(const __grid_constant__ PackP p) {
-  pdl_enter();
+  ST_BEGIN(ST_PACK);
+  pdl_enter_k(ST_PACK);
   __shared__ float t[32][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 256 threads: 8 rows per pass
   // W1 tiles (grid-stride: PACK_GRID > 0 runs the pack in fewer, longer blocks)
@@ -1044,7 +1057,107 @@ __global__ void pack_weights(const __grid_constant__ PackP p) {
       p.w2t[e] = tf32f(v);
     }
   }
+  ST_END(ST_PACK);
 }
+// ---------------------------------------------------------- fused solver
+// The TF32 plan's solver (a17, S:536-544 / R11): one launch that, per
+// parameter, takes the gradient (conv bucket: the fixed-order sum of the
+// weight-gradient partials, the same order as reduce_partials_multi, written
+// back to the gradient blob; ip bucket: already reduced), applies the SGD
+// update (sgd_one) and writes the TF32 copies the next step's contractions
+// read (W1f, W1t, W2c, W2d -- the weight pack, so no packing launch opens the
+// next step).  Blocks [0, W1_TILES): a 32 x 32 tile of ip1's weights (W1t
+// through a shared-memory transpose); then 32-output blocks over the reduce
+// segments (8 warps over the splits, warp 0 sums the 8 in order and updates);
+// then grid-stride blocks over the plain ranges.  A single-GPU whole step
+// splits it: the ip layers' part on the backward's side branch (their
+// gradients are final after ip1's weight gradient; it overlaps the conv
+// backward), the conv bucket's at the end.  w1_tiles = 0: no ip1 weights.
+__global__ void __launch_bounds__(256) lenet_solver(const __grid_constant__ SolverP p) {
+  const int stk = p.w1_tiles ? ST_OTHER : ST_SGD;  // (step trace: the ip part / the rest)
+  ST_BEGIN(stk);
+  pdl_enter_k(stk);
+  const float lr = p.lr_dev ? __ldg(p.lr_dev) : p.lr;
+  const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+  if ((int)blockIdx.x < p.w1_tiles) {
+    __shared__ float t[32][33];
+    const int tile = blockIdx.x, k0 = (tile % 25) * 32, o0 = (tile / 25) * 32;
+    float w[4], v[4], g[4];  // the tile's four rows per thread: all loads in flight together
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = o0 + wp + 8 * u;
+      const long long i = p.w1_off + (long long)min(o, 499) * 800 + k0 + lane;
+      w[u] = __ldcg(p.w + i), v[u] = __ldcg(p.v + i), g[u] = __ldcg(p.g + i);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int o = o0 + wp + 8 * u;
+      float wf = 0.f;
+      if (o < 500) {
+        const long long i = p.w1_off + (long long)o * 800 + k0 + lane;
+        sgd_one(w[u], g[u], v[u], lr, p.mom, p.decay, p.gscale);
+        p.w[i] = w[u];
+        p.v[i] = v[u];
+        wf = tf32f(w[u]);
+        p.w1f[(size_t)o * 800 + k0 + lane] = wf;
+      }
+      t[wp + 8 * u][lane] = wf;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 4; ++u) p.w1t[(size_t)(k0 + wp + 8 * u) * 512 + o0 + lane] = t[lane][wp + 8 * u];
+  } else if ((int)blockIdx.x < p.w1_tiles + p.seg_blocks) {
+    __shared__ float sm[8][33];
+    int b = blockIdx.x - p.w1_tiles, k = 0;
+    while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
+    const ReduceP& s = p.seg[k];
+    const int i = b * 32 + lane;
+    float acc = 0.f;
+    if (i < s.n) {  // splits wp, wp+8, ... ascending, 8 loads in flight (reduce_partials_multi's order)
+      int j = wp;
+      for (; j + 56 < s.splits; j += 64) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = __ldcg(s.part + (long long)(j + 8 * q) * s.stride + i);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc += v[q];
+      }
+      for (; j < s.splits; j += 8) acc += __ldcg(s.part + (long long)j * s.stride + i);
+    }
+    sm[wp][lane] = acc;
+    __syncthreads();
+    if (wp == 0 && i < s.n) {
+      float r = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) r += sm[q][lane];
+      if (s.part != s.out) s.out[i] = r;  // the reduced gradient stays readable
+      const long long e = (s.out - p.g) + i;
+      float w = p.w[e], v = p.v[e];
+      sgd_one(w, r, v, lr, p.mom, p.decay, p.gscale);
+      p.w[e] = w;
+      p.v[e] = v;
+      const long long q2 = e - p.w2_off;
+      if (q2 >= 0 && q2 < 25000) {  // conv2 weight (f, c, i, j): its W2c and W2d slots
+        const int f = (int)q2 / 500, c = ((int)q2 / 25) % 20, ii = ((int)q2 / 5) % 5, jj = (int)q2 % 5;
+        const float wf = tf32f(w);
+        p.w2c[(ii * 5 + jj) * 1000 + (c >> 2) * 200 + f * 4 + (c & 3)] = wf;
+        p.w2t[((ii * dg::PLANES + (f >> 2)) * dg::AROWS + c * 5 + jj) * 4 + (f & 3)] = wf;
+      }
+    }
+  } else {
+    const int nb = gridDim.x - p.w1_tiles - p.seg_blocks;
+    const int t0 = (blockIdx.x - p.w1_tiles - p.seg_blocks) * 256 + tid;
+    for (int r = 0; r < p.nplain; ++r)
+      for (long long e = p.plain_lo[r] + t0; e < p.plain_hi[r]; e += (long long)nb * 256) {
+        float w = p.w[e], v = p.v[e];
+        sgd_one(w, p.g[e], v, lr, p.mom, p.decay, p.gscale);
+        p.w[e] = w;
+        p.v[e] = v;
+      }
+  }
+  ST_END(stk);
+}
+
 // p1c (conv2 forward operand, see conv2_fwd_persistent) from an NCHW pool1
 // blob, TF32-rounded: used when pool1 is overwritten through the ABI (the
 // forward pass writes p1c directly from conv1+pool1).
@@ -1074,6 +1187,8 @@ __global__ void pack_p1c_k(const __grid_constant__ PackP1cArgs a) {
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+PN_STEPTRACE_TU(st_set_tc)
+
 static EncodeTiledFn encode_fn() {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
@@ -1147,6 +1262,15 @@ cudaError_t setup() {
 bool tensor_maps_ok() { return g_tmap_ok; }
 
 static unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
+
+Launch lenet_solver_launch(const SolverP& p0) {
+  SolverP p = p0;
+  p.seg_blocks = 0;
+  for (int k = 0; k < p.nseg; ++k) p.seg_blocks += (p.seg[k].n + 31) / 32;
+  Launch l;
+  l.set((const void*)lenet_solver, dim3(p.w1_tiles + p.seg_blocks + (p.nplain ? 8 : 0)), dim3(256), 0, p);
+  return l;
+}
 
 Launch pack_weights_launch(const PackP& p) {
   Launch l;

@@ -91,6 +91,7 @@ __global__ void __launch_bounds__(c1::THREADS, 1) conv1_pool1_tc(const __grid_co
   using namespace c1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  ST_BEGIN(ST_CONV1);
   const uint32_t B_s = smem_u32(smem), X_s = B_s + B_BYTES, S_s = X_s + XS_FLOATS * 4;
   // afull[set]: the batch's SUP tiles built (SUP warps arrive); mdone[set]:
   // its MMAs retired (one commit: frees the A tiles and fills the
@@ -275,9 +276,12 @@ __global__ void __launch_bounds__(c1::THREADS, 1) conv1_pool1_tc(const __grid_co
   tc_fence_before();
   __syncthreads();
   if (tid == 0) stamp(8);
-  pdl_enter();
+  pdl_enter_k(ST_CONV1);
+  ST_END(ST_CONV1);
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
+
+PN_STEPTRACE_TU(st_set_c1)
 
 cudaError_t conv1_setup() {
   return cudaFuncSetAttribute((const void*)conv1_pool1_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, c1::SMEM);

@@ -199,6 +199,14 @@ class Net:
         check(lib().net_infer(self._h, _ptr(x, 'f32'), _ptr(labels, 'i32'), _ptr(loss, 'f32'),
                               _stream(stream)))
 
+    def net_steptrace(self, read=True):
+        """Dev-only (a -DPN_STEPTRACE build): the per-kernel in-graph timeline
+        recorded since the last call, as a list of 16 (entry, waited, exit) ns,
+        then re-arm."""
+        buf = (ctypes.c_ulonglong * 48)()
+        check(lib().net_steptrace(self._h, buf if read else None))
+        return [(buf[3 * k], buf[3 * k + 1], buf[3 * k + 2]) for k in range(16)]
+
     def net_sync_errors(self, stream=None):
         check(lib().net_sync_errors(self._h, _stream(stream)))
 
@@ -211,6 +219,16 @@ class Net:
             s = ctypes.c_char_p()
             check(lib().net_stage_name(self._h, phase, i, ctypes.byref(s)))
             out.append(s.value.decode())
+        return out
+
+    def stage_modes(self, phase):
+        """Per stage: 0 always, 1 only in phases run on their own, 2 only in a
+        whole captured step (net_stage_mode)."""
+        out = []
+        for i in range(len(self.stages(phase))):
+            m = ctypes.c_int()
+            check(lib().net_stage_mode(self._h, phase, i, ctypes.byref(m)))
+            out.append(m.value)
         return out
 
     def net_run_stage(self, phase, i, x=None, labels=None, stream=None):

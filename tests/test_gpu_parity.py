@@ -156,12 +156,16 @@ def test_net_forward_backward(spec, N, tf32, layerwise):
     check_net_level(net, ref, params, out, gref, loss.item(), rtol)
 
 
-def test_train_step_graph_equals_eager_and_is_deterministic():
+@pytest.mark.parametrize("tf32", [False, True])
+def test_train_step_graph_equals_eager_and_is_deterministic(tf32):
+    """The whole-step graph (TF32: loss sum on the side branch, conv bucket
+    reduced inside the solver) is bitwise the eager phases (separate bucket
+    reduction, then the solver) and reruns bitwise."""
     N = 64
     sgd = make_sgd()
     results = []
     for mode in ("eager", "graph", "graph"):
-        net, ref, params, x, y = make("lenet", N)
+        net, ref, params, x, y = make("lenet", N, tf32)
         xd, yd = cuda(x), cuda(y)
         loss = torch.zeros(1, device="cuda", dtype=torch.float32)
         for it in range(3):
@@ -177,6 +181,30 @@ def test_train_step_graph_equals_eager_and_is_deterministic():
         assert_bitwise("eager vs graph", a, b)
     for a, b in zip(results[1][:-1], results[2][:-1]):
         assert_bitwise("graph rerun", a, b)
+
+
+def test_solver_weight_copies_match_a_fresh_pack():
+    """The TF32 plan's solver writes the tensor-core weight copies (W1f, W1t,
+    W2c, W2d) with the update; a forward and backward through those copies is
+    bitwise the same as through copies packed from the updated parameters
+    (re-set through the ABI: the pack runs before the next pass)."""
+    N = 64
+    net, ref, params, x, y = make("lenet", N, True)
+    sgd = make_sgd()
+    xd, yd = cuda(x), cuda(y)
+    for it in range(3):
+        net.net_train_step(xd, yd, sgd, it)
+    outs = []
+    for repack in (False, True):
+        if repack:
+            for k in params:
+                net.net_set_param(k, net.net_get_blob(k).clone())
+        net.net_forward(xd, yd)
+        net.net_backward()
+        outs.append([host(net.net_get_blob(b)) for b in ("ip1", "ip2")] +
+                    [host(net.net_get_blob(k, PN_DIFF)) for k in params])
+    for a, b in zip(*outs):
+        assert_bitwise("solver-written vs packed TF32 copies", a, b)
 
 
 @pytest.mark.parametrize("tf32", [False, True])

@@ -24,7 +24,7 @@ STAGE_OF = {"conv2_fwd_persistent": "conv2+pool2[tc]", "IpFwd": "ip1+relu[tc]", 
             "conv2_dgrad_persistent": "conv2.dgrad[tc]", "conv2_wgrad_persistent": "conv2.wgrad[tc]",
             "lenet_conv1_wgrad": "conv1.wgrad", "lenet_conv1_pool1": "conv1+pool1",
             "lenet_ip2_loss": "ip2+softmax_loss", "lenet_ip2_bwd": "ip2.bwd+relu1.bwd",
-            "pack_weights": "wpack[tc]", "sgd_update_kernel": "sgd"}
+            "pack_weights": "wpack[tc]", "sgd_update_kernel": "sgd", "lenet_solver": "reduce+solver[tc]"}
 
 
 def launches(path):
