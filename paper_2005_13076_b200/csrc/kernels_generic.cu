@@ -9,6 +9,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "reduce.cuh"
 #include "sgd.cuh"
 
 namespace pn {
@@ -171,19 +172,7 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
   const ReduceP& s = p.seg[k];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int i = b * 32 + lane;
-  float acc = 0.f;
-  if (i < s.n) {  // splits w, w+8, ... in ascending order; loads issued 8 at a time
-    int j = w;
-    for (; j + 56 < s.splits; j += 64) {
-      float v[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = __ldcg(s.part + (long long)(j + 8 * q) * s.stride + i);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc += v[q];
-    }
-    for (; j < s.splits; j += 8) acc += __ldcg(s.part + (long long)j * s.stride + i);
-  }
-  sm[w][lane] = acc;
+  sm[w][lane] = split_sum_warp(s, i, w);  // splits w, w+8, ... ascending (reduce.cuh)
   __syncthreads();
   if (w == 0 && i < s.n) {
     float r = 0.f;

@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "solver.cuh"
 
 namespace pn {
 
@@ -545,7 +546,7 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // dp1 comes from conv2's data gradient two launches back (the predecessor,
 // conv2's weight gradient, produces nothing read here): the kernel runs
 // alongside it and waits only at the end (pdl.cuh).
-__global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
+__global__ void __launch_bounds__(320, 2) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
   __shared__ float xs[CW_IMGS][784];
   ST_BEGIN(ST_CONV1W);
   const int s = blockIdx.x;
@@ -610,7 +611,13 @@ __global__ void __launch_bounds__(320) lenet_conv1_wgrad(const __grid_constant__
     for (int t = 0; t < 25; ++t) p.part_w[(long long)s * p.pstride + f * 25 + t] = acc[t];
     p.part_b[(long long)s * p.pstride + f] = bacc;
   }
+  // dp1 came from two launches back; the predecessor (conv2's weight
+  // gradient) runs alongside: wait for it at the end (pdl.cuh)
   pdl_enter_k(ST_CONV1W);
+  if (p.tail) {  // a single-GPU whole step: the conv bucket's solver (solver.cuh)
+    grid_barrier(p.bar, gridDim.x);
+    solver_tail(p.sp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+  }
   ST_END(ST_CONV1W);
 }
 

@@ -283,6 +283,8 @@ struct pn_net {
   // TF32 fused plan: the packed weight copies (pack.w1f ...) no longer match
   // the parameters (set through the ABI): packed before the next run
   bool pack_dirty = true;
+  unsigned long long* bar = nullptr;
+  bool conv_tail = false;  // the conv bucket's solver as conv1's weight-gradient tail (build_fused_lenet)
   std::vector<ReduceP> conv_segs;  // the conv bucket's partial sums (the step's solver reduces them)
 
   // data parallel
@@ -561,6 +563,7 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->pack.w1t, tc::kW1tFloats));
     TRY(net->alloc(&net->pack.w2c, tc::kW2cFloats));
     TRY(net->alloc(&net->pack.w2t, tc::kW2tFloats));
+    TRY(net->alloc(&net->bar, 1));  // grid-barrier counter of the conv solver tail (conv1 weight gradient)
     net->npad = (net->batch + 3) & ~3;  // TMA row pitch must be a multiple of 16 B
     TRY(net->alloc(&net->p2T, (size_t)800 * net->npad));
     TRY(net->alloc(&net->p1c, (size_t)((net->batch + 1) / 2) * tc::kP1cPairFloats));
@@ -956,6 +959,12 @@ static void build_fused_lenet(pn_net* net) {
   // previous step (lenet_solver), or packed once after the parameters were
   // set through the ABI (ensure_packed)
   const bool dp = net->comm || net->loop;
+  net->conv_tail = false;
+  if (net->tf32 && !dp && !getenv("PN_NO_TAIL")) {  // every conv1 weight-gradient block resident at the barrier
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)lenet_conv1_wgrad, 320, 0);
+    net->conv_tail = c1.splits <= occ * net->tc_sms;
+  }
   if (net->tf32) {
     net->pack.w1 = P + i1.off;
     net->pack.w2 = P + c2.off;
@@ -1046,7 +1055,7 @@ static void build_fused_lenet(pn_net* net) {
     }
     add(bwd, "ip1.dgrad+unpool2[tc]",
         tc::ip1_dgrad_unpool_launch(net->da1r, net->pack.w1t, p2.m8, cv2.diff, net->part_db2, N));
-    if (fork && !dp) {
+    if (fork && net->conv_tail) {
       // a whole single-GPU step updates the ip layers on the side branch once
       // ip1's data gradient (the last reader of W1t) is done: overlaps the conv backward
       add_fork(net, bwd, "fork2[side]", net->ev_ipd);
@@ -1106,11 +1115,31 @@ static void build_fused_lenet(pn_net* net) {
     });
     conv_segs.push_back(seg(net->partials + c1.part_off, G + c1.off, 520, c1.splits, 520));
   }
-  add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
   net->conv_segs = conv_segs;
-  // a whole single-GPU TF32 step reduces the conv bucket inside the solver
-  // (build_update); with data parallelism the reduced bucket is all-reduced first
-  if (net->tf32 && !dp) bwd.back().mode = 1;
+  if (net->conv_tail) {
+    // a whole single-GPU TF32 step ends in conv1's weight gradient: after a
+    // grid barrier its threads reduce the conv bucket's partials, apply SGD
+    // and write the W2 copies (no bucket-reduction or solver launch); with
+    // data parallelism the bucket is reduced and all-reduced first, then the
+    // solver (phase 2)
+    bwd.back().mode = 1;
+    Stage t = bwd.back();
+    t.name = "conv1.wgrad+solver";
+    t.mode = 2;
+    Conv1WgradP& q = t.L.params<Conv1WgradP>();
+    q.tail = 1;
+    q.bar = net->bar;
+    q.sp = solver_stage(net, "", false, true, &net->conv_segs).L.params<SolverP>();
+    auto base = t.patch;
+    t.patch = [base](Launch& l, const StepArgs& a) {
+      base(l, a);
+      SolverP& s = l.params<Conv1WgradP>().sp;
+      s.lr = a.lr; s.mom = a.mom; s.decay = a.decay; s.gscale = a.gscale; s.lr_dev = a.lr_dev;
+    };
+    bwd.push_back(t);
+  }
+  add_reduce_multi(bwd, "conv.bucket_reduce", conv_segs);
+  if (net->conv_tail) bwd.back().mode = 1;
   if (fork) {  // the ip branch joins before the solver (its gradients are ready)
     Stage j;
     j.name = "join[side]";
@@ -1128,7 +1157,7 @@ static void build_fused_lenet(pn_net* net) {
 static Stage solver_stage(pn_net* net, const std::string& name, bool ip, bool conv, const std::vector<ReduceP>* segs) {
   const Layer &c1 = net->layers[0], &c2 = net->layers[2], &i1 = net->layers[4], &i2 = net->layers[6];
   float* G = net->grads;
-  tc::SolverP p{};
+  SolverP p{};
   p.w = net->params, p.g = G, p.v = net->hist;
   p.w1_off = i1.off, p.w2_off = c2.off;
   p.w1f = net->pack.w1f, p.w1t = net->pack.w1t, p.w2c = net->pack.w2c, p.w2t = net->pack.w2t;
@@ -1151,7 +1180,7 @@ static Stage solver_stage(pn_net* net, const std::string& name, bool ip, bool co
   s.name = name;
   s.L = tc::lenet_solver_launch(p);
   s.patch = [](Launch& l, const StepArgs& a) {
-    tc::SolverP& q = l.params<tc::SolverP>();
+    SolverP& q = l.params<SolverP>();
     q.lr = a.lr; q.mom = a.mom; q.decay = a.decay; q.gscale = a.gscale; q.lr_dev = a.lr_dev;
   };
   return s;
@@ -1161,13 +1190,9 @@ static void build_update(pn_net* net) {
   if (net->fused && net->tf32) {  // reduce (conv bucket) + SGD + the TF32 weight copies
     const bool dp = net->comm || net->loop;
     net->phase[2].push_back(solver_stage(net, "solver[tc]", true, true, nullptr));
-    if (!dp) {
-      // the whole single-GPU step: the ip part ran on the side branch (build_fused_lenet);
-      // the conv bucket's partials are summed here (reduce_partials_multi's order)
-      net->phase[2].back().mode = 1;
-      net->phase[2].push_back(solver_stage(net, "conv.reduce+solver[tc]", false, true, &net->conv_segs));
-      net->phase[2].back().mode = 2;
-    }
+    // the whole single-GPU step: the ip part ran on the side branch and the
+    // conv bucket's at the end of conv1's weight gradient (build_fused_lenet)
+    if (net->conv_tail) net->phase[2].back().mode = 1;
     return;
   }
   SgdP p{net->params, net->grads, net->hist, net->nparams, 0.f, 0.f, 0.f, 1.f, nullptr};
@@ -1288,6 +1313,16 @@ static pn_status build_plan(pn_net* net) {
   TRY(add_accuracy(net));
   build_update(net);
   add_dp_stages(net);
+  {  // side-branch kernels at the highest launch priority: scheduled ahead of the
+     // pending CTAs of the persistent conv backward kernels (PN_SIDE_PRIO=0: off)
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    const char* e = getenv("PN_SIDE_PRIO");
+    if (!(e && e[0] == '0'))
+      for (auto& ph : net->phase)
+        for (auto& s : ph)
+          if (s.side && !s.custom) s.L.prio = hi;
+  }
   int n = 0;
   for (auto& ph : net->phase)
     for (auto& s : ph)
@@ -1506,7 +1541,13 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }
   if (net->fused && net->tf32) {  // side stream of the single-GPU backward (build_fused_lenet)
-    CU(cudaStreamCreateWithFlags(&net->side, cudaStreamNonBlocking));
+    {  // the side branch at the highest priority: its small kernels are scheduled ahead of the
+       // pending CTAs of the persistent conv backward kernels (PN_SIDE_PRIO=0: default priority)
+      int lo = 0, hi = 0;
+      CU(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      const char* e = getenv("PN_SIDE_PRIO");
+      CU(cudaStreamCreateWithPriority(&net->side, cudaStreamNonBlocking, (e && e[0] == '0') ? 0 : hi));
+    }
     CU(cudaEventCreateWithFlags(&net->ev_fork, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&net->ev_join, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&net->ev_ipd, cudaEventDisableTiming));

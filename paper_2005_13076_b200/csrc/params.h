@@ -41,6 +41,23 @@ struct ReduceMultiP {  // several ReduceP segments in one launch
   int nseg, total;
   int late;  // inputs come from >= 2 launches back: wait on the predecessor only at the end (pdl.cuh)
 };
+// The TF32 LeNet plan's fused solver (tc.cu lenet_solver, solver.cuh solver_tail):
+// reduce + SGD + the TF32 weight copies
+struct SolverP {
+  float* w;        // flat parameters
+  float* g;        // flat gradients
+  float* v;        // flat momentum history
+  float lr, mom, decay, gscale;
+  const float* lr_dev;
+  long long w1_off, w2_off;  // ip1.w / conv2.w offsets in the flat buffers
+  float *w1f, *w1t, *w2c, *w2t;
+  ReduceP seg[4];  // gradient = fixed-order sum of partials (part == out: already reduced)
+  int nseg, seg_blocks;
+  int w1_tiles;  // 0, or the 400 W1 tiles (ip1 weights + W1f / W1t)
+  long long plain_lo[3], plain_hi[3];  // other parameters (gradients already reduced)
+  int nplain;
+};
+
 struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   const float* x;
   float* y;
@@ -202,6 +219,9 @@ struct Conv1WgradP {  // dp1 + m1 + x -> partial dW1, db1
   const uint8_t* x8;  // optional byte input, as Conv1Pool1P
   float x_scale;
   const float* x_mean;
+  int tail;                 // 1: the conv bucket's solver after a grid barrier (solver.cuh)
+  unsigned long long* bar;  // grid-barrier counter (monotonic)
+  SolverP sp;               // the conv bucket: reduce segments, SGD, W2c / W2d copies
 };
 struct LoopSumP {  // test-hook exchange: rank-order sum of one bucket over n ranks' buffers (net.cu)
   float* buf[8];
@@ -257,6 +277,7 @@ struct GmP {  // gm[f][n*HoWo + pos] = tf32(g[n][f][pos])
   float* gm;  // [rows][pitch]
   int N, F, HoWo, pitch;
 };
+
 struct PackPlainP {  // TF32 copy of W [F][K] as [F][pitch]
   const float* w;
   float* out;

@@ -37,6 +37,7 @@ struct Launch {
   const void* func = nullptr;
   dim3 grid, block;
   dim3 cluster{1, 1, 1};  // thread-block cluster dims (1 = none)
+  int prio = 0;           // launch priority attribute (0 = the stream's)
   size_t smem = 0;
   std::vector<unsigned char> arg;
   template <class P>
@@ -70,7 +71,7 @@ struct Launch {
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[3];
     unsigned n = 0;
     if (pdl_ok && pdl()) {
       at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -81,6 +82,10 @@ struct Launch {
       at[n].val.clusterDim.x = cluster.x;
       at[n].val.clusterDim.y = cluster.y;
       at[n++].val.clusterDim.z = cluster.z;
+    }
+    if (prio != 0) {
+      at[n].id = cudaLaunchAttributePriority;
+      at[n++].val.priority = prio;
     }
     cfg.attrs = at;
     cfg.numAttrs = n;

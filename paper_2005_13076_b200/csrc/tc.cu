@@ -26,7 +26,9 @@
 #include <cstring>
 
 #include "pdl.cuh"
+#include "reduce.cuh"
 #include "sgd.cuh"
+#include "solver.cuh"
 #include "tc.h"
 #include "tc_ptx.cuh"
 
@@ -615,8 +617,10 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
 #define DG_RESTRICT 1
 #endif
 namespace dg {
-constexpr int PLANES = 14;                          // 56 f (50 + zeros), 7 K steps of 8
+constexpr int PLANES = 14;
+static_assert(PLANES == kW2dPlanes, "W2d layout (solver.cuh)");                          // 56 f (50 + zeros), 7 K steps of 8
 constexpr int AROWS = 104;                          // (c,j) rows 0..99 + 4 zero rows
+static_assert(AROWS == kW2dRows, "W2d layout (solver.cuh)");
 constexpr int A_PLANE = AROWS * 16;                 // 1664 B
 constexpr int A_TAP = PLANES * A_PLANE;             // 23296 B
 constexpr int A_BYTES = 5 * A_TAP + 384;            // + the rows 104..127 the M=128 MMA over-reads
@@ -852,6 +856,7 @@ struct Params {
   int N, splits, pstride;
 };
 }  // namespace wg
+
 
 __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const __grid_constant__ wg::Params p) {
   using namespace wg;
@@ -1112,19 +1117,7 @@ __global__ void __launch_bounds__(256) lenet_solver(const __grid_constant__ Solv
     while (k < p.nseg - 1 && b >= (p.seg[k].n + 31) / 32) b -= (p.seg[k++].n + 31) / 32;
     const ReduceP& s = p.seg[k];
     const int i = b * 32 + lane;
-    float acc = 0.f;
-    if (i < s.n) {  // splits wp, wp+8, ... ascending, 8 loads in flight (reduce_partials_multi's order)
-      int j = wp;
-      for (; j + 56 < s.splits; j += 64) {
-        float v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = __ldcg(s.part + (long long)(j + 8 * q) * s.stride + i);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc += v[q];
-      }
-      for (; j < s.splits; j += 8) acc += __ldcg(s.part + (long long)j * s.stride + i);
-    }
-    sm[wp][lane] = acc;
+    sm[wp][lane] = split_sum_warp(s, i, wp);  // reduce_partials_multi's order (reduce.cuh)
     __syncthreads();
     if (wp == 0 && i < s.n) {
       float r = 0.f;

@@ -28,21 +28,7 @@ constexpr int kW1fFloats = 500 * 800, kW1tFloats = 800 * 512, kW2cFloats = 25000
 cudaError_t setup();    // driver entry point + opt-in shared memory sizes
 bool tensor_maps_ok();  // false if any cuTensorMapEncodeTiled call failed
 Launch pack_weights_launch(const PackP& p);
-// The fused solver (reduce + SGD + TF32 weight copies; tc.cu "fused solver")
-struct SolverP {
-  float* w;        // flat parameters
-  float* g;        // flat gradients
-  float* v;        // flat momentum history
-  float lr, mom, decay, gscale;
-  const float* lr_dev;
-  long long w1_off, w2_off;  // ip1.w / conv2.w offsets in the flat buffers
-  float *w1f, *w1t, *w2c, *w2t;
-  ReduceP seg[4];  // gradient = fixed-order sum of partials (part == out: already reduced)
-  int nseg, seg_blocks;
-  int w1_tiles;  // 0, or the 400 W1 tiles (ip1 weights + W1f / W1t)
-  long long plain_lo[3], plain_hi[3];  // other parameters (gradients already reduced)
-  int nplain;
-};
+// the fused solver (reduce + SGD + TF32 weight copies; tc.cu "fused solver")
 Launch lenet_solver_launch(const SolverP& p);
 // conv2 forward operand layout p1c: per image pair [5 cc][12 h][2 n][12 w][4 c] floats
 constexpr int kP1cPairFloats = 5 * 12 * 2 * 12 * 4;
