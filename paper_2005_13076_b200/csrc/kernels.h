@@ -15,6 +15,8 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
 template <int KH, int KW, int SH, int SW>
 __global__ void pool_bwd_plane(const __grid_constant__ PoolBwdP p);
 __global__ void gemm_generic(const __grid_constant__ GemmP p);
+template <int AT, int BT>
+__global__ void gemm_tiled(const __grid_constant__ GemmP p);
 __global__ void ip_fwd_rows(const __grid_constant__ IpRowsP p);
 __global__ void colsum_generic(const __grid_constant__ ColSumP p);
 __global__ void relu_fwd_generic(const __grid_constant__ ReluP p);

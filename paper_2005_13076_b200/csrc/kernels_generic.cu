@@ -481,6 +481,135 @@ __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ Gemm
   }
 }
 
+// Register-tiled fp32 GEMM (the fp32 plans' inner products: LeNet ip1 forward,
+// weight and data gradients; the layerwise plans' IP layers).  C = A B as
+// gemm_generic, with compile-time operand layouts: AT = 0 A(m,k) at
+// A[m*sam + k] (K-contiguous), AT = 1 at A[k*sak + m] (M-contiguous); BT = 0
+// B(k,n) at B[n*sbn + k], BT = 1 at B[k*sbk + n].  Tile 64 x 32, K step 16,
+// 128 threads x (4 x 4) outputs (float4 shared loads), float4 global loads
+// staged through registers one K step ahead into double-buffered shared
+// tiles (one barrier per step).  fp32 FMAs in ascending k per output.
+template <int AT, int BT>
+__global__ void __launch_bounds__(128) gemm_tiled(const __grid_constant__ GemmP p) {
+  pdl_enter();
+  constexpr int BM = 64, BN = 32, BK = 16;
+  __shared__ __align__(16) float As[2][BK][BM + 4];
+  __shared__ __align__(16) float Bs[2][BK][BN + 4];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int tm = (tid >> 3) * 4, tn = (tid & 7) * 4;
+  float4 ra[2], rb;
+  auto load = [&](int k0) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + 128 * r;  // 256 float4 of A's 64 x 16 tile
+      float v[4];
+      if (AT == 0) {  // row m = e / 4, k = 4 (e % 4) .. +3
+        const int m = m0 + (e >> 2), k = k0 + 4 * (e & 3);
+        if (m < p.M && k + 3 < p.K) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(p.A + (long long)m * p.sam + k));
+          v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (m < p.M && k + q < p.K) ? __ldg(p.A + (long long)m * p.sam + k + q) : 0.f;
+        }
+      } else {  // k = e / 16, m = 4 (e % 16) .. +3
+        const int k = k0 + (e >> 4), m = m0 + 4 * (e & 15);
+        if (k < p.K && m + 3 < p.M) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(p.A + (long long)k * p.sak + m));
+          v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (k < p.K && m + q < p.M) ? __ldg(p.A + (long long)k * p.sak + m + q) : 0.f;
+        }
+      }
+      ra[r] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    {
+      const int e = tid;  // 128 float4 of B's 16 x 32 tile
+      float v[4];
+      if (BT == 0) {  // n = e / 4, k = 4 (e % 4) .. +3
+        const int n = n0 + (e >> 2), k = k0 + 4 * (e & 3);
+        if (n < p.N && k + 3 < p.K) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(p.B + (long long)n * p.sbn + k));
+          v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (n < p.N && k + q < p.K) ? __ldg(p.B + (long long)n * p.sbn + k + q) : 0.f;
+        }
+      } else {  // k = e / 8, n = 4 (e % 8) .. +3
+        const int k = k0 + (e >> 3), n = n0 + 4 * (e & 7);
+        if (k < p.K && n + 3 < p.N) {
+          const float4 t = __ldg(reinterpret_cast<const float4*>(p.B + (long long)k * p.sbk + n));
+          v[0] = t.x, v[1] = t.y, v[2] = t.z, v[3] = t.w;
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (k < p.K && n + q < p.N) ? __ldg(p.B + (long long)k * p.sbk + n + q) : 0.f;
+        }
+      }
+      rb = make_float4(v[0], v[1], v[2], v[3]);
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const int e = tid + 128 * r;
+      if (AT == 0) {
+        const int m = e >> 2, k = 4 * (e & 3);
+        As[buf][k][m] = ra[r].x, As[buf][k + 1][m] = ra[r].y, As[buf][k + 2][m] = ra[r].z, As[buf][k + 3][m] = ra[r].w;
+      } else {
+        *reinterpret_cast<float4*>(&As[buf][e >> 4][4 * (e & 15)]) = ra[r];
+      }
+    }
+    if (BT == 0) {
+      const int n = tid >> 2, k = 4 * (tid & 3);
+      Bs[buf][k][n] = rb.x, Bs[buf][k + 1][n] = rb.y, Bs[buf][k + 2][n] = rb.z, Bs[buf][k + 3][n] = rb.w;
+    } else {
+      *reinterpret_cast<float4*>(&Bs[buf][tid >> 3][4 * (tid & 7)]) = rb;
+    }
+  };
+  float acc[4][4] = {};
+  const int nk = (p.K + BK - 1) / BK;
+  load(0);
+  store(0);
+  __syncthreads();
+#pragma unroll 1
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load((kt + 1) * BK);  // next step's loads in flight under this step's FMAs
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][tm]);
+      const float4 b = *reinterpret_cast<const float4*>(&Bs[buf][kk][tn]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    if (kt + 1 < nk) store(buf ^ 1);  // the other buffer: last read one step ago (barrier below)
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + tm + i;
+    if (gm >= p.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tn + j;
+      if (gn >= p.N) continue;
+      float v = acc[i][j];
+      if (p.bias) v += p.bias[gn];
+      if (p.relu) v = v > 0.f ? v : 0.f;
+      p.C[(long long)gm * p.N + gn] = v;
+    }
+  }
+}
+template __global__ void gemm_tiled<0, 0>(const __grid_constant__ GemmP);
+template __global__ void gemm_tiled<0, 1>(const __grid_constant__ GemmP);
+template __global__ void gemm_tiled<1, 0>(const __grid_constant__ GemmP);
+template __global__ void gemm_tiled<1, 1>(const __grid_constant__ GemmP);
+
 // Inner-product forward for few outputs and long K (cifar10_quick ip1/ip2,
 // the AlexNet trunk's classifier): block = 4 rows x 8 outputs, its
 // 8 warps split K (float4 lanes), warp-shuffle then fixed-order cross-warp

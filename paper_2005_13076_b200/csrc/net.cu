@@ -685,6 +685,24 @@ static void add_loss(pn_net* net, std::vector<Stage>& fwd) {
   add(fwd, "loss_reduce", l, [](Launch& l, const StepArgs& a) { l.params<LossReduceP>().loss_out = a.loss; });
 }
 
+// C = A B on the register-tiled fp32 GEMM when the operand layouts allow
+// float4 loads (a unit stride on K or on M / N, the other a multiple of 4,
+// 16-B aligned bases), else the generic strided kernel
+static Launch gemm_launch(const GemmP& g) {
+  Launch l;
+  auto al = [](const void* p) { return ((uintptr_t)p & 15) == 0; };
+  const int at = g.sak == 1 && g.sam % 4 == 0 ? 0 : (g.sam == 1 && g.sak % 4 == 0 ? 1 : -1);
+  const int bt = g.sbk == 1 && g.sbn % 4 == 0 ? 0 : (g.sbn == 1 && g.sbk % 4 == 0 ? 1 : -1);
+  if (at < 0 || bt < 0 || !al(g.A) || !al(g.B)) {
+    l.set((const void*)gemm_generic, dim3(cdiv(g.N, 64), cdiv(g.M, 64)), dim3(256), 0, g);
+    return l;
+  }
+  const void* f = at == 0 ? (bt == 0 ? (const void*)gemm_tiled<0, 0> : (const void*)gemm_tiled<0, 1>)
+                          : (bt == 0 ? (const void*)gemm_tiled<1, 0> : (const void*)gemm_tiled<1, 1>);
+  l.set(f, dim3(cdiv(g.N, 32), cdiv(g.M, 64)), dim3(128), 0, g);
+  return l;
+}
+
 static void build_layerwise(pn_net* net) {
   auto& fwd = net->phase[0];
   auto& bwd = net->phase[1];
@@ -779,7 +797,7 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_IP) {
       GemmP p{x, net->params + L.off, top->data, L.bias ? net->params + L.off + L.wcount : nullptr,
               N, L.Nout, L.K, L.K, 1, 1, L.K, 0};
-      l.set((const void*)gemm_generic, dim3(cdiv(L.Nout, 64), cdiv(N, 64)), dim3(256), 0, p);
+      l = gemm_launch(p);
       add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().A = a.x; }
                                        : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_SOFTMAX) {
@@ -898,7 +916,7 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_IP) {
       // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
       GemmP w{top.diff, x, net->grads + L.off, nullptr, L.Nout, L.K, N, 1, L.Nout, L.K, 1, 0};
-      l.set((const void*)gemm_generic, dim3(cdiv(L.K, 64), cdiv(L.Nout, 64)), dim3(256), 0, w);
+      l = gemm_launch(w);
       add(bwd, L.name + ".wgrad", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().B = a.x; }
                                          : std::function<void(Launch&, const StepArgs&)>());
       if (L.bcount) {
@@ -910,7 +928,7 @@ static void build_layerwise(pn_net* net) {
       if (bot) {
         GemmP d{top.diff, net->params + L.off, bot->diff, nullptr, N, L.K, L.Nout, L.Nout, 1, L.K, 1, 0};
         Launch l3;
-        l3.set((const void*)gemm_generic, dim3(cdiv(L.K, 64), cdiv(N, 64)), dim3(256), 0, d);
+        l3 = gemm_launch(d);
         add(bwd, L.name + ".dgrad", l3);
       }
     } else if (L.type == L_SOFTMAX) {
@@ -1002,7 +1020,7 @@ static void build_fused_lenet(pn_net* net) {
   } else {
     GemmP g{p2.data, P + i1.off, a1.data, P + i1.off + i1.wcount, N, 500, 800, 800, 1, 1, 800, 1};
     Launch l;
-    l.set((const void*)gemm_generic, dim3(cdiv(500, 64), cdiv(N, 64)), dim3(256), 0, g);
+    l = gemm_launch(g);
     add(fwd, "ip1+relu", l);
   }
   {
@@ -1068,7 +1086,7 @@ static void build_fused_lenet(pn_net* net) {
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
     Launch l;
-    l.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(500, 64)), dim3(256), 0, w);
+    l = gemm_launch(w);
     add(bwd, "ip1.wgrad", l);
     ColSumP c{a1.diff, G + i1.off + i1.wcount, N, 500};
     Launch l2;
@@ -1077,7 +1095,7 @@ static void build_fused_lenet(pn_net* net) {
     add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
     GemmP d{a1.diff, P + i1.off, p2.diff, nullptr, N, 800, 500, 500, 1, 800, 1, 0};
     Launch l3;
-    l3.set((const void*)gemm_generic, dim3(cdiv(800, 64), cdiv(N, 64)), dim3(256), 0, d);
+    l3 = gemm_launch(d);
     add(bwd, "ip1.dgrad", l3);
     Unpool2P u{p2.diff, p2.m8, cv2.diff, N};
     Launch l4;
