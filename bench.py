@@ -507,6 +507,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the fp32-class sub-record")
     ap.add_argument("--fp32-steps", type=int, default=300)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="N > 1: bucketed NCCL allreduces + solver (default), or the fused exchange + solver "
+                         "kernel over NCCL symmetric windows (SURVEY 8(f) NEXT #1)")
     args = ap.parse_args()
     dflt = {"lenet": (20000, 200), "cifar10_quick": (2000, 50), "alexnet_conv": (40, 5),
             "alexnet_grouped": (40, 5)}[args.workload]
@@ -541,7 +544,7 @@ def main():
     params = synth.xavier_params(learn, seed=2, bias="zero")
     net.set_params(params)
     if world > 1:
-        dp_bootstrap(net, dist)   # library-owned NCCL communicator (id via the torch PG)
+        dp_bootstrap(net, dist, fused=args.exchange == "fused")   # library-owned NCCL communicator (id via the torch PG)
 
     # resident synthetic dataset (> L2), distinct per rank
     gen = {"lenet": synth.mnist_like_fast, "cifar10_quick": synth.cifar_like_fast,
@@ -702,7 +705,7 @@ def main():
         "data": "synthetic",
         "config": {"workload": WL["desc"],
                    "global_batch": BATCH * world, "per_gpu_batch": BATCH,
-                   "parallelism": f"dp{world}", "l2": f"inputs larger than L2: {NB} resident "
+                   "parallelism": f"dp{world}", "exchange": args.exchange if world > 1 else None, "l2": f"inputs larger than L2: {NB} resident "
                    f"batches ({NB * BATCH * img_floats * 4 / 1e6:.0f} MB) cycled",
                    "final_loss": final_loss},
         "e2e": e2e,

@@ -222,6 +222,20 @@ pn_status net_profile_stages(pn_net* net, const float* x,
 /* Number of kernels one net_train_step launches on the device. */
 pn_status net_launches_per_step(const pn_net* net, int* n);
 
+/* SURVEY §8(f) NEXT #1 (P:76 multi-GPU roadmap; P:94 / S:536-544 solver):
+ * fuse the gradient exchange with the solver.  Collective over the ranks of
+ * net_dp_init (every rank calls it, after net_dp_init).  The flat gradient,
+ * parameter and momentum buffers become NCCL symmetric windows (parameters
+ * and momentum are moved into ncclMemAlloc memory, values kept; pointers from
+ * net_blob_ptr taken before are stale) and the backward's bucket allreduces
+ * plus the solver are replaced by one kernel: an NVLink barrier, each rank
+ * reduces its shard of the gradients over the ranks (NVLS multimem
+ * ld_reduce, or peer loads in rank order when the team has no multicast
+ * object), applies SGD and stores the updated shard of w and the momentum to
+ * every rank, a second barrier.  PN_ERR_STATE without a communicator,
+ * PN_ERR_NCCL when NCCL refuses the windows or the device communicator. */
+pn_status net_dp_fused_exchange(pn_net* net);
+
 /* Dev-only: in-graph step timeline.  Only in a library built with
  * -DPN_STEPTRACE (else PN_ERR_STATE).  Synchronises the device; when
  * host_out is non-NULL copies the per-kernel record gathered since the last

@@ -21,7 +21,7 @@ EXPORTS = ["net_create", "net_destroy", "pn_last_error", "net_blob_count", "net_
            "net_param_count", "net_blob_ptr", "net_set_param", "net_get_blob", "net_put_blob",
            "net_forward", "net_backward", "sgd_update", "net_train_step", "net_train_step_host",
            "net_infer", "net_stage_count", "net_stage_name", "net_stage_mode", "net_run_stage", "net_profile_stages",
-           "net_launches_per_step", "net_steptrace", "net_sync_errors", "pn_nccl_unique_id", "net_dp_init",
+           "net_launches_per_step", "net_steptrace", "net_sync_errors", "pn_nccl_unique_id", "net_dp_init", "net_dp_fused_exchange",
            "net_set_input_transform", "net_train_step_u8", "net_train_steps_u8_host", "pn_idx_read",
            "pn_cifar_read", "pn_loopback_create", "pn_loopback_destroy", "net_dp_init_loopback"]
 
@@ -79,6 +79,7 @@ def lib():
             "net_sync_errors": [_vp, _vp],
             "pn_nccl_unique_id": [_vp],
             "net_dp_init": [_vp, _i, _i, _vp],
+            "net_dp_fused_exchange": [_vp],
             "net_set_input_transform": [_vp, ctypes.c_float, _vp, _i64],
             "net_train_step_u8": [_vp, _vp, _vp, ctypes.POINTER(pn_sgd), _i64, _vp, _vp],
             "net_train_steps_u8_host": [_vp, _vp, _vp, _i64, ctypes.POINTER(pn_sgd), _i64, _vp, _vp],

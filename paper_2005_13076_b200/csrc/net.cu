@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "../../include/pn.h"
+#include "dp_exchange.h"
 #include "kernels.h"
 #include "runtime.h"
 #include "tc.h"
@@ -293,6 +294,11 @@ struct pn_net {
   pn_loop* loop = nullptr;          // test-hook exchange (instead of comm)
   void* nccl_grads = nullptr;       // gradient buffer from ncclMemAlloc (registered with the communicator)
   void* nccl_reg = nullptr;         // ncclCommRegister handle
+  // the fused exchange + solver (net_dp_fused_exchange, dp_exchange.cu): parameters and
+  // momentum moved to ncclMemAlloc buffers, the three symmetric windows, the device communicator
+  DpxState* dpx = nullptr;
+  void* nccl_params = nullptr;
+  void* nccl_hist = nullptr;
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ip = nullptr, ev_conv = nullptr, ev_done = nullptr;
   // single-GPU step: a side stream for independent backward branches
@@ -1205,6 +1211,16 @@ static Stage solver_stage(pn_net* net, const std::string& name, bool ip, bool co
 }
 
 static void build_update(pn_net* net) {
+  if (net->dpx) {  // data parallel, fused: the exchange and the solver in one kernel (dp_exchange.cu)
+    add(net->phase[2], "exchange+solver[nvlink]", dpx_launch(net->dpx, net->params, net->hist, net->nparams),
+        [](Launch& l, const StepArgs& a) { dpx_patch(l, a.lr, a.mom, a.decay, a.gscale, a.lr_dev); });
+    if (net->fused && net->tf32) {  // the TF32 weight copies of the exchanged parameters
+      net->pack.w1 = net->params + net->layers[4].off;
+      net->pack.w2 = net->params + net->layers[2].off;
+      add(net->phase[2], "wpack[tc]", tc::pack_weights_launch(net->pack));
+    }
+    return;
+  }
   if (net->fused && net->tf32) {  // reduce (conv bucket) + SGD + the TF32 weight copies
     const bool dp = net->comm || net->loop;
     net->phase[2].push_back(solver_stage(net, "solver[tc]", true, true, nullptr));
@@ -1236,6 +1252,7 @@ __global__ void loopback_sum(const __grid_constant__ LoopSumP p) {
 
 static void add_dp_stages(pn_net* net) {
   if (!net->comm && !net->loop) return;  // (a 1-rank communicator still runs the full exchange path)
+  if (net->dpx) return;                  // the fused exchange runs in the solver's place (build_update)
   auto& bwd = net->phase[1];
   // position: after the last stage producing a gradient of the ip bucket
   // (the inner-product layers' parameters, which lead the flat buffer):
@@ -1583,8 +1600,11 @@ extern "C" void net_destroy(pn_net* net) {
   cudaDeviceSynchronize();
   drop_graphs(net);
   if (net->cap) cudaStreamDestroy(net->cap);
+  if (net->dpx) dpx_destroy(net->dpx);
   if (net->comm && net->nccl_reg) ncclCommDeregister(net->comm, net->nccl_reg);
   if (net->nccl_grads) ncclMemFree(net->nccl_grads);
+  if (net->nccl_params) ncclMemFree(net->nccl_params);
+  if (net->nccl_hist) ncclMemFree(net->nccl_hist);
   if (net->comm) ncclCommDestroy(net->comm);
   if (net->comm_stream) cudaStreamDestroy(net->comm_stream);
   for (cudaEvent_t e : {net->ev_ip, net->ev_conv, net->ev_done, net->ev_fork, net->ev_join, net->ev_ipd})
@@ -2242,6 +2262,39 @@ static void repoint_diffs(pn_net* net) {
     if (wi >= 0) net->blobs[wi].diff = net->grads + L.off;
     if (bi >= 0) net->blobs[bi].diff = net->grads + L.off + L.wcount;
   }
+}
+
+// NEXT #1: the exchange and the solver fused into one kernel
+// over NCCL symmetric windows (dp_exchange.cu).  Collective: every rank calls
+// it after net_dp_init.  Parameters and momentum move into ncclMemAlloc
+// buffers (their contents kept), the plan is rebuilt.
+extern "C" pn_status net_dp_fused_exchange(pn_net* net) {
+  CHECK_NET(net);
+  if (!net->comm) return fail(PN_ERR_STATE, "net_dp_fused_exchange needs net_dp_init (an NCCL communicator)");
+  if (net->dpx) return PN_OK;
+  CU(cudaSetDevice(net->device));
+  CU(cudaDeviceSynchronize());
+  const size_t bytes = (size_t)net->nparams * 4;
+  void *P = nullptr, *V = nullptr;
+  NC(ncclMemAlloc(&P, bytes));
+  NC(ncclMemAlloc(&V, bytes));
+  CU(cudaMemcpy(P, net->params, bytes, cudaMemcpyDeviceToDevice));
+  CU(cudaMemcpy(V, net->hist, bytes, cudaMemcpyDeviceToDevice));
+  net->nccl_params = P, net->nccl_hist = V;
+  net->params = (float*)P, net->hist = (float*)V;
+  for (auto& L : net->layers) {
+    if (L.off < 0) continue;
+    int wi = net->blob(L.name + ".w"), bi = net->blob(L.name + ".b");
+    if (wi >= 0) net->blobs[wi].data = net->params + L.off, net->blobs[wi].hist = net->hist + L.off;
+    if (bi >= 0) net->blobs[bi].data = net->params + L.off + L.wcount, net->blobs[bi].hist = net->hist + L.off + L.wcount;
+  }
+  std::string err;
+  if (dpx_setup(net->comm, net->grads, net->params, net->hist, net->nparams, net->tc_sms, &net->dpx, &err) != PN_OK)
+    return fail(PN_ERR_NCCL, err);
+  net->pack_dirty = true;
+  drop_graphs(net);
+  TRY(build_plan(net));
+  return PN_OK;
 }
 
 extern "C" pn_status net_dp_init(pn_net* net, int nranks, int rank, const void* id128) {

@@ -16,7 +16,7 @@ def shard_rows(global_batch, world, rank):
     return rank * b, (rank + 1) * b
 
 
-def dp_bootstrap(net, dist):
+def dp_bootstrap(net, dist, fused=False):
     """Rank 0 asks the library for an NCCL unique id, broadcasts its 128 bytes
     over the process group; every rank then joins the library communicator
     (net_dp_init).  Returns (world, rank)."""
@@ -28,6 +28,8 @@ def dp_bootstrap(net, dist):
         uid.copy_(torch.frombuffer(bytearray(net.pn_nccl_unique_id()), dtype=torch.uint8))
     dist.broadcast(uid, 0)
     net.net_dp_init(world, rank, bytes(uid.cpu().numpy().tobytes()))
+    if fused:  # NEXT #1: exchange + solver fused over NCCL symmetric windows
+        net.net_dp_fused_exchange()
     return world, rank
 
 

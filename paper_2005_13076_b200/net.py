@@ -260,6 +260,11 @@ class Net:
         buf = (ctypes.c_ubyte * 128).from_buffer_copy(uid)
         check(lib().net_dp_init(self._h, nranks, rank, buf))
 
+    def net_dp_fused_exchange(self):
+        """NEXT #1: the exchange + solver as one kernel over NCCL symmetric
+        windows (collective; after net_dp_init)."""
+        check(lib().net_dp_fused_exchange(self._h))
+
     def net_dp_init_loopback(self, group, rank):
         """Test hook (include/pn.h): join a LoopbackGroup as `rank`."""
         check(lib().net_dp_init_loopback(self._h, group.handle, rank))

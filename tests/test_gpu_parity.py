@@ -413,6 +413,33 @@ def test_dp_single_rank_communicator_matches_local_step(tf32):
         assert_bitwise("dp(1) vs local", a, b)
 
 
+@pytest.mark.parametrize("tf32,layerwise", [(False, False), (True, False), (True, True)])
+def test_dp_fused_exchange_single_rank_matches_local_step(tf32, layerwise):
+    """SURVEY §8(f) NEXT #1 on a 1-rank communicator: the exchange + solver
+    kernel over NCCL symmetric windows (one LSA peer: the rank-order peer sum
+    of one gradient, then SGD and the stores to every rank's window) replaces
+    the allreduces and the solver and reproduces the local step bitwise, over
+    several steps (the parameters and momentum it stores feed the next one)."""
+    N = 64
+    sgd = make_sgd()
+    res = []
+    for dp in (False, True):
+        net, ref, params, x, y = make("lenet", N, tf32, layerwise)
+        if dp:
+            net.net_dp_init(1, 0, Net.pn_nccl_unique_id())
+            net.net_dp_fused_exchange()
+            assert "exchange+solver[nvlink]" in net.stages(2)
+            assert not any(s.startswith("allreduce") for s in net.stages(1))
+        xd, yd = cuda(x), cuda(y)
+        for it in range(3):
+            net.net_train_step(xd, yd, sgd, it)
+        net.net_sync_errors()
+        res.append([host(net.net_get_blob(k)) for k in params] + [host(net.net_get_blob(k, PN_HISTORY)) for k in params])
+        net.close()
+    for a, b in zip(*res):
+        assert_bitwise("fused exchange dp(1) vs local", a, b)
+
+
 @pytest.mark.parametrize("spec,N,tf32", [("lenet", 64, True), ("lenet", 64, False), ("cifar10_quick", 8, True)])
 def test_dp_bucket_allreduce_follows_its_gradients(spec, N, tf32):
     """The ip-bucket allreduce is placed after every stage that writes an
