@@ -52,14 +52,21 @@ __device__ __forceinline__ void tmem_alloc(uint32_t* dst, uint32_t ncols) {
 __device__ __forceinline__ void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// The accumulate flag as an immediate operand: a predicate register set just
+// before the MMA costs the single issuing thread 16-70 extra cycles per MMA
+// (tools/mma_rate.cu: 45 cycles at small N with an immediate, 61 with a
+// predicate, 115 with one computed in a rolled loop); a uniform branch on the
+// flag folds away where it is a compile-time constant (unrolled loops).
 __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
+  if (accumulate)
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;" ::"r"(d_tmem), "l"(adesc), "l"(bdesc),
+                 "r"(idesc)
+                 : "memory");
+  else
+    asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 0;" ::"r"(d_tmem), "l"(adesc), "l"(bdesc),
+                 "r"(idesc)
+                 : "memory");
 }
 // the same with a compile-time accumulate flag (no predicate setup per MMA:
 // single-thread issue is ~45 cycles per small-N MMA at best, tools/mma_rate.cu)

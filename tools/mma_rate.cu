@@ -55,6 +55,24 @@ __global__ void bench(int kind, int N, int sw, int reps, unsigned long long* out
                            "l"(a0 + (uint64_t)(((i * 24 + j) * 16 + ks * 2 * 4608) >> 4)),
                            "l"(b0 + (uint64_t)(((i * 5 + j) * 4000 + ks * 1600) >> 4)), "r"(idesc));
       }
+    } else if (kind == 5) {  // unrolled x16 with a runtime predicate (setp per MMA)
+      for (int r = 0; r < reps; r += 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(tb),
+                       "l"(ad + 2 * u), "l"(bd + 2 * u), "r"(idesc), "r"(r | u));
+      }
+    } else if (kind == 6) {  // not unrolled, constant accumulate
+      for (int r = 0; r < reps; ++r)
+        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;" ::"r"(tb), "l"(ad + 2 * (r & 3)), "l"(bd + 2 * (r & 3)),
+                     "r"(idesc));
+    } else if (kind == 4) {  // A in tensor memory (columns 128.. of the allocation), unrolled x16, tf32
+      for (int r = 0; r < reps; r += 16) {
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, 1;" ::"r"(tb), "r"(tb + 128 + 8 * (u & 7)),
+                       "l"(bd + 2 * u), "r"(idesc));
+      }
     } else if (kind >= 2) {  // unrolled x16, accumulate, tf32
       for (int r = 0; r < reps; r += 16) {
 #pragma unroll
@@ -85,13 +103,13 @@ int main() {
   cudaMalloc(&d, 8);
   cudaFuncSetAttribute(bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   const int reps = 1500;
-  for (int kind = 0; kind < 4; ++kind)
-    for (int sw = 0; sw < 2; ++sw)
-      for (int N : {32, 64, 128, 256}) {
+  for (int kind = 0; kind < 7; ++kind)
+    for (int sw = 1; sw < 2; ++sw)
+      for (int N : {32, 64, 128, 192}) {
         bench<<<1, 128, 200 * 1024>>>(kind, N, sw, reps, d);
         unsigned long long c;
         cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
-        printf("%s %-6s M=128 N=%3d K=%2d: %6.1f cycles/MMA  (%s)\n", kind == 1 ? "f16 " : kind == 2 ? "tf32u" : kind == 3 ? "conv2" : "tf32", sw ? "sw128" : "noswz", N,
+        printf("%s %-6s M=128 N=%3d K=%2d: %6.1f cycles/MMA  (%s)\n", kind == 1 ? "f16 " : kind == 2 ? "tf32u" : kind == 3 ? "conv2" : kind == 4 ? "tf32ts" : kind == 5 ? "tf32p" : kind == 6 ? "tf32l" : "tf32", sw ? "sw128" : "noswz", N,
                kind == 1 ? 16 : 8, (double)c / reps, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
