@@ -184,6 +184,167 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
   ST_END(stk);
 }
 
+// ---------------------------------------------------------------- stem
+// The cifar10_quick stem (conv1 -> MAX pool1 -> in-place ReLU; Caffe
+// pooling R4/R5) fused: the conv output never reaches HBM.
+// Forward: block = (image n, 8 filters): the zero-padded image in shared
+// memory, the 8 filters' conv plane computed there (thread = 4 adjacent
+// outputs x 8 filters, fp32 FMAs in ascending (c, i, j)), + bias (one fp32
+// add, as the conv epilogue), then the pooled max over each window in
+// row-major scan order (strict >: the first maximum) with its origin, and
+// the ReLU: y = max(best, 0).
+constexpr int STEM_FG = STEM_FG_HOST;
+__global__ void __launch_bounds__(256) stem_fwd(const __grid_constant__ StemP p) {
+  pdl_enter();
+  extern __shared__ __align__(16) float sm[];
+  const int n = blockIdx.y, f0 = blockIdx.x * STEM_FG, tid = threadIdx.x;
+  const int Hpad = p.H + 2 * p.ph, Wpad = p.W + 2 * p.pw, K = p.C * p.kh * p.kw;
+  const int Wq = (p.Wo + 3) & ~3;                 // conv plane row pitch (4-output strips)
+  float* xs = sm;                                 // [C][Hpad][Wpad + 8]
+  const int xpitch = Wpad + 8;
+  float* ws = xs + p.C * Hpad * xpitch;           // [K][8 filters]
+  float* cs = ws + K * STEM_FG;                   // [8][Ho][Wq]
+  for (int i = tid; i < p.C * Hpad * xpitch; i += 256) {
+    const int c = i / (Hpad * xpitch), r = i - c * Hpad * xpitch, h = r / xpitch - p.ph, w = r % xpitch - p.pw;
+    xs[i] = (h >= 0 && h < p.H && w >= 0 && w < p.W) ? __ldg(p.x + (((size_t)n * p.C + c) * p.H + h) * p.W + w) : 0.f;
+  }
+  for (int i = tid; i < K * STEM_FG; i += 256) {
+    const int k = i / STEM_FG, f = f0 + i % STEM_FG;
+    ws[i] = f < p.F ? __ldg(p.w + (size_t)f * K + k) : 0.f;
+  }
+  __syncthreads();
+  const int strips = p.Ho * (Wq / 4);
+  for (int s = tid; s < strips; s += 256) {
+    const int h = s / (Wq / 4), w0 = (s % (Wq / 4)) * 4;
+    float acc[4][STEM_FG];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+      for (int f = 0; f < STEM_FG; ++f) acc[q][f] = 0.f;
+    for (int c = 0; c < p.C; ++c)
+#pragma unroll 1
+      for (int i = 0; i < 5; ++i) {  // (the stem's kernel is 5 x 5: net.cu checks)
+        const float* xr = xs + (c * Hpad + h + i) * xpitch + w0;
+        float xv[8];  // the 4 outputs' row segment: w0 .. w0 + 3 + (kw - 1)
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = xr[u];
+        const float* wr = ws + ((c * 5 + i) * 5) * STEM_FG;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          const float4 wa = *reinterpret_cast<const float4*>(wr + j * STEM_FG);
+          const float4 wb = *reinterpret_cast<const float4*>(wr + j * STEM_FG + 4);
+          const float wv[8] = {wa.x, wa.y, wa.z, wa.w, wb.x, wb.y, wb.z, wb.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int f = 0; f < STEM_FG; ++f) acc[q][f] = fmaf(wv[f], xv[q + j], acc[q][f]);
+        }
+      }
+#pragma unroll
+    for (int f = 0; f < STEM_FG; ++f) {
+      const float bb = (p.b && f0 + f < p.F) ? __ldg(p.b + f0 + f) : 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (w0 + q < p.Wo) cs[(f * p.Ho + h) * Wq + w0 + q] = p.b ? acc[q][f] + bb : acc[q][f];
+    }
+  }
+  __syncthreads();
+  const int HWp = p.Hp * p.Wp;
+  for (int e = tid; e < STEM_FG * HWp; e += 256) {
+    const int f = e / HWp, r = e - f * HWp;
+    if (f0 + f >= p.F) continue;
+    const int a = r / p.Wp, bq = r - a * p.Wp;
+    int hs = a * p.ps - p.pp, wst = bq * p.ps - p.pp;
+    int he = min(hs + p.pk, p.Ho + p.pp), we = min(wst + p.pk, p.Wo + p.pp);
+    hs = max(hs, 0);
+    wst = max(wst, 0);
+    he = min(he, p.Ho);
+    we = min(we, p.Wo);
+    const float* cp = cs + f * p.Ho * Wq;
+    float best = cp[hs * Wq + wst];
+    int arg = hs * p.Wo + wst;
+    for (int h = hs; h < he; ++h)
+      for (int w = wst; w < we; ++w) {
+        const float v = cp[h * Wq + w];
+        if (v > best) {
+          best = v;
+          arg = h * p.Wo + w;
+        }
+      }
+    const size_t idx = ((size_t)n * p.F + f0 + f) * HWp + r;
+    p.y[idx] = p.relu ? fmaxf(best, 0.f) : best;
+    p.mask[idx] = arg;
+  }
+}
+
+// Weight gradient of the stem: dW[f,c,i,j] = sum_n sum_q g[n,f,q] x[n,c,
+// h_q+i-ph, w_q+j-pw] with (h_q, w_q) the conv position pool q routed its
+// gradient to (P:220-222 composed with the conv weight gradient; no
+// conv-output gradient is formed: overlapping windows that pick the same
+// position just add), db[f] = sum g.  g = dy: the ReLU's backward was applied
+// by its consumer (the next conv's data gradient).  grid = (filter groups of
+// 8, image splits); thread = (filter, lane): the lane's pooled positions,
+// its 75 (C kh kw) accumulators in registers; the split's images staged one
+// at a time (zero-padded); lanes combined by shuffles; one partial per split.
+constexpr int STEM_KMAX = kStemKmax;
+__global__ void __launch_bounds__(256) stem_wgrad(const __grid_constant__ StemP p) {
+  pdl_enter();
+  extern __shared__ __align__(16) float sm[];
+  const int s = blockIdx.y, f = blockIdx.x * STEM_FG + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
+  const int Hpad = p.H + 2 * p.ph, Wpad = p.W + 2 * p.pw, HWp = p.Hp * p.Wp;
+  const bool live = f < p.F;
+  float acc[STEM_KMAX], bacc = 0.f;
+#pragma unroll
+  for (int k = 0; k < STEM_KMAX; ++k) acc[k] = 0.f;
+  constexpr int QMAX = 8;  // pooled positions per lane and image (Hp Wp <= 256: net.cu checks)
+  for (int n = n0; n < n1; ++n) {
+    // this image's (gradient, origin) pairs of the lane, loads in flight with the staging
+    const size_t base = ((size_t)n * p.F + (live ? f : 0)) * HWp;
+    float gq[QMAX];
+    int oq[QMAX];
+#pragma unroll
+    for (int t = 0; t < QMAX; ++t) {
+      const int q = lane + 32 * t;
+      gq[t] = (live && q < HWp) ? __ldg(p.dy + base + q) : 0.f;
+      oq[t] = (live && q < HWp) ? __ldg(p.mask + base + q) : 0;
+    }
+    __syncthreads();  // the previous image's reads are done
+    for (int i = threadIdx.x; i < p.C * Hpad * Wpad; i += 256) {
+      const int c = i / (Hpad * Wpad), r = i - c * Hpad * Wpad, h = r / Wpad - p.ph, w = r % Wpad - p.pw;
+      sm[i] = (h >= 0 && h < p.H && w >= 0 && w < p.W) ? __ldg(p.x + (((size_t)n * p.C + c) * p.H + h) * p.W + w) : 0.f;
+    }
+    __syncthreads();
+    if (!live) continue;
+#pragma unroll
+    for (int t = 0; t < QMAX; ++t) {
+      if (lane + 32 * t >= HWp) break;
+      const float g = gq[t];
+      const int o = oq[t], h = o / p.Wo, w = o - h * p.Wo;
+      bacc += g;
+      const float* xp = sm + h * Wpad + w;  // conv output (h, w) reads padded rows h..h+kh-1
+#pragma unroll
+      for (int k = 0; k < STEM_KMAX; ++k) {
+        const int c = k / 25, i = (k / 5) % 5, j = k % 5;  // (C kh kw = 3 x 5 x 5)
+        acc[k] = fmaf(g, xp[(c * Hpad + i) * Wpad + j], acc[k]);
+      }
+    }
+  }
+  if (!live) return;
+#pragma unroll
+  for (int k = 0; k < STEM_KMAX; ++k)
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], m);
+#pragma unroll
+  for (int m = 16; m > 0; m >>= 1) bacc += __shfl_xor_sync(0xffffffffu, bacc, m);
+  if (lane == 0) {
+    float* out = p.part_w + (size_t)s * p.pstride;
+#pragma unroll
+    for (int k = 0; k < STEM_KMAX; ++k) out[f * STEM_KMAX + k] = acc[k];
+    if (p.b) out[p.F * STEM_KMAX + f] = bacc;
+  }
+}
+
 // ------------------------------------------------------------------ pooling
 // P:215-220; Caffe window (R4-R6).  MAX keeps the first maximum of
 // a row-major scan (strict >) and stores its plane-local index h*W+w.

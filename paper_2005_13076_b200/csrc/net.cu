@@ -84,6 +84,7 @@ struct Layer {
   // materialised TF32 operands (plan tp, weight copy Wf [F][kp]); data
   // gradient as an implicit GEMM over gathered G (swizzled W' image bdg)
   bool tc_conv = false, tc_dgrad = false, tma_fwd = false;
+  bool stem = false;  // layerwise TF32 plan: conv -> MAX pool -> in-place ReLU fused (stem_fwd / stem_wgrad)
   bool tap_fwd = false, tap_dgrad = false;  // stride-1 tap GEMM over NHWC (tc_conv.cu)
   int cp_in = 0, cp_out = 0;                // NHWC channel pitches of x and of G
   float* wtap_f = nullptr;                  // [T][F][cp_in]
@@ -553,6 +554,8 @@ static pn_status allocate(pn_net* net) {
       L.splits = std::max(1, std::min(net->batch, WG2_SPLITS > 0 ? WG2_SPLITS : net->tc_sms / 4));
     if (net->fused && !net->tf32 && &L == &net->layers[2])  // fp32 SIMT conv2 weight gradient: one block per SM
       L.splits = std::max(1, std::min(net->batch, net->tc_sms));
+    if (L.stem)  // two blocks per SM over (filter groups of 8) x image splits
+      L.splits = std::max(1, std::min(net->batch, 2 * net->tc_sms / ((L.F + STEM_FG_HOST - 1) / STEM_FG_HOST)));
     if (L.tc_conv) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
                                 net->tc_sms, L.G);
@@ -606,10 +609,11 @@ static pn_status allocate(pn_net* net) {
     skip_data1 = net->layers[0].top;
     skip_data2 = net->layers[2].top;
   }
+  if (net->layers[0].stem) skip_data1 = net->layers[0].top;  // the stem's conv output stays on chip
   for (auto& b : net->blobs) {
     if (b.is_param || b.is_input) continue;
     int64_t n = b.count();
-    if (b.name == skip_data1) { b.materialised = false; continue; }
+    if (b.name == skip_data1) { b.materialised = false; continue; }  // (no data, no gradient)
     if (b.name == skip_data2) b.materialised = false;
     else TRY(net->alloc(&b.data, n));
     TRY(net->alloc(&b.diff, n));
@@ -691,6 +695,48 @@ static void add_loss(pn_net* net, std::vector<Stage>& fwd) {
   add(fwd, "loss_reduce", l, [](Launch& l, const StepArgs& a) { l.params<LossReduceP>().loss_out = a.loss; });
 }
 
+// The layerwise TF32 plan's stem: a first convolution on the data input
+// (stride 1, 3 x 5 x 5 filters), read only by a MAX pooling layer whose output
+// an in-place ReLU (slope 0) follows -- cifar10_quick's conv1 -> pool1 ->
+// relu1.  Fused by stem_fwd (the conv plane stays in shared memory)
+// and stem_wgrad (the weight gradient straight from the pooled gradient and
+// origins).
+static bool is_stem(const pn_net* net) {
+  if (!net->tf32 || net->layers.size() < 3) return false;
+  const Layer &C = net->layers[0], &P = net->layers[1], &R = net->layers[2];
+  if (C.type != L_CONV || C.bottom != net->input_name || C.G != 1 || C.in[1] != 3 || C.kh != 5 || C.kw != 5 ||
+      C.sh != 1 || C.sw != 1 || C.top == C.bottom)
+    return false;
+  if (P.type != L_POOL || P.method != 0 || P.bottom != C.top || P.top == C.top || P.kh != P.kw || P.sh != P.sw ||
+      P.ph != P.pw)
+    return false;
+  if (R.type != L_RELU || R.bottom != P.top || R.top != P.top || R.slope != 0.f) return false;
+  if (P.out[2] * P.out[3] > 256 || C.out[3] > 64) return false;  // stem_wgrad: <= 8 pooled positions per lane
+  for (size_t i = 2; i < net->layers.size(); ++i)
+    if (net->layers[i].bottom == C.top) return false;
+  for (const Layer& A : net->acc_layers)
+    if (A.bottom == C.top) return false;
+  return true;
+}
+static size_t stem_fwd_smem(const Layer& C) {
+  const int Hpad = C.in[2] + 2 * C.ph, Wpad = C.in[3] + 2 * C.pw, Wq = (C.out[3] + 3) & ~3;
+  return (size_t)(C.in[1] * Hpad * (Wpad + 8) + C.in[1] * C.kh * C.kw * STEM_FG_HOST + STEM_FG_HOST * C.out[2] * Wq) * 4;
+}
+static StemP stem_params(pn_net* net) {
+  const Layer &C = net->layers[0], &P = net->layers[1];
+  Blob& y = net->blobs[net->blob(P.top)];
+  StemP s{};
+  s.w = net->params + C.off;
+  s.b = C.bias ? net->params + C.off + C.wcount : nullptr;
+  s.y = y.data, s.mask = y.m32, s.dy = y.diff;
+  s.part_w = net->partials + C.part_off;
+  s.N = net->batch, s.C = C.in[1], s.H = C.in[2], s.W = C.in[3], s.F = C.F, s.kh = C.kh, s.kw = C.kw;
+  s.ph = C.ph, s.pw = C.pw, s.Ho = C.out[2], s.Wo = C.out[3];
+  s.pk = P.kh, s.ps = P.sh, s.pp = P.ph, s.Hp = P.out[2], s.Wp = P.out[3];
+  s.splits = C.splits, s.pstride = (int)(C.wcount + C.bcount), s.relu = 1;
+  return s;
+}
+
 // C = A B on the register-tiled fp32 GEMM when the operand layouts allow
 // float4 loads (a unit stride on K or on M / N, the other a multiple of 4,
 // 16-B aligned bases), else the generic strided kernel
@@ -722,6 +768,7 @@ static void build_layerwise(pn_net* net) {
     if (L.type == L_CONV && L.tc_conv && R.type == L_RELU && R.bottom == L.top && R.top == L.top && R.slope == 0.f)
       relu_in_conv[li + 1] = true;
   }
+  const bool stem = net->layers[0].stem;
   for (size_t li = 0; li < net->layers.size(); ++li) {
     Layer& L = net->layers[li];
     bool isx = false;
@@ -729,6 +776,14 @@ static void build_layerwise(pn_net* net) {
     Blob* top = L.type == L_LOSS ? nullptr : &net->blobs[net->blob(L.top)];
     Launch l;
     if (relu_in_conv[li]) continue;
+    if (stem && li <= 2) {  // conv -> MAX pool -> ReLU in one kernel (is_stem)
+      if (li == 0) {
+        l.set((const void*)stem_fwd, dim3(cdiv(L.F, STEM_FG_HOST), N), dim3(256), stem_fwd_smem(L), stem_params(net));
+        add(fwd, L.name + "+" + net->layers[1].name + "+" + net->layers[2].name + ".fwd", l,
+            [](Launch& l, const StepArgs& a) { l.params<StemP>().x = a.x; });
+      }
+      continue;
+    }
     if (L.type == L_CONV && L.tc_conv) {
       // im2col + GEMM, engine chosen at net_create:
       // stride-1 tap GEMM over NHWC, materialised TF32 column matrix col
@@ -843,6 +898,16 @@ static void build_layerwise(pn_net* net) {
     const float* x = in_data(net, L, &isx);
     if (L.type == L_LOSS) continue;  // gradient produced with the forward
     if (relu_bwd_fused[li]) continue;
+    if (stem && li <= 2) {  // the stem's backward: its weight gradient from the pooled gradient (is_stem)
+      if (li == 0) {
+        Launch l;
+        l.set((const void*)stem_wgrad, dim3(cdiv(L.F, STEM_FG_HOST), L.splits), dim3(256),
+              (size_t)L.in[1] * (L.in[2] + 2 * L.ph) * (L.in[3] + 2 * L.pw) * 4, stem_params(net));
+        add(bwd, L.name + ".wgrad", l, [](Launch& l, const StepArgs& a) { l.params<StemP>().x = a.x; });
+        add_reduce(net, bwd, L);
+      }
+      continue;
+    }
     const float* relu_y = (li > 0 && relu_bwd_fused[li - 1]) ? net->blobs[net->blob(L.bottom)].data : nullptr;
     Blob& top = net->blobs[net->blob(L.top)];
     Blob* bot = isx ? nullptr : &net->blobs[net->blob(L.bottom)];
@@ -1536,8 +1601,9 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     // layerwise TF32 plan: every convolution on the general tcgen05 kernels
     // (tc_conv.cu); the data gradient needs stride 1 and pad < kernel (else
     // the generic fp32 kernel computes it)
+    net->layers[0].stem = is_stem(net.get()) && !getenv("PN_NO_STEM");
     for (auto& L : net->layers) {
-      if (L.type != L_CONV) continue;
+      if (L.type != L_CONV || L.stem) continue;
       const int Cg = L.in[1] / L.G, Fg = L.F / L.G;
       // grouped layers run on the tap GEMM only: stride 1,
       // >= 16 channels per group (else the generic fp32 kernels)
@@ -1567,6 +1633,8 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     }
   }
   TRY(allocate(net.get()));
+  if (net->layers[0].stem) CU(cudaFuncSetAttribute((const void*)stem_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   stem_fwd_smem(net->layers[0])));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (50 * 20 * 28 + 2 * 2880) * 4));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_dgrad_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -58,6 +58,20 @@ struct SolverP {
   int nplain;
 };
 
+// The layerwise plans' stem: conv (stride 1, the data input) -> MAX pool ->
+// in-place ReLU fused (kernels_generic.cu stem_fwd / stem_wgrad)
+struct StemP {
+  const float* x;      // [N][C][H][W]
+  const float* w;      // [F][C][kh][kw]
+  const float* b;      // [F] or nullptr
+  float* y;            // pooled, ReLU'd output [N][F][Hp][Wp]
+  int32_t* mask;       // pool origins (plane-local h*Wo + w of the conv output)
+  const float* dy;     // gradient w.r.t. y (ReLU already back-propagated by its consumer)
+  float* part_w;       // [splits][pstride] weight-gradient partials (+ bias at F*C*kh*kw)
+  int N, C, H, W, F, kh, kw, ph, pw, Ho, Wo;
+  int pk, ps, pp, Hp, Wp;  // pool kernel, stride, pad (square), output
+  int splits, pstride, relu;
+};
 struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   const float* x;
   float* y;

@@ -13,8 +13,9 @@ import pytest
 import torch
 
 from oracle.net import OracleNet
-from paper_2005_13076_b200 import PN_DIFF, Net, spec_text, synth
-from parity import RTOL, assert_close, assert_norm, report
+from paper_2005_13076_b200 import PN_DIFF, PN_MASK, Net, spec_text, synth
+from oracle import capi
+from parity import RTOL, assert_close, assert_norm, check_mask, report
 from test_gpu_parity import check_net_level
 
 pytestmark = pytest.mark.gpu
@@ -113,6 +114,10 @@ def test_conv_tc_teacher_forced(case):
     assert convs
     for L in convs:
         name = L["name"]
+        stem = [st for st in fwd if st.startswith(name + "+")]
+        if stem:  # conv -> MAX pool -> ReLU fused (net.cu is_stem): checked as one unit
+            check_stem(net, ref, out, gref, L, stem[0], xd, yd)
+            continue
         fst = [st for st in fwd if st.startswith(name + ".fwd")]
         on_tc = fst and fst[0].endswith("[tc]")
         # grouped layers the tensor-core engines do not cover (strided) run generic fp32
@@ -154,6 +159,32 @@ def test_conv_tc_teacher_forced(case):
             assert_close(f"{name} dgrad", host(net.net_get_blob(L["bottom"], PN_DIFF)), want,
                          gs[name + ".dx"], rtol)
     net.close()
+
+
+def check_stem(net, ref, out, gref, L, stage, xd, yd):
+    """The layerwise plan's stem (cifar10_quick conv1 -> pool1 -> relu1, one
+    fp32 kernel each way): the pooled, ReLU'd output against the oracle's relu1
+    output per element (scale: the conv's |terms| through the max), the pool
+    origins bit-exact up to listed near-ties, and the weight / bias gradients
+    from the oracle's pooled gradient and origins."""
+    P = [M for M in ref.layers if M["bottom"] == L["top"]][0]
+    R = [M for M in ref.layers if M["type"] == "ReLU" and M["bottom"] == P["top"]][0]
+    run_stage(net, 0, stage, xd, yd)
+    S = out["scales"][L["name"]]
+    Sp = capi.pool_fwd(S, capi.MAX, P["k"], P["s"], P["p"])[0]  # the largest conv scale of each window
+    assert_close(f"{stage}", host(net.net_get_blob(P["top"])), out["blobs"][R["name"]], Sp, RTOL[False])
+    check_mask(f"{stage} mask", host(net.net_get_blob(P["top"], PN_MASK)), out["masks"][P["name"]],
+               out["blobs"][L["name"]], S, tuple(L["out_shape"][2:]), P["k"][0], P["s"][0], P["p"][0], RTOL[False])
+    net.net_put_blob(P["top"], gref["diffs"][R["name"]].astype(np.float32), PN_DIFF)
+    net.net_put_blob(P["top"], out["masks"][P["name"]], PN_MASK)
+    for st in net.stages(1):
+        if st.startswith(L["name"] + ".wgrad"):
+            run_stage(net, 1, st, xd, yd)
+    gs = gref["scales"]
+    assert_close(f"{L['name']}.w grad (stem)", host(net.net_get_blob(L["name"] + ".w", PN_DIFF)),
+                 gref["grads"][L["name"] + ".w"], gs[L["name"] + ".w"], RTOL[False])
+    assert_close(f"{L['name']}.b grad (stem)", host(net.net_get_blob(L["name"] + ".b", PN_DIFF)).ravel(),
+                 gref["grads"][L["name"] + ".b"], gs[L["name"] + ".b"], RTOL[False])
 
 
 def bottom_layer(ref, L):
