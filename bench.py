@@ -130,6 +130,10 @@ def stage_work(name, N):
         # conv partials it sums are this implementation's, not the method's)
         "solver": (0, 431080 * 4 * 5),
         "reduce+solver": (0, 431080 * 4 * 5),
+        "ip.solver": (0, 405510 * 4 * 5),       # the ip layers' parameters (side branch)
+        "exchange+solver": (0, 431080 * 4 * 5),  # NEXT #1 (data parallel, fused): its local traffic
+        # conv1's weight gradient + the conv bucket's solver tail (25,570 parameters)
+        "conv1.wgrad+solver": (2 * 144 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1 + 25570 * 4 * 5),
     }
     base = name.split("[")[0]
     if base.endswith(".wgrad_reduce"):

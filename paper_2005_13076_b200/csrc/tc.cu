@@ -95,11 +95,11 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ float ld_cluster(uint32_t local_addr, uint32_t rank) {
+__device__ __forceinline__ float4 ld_cluster4(uint32_t local_addr, uint32_t rank) {
   uint32_t a;
   asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(local_addr), "r"(rank));
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
 }
 }  // namespace ipk
@@ -107,7 +107,7 @@ __device__ __forceinline__ float ld_cluster(uint32_t local_addr, uint32_t rank) 
 template <class Op>
 __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant__ typename Op::Params prm) {
   using namespace ipk;
-  constexpr int BN = Op::BN, CPB = BN + 1;  // tile width, C pitch (floats)
+  constexpr int BN = Op::BN, CPB = BN + 4;  // tile width, C pitch (floats; rows 16-B aligned)
   constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES, STAGES = Op::STAGES;
   static_assert(128 * CPB * 4 <= STAGES * STAGE, "C fits the ring");
   static_assert(BN == 32 || BN == 64 || BN == 128, "tile width");
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
         for (int j = 0; j < 32; ++j) v[j] = 0.f;
       }
 #pragma unroll
-      for (int j = 0; j < 32; ++j) stsf(sbase + 4 * (row * CPB + c0 + j), v[j]);
+      for (int j = 0; j < 32; j += 4) sts128(sbase + 4 * (row * CPB + c0 + j), f4(v[j], v[j + 1], v[j + 2], v[j + 3]));
     }
   }
   tc_fence_before();
@@ -204,17 +204,18 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
     cluster_sync();  // every partial tile of the cluster complete
     if (tid == 0) stamp(3);
     // rows [ROWS rank, +ROWS): the SPLIT partials summed in rank order, in
-    // place in the local C (no other CTA reads this CTA's own rows)
-    for (int u = tid; u < ROWS * BN; u += THREADS) {
-      const int r = ROWS * (int)rank + u / BN, col = u % BN;
+    // place in the local C (no other CTA reads this CTA's own rows); float4
+    // DSMEM loads, every source of an item in flight together
+    for (int u = tid; u < ROWS * BN / 4; u += THREADS) {
+      const int r = ROWS * (int)rank + u / (BN / 4), col = 4 * (u % (BN / 4));
       const uint32_t addr = sbase + 4 * (r * CPB + col);
-      float t[SPLIT];
+      float4 t[SPLIT];
 #pragma unroll
-      for (int q = 0; q < SPLIT; ++q) t[q] = q == (int)rank ? ldsf(addr) : ld_cluster(addr, (uint32_t)q);
-      float acc = t[0];
+      for (int q = 0; q < SPLIT; ++q) t[q] = ld_cluster4(addr, (uint32_t)q);  // (the own rank: a local address)
+      float4 acc = t[0];
 #pragma unroll
-      for (int q = 1; q < SPLIT; ++q) acc += t[q];
-      stsf(addr, acc);
+      for (int q = 1; q < SPLIT; ++q) acc.x += t[q].x, acc.y += t[q].y, acc.z += t[q].z, acc.w += t[q].w;
+      sts128(addr, acc);
     }
     cluster_sync();  // the other CTAs' reads of this CTA's C are done; local sums visible
   } else {
