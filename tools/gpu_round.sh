@@ -19,6 +19,9 @@ for step in "$@"; do
         timeout 600 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 \
           python -c "import __graft_entry__ as g; g.smoke()" > $out/sanitizer_$tool.log 2>&1
         echo "sanitizer $tool rc=$?"; tail -4 $out/sanitizer_$tool.log
+        timeout 900 /usr/local/cuda/bin/compute-sanitizer --tool $tool --print-limit 20 \
+          python tools/sanitize_extra.py > $out/sanitizer_extra_$tool.log 2>&1
+        echo "sanitizer (extra plans) $tool rc=$?"; tail -4 $out/sanitizer_extra_$tool.log
       done ;;
     bench)
       timeout 600 python bench.py > $out/bench.json 2> $out/bench.err; echo "bench rc=$?"; tail -c 3000 $out/bench.json ;;
