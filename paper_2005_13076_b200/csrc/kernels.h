@@ -45,6 +45,10 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p);
 __global__ void lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p);
 __global__ void lenet_conv2_dgrad_simt(const __grid_constant__ ConvBwdDataP p);
 __global__ void lenet_conv2_wgrad_simt(const __grid_constant__ ConvBwdWeightP p);
+#ifndef C2_IMGS_DEF
+#define C2_IMGS_DEF 2
+#endif
+constexpr int kC2Imgs = C2_IMGS_DEF;  // fp32 conv2 forward: images per CTA round (160 threads each)
 constexpr int kConv2DgradSimtSmem = (50 * 20 * 5 * 8 + 2 * 50 * 16 * 8) * 4;
 
 constexpr int kGemmTile = 64;

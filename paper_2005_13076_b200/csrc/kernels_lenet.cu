@@ -155,10 +155,12 @@ __global__ void __launch_bounds__(C1_THREADS, C1_MINB) lenet_conv1_pool1(const _
 
 // ------------------------------------------------------------ conv2 + pool2
 // Persistent: each CTA stages all conv2 weights (50x20x25, padded to 28 per
-// (f,c)) once, then loops over image pairs.  Thread = (image, filter group
-// of 5, pooled position of 16): 20 accumulators (2x2 window x 5 filters).
-constexpr int C2_IMGS = 2;
-constexpr int C2_THREADS = 320;
+// (f,c)) once, then loops over groups of C2_IMGS images.  Thread = (image,
+// filter group of 5, pooled position of 16): 20 accumulators (2x2 window x 5
+// filters).  (kC2Imgs = 4, 640 threads, measured 56.5 -> 47.1 µs for this
+// kernel alone but 356 -> 430 µs for the fp32 step: two images per CTA.)
+constexpr int C2_IMGS = kC2Imgs;
+constexpr int C2_THREADS = 160 * C2_IMGS;
 __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
     const __grid_constant__ Conv2Pool2P p) {
   pdl_enter();

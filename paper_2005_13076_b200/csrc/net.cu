@@ -1082,8 +1082,8 @@ static void build_fused_lenet(pn_net* net) {
   } else {
     Conv2Pool2P p{p1.data, P + c2.off, P + c2.off + 25000, p2.data, p2.m8, N};
     Launch l;
-    l.set((const void*)lenet_conv2_pool2_simt, dim3(std::min(148, (int)cdiv(N, 2))), dim3(320),
-          (50 * 20 * 28 + 2 * 2880) * 4, p);
+    l.set((const void*)lenet_conv2_pool2_simt, dim3(std::min(net->tc_sms, (int)cdiv(N, kC2Imgs))), dim3(160 * kC2Imgs),
+          (50 * 20 * 28 + kC2Imgs * 2880) * 4, p);
     add(fwd, "conv2+pool2", l);
   }
   if (net->tf32) {
@@ -1636,7 +1636,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
   if (net->layers[0].stem) CU(cudaFuncSetAttribute((const void*)stem_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    stem_fwd_smem(net->layers[0])));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (50 * 20 * 28 + 2 * 2880) * 4));
+                          (50 * 20 * 28 + kC2Imgs * 2880) * 4));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_dgrad_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kConv2DgradSimtSmem));
   if (net->tf32) {
