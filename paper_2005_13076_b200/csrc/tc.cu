@@ -64,6 +64,9 @@ namespace tc {
 #ifndef WG_SLOTS
 #define WG_SLOTS 6
 #endif
+#ifndef WG_ABUF
+#define WG_ABUF 2  // conv2 weight gradient: A tiles in flight (A/B: 3-4 with fewer image slots measured slower)
+#endif
 #ifndef PACK_GRID
 #define PACK_GRID 0  // weight-pack blocks (0: one per W1 tile)
 #endif
@@ -849,7 +852,9 @@ constexpr int A_BYTES = 2 * 128 * 128;   // 2 K-chunks (32 positions each) x 128
 constexpr int G_BYTES = 2 * 64 * 128;    // 2 K-chunks x 64 f rows x 128 B
 constexpr int P_BYTES = 6 * 144 * 4;     // <= 6 input channels of one image
 constexpr int SLOTS = WG_SLOTS;  // images in flight
-constexpr int SMEM = 2 * A_BYTES + SLOTS * G_BYTES + SLOTS * P_BYTES + 1024;
+constexpr int NA = WG_ABUF;      // A tiles in flight (builders vs MMAs)
+constexpr int SMEM = NA * A_BYTES + SLOTS * G_BYTES + SLOTS * P_BYTES + 1024;
+static_assert(SMEM <= 227 * 1024, "shared memory");
 struct Params {
   CUtensorMap tg;  // G2 as {64 p, 50 f, N n}
   const float* p1;
@@ -863,8 +868,8 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   using namespace wg;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t A_s = smem_u32(smem), G_s = A_s + 2 * A_BYTES, P_s = G_s + SLOTS * G_BYTES;
-  __shared__ __align__(8) uint64_t full[SLOTS], sfree[SLOTS], afull[2], afree[2], done;
+  const uint32_t A_s = smem_u32(smem), G_s = A_s + NA * A_BYTES, P_s = G_s + SLOTS * G_BYTES;
+  __shared__ __align__(8) uint64_t full[SLOTS], sfree[SLOTS], afull[NA], afree[NA], done;
   __shared__ uint32_t tmem_base;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int m = blockIdx.x, split = blockIdx.y;
@@ -879,7 +884,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
       mbar_init(smem_u32(&full[s]), 1);
       mbar_init(smem_u32(&sfree[s]), NB + 1);  // builders done with P + MMA done with G
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NA; ++b) {
       mbar_init(smem_u32(&afull[b]), NB);
       mbar_init(smem_u32(&afree[b]), 1);
     }
@@ -889,7 +894,7 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
   }
   if (warp == 0) tmem_alloc(&tmem_base, 64);
   // rows no builder writes (tile 3 beyond row 499) stay zero
-  for (int i = tid; i < 2 * A_BYTES / 16; i += THREADS_W) sts128(A_s + 16 * i, zero4());
+  for (int i = tid; i < NA * A_BYTES / 16; i += THREADS_W) sts128(A_s + 16 * i, zero4());
   fence_proxy_async();
   tc_fence_before();
   __syncthreads();
@@ -916,10 +921,10 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
     constexpr uint32_t idesc = make_idesc(128, 64);
 #pragma unroll 1
     for (int t = 0; t < nimg; ++t) {
-      const int s = t % SLOTS, b = t & 1;
+      const int s = t % SLOTS, b = t % NA;
       mbar_wait(smem_u32(&full[s]), (t / SLOTS) & 1);
       if (t < 4) stamp(1 + t);  // image t landed
-      mbar_wait(smem_u32(&afull[b]), (t >> 1) & 1);
+      mbar_wait(smem_u32(&afull[b]), (t / NA) & 1);
       if (t < 4) stamp(5 + t);  // A tile t built
       tc_fence_after();
       const uint32_t Ab = A_s + b * A_BYTES, Gb = G_s + s * G_BYTES;
@@ -945,9 +950,9 @@ __global__ void __launch_bounds__(wg::THREADS_W, 1) conv2_wgrad_persistent(const
     const int q0 = (ho & 3) * 2;
 #pragma unroll 1
     for (int t = 0; t < nimg; ++t) {
-      const int s = t % SLOTS, b = t & 1;
+      const int s = t % SLOTS, b = t % NA;
       mbar_wait(smem_u32(&full[s]), (t / SLOTS) & 1);
-      if (t >= 2) mbar_wait(smem_u32(&afree[b]), ((t >> 1) - 1) & 1);
+      if (t >= NA) mbar_wait(smem_u32(&afree[b]), ((t / NA) - 1) & 1);
       if (active) {
         float x[12];
         const uint32_t src = P_s + s * P_BYTES + src_off;
