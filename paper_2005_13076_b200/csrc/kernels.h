@@ -15,6 +15,7 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
 template <int KH, int KW, int SH, int SW>
 __global__ void pool_bwd_plane(const __grid_constant__ PoolBwdP p);
 __global__ void gemm_generic(const __grid_constant__ GemmP p);
+__global__ void gemm_splitk_reduce(const __grid_constant__ GemmP p);
 __global__ void stem_fwd(const __grid_constant__ StemP p);
 __global__ void stem_wgrad(const __grid_constant__ StemP p);
 constexpr int kStemKmax = 75;  // stem_wgrad: C x kh x kw (the cifar10_quick stem: 3 x 5 x 5)

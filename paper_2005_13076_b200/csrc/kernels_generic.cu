@@ -730,14 +730,15 @@ __global__ void __launch_bounds__(128) gemm_tiled(const __grid_constant__ GemmP 
     }
   };
   float acc[4][4] = {};
-  const int nk = (p.K + BK - 1) / BK;
-  load(0);
+  const int nkt = (p.K + BK - 1) / BK, S = p.splits > 1 ? p.splits : 1;  // K steps of this z slice
+  const int kt0 = (int)((long long)nkt * blockIdx.z / S), kt1 = (int)((long long)nkt * (blockIdx.z + 1) / S);
+  load(kt0 * BK);
   store(0);
   __syncthreads();
 #pragma unroll 1
-  for (int kt = 0; kt < nk; ++kt) {
-    const int buf = kt & 1;
-    if (kt + 1 < nk) load((kt + 1) * BK);  // next step's loads in flight under this step's FMAs
+  for (int kt = kt0; kt < kt1; ++kt) {
+    const int buf = (kt - kt0) & 1;
+    if (kt + 1 < kt1) load((kt + 1) * BK);  // next step's loads in flight under this step's FMAs
 #pragma unroll
     for (int kk = 0; kk < BK; ++kk) {
       const float4 a = *reinterpret_cast<const float4*>(&As[buf][kk][tm]);
@@ -748,8 +749,20 @@ __global__ void __launch_bounds__(128) gemm_tiled(const __grid_constant__ GemmP 
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
     }
-    if (kt + 1 < nk) store(buf ^ 1);  // the other buffer: last read one step ago (barrier below)
+    if (kt + 1 < kt1) store(buf ^ 1);  // the other buffer: last read one step ago (barrier below)
     __syncthreads();
+  }
+  if (S > 1) {  // K split: the raw partial of this slice (bias / ReLU in gemm_splitk_reduce)
+    float* out = p.part + (size_t)blockIdx.z * p.M * p.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + tm + i;
+      if (gm >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n0 + tn + j < p.N) out[(long long)gm * p.N + n0 + tn + j] = acc[i][j];
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -764,6 +777,18 @@ __global__ void __launch_bounds__(128) gemm_tiled(const __grid_constant__ GemmP 
       if (p.relu) v = v > 0.f ? v : 0.f;
       p.C[(long long)gm * p.N + gn] = v;
     }
+  }
+}
+// C = sum over the K slices (ascending z: a fixed order) + bias, ReLU
+__global__ void __launch_bounds__(256) gemm_splitk_reduce(const __grid_constant__ GemmP p) {
+  pdl_enter();
+  const long long MN = (long long)p.M * p.N;
+  for (long long i = blockIdx.x * 256LL + threadIdx.x; i < MN; i += (long long)gridDim.x * 256) {
+    float v = p.part[i];
+    for (int z = 1; z < p.splits; ++z) v += p.part[z * MN + i];
+    if (p.bias) v += p.bias[i % p.N];
+    if (p.relu) v = v > 0.f ? v : 0.f;
+    p.C[i] = v;
   }
 }
 template __global__ void gemm_tiled<0, 0>(const __grid_constant__ GemmP);

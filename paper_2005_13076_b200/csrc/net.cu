@@ -310,6 +310,8 @@ struct pn_net {
   bool tmap_failed = false;
   // layerwise TF32 plan: shared workspaces of the weight-gradient operands
   float* col_ws = nullptr;  // colT [kpad][pitch]
+  float* gemm_ws = nullptr;  // split-K partials of the register-tiled fp32 GEMM (add_gemm)
+  size_t gemm_ws_floats = 0;
   float* gm_ws = nullptr;   // Gm   [fpad][pitch]
 
   int blob(const std::string& n) const {
@@ -601,6 +603,17 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->gm_ws, gm_n));
   }
   TRY(net->alloc(&net->err, 1));
+  {  // split-K workspace of the fp32 inner products (up to 8 slices of the largest of their GEMMs)
+    size_t mx = 0;
+    const bool fp32_ip = !(net->fused && net->tf32);
+    for (auto& L : net->layers)
+      if (L.type == L_IP && fp32_ip)
+        mx = std::max({mx, (size_t)net->batch * L.Nout, (size_t)L.Nout * L.K, (size_t)net->batch * L.K});
+    if (mx) {
+      net->gemm_ws_floats = 8 * mx;
+      TRY(net->alloc(&net->gemm_ws, net->gemm_ws_floats));
+    }
+  }
   if (!net->acc_layers.empty()) TRY(net->alloc(&net->acc_flags, net->batch));
   // activation blobs (the fused plan never stores conv1's output or its
   // gradient, nor conv2's output; conv2's gradient is the dense unpooled G2)
@@ -746,13 +759,49 @@ static Launch gemm_launch(const GemmP& g) {
   const int at = g.sak == 1 && g.sam % 4 == 0 ? 0 : (g.sam == 1 && g.sak % 4 == 0 ? 1 : -1);
   const int bt = g.sbk == 1 && g.sbn % 4 == 0 ? 0 : (g.sbn == 1 && g.sbk % 4 == 0 ? 1 : -1);
   if (at < 0 || bt < 0 || !al(g.A) || !al(g.B)) {
-    l.set((const void*)gemm_generic, dim3(cdiv(g.N, 64), cdiv(g.M, 64)), dim3(256), 0, g);
+    GemmP q = g;
+    q.splits = 1;
+    l.set((const void*)gemm_generic, dim3(cdiv(g.N, 64), cdiv(g.M, 64)), dim3(256), 0, q);
     return l;
   }
   const void* f = at == 0 ? (bt == 0 ? (const void*)gemm_tiled<0, 0> : (const void*)gemm_tiled<0, 1>)
                           : (bt == 0 ? (const void*)gemm_tiled<1, 0> : (const void*)gemm_tiled<1, 1>);
-  l.set(f, dim3(cdiv(g.N, 32), cdiv(g.M, 64)), dim3(128), 0, g);
+  l.set(f, dim3(cdiv(g.N, 32), cdiv(g.M, 64), std::max(1, g.splits)), dim3(128), 0, g);
   return l;
+}
+
+// K split for the register-tiled GEMM: about four 128-thread blocks per SM,
+// >= 4 K steps of 16 per slice, <= 8 slices (the fp32 plans' 64 x 32 tiles
+// alone leave most SMs with one block)
+static int gemm_splits(const pn_net* net, const GemmP& g) {
+  const long long blocks = (long long)cdiv(g.N, 32) * cdiv(g.M, 64);
+  const int nkt = (g.K + 15) / 16;
+  int s = (int)std::min<long long>(8, std::max<long long>(1, 4LL * net->tc_sms / blocks));
+  s = std::max(1, std::min(s, nkt / 4));
+  return getenv("PN_NO_SPLITK") ? 1 : s;
+}
+
+// C = A B as stages: the GEMM (K split into raw partials in gemm_ws when it
+// pays) + the fixed-order sum of the slices with bias / ReLU
+static void add_gemm(pn_net* net, std::vector<Stage>& v, const std::string& name, GemmP g,
+                     std::function<void(Launch&, const StepArgs&)> patch = nullptr) {
+  g.splits = 1;
+  Launch l = gemm_launch(g);
+  if (l.func != (const void*)gemm_generic) {
+    const int s = gemm_splits(net, g);
+    if (s > 1 && (size_t)s * g.M * g.N <= net->gemm_ws_floats) {
+      g.splits = s;
+      g.part = net->gemm_ws;
+      l = gemm_launch(g);
+      add(v, name, l, patch);
+      Launch r;
+      r.set((const void*)gemm_splitk_reduce,
+            dim3((unsigned)std::min<long long>(8LL * net->tc_sms, cdiv((long long)g.M * g.N, 256))), dim3(256), 0, g);
+      add(v, name + ".splitk_reduce", r);
+      return;
+    }
+  }
+  add(v, name, l, patch);
 }
 
 static void build_layerwise(pn_net* net) {
@@ -858,9 +907,8 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_IP) {
       GemmP p{x, net->params + L.off, top->data, L.bias ? net->params + L.off + L.wcount : nullptr,
               N, L.Nout, L.K, L.K, 1, 1, L.K, 0};
-      l = gemm_launch(p);
-      add(fwd, L.name + ".fwd", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().A = a.x; }
-                                       : std::function<void(Launch&, const StepArgs&)>());
+      add_gemm(net, fwd, L.name + ".fwd", p, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().A = a.x; }
+                                                 : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_SOFTMAX) {
       SoftmaxP p{x, nullptr, top->data, N, L.in[1] * L.in[2] * L.in[3]};
       l.set((const void*)softmax_fwd_generic, dim3(cdiv(N, 8)), dim3(256), 0, p);
@@ -987,9 +1035,8 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_IP) {
       // dW = dy^T x : A(m=o,k=n) = dy[n*Nout+o], B(k=n, n=k') = x[n*K+k']
       GemmP w{top.diff, x, net->grads + L.off, nullptr, L.Nout, L.K, N, 1, L.Nout, L.K, 1, 0};
-      l = gemm_launch(w);
-      add(bwd, L.name + ".wgrad", l, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().B = a.x; }
-                                         : std::function<void(Launch&, const StepArgs&)>());
+      add_gemm(net, bwd, L.name + ".wgrad", w, isx ? [](Launch& l, const StepArgs& a) { l.params<GemmP>().B = a.x; }
+                                                   : std::function<void(Launch&, const StepArgs&)>());
       if (L.bcount) {
         ColSumP c{top.diff, net->grads + L.off + L.wcount, N, L.Nout};
         Launch l2;
@@ -998,9 +1045,7 @@ static void build_layerwise(pn_net* net) {
       }
       if (bot) {
         GemmP d{top.diff, net->params + L.off, bot->diff, nullptr, N, L.K, L.Nout, L.Nout, 1, L.K, 1, 0};
-        Launch l3;
-        l3 = gemm_launch(d);
-        add(bwd, L.name + ".dgrad", l3);
+        add_gemm(net, bwd, L.name + ".dgrad", d);
       }
     } else if (L.type == L_SOFTMAX) {
       if (bot) {
@@ -1090,9 +1135,7 @@ static void build_fused_lenet(pn_net* net) {
     add(fwd, "ip1+relu[tc]", tc::ip1_fwd_launch(p2.data, net->pack.w1f, P + i1.off + i1.wcount, a1.data, N));
   } else {
     GemmP g{p2.data, P + i1.off, a1.data, P + i1.off + i1.wcount, N, 500, 800, 800, 1, 1, 800, 1};
-    Launch l;
-    l = gemm_launch(g);
-    add(fwd, "ip1+relu", l);
+    add_gemm(net, fwd, "ip1+relu", g);
   }
   {
     Ip2LossP p{a1.data, P + i2.off, P + i2.off + 5000, nullptr, lg.data,
@@ -1156,18 +1199,14 @@ static void build_fused_lenet(pn_net* net) {
     conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
-    Launch l;
-    l = gemm_launch(w);
-    add(bwd, "ip1.wgrad", l);
+    add_gemm(net, bwd, "ip1.wgrad", w);
     ColSumP c{a1.diff, G + i1.off + i1.wcount, N, 500};
     Launch l2;
     l2.set((const void*)colsum_generic, dim3(500), dim3(256), 0, c);
     add(bwd, "ip1.bgrad", l2);
     add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
     GemmP d{a1.diff, P + i1.off, p2.diff, nullptr, N, 800, 500, 500, 1, 800, 1, 0};
-    Launch l3;
-    l3 = gemm_launch(d);
-    add(bwd, "ip1.dgrad", l3);
+    add_gemm(net, bwd, "ip1.dgrad", d);
     Unpool2P u{p2.diff, p2.m8, cv2.diff, N};
     Launch l4;
     l4.set((const void*)lenet_unpool2, dim3(cdiv((long long)N * 3200, 256)), dim3(256), 0, u);

@@ -93,6 +93,8 @@ struct GemmP {  // C[m,n] = sum_k A(m,k) B(k,n) (+ bias[n]) (relu)
   int M, N, K;
   long long sam, sak, sbk, sbn;
   int relu;
+  int splits;   // gemm_tiled: > 1 = K split over gridDim.z, raw partials to part[z][M][N] (gemm_splitk_reduce adds them)
+  float* part;
 };
 struct ColSumP {  // out[n] = sum_m a[m*N + n]
   const float* a;
