@@ -413,7 +413,12 @@ constexpr int B_BYTES = 99 * 1024;             // 25 taps + >= 1024 B zero pad
 constexpr int C_PITCH = 50;                    // floats per C row (+ skew below)
 constexpr int C_BYTES = 25 * 1024 + 1024;      // 128 x 50 floats + max skew
 constexpr int STAGES = CF_STAGES;
-constexpr int THREADS_F = 192;
+#ifndef CF_POOL_WARPS
+#define CF_POOL_WARPS 4  // extra warps that join the pooling phase of the epilogue
+#endif
+constexpr int POOLW = CF_POOL_WARPS;
+constexpr int THREADS_F = 192 + 32 * POOLW;
+constexpr int EPI_T = 128 + 32 * POOLW;  // threads of the pooling phase
 constexpr int SMEM = B_BYTES + STAGES * A_BYTES + C_BYTES + 1024;
 static_assert(25 * TAP_BYTES + 1024 <= B_BYTES, "B pad");
 struct Params {
@@ -528,33 +533,42 @@ __global__ void __launch_bounds__(cf::THREADS_F, 1) conv2_fwd_persistent(const _
       mma_commit(smem_u32(&tfull[b]));
     }
   } else if (warp >= 2) {
-    // ---- epilogue (128 threads): TMEM lane quadrant q = warp % 4 = rows 32q..
+    // ---- epilogue: warps 2-5 (TMEM lane quadrant q = warp % 4 = rows 32q..)
+    // drain the accumulator into the shared C tile; they and POOLW more warps
+    // then pool it (800 pooled outputs per pair over EPI_T threads)
+    const bool drains = warp < 6;
     const int quad = warp & 3, row = quad * 32 + lane, et = tid - 64;
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
       const int b = it & 1, pair = pair0 + it;
-      mbar_wait(smem_u32(&tfull[b]), (it >> 1) & 1);
-      if (warp == 2 && lane == 0 && it < 4) stamp(6 + it);  // accumulator ready
-      __syncwarp();
-      tc_fence_after();
+      if (drains) {
+        mbar_wait(smem_u32(&tfull[b]), (it >> 1) & 1);
+        if (warp == 2 && lane == 0 && it < 4) stamp(6 + it);  // accumulator ready
+        __syncwarp();
+        tc_fence_after();
+      }
       float v[64];
+      if (drains) {
 #pragma unroll
-      for (int c0 = 0; c0 < 64; c0 += 16)
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 64 + c0, *reinterpret_cast<float(*)[16]>(v + c0));
-      tc_fence_before();
-      if (warp == 2 && lane == 0 && it == 0) stamp(11);
-      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // C free (previous pair pooled)
+        for (int c0 = 0; c0 < 64; c0 += 16)
+          tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * 64 + c0, *reinterpret_cast<float(*)[16]>(v + c0));
+        tc_fence_before();
+        if (warp == 2 && lane == 0 && it == 0) stamp(11);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[b])) : "memory");
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(EPI_T) : "memory");  // C free (previous pair pooled)
+      if (drains) {
 #pragma unroll
-      for (int f = 0; f < 50; f += 2)
-        asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(c_addr(C_s, row, f)), "f"(v[f]), "f"(v[f + 1])
-                     : "memory");
-      asm volatile("bar.sync 1, 128;" ::: "memory");  // C complete
+        for (int f = 0; f < 50; f += 2)
+          asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(c_addr(C_s, row, f)), "f"(v[f]), "f"(v[f + 1])
+                       : "memory");
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(EPI_T) : "memory");  // C complete
       if (warp == 2 && lane == 0 && it == 0) stamp(12);
       const int n0 = 2 * pair;
 #pragma unroll
-      for (int q = 0; q < 7; ++q) {  // 800 pooled (f, ph, pw) over 128 threads
-        const int k = et + 128 * q;
+      for (int q = 0; q < (800 + EPI_T - 1) / EPI_T; ++q) {  // 800 pooled (f, ph, pw) over EPI_T threads
+        const int k = et + EPI_T * q;
         if (k >= 800) break;
         const int f = k >> 4, ph = (k >> 2) & 3, pw = k & 3;
         const float bias = bias_s[f];
