@@ -18,6 +18,7 @@ __global__ void gemm_generic(const __grid_constant__ GemmP p);
 __global__ void gemm_splitk_reduce(const __grid_constant__ GemmP p);
 __global__ void stem_fwd(const __grid_constant__ StemP p);
 __global__ void stem_wgrad(const __grid_constant__ StemP p);
+size_t stem_wgrad_smem(int C, int H, int W, int ph, int pw, int HWp);
 constexpr int kStemKmax = 75;  // stem_wgrad: C x kh x kw (the cifar10_quick stem: 3 x 5 x 5)
 constexpr int STEM_FG_HOST = 8;  // stem kernels: filters per block (kernels_generic.cu STEM_FG)
 template <int AT, int BT>

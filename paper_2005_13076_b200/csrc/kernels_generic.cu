@@ -225,9 +225,11 @@ __global__ void __launch_bounds__(256) stem_fwd(const __grid_constant__ StemP p)
 #pragma unroll 1
       for (int i = 0; i < 5; ++i) {  // (the stem's kernel is 5 x 5: net.cu checks)
         const float* xr = xs + (c * Hpad + h + i) * xpitch + w0;
-        float xv[8];  // the 4 outputs' row segment: w0 .. w0 + 3 + (kw - 1)
-#pragma unroll
-        for (int u = 0; u < 8; ++u) xv[u] = xr[u];
+        float xv[8];  // the 4 outputs' row segment: w0 .. w0 + 3 + (kw - 1), two 16-B loads
+        {  // (w0 and the row pitch are multiples of 4 floats: conflict-free quarter-warp phases)
+          const float4 a = *reinterpret_cast<const float4*>(xr), b = *reinterpret_cast<const float4*>(xr + 4);
+          xv[0] = a.x, xv[1] = a.y, xv[2] = a.z, xv[3] = a.w, xv[4] = b.x, xv[5] = b.y, xv[6] = b.z, xv[7] = b.w;
+        }
         const float* wr = ws + ((c * 5 + i) * 5) * STEM_FG;
 #pragma unroll
         for (int j = 0; j < 5; ++j) {
@@ -282,47 +284,49 @@ __global__ void __launch_bounds__(256) stem_fwd(const __grid_constant__ StemP p)
 // gradient to (P:220-222 composed with the conv weight gradient; no
 // conv-output gradient is formed: overlapping windows that pick the same
 // position just add), db[f] = sum g.  g = dy: the ReLU's backward was applied
-// by its consumer (the next conv's data gradient).  grid = (filter groups of
-// 8, image splits); thread = (filter, lane): the lane's pooled positions,
-// its 75 (C kh kw) accumulators in registers; the split's images staged one
-// at a time (zero-padded); lanes combined by shuffles; one partial per split.
+// by its consumer (the next conv's data gradient).  grid = image splits;
+// lane = filter (F <= 32), warp w the pooled positions q = w, w+8, ...: at a
+// given q the 32 filters' windows start at <= 9 distinct origins (dy, dx in
+// the pooling window), whose words fall in distinct banks (dy * Wpad + dx
+// mod 32), so every window load of the warp is one conflict-free wavefront
+// (lanes on one q but different positions gathered the same rows in many
+// banks).  The image's gradients and origins are staged per filter row
+// (pitch HWp + 1: conflict-free column reads), the 75 accumulators of a
+// thread cover its filter's taps; warps combined in order at the end.
 constexpr int STEM_KMAX = kStemKmax;
 __global__ void __launch_bounds__(256) stem_wgrad(const __grid_constant__ StemP p) {
   pdl_enter();
   extern __shared__ __align__(16) float sm[];
-  const int s = blockIdx.y, f = blockIdx.x * STEM_FG + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  const int s = blockIdx.x, f = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
-  const int Hpad = p.H + 2 * p.ph, Wpad = p.W + 2 * p.pw, HWp = p.Hp * p.Wp;
+  const int Hpad = p.H + 2 * p.ph, Wpad = p.W + 2 * p.pw, HWp = p.Hp * p.Wp, GP = HWp + 1;
+  const int XN = p.C * Hpad * Wpad;
+  float* xs = sm;                              // [C][Hpad][Wpad] zero-padded image
+  float* gs = xs + XN;                         // [32 f][GP] gradients
+  int* os = reinterpret_cast<int*>(gs + 32 * GP);  // [32 f][GP] origins
   const bool live = f < p.F;
   float acc[STEM_KMAX], bacc = 0.f;
 #pragma unroll
   for (int k = 0; k < STEM_KMAX; ++k) acc[k] = 0.f;
-  constexpr int QMAX = 8;  // pooled positions per lane and image (Hp Wp <= 256: net.cu checks)
   for (int n = n0; n < n1; ++n) {
-    // this image's (gradient, origin) pairs of the lane, loads in flight with the staging
-    const size_t base = ((size_t)n * p.F + (live ? f : 0)) * HWp;
-    float gq[QMAX];
-    int oq[QMAX];
-#pragma unroll
-    for (int t = 0; t < QMAX; ++t) {
-      const int q = lane + 32 * t;
-      gq[t] = (live && q < HWp) ? __ldg(p.dy + base + q) : 0.f;
-      oq[t] = (live && q < HWp) ? __ldg(p.mask + base + q) : 0;
-    }
     __syncthreads();  // the previous image's reads are done
-    for (int i = threadIdx.x; i < p.C * Hpad * Wpad; i += 256) {
-      const int c = i / (Hpad * Wpad), r = i - c * Hpad * Wpad, h = r / Wpad - p.ph, w = r % Wpad - p.pw;
-      sm[i] = (h >= 0 && h < p.H && w >= 0 && w < p.W) ? __ldg(p.x + (((size_t)n * p.C + c) * p.H + h) * p.W + w) : 0.f;
+    for (int i = threadIdx.x; i < XN; i += 256) {
+      const int c = i / (Hpad * Wpad), r = i - c * Hpad * Wpad, h = r / Wpad - p.ph, ww = r % Wpad - p.pw;
+      xs[i] = (h >= 0 && h < p.H && ww >= 0 && ww < p.W) ? __ldg(p.x + (((size_t)n * p.C + c) * p.H + h) * p.W + ww) : 0.f;
+    }
+    for (int i = threadIdx.x; i < p.F * HWp; i += 256) {  // coalesced along q
+      const int ff = i / HWp, q = i - ff * HWp;
+      const size_t src = ((size_t)n * p.F + ff) * HWp + q;
+      gs[ff * GP + q] = __ldg(p.dy + src);
+      os[ff * GP + q] = __ldg(p.mask + src);
     }
     __syncthreads();
     if (!live) continue;
-#pragma unroll
-    for (int t = 0; t < QMAX; ++t) {
-      if (lane + 32 * t >= HWp) break;
-      const float g = gq[t];
-      const int o = oq[t], h = o / p.Wo, w = o - h * p.Wo;
+    for (int q = w; q < HWp; q += 8) {
+      const float g = gs[f * GP + q];
+      const int o = os[f * GP + q], h = o / p.Wo, ww = o - h * p.Wo;
       bacc += g;
-      const float* xp = sm + h * Wpad + w;  // conv output (h, w) reads padded rows h..h+kh-1
+      const float* xp = xs + h * Wpad + ww;  // conv output (h, w) reads padded rows h..h+kh-1
 #pragma unroll
       for (int k = 0; k < STEM_KMAX; ++k) {
         const int c = k / 25, i = (k / 5) % 5, j = k % 5;  // (C kh kw = 3 x 5 x 5)
@@ -330,19 +334,30 @@ __global__ void __launch_bounds__(256) stem_wgrad(const __grid_constant__ StemP 
       }
     }
   }
-  if (!live) return;
+  // combine the 8 warps in order: [w][f][76] over the staging area
+  __syncthreads();
+  float* red = sm;
+  if (live) {
 #pragma unroll
-  for (int k = 0; k < STEM_KMAX; ++k)
-#pragma unroll
-    for (int m = 16; m > 0; m >>= 1) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], m);
-#pragma unroll
-  for (int m = 16; m > 0; m >>= 1) bacc += __shfl_xor_sync(0xffffffffu, bacc, m);
-  if (lane == 0) {
-    float* out = p.part_w + (size_t)s * p.pstride;
-#pragma unroll
-    for (int k = 0; k < STEM_KMAX; ++k) out[f * STEM_KMAX + k] = acc[k];
-    if (p.b) out[p.F * STEM_KMAX + f] = bacc;
+    for (int k = 0; k < STEM_KMAX; ++k) red[(w * 32 + f) * (STEM_KMAX + 1) + k] = acc[k];
+    red[(w * 32 + f) * (STEM_KMAX + 1) + STEM_KMAX] = bacc;
   }
+  __syncthreads();
+  float* out = p.part_w + (size_t)s * p.pstride;
+  for (int e = threadIdx.x; e < p.F * (STEM_KMAX + 1); e += 256) {
+    const int ff = e / (STEM_KMAX + 1), k = e - ff * (STEM_KMAX + 1);
+    float v = 0.f;
+#pragma unroll
+    for (int ww = 0; ww < 8; ++ww) v += red[(ww * 32 + ff) * (STEM_KMAX + 1) + k];
+    if (k < STEM_KMAX) out[ff * STEM_KMAX + k] = v;
+    else if (p.b) out[p.F * STEM_KMAX + ff] = v;
+  }
+}
+
+size_t stem_wgrad_smem(int C, int H, int W, int ph, int pw, int HWp) {
+  const size_t a = (size_t)C * (H + 2 * ph) * (W + 2 * pw) + 2 * 32 * (size_t)(HWp + 1);
+  const size_t r = (size_t)8 * 32 * (kStemKmax + 1);
+  return 4 * (a > r ? a : r);
 }
 
 // ------------------------------------------------------------------ pooling

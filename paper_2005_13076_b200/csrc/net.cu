@@ -556,8 +556,8 @@ static pn_status allocate(pn_net* net) {
       L.splits = std::max(1, std::min(net->batch, WG2_SPLITS > 0 ? WG2_SPLITS : net->tc_sms / 4));
     if (net->fused && !net->tf32 && &L == &net->layers[2])  // fp32 SIMT conv2 weight gradient: one block per SM
       L.splits = std::max(1, std::min(net->batch, net->tc_sms));
-    if (L.stem)  // two blocks per SM over (filter groups of 8) x image splits
-      L.splits = std::max(1, std::min(net->batch, 2 * net->tc_sms / ((L.F + STEM_FG_HOST - 1) / STEM_FG_HOST)));
+    if (L.stem)  // stem_wgrad: two blocks per SM over image splits
+      L.splits = std::max(1, std::min(net->batch, 2 * net->tc_sms));
     if (L.tc_conv) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
                                 net->tc_sms, L.G);
@@ -724,7 +724,7 @@ static bool is_stem(const pn_net* net) {
       P.ph != P.pw)
     return false;
   if (R.type != L_RELU || R.bottom != P.top || R.top != P.top || R.slope != 0.f) return false;
-  if (P.out[2] * P.out[3] > 256 || C.out[3] > 64) return false;  // stem_wgrad: <= 8 pooled positions per lane
+  if (C.F > 32) return false;  // stem_wgrad: lane = filter
   for (size_t i = 2; i < net->layers.size(); ++i)
     if (net->layers[i].bottom == C.top) return false;
   for (const Layer& A : net->acc_layers)
@@ -949,8 +949,9 @@ static void build_layerwise(pn_net* net) {
     if (stem && li <= 2) {  // the stem's backward: its weight gradient from the pooled gradient (is_stem)
       if (li == 0) {
         Launch l;
-        l.set((const void*)stem_wgrad, dim3(cdiv(L.F, STEM_FG_HOST), L.splits), dim3(256),
-              (size_t)L.in[1] * (L.in[2] + 2 * L.ph) * (L.in[3] + 2 * L.pw) * 4, stem_params(net));
+        const Layer& Pl = net->layers[1];
+        l.set((const void*)stem_wgrad, dim3(L.splits), dim3(256),
+              stem_wgrad_smem(L.in[1], L.in[2], L.in[3], L.ph, L.pw, Pl.out[2] * Pl.out[3]), stem_params(net));
         add(bwd, L.name + ".wgrad", l, [](Launch& l, const StepArgs& a) { l.params<StemP>().x = a.x; });
         add_reduce(net, bwd, L);
       }
@@ -1672,8 +1673,12 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     }
   }
   TRY(allocate(net.get()));
-  if (net->layers[0].stem) CU(cudaFuncSetAttribute((const void*)stem_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   stem_fwd_smem(net->layers[0])));
+  if (net->layers[0].stem) {
+    const Layer &C = net->layers[0], &P = net->layers[1];
+    CU(cudaFuncSetAttribute((const void*)stem_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, stem_fwd_smem(C)));
+    CU(cudaFuncSetAttribute((const void*)stem_wgrad, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)stem_wgrad_smem(C.in[1], C.in[2], C.in[3], C.ph, C.pw, P.out[2] * P.out[3])));
+  }
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_pool2_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (50 * 20 * 28 + kC2Imgs * 2880) * 4));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_dgrad_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
