@@ -153,7 +153,7 @@ def test_pipelined_host_steps_equal_device_steps():
     import torch
 
     from paper_2005_13076_b200 import Net, make_sgd
-    N, S = 64, 5
+    N, S = 64, 13  # two multi-step graphs of 6 (PIPE_SLOTS) + one step on its own
     x8, y = synth.mnist_like_fast_u8(N * S, seed=9)
     x8 = x8.reshape(S, N, 1, 28, 28)
     y = y.reshape(S, N)
@@ -184,7 +184,7 @@ def test_pipelined_host_steps_follow_changed_solver_settings():
     import torch
 
     from paper_2005_13076_b200 import Net, make_sgd
-    N, S = 64, 3
+    N, S = 64, 7  # per call: one multi-step graph of 6 (PIPE_SLOTS) + one step on its own
     x8, y = synth.mnist_like_fast_u8(N * 2 * S, seed=11)
     x8 = x8.reshape(2 * S, N, 1, 28, 28)
     y = y.reshape(2 * S, N)
