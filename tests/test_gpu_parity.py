@@ -156,12 +156,13 @@ def test_net_forward_backward(spec, N, tf32, layerwise):
     check_net_level(net, ref, params, out, gref, loss.item(), rtol)
 
 
-@pytest.mark.parametrize("tf32", [False, True])
-def test_train_step_graph_equals_eager_and_is_deterministic(tf32):
-    """The whole-step graph (TF32: loss sum on the side branch, conv bucket
-    reduced inside the solver) is bitwise the eager phases (separate bucket
-    reduction, then the solver) and reruns bitwise."""
-    N = 64
+@pytest.mark.parametrize("tf32,N", [(False, 64), (True, 64), (True, 1), (True, 37), (True, 512)])
+def test_train_step_graph_equals_eager_and_is_deterministic(tf32, N):
+    """The whole-step graph (TF32: loss sum and the ip layers' solver on the
+    side branch, the conv bucket reduced and updated in conv1's weight-gradient
+    tail after a grid barrier over its blocks -- 256 of them at N = 512) is
+    bitwise the eager phases (separate bucket reduction, then the solver) and
+    reruns bitwise; degenerate, ragged and the bench's batch."""
     sgd = make_sgd()
     results = []
     for mode in ("eager", "graph", "graph"):
