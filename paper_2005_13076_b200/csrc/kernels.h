@@ -60,7 +60,7 @@ constexpr int kGemmTile = 64;
 constexpr int kWgradSplits = KWG;
 // conv1 weight gradient (fused LeNet plan): images per block
 #ifndef CW_IMGS_DEF
-#define CW_IMGS_DEF 2
+#define CW_IMGS_DEF 4
 #endif
 constexpr int CW_IMGS = CW_IMGS_DEF;
 // ip2 + softmax-loss: samples (warps) per block

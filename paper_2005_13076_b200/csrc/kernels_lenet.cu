@@ -541,32 +541,40 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 // ---------------------------------------------------- conv1 weight gradient
 // dW1[f,i,j] = sum_n sum_q dp1[n,f,q] * x[n, h_q + i, w_q + j] where (h_q,w_q)
 // is the conv1 position pool1 routed gradient q to (P:220-222 composed with
-// S:351); db1[f] = sum dp1.  grid = splits over images (<= 2 images per
-// block), block = 320 threads (20 filters x 16 lanes), images staged in smem;
-// every (gradient, origin) pair of the block is loaded up front so the 36
-// global loads per thread are in flight together.
+// S:351); db1[f] = sum dp1.  grid = splits over images (<= CW_IMGS images
+// per block), block = 320 threads (20 filters x 16 lanes), images staged in
+// smem; the (gradient, origin) pairs of two images at a time in registers
+// (18 global loads per thread in flight together).
 // dp1 comes from conv2's data gradient two launches back (the predecessor,
 // conv2's weight gradient, produces nothing read here): the kernel runs
 // alongside it and waits only at the end (pdl.cuh).
-__global__ void __launch_bounds__(320, 2) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
+#ifndef C1W_MINB
+#define C1W_MINB 2
+#endif
+__global__ void __launch_bounds__(320, C1W_MINB) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
   __shared__ float xs[CW_IMGS][784];
   ST_BEGIN(ST_CONV1W);
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
   const int cnt = min(CW_IMGS, n1 - n0);
   const int f = threadIdx.x / 16, l = threadIdx.x % 16;
-  float g[CW_IMGS * 9];
-  int off[CW_IMGS * 9];
+  // images in chunks of CH: one chunk's (gradient, origin) pairs in registers
+  constexpr int CH = CW_IMGS < 2 ? CW_IMGS : 2;
+  float g[CH * 9];
+  int off[CH * 9];
+  auto load_chunk = [&](int c0) {
 #pragma unroll
-  for (int im = 0; im < CW_IMGS; ++im)
+    for (int im = 0; im < CH; ++im)
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      const bool v = im < cnt;
-      const long long idx = ((long long)(n0 + (v ? im : 0)) * 20 + f) * 144 + l + 16 * t;
-      g[im * 9 + t] = v ? __ldg(p.dp1 + idx) : 0.f;
-      off[im * 9 + t] = v ? (int)__ldg(p.m1 + idx) : 0;
-    }
-  {  // staging loads all in flight together
+      for (int t = 0; t < 9; ++t) {
+        const bool v = c0 + im < cnt;
+        const long long idx = ((long long)(n0 + (v ? c0 + im : 0)) * 20 + f) * 144 + l + 16 * t;
+        g[im * 9 + t] = v ? __ldg(p.dp1 + idx) : 0.f;
+        off[im * 9 + t] = v ? (int)__ldg(p.m1 + idx) : 0;
+      }
+  };
+  load_chunk(0);
+  {  // staging loads all in flight together (with the first chunk's)
     constexpr int PER = (CW_IMGS * 784 + 319) / 320;
     float v[PER];
 #pragma unroll
@@ -584,21 +592,25 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_wgrad(const __grid_constan
   float acc[25], bacc = 0.f;
 #pragma unroll
   for (int t = 0; t < 25; ++t) acc[t] = 0.f;
+#pragma unroll 1
+  for (int c0 = 0; c0 < cnt; c0 += CH) {
+    if (c0 > 0) load_chunk(c0);
 #pragma unroll
-  for (int im = 0; im < CW_IMGS; ++im) {
-    if (im >= cnt) break;
+    for (int im = 0; im < CH; ++im) {
+      if (c0 + im >= cnt) break;
 #pragma unroll
-    for (int t = 0; t < 9; ++t) {
-      const int q = l + 16 * t;
-      const float gv = g[im * 9 + t];
-      const int o = off[im * 9 + t];
-      const int h = 2 * (q / 12) + (o >> 1), w = 2 * (q % 12) + (o & 1);
-      bacc += gv;
-      const float* xp = &xs[im][h * 28 + w];
+      for (int t = 0; t < 9; ++t) {
+        const int q = l + 16 * t;
+        const float gv = g[im * 9 + t];
+        const int o = off[im * 9 + t];
+        bacc += gv;
+        const int h = 2 * (q / 12) + (o >> 1), w = 2 * (q % 12) + (o & 1);
+        const float* xp = &xs[c0 + im][h * 28 + w];
 #pragma unroll
-      for (int i = 0; i < 5; ++i)
+        for (int i = 0; i < 5; ++i)
 #pragma unroll
-        for (int j = 0; j < 5; ++j) acc[i * 5 + j] = fmaf(gv, xp[i * 28 + j], acc[i * 5 + j]);
+          for (int j = 0; j < 5; ++j) acc[i * 5 + j] = fmaf(gv, xp[i * 28 + j], acc[i * 5 + j]);
+      }
     }
   }
 #pragma unroll
@@ -613,11 +625,13 @@ __global__ void __launch_bounds__(320, 2) lenet_conv1_wgrad(const __grid_constan
     for (int t = 0; t < 25; ++t) p.part_w[(long long)s * p.pstride + f * 25 + t] = acc[t];
     p.part_b[(long long)s * p.pstride + f] = bacc;
   }
+  if (threadIdx.x == 0) st_mark(ST_RED_CONV, 2);  // (step trace: the last block's partials written)
   // dp1 came from two launches back; the predecessor (conv2's weight
   // gradient) runs alongside: wait for it at the end (pdl.cuh)
   pdl_enter_k(ST_CONV1W);
   if (p.tail) {  // a single-GPU whole step: the conv bucket's solver (solver.cuh)
     grid_barrier(p.bar, gridDim.x);
+    if (threadIdx.x == 0) st_mark(ST_RED_CONV, 0);  // (step trace: the first block past the barrier)
     solver_tail(p.sp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
   }
   ST_END(ST_CONV1W);

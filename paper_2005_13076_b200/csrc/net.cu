@@ -548,8 +548,10 @@ static pn_status allocate(pn_net* net) {
   int64_t poff = 0;
   for (auto& L : net->layers) {
     if (L.off < 0) continue;
-    // conv1's fused weight gradient is a light SIMT kernel: give it more
-    // CTAs (2 images each)
+    // conv1's fused weight gradient is a light SIMT kernel: CW_IMGS images per
+    // CTA (4 at batch 512: 128 CTAs, each beside a conv2 weight-gradient CTA;
+    // spreading them over all 148 SMs measured 12 us slower -- the grid barrier
+    // of the conv tail then waits for SMs other kernels hold)
     L.splits = (net->fused && &L == &net->layers[0]) ? (net->batch + CW_IMGS - 1) / CW_IMGS : kWgradSplits;
     // the tensor-core conv2 weight gradient runs 4 row tiles x splits CTAs: one per SM
     if (net->fused && net->tf32 && &L == &net->layers[2])  // conv2 weight gradient: one CTA per SM (4 row tiles)

@@ -12,7 +12,7 @@ import torch
 from paper_2005_13076_b200 import Net, make_sgd, synth
 
 NAMES = ["pack", "conv1+pool1", "conv2+pool2", "ip1 fwd", "ip2+loss", "loss_reduce", "ip2 bwd", "ip1 wgrad",
-         "ip1 dgrad", "reduce[ip]", "conv2 dgrad", "conv2 wgrad", "conv1 wgrad", "reduce[conv]", "solver", "solver (ip)"]
+         "ip1 dgrad", "reduce[ip]", "conv2 dgrad", "conv2 wgrad", "conv1 wgrad", "c1w barrier", "solver", "solver (ip)"]
 B = 512
 tf32 = (sys.argv[1] if len(sys.argv) > 1 else "tf32") == "tf32"
 net = Net("lenet", B, tf32=tf32)

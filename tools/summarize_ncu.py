@@ -22,9 +22,10 @@ os.makedirs(PROF, exist_ok=True)
 STAGE_OF = {"conv2_fwd_persistent": "conv2+pool2[tc]", "IpFwd": "ip1+relu[tc]", "IpWgrad": "ip1.wgrad[tc]",
             "IpDgradUnpool": "ip1.dgrad+unpool2[tc]", "reduce_partials_multi": "conv.bucket_reduce",
             "conv2_dgrad_persistent": "conv2.dgrad[tc]", "conv2_wgrad_persistent": "conv2.wgrad[tc]",
-            "lenet_conv1_wgrad": "conv1.wgrad", "lenet_conv1_pool1": "conv1+pool1",
+            "lenet_conv1_wgrad": ("conv1.wgrad", "conv1.wgrad+solver"), "lenet_conv1_pool1": "conv1+pool1",
+            "conv1_pool1_tc": "conv1+pool1[tc]",
             "lenet_ip2_loss": "ip2+softmax_loss", "lenet_ip2_bwd": "ip2.bwd+relu1.bwd",
-            "pack_weights": "wpack[tc]", "sgd_update_kernel": "sgd", "lenet_solver": "reduce+solver[tc]"}
+            "pack_weights": "wpack[tc]", "sgd_update_kernel": "sgd", "lenet_solver": ("ip.solver[tc]", "reduce+solver[tc]")}
 
 
 def launches(path):
@@ -104,7 +105,9 @@ for rep in sorted(glob.glob(os.path.join(OUT, "full_*.ncu-rep"))):
             v, u = d[x]
             v = float(v.replace(",", ""))
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-        traffic["tf32"][STAGE_OF.get(k, k)] = b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
+        names = STAGE_OF.get(k, k)
+        for nm in names if isinstance(names, tuple) else (names,):
+            traffic["tf32"][nm] = b("dram__bytes_read.sum") + b("dram__bytes_write.sum")
     except (KeyError, ValueError):
         pass
 open(os.path.join(PROF, f"{TAG}_kernels.md"), "w").write("\n".join(md) + "\n")
