@@ -630,9 +630,11 @@ __global__ void __launch_bounds__(320, C1W_MINB) lenet_conv1_wgrad(const __grid_
   // gradient) runs alongside: wait for it at the end (pdl.cuh)
   pdl_enter_k(ST_CONV1W);
   if (p.tail) {  // a single-GPU whole step: the conv bucket's solver (solver.cuh)
+    // (updating conv2's outputs before the barrier -- its partials are final
+    // after the PDL wait -- measured slower, statically or claimed: DESIGN §9)
     grid_barrier(p.bar, gridDim.x);
     if (threadIdx.x == 0) st_mark(ST_RED_CONV, 0);  // (step trace: the first block past the barrier)
-    solver_tail(p.sp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x);
+    solver_tail(p.sp, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, 0, p.sp.nseg);
   }
   ST_END(ST_CONV1W);
 }
