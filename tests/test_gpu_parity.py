@@ -176,12 +176,15 @@ def test_train_step_graph_equals_eager_and_is_deterministic(tf32, N):
                 net.sgd_update(sgd, it)
             else:
                 net.net_train_step(xd, yd, sgd, it, loss)
-        results.append([host(net.net_get_blob(k)) for k in params] + [loss.item()])
+        # + the head's outputs of the last step (TF32 graph: ip2 + softmax-loss
+        # + ip2's backward inside ip1's forward launch, tc.cu IpFwdHead)
+        head = [host(net.net_get_blob(k)) for k in ("ip2", "prob", "pred")] + [host(net.net_get_blob("ip1", 1))]
+        results.append([host(net.net_get_blob(k)) for k in params] + head + [np.float32(loss.item())])
         net.close()
-    for a, b in zip(results[0][:-1], results[1][:-1]):
-        assert_bitwise("eager vs graph", a, b)
-    for a, b in zip(results[1][:-1], results[2][:-1]):
-        assert_bitwise("graph rerun", a, b)
+    for a, b in zip(results[0], results[1]):
+        assert_bitwise("eager vs graph", np.asarray(a), np.asarray(b))
+    for a, b in zip(results[1], results[2]):
+        assert_bitwise("graph rerun", np.asarray(a), np.asarray(b))
 
 
 def test_solver_weight_copies_match_a_fresh_pack():
