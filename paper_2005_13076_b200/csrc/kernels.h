@@ -12,6 +12,8 @@ __global__ void reduce_partials(const __grid_constant__ ReduceP p);
 __global__ void reduce_partials_multi(const __grid_constant__ ReduceMultiP p);
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p);
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p);
+// planes per block of pool_bwd_plane (inputs per plane HW)
+__host__ __device__ inline int pool_bwd_planes(int HW) { return HW >= 1024 ? 1 : 1024 / HW; }
 template <int KH, int KW, int SH, int SW>
 __global__ void pool_bwd_plane(const __grid_constant__ PoolBwdP p);
 __global__ void gemm_generic(const __grid_constant__ GemmP p);

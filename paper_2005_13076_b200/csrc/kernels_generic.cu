@@ -377,21 +377,24 @@ __device__ __forceinline__ int qdiv(int a, int d) {
 // grid (positions of a plane / 256, planes): one output per thread, no
 // 64-bit or long integer division on the per-element path
 __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
+  // thread per output over all planes (grid-stride): small planes (cifar's
+  // 8x8 / 4x4 outputs) keep every lane busy
   pdl_enter();
-  const int HWp = p.Hp * p.Wp, planes = p.N * p.C;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= HWp) return;
-  const int a = qdiv(r, p.Wp), b = r - a * p.Wp;
-  int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
-  int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
-  const int size = (he - hs) * (we - ws);
-  hs = max(hs, 0);
-  ws = max(ws, 0);
-  he = min(he, p.H);
-  we = min(we, p.W);
-  for (int nc = blockIdx.y; nc < planes; nc += gridDim.y) {
+  const int HWp = p.Hp * p.Wp;
+  const long long total = (long long)p.N * p.C * HWp;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long nc = idx / HWp;
+    const int r = (int)(idx - nc * HWp);
+    const int a = qdiv(r, p.Wp), b = r - a * p.Wp;
+    int hs = a * p.sh - p.ph, ws = b * p.sw - p.pw;
+    int he = min(hs + p.kh, p.H + p.ph), we = min(ws + p.kw, p.W + p.pw);
+    const int size = (he - hs) * (we - ws);
+    hs = max(hs, 0);
+    ws = max(ws, 0);
+    he = min(he, p.H);
+    we = min(we, p.W);
     const float* xp = p.x + (size_t)nc * p.H * p.W;
-    const size_t idx = (size_t)nc * HWp + r;
     if (p.method == 0) {
       float best = __ldg(xp + hs * p.W + ws);
       int arg = hs * p.W + ws;
@@ -419,25 +422,29 @@ __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
 // in-place ReLU below the pool is back-propagated here too: its
 // backward stage disappears.
 __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
+  // thread per input over all planes (grid-stride); each gathers its windows
+  // in ascending output order (bit-exact with pool_bwd_plane and the scatter
+  // order)
   pdl_enter();
-  const int HW = p.H * p.W, planes = p.N * p.C;
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= HW) return;
-  const int h = qdiv(r, p.W), w = r - h * p.W;
-  const int a0 = (h + p.ph < p.kh) ? 0 : qdiv(h + p.ph - p.kh, p.sh) + 1;
-  const int a1 = min(qdiv(h + p.ph, p.sh), p.Hp - 1);
-  const int b0 = (w + p.pw < p.kw) ? 0 : qdiv(w + p.pw - p.kw, p.sw) + 1;
-  const int b1 = min(qdiv(w + p.pw, p.sw), p.Wp - 1);
-  for (int nc = blockIdx.y; nc < planes; nc += gridDim.y) {
-    const float* dyp = p.dy + (size_t)nc * p.Hp * p.Wp;
-    const size_t idx = (size_t)nc * HW + r;
+  const int HW = p.H * p.W, HWp = p.Hp * p.Wp;
+  const long long total = (long long)p.N * p.C * HW;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long nc = idx / HW;
+    const int r = (int)(idx - nc * HW);
+    const int h = qdiv(r, p.W), w = r - h * p.W;
+    const int a0 = (h + p.ph < p.kh) ? 0 : qdiv(h + p.ph - p.kh, p.sh) + 1;
+    const int a1 = min(qdiv(h + p.ph, p.sh), p.Hp - 1);
+    const int b0 = (w + p.pw < p.kw) ? 0 : qdiv(w + p.pw - p.kw, p.sw) + 1;
+    const int b1 = min(qdiv(w + p.pw, p.sw), p.Wp - 1);
+    const float* dyp = p.dy + (size_t)nc * HWp;
+    const float y = p.relu_y ? __ldg(p.relu_y + idx) : 1.f;
     float acc = 0.f;
     if (p.method == 0) {
-      const int32_t* mp = p.mask + (size_t)nc * p.Hp * p.Wp;
-      const int me = h * p.W + w;
+      const int32_t* mp = p.mask + (size_t)nc * HWp;
       for (int a = a0; a <= a1; ++a)
         for (int b = b0; b <= b1; ++b)
-          if (__ldg(mp + a * p.Wp + b) == me) acc += __ldg(dyp + a * p.Wp + b);
+          if (__ldg(mp + a * p.Wp + b) == r) acc += __ldg(dyp + a * p.Wp + b);
     } else {
       for (int a = a0; a <= a1; ++a)
         for (int b = b0; b <= b1; ++b) {
@@ -447,25 +454,27 @@ __global__ void pool_bwd_generic(const __grid_constant__ PoolBwdP p) {
           acc += __fdiv_rn(__ldg(dyp + a * p.Wp + b), (float)size);
         }
     }
-    if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) acc = 0.f;
+    if (p.relu_y && !(y > 0.f)) acc = 0.f;
     p.dx[idx] = acc;
   }
 }
 
-// Pool backward, one block per (n, c) plane staged in shared memory: the
-// plane's output gradients (divided by the window size for AVE, the same
-// IEEE quotient the oracle adds) and max-pool origins are read once,
-// coalesced; each input then gathers its <= ceil(k/s)^2 windows from shared
-// memory in ascending output order (bit-exact with the scatter order).
-// Window ranges per input row / column come from two small tables.
+// Pool backward, a block per group of P = max(1, 1024 / (H W)) consecutive
+// (n, c) planes staged in shared memory (small planes -- cifar's 8 x 8 and
+// 16 x 16 -- keep every thread busy): the planes' output gradients (divided
+// by the window size for AVE, the same IEEE quotient the oracle adds) and
+// max-pool origins are read once, coalesced; each input then gathers its
+// <= ceil(k/s)^2 windows from shared memory in ascending output order
+// (bit-exact with the scatter order).  Window ranges per input row /
+// column come from two small tables.
 template <int KH, int KW, int SH, int SW>  // window / stride fixed at compile time when nonzero
 __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ PoolBwdP p) {
   const int kh = KH ? KH : p.kh, kw = KW ? KW : p.kw, sh = SH ? SH : p.sh, sw = SW ? SW : p.sw;
   extern __shared__ __align__(16) uint8_t psm[];
-  const int HWp = p.Hp * p.Wp, HW = p.H * p.W;
+  const int HWp = p.Hp * p.Wp, HW = p.H * p.W, P = pool_bwd_planes(HW);
   float* d = reinterpret_cast<float*>(psm);
-  int* m = reinterpret_cast<int*>(d + HWp);
-  short2* arow = reinterpret_cast<short2*>(m + HWp);
+  int* m = reinterpret_cast<int*>(d + P * HWp);
+  short2* arow = reinterpret_cast<short2*>(m + P * HWp);
   short2* bcol = arow + p.H;
   for (int h = threadIdx.x; h < p.H; h += blockDim.x) {
     const int a0 = (h + p.ph < kh) ? 0 : (h + p.ph - kh) / sh + 1;
@@ -476,15 +485,17 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
     bcol[w] = make_short2((short)b0, (short)min((w + p.pw) / sw, p.Wp - 1));
   }
   pdl_enter();
-  for (int nc = blockIdx.x; nc < p.N * p.C; nc += gridDim.x) {
+  const long long NC = (long long)p.N * p.C;
+  for (long long nc0 = (long long)blockIdx.x * P; nc0 < NC; nc0 += (long long)gridDim.x * P) {
+    const int np = (int)min((long long)P, NC - nc0);
     __syncthreads();
-    const float* dyp = p.dy + (size_t)nc * HWp;
-    for (int o = threadIdx.x; o < HWp; o += blockDim.x) {
+    const float* dyp = p.dy + (size_t)nc0 * HWp;
+    for (int o = threadIdx.x; o < np * HWp; o += blockDim.x) {
       float v = __ldg(dyp + o);
       if (p.method == 0) {
-        m[o] = __ldg(p.mask + (size_t)nc * HWp + o);
+        m[o] = __ldg(p.mask + (size_t)nc0 * HWp + o);
       } else {
-        const int a = o / p.Wp, b = o - a * p.Wp;
+        const int ol = o % HWp, a = ol / p.Wp, b = ol - a * p.Wp;
         const int hs = a * sh - p.ph, ws = b * sw - p.pw;
         const int he = min(hs + kh, p.H + p.ph), we = min(ws + kw, p.W + p.pw);
         v = __fdiv_rn(v, (float)((he - hs) * (we - ws)));
@@ -493,18 +504,19 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
     }
     __syncthreads();
     // 4 inputs per thread per pass: their ReLU-output loads are issued together
-    for (int r0 = threadIdx.x; r0 < HW; r0 += 4 * blockDim.x) {
+    for (int r0 = threadIdx.x; r0 < np * HW; r0 += 4 * blockDim.x) {
       float y[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r0 + u * blockDim.x;
-        y[u] = (p.relu_y && r < HW) ? __ldg(p.relu_y + (size_t)nc * HW + r) : 1.f;
+        y[u] = (p.relu_y && r < np * HW) ? __ldg(p.relu_y + (size_t)nc0 * HW + r) : 1.f;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int r = r0 + u * blockDim.x;
-        if (r >= HW) break;
-        const int h = r / p.W, w = r - h * p.W;
+        if (r >= np * HW) break;
+        const int pi = r / HW, rl = r - pi * HW, h = rl / p.W, w = rl - h * p.W;
+        const int pb = pi * HWp;
         const short2 ar = arow[h], bc = bcol[w];
         float acc = 0.f;
         if (KH && SH && KW && SW) {  // at most ceil(k/s) windows per dimension: unrolled, ascending
@@ -515,19 +527,19 @@ __global__ void __launch_bounds__(256) pool_bwd_plane(const __grid_constant__ Po
             for (int ib = 0; ib < NB; ++ib) {
               const int a = ar.x + ia, b = bc.x + ib;
               if (a <= ar.y && b <= bc.y) {
-                const int o = a * p.Wp + b;
-                if (p.method != 0 || m[o] == r) acc += d[o];
+                const int o = pb + a * p.Wp + b;
+                if (p.method != 0 || m[o] == rl) acc += d[o];
               }
             }
         } else {
           for (int a = ar.x; a <= ar.y; ++a)
             for (int b = bc.x; b <= bc.y; ++b) {
-              const int o = a * p.Wp + b;
-              if (p.method != 0 || m[o] == r) acc += d[o];
+              const int o = pb + a * p.Wp + b;
+              if (p.method != 0 || m[o] == rl) acc += d[o];
             }
         }
         if (!(y[u] > 0.f)) acc = 0.f;
-        p.dx[(size_t)nc * HW + r] = acc;
+        p.dx[(size_t)nc0 * HW + r] = acc;
       }
     }
   }
@@ -612,7 +624,10 @@ __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ Gemm
   const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
   const int tm = (tid / 16) * 4, tn = (tid % 16) * 4;
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < p.K; k0 += 16) {
+  // K split over gridDim.z (splits > 1): slice z takes K tiles [nkt z / S, nkt (z+1) / S)
+  const int S = max(1, p.splits), nkt = (p.K + 15) / 16;
+  const int kt0 = (int)((long long)nkt * blockIdx.z / S), kt1 = (int)((long long)nkt * (blockIdx.z + 1) / S);
+  for (int k0 = 16 * kt0; k0 < 16 * kt1; k0 += 16) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       int e = tid + 256 * r;
@@ -640,6 +655,18 @@ __global__ void __launch_bounds__(256) gemm_generic(const __grid_constant__ Gemm
         for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
     }
     __syncthreads();
+  }
+  if (S > 1) {  // the raw partial of this slice (bias / ReLU in gemm_splitk_reduce)
+    float* out = p.part + (size_t)blockIdx.z * p.M * p.N;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int gm = m0 + tm + i;
+      if (gm >= p.M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (n0 + tn + j < p.N) out[(long long)gm * p.N + n0 + tn + j] = acc[i][j];
+    }
+    return;
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {

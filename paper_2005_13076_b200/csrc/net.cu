@@ -672,12 +672,15 @@ static void add(std::vector<Stage>& v, const std::string& name, const Launch& L,
 }
 
 // grads[w (and b)] = sum over the layer's split partials (fixed order)
+static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs,
+                             bool late = false);
+// a layer's split weight-gradient partials: 8 warps per 32 outputs, every
+// load of a pass in flight (reduce.cuh) -- hundreds of splits (stem_wgrad)
+// in two L2 round trips instead of one per 8 splits
 static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L, bool with_bias = true) {
   const int stride = (int)(L.wcount + L.bcount);
   ReduceP r{net->partials + L.part_off, net->grads + L.off, with_bias ? stride : (int)L.wcount, L.splits, stride};
-  Launch l;
-  l.set((const void*)reduce_partials, dim3(cdiv(r.n, 256)), dim3(256), 0, r);
-  add(v, L.name + ".wgrad_reduce", l);
+  add_reduce_multi(v, L.name + ".wgrad_reduce", {r});
 }
 
 static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const float* part, float* out, int n,
@@ -689,7 +692,7 @@ static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const
 }
 
 static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs,
-                             bool late = false) {
+                             bool late) {
   ReduceMultiP m{};
   m.late = late ? 1 : 0;
   m.nseg = (int)segs.size();
@@ -761,9 +764,7 @@ static Launch gemm_launch(const GemmP& g) {
   const int at = g.sak == 1 && g.sam % 4 == 0 ? 0 : (g.sam == 1 && g.sak % 4 == 0 ? 1 : -1);
   const int bt = g.sbk == 1 && g.sbn % 4 == 0 ? 0 : (g.sbn == 1 && g.sbk % 4 == 0 ? 1 : -1);
   if (at < 0 || bt < 0 || !al(g.A) || !al(g.B)) {
-    GemmP q = g;
-    q.splits = 1;
-    l.set((const void*)gemm_generic, dim3(cdiv(g.N, 64), cdiv(g.M, 64)), dim3(256), 0, q);
+    l.set((const void*)gemm_generic, dim3(cdiv(g.N, 64), cdiv(g.M, 64), std::max(1, g.splits)), dim3(256), 0, g);
     return l;
   }
   const void* f = at == 0 ? (bt == 0 ? (const void*)gemm_tiled<0, 0> : (const void*)gemm_tiled<0, 1>)
@@ -775,11 +776,13 @@ static Launch gemm_launch(const GemmP& g) {
 // K split for the register-tiled GEMM: about four 128-thread blocks per SM,
 // >= 4 K steps of 16 per slice, <= 8 slices (the fp32 plans' 64 x 32 tiles
 // alone leave most SMs with one block)
-static int gemm_splits(const pn_net* net, const GemmP& g) {
-  const long long blocks = (long long)cdiv(g.N, 32) * cdiv(g.M, 64);
+static int gemm_splits(const pn_net* net, const GemmP& g, bool generic) {
+  const long long blocks = generic ? (long long)cdiv(g.N, 64) * cdiv(g.M, 64) : (long long)cdiv(g.N, 32) * cdiv(g.M, 64);
   const int nkt = (g.K + 15) / 16;
-  int s = (int)std::min<long long>(8, std::max<long long>(1, 4LL * net->tc_sms / blocks));
-  s = std::max(1, std::min(s, nkt / 4));
+  // the generic 64 x 64 kernel (odd strides: e.g. a 10-output layer's weight
+  // gradient, one tile over K = batch) splits down to 2 K steps per slice
+  int s = (int)std::min<long long>(generic ? 16 : 8, std::max<long long>(1, 4LL * net->tc_sms / blocks));
+  s = std::max(1, std::min(s, nkt / (generic ? 2 : 4)));
   return getenv("PN_NO_SPLITK") ? 1 : s;
 }
 
@@ -789,8 +792,8 @@ static void add_gemm(pn_net* net, std::vector<Stage>& v, const std::string& name
                      std::function<void(Launch&, const StepArgs&)> patch = nullptr) {
   g.splits = 1;
   Launch l = gemm_launch(g);
-  if (l.func != (const void*)gemm_generic) {
-    const int s = gemm_splits(net, g);
+  {
+    const int s = gemm_splits(net, g, l.func == (const void*)gemm_generic);
     if (s > 1 && (size_t)s * g.M * g.N <= net->gemm_ws_floats) {
       g.splits = s;
       g.part = net->gemm_ws;
@@ -896,8 +899,8 @@ static void build_layerwise(pn_net* net) {
     } else if (L.type == L_POOL) {
       PoolFwdP p{x, top->data, top->m32, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
                  L.out[2], L.out[3], L.method};
-      l.set((const void*)pool_fwd_generic, dim3(cdiv(L.out[2] * L.out[3], 256), std::min(N * L.in[1], 65535)),
-            dim3(256), 0, p);
+      l.set((const void*)pool_fwd_generic,
+            dim3((unsigned)std::min<long long>(cdiv(top->count(), 256), 16LL * net->tc_sms)), dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l);
     } else if (L.type == L_IP && (long long)cdiv(L.Nout, 64) * cdiv(N, 64) < net->tc_sms) {
       // few output tiles: split-K rows kernel instead of the 64x64-tile GEMM
@@ -1024,15 +1027,17 @@ static void build_layerwise(pn_net* net) {
       PoolBwdP p{top.diff, top.m32, bot->diff, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
                  L.out[2], L.out[3], L.method, relu_y};
       // plane-staged kernel when a plane's gradients + origins fit shared memory
-      const size_t psmem = (size_t)L.out[2] * L.out[3] * 8 + (size_t)(L.in[2] + L.in[3]) * 4 + 16;
+      const int P = pool_bwd_planes(L.in[2] * L.in[3]);
+      const size_t psmem = (size_t)P * L.out[2] * L.out[3] * 8 + (size_t)(L.in[2] + L.in[3]) * 4 + 16;
       if (psmem <= 48 * 1024) {  // (3x3 / 2x2 stride-2 windows: compile-time geometry)
         const void* fn = (L.kh == 3 && L.kw == 3 && L.sh == 2 && L.sw == 2) ? (const void*)pool_bwd_plane<3, 3, 2, 2>
                          : (L.kh == 2 && L.kw == 2 && L.sh == 2 && L.sw == 2) ? (const void*)pool_bwd_plane<2, 2, 2, 2>
                                                                                : (const void*)pool_bwd_plane<0, 0, 0, 0>;
-        l.set(fn, dim3(std::min(N * L.in[1], 16 * net->tc_sms)), dim3(256), psmem, p);
+        l.set(fn, dim3((unsigned)std::min<long long>(cdiv((long long)N * L.in[1], P), 16LL * net->tc_sms)), dim3(256),
+              psmem, p);
       } else {
-        l.set((const void*)pool_bwd_generic, dim3(cdiv(L.in[2] * L.in[3], 256), std::min(N * L.in[1], 65535)),
-              dim3(256), 0, p);
+        l.set((const void*)pool_bwd_generic,
+              dim3((unsigned)std::min<long long>(cdiv(bot->count(), 256), 16LL * net->tc_sms)), dim3(256), 0, p);
       }
       add(bwd, L.name + (relu_y ? ".bwd+relu_bwd" : ".bwd"), l);
     } else if (L.type == L_IP) {
