@@ -124,7 +124,10 @@ def stage_work(name, N):
         "pool2.bwd": (0, N * (800 * 4 + 800 + 3200 * 4)),
         "conv2.dgrad": (2 * 64 * 500 * 50 * N, N * (3200 * 4 + 2880 * 4) + W2),
         "conv2.wgrad": (2 * 64 * 500 * 50 * N, N * (3200 * 4 + 2880 * 4) + 32 * W2),
-        "conv1.wgrad": (2 * 144 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1),
+        # conv1's weight gradient at the method's dense work (the
+        # im2col GEMM over the unpooled 24x24 gradient, 0.576 MFLOP/img); the
+        # kernel itself touches only pool1's routed quarter
+        "conv1.wgrad": (2 * 576 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1),
         "sgd": (0, 431080 * 4 * 5),
         # the fused solver: SGD's 20 B/param (its TF32 weight copies and the
         # conv partials it sums are this implementation's, not the method's)
@@ -133,7 +136,7 @@ def stage_work(name, N):
         "ip.solver": (0, 405510 * 4 * 5),       # the ip layers' parameters (side branch)
         "exchange+solver": (0, 431080 * 4 * 5),  # NEXT #1 (data parallel, fused): its local traffic
         # conv1's weight gradient + the conv bucket's solver tail (25,570 parameters)
-        "conv1.wgrad+solver": (2 * 144 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1 + 25570 * 4 * 5),
+        "conv1.wgrad+solver": (2 * 576 * 25 * 20 * N, N * (2880 * 4 + 2880 + 784 * 4) + 32 * W1 + 25570 * 4 * 5),
     }
     base = name.split("[")[0]
     if base.endswith(".wgrad_reduce"):
