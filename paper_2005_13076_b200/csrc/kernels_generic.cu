@@ -178,7 +178,7 @@ __global__ void __launch_bounds__(256) reduce_partials_multi(const __grid_consta
     float r = 0.f;
 #pragma unroll
     for (int q = 0; q < 8; ++q) r += sm[q][lane];
-    s.out[i] = r;
+    s.out[reduce_out_index(s, i)] = r;
   }
   if (p.late) pdl_enter_k(stk);
   ST_END(stk);

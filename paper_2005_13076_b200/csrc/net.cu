@@ -86,6 +86,7 @@ struct Layer {
   bool tc_conv = false, tc_dgrad = false, tma_fwd = false;
   bool stem = false;  // layerwise TF32 plan: conv -> MAX pool -> in-place ReLU fused (stem_fwd / stem_wgrad)
   bool tap_fwd = false, tap_dgrad = false;  // stride-1 tap GEMM over NHWC (tc_conv.cu)
+  bool wtap = false;  // weight gradient as a tap GEMM over shifted X boxes (tc_conv.cu conv_wgrad_taps)
   int cp_in = 0, cp_out = 0;                // NHWC channel pitches of x and of G
   float* wtap_f = nullptr;                  // [T][F][cp_in]
   float* wtap_d = nullptr;                  // [T][C][cp_out]
@@ -564,6 +565,8 @@ static pn_status allocate(pn_net* net) {
       L.tp = tcc::conv_tma_plan(net->batch, L.in[1], L.kh, L.kw, L.F, L.out[2], L.out[3], L.bias ? 1 : 0,
                                 net->tc_sms, L.G);
       L.splits = L.tp.wg_splits;
+      L.wtap = tcc::wgrad_taps_ok(L.in[1], L.in[3], L.out[3], L.F, L.kh, L.kw, L.sh, L.sw, L.G);
+      if (L.wtap) L.splits = tcc::wgrad_taps_splits(net->batch, L.out[2], L.out[3], L.in[1], L.F, L.kh, L.kw, net->tc_sms);
     }
     L.part_off = poff;
     poff += (int64_t)L.splits * (L.wcount + L.bcount);
@@ -597,6 +600,7 @@ static pn_status allocate(pn_net* net) {
       if (L.tap_dgrad) col_n = std::max(col_n, (size_t)net->batch * L.out[2] * L.out[3] * L.cp_out * L.G);
       if (L.tc_dgrad && !L.tap_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
       col_n = std::max(col_n, L.tp.col_floats);
+      if (L.wtap) col_n = std::max(col_n, (size_t)net->batch * L.in[1] * L.in[2] * L.in[3] * L.kw);  // X's shifted copies
       gm_n = std::max(gm_n, L.tp.g_floats);
     }
   }
@@ -680,6 +684,7 @@ static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, con
 static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L, bool with_bias = true) {
   const int stride = (int)(L.wcount + L.bcount);
   ReduceP r{net->partials + L.part_off, net->grads + L.off, with_bias ? stride : (int)L.wcount, L.splits, stride};
+  if (L.wtap) r.pw = (int)L.wcount, r.pk = L.in[1] * L.kh * L.kw, r.pc = L.in[1], r.pt = L.kh * L.kw;
   add_reduce_multi(v, L.name + ".wgrad_reduce", {r});
 }
 
@@ -970,17 +975,32 @@ static void build_layerwise(pn_net* net) {
       // weight gradient: colT = im2col(x)^T and Gm = G as [F][m] (TF32), then the
       // TMA-fed GEMM into split partials, then their fixed-order sum
       const int K = L.tp.K;
-      Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
-                  L.out[3], K, L.G * (K + (L.bias ? 1 : 0)), L.tp.pitch_m, L.G, K + (L.bias ? 1 : 0)};
-      add(bwd, L.name + ".wgrad.im2col[tc]", tcc::im2col_t_launch(ic),
-          isx ? [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; }
-              : std::function<void(Launch&, const StepArgs&)>());
-      GmP gp{top.diff, net->gm_ws, N, L.F, L.out[2] * L.out[3], L.tp.pitch_m};
-      add(bwd, L.name + ".wgrad.gm[tc]", tcc::gm_launch(gp));
       Launch lw;
-      if (!tcc::gemm_wgrad_launch(L.tp, net->col_ws, net->gm_ws, net->partials + L.part_off,
-                                  (int)(L.wcount + L.bcount), &lw))
-        net->tmap_failed = true;
+      bool ok;
+      if (L.wtap) {
+        // the tap GEMM over TMA-staged segments (no column matrix): X as kw
+        // column-shifted TF32 copies in the column workspace, G as Gw
+        tcc::ShiftCopyP xc{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kw, L.pw};
+        add(bwd, L.name + ".wgrad.xshift[tc]", tcc::shift_copies_launch(xc),
+            isx ? [](Launch& l, const StepArgs& a) { l.params<tcc::ShiftCopyP>().x = a.x; }
+                : std::function<void(Launch&, const StepArgs&)>());
+        tcc::GwP gp{top.diff, net->gm_ws, N, L.F, L.out[2], L.out[3]};
+        add(bwd, L.name + ".wgrad.gw[tc]", tcc::gw_launch(gp));
+        ok = tcc::wgrad_taps_launch(net->col_ws, net->gm_ws, N, L.in[1], L.in[2], L.in[3], L.out[2], L.out[3], L.F,
+                                    L.kh, L.kw, L.ph, L.pw, L.bias ? 1 : 0, net->partials + L.part_off,
+                                    (int)(L.wcount + L.bcount), L.splits, &lw);
+      } else {
+        Im2colTP ic{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw, L.out[2],
+                    L.out[3], K, L.G * (K + (L.bias ? 1 : 0)), L.tp.pitch_m, L.G, K + (L.bias ? 1 : 0)};
+        add(bwd, L.name + ".wgrad.im2col[tc]", tcc::im2col_t_launch(ic),
+            isx ? [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; }
+                : std::function<void(Launch&, const StepArgs&)>());
+        GmP gp{top.diff, net->gm_ws, N, L.F, L.out[2] * L.out[3], L.tp.pitch_m};
+        add(bwd, L.name + ".wgrad.gm[tc]", tcc::gm_launch(gp));
+        ok = tcc::gemm_wgrad_launch(L.tp, net->col_ws, net->gm_ws, net->partials + L.part_off,
+                                    (int)(L.wcount + L.bcount), &lw);
+      }
+      if (!ok) net->tmap_failed = true;
       add(bwd, L.name + ".wgrad[tc]", lw);
       add_reduce(net, bwd, L);
       if (bot && L.tap_dgrad) {

@@ -35,7 +35,15 @@ struct ReduceP {  // out[i] = sum_s part[s*stride + i], i < n (fixed order s = 0
   const float* part;
   float* out;
   int n, splits, stride;
+  // pc > 0: the partials of i < pw are a conv weight gradient in [f][t][c]
+  // order (tc_conv.cu conv_wgrad_taps); out index f*pk + c*pt + t (pk = C*T)
+  int pw, pk, pc, pt;
 };
+__host__ __device__ inline int reduce_out_index(const ReduceP& s, int i) {
+  if (s.pc <= 0 || i >= s.pw) return i;
+  const int f = i / s.pk, r = i - f * s.pk, t = r / s.pc, c = r - t * s.pc;
+  return f * s.pk + c * s.pt + t;
+}
 struct ReduceMultiP {  // several ReduceP segments in one launch
   ReduceP seg[6];
   int nseg, total;

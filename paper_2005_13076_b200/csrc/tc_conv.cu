@@ -34,6 +34,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "params.h"
@@ -828,6 +829,172 @@ Launch pack_plain_launch(const PackPlainP& p) {
   return l;
 }
 
+// ======================================= weight gradient as a tap GEMM
+// (tc_conv.h ConvWtapP).  The operands are TF32 copies laid out for it:
+//   Xs[n][y][j][c][x] = X[n][c][y][x + j - pw]  (kw column-shifted rows; a TMA
+//                       box must start 16-byte aligned in its innermost
+//                       dimension, so the column shift is baked into a copy)
+//   Gw[n][yo][f][xo]  = G[n][f][yo][xo]
+// A CTA takes whole segments of R output rows of one image.  Per segment ONE
+// 5-D TMA box brings input rows ys - ph .. ys + R - 1 + kh - ph (R + kh rows,
+// zero-filled outside the image) of every copy j and channel c, as blocks of C
+// rows x Wo TF32 (row = one swizzle span: Wo = 8 / 16 / 32 -> 32 / 64 / 128 B),
+// block index (row - ys + ph) kw + j; and one 4-D box brings G's R rows.
+// For output row q of the segment, tap t = (i, j) reads input row q + i, copy
+// j: block q kw + t -- so the 128-row accumulator tile m (taps 4m .. 4m+3 when
+// C = 32: rows = (tap slot, c)) is the contiguous run of blocks q kw + 4m ..,
+// one MMA descriptor, no copy per tap.  (Blocks past tap T - 1 are the next
+// row's: their rows of the accumulator are ignored.)  The bias gradient is one
+// more tile against a constant all-ones A operand.  TMEM: (MT + 1) x F
+// columns.  warp 0 lane 0 TMA (2 segment stages), warp 1 lane 0 MMA, warps 2-5
+// write the CTA's split partials at the end.
+__device__ __forceinline__ uint64_t make_desc_sw(uint32_t saddr, uint32_t sbo, uint64_t layout) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         ((uint64_t)1 << 46) | (layout << 61);
+}
+__device__ __forceinline__ void tma5d(uint32_t dst, const CUtensorMap* m, int c0, int c1, int c2, int c3, int c4,
+                                      uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], "
+      "[%7];" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(bar)
+      : "memory");
+}
+template <int WO>
+__global__ void __launch_bounds__(192, 1) conv_wgrad_taps(const __grid_constant__ ConvWtapP p) {
+  constexpr int ROWB = WO * 4;  // bytes of one operand row = the swizzle span
+  constexpr uint32_t SBO = 8 * ROWB;
+  constexpr uint64_t LAYOUT = WO == 32 ? 2 : (WO == 16 ? 4 : 6);  // SWIZZLE_128B / 64B / 32B
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t full[2], empty[2], done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t sbase = smem_u32(smem);
+  const uint32_t ones = sbase + 2 * p.stage_bytes;  // 128 rows of 1.0 (the bias tile's A)
+  const int BLK = p.C * ROWB, XB = p.x_bytes;        // one (row, copy) block; X part of a stage
+  const int s0 = (int)((long long)p.segs * blockIdx.x / gridDim.x);
+  const int ns = (int)((long long)p.segs * (blockIdx.x + 1) / gridDim.x) - s0;
+  if (tid == 0) {
+    for (int st = 0; st < 2; ++st) {
+      mbar_init(smem_u32(&full[st]), 1);
+      mbar_init(smem_u32(&empty[st]), 1);
+    }
+    mbar_init(smem_u32(&done), 1);
+    fence_barrier_init();
+    prefetch_tmap(&p.tx);
+    prefetch_tmap(&p.tg);
+  }
+  if (warp == 0) tmem_alloc(&tmem_base, p.tmem_cols);
+  for (int u = tid; u < 128 * ROWB / 16; u += blockDim.x) sts128(ones + 16 * u, f4(1.f, 1.f, 1.f, 1.f));
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tmem_base;
+  pdl_enter();
+  if (tid == 0) {  // TMA producer: one segment per stage
+    for (int g = 0; g < ns; ++g) {
+      const int st = g & 1, sg = s0 + g, n = sg / p.seg_per_img, ys = (sg - n * p.seg_per_img) * p.R;
+      if (g >= 2) mbar_wait(smem_u32(&empty[st]), ((g >> 1) - 1) & 1);
+      const uint32_t bar = smem_u32(&full[st]), As = sbase + st * p.stage_bytes;
+      mbar_expect_tx(bar, (uint32_t)p.stage_bytes);
+      tma5d(As, &p.tx, 0, 0, 0, ys - p.ph, n, bar);
+      tma4d(As + XB, &p.tg, 0, 0, ys, n, bar);
+    }
+  } else if (tid == 32) {  // MMA issuer
+    const uint32_t idesc = make_idesc(128, p.F);
+    for (int g = 0; g < ns; ++g) {
+      const int st = g & 1, sg = s0 + g, n = sg / p.seg_per_img, ys = (sg - n * p.seg_per_img) * p.R;
+      const int nq = min(p.R, p.Ho - ys);
+      mbar_wait(smem_u32(&full[st]), (g >> 1) & 1);
+      tc_fence_after();
+      const uint32_t As = sbase + st * p.stage_bytes, Bs = As + XB;
+      for (int q = 0; q < nq; ++q) {
+#pragma unroll
+        for (int k = 0; k < WO / 8; ++k) {
+          const uint32_t acc = (g | q | k) != 0;
+          const uint64_t bd = make_desc_sw(Bs + q * p.F * ROWB + k * 32, SBO, LAYOUT);
+          for (int m = 0; m < p.MT; ++m)
+            mma_tf32(tbase + m * p.F, make_desc_sw(As + (q * p.kw + m * p.TPT) * BLK + k * 32, SBO, LAYOUT), bd, idesc,
+                     acc);
+          mma_tf32(tbase + p.MT * p.F, make_desc_sw(ones + k * 32, SBO, LAYOUT), bd, idesc, acc);
+        }
+      }
+      mma_commit(smem_u32(&empty[st]));
+    }
+    if (ns > 0) mma_commit(smem_u32(&done));
+  } else if (warp >= 2) {  // epilogue: row r of tile m = (tap slot, channel)
+    const int quad = warp & 3, r = quad * 32 + lane, sl = r / p.C, ch = r - sl * p.C;
+    if (ns > 0) {
+      mbar_wait(smem_u32(&done), 0);
+      __syncwarp();
+      tc_fence_after();
+    }
+    float* pb = p.part + (size_t)blockIdx.x * p.pstride;
+    for (int m = 0; m <= p.MT; ++m) {
+      const int tap = m * p.TPT + sl;
+      for (int f0 = 0; f0 < p.F; f0 += 16) {
+        float v[16];
+        if (ns > 0) {
+          tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + m * p.F + f0, v);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = 0.f;
+        }
+        if (m < p.MT && tap < p.T) {  // [f][t][c] = [f][128 m + r]: a warp's 32 rows in one line
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pb[(size_t)(f0 + q) * p.K + m * 128 + r] = v[q];
+        } else if (m == p.MT && p.bias && r == 0) {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) pb[(size_t)p.F * p.K + f0 + q] = v[q];
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tbase, p.tmem_cols);
+}
+
+// Xs[n][y][j][c][x] = tf32(X[n][c][y][x + j - pw]) (0 outside the row): a
+// block per input row (n, y); W and C powers of two (shifts, no division)
+__global__ void __launch_bounds__(256) tf32_shift_copies(const __grid_constant__ ShiftCopyP p) {
+  pdl_enter();
+  const int lw = __ffs(p.W) - 1, lc = __ffs(p.C) - 1, per = p.kw << (lc + lw);
+  for (int row = blockIdx.x; row < p.N * p.H; row += gridDim.x) {
+    const int n = row / p.H, y = row - n * p.H;
+    const float* xr = p.x + ((size_t)n * p.C * p.H + y) * p.W;  // + c H W + x
+    float* o = p.out + (size_t)row * per;
+    for (int u = threadIdx.x; u < per; u += 256) {
+      const int x = u & (p.W - 1), c = (u >> lw) & (p.C - 1), j = u >> (lw + lc), xs = x + j - p.pw;
+      o[u] = (xs >= 0 && xs < p.W) ? tf32f(__ldg(xr + (size_t)c * p.H * p.W + xs)) : 0.f;
+    }
+  }
+}
+// Gw[n][yo][f][xo] = tf32(G[n][f][yo][xo]): a block per output row (n, yo)
+__global__ void __launch_bounds__(256) tf32_gw(const __grid_constant__ GwP p) {
+  pdl_enter();
+  const int lw = __ffs(p.Wo) - 1, per = p.F << lw;
+  for (int row = blockIdx.x; row < p.N * p.Ho; row += gridDim.x) {
+    const int n = row / p.Ho, y = row - n * p.Ho;
+    const float* g = p.g + ((size_t)n * p.F * p.Ho + y) * p.Wo;  // + f Ho Wo + x
+    float* o = p.out + (size_t)row * per;
+    for (int u = threadIdx.x; u < per; u += 256)
+      o[u] = tf32f(__ldg(g + (size_t)(u >> lw) * p.Ho * p.Wo + (u & (p.Wo - 1))));
+  }
+}
+Launch shift_copies_launch(const ShiftCopyP& p) {
+  Launch l;
+  l.set((const void*)tf32_shift_copies, dim3((unsigned)std::min(p.N * p.H, 148 * 8)), dim3(256), 0, p);
+  return l;
+}
+Launch gw_launch(const GwP& p) {
+  Launch l;
+  l.set((const void*)tf32_gw, dim3((unsigned)std::min(p.N * p.Ho, 148 * 8)), dim3(256), 0, p);
+  return l;
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -993,6 +1160,82 @@ Launch pack_taps_launch(const PackTapsP& p) {
   return l;
 }
 
+// ---- weight gradient as a tap GEMM
+static constexpr size_t kWtapSmemMax = 220 * 1024;
+static int wtap_mt(int C, int T) { return (T + 128 / C - 1) / (128 / C); }
+// rows per segment: the largest power of two <= Ho whose two stages (+ the
+// ones tile) fit shared memory; 0 if none
+static int wtap_rows(int C, int Ho, int Wo, int F, int kh, int kw, size_t* stage) {
+  for (int R = 1 << 5; R >= 1; R >>= 1) {
+    if (R > Ho && R > 1) continue;
+    const size_t st = (size_t)(R + kh) * kw * C * Wo * 4 + (size_t)R * F * Wo * 4;
+    if (2 * st + 128 * Wo * 4 <= kWtapSmemMax) {
+      if (stage) *stage = st;
+      return R;
+    }
+  }
+  return 0;
+}
+bool wgrad_taps_ok(int C, int W, int Wo, int F, int kh, int kw, int sh, int sw, int G) {
+  if (getenv("PN_NO_WTAP")) return false;
+  if (G != 1 || sh != 1 || sw != 1 || W != Wo) return false;
+  // (Wo = 8: 32-byte TMA rows -- measured slower than the materialised
+  // column matrix on cifar10_quick conv3, 43 vs 35 us with its copies)
+  if (!(C == 16 || C == 32 || C == 64 || C == 128) || !(Wo == 16 || Wo == 32)) return false;
+  if (F % 16 || F < 16 || F > 256) return false;
+  const int MT = wtap_mt(C, kh * kw);
+  return (MT + 1) * F <= 512 && wtap_rows(C, 1 << 5, Wo, F, kh, kw, nullptr) > 0;
+}
+// CTAs: at least 4 segments each (every CTA writes a whole (C T + 1) F
+// partial), at most one per SM
+int wgrad_taps_splits(int N, int Ho, int Wo, int C, int F, int kh, int kw, int sms) {
+  const int R = wtap_rows(C, Ho, Wo, F, kh, kw, nullptr), segs = N * ((Ho + R - 1) / R);
+  return std::max(1, std::min(sms, segs / 4));
+}
+
+bool wgrad_taps_launch(const float* xs, const float* gw, int N, int C, int H, int W, int Ho, int Wo, int F, int kh,
+                       int kw, int ph, int pw, int bias, float* part, int pstride, int splits, Launch* l) {
+  ConvWtapP p{};
+  EncodeTiledFn fn = encode_fn();
+  const CUtensorMapSwizzle sw = Wo == 32 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                         : (Wo == 16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  size_t stage = 0;
+  p.R = wtap_rows(C, Ho, Wo, F, kh, kw, &stage);
+  bool ok = fn != nullptr && p.R > 0;
+  {  // Xs [n][y][j][c][x]: box {Wo, C, kw, R + kh, 1}
+    cuuint64_t dims[5] = {(cuuint64_t)W, (cuuint64_t)C, (cuuint64_t)kw, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[4] = {(cuuint64_t)W * 4, (cuuint64_t)C * W * 4, (cuuint64_t)kw * C * W * 4,
+                             (cuuint64_t)H * kw * C * W * 4};
+    cuuint32_t box[5] = {(cuuint32_t)Wo, (cuuint32_t)C, (cuuint32_t)kw, (cuuint32_t)(p.R + kh), 1};
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    ok = ok && fn(&p.tx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)xs, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  {  // Gw [n][yo][f][xo]: box {Wo, F, R, 1}
+    cuuint64_t dims[4] = {(cuuint64_t)Wo, (cuuint64_t)F, (cuuint64_t)Ho, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)Wo * 4, (cuuint64_t)F * Wo * 4, (cuuint64_t)Ho * F * Wo * 4};
+    cuuint32_t box[4] = {(cuuint32_t)Wo, (cuuint32_t)F, (cuuint32_t)p.R, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    ok = ok && fn(&p.tg, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)gw, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+  }
+  p.part = part;
+  p.N = N, p.C = C, p.Ho = Ho, p.Wo = Wo, p.F = F, p.kh = kh, p.kw = kw, p.ph = ph, p.pw = pw;
+  p.T = kh * kw, p.K = C * kh * kw, p.bias = bias, p.pstride = pstride;
+  p.TPT = 128 / C;
+  p.MT = wtap_mt(C, p.T);
+  p.x_bytes = (p.R + kh) * kw * C * Wo * 4;
+  p.stage_bytes = (int)stage;
+  p.seg_per_img = (Ho + p.R - 1) / p.R;
+  p.segs = N * p.seg_per_img;
+  p.tmem_cols = pow2_at_least((p.MT + 1) * F, 32);
+  const void* f = Wo == 32 ? (const void*)conv_wgrad_taps<32>
+                           : (Wo == 16 ? (const void*)conv_wgrad_taps<16> : (const void*)conv_wgrad_taps<8>);
+  l->set(f, dim3(std::max(1, splits)), dim3(192), 1024 + 2 * stage + (size_t)128 * Wo * 4, p);
+  return ok;
+}
 cudaError_t setup(int max_nk) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -1013,6 +1256,8 @@ cudaError_t setup(int max_nk) {
     e = cudaFuncSetAttribute((const void*)tc_persistent<BN, TapOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
   SETT(32) SETT(64) SETT(128) SETT(192) SETT(256)
 #undef SETT
+  for (const void* f : {(const void*)conv_wgrad_taps<8>, (const void*)conv_wgrad_taps<16>, (const void*)conv_wgrad_taps<32>})
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kWtapSmemMax + 1024));
   return e;
 }
 

@@ -70,6 +70,38 @@ bool tap_launch(const float* nhwc, int N, int Hin, int Win, int cp, const float*
                 int kw, int ph, int pw, int sgn, int Ho, int Wo, int F, const float* bias, int relu,
                 const float* relu_y, float* out, Launch* l, int G = 1, int cpg = 0);
 Launch nhwc_launch(const NhwcP& p);
+
+// ---- weight gradient as a tap GEMM over TMA-staged segments (no im2col)
+// dW[f, c, i, j] = sum_{n, yo, xo} G[n, f, yo, xo] X[n, c, yo + i - ph, xo + j - pw]
+// for stride-1, ungrouped layers with W = Wo in {8, 16, 32}, C in {16, 32,
+// 64, 128}, F % 16 == 0 (F <= 256): the accumulator rows are (tap, c), the
+// contraction runs over output positions, one TMA box per segment of R output
+// rows brings every shifted input row it needs (tc_conv.cu conv_wgrad_taps).
+// Split partials per CTA (segments split evenly) in [f][tap][c] order, summed
+// and permuted to [f][c][tap] by wgrad_reduce (ReduceP pc/pk/pt).
+struct ShiftCopyP {  // out[n][y][j][c][x] = tf32(x[n][c][y][x + j - pw]), 0 outside
+  const float* x;
+  float* out;
+  int N, C, H, W, kw, pw;
+};
+struct GwP {  // out[n][yo][f][xo] = tf32(g[n][f][yo][xo])
+  const float* g;
+  float* out;
+  int N, F, Ho, Wo;
+};
+struct ConvWtapP {
+  CUtensorMap tx;  // Xs {W, C, kw, H, N}, box {Wo, C, kw, R + kh, 1}
+  CUtensorMap tg;  // Gw {Wo, F, Ho, N}, box {Wo, F, R, 1}
+  float* part;     // [splits][pstride]: f*K + t*C + c (t = tap; the reduce permutes); bias at F*K + f
+  int N, C, Ho, Wo, F, kh, kw, ph, pw, T, K, bias, pstride;
+  int MT, TPT, R, x_bytes, stage_bytes, seg_per_img, segs, tmem_cols;
+};
+Launch shift_copies_launch(const ShiftCopyP& p);
+Launch gw_launch(const GwP& p);
+bool wgrad_taps_ok(int C, int W, int Wo, int F, int kh, int kw, int sh, int sw, int G);
+int wgrad_taps_splits(int N, int Ho, int Wo, int C, int F, int kh, int kw, int sms);  // CTAs = split partials
+bool wgrad_taps_launch(const float* xs, const float* gw, int N, int C, int H, int W, int Ho, int Wo, int F, int kh,
+                       int kw, int ph, int pw, int bias, float* part, int pstride, int splits, Launch* l);
 Launch pack_taps_launch(const PackTapsP& p);
 }  // namespace tcc
 }  // namespace pn
