@@ -87,6 +87,11 @@ struct Layer {
   bool stem = false;  // layerwise TF32 plan: conv -> MAX pool -> in-place ReLU fused (stem_fwd / stem_wgrad)
   bool tap_fwd = false, tap_dgrad = false;  // stride-1 tap GEMM over NHWC (tc_conv.cu)
   bool wtap = false;  // weight gradient as a tap GEMM over shifted X boxes (tc_conv.cu conv_wgrad_taps)
+  // forward / data gradient over halo-staged channel planes (tc_plane.cu)
+  bool plane_f = false, plane_d = false;
+  tcc::PlanePlan pf{}, pd{};
+  float* wpl_f = nullptr;  // [T][Kq][F][4]
+  float* wpl_d = nullptr;  // [T][Kq][C][4]
   int cp_in = 0, cp_out = 0;                // NHWC channel pitches of x and of G
   float* wtap_f = nullptr;                  // [T][F][cp_in]
   float* wtap_d = nullptr;                  // [T][C][cp_out]
@@ -596,6 +601,10 @@ static pn_status allocate(pn_net* net) {
       else if (L.tma_fwd) TRY(net->alloc(&L.wf, (size_t)L.F * L.tp.kp));
       else TRY(net->alloc(&L.bfwd, (size_t)L.fwd_rows * L.fwd_nk * 32));
       if (L.tap_dgrad) TRY(net->alloc(&L.wtap_d, T * L.in[1] * L.cp_out));
+      if (L.plane_f) TRY(net->alloc(&L.wpl_f, T * L.pf.Kq * L.F * 4));
+      if (L.plane_d) TRY(net->alloc(&L.wpl_d, T * L.pd.Kq * L.in[1] * 4));
+      if (L.plane_f) col_n = std::max(col_n, (size_t)L.pf.tiles * L.pf.a_bytes / 4);
+      if (L.plane_d) col_n = std::max(col_n, (size_t)L.pd.tiles * L.pd.a_bytes / 4);
       if (L.tap_fwd) col_n = std::max(col_n, (size_t)net->batch * L.in[2] * L.in[3] * L.cp_in * L.G);
       if (L.tap_dgrad) col_n = std::max(col_n, (size_t)net->batch * L.out[2] * L.out[3] * L.cp_out * L.G);
       if (L.tc_dgrad && !L.tap_dgrad) TRY(net->alloc(&L.bdg, (size_t)L.dg_rows * L.dg_nk * 32));
@@ -851,7 +860,10 @@ static void build_layerwise(pn_net* net) {
       const bool relu = li + 1 < net->layers.size() && relu_in_conv[li + 1];
       const float* bias = L.bias ? net->params + L.off + L.wcount : nullptr;
       auto xpatch = [](Launch& l, const StepArgs& a) { l.params<Im2colTP>().x = a.x; };
-      if (L.tap_fwd) {
+      if (L.plane_f) {
+        add(fwd, L.name + ".wpack[tc]", tcc::plane_wpack_launch(L.pf, net->params + L.off, L.wpl_f, L.in[1], L.F, L.kh,
+                                                                L.kw, 0));
+      } else if (L.tap_fwd) {
         PackTapsP pk{net->params + L.off, L.wtap_f, L.F, L.in[1], L.kh, L.kw, L.cp_in, 0, L.G};
         add(fwd, L.name + ".wpack[tc]", tcc::pack_taps_launch(pk));
       } else if (L.tma_fwd) {
@@ -861,14 +873,26 @@ static void build_layerwise(pn_net* net) {
         ConvPackP pk{net->params + L.off, L.bfwd, L.F, L.in[1], L.kh, L.kw, L.fwd_rows, L.fwd_nk, 0};
         add(fwd, L.name + ".wpack[tc]", tcc::pack_launch(pk));
       }
-      if (L.tap_dgrad) {
+      if (L.plane_d) {
+        add(fwd, L.name + ".wpack_dgrad[tc]", tcc::plane_wpack_launch(L.pd, net->params + L.off, L.wpl_d, L.F,
+                                                                      L.in[1], L.kh, L.kw, 1));
+      } else if (L.tap_dgrad) {
         PackTapsP pd{net->params + L.off, L.wtap_d, L.F, L.in[1], L.kh, L.kw, L.cp_out, 1, L.G};
         add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_taps_launch(pd));
       } else if (L.tc_dgrad) {
         ConvPackP pd{net->params + L.off, L.bdg, L.F, L.in[1], L.kh, L.kw, L.dg_rows, L.dg_nk, 1};
         add(fwd, L.name + ".wpack_dgrad[tc]", tcc::pack_launch(pd));
       }
-      if (L.tap_fwd) {
+      if (L.plane_f) {
+        // stride 1: halo-staged channel planes (TF32), then the plane tap GEMM
+        add(fwd, L.name + ".planes[tc]",
+            tcc::plane_pack_launch(L.pf, x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.ph, L.pw),
+            isx ? [](Launch& l, const StepArgs& a) { l.params<tcc::PlanePackP>().src = a.x; }
+                : std::function<void(Launch&, const StepArgs&)>());
+        add(fwd, L.name + (relu ? ".fwd+relu[tc]" : ".fwd[tc]"),
+            tcc::plane_conv_launch(L.pf, net->col_ws, L.wpl_f, bias, nullptr, top->data, N, L.out[2], L.out[3], L.F,
+                                   L.kh, L.kw, relu ? 1 : 0, net->tc_sms));
+      } else if (L.tap_fwd) {
         // stride 1: x to NHWC (TF32), then the tap GEMM (no column matrix)
         NhwcP nh{x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.cp_in * L.G, L.G, L.cp_in};
         add(fwd, L.name + ".nhwc[tc]", tcc::nhwc_launch(nh),
@@ -1003,7 +1027,16 @@ static void build_layerwise(pn_net* net) {
       if (!ok) net->tmap_failed = true;
       add(bwd, L.name + ".wgrad[tc]", lw);
       add_reduce(net, bwd, L);
-      if (bot && L.tap_dgrad) {
+      if (bot && L.plane_d) {
+        // data gradient as the convolution of G with the flipped,
+        // channel-transposed filter (pad k - 1 - p) over halo-staged planes of G
+        add(bwd, L.name + ".dgrad.planes[tc]",
+            tcc::plane_pack_launch(L.pd, top.diff, net->col_ws, N, L.F, L.out[2], L.out[3], L.kh - 1 - L.ph,
+                                   L.kw - 1 - L.pw));
+        add(bwd, L.name + (relu_y ? ".dgrad+relu_bwd[tc]" : ".dgrad[tc]"),
+            tcc::plane_conv_launch(L.pd, net->col_ws, L.wpl_d, nullptr, relu_y, bot->diff, N, L.in[2], L.in[3],
+                                   L.in[1], L.kh, L.kw, 0, net->tc_sms));
+      } else if (bot && L.tap_dgrad) {
         // data gradient: col2im(W^T G) = sum over taps of G shifted
         // by (p - i, p - j) times W_t^T -- G to NHWC, then the tap GEMM
         NhwcP nh{top.diff, net->col_ws, N, L.F, L.out[2], L.out[3], L.cp_out * L.G, L.G, L.cp_out};
@@ -1692,6 +1725,10 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
       }
       L.tc_dgrad = L.bottom != net->input_name && L.sh == 1 && L.sw == 1 && L.ph < L.kh && L.pw < L.kw;
       L.tap_dgrad = L.tc_dgrad && Fg >= 16;
+      L.plane_f = L.tap_fwd && L.G == 1 &&
+                  tcc::plane_plan(batch, L.in[1], L.out[2], L.out[3], L.F, L.kh, L.kw, &L.pf);
+      L.plane_d = L.tap_dgrad && L.G == 1 &&
+                  tcc::plane_plan(batch, L.F, L.in[2], L.in[3], L.in[1], L.kh, L.kw, &L.pd);
       if (L.tc_dgrad && !L.tap_dgrad) {
         L.dg_rows = tcc::fwd_rows_pad(L.in[1]);
         L.dg_nk = (L.F * L.kh * L.kw + 31) / 32;

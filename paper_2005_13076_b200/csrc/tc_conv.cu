@@ -1256,6 +1256,7 @@ cudaError_t setup(int max_nk) {
     e = cudaFuncSetAttribute((const void*)tc_persistent<BN, TapOp>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tw_smem<BN>());
   SETT(32) SETT(64) SETT(128) SETT(192) SETT(256)
 #undef SETT
+  if (e == cudaSuccess) e = plane_setup();
   for (const void* f : {(const void*)conv_wgrad_taps<8>, (const void*)conv_wgrad_taps<16>, (const void*)conv_wgrad_taps<32>})
     if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kWtapSmemMax + 1024));
   return e;

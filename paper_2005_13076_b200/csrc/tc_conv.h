@@ -103,5 +103,40 @@ int wgrad_taps_splits(int N, int Ho, int Wo, int C, int F, int kh, int kw, int s
 bool wgrad_taps_launch(const float* xs, const float* gw, int N, int C, int H, int W, int Ho, int Wo, int F, int kh,
                        int kw, int ph, int pw, int bias, float* part, int pstride, int splits, Launch* l);
 Launch pack_taps_launch(const PackTapsP& p);
+
+// ---- stride-1 convolution over halo-staged 4-channel planes (tc_plane.cu):
+// forward (+bias, ReLU) and data gradient (+ the in-place ReLU's mask)
+struct PlanePlan {
+  int TY, TN, HY, HX, Kq, a_bytes, w_bytes, stages, tiles_x, tiles_y, tiles;
+  size_t smem;
+};
+struct PlanePackP {  // A blocks [tile][cq][HY][TN][HX][4] (TF32)
+  const float* src;
+  float* out;
+  int N, C, H, W, ph, pw, Kq, HY, HX, TY, TN, tiles, tiles_x, tiles_y;
+};
+struct PlaneWpackP {  // B [t][cq][o][4] (TF32); mode 0 forward, 1 data gradient
+  const float* w;
+  float* out;
+  int Cin, Nout, kh, kw, Kq, mode;
+};
+struct PlaneConvP {
+  const float* src;     // A blocks
+  const float* wts;     // B
+  const float* bias;    // forward bias (nullable)
+  const float* relu_y;  // data gradient: the in-place ReLU's output (nullable)
+  float* out;           // NCHW [N][Nout][Ho][Wo]
+  int N, Ho, Wo, Nout, Kq, kh, kw, TY, TN, HY, HX, tiles, tiles_x, tiles_y, a_bytes, w_bytes, relu, stages;
+  int tmem_cols;
+};
+bool plane_plan(int N, int Cin, int Ho, int Wo, int Nout, int kh, int kw, PlanePlan* pl);
+Launch plane_pack_launch(const PlanePlan& pl, const float* src, float* out, int N, int C, int H, int W, int ph,
+                         int pw);
+Launch plane_wpack_launch(const PlanePlan& pl, const float* w, float* out, int Cin, int Nout, int kh, int kw,
+                          int mode);
+Launch plane_conv_launch(const PlanePlan& pl, const float* src, const float* wts, const float* bias,
+                         const float* relu_y, float* out, int N, int Ho, int Wo, int Nout, int kh, int kw, int relu,
+                         int sms);
+cudaError_t plane_setup();
 }  // namespace tcc
 }  // namespace pn
