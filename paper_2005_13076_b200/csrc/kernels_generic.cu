@@ -406,13 +406,14 @@ __global__ void pool_fwd_generic(const __grid_constant__ PoolFwdP p) {
             arg = h * p.W + w;
           }
         }
-      p.y[idx] = best;
+      p.y[idx] = p.relu ? fmaxf(best, 0.f) : best;
       p.mask[idx] = arg;
     } else {
       float acc = 0.f;
       for (int h = hs; h < he; ++h)
         for (int w = ws; w < we; ++w) acc += __ldg(xp + h * p.W + w);
-      p.y[idx] = __fdiv_rn(acc, (float)size);
+      const float v = __fdiv_rn(acc, (float)size);
+      p.y[idx] = p.relu ? fmaxf(v, 0.f) : v;
     }
   }
 }

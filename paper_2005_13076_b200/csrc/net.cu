@@ -85,6 +85,10 @@ struct Layer {
   // gradient as an implicit GEMM over gathered G (swizzled W' image bdg)
   bool tc_conv = false, tc_dgrad = false, tma_fwd = false;
   bool stem = false;  // layerwise TF32 plan: conv -> MAX pool -> in-place ReLU fused (stem_fwd / stem_wgrad)
+  // the stem's forward as the plane tap GEMM (TF32) + pooling with the ReLU
+  // fused (conv output in stem_conv), its backward still stem_wgrad
+  bool stem_plane = false;
+  float* stem_conv = nullptr;
   bool tap_fwd = false, tap_dgrad = false;  // stride-1 tap GEMM over NHWC (tc_conv.cu)
   bool wtap = false;  // weight gradient as a tap GEMM over shifted X boxes (tc_conv.cu conv_wgrad_taps)
   // forward / data gradient over halo-staged channel planes (tc_plane.cu)
@@ -594,6 +598,12 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->part_db2, (size_t)tc::db2_partials(net->batch) * 50));
   }
   size_t col_n = 0, gm_n = 0;
+  if (net->layers[0].stem_plane) {
+    Layer& S0 = net->layers[0];
+    TRY(net->alloc(&S0.wpl_f, (size_t)S0.kh * S0.kw * S0.pf.Kq * S0.F * 4));
+    TRY(net->alloc(&S0.stem_conv, (size_t)net->batch * S0.F * S0.out[2] * S0.out[3]));
+    col_n = std::max(col_n, (size_t)S0.pf.tiles * S0.pf.a_bytes / 4);
+  }
   for (auto& L : net->layers) {  // layerwise TF32 plan: packed conv weight images, wgrad workspaces
     if (L.tc_conv) {
       const size_t T = (size_t)L.kh * L.kw;
@@ -845,7 +855,26 @@ static void build_layerwise(pn_net* net) {
     Launch l;
     if (relu_in_conv[li]) continue;
     if (stem && li <= 2) {  // conv -> MAX pool -> ReLU in one kernel (is_stem)
-      if (li == 0) {
+      if (li == 0 && L.stem_plane) {
+        // conv1 on the tensor cores (plane tap GEMM, + bias), then pool1 with
+        // relu1 fused (the mask is the pooling's, as stem_wgrad reads it)
+        const Layer& Pl = net->layers[1];
+        Blob& py = net->blobs[net->blob(Pl.top)];
+        add(fwd, L.name + ".wpack[tc]", tcc::plane_wpack_launch(L.pf, net->params + L.off, L.wpl_f, L.in[1], L.F, L.kh,
+                                                                L.kw, 0));
+        add(fwd, L.name + ".planes[tc]",
+            tcc::plane_pack_launch(L.pf, x, net->col_ws, N, L.in[1], L.in[2], L.in[3], L.ph, L.pw),
+            [](Launch& l, const StepArgs& a) { l.params<tcc::PlanePackP>().src = a.x; });
+        add(fwd, L.name + ".fwd[tc]",
+            tcc::plane_conv_launch(L.pf, net->col_ws, L.wpl_f, L.bias ? net->params + L.off + L.wcount : nullptr,
+                                   nullptr, L.stem_conv, N, L.out[2], L.out[3], L.F, L.kh, L.kw, 0, net->tc_sms));
+        PoolFwdP pp{L.stem_conv, py.data, py.m32, N, L.F, L.out[2], L.out[3], Pl.kh, Pl.kw, Pl.sh, Pl.sw, Pl.ph, Pl.pw,
+                    Pl.out[2], Pl.out[3], 0, 1};
+        Launch lp;
+        lp.set((const void*)pool_fwd_generic,
+               dim3((unsigned)std::min<long long>(cdiv(py.count(), 256), 16LL * net->tc_sms)), dim3(256), 0, pp);
+        add(fwd, Pl.name + "+" + net->layers[2].name + ".fwd", lp);
+      } else if (li == 0) {
         l.set((const void*)stem_fwd, dim3(cdiv(L.F, STEM_FG_HOST), N), dim3(256), stem_fwd_smem(L), stem_params(net));
         add(fwd, L.name + "+" + net->layers[1].name + "+" + net->layers[2].name + ".fwd", l,
             [](Launch& l, const StepArgs& a) { l.params<StemP>().x = a.x; });
@@ -927,7 +956,7 @@ static void build_layerwise(pn_net* net) {
                                        : std::function<void(Launch&, const StepArgs&)>());
     } else if (L.type == L_POOL) {
       PoolFwdP p{x, top->data, top->m32, N, L.in[1], L.in[2], L.in[3], L.kh, L.kw, L.sh, L.sw, L.ph, L.pw,
-                 L.out[2], L.out[3], L.method};
+                 L.out[2], L.out[3], L.method, 0};
       l.set((const void*)pool_fwd_generic,
             dim3((unsigned)std::min<long long>(cdiv(top->count(), 256), 16LL * net->tc_sms)), dim3(256), 0, p);
       add(fwd, L.name + ".fwd", l);
@@ -1702,6 +1731,11 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
     // (tc_conv.cu); the data gradient needs stride 1 and pad < kernel (else
     // the generic fp32 kernel computes it)
     net->layers[0].stem = is_stem(net.get()) && !getenv("PN_NO_STEM");
+    {
+      Layer& S0 = net->layers[0];
+      S0.stem_plane = S0.stem && !getenv("PN_NO_STEM_PLANE") && S0.sh == 1 && S0.sw == 1 && S0.G == 1 &&
+                      tcc::plane_plan(batch, S0.in[1], S0.out[2], S0.out[3], S0.F, S0.kh, S0.kw, &S0.pf);
+    }
     for (auto& L : net->layers) {
       if (L.type != L_CONV || L.stem) continue;
       const int Cg = L.in[1] / L.G, Fg = L.F / L.G;

@@ -85,6 +85,7 @@ struct PoolFwdP {  // P:215-220; S:357-365 (method 0 MAX, 1 AVE)
   float* y;
   int32_t* mask;
   int N, C, H, W, kh, kw, sh, sw, ph, pw, Hp, Wp, method;
+  int relu;  // 1: an in-place ReLU follows (y = max(pooled, 0); the mask is the pooling's)
 };
 struct PoolBwdP {  // P:220-222; gather form, ascending output order
   const float* dy;

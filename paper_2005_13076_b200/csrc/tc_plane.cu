@@ -264,7 +264,8 @@ Launch plane_conv_launch(const PlanePlan& pl, const float* src, const float* wts
   PlaneConvP p{src, wts, bias, relu_y, out, N, Ho, Wo, Nout, pl.Kq, kh, kw, pl.TY, pl.TN, pl.HY, pl.HX,
                pl.tiles, pl.tiles_x, pl.tiles_y, pl.a_bytes, pl.w_bytes, relu, pl.stages, pow2_ge(2 * Nout, 32)};
   Launch l;
-  const void* f = (kh == 5 && kw == 5 && pl.Kq == 8)   ? (const void*)conv_plane_taps<5, 5, 4>
+  const void* f = (kh == 5 && kw == 5 && pl.Kq == 2)   ? (const void*)conv_plane_taps<5, 5, 1>
+                  : (kh == 5 && kw == 5 && pl.Kq == 8)  ? (const void*)conv_plane_taps<5, 5, 4>
                   : (kh == 5 && kw == 5 && pl.Kq == 16) ? (const void*)conv_plane_taps<5, 5, 8>
                   : (kh == 3 && kw == 3 && pl.Kq == 8)  ? (const void*)conv_plane_taps<3, 3, 4>
                                                         : (const void*)conv_plane_taps<0, 0, 0>;
@@ -273,7 +274,7 @@ Launch plane_conv_launch(const PlanePlan& pl, const float* src, const float* wts
 }
 cudaError_t plane_setup() {
   cudaError_t e = cudaSuccess;
-  for (const void* f : {(const void*)conv_plane_taps<5, 5, 4>, (const void*)conv_plane_taps<5, 5, 8>,
+  for (const void* f : {(const void*)conv_plane_taps<5, 5, 1>, (const void*)conv_plane_taps<5, 5, 4>, (const void*)conv_plane_taps<5, 5, 8>,
                         (const void*)conv_plane_taps<3, 3, 4>, (const void*)conv_plane_taps<0, 0, 0>})
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kPlaneSmemMax + 1024));

@@ -116,7 +116,13 @@ def test_conv_tc_teacher_forced(case):
         name = L["name"]
         stem = [st for st in fwd if st.startswith(name + "+")]
         if stem:  # conv -> MAX pool -> ReLU fused (net.cu is_stem): checked as one unit
-            check_stem(net, ref, out, gref, L, stem[0], xd, yd)
+            check_stem(net, ref, out, gref, L, stem, xd, yd, RTOL[False])
+            continue
+        P = [M for M in ref.layers if M["bottom"] == L["top"]]
+        pool_relu = [st for st in fwd if P and st.startswith(P[0]["name"] + "+") and st.endswith(".fwd")]
+        if pool_relu:  # the stem's forward on the tensor cores (plane tap GEMM) + pooling with the ReLU fused
+            stages = [st for st in fwd if st.startswith(name + ".")] + pool_relu
+            check_stem(net, ref, out, gref, L, stages, xd, yd, RTOL[True])
             continue
         fst = [st for st in fwd if st.startswith(name + ".fwd")]
         on_tc = fst and fst[0].endswith("[tc]")
@@ -161,20 +167,24 @@ def test_conv_tc_teacher_forced(case):
     net.close()
 
 
-def check_stem(net, ref, out, gref, L, stage, xd, yd):
-    """The layerwise plan's stem (cifar10_quick conv1 -> pool1 -> relu1, one
-    fp32 kernel each way): the pooled, ReLU'd output against the oracle's relu1
-    output per element (scale: the conv's |terms| through the max), the pool
-    origins bit-exact up to listed near-ties, and the weight / bias gradients
-    from the oracle's pooled gradient and origins."""
+def check_stem(net, ref, out, gref, L, stages, xd, yd, fwd_rtol):
+    """The layerwise plan's stem (cifar10_quick conv1 -> pool1 -> relu1; the
+    forward one fp32 kernel, or the TF32 plane tap GEMM + pooling with the
+    ReLU fused -- fwd_rtol the class of its contraction; the backward one fp32
+    kernel): the pooled, ReLU'd output against the oracle's relu1 output per
+    element (scale: the conv's |terms| through the max), the pool origins
+    bit-exact up to listed near-ties, and the weight / bias gradients from the
+    oracle's pooled gradient and origins."""
     P = [M for M in ref.layers if M["bottom"] == L["top"]][0]
     R = [M for M in ref.layers if M["type"] == "ReLU" and M["bottom"] == P["top"]][0]
-    run_stage(net, 0, stage, xd, yd)
+    for st in stages:
+        run_stage(net, 0, st, xd, yd)
+    stage = "+".join(stages)
     S = out["scales"][L["name"]]
     Sp = capi.pool_fwd(S, capi.MAX, P["k"], P["s"], P["p"])[0]  # the largest conv scale of each window
-    assert_close(f"{stage}", host(net.net_get_blob(P["top"])), out["blobs"][R["name"]], Sp, RTOL[False])
+    assert_close(f"{stage}", host(net.net_get_blob(P["top"])), out["blobs"][R["name"]], Sp, fwd_rtol)
     check_mask(f"{stage} mask", host(net.net_get_blob(P["top"], PN_MASK)), out["masks"][P["name"]],
-               out["blobs"][L["name"]], S, tuple(L["out_shape"][2:]), P["k"][0], P["s"][0], P["p"][0], RTOL[False])
+               out["blobs"][L["name"]], S, tuple(L["out_shape"][2:]), P["k"][0], P["s"][0], P["p"][0], fwd_rtol)
     net.net_put_blob(P["top"], gref["diffs"][R["name"]].astype(np.float32), PN_DIFF)
     net.net_put_blob(P["top"], out["masks"][P["name"]], PN_MASK)
     for st in net.stages(1):
