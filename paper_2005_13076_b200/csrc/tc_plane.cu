@@ -40,28 +40,29 @@ constexpr size_t kPlaneSmemMax = 220 * 1024;
 
 // A blocks: element (tile, cq, hy, n, hx, c4) = tf32(src[n0 + n][4 cq + c4][y0 + hy - ph][x0 + hx - pw])
 __global__ void __launch_bounds__(256) plane_pack(const __grid_constant__ PlanePackP p) {
-  // a block per tile (grid-stride), 32-bit index arithmetic inside it
+  // a block per tile (grid-stride); thread = one halo position (hy, n, hx),
+  // all its channel quads (loads in flight together, one float4 store per plane)
   pdl_enter();
-  const int per_tile = p.Kq * p.HY * p.TN * p.HX;  // float4 per block
+  const int pos = p.HY * p.TN * p.HX, HW = p.H * p.W;
   for (int tile = blockIdx.x; tile < p.tiles; tile += gridDim.x) {
     const int tx = tile % p.tiles_x, t2 = tile / p.tiles_x, ty = t2 % p.tiles_y, nb = t2 / p.tiles_y;
-    float4* o = reinterpret_cast<float4*>(p.out) + (size_t)tile * per_tile;
-    for (int r0 = threadIdx.x; r0 < per_tile; r0 += 256) {
-      int r = r0;
-      const int hx = r % p.HX;
-      r /= p.HX;
-      const int nn = r % p.TN;
-      r /= p.TN;
-      const int hy = r % p.HY, cq = r / p.HY;
+    float4* o = reinterpret_cast<float4*>(p.out) + (size_t)tile * p.Kq * pos;
+    for (int r = threadIdx.x; r < pos; r += 256) {
+      const int hx = r % p.HX, r2 = r / p.HX, nn = r2 % p.TN, hy = r2 / p.TN;
       const int n = nb * p.TN + nn, y = ty * p.TY + hy - p.ph, x = tx * 8 + hx - p.pw;
-      float v[4] = {0.f, 0.f, 0.f, 0.f};
-      if (n < p.N && y >= 0 && y < p.H && x >= 0 && x < p.W) {
-        const float* s = p.src + (((size_t)n * p.C) * p.H + y) * p.W + x;
+      const bool in = n < p.N && y >= 0 && y < p.H && x >= 0 && x < p.W;
+      const float* s = p.src + (((size_t)n * p.C) * p.H + y) * p.W + x;
+      for (int cq0 = 0; cq0 < p.Kq; cq0 += 4) {
+        float v[16];
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (4 * cq + q < p.C) v[q] = tf32f(__ldg(s + (size_t)(4 * cq + q) * p.H * p.W));
+        for (int q = 0; q < 16; ++q) {
+          const int c = 4 * cq0 + q;
+          v[q] = (in && c < p.C) ? tf32f(__ldg(s + (size_t)c * HW)) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (cq0 + k < p.Kq) o[(size_t)(cq0 + k) * pos + r] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
       }
-      o[r0] = make_float4(v[0], v[1], v[2], v[3]);
     }
   }
 }
@@ -101,7 +102,9 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
   const uint32_t W_s = smem_u32(smem), A_s = W_s + (uint32_t)((p.w_bytes + 1023) & ~1023);
   __shared__ __align__(8) uint64_t wbar, full[PL_MAX_STAGES], empty[PL_MAX_STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
+  __shared__ float bias_s[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, S = p.stages;
+  for (int o = tid; o < p.Nout; o += blockDim.x) bias_s[o] = p.bias ? __ldg(p.bias + o) : 0.f;
   const int mine = p.tiles > (int)blockIdx.x ? (p.tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
   if (tid == 0) {
     mbar_init(smem_u32(&wbar), 1);
@@ -193,17 +196,19 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
       tc_fence_after();
       const size_t HW = (size_t)p.Ho * p.Wo, base = (size_t)n * p.Nout * HW + (size_t)oy * p.Wo + ox;
       for (int o0 = 0; o0 < p.Nout; o0 += 16) {
-        float v[16];
-        tmem_ld16(tbase + ((uint32_t)(quad * 32) << 16) + b * p.Nout + o0, v);
+        float v[16], m[16];
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + b * p.Nout + o0, v);
+        // the in-place ReLU's outputs of these 16 channels: every load in flight together
+#pragma unroll
+        for (int q = 0; q < 16; ++q) m[q] = (p.relu_y && live) ? __ldg(p.relu_y + base + (size_t)(o0 + q) * HW) : 1.f;
+        tmem_ld_wait();
         if (!live) continue;
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-          const size_t idx = base + (size_t)(o0 + q) * HW;
-          float o = v[q];
-          if (p.bias) o += __ldg(p.bias + o0 + q);
+          float o = v[q] + bias_s[o0 + q];
           if (p.relu) o = fmaxf(o, 0.f);
-          if (p.relu_y && !(__ldg(p.relu_y + idx) > 0.f)) o = 0.f;
-          p.out[idx] = o;
+          if (!(m[q] > 0.f)) o = 0.f;
+          p.out[base + (size_t)(o0 + q) * HW] = o;
         }
       }
       tc_fence_before();
