@@ -61,7 +61,15 @@ ALEX_SMALL_GROUPED = conv_spec(3, 67, 67, [("conv1", 96, 11, 4, 0, (3, 2)), ("co
 GROUPED_ODD = conv_spec(6, 11, 9, [("ga", 48, 3, 1, 1), ("gb", 48, 3, 1, 1), ("gc", 36, 3, 2, 1)],
                         groups={"gb": 3, "gc": 2})
 
+# the round-2 stride-1 engines off cifar10_quick's shapes: pb runs the plane
+# tap GEMM's runtime-geometry path (forward, Kc = 16) and its unrolled one
+# (data gradient), and the tap weight gradient with 8 taps per accumulator
+# tile (C = 16); pc (8 x 8 maps) the plane tiles of two images (TN = 2) over a
+# ragged batch
+PLANES = conv_spec(4, 16, 16, [("pa", 16, 3, 1, 1), ("pb", 32, 5, 1, 2, (2, 2)), ("pc", 16, 3, 1, 1)])
+
 CASES = {"cifar10_quick": (lambda: spec_text("cifar10_quick"), 8),
+         "planes": (lambda: PLANES, 5),
          "alexnet_small": (lambda: ALEX_SMALL, 2),
          "alexnet_small_grouped": (lambda: ALEX_SMALL_GROUPED, 2),
          "grouped_odd": (lambda: GROUPED_ODD, 3),
@@ -209,7 +217,7 @@ def top_diff(ref, gref, L):
     return gref["diffs"][nxt[0]["name"]]
 
 
-@pytest.mark.parametrize("case,N", [("cifar10_quick", 16), ("cifar10_quick", 37), ("alexnet_small", 2),
+@pytest.mark.parametrize("case,N", [("cifar10_quick", 16), ("cifar10_quick", 37), ("planes", 5), ("alexnet_small", 2),
                                     ("alexnet_small_grouped", 2), ("grouped_odd", 5)])
 def test_conv_tc_net_level(case, N):
     """Whole layerwise TF32 step (forward, backward) vs the oracle: loss and
