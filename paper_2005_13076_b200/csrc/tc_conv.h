@@ -108,6 +108,7 @@ Launch pack_taps_launch(const PackTapsP& p);
 // forward (+bias, ReLU) and data gradient (+ the in-place ReLU's mask)
 struct PlanePlan {
   int TY, TN, HY, HX, Kq, a_bytes, w_bytes, stages, tiles_x, tiles_y, tiles;
+  int ns;  // output-channel splits (w_bytes = one split's weights)
   size_t smem;
 };
 struct PlanePackP {  // A blocks [tile][cq][HY][TN][HX][4] (TF32)
@@ -115,10 +116,10 @@ struct PlanePackP {  // A blocks [tile][cq][HY][TN][HX][4] (TF32)
   float* out;
   int N, C, H, W, ph, pw, Kq, HY, HX, TY, TN, tiles, tiles_x, tiles_y;
 };
-struct PlaneWpackP {  // B [t][cq][o][4] (TF32); mode 0 forward, 1 data gradient
+struct PlaneWpackP {  // B [split][t][cq][o][4] (TF32); mode 0 forward, 1 data gradient
   const float* w;
   float* out;
-  int Cin, Nout, kh, kw, Kq, mode;
+  int Cin, Nout, kh, kw, Kq, mode, ns;
 };
 struct PlaneConvP {
   const float* src;     // A blocks
@@ -128,6 +129,7 @@ struct PlaneConvP {
   float* out;           // NCHW [N][Nout][Ho][Wo]
   int N, Ho, Wo, Nout, Kq, kh, kw, TY, TN, HY, HX, tiles, tiles_x, tiles_y, a_bytes, w_bytes, relu, stages;
   int tmem_cols;
+  int ns;  // output-channel splits: CTA b computes split b % ns
 };
 bool plane_plan(int N, int Cin, int Ho, int Wo, int Nout, int kh, int kw, PlanePlan* pl);
 Launch plane_pack_launch(const PlanePlan& pl, const float* src, float* out, int N, int C, int H, int W, int ph,

@@ -67,20 +67,23 @@ __global__ void __launch_bounds__(256) plane_pack(const __grid_constant__ PlaneP
   }
 }
 
-// B: [t][cq][o][4 c]; mode 0 (forward) = W[o][c][i][j]; mode 1 (data
+// B: [split][t][cq][o][4 c] (output channels in ns splits of Nout / ns);
+// mode 0 (forward) = W[o][c][i][j]; mode 1 (data
 // gradient) = W[c][o][kh-1-i][kw-1-j] (rows o = the layer's input channels,
 // inner c = its output channels)
 __global__ void __launch_bounds__(256) plane_wpack(const __grid_constant__ PlaneWpackP p) {
   pdl_enter();
-  const int T = p.kh * p.kw;
+  const int T = p.kh * p.kw, nos = p.Nout / p.ns;
   const long long total = (long long)T * p.Kq * p.Nout * 4;
   for (long long e = blockIdx.x * 256LL + threadIdx.x; e < total; e += (long long)gridDim.x * 256) {
     int r = (int)e;
     const int c4 = r & 3;
     r >>= 2;
-    const int o = r % p.Nout;
-    r /= p.Nout;
-    const int cq = r % p.Kq, t = r / p.Kq, i = t / p.kw, j = t - i * p.kw, c = 4 * cq + c4;
+    const int ol = r % nos;
+    r /= nos;
+    const int cq = r % p.Kq;
+    r /= p.Kq;
+    const int t = r % T, o = (r / T) * nos + ol, i = t / p.kw, j = t - i * p.kw, c = 4 * cq + c4;
     float v = 0.f;
     if (p.mode == 0) {
       if (c < p.Cin) v = p.w[(((size_t)o * p.Cin + c) * p.kh + i) * p.kw + j];
@@ -104,8 +107,10 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
   __shared__ uint32_t tmem_base;
   __shared__ float bias_s[256];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, S = p.stages;
-  for (int o = tid; o < p.Nout; o += blockDim.x) bias_s[o] = p.bias ? __ldg(p.bias + o) : 0.f;
-  const int mine = p.tiles > (int)blockIdx.x ? (p.tiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // output-channel split: this CTA's channels [half nos, + nos), tiles cta, cta + nct, ...
+  const int half = blockIdx.x % p.ns, cta = blockIdx.x / p.ns, nct = gridDim.x / p.ns, nos = p.Nout / p.ns;
+  for (int o = tid; o < nos; o += blockDim.x) bias_s[o] = p.bias ? __ldg(p.bias + half * nos + o) : 0.f;
+  const int mine = p.tiles > cta ? (p.tiles - 1 - cta) / nct + 1 : 0;
   if (tid == 0) {
     mbar_init(smem_u32(&wbar), 1);
     for (int s = 0; s < S; ++s) {
@@ -129,20 +134,21 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
     if (mine > 0) {
       mbar_expect_tx(smem_u32(&wbar), (uint32_t)p.w_bytes);
       for (int off = 0; off < p.w_bytes; off += 32768)
-        bulk_g2s(W_s + off, (const uint8_t*)p.wts + off, (uint32_t)min(32768, p.w_bytes - off), smem_u32(&wbar));
+        bulk_g2s(W_s + off, (const uint8_t*)p.wts + (size_t)half * p.w_bytes + off,
+                 (uint32_t)min(32768, p.w_bytes - off), smem_u32(&wbar));
     }
     pdl_enter();
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
-      const int s = it % S, tile = blockIdx.x + it * gridDim.x;
+      const int s = it % S, tile = cta + it * nct;
       if (it >= S) mbar_wait(smem_u32(&empty[s]), ((it / S) - 1) & 1);
       mbar_expect_tx(smem_u32(&full[s]), (uint32_t)p.a_bytes);
       bulk_g2s(A_s + s * p.a_bytes, (const uint8_t*)p.src + (size_t)tile * p.a_bytes, (uint32_t)p.a_bytes,
                smem_u32(&full[s]));
     }
   } else if (tid == 32) {
-    const uint32_t idesc = make_idesc(128, p.Nout);
-    const uint32_t plane = (uint32_t)(p.HY * p.TN * p.HX * 16), lbo_b = (uint32_t)(p.Nout * 16);
+    const uint32_t idesc = make_idesc(128, nos);
+    const uint32_t plane = (uint32_t)(p.HY * p.TN * p.HX * 16), lbo_b = (uint32_t)(nos * 16);
     const uint32_t tap_b = (uint32_t)p.Kq * lbo_b;
     const uint64_t bd0 = make_desc_ns(W_s, lbo_b, 128);
     if (mine > 0) {
@@ -155,7 +161,7 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
       mbar_wait(smem_u32(&full[s]), (it / S) & 1);
       if (it >= 2) mbar_wait(smem_u32(&tempty[b]), ((it >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t d = tbase + b * p.Nout;
+      const uint32_t d = tbase + b * nos;
       const uint64_t ad0 = make_desc_ns(A_s + s * p.a_bytes, plane, (uint32_t)(p.HX * 16));
       if constexpr (KH > 0) {
         const uint32_t row = (uint32_t)(p.TN * p.HX * 16);
@@ -187,17 +193,18 @@ __global__ void __launch_bounds__(192, 1) conv_plane_taps(const __grid_constant_
     const int x = r & 7, g = r >> 3, nn = g % p.TN, y = g / p.TN;
 #pragma unroll 1
     for (int it = 0; it < mine; ++it) {
-      const int b = it & 1, tile = blockIdx.x + it * gridDim.x;
+      const int b = it & 1, tile = cta + it * nct;
       const int tx = tile % p.tiles_x, t2 = tile / p.tiles_x, ty = t2 % p.tiles_y, nb = t2 / p.tiles_y;
       const int n = nb * p.TN + nn, oy = ty * p.TY + y, ox = tx * 8 + x;
       const bool live = n < p.N && oy < p.Ho && ox < p.Wo;
       mbar_wait(smem_u32(&tfull[b]), (it >> 1) & 1);
       __syncwarp();
       tc_fence_after();
-      const size_t HW = (size_t)p.Ho * p.Wo, base = (size_t)n * p.Nout * HW + (size_t)oy * p.Wo + ox;
-      for (int o0 = 0; o0 < p.Nout; o0 += 16) {
+      const size_t HW = (size_t)p.Ho * p.Wo;
+      const size_t base = ((size_t)n * p.Nout + half * nos) * HW + (size_t)oy * p.Wo + ox;
+      for (int o0 = 0; o0 < nos; o0 += 16) {
         float v[16], m[16];
-        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + b * p.Nout + o0, v);
+        tmem_ld16_nowait(tbase + ((uint32_t)(quad * 32) << 16) + b * nos + o0, v);
         // the in-place ReLU's outputs of these 16 channels: every load in flight together
 #pragma unroll
         for (int q = 0; q < 16; ++q) m[q] = (p.relu_y && live) ? __ldg(p.relu_y + base + (size_t)(o0 + q) * HW) : 1.f;
@@ -238,9 +245,15 @@ bool plane_plan(int N, int Cin, int Ho, int Wo, int Nout, int kh, int kw, PlaneP
   q.HY = q.TY + kh - 1, q.HX = 8 + kw - 1;
   q.Kq = (Cin + 7) / 8 * 2;
   q.a_bytes = q.Kq * q.HY * q.TN * q.HX * 16;
-  q.w_bytes = kh * kw * q.Kq * Nout * 16;
-  const size_t wpad = ((size_t)q.w_bytes + 1023) & ~(size_t)1023;
-  if (wpad + 2 * (size_t)q.a_bytes > kPlaneSmemMax) return false;
+  // the output channels in one or two splits (each CTA stages one split's weights)
+  size_t wpad = 0;
+  for (q.ns = 1; q.ns <= 2; ++q.ns) {
+    if (Nout % q.ns || (Nout / q.ns) % 16) continue;
+    q.w_bytes = kh * kw * q.Kq * (Nout / q.ns) * 16;
+    wpad = ((size_t)q.w_bytes + 1023) & ~(size_t)1023;
+    if (wpad + 2 * (size_t)q.a_bytes <= kPlaneSmemMax) break;
+  }
+  if (q.ns > 2) return false;
   q.stages = (int)std::min<size_t>(PL_MAX_STAGES, (kPlaneSmemMax - wpad) / q.a_bytes);
   q.tiles_x = Wo / 8, q.tiles_y = Ho / q.TY;
   q.tiles = (N + q.TN - 1) / q.TN * q.tiles_y * q.tiles_x;
@@ -257,7 +270,7 @@ Launch plane_pack_launch(const PlanePlan& pl, const float* src, float* out, int 
 }
 Launch plane_wpack_launch(const PlanePlan& pl, const float* w, float* out, int Cin, int Nout, int kh, int kw,
                           int mode) {
-  PlaneWpackP p{w, out, Cin, Nout, kh, kw, pl.Kq, mode};
+  PlaneWpackP p{w, out, Cin, Nout, kh, kw, pl.Kq, mode, pl.ns};
   Launch l;
   const long long total = (long long)kh * kw * pl.Kq * Nout * 4;
   l.set((const void*)plane_wpack, dim3((unsigned)std::min<long long>((total + 255) / 256, 148LL * 8)), dim3(256), 0, p);
@@ -267,14 +280,16 @@ Launch plane_conv_launch(const PlanePlan& pl, const float* src, const float* wts
                          const float* relu_y, float* out, int N, int Ho, int Wo, int Nout, int kh, int kw, int relu,
                          int sms) {
   PlaneConvP p{src, wts, bias, relu_y, out, N, Ho, Wo, Nout, pl.Kq, kh, kw, pl.TY, pl.TN, pl.HY, pl.HX,
-               pl.tiles, pl.tiles_x, pl.tiles_y, pl.a_bytes, pl.w_bytes, relu, pl.stages, pow2_ge(2 * Nout, 32)};
+               pl.tiles, pl.tiles_x, pl.tiles_y, pl.a_bytes, pl.w_bytes, relu, pl.stages,
+               pow2_ge(2 * Nout / pl.ns, 32), pl.ns};
   Launch l;
   const void* f = (kh == 5 && kw == 5 && pl.Kq == 2)   ? (const void*)conv_plane_taps<5, 5, 1>
                   : (kh == 5 && kw == 5 && pl.Kq == 8)  ? (const void*)conv_plane_taps<5, 5, 4>
                   : (kh == 5 && kw == 5 && pl.Kq == 16) ? (const void*)conv_plane_taps<5, 5, 8>
                   : (kh == 3 && kw == 3 && pl.Kq == 8)  ? (const void*)conv_plane_taps<3, 3, 4>
                                                         : (const void*)conv_plane_taps<0, 0, 0>;
-  l.set(f, dim3((unsigned)std::max(1, std::min(pl.tiles, sms))), dim3(192), pl.smem, p);
+  const int grid = std::max(pl.ns, std::min(pl.tiles * pl.ns, sms) / pl.ns * pl.ns);  // a multiple of ns
+  l.set(f, dim3((unsigned)grid), dim3(192), pl.smem, p);
   return l;
 }
 cudaError_t plane_setup() {
