@@ -436,9 +436,10 @@ def run_reference(args):
     return 0
 
 
-def fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd):
+def fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd, x3=True):
     """The paper-precision path (fp32 blobs, fp32-class arithmetic: the
-    PN_FP32 fused plan) on the same workload: device-timed value, end to end
+    PN_FP32 fused plan, with ip1's contractions on 3xTF32 tensor cores when
+    x3 -- PN_3XTF32) on the same workload: device-timed value, end to end
     from host bytes, and its dominant stage's roofline."""
     import torch
     import torch.distributed as dist
@@ -446,7 +447,7 @@ def fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd):
     from paper_2005_13076_b200 import Net, synth
     from paper_2005_13076_b200.dp import dp_bootstrap, max_over_ranks
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    net = Net("lenet", BATCH, device=local, tf32=False)
+    net = Net("lenet", BATCH, device=local, tf32=False, x3=x3)
     net.set_params(params)
     if world > 1:
         dp_bootstrap(net, dist)
@@ -489,7 +490,9 @@ def fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd):
     per_layer = lenet_layer_roofline(BATCH, pk, pk["fp32"])
     net.close()
     return {"value": world * BATCH * steps / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
-            "dtype": "f32", "plan": "fused LeNet, PN_FP32 (fp32 SIMT kernels, 1e-5 class)",
+            "dtype": "f32", "plan": ("fused LeNet, PN_FP32 | PN_3XTF32 (1e-5 class: fp32 SIMT convolutions, ip1 as "
+                                     "3xTF32 tcgen05 MMAs over hi/lo operand copies)" if x3 else
+                                     "fused LeNet, PN_FP32 (fp32 SIMT kernels, 1e-5 class)"),
             "e2e": {"value": world * BATCH * ring / (ms_e2e / 1e3), "unit": UNIT,
                     "h2d_bytes_per_step": BATCH * 784 + BATCH * 4, "d2h_bytes_per_step": 4, "steps": ring,
                     "path": "byte batches, pipelined (net_train_steps_u8_host)"},
@@ -733,7 +736,9 @@ def main():
                                            "frac_tf32_peak": round(r["flops"] / (r["ms"] / 1e3) / 1e12 / tf32_peak, 4)}
                               for r in rows if r["flops"] and "[tc]" in r["stage"]}
     if args.workload == "lenet" and tf32 and not args.no_fp32:
-        line["fp32"] = fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd)
+        line["fp32"] = fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd, x3=True)
+        simt = fp32_record(args, world, BATCH, NB, X, Y, params, pk, sgd, x3=False)
+        line["fp32"]["simt_only"] = {"value": simt["value"], "ms_per_step": simt["ms_per_step"], "plan": simt["plan"]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.workload)
         line["cpu_baseline_threaded"] = cpu_baseline_threaded(args.workload)

@@ -63,9 +63,14 @@ enum {
   PN_FP32 = 0,      /* fp32 SIMT FFMA contractions (1e-5 parity class)        */
   PN_TF32 = 1,      /* TF32 tcgen05 tensor-core contractions, fp32 accumulate,
                        operands rounded to nearest (2e-3 parity class)         */
-  PN_LAYERWISE = 2  /* one generic kernel per layer, every blob materialised
+  PN_LAYERWISE = 2, /* one generic kernel per layer, every blob materialised
                        (debug / teacher-forcing plan); default is the fused
                        plan when the net matches a fused pattern              */
+  PN_3XTF32 = 4     /* with PN_FP32 on the fused LeNet plan: ip1's three
+                       contractions as 3xTF32 tcgen05 MMAs over hi / lo
+                       operand copies (x = hi + lo; A_lo B_hi + A_hi B_lo +
+                       A_hi B_hi, fp32 accumulate): 1e-5 parity class; ignored
+                       with PN_TF32 or on the layerwise plan                  */
 };
 
 /* which buffer of a blob */
@@ -82,7 +87,8 @@ typedef struct {
 /* Build a net.  spec_text: NUL-terminated "[input]" + "[layer]"
  * sections of key = value lines (unknown keys are PN_ERR_PARSE).
  * batch: images per forward on this device (fixed for the net's lifetime).
- * device: CUDA ordinal.  flags: PN_FP32 | PN_TF32, optionally | PN_LAYERWISE.
+ * device: CUDA ordinal.  flags: PN_FP32 | PN_TF32, optionally | PN_LAYERWISE
+ * (and PN_FP32 | PN_3XTF32: the fp32 class with ip1 on 3xTF32 tensor cores).
  * Parameters start at zero; set them with net_set_param. */
 pn_status net_create(const char* spec_text, int batch, int device, int flags,
                      pn_net** out);

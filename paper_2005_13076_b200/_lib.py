@@ -13,7 +13,7 @@ PN_OK = 0
 STATUS = {0: "PN_OK", 1: "PN_ERR_INVALID_ARG", 2: "PN_ERR_PARSE", 3: "PN_ERR_UNKNOWN_LAYER",
           4: "PN_ERR_DANGLING_BLOB", 5: "PN_ERR_SHAPE", 6: "PN_ERR_LABEL_RANGE", 7: "PN_ERR_CUDA",
           8: "PN_ERR_NCCL", 9: "PN_ERR_STATE"}
-PN_FP32, PN_TF32, PN_LAYERWISE = 0, 1, 2
+PN_FP32, PN_TF32, PN_LAYERWISE, PN_3XTF32 = 0, 1, 2, 4
 PN_DATA, PN_DIFF, PN_MASK, PN_HISTORY = 0, 1, 2, 3
 
 # every exported entry point of include/pn.h (checked by tests/test_abi.py)

@@ -228,6 +228,12 @@ struct pn_loop {
 struct pn_net {
   int device = 0, batch = 0, flags = 0;
   bool tf32 = false, fused = false;
+  // PN_3XTF32 (fused fp32 LeNet plan): ip1's contractions as 3xTF32 on the tensor
+  // cores over per-step hi / lo operand copies (tc.cu Ip3Fwd / Ip3Grad)
+  bool x3 = false;
+  float *w1h = nullptr, *w1l = nullptr, *w1th = nullptr, *w1tl = nullptr;     // [500][800], [800][512]
+  float *p2h = nullptr, *p2l = nullptr, *p2Th = nullptr, *p2Tl = nullptr;     // [N][800], [800][npad]
+  float *da1h = nullptr, *da1l = nullptr, *da1Th = nullptr, *da1Tl = nullptr; // [N][500], [500][npad]
   std::vector<Layer> layers;
   std::vector<Layer> acc_layers;  // Accuracy (forward only; read the chain's blobs)
   std::vector<Blob> blobs;
@@ -596,6 +602,16 @@ static pn_status allocate(pn_net* net) {
     TRY(net->alloc(&net->da1rT, (size_t)500 * net->npad));
     TRY(net->alloc(&net->part_b1, (size_t)kWgradSplits * 500));
     TRY(net->alloc(&net->part_db2, (size_t)tc::db2_partials(net->batch) * 50));
+  }
+  if (net->x3) {
+    const size_t N = net->batch;
+    net->npad = (net->batch + 3) & ~3;
+    for (float** b : {&net->w1h, &net->w1l}) TRY(net->alloc(b, (size_t)500 * 800));
+    for (float** b : {&net->w1th, &net->w1tl}) TRY(net->alloc(b, (size_t)800 * 512));
+    for (float** b : {&net->p2h, &net->p2l}) TRY(net->alloc(b, N * 800));
+    for (float** b : {&net->p2Th, &net->p2Tl}) TRY(net->alloc(b, (size_t)800 * net->npad));
+    for (float** b : {&net->da1h, &net->da1l}) TRY(net->alloc(b, N * 500));
+    for (float** b : {&net->da1Th, &net->da1Tl}) TRY(net->alloc(b, (size_t)500 * net->npad));
   }
   size_t col_n = 0, gm_n = 0;
   if (net->layers[0].stem_plane) {
@@ -1184,6 +1200,8 @@ static void build_fused_lenet(pn_net* net) {
   // set through the ABI (ensure_packed)
   const bool dp = net->comm || net->loop;
   net->conv_tail = false;
+  if (net->x3)  // W1 as hi / lo copies (+ transposes) first: off ip1's critical path (read after conv1, conv2)
+    add(fwd, "ip1.wsplit[3x]", tc::split3_launch({P + i1.off, net->w1h, net->w1l, net->w1th, net->w1tl, 500, 800, 512}));
   if (net->tf32 && !dp && !getenv("PN_NO_TAIL")) {  // every conv1 weight-gradient block resident at the barrier
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)lenet_conv1_wgrad, 320, 0);
@@ -1223,6 +1241,11 @@ static void build_fused_lenet(pn_net* net) {
   }
   if (net->tf32) {
     add(fwd, "ip1+relu[tc]", tc::ip1_fwd_launch(p2.data, net->pack.w1f, P + i1.off + i1.wcount, a1.data, N));
+  } else if (net->x3) {
+    // W1 and p2 as hi / lo copies (+ the transposes the gradients read), then 3xTF32
+    add(fwd, "p2.split[3x]", tc::split3_launch({p2.data, net->p2h, net->p2l, net->p2Th, net->p2Tl, N, 800, net->npad}));
+    add(fwd, "ip1+relu[3x]",
+        tc::ip1_fwd3_launch(net->p2h, net->p2l, net->w1h, net->w1l, P + i1.off + i1.wcount, a1.data, N));
   } else {
     GemmP g{p2.data, P + i1.off, a1.data, P + i1.off + i1.wcount, N, 500, 800, 800, 1, 1, 800, 1};
     add_gemm(net, fwd, "ip1+relu", g);
@@ -1287,6 +1310,23 @@ static void build_fused_lenet(pn_net* net) {
       bwd.back().mode = 2;
     }
     conv_segs.push_back(seg(net->part_db2, G + c2.off + 25000, 50, tc::db2_partials(N), 50));
+  } else if (net->x3) {
+    add(bwd, "da1.split[3x]", tc::split3_launch({a1.diff, net->da1h, net->da1l, net->da1Th, net->da1Tl, N, 500, net->npad}));
+    // dW1[o][k] = sum_n da1[n][o] p2[n][k]: A = da1^T [500][N], B = p2^T [800][N]
+    add(bwd, "ip1.wgrad[3x]", tc::ip1_grad3_launch(net->da1Th, net->da1Tl, 500, N, net->npad, net->p2Th, net->p2Tl, 800,
+                                                    net->npad, G + i1.off, 800));
+    ColSumP c{a1.diff, G + i1.off + i1.wcount, N, 500};
+    Launch l2;
+    l2.set((const void*)colsum_generic, dim3(500), dim3(256), 0, c);
+    add(bwd, "ip1.bgrad", l2);
+    add_reduce_multi(bwd, "ip.bucket_reduce", ip_segs, true);
+    // dp2[n][k] = sum_o da1[n][o] W1[o][k]: A = da1 [N][500], B = W1^T [800][512]
+    add(bwd, "ip1.dgrad[3x]", tc::ip1_grad3_launch(net->da1h, net->da1l, N, 500, 500, net->w1th, net->w1tl, 800, 512,
+                                                    p2.diff, 800));
+    Unpool2P u{p2.diff, p2.m8, cv2.diff, N};
+    Launch l4;
+    l4.set((const void*)lenet_unpool2, dim3(cdiv((long long)N * 3200, 256)), dim3(256), 0, u);
+    add(bwd, "pool2.bwd", l4);
   } else {
     GemmP w{a1.diff, p2.data, G + i1.off, nullptr, 500, 800, N, 1, 500, 800, 1, 0};
     add_gemm(net, bwd, "ip1.wgrad", w);
@@ -1712,7 +1752,7 @@ static void drop_graphs(pn_net* net) {
   if (!(n)) return fail(PN_ERR_INVALID_ARG, "net is NULL")
 
 extern "C" pn_status net_create(const char* spec, int batch, int device, int flags, pn_net** out) {
-  if (!spec || !out || batch <= 0 || device < 0 || (flags & ~3)) return fail(PN_ERR_INVALID_ARG, "net_create: bad argument");
+  if (!spec || !out || batch <= 0 || device < 0 || (flags & ~7)) return fail(PN_ERR_INVALID_ARG, "net_create: bad argument");
   *out = nullptr;
   std::unique_ptr<pn_net> net(new pn_net());
   net->device = device;
@@ -1722,6 +1762,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
   TRY(parse_and_infer(net.get(), spec));  // host-only: spec errors need no GPU
   CU(cudaSetDevice(device));
   net->fused = !(flags & PN_LAYERWISE) && is_lenet(net.get());
+  net->x3 = (flags & PN_3XTF32) && !net->tf32 && net->fused;
   int sms = 0;
   CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   net->tc_sms = sms;
@@ -1781,7 +1822,7 @@ extern "C" pn_status net_create(const char* spec, int batch, int device, int fla
                           (50 * 20 * 28 + kC2Imgs * 2880) * 4));
   CU(cudaFuncSetAttribute((const void*)lenet_conv2_dgrad_simt, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           kConv2DgradSimtSmem));
-  if (net->tf32) {
+  if (net->tf32 || net->x3) {
     cudaError_t e = net->fused ? tc::setup() : tcc::setup(max_nk);
     if (e != cudaSuccess) return fail(PN_ERR_CUDA, std::string("tc setup: ") + cudaGetErrorString(e));
   }

@@ -111,7 +111,9 @@ template <class Op>
 __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant__ typename Op::Params prm) {
   using namespace ipk;
   constexpr int BN = Op::BN, CPB = BN + 4;  // tile width, C pitch (floats; rows 16-B aligned)
-  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = A_BYTES + B_BYTES, STAGES = Op::STAGES;
+  // Op::X3 (3xTF32): each operand chunk staged as hi and lo copies (A_hi A_lo B_hi B_lo)
+  constexpr int X = Op::X3 ? 2 : 1;
+  constexpr int A_BYTES = 128 * 128, B_BYTES = BN * 128, STAGE = X * (A_BYTES + B_BYTES), STAGES = Op::STAGES;
   static_assert(128 * CPB * 4 <= STAGES * STAGE, "C fits the ring");
   static_assert(BN == 32 || BN == 64 || BN == 128, "tile width");
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -149,14 +151,14 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
       mbar_expect_tx(bar, STAGE);
       if (Op::A_EARLY) op.issue_a(c0 + c, As, bar);
-      if (Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+      if (Op::B_EARLY) op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
     pdl_enter_k(Op::ST);
     stamp(1);
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
       if (!Op::A_EARLY) op.issue_a(c0 + c, As, bar);
-      if (!Op::B_EARLY) op.issue_b(c0 + c, As + A_BYTES, bar);
+      if (!Op::B_EARLY) op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
     for (int c = STAGES; c < my; ++c) {
       const int st = c % STAGES;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
       const uint32_t As = sbase + st * STAGE, bar = smem_u32(&full[st]);
       mbar_expect_tx(bar, STAGE);
       op.issue_a(c0 + c, As, bar);
-      op.issue_b(c0 + c, As + A_BYTES, bar);
+      op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
   } else if (tid == 32) {
     constexpr uint32_t idesc = make_idesc(128, BN);
@@ -172,9 +174,18 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
       const int st = c % STAGES;
       mbar_wait(smem_u32(&full[st]), (c / STAGES) & 1);
       tc_fence_after();
-      const uint32_t As = sbase + st * STAGE, Bs = As + A_BYTES;
+      const uint32_t As = sbase + st * STAGE, Bs = As + X * A_BYTES;
+      if constexpr (Op::X3) {  // A_lo B_hi + A_hi B_lo + A_hi B_hi (the A_lo B_lo term dropped)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+        for (int k = 0; k < 4; ++k) {
+          mma_tf32(tbase, make_desc(As + A_BYTES + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+          mma_tf32_c<1>(tbase, make_desc(As + k * 32), make_desc(Bs + B_BYTES + k * 32), idesc);
+          mma_tf32_c<1>(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
+      }
       mma_commit(smem_u32(&empty[st]));
     }
     if (my > 0) mma_commit(smem_u32(&done));
@@ -250,7 +261,7 @@ struct IpFwd {
     int M, K, Nout;
   };
   static constexpr int RED_FLOATS = 0, STAGES = IPF_STAGES, EPI_BYTES = 0, SPLIT = IPF_SPLIT, BN = IPF_BN;
-  static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr bool A_EARLY = false, B_EARLY = true, X3 = false;
   static constexpr int ST = ST_IPF;
   const Params& p;
   int m0, o0;
@@ -287,7 +298,7 @@ struct IpWgrad {
     int M, K, Nout;  // M = batch (contraction), K = 800 (cols), Nout = 500 (rows)
   };
   static constexpr int RED_FLOATS = 0, STAGES = IPG_STAGES, EPI_BYTES = 0, SPLIT = IPG_SPLIT, BN = IPG_BN;
-  static constexpr bool A_EARLY = false, B_EARLY = true;
+  static constexpr bool A_EARLY = false, B_EARLY = true, X3 = false;
   static constexpr int ST = ST_IPG;
   const Params& p;
   int o0, k0;
@@ -329,7 +340,7 @@ struct IpDgradUnpool {
   static constexpr int SPLIT = IPD_SPLIT, ROWS = 128 / SPLIT, STAGES = IPD_STAGES, BN = IPD_BN, FT = BN / 16;
   static constexpr int RED_FLOATS = FT * ROWS;  // red: [filter in tile][owned row]
   static constexpr int EPI_BYTES = ROWS * BN;   // the owned rows' pool2 origins [row][FT x 16]
-  static constexpr bool A_EARLY = !FORK_PDL, B_EARLY = true;  // (FORK_PDL: da1r from the immediate predecessor)
+  static constexpr bool A_EARLY = !FORK_PDL, B_EARLY = true, X3 = false;  // (FORK_PDL: da1r from the immediate predecessor)
   static constexpr int ST = ST_IPD;
   const Params& p;
   int m0, k0;
@@ -378,6 +389,121 @@ struct IpDgradUnpool {
     }
   }
 };
+
+// ---------------------------- ip1 at fp32 class: 3xTF32 on the tensor cores
+// The fp32 plan's PN_3XTF32 variant of the three ip1 contractions: every
+// operand x is split once per step (split3) into hi = x with its 13 low
+// mantissa bits cleared (exact in TF32) and lo = TF32(x - hi) (x - hi is
+// exact in fp32), and the tile accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi
+// in TMEM (fp32); the dropped A_lo B_lo and the rounding of lo are below
+// 2^-20 |a b| per product, the fp32 class (R21).  Same tiles,
+// rings and epilogues as the TF32 Ops, each chunk staged as hi + lo copies.
+struct Ip3Fwd {  // y = relu(p2 W1^T + b): IpFwd's tiles (K split over a cluster)
+  struct Params {
+    CUtensorMap ta, tal, tb, tbl;
+    const float* b;
+    float* y;
+    int M, K, Nout;
+  };
+  static constexpr int RED_FLOATS = 0, STAGES = 4, EPI_BYTES = 0, SPLIT = IPF_SPLIT, BN = IPF_BN;
+  static constexpr bool A_EARLY = false, B_EARLY = true, X3 = true;
+  static constexpr int ST = ST_IPF;
+  const Params& p;
+  int m0, o0;
+  __device__ Ip3Fwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * BN) {}
+  __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
+  __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tal); prefetch_tmap(&p.tb); prefetch_tmap(&p.tbl); }
+  __device__ void issue_a(int c, uint32_t s, uint32_t bar) {
+    tma2d(s, &p.ta, c * BK, m0, bar);
+    tma2d(s + 128 * 128, &p.tal, c * BK, m0, bar);
+  }
+  __device__ void issue_b(int c, uint32_t s, uint32_t bar) {
+    tma2d(s, &p.tb, c * BK, o0, bar);
+    tma2d(s + BN * 128, &p.tbl, c * BK, o0, bar);
+  }
+  __device__ void stage_epilogue(int, uint8_t*, int) {}
+  __device__ void store(int row, int, int half, const float (&v)[16], float*, const uint8_t*) const {
+    const int m = m0 + row;
+    if (m >= p.M) return;
+#pragma unroll
+    for (int c = 0; c < 16; c += 4) {
+      const int o = o0 + 16 * half + c;
+      if (o >= p.Nout) break;
+      float4 r = f4(v[c] + __ldg(p.b + o), v[c + 1] + __ldg(p.b + o + 1), v[c + 2] + __ldg(p.b + o + 2),
+                    v[c + 3] + __ldg(p.b + o + 3));
+      r.x = fmaxf(r.x, 0.f); r.y = fmaxf(r.y, 0.f); r.z = fmaxf(r.z, 0.f); r.w = fmaxf(r.w, 0.f);
+      *reinterpret_cast<float4*>(p.y + (size_t)m * p.Nout + o) = r;
+    }
+  }
+  __device__ void finish(int, const float*, int) const {}
+};
+// dW1 = da1^T p2 (K = batch) and dp2 = da1 W1 (K = 500 -> 512): rows r0 + row,
+// 16 columns per call, out[r][c] fp32 (row pitch ldo)
+struct Ip3Grad {
+  struct Params {
+    CUtensorMap ta, tal, tb, tbl;
+    float* out;
+    int rows, cols, ldo, nk;  // output rows / cols, K chunks of 32
+  };
+  static constexpr int RED_FLOATS = 0, STAGES = 5, EPI_BYTES = 0, SPLIT = 1, BN = 32;
+  static constexpr bool A_EARLY = false, B_EARLY = false, X3 = true;
+  static constexpr int ST = ST_IPG;
+  const Params& p;
+  int r0, c0;
+  __device__ Ip3Grad(const Params& q) : p(q), r0(blockIdx.y * 128), c0(blockIdx.x * BN) {}
+  __device__ int num_k_chunks() const { return p.nk; }
+  __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tal); prefetch_tmap(&p.tb); prefetch_tmap(&p.tbl); }
+  __device__ void issue_a(int c, uint32_t s, uint32_t bar) {
+    tma2d(s, &p.ta, c * BK, r0, bar);
+    tma2d(s + 128 * 128, &p.tal, c * BK, r0, bar);
+  }
+  __device__ void issue_b(int c, uint32_t s, uint32_t bar) {
+    tma2d(s, &p.tb, c * BK, c0, bar);
+    tma2d(s + BN * 128, &p.tbl, c * BK, c0, bar);
+  }
+  __device__ void stage_epilogue(int, uint8_t*, int) {}
+  __device__ void store(int row, int, int half, const float (&v)[16], float*, const uint8_t*) const {
+    const int r = r0 + row;
+    if (r >= p.rows) return;
+#pragma unroll
+    for (int c = 0; c < 16; c += 4) {
+      const int k = c0 + 16 * half + c;
+      if (k < p.cols) *reinterpret_cast<float4*>(p.out + (size_t)r * p.ldo + k) = f4(v[c], v[c + 1], v[c + 2], v[c + 3]);
+    }
+  }
+  __device__ void finish(int, const float*, int) const {}
+};
+// hi / lo copies of src [R][C] (and transposed [C][ldt]); null outputs
+// skipped.  32 x 32 tiles: coalesced reads and row-major writes, the
+// transposes through a padded shared tile (coalesced writes too).
+__global__ void __launch_bounds__(256) split3(const __grid_constant__ Split3P p) {
+  __shared__ float th[32][33], tl[32][33];
+  pdl_enter();
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int r = r0 + ty + 8 * k, c = c0 + tx;
+    float hi = 0.f, lo = 0.f;
+    if (r < p.R && c < p.C) {
+      const float x = __ldg(p.src + (size_t)r * p.C + c);
+      hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+      lo = tf32f(x - hi);
+      if (p.hi) p.hi[(size_t)r * p.C + c] = hi, p.lo[(size_t)r * p.C + c] = lo;
+    }
+    th[ty + 8 * k][tx] = hi, tl[ty + 8 * k][tx] = lo;
+  }
+  if (!p.hiT) return;
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int c = c0 + ty + 8 * k, r = r0 + tx;
+    if (c < p.C && r < p.R) {
+      p.hiT[(size_t)c * p.ldt + r] = th[tx][ty + 8 * k];
+      p.loT[(size_t)c * p.ldt + r] = tl[tx][ty + 8 * k];
+    }
+  }
+}
 
 // ------------------------- conv2 + bias + pool2 (+mask), persistent tap GEMM
 // conv2 as 25 tap GEMMs accumulated in TMEM, with NO im2col:
@@ -1247,7 +1373,7 @@ static CUtensorMap tmap_g2(const float* base, uint64_t N) {
 
 template <class Op>
 static constexpr size_t ip_smem() {  // the ring + 1 KB alignment slack
-  return (size_t)Op::STAGES * (128 * 128 + Op::BN * 128) + 1024;
+  return (size_t)Op::STAGES * (Op::X3 ? 2 : 1) * (128 * 128 + Op::BN * 128) + 1024;
 }
 template <class Op>
 static cudaError_t opt_in() {
@@ -1260,6 +1386,8 @@ cudaError_t setup() {
   if ((e = opt_in<IpFwd>()) != cudaSuccess) return e;
   if ((e = opt_in<IpWgrad>()) != cudaSuccess) return e;
   if ((e = opt_in<IpDgradUnpool>()) != cudaSuccess) return e;
+  if ((e = opt_in<Ip3Fwd>()) != cudaSuccess) return e;
+  if ((e = opt_in<Ip3Grad>()) != cudaSuccess) return e;
   if ((e = cudaFuncSetAttribute((const void*)conv2_wgrad_persistent, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 wg::SMEM)) != cudaSuccess)
     return e;
@@ -1316,6 +1444,32 @@ Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* 
   l.set((const void*)ip_tile<IpFwd>, dim3(IpFwd::SPLIT * cdiv(500, IpFwd::BN), cdiv(N, 128)), dim3(ipk::THREADS),
         ip_smem<IpFwd>(), p);
   l.cluster = dim3(IpFwd::SPLIT, 1, 1);
+  return l;
+}
+
+Launch split3_launch(const Split3P& p) {
+  Launch l;
+  l.set((const void*)split3, dim3(cdiv(p.C, 32), cdiv(p.R, 32)), dim3(256), 0, p);
+  return l;
+}
+Launch ip1_fwd3_launch(const float* p2h, const float* p2l, const float* w1h, const float* w1l, const float* b, float* y,
+                       int N) {
+  Launch l;
+  Ip3Fwd::Params p{tmap2d(p2h, N, 800, 800, 128), tmap2d(p2l, N, 800, 800, 128), tmap2d(w1h, 500, 800, 800, Ip3Fwd::BN),
+                   tmap2d(w1l, 500, 800, 800, Ip3Fwd::BN), b, y, N, 800, 500};
+  l.set((const void*)ip_tile<Ip3Fwd>, dim3(Ip3Fwd::SPLIT * cdiv(500, Ip3Fwd::BN), cdiv(N, 128)), dim3(ipk::THREADS),
+        ip_smem<Ip3Fwd>(), p);
+  l.cluster = dim3(Ip3Fwd::SPLIT, 1, 1);
+  return l;
+}
+// out[rows][cols] = A B^T with A = [rows][K] (hi / lo, pitch lda), B = [cols][K] (pitch ldb)
+Launch ip1_grad3_launch(const float* ah, const float* al, int rows, int K, int lda, const float* bh, const float* bl,
+                        int cols, int ldb, float* out, int ldo) {
+  Launch l;
+  Ip3Grad::Params p{tmap2d(ah, rows, K, lda, 128), tmap2d(al, rows, K, lda, 128), tmap2d(bh, cols, K, ldb, Ip3Grad::BN),
+                    tmap2d(bl, cols, K, ldb, Ip3Grad::BN), out, rows, cols, ldo, (int)cdiv(K, 32)};
+  l.set((const void*)ip_tile<Ip3Grad>, dim3(cdiv(cols, Ip3Grad::BN), cdiv(rows, 128)), dim3(ipk::THREADS),
+        ip_smem<Ip3Grad>(), p);
   return l;
 }
 

@@ -38,6 +38,20 @@ Launch pack_p1c_launch(const float* p1, float* p1c, int N);
 // the three ip1 GEMMs as 128-row tiles (ip_tile<Op>: per-layer tile width and K
 // split over a cluster, partials reduced in DSMEM)
 Launch ip1_fwd_launch(const float* p2, const float* w1f, const float* b, float* y, int N);
+// fp32 class (PN_3XTF32): the ip1 contractions as 3xTF32 over hi / lo operand copies
+struct Split3P {  // hi / lo [R][C] and their transposes [C][ldt] (null: skipped)
+  const float* src;
+  float* hi;
+  float* lo;
+  float* hiT;
+  float* loT;
+  int R, C, ldt;
+};
+Launch split3_launch(const Split3P& p);
+Launch ip1_fwd3_launch(const float* p2h, const float* p2l, const float* w1h, const float* w1l, const float* b, float* y,
+                       int N);
+Launch ip1_grad3_launch(const float* ah, const float* al, int rows, int K, int lda, const float* bh, const float* bl,
+                        int cols, int ldb, float* out, int ldo);
 Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, int npad);
 Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_t* m2, float* g2, float* part_db2,
                                int N);

@@ -52,9 +52,12 @@ def make_sgd(base_lr=0.01, momentum=0.9, weight_decay=5e-4, lr_policy="inv", gam
 class Net:
     """One net per device: net_create / net_forward / net_backward / sgd_update."""
 
-    def __init__(self, spec, batch, device=0, tf32=False, layerwise=False):
+    def __init__(self, spec, batch, device=0, tf32=False, layerwise=False, x3=False):
+        """x3: the fp32 class (tf32=False) with ip1's contractions as 3xTF32
+        tensor-core MMAs (PN_3XTF32)."""
         text = spec_text(spec) if "\n" not in spec else spec
-        flags = (_lib.PN_TF32 if tf32 else 0) | (_lib.PN_LAYERWISE if layerwise else 0)
+        flags = ((_lib.PN_TF32 if tf32 else 0) | (_lib.PN_LAYERWISE if layerwise else 0)
+                 | (_lib.PN_3XTF32 if x3 else 0))
         h = ctypes.c_void_p()
         check(lib().net_create(text.encode(), batch, device, flags, ctypes.byref(h)))
         self._h = h

@@ -27,11 +27,11 @@ from parity import RTOL, assert_bitwise, assert_close, assert_norm, check_mask, 
 pytestmark = pytest.mark.gpu
 
 
-def make(spec, N, tf32=False, layerwise=False, seed_x=1, seed_w=2):
+def make(spec, N, tf32=False, layerwise=False, seed_x=1, seed_w=2, x3=False):
     ref = OracleNet(spec_text(spec), N)
     params = synth.xavier_params(ref.learnable(), seed=seed_w, bias="uniform")
     ref.set_params(params)
-    net = Net(spec, N, tf32=tf32, layerwise=layerwise)
+    net = Net(spec, N, tf32=tf32, layerwise=layerwise, x3=x3)
     net.set_params(params)
     if spec == "lenet":
         x, y = synth.mnist_like(N, seed=seed_x)
@@ -185,6 +185,42 @@ def test_train_step_graph_equals_eager_and_is_deterministic(tf32, N):
         assert_bitwise("eager vs graph", np.asarray(a), np.asarray(b))
     for a, b in zip(results[1], results[2]):
         assert_bitwise("graph rerun", np.asarray(a), np.asarray(b))
+
+
+@pytest.mark.parametrize("N", [37, 64, 512])
+def test_fp32_class_with_3xtf32_inner_product(N):
+    """PN_3XTF32 (DESIGN R20): the fused fp32 plan with ip1's three
+    contractions as 3xTF32 tcgen05 MMAs over hi / lo operand copies -- one
+    step at the fp32 class (rtol 1e-5, net-level bounds: loss, blobs, masks,
+    predictions, every gradient); two steps of eager phases bitwise equal to
+    two graph-replayed steps."""
+    net, ref, params, x, y = make("lenet", N, False, x3=True)
+    assert "ip1+relu[3x]" in net.stages(0) and "ip1.dgrad[3x]" in net.stages(1)
+    xd, yd = cuda(x), cuda(y)
+    loss = torch.zeros(1, device="cuda", dtype=torch.float32)
+    net.net_forward(xd, yd, loss)
+    net.net_backward()
+    net.net_sync_errors()
+    out = ref.forward(x, y)
+    gref = ref.backward()
+    check_net_level(net, ref, params, out, gref, loss.item(), RTOL[False], tag="3xtf32")
+    net.close()
+    sgd = make_sgd()
+    res = []
+    for mode in ("eager", "graph"):
+        net, ref, params, x, y = make("lenet", N, False, x3=True)
+        xd, yd = cuda(x), cuda(y)
+        for it in range(2):
+            if mode == "eager":
+                net.net_forward(xd, yd, loss)
+                net.net_backward()
+                net.sgd_update(sgd, it)
+            else:
+                net.net_train_step(xd, yd, sgd, it, loss)
+        res.append([host(net.net_get_blob(k)) for k in params])
+        net.close()
+    for a, b in zip(res[0], res[1]):
+        assert_bitwise("3xtf32 eager vs graph", a, b)
 
 
 def test_solver_weight_copies_match_a_fresh_pack():
