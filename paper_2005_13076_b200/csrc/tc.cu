@@ -85,6 +85,14 @@ namespace tc {
 #ifndef IPG_SPLIT
 #define IPG_SPLIT 1
 #endif
+// column tiles per cluster sharing (TMA multicast) each A chunk of the ip1
+// weight / data gradients (1: every CTA loads its own)
+#ifndef IPG_MC
+#define IPG_MC 1
+#endif
+#ifndef IPD_MC
+#define IPD_MC 1
+#endif
 #ifndef IPG_BN
 #define IPG_BN 32
 #endif
@@ -104,6 +112,23 @@ __device__ __forceinline__ float4 ld_cluster4(uint32_t local_addr, uint32_t rank
   float4 v;
   asm volatile("ld.shared::cluster.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
   return v;
+}
+// TMA 2-D box multicast to the CTAs of `mask` in the cluster (same smem
+// offset, complete_tx on each one's mbarrier at the same offset)
+__device__ __forceinline__ void tma2d_mc(uint32_t dst, const CUtensorMap* m, int c0, int c1, uint32_t bar,
+                                         uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, "
+      "%3}], [%4], %5;" ::"r"(dst),
+      "l"(m), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+      : "memory");
+}
+// tcgen05.commit arriving on the mbarrier at `bar`'s offset in every CTA of `mask`
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(mask)
+               : "memory");
 }
 }  // namespace ipk
 
@@ -125,6 +150,13 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int SPLIT = Op::SPLIT, ROWS = 128 / SPLIT;  // K split over a cluster of SPLIT CTAs, or the whole K
   const uint32_t rank = SPLIT > 1 ? cluster_rank() : 0u;  // cluster = (SPLIT, 1, 1): blockIdx.x = SPLIT * column + rank
+  // Op::MC > 1: a cluster of MC column tiles (same rows) shares each A chunk --
+  // chunk c loaded by CTA c % MC and multicast to all; each stage is freed by
+  // all MC consumers (their MMA commits arrive on every CTA's empty barrier)
+  constexpr int MC = Op::MC;
+  static_assert(MC == 1 || SPLIT == 1, "A multicast with a split K cluster");
+  const uint32_t mrank = MC > 1 ? cluster_rank() : 0u;
+  constexpr uint16_t MMASK = (uint16_t)((1u << MC) - 1);
   Op op(prm);
   const int nk = op.num_k_chunks(), c0 = (int)rank * nk / SPLIT, my = ((int)rank + 1) * nk / SPLIT - c0;
   const uint32_t sbase = smem_u32(smem);
@@ -132,7 +164,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   if (tid == 0) {
     for (int c = 0; c < STAGES; ++c) {
       mbar_init(smem_u32(&full[c]), 1);
-      mbar_init(smem_u32(&empty[c]), 1);
+      mbar_init(smem_u32(&empty[c]), MC);
     }
     mbar_init(smem_u32(&done), 1);
     fence_barrier_init();
@@ -142,6 +174,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   op.stage_epilogue(tid, epi_s, (int)rank);  // epilogue inputs from >= 2 launches back
   tc_fence_before();
   __syncthreads();
+  if (MC > 1) cluster_sync();  // every CTA's barriers initialised before any multicast lands
   tc_fence_after();
   const uint32_t tbase = tmem_base;
   if (tid == 0) stamp(0);
@@ -150,14 +183,14 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
       mbar_expect_tx(bar, STAGE);
-      if (Op::A_EARLY) op.issue_a(c0 + c, As, bar);
+      if (Op::A_EARLY && (MC == 1 || (c0 + c) % MC == (int)mrank)) op.issue_a_mc(c0 + c, As, bar, MMASK);
       if (Op::B_EARLY) op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
     pdl_enter_k(Op::ST);
     stamp(1);
     for (int c = 0; c < pre; ++c) {
       const uint32_t As = sbase + c * STAGE, bar = smem_u32(&full[c]);
-      if (!Op::A_EARLY) op.issue_a(c0 + c, As, bar);
+      if (!Op::A_EARLY && (MC == 1 || (c0 + c) % MC == (int)mrank)) op.issue_a_mc(c0 + c, As, bar, MMASK);
       if (!Op::B_EARLY) op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
     for (int c = STAGES; c < my; ++c) {
@@ -165,7 +198,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
       mbar_wait(smem_u32(&empty[st]), ((c / STAGES) - 1) & 1);
       const uint32_t As = sbase + st * STAGE, bar = smem_u32(&full[st]);
       mbar_expect_tx(bar, STAGE);
-      op.issue_a(c0 + c, As, bar);
+      if (MC == 1 || (c0 + c) % MC == (int)mrank) op.issue_a_mc(c0 + c, As, bar, MMASK);
       op.issue_b(c0 + c, As + X * A_BYTES, bar);
     }
   } else if (tid == 32) {
@@ -186,7 +219,8 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
 #pragma unroll
         for (int k = 0; k < 4; ++k) mma_tf32(tbase, make_desc(As + k * 32), make_desc(Bs + k * 32), idesc, (c | k) != 0);
       }
-      mma_commit(smem_u32(&empty[st]));
+      if (MC > 1) mma_commit_mc(smem_u32(&empty[st]), MMASK);
+      else mma_commit(smem_u32(&empty[st]));
     }
     if (my > 0) mma_commit(smem_u32(&done));
   } else if (warp >= 2) {
@@ -247,6 +281,7 @@ __global__ void __launch_bounds__(ipk::THREADS, 1) ip_tile(const __grid_constant
   if (tid == 0) stamp(4);
   op.finish(tid, red, (int)rank);
   ST_END(Op::ST);
+  if (MC > 1) cluster_sync();  // no CTA leaves while a peer's MMA commits may still arrive on its barriers
   if (warp == 0) tmem_dealloc(tbase, BN);
 }
 
@@ -268,7 +303,8 @@ struct IpFwd {
   __device__ IpFwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
+  static constexpr int MC = 1;
+  __device__ void issue_a_mc(int c, uint32_t s, uint32_t bar, uint16_t) { tma2d(s, &p.ta, c * BK, m0, bar); }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, o0, bar); }
   __device__ void stage_epilogue(int, uint8_t*, int) {}
   __device__ void store(int row, int, int half, const float (&v)[16], float*, const uint8_t*) const {
@@ -305,7 +341,11 @@ struct IpWgrad {
   __device__ IpWgrad(const Params& q) : p(q), o0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return (p.M + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, o0, bar); }
+  static constexpr int MC = IPG_MC;
+  __device__ void issue_a_mc(int c, uint32_t s, uint32_t bar, uint16_t mask) {
+    if (MC > 1) ipk::tma2d_mc(s, &p.ta, c * BK, o0, bar, mask);
+    else tma2d(s, &p.ta, c * BK, o0, bar);
+  }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
   __device__ void stage_epilogue(int, uint8_t*, int) {}
   __device__ void store(int row, int, int half, const float (&v)[16], float*, const uint8_t*) const {
@@ -347,7 +387,11 @@ struct IpDgradUnpool {
   __device__ IpDgradUnpool(const Params& q) : p(q), m0(blockIdx.y * 128), k0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return 16; }  // 500 -> 512
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tb); }
-  __device__ void issue_a(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.ta, c * BK, m0, bar); }
+  static constexpr int MC = IPD_MC;
+  __device__ void issue_a_mc(int c, uint32_t s, uint32_t bar, uint16_t mask) {
+    if (MC > 1) ipk::tma2d_mc(s, &p.ta, c * BK, m0, bar, mask);
+    else tma2d(s, &p.ta, c * BK, m0, bar);
+  }
   __device__ void issue_b(int c, uint32_t s, uint32_t bar) { tma2d(s, &p.tb, c * BK, k0, bar); }
   __device__ void stage_epilogue(int tid, uint8_t* es, int rank) {  // conv2's forward wrote them, many launches back
     for (int u = tid; u < FT * ROWS; u += ipk::THREADS) {
@@ -413,7 +457,8 @@ struct Ip3Fwd {  // y = relu(p2 W1^T + b): IpFwd's tiles (K split over a cluster
   __device__ Ip3Fwd(const Params& q) : p(q), m0(blockIdx.y * 128), o0((blockIdx.x / SPLIT) * BN) {}
   __device__ int num_k_chunks() const { return (p.K + BK - 1) / BK; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tal); prefetch_tmap(&p.tb); prefetch_tmap(&p.tbl); }
-  __device__ void issue_a(int c, uint32_t s, uint32_t bar) {
+  static constexpr int MC = 1;
+  __device__ void issue_a_mc(int c, uint32_t s, uint32_t bar, uint16_t) {
     tma2d(s, &p.ta, c * BK, m0, bar);
     tma2d(s + 128 * 128, &p.tal, c * BK, m0, bar);
   }
@@ -453,7 +498,8 @@ struct Ip3Grad {
   __device__ Ip3Grad(const Params& q) : p(q), r0(blockIdx.y * 128), c0(blockIdx.x * BN) {}
   __device__ int num_k_chunks() const { return p.nk; }
   __device__ void prefetch() { prefetch_tmap(&p.ta); prefetch_tmap(&p.tal); prefetch_tmap(&p.tb); prefetch_tmap(&p.tbl); }
-  __device__ void issue_a(int c, uint32_t s, uint32_t bar) {
+  static constexpr int MC = 1;
+  __device__ void issue_a_mc(int c, uint32_t s, uint32_t bar, uint16_t) {
     tma2d(s, &p.ta, c * BK, r0, bar);
     tma2d(s + 128 * 128, &p.tal, c * BK, r0, bar);
   }
@@ -1478,7 +1524,7 @@ Launch ip1_wgrad_launch(const float* da1T, const float* p2T, float* dw, int N, i
   IpWgrad::Params p{tmap2d(da1T, 500, N, npad, 128), tmap2d(p2T, 800, N, npad, IpWgrad::BN), dw, N, 800, 500};
   l.set((const void*)ip_tile<IpWgrad>, dim3(IpWgrad::SPLIT * cdiv(800, IpWgrad::BN), cdiv(500, 128)), dim3(ipk::THREADS),
         ip_smem<IpWgrad>(), p);
-  l.cluster = dim3(IpWgrad::SPLIT, 1, 1);
+  l.cluster = dim3(IpWgrad::SPLIT * IpWgrad::MC, 1, 1);
   return l;
 }
 
@@ -1489,7 +1535,7 @@ Launch ip1_dgrad_unpool_launch(const float* da1r, const float* w1t, const uint8_
                           part_db2, N};
   l.set((const void*)ip_tile<IpDgradUnpool>, dim3(IpDgradUnpool::SPLIT * cdiv(800, IpDgradUnpool::BN), cdiv(N, 128)),
         dim3(ipk::THREADS), ip_smem<IpDgradUnpool>(), p);
-  l.cluster = dim3(IpDgradUnpool::SPLIT, 1, 1);
+  l.cluster = dim3(IpDgradUnpool::SPLIT * IpDgradUnpool::MC, 1, 1);
   return l;
 }
 
