@@ -898,7 +898,7 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_taps(const __grid_constant_
       const int st = g & 1, sg = s0 + g, n = sg / p.seg_per_img, ys = (sg - n * p.seg_per_img) * p.R;
       if (g >= 2) mbar_wait(smem_u32(&empty[st]), ((g >> 1) - 1) & 1);
       const uint32_t bar = smem_u32(&full[st]), As = sbase + st * p.stage_bytes;
-      mbar_expect_tx(bar, (uint32_t)p.stage_bytes);
+      mbar_expect_tx(bar, (uint32_t)p.tx_bytes);  // the two boxes (the pad after X is never written)
       tma5d(As, &p.tx, 0, 0, 0, ys - p.ph, n, bar);
       tma4d(As + XB, &p.tg, 0, 0, ys, n, bar);
     }
@@ -1165,10 +1165,18 @@ static constexpr size_t kWtapSmemMax = 220 * 1024;
 static int wtap_mt(int C, int T) { return (T + 128 / C - 1) / (128 / C); }
 // rows per segment: the largest power of two <= Ho whose two stages (+ the
 // ones tile) fit shared memory; 0 if none
+// X part of a stage: the R + kh staged input rows' kw C-row blocks, plus the
+// blocks the last accumulator tile of the last output row reads past them
+// (tap slots >= T: ignored rows, but the reads must stay in the stage)
+static size_t wtap_x_bytes(int R, int C, int Wo, int kh, int kw) {
+  const int T = kh * kw, MT = wtap_mt(C, T), TPT = 128 / C;
+  const int blocks = std::max((R + kh) * kw, (R - 1) * kw + MT * TPT);
+  return (size_t)blocks * C * Wo * 4;
+}
 static int wtap_rows(int C, int Ho, int Wo, int F, int kh, int kw, size_t* stage) {
   for (int R = 1 << 5; R >= 1; R >>= 1) {
     if (R > Ho && R > 1) continue;
-    const size_t st = (size_t)(R + kh) * kw * C * Wo * 4 + (size_t)R * F * Wo * 4;
+    const size_t st = wtap_x_bytes(R, C, Wo, kh, kw) + (size_t)R * F * Wo * 4;
     if (2 * st + 128 * Wo * 4 <= kWtapSmemMax) {
       if (stage) *stage = st;
       return R;
@@ -1226,8 +1234,9 @@ bool wgrad_taps_launch(const float* xs, const float* gw, int N, int C, int H, in
   p.T = kh * kw, p.K = C * kh * kw, p.bias = bias, p.pstride = pstride;
   p.TPT = 128 / C;
   p.MT = wtap_mt(C, p.T);
-  p.x_bytes = (p.R + kh) * kw * C * Wo * 4;
+  p.x_bytes = (int)wtap_x_bytes(p.R, C, Wo, kh, kw);  // (the X box fills its first (R + kh) kw blocks)
   p.stage_bytes = (int)stage;
+  p.tx_bytes = (p.R + kh) * kw * C * Wo * 4 + p.R * F * Wo * 4;
   p.seg_per_img = (Ho + p.R - 1) / p.R;
   p.segs = N * p.seg_per_img;
   p.tmem_cols = pow2_at_least((p.MT + 1) * F, 32);

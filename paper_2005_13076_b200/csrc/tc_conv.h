@@ -94,7 +94,7 @@ struct ConvWtapP {
   CUtensorMap tg;  // Gw {Wo, F, Ho, N}, box {Wo, F, R, 1}
   float* part;     // [splits][pstride]: f*K + t*C + c (t = tap; the reduce permutes); bias at F*K + f
   int N, C, Ho, Wo, F, kh, kw, ph, pw, T, K, bias, pstride;
-  int MT, TPT, R, x_bytes, stage_bytes, seg_per_img, segs, tmem_cols;
+  int MT, TPT, R, x_bytes, stage_bytes, tx_bytes, seg_per_img, segs, tmem_cols;
 };
 Launch shift_copies_launch(const ShiftCopyP& p);
 Launch gw_launch(const GwP& p);
