@@ -288,7 +288,9 @@ Launch plane_conv_launch(const PlanePlan& pl, const float* src, const float* wts
                   : (kh == 5 && kw == 5 && pl.Kq == 16) ? (const void*)conv_plane_taps<5, 5, 8>
                   : (kh == 3 && kw == 3 && pl.Kq == 8)  ? (const void*)conv_plane_taps<3, 3, 4>
                                                         : (const void*)conv_plane_taps<0, 0, 0>;
-  const int grid = std::max(pl.ns, std::min(pl.tiles * pl.ns, sms) / pl.ns * pl.ns);  // a multiple of ns
+  int grid = std::max(pl.ns, std::min(pl.tiles * pl.ns, sms) / pl.ns * pl.ns);  // a multiple of ns
+  if (const char* e = getenv("PN_PLANE_CTAS"))  // test hook: fewer CTAs, so small batches wrap the ring
+    grid = std::max(1, std::min(grid / pl.ns, atoi(e))) * pl.ns;
   l.set(f, dim3((unsigned)grid), dim3(192), pl.smem, p);
   return l;
 }

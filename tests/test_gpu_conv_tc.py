@@ -175,6 +175,16 @@ def test_conv_tc_teacher_forced(case):
     net.close()
 
 
+def test_conv_tc_teacher_forced_ring_wrap(monkeypatch):
+    """The plane tap GEMM with its grid capped at 3 CTAs (PN_PLANE_CTAS test
+    hook): at cifar10_quick's test batch every CTA then takes 5-6 tiles (16
+    conv2 tiles, 64 stem tiles), so the 4-stage A ring wraps and both TMEM
+    accumulators alternate, element-wise against the oracle as above."""
+    monkeypatch.setenv("PN_PLANE_CTAS", "3")
+    test_conv_tc_teacher_forced("cifar10_quick")
+    test_conv_tc_teacher_forced("planes")
+
+
 def check_stem(net, ref, out, gref, L, stages, xd, yd, fwd_rtol):
     """The layerwise plan's stem (cifar10_quick conv1 -> pool1 -> relu1; the
     forward one fp32 kernel, or the TF32 plane tap GEMM + pooling with the
