@@ -249,7 +249,6 @@ __global__ void __launch_bounds__(C2_THREADS, 1) lenet_conv2_pool2_simt(
 // taps W2[f,c,i,:] -> 40 FMAs.  Persistent blocks of 480 threads over image
 // pairs; W2 staged once ([f][c][i][8], taps padded), G2 per pair.
 constexpr int C2D_THREADS = 480;
-constexpr int C2D_SMEM = (50 * 20 * 5 * 8 + 2 * 50 * 16 * 8) * 4;
 __global__ void __launch_bounds__(C2D_THREADS, 1) lenet_conv2_dgrad_simt(const __grid_constant__ ConvBwdDataP p) {
   extern __shared__ __align__(16) float c2d_smem[];
   float* ws = c2d_smem;                    // [50 f][20 c][5 i][8]

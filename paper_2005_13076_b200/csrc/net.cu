@@ -723,13 +723,6 @@ static void add_reduce(pn_net* net, std::vector<Stage>& v, const Layer& L, bool 
   add_reduce_multi(v, L.name + ".wgrad_reduce", {r});
 }
 
-static void add_reduce_raw(std::vector<Stage>& v, const std::string& name, const float* part, float* out, int n,
-                           int splits) {
-  ReduceP r{part, out, n, splits, n};
-  Launch l;
-  l.set((const void*)reduce_partials, dim3(cdiv(n, 256)), dim3(256), 0, r);
-  add(v, name, l);
-}
 
 static void add_reduce_multi(std::vector<Stage>& v, const std::string& name, const std::vector<ReduceP>& segs,
                              bool late) {
@@ -1456,7 +1449,6 @@ static void build_update(pn_net* net) {
     return;
   }
   if (net->fused && net->tf32) {  // reduce (conv bucket) + SGD + the TF32 weight copies
-    const bool dp = net->comm || net->loop;
     net->phase[2].push_back(solver_stage(net, "solver[tc]", true, true, nullptr));
     // the whole single-GPU step: the ip part ran on the side branch and the
     // conv bucket's at the end of conv1's weight gradient (build_fused_lenet)

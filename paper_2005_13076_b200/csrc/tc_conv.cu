@@ -925,7 +925,7 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_taps(const __grid_constant_
     }
     if (ns > 0) mma_commit(smem_u32(&done));
   } else if (warp >= 2) {  // epilogue: row r of tile m = (tap slot, channel)
-    const int quad = warp & 3, r = quad * 32 + lane, sl = r / p.C, ch = r - sl * p.C;
+    const int quad = warp & 3, r = quad * 32 + lane, sl = r / p.C;  // (channel r % C: the partial's inner index)
     if (ns > 0) {
       mbar_wait(smem_u32(&done), 0);
       __syncwarp();
