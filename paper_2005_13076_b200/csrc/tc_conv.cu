@@ -18,6 +18,10 @@
 //                materialised alternative (a K x M column gradient written
 //                and re-read, then col2im) measured slower, since the
 //                contraction over F is short and the column matrix large
+// Round 2 adds, for stride-1 layers where they apply: the
+// weight gradient as a tap GEMM over TMA-staged segments of column-shifted
+// X copies (conv_wgrad_taps: no column matrix) and, in tc_plane.cu, the
+// forward / data gradient over halo-staged channel planes.
 // m = (n, ho, wo), k = (c, i, j), f = output channel.  B200 has the HBM (180
 // GB, ~7 TB/s) to make the materialisation cheaper than gathering operands
 // element by element into shared memory (which measured at 5-35% of the TF32

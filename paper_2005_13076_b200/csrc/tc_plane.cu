@@ -1,7 +1,8 @@
 // tc_plane.cu -- stride-1 convolution (forward, and data gradient as the
 // convolution of G with the flipped, channel-transposed filter) as a tap GEMM
 // over halo-staged activation blocks, for the layerwise TF32 plan
-// (cifar10_quick conv2).  The LeNet conv2 forward's
+// (cifar10_quick: conv1 -- the stem's forward --, conv2 forward and data
+// gradient, conv3 forward).  The LeNet conv2 forward's
 // scheme (tc.cu conv2_fwd_persistent) for any stride-1 layer whose output
 // rows are a multiple of 8 wide:
 //   * an output tile is 128 positions = TY rows x TN images x 8 columns
@@ -15,6 +16,8 @@
 //     by (i TN HX + j) * 16 B -- no im2col, no per-tap load;
 //   * B = every tap's weights [t][cq][o][4 c], staged once per CTA (no-swizzle,
 //     LBO = Nout * 16 B, SBO = 128 B), packed once per step by plane_wpack;
+//     when they do not fit beside the ring, the output channels go in two
+//     splits (CTA b computes split b % 2 and stages only its weights);
 //   * persistent over tiles: warp 0 lane 0 bulk copies (weights, then an
 //     A-block ring), warp 1 lane 0 issues T x Kc/8 tcgen05.mma (M = 128,
 //     N = Nout, K = 8) per tile into one of two TMEM accumulators, warps 2-5
