@@ -511,7 +511,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=None, help="default: 200 / 50 / 5")
     ap.add_argument("--workload", default="lenet", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32"])
+    ap.add_argument("--precision", default="tf32", choices=["tf32", "fp32", "fp32x3"],
+                    help="headline plan: TF32 tensor cores, fp32 SIMT, or fp32 class with ip1 on 3xTF32 (PN_3XTF32)")
     ap.add_argument("--e2e-steps", type=int, default=2000)
     ap.add_argument("--profile-steps", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -545,7 +546,7 @@ def main():
     WL = WORKLOADS[args.workload]
     BATCH, NB = WL["batch"], WL["nb"]
     layers = parse_layers(spec_text(WL["spec"]))
-    net = Net(WL["spec"], BATCH, device=local, tf32=tf32)
+    net = Net(WL["spec"], BATCH, device=local, tf32=tf32, x3=args.precision == "fp32x3")
     learn = []
     for L in layers:
         if "params" in L:
