@@ -45,6 +45,20 @@ __device__ __forceinline__ float in_x(const float* x, const uint8_t* x8, float s
   const float v = __fmul_rn((float)__ldg(x8 + i), scale);
   return mean ? __fsub_rn(v, __ldg(mean + i % 784)) : v;
 }
+// four consecutive values at base (a multiple of 4, pixel base % 784 = pix):
+// one 16-B float or 4-B byte load, in_x's per-element normalisation
+__device__ __forceinline__ float4 in_x4(const float* x, const uint8_t* x8, float scale, const float* mean,
+                                       long long base, int pix) {
+  if (!x8) return __ldg(reinterpret_cast<const float4*>(x + base));
+  const uchar4 b = __ldg(reinterpret_cast<const uchar4*>(x8 + base));
+  float4 v = make_float4(__fmul_rn((float)b.x, scale), __fmul_rn((float)b.y, scale), __fmul_rn((float)b.z, scale),
+                         __fmul_rn((float)b.w, scale));
+  if (mean) {
+    const float4 m = __ldg(reinterpret_cast<const float4*>(mean + pix));
+    v = make_float4(__fsub_rn(v.x, m.x), __fsub_rn(v.y, m.y), __fsub_rn(v.z, m.z), __fsub_rn(v.w, m.w));
+  }
+  return v;
+}
 
 constexpr int C1_MAXIMG = 4;  // images a block's item range can touch
 constexpr int C1_PAIRS = C1_FPT / 2;    // filter pairs per thread (one FFMA2 lane pair each)
@@ -551,7 +565,7 @@ __global__ void lenet_unpool2(const __grid_constant__ Unpool2P p) {
 #define C1W_MINB 2
 #endif
 __global__ void __launch_bounds__(320, C1W_MINB) lenet_conv1_wgrad(const __grid_constant__ Conv1WgradP p) {
-  __shared__ float xs[CW_IMGS][784];
+  __shared__ __align__(16) float xs[CW_IMGS][784];
   ST_BEGIN(ST_CONV1W);
   const int s = blockIdx.x;
   const int n0 = (int)((long long)p.N * s / p.splits), n1 = (int)((long long)p.N * (s + 1) / p.splits);
@@ -573,18 +587,37 @@ __global__ void __launch_bounds__(320, C1W_MINB) lenet_conv1_wgrad(const __grid_
       }
   };
   load_chunk(0);
-  {  // staging loads all in flight together (with the first chunk's)
-    constexpr int PER = (CW_IMGS * 784 + 319) / 320;
-    float v[PER];
+  {  // staging loads all in flight together (with the first chunk's); 4
+     // values per load when the input is aligned (784 = 196 x 4)
+    const bool vec = ((reinterpret_cast<uintptr_t>(p.x8 ? (const void*)p.x8 : (const void*)p.x) &
+                       (p.x8 ? 3 : 15)) == 0);
+    if (vec) {
+      constexpr int PER4 = (CW_IMGS * 196 + 319) / 320;
+      float4 v[PER4];
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + 320 * k;
-      v[k] = i < cnt * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + i) : 0.f;
-    }
+      for (int k = 0; k < PER4; ++k) {
+        const int i4 = threadIdx.x + 320 * k;
+        v[k] = i4 < cnt * 196 ? in_x4(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + 4 * i4, (4 * i4) % 784)
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + 320 * k;
-      if (i < cnt * 784) xs[i / 784][i % 784] = v[k];
+      for (int k = 0; k < PER4; ++k) {
+        const int i4 = threadIdx.x + 320 * k;
+        if (i4 < cnt * 196) reinterpret_cast<float4*>(&xs[0][0])[i4] = v[k];  // xs rows of 784: contiguous
+      }
+    } else {
+      constexpr int PER = (CW_IMGS * 784 + 319) / 320;
+      float v[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = threadIdx.x + 320 * k;
+        v[k] = i < cnt * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)n0 * 784 + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = threadIdx.x + 320 * k;
+        if (i < cnt * 784) xs[i / 784][i % 784] = v[k];
+      }
     }
   }
   __syncthreads();

@@ -78,6 +78,20 @@ __device__ __forceinline__ float c1_in(const Conv1Pool1P& p, long long i) {
   const float v = __fmul_rn((float)__ldg(p.x8 + i), p.x_scale);
   return p.x_mean ? __fsub_rn(v, __ldg(p.x_mean + i % 784)) : v;
 }
+// four consecutive input values at base (a multiple of 4; pixel base % 784 =
+// pix): one 16-B float load or one 4-B byte load, the same per-element
+// normalisation as c1_in
+__device__ __forceinline__ float4 c1_in4(const Conv1Pool1P& p, long long base, int pix) {
+  if (!p.x8) return __ldg(reinterpret_cast<const float4*>(p.x + base));
+  const uchar4 b = __ldg(reinterpret_cast<const uchar4*>(p.x8 + base));
+  float4 v = make_float4(__fmul_rn((float)b.x, p.x_scale), __fmul_rn((float)b.y, p.x_scale),
+                         __fmul_rn((float)b.z, p.x_scale), __fmul_rn((float)b.w, p.x_scale));
+  if (p.x_mean) {
+    const float4 m = __ldg(reinterpret_cast<const float4*>(p.x_mean + pix));
+    v = make_float4(__fsub_rn(v.x, m.x), __fsub_rn(v.y, m.y), __fsub_rn(v.z, m.z), __fsub_rn(v.w, m.w));
+  }
+  return v;
+}
 
 __device__ __forceinline__ float4 ld_shared_f4(uint32_t addr) {
   float4 v;
@@ -122,17 +136,34 @@ __global__ void __launch_bounds__(c1::THREADS, 1) conv1_pool1_tc(const __grid_co
   // ---- prologue: the range's images (TF32) and the weight tile
   {
     const int nimg = n_hi - n_lo + 1, total = nimg * 784;
-    constexpr int PER = (MAXIMG * 784 + THREADS - 1) / THREADS;
-    float v[PER];
+    const bool vec = ((reinterpret_cast<uintptr_t>(p.x8 ? (const void*)p.x8 : (const void*)p.x) &
+                       (p.x8 ? 3 : 15)) == 0);
+    if (vec) {  // 4 values per load (784 = 196 x 4: a group never straddles images)
+      constexpr int PER4 = (MAXIMG * 196 + THREADS - 1) / THREADS;
+      float4 v[PER4];
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + THREADS * u;
-      v[u] = i < total ? c1_in(p, (long long)n_lo * 784 + i) : 0.f;
-    }
+      for (int u = 0; u < PER4; ++u) {
+        const int i4 = tid + THREADS * u;
+        v[u] = 4 * i4 < total ? c1_in4(p, (long long)n_lo * 784 + 4 * i4, (4 * i4) % 784) : zero4();
+      }
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const int i = tid + THREADS * u;
-      if (i < total) stsf(X_s + 4 * i, tf32f(v[u]));
+      for (int u = 0; u < PER4; ++u) {
+        const int i4 = tid + THREADS * u;
+        if (4 * i4 < total) sts128(X_s + 16 * i4, f4(tf32f(v[u].x), tf32f(v[u].y), tf32f(v[u].z), tf32f(v[u].w)));
+      }
+    } else {
+      constexpr int PER = (MAXIMG * 784 + THREADS - 1) / THREADS;
+      float v[PER];
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int i = tid + THREADS * u;
+        v[u] = i < total ? c1_in(p, (long long)n_lo * 784 + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) {
+        const int i = tid + THREADS * u;
+        if (i < total) stsf(X_s + 4 * i, tf32f(v[u]));
+      }
     }
     // B[f][k] = W[f, k] for f < 20, k < 25, else 0 (SW128, K-major)
     for (int u = tid; u < 32 * 8; u += THREADS) {
