@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(C1_THREADS, C1_MINB) lenet_conv1_pool1(const _
   // step's SGD) is complete at launch and the predecessor (the TF32 weight
   // packing) touches none of it: run alongside it, wait only at the end
   // (pdl.cuh)
-  __shared__ float xs[C1_MAXIMG][28 * 28];
+  __shared__ __align__(16) float xs[C1_MAXIMG][28 * 28];
   const int i0 = blockIdx.x * p.per_block, i1 = min(i0 + p.per_block, p.N * 144);
   if (i0 >= i1) {
     pdl_enter();
@@ -76,18 +76,37 @@ __global__ void __launch_bounds__(C1_THREADS, C1_MINB) lenet_conv1_pool1(const _
   const int nlo = i0 / 144, nimg = (i1 - 1) / 144 - nlo + 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int f0 = C1_FPT * warp;  // this warp's filters f0 .. f0 + C1_FPT - 1
-  {  // every load of the staging issued before the first store (one HBM round trip)
-    constexpr int PER = (C1_MAXIMG * 784 + C1_THREADS - 1) / C1_THREADS;
-    float v[PER];
+  {  // every load of the staging issued before the first store (one HBM round
+     // trip); 4 values per load when the input is aligned (784 = 196 x 4)
+    const bool vec = ((reinterpret_cast<uintptr_t>(p.x8 ? (const void*)p.x8 : (const void*)p.x) &
+                       (p.x8 ? 3 : 15)) == 0);
+    if (vec) {
+      constexpr int PER4 = (C1_MAXIMG * 196 + C1_THREADS - 1) / C1_THREADS;
+      float4 v[PER4];
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + C1_THREADS * k;
-      v[k] = i < nimg * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i) : 0.f;
-    }
+      for (int k = 0; k < PER4; ++k) {
+        const int i4 = threadIdx.x + C1_THREADS * k;
+        v[k] = i4 < nimg * 196 ? in_x4(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + 4 * i4, (4 * i4) % 784)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
 #pragma unroll
-    for (int k = 0; k < PER; ++k) {
-      const int i = threadIdx.x + C1_THREADS * k;
-      if (i < nimg * 784) xs[i / 784][i % 784] = v[k];
+      for (int k = 0; k < PER4; ++k) {
+        const int i4 = threadIdx.x + C1_THREADS * k;
+        if (i4 < nimg * 196) reinterpret_cast<float4*>(&xs[0][0])[i4] = v[k];
+      }
+    } else {
+      constexpr int PER = (C1_MAXIMG * 784 + C1_THREADS - 1) / C1_THREADS;
+      float v[PER];
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = threadIdx.x + C1_THREADS * k;
+        v[k] = i < nimg * 784 ? in_x(p.x, p.x8, p.x_scale, p.x_mean, (long long)nlo * 784 + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < PER; ++k) {
+        const int i = threadIdx.x + C1_THREADS * k;
+        if (i < nimg * 784) xs[i / 784][i % 784] = v[k];
+      }
     }
   }
   unsigned long long wp[C1_PAIRS][25];
