@@ -54,6 +54,9 @@ constexpr int WARPS = 17, THREADS = WARPS * 32;
 #ifndef C1_SUP
 #define C1_SUP 1
 #endif
+#ifndef C1_EARLY_TRIGGER
+#define C1_EARLY_TRIGGER 1
+#endif
 #ifndef C1_NSET
 #define C1_NSET 4
 #endif
@@ -110,6 +113,10 @@ __global__ void __launch_bounds__(c1::THREADS, 1) conv1_pool1_tc(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   ST_BEGIN(ST_CONV1);
+  // the step's first kernel: no programmatic predecessor (its wait below is
+  // trivial), so let conv2's forward launch at once -- its CTAs take the SMs
+  // these CTAs leave and stage W2 while the last conv1 tiles finish
+  if (C1_EARLY_TRIGGER) pdl_trigger();
   const uint32_t B_s = smem_u32(smem), X_s = B_s + B_BYTES, S_s = X_s + XS_FLOATS * 4;
   // afull[set]: the batch's SUP tiles built (SUP warps arrive); mdone[set]:
   // its MMAs retired (one commit: frees the A tiles and fills the
