@@ -482,6 +482,9 @@ __global__ void __launch_bounds__(IP2_SPB * 32) lenet_ip2_loss(const __grid_cons
 // partial dW2[o,k] = sum_{m in split} dz[m,o] a1[m,k];  partial db2[o].
 // Rows go in chunks of 16 with all 16 a1 loads issued together; the TF32
 // transpose da1rT[k][m..m+15] is written as 4 x 16 B per thread.
+#ifndef IP2B_EARLY_TRIGGER
+#define IP2B_EARLY_TRIGGER 0
+#endif
 __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2BwdP p) {
   const int k = blockIdx.x * 128 + threadIdx.x;
   const int s = blockIdx.y;
@@ -499,6 +502,7 @@ __global__ void __launch_bounds__(128) lenet_ip2_bwd(const __grid_constant__ Ip2
   // (its loss sum runs on the side branch), two launches back otherwise --
   // wait for it after the weight loads; let the successor launch at the end
   pdl_wait();
+  if (IP2B_EARLY_TRIGGER) pdl_trigger();  // ip1's data gradient may launch now (it waits for this kernel)
   if (threadIdx.x == 0) st_mark(ST_IP2B, 1);
   float bacc = 0.f, b1acc = 0.f;
   for (int mb = m0; mb < m1; mb += 16) {
