@@ -962,30 +962,69 @@ __global__ void __launch_bounds__(192, 1) conv_wgrad_taps(const __grid_constant_
 }
 
 // Xs[n][y][j][c][x] = tf32(X[n][c][y][x + j - pw]) (0 outside the row): a
-// block per input row (n, y); W and C powers of two (shifts, no division)
+// block per input row (n, y); W and C powers of two (shifts, no division).
+// The row's C x W inputs are staged once in shared memory (16-B loads when
+// the rows are 16-B aligned) and each copy is written as 16-B stores.
 __global__ void __launch_bounds__(256) tf32_shift_copies(const __grid_constant__ ShiftCopyP p) {
+  __shared__ __align__(16) float xs_row[128 * 32];  // C W <= 4096 (wgrad_taps_ok)
   pdl_enter();
-  const int lw = __ffs(p.W) - 1, lc = __ffs(p.C) - 1, per = p.kw << (lc + lw);
+  const int lw = __ffs(p.W) - 1, lc = __ffs(p.C) - 1, cw = 1 << (lc + lw), per4 = (p.kw << (lc + lw)) >> 2;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.x) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0;
   for (int row = blockIdx.x; row < p.N * p.H; row += gridDim.x) {
     const int n = row / p.H, y = row - n * p.H;
     const float* xr = p.x + ((size_t)n * p.C * p.H + y) * p.W;  // + c H W + x
-    float* o = p.out + (size_t)row * per;
-    for (int u = threadIdx.x; u < per; u += 256) {
-      const int x = u & (p.W - 1), c = (u >> lw) & (p.C - 1), j = u >> (lw + lc), xs = x + j - p.pw;
-      o[u] = (xs >= 0 && xs < p.W) ? tf32f(__ldg(xr + (size_t)c * p.H * p.W + xs)) : 0.f;
+    __syncthreads();  // the previous row's copies are written
+    if (vec) {
+      for (int u = threadIdx.x; u < cw >> 2; u += 256) {
+        const int c = (u << 2) >> lw, x = (u << 2) & (p.W - 1);
+        float4 v = __ldg(reinterpret_cast<const float4*>(xr + (size_t)c * p.H * p.W + x));
+        v.x = tf32f(v.x); v.y = tf32f(v.y); v.z = tf32f(v.z); v.w = tf32f(v.w);
+        reinterpret_cast<float4*>(xs_row)[u] = v;
+      }
+    } else {
+      for (int u = threadIdx.x; u < cw; u += 256)
+        xs_row[u] = tf32f(__ldg(xr + (size_t)(u >> lw) * p.H * p.W + (u & (p.W - 1))));
+    }
+    __syncthreads();
+    float* o = p.out + (size_t)row * (per4 << 2);
+    for (int u = threadIdx.x; u < per4; u += 256) {
+      const int e = u << 2, x = e & (p.W - 1), c = (e >> lw) & (p.C - 1), j = e >> (lw + lc);
+      const float* src = xs_row + (c << lw);
+      float v[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int xs = x + q + j - p.pw;
+        v[q] = (xs >= 0 && xs < p.W) ? src[xs] : 0.f;
+      }
+      if (vec) reinterpret_cast<float4*>(o)[u] = make_float4(v[0], v[1], v[2], v[3]);
+      else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) o[e + q] = v[q];
+      }
     }
   }
 }
-// Gw[n][yo][f][xo] = tf32(G[n][f][yo][xo]): a block per output row (n, yo)
+// Gw[n][yo][f][xo] = tf32(G[n][f][yo][xo]): a block per output row (n, yo),
+// 16-B loads and stores when aligned (Wo a power of two >= 4)
 __global__ void __launch_bounds__(256) tf32_gw(const __grid_constant__ GwP p) {
   pdl_enter();
   const int lw = __ffs(p.Wo) - 1, per = p.F << lw;
+  const bool vec = ((reinterpret_cast<uintptr_t>(p.g) | reinterpret_cast<uintptr_t>(p.out)) & 15) == 0 && p.Wo >= 4;
   for (int row = blockIdx.x; row < p.N * p.Ho; row += gridDim.x) {
     const int n = row / p.Ho, y = row - n * p.Ho;
     const float* g = p.g + ((size_t)n * p.F * p.Ho + y) * p.Wo;  // + f Ho Wo + x
     float* o = p.out + (size_t)row * per;
-    for (int u = threadIdx.x; u < per; u += 256)
-      o[u] = tf32f(__ldg(g + (size_t)(u >> lw) * p.Ho * p.Wo + (u & (p.Wo - 1))));
+    if (vec) {
+      for (int u = threadIdx.x; u < per >> 2; u += 256) {
+        const int e = u << 2;
+        float4 v = __ldg(reinterpret_cast<const float4*>(g + (size_t)(e >> lw) * p.Ho * p.Wo + (e & (p.Wo - 1))));
+        v.x = tf32f(v.x); v.y = tf32f(v.y); v.z = tf32f(v.z); v.w = tf32f(v.w);
+        reinterpret_cast<float4*>(o)[u] = v;
+      }
+    } else {
+      for (int u = threadIdx.x; u < per; u += 256)
+        o[u] = tf32f(__ldg(g + (size_t)(u >> lw) * p.Ho * p.Wo + (u & (p.Wo - 1))));
+    }
   }
 }
 Launch shift_copies_launch(const ShiftCopyP& p) {
